@@ -1,0 +1,186 @@
+/*
+ * disc.h -- C ABI of libdisc, the B200-native (sm_100a) DISC per-frame mapping hot path.
+ *
+ * DISC (arXiv 2603.03935) §III: each frame's instance masks are back-projected through
+ * depth and pose into voxel keys, hashed into a GPU-resident voxel map, the exact
+ * voxel overlap of every new segment with the map's instances is counted,
+ * instances are associated / merged on the fly when overlap and visual similarity suffice
+ * (P:98), and dense ViT patch tokens are pooled under each mask weighted by the
+ * distinctiveness map D (Eq.1) into per-instance embeddings that are replaced on
+ * fusion by the observation of higher quality Q (Eq.2-3).
+ *
+ * Citations: P:n = PAPER.md line n; S:n = SPEC.md line n; R<k> = reading k in DESIGN.md §3
+ * (SURVEY.md §8(c) C.3).  The operation a call performs is defined step by step in
+ * DESIGN.md §2 (= SURVEY §8(c) C.2, O0-O13).
+ *
+ * Conventions
+ *  - Plain C, no CUDA types: a stream is passed as `void*` (a cudaStream_t; NULL = legacy
+ *    default stream).  Device pointers are CUDA device addresses on the map's device.
+ *  - Ownership: the caller owns every input buffer; device inputs must stay valid until the
+ *    work enqueued on `stream` completes (stream-ordered, as in cuBLAS).  The library owns
+ *    all map state (device memory allocated in disc_map_create, freed in destroy).
+ *    Outputs go to caller-allocated HOST buffers.  Getters called with NULL output
+ *    buffers return the required count in *n_out; a short `cap` returns DISC_ERR_INVALID.
+ *  - Errors: argument / frame validation failures return DISC_ERR_INVALID before any
+ *    mutation (non-rigid pose S:118, dims, capacities, thresholds S:320).  Per-segment
+ *    problems never fail a frame; they are counted in the report by reason.
+ *    Capacity, CUDA and internal errors are sticky: the map is poisoned, later calls
+ *    return the same code, disc_last_error() gives the text.  Capacity overflow detected on
+ *    the device is reported at the next synchronising call (one that fills a host buffer).
+ *  - Threading: one writer per map.  Query / get calls must not run concurrently
+ *    with integrate calls on the same map.
+ *  - No CPU fallback: every step of the path runs in libdisc's sm_100a kernels.
+ */
+#ifndef DISC_H
+#define DISC_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DISC_OK = 0,
+  DISC_ERR_INVALID = 2,      /* bad argument / frame / config; nothing was mutated        */
+  DISC_ERR_INTERNAL = 4,
+  DISC_ERR_CAPACITY = 5,     /* a configured capacity was exceeded (sticky)               */
+  DISC_ERR_CUDA = 6,         /* CUDA runtime error (sticky)                               */
+  DISC_ERR_NCCL = 7,
+  DISC_ERR_UNSUPPORTED = 8
+} disc_status;
+
+typedef struct disc_map disc_map;  /* opaque, library-owned */
+
+typedef struct {
+  /* method parameters */
+  float voxel_size;        /* r (m) > 0        */
+  float tau_geo;           /* overlap_min threshold in (0,1], default 0.3   R10, S:356       */
+  float tau_vis;           /* tracking cosine threshold in [-1,1], 0.8      R11, R15  */
+  float depth_min, depth_max;        /* exclusive validity window 0.1/10  R4 */
+  float mask_min_conf;     /* 0.5                                           R8        */
+  float mask_max_aspect;   /* 10 (long/short bbox side, inclusive)          R8        */
+  int32_t mask_min_area;   /* 400 pixels (inclusive)                        R8        */
+  float cover_min;         /* 0.25 (patch coverage threshold, inclusive)   R17, R18  */
+  float lambda_size;       /* 3.3            */
+  float eps_distinct;      /* 1e-6                                          Eq.1, R16        */
+  int32_t feat_dim;        /* Df > 0, multiple of 4 (CLIP token width)                       */
+  int32_t track_dim;       /* Dt >= 0; 0 = no visual gate (DINO tracking width)              */
+  /* capacities (device memory is sized from these at create time) */
+  int64_t max_memberships; /* live (key, instance) pairs; voxel hash sized 2x               */
+  int32_t max_instances;   /* instance ids ever created (ids are never reused, R13)          */
+  int32_t max_masks;       /* S per frame, <= 255                                            */
+  int32_t max_pixels;      /* H*W per frame                                                  */
+  int32_t max_patches;     /* Hp*Wp per frame                                                */
+  int32_t max_pairs_per_frame; /* unique (mask, voxel) pairs per frame, <= 2^22              */
+  int32_t window;          /* frames per stage-1 batch in disc_integrate_frames, 1..32       */
+  int32_t device;          /* CUDA ordinal                                                   */
+  /* sharding (reserved; must be 1 / 0 / NULL in this version) */
+  int32_t world_size, rank;
+  const void* nccl_unique_id;
+} disc_config;
+
+typedef struct {
+  int64_t frame_id;
+  int32_t height, width;               /* H_img, W_img                                      */
+  float fx, fy, cx, cy;                /* pinhole intrinsics; pixel (u,v) integer (R1)       */
+  float pose[16];                      /* camera->world, row-major, OpenCV axes (R3); host   */
+  const float* depth;                  /* [H][W] z-depth, metres (R2)                        */
+  int32_t num_masks;                   /* S >= 0                                             */
+  const uint8_t* masks;                /* [S][H][W], nonzero = in mask (R9: may overlap)     */
+  const float* mask_conf;              /* [S] or NULL (= 1.0)                                */
+  int32_t patch_h, patch_w;            /* Hp in [1,H], Wp in [1,W]; pixel -> patch by floor  */
+                                       /* (v Hp / H, u Wp / W) (R17)                         */
+  const float* patch_feats;            /* [Hp][Wp][Df] fp32 CLIP tokens, or NULL: geometry-  */
+                                       /* only mode (no embedding, Q = -1)                   */
+  const float* global_embed;           /* [Df] or NULL (S_sem = 1)                           */
+  const uint16_t* track_feats;         /* [Hp][Wp][Dt] bf16 bit patterns; required iff Dt>0  */
+} disc_frame;
+
+typedef struct {                       /* per-frame report                     */
+  int32_t kept, drop_area, drop_conf, drop_aspect, drop_nodepth, drop_nofeat;
+  int64_t key_out_of_range;            /* depth-valid pixels with a key outside +-2^20 (R6) */
+  int64_t unique_pairs;                /* U = sum over kept s of |V_s|                      */
+  int64_t edges;                       /* qualifying (s, j) edges (O10)                     */
+  int64_t created, merged_away;
+  int64_t new_memberships;             /* net growth of the membership relation             */
+  int64_t relabeled;                   /* sum of |V_j| over merged-away instances j         */
+  int64_t live_instances, live_memberships;
+} disc_frame_report;
+
+typedef struct {
+  int64_t id, voxel_count, last_seen;
+  int32_t obs_count;
+  float q;                             /* quality of the kept embedding; -1 = none          */
+  int32_t aabb_min[3], aabb_max[3];    /* key-space bounds of the voxel set                  */
+} disc_instance;
+
+typedef struct {                       /* last-frame debug export (parity tests)            */
+  int32_t num_masks;                   /* out                                                */
+  int32_t* status;                     /* [S] 0 kept,1 area,2 conf,3 aspect,4 nodepth,5 nofeat */
+  int64_t* area;                       /* [S]                                                */
+  int32_t* bbox;                       /* [S][4] umin, vmin, umax, vmax                      */
+  int64_t* vs;                         /* [S] |V_s|                                          */
+  int64_t* target;                     /* [S] instance id the detection was fused into, -1   */
+  float* factors;                      /* [S][6] s_size, s_angle, s_sem, s_dist, q, dbar     */
+  float* embed;                        /* [S][Df] e_s                                        */
+  double* track;                       /* [S][Dt] t_s                                        */
+  int64_t pair_cap;                    /* capacity of pair_s / pair_key                      */
+  int32_t* pair_s;                     /* unique (s, key) pairs of kept detections, any order */
+  uint64_t* pair_key;                  /* packed keys (R6)                                    */
+  int64_t n_pairs;                     /* out                                                */
+  int64_t trip_cap;
+  int32_t* trip_s;                     /* C triples (s, j, c) over kept s, frame-start j      */
+  int64_t* trip_j;
+  int64_t* trip_c;
+  int32_t* trip_edge;
+  int64_t n_trip;                      /* out                                                */
+} disc_frame_debug;
+
+typedef struct {                       /* timing of the dominant kernels (disc_set_timing)  */
+  int64_t frames;
+  double k1_ms;                        /* mask pass + back-projection + dedup (K1)          */
+  int64_t k1_launches;
+  double stage1_ms, stage2_ms;         /* whole stage-1 batch / sum of stage-2 frame loops  */
+  int64_t mask_bytes, depth_bytes, track_bytes, feat_bytes; /* algorithmic input bytes      */
+  int64_t pairs, map_inserts, relabels; /* U, new memberships written, relabel probes        */
+} disc_stats;
+
+/* Fill *c with the defaults named above (capacities sized for a Replica-shaped stream). */
+disc_status disc_config_init(disc_config* c);
+disc_status disc_map_create(const disc_config* cfg, disc_map** out);
+void disc_map_destroy(disc_map* m);
+
+/* One frame, device-resident inputs (O0-O13).  report (host) may be NULL; a non-NULL
+ * report synchronises the stream. */
+disc_status disc_integrate_frame(disc_map* m, const disc_frame* f, void* stream,
+                                 disc_frame_report* report);
+/* == n sequential disc_integrate_frame calls; batches stage 1 (per-frame independent work)
+ * over windows of cfg.window frames.  report: host array [n] or NULL. */
+disc_status disc_integrate_frames(disc_map* m, const disc_frame* f, int32_t n, void* stream,
+                                  disc_frame_report* report);
+/* Same, but every data pointer of f[i] is HOST memory (pinned for full speed): the
+ * library copies each window's inputs to device staging buffers on `stream`. */
+disc_status disc_integrate_frames_host(disc_map* m, const disc_frame* f, int32_t n, void* stream,
+                                       disc_frame_report* report);
+
+/* Q1: top-k live instances by cosine e_j . q/|q|, ties by ascending id.
+ * q: host [Df]; ids/scores: host [k]; synchronises. */
+disc_status disc_query(disc_map* m, const float* q, int32_t k, int64_t* ids, float* scores,
+                       int32_t* n_out);
+/* Q2: live instances, ascending id; embeds host [cap][Df] or NULL; track host [cap][Dt] or
+ * NULL (fp64 sums T_j, R15). */
+disc_status disc_get_instances(disc_map* m, disc_instance* out, float* embeds, double* track,
+                               int32_t cap, int32_t* n_out);
+/* membership relation {(key, id)} (any order); keys packed per R6. */
+disc_status disc_get_memberships(disc_map* m, uint64_t* keys, int64_t* ids, int64_t cap,
+                                 int64_t* n_out);
+disc_status disc_debug_last_frame(disc_map* m, disc_frame_debug* d);
+disc_status disc_set_timing(disc_map* m, int32_t on);
+disc_status disc_get_stats(disc_map* m, disc_stats* s);
+disc_status disc_sync(disc_map* m);    /* wait for the map's work; surfaces device errors */
+const char* disc_last_error(const disc_map* m);
+const char* disc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

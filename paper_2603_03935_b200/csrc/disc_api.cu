@@ -1,0 +1,679 @@
+// disc_api.cu -- libdisc's C ABI (include/disc.h): validation, device memory ownership,
+// stream-ordered orchestration of the stage-1 window kernels and the per-frame stage-2
+// kernels, error stickiness, exports.
+//
+// Every step of the hot path runs in the kernels of k_frame.cu / k_map.cu; this file only
+// validates, sizes, launches and copies.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "disc_common.cuh"
+#include "disc_launch.h"
+
+using namespace disc;
+
+struct EvPair {
+  cudaEvent_t a, b;
+  int kind;  // 0 = K1, 1 = stage 1, 2 = stage 2
+};
+
+struct disc_map {
+  disc_config cfg;
+  Params P;
+  int dev = 0, nsm = 148;
+  MapState M{};
+  WinBufs W{};
+  FrameScratch X{};
+  int* d_err = nullptr;
+  int* h_err = nullptr;                 // pinned
+  disc_frame_report* h_rep = nullptr;   // pinned [MAXWIN]
+  std::vector<void*> allocs;
+  disc_status sticky = DISC_OK;
+  std::string err;
+  cudaStream_t last_stream = nullptr;
+  // last frame (debug export)
+  bool have_last = false;
+  int last_f = 0;
+  FrameDesc last_fd{};
+  bool last_sem = false;
+  // timing
+  bool timing = false;
+  std::vector<EvPair> ev_pending;
+  std::vector<cudaEvent_t> ev_pool;
+  disc_stats stats{};
+  // host-input staging
+  uint8_t* stage = nullptr;
+  size_t stage_bytes = 0;
+  // export scratch
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+};
+
+namespace {
+
+const char* VERSION = "libdisc 0.1 (sm_100a)";
+
+template <typename T>
+T* dalloc(disc_map* m, size_t n, int fill = 0) {
+  void* p = nullptr;
+  const size_t b = n * sizeof(T) > 0 ? n * sizeof(T) : 16;
+  if (cudaMalloc(&p, b) != cudaSuccess) return nullptr;
+  cudaMemset(p, fill, b);
+  m->allocs.push_back(p);
+  return (T*)p;
+}
+
+uint64_t next_pow2(uint64_t x) {
+  uint64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+disc_status fail(disc_map* m, disc_status st, const std::string& msg) {
+  if (m) {
+    m->err = msg;
+    if (st != DISC_ERR_INVALID) m->sticky = st;
+  }
+  return st;
+}
+
+disc_status cuda_check(disc_map* m, const char* where) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(m, DISC_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+  return DISC_OK;
+}
+
+const char* dev_err_text(int code) {
+  switch (code) {
+    case DERR_FRAME_PAIRS: return "per-frame (mask, voxel) pair table full: raise max_pairs_per_frame";
+    case DERR_MAP_KEYS: return "voxel hash full: raise max_memberships";
+    case DERR_OVF_POOL: return "overflow label chunks exhausted: raise max_memberships";
+    case DERR_ARENA: return "instance key-list arena exhausted: raise max_memberships";
+    case DERR_TRIPLES: return "per-frame (segment, instance) count table full";
+    case DERR_INSTANCES: return "max_instances exceeded";
+    case DERR_STAGE: return "per-frame staging list full: raise max_memberships";
+    default: return "device error";
+  }
+}
+
+// synchronise the stream and surface device-side errors
+disc_status sync_check(disc_map* m, cudaStream_t st) {
+  if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_check(m, "cudaStreamSynchronize");
+  if (cudaMemcpy(m->h_err, m->d_err, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return cuda_check(m, "error flag");
+  if (*m->h_err) return fail(m, DISC_ERR_CAPACITY, dev_err_text(*m->h_err));
+  return DISC_OK;
+}
+
+bool pose_rigid(const float* P) {   // A0, S:116-118 (same decision rule as documented in disc.h)
+  for (int i = 0; i < 16; ++i)
+    if (!std::isfinite(P[i])) return false;
+  if (P[12] != 0.0f || P[13] != 0.0f || P[14] != 0.0f || P[15] != 1.0f) return false;
+  double R[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) R[i][j] = (double)P[4 * i + j];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      const double s = R[0][i] * R[0][j] + R[1][i] * R[1][j] + R[2][i] * R[2][j];
+      if (std::fabs(s - (i == j ? 1.0 : 0.0)) > 1e-5) return false;
+    }
+  const double det = R[0][0] * (R[1][1] * R[2][2] - R[1][2] * R[2][1]) -
+                     R[0][1] * (R[1][0] * R[2][2] - R[1][2] * R[2][0]) +
+                     R[0][2] * (R[1][0] * R[2][1] - R[1][1] * R[2][0]);
+  return std::fabs(det - 1.0) <= 1e-5;
+}
+
+std::string validate_frame(const disc_map* m, const disc_frame& f, bool host) {
+  const disc_config& c = m->cfg;
+  if (f.height <= 0 || f.width <= 0) return "bad image dims";
+  if ((int64_t)f.height * f.width > c.max_pixels) return "H*W exceeds max_pixels";
+  if (!f.depth) return "null depth";
+  if (f.num_masks < 0 || f.num_masks > c.max_masks) return "num_masks outside [0, max_masks]";
+  if (f.num_masks > 0 && !f.masks) return "null masks";
+  if (f.patch_h < 1 || f.patch_h > f.height || f.patch_w < 1 || f.patch_w > f.width) return "bad patch grid";
+  if ((int64_t)f.patch_h * f.patch_w > c.max_patches) return "Hp*Wp exceeds max_patches";
+  if (f.patch_w > 65535) return "patch_w too large";
+  if (c.track_dim > 0 && !f.track_feats) return "track_dim > 0 requires track_feats";
+  if (!(f.fx != 0.0f && f.fy != 0.0f) || !std::isfinite(f.fx) || !std::isfinite(f.fy) || !std::isfinite(f.cx) ||
+      !std::isfinite(f.cy))
+    return "bad intrinsics";
+  if (!pose_rigid(f.pose)) return "non-rigid pose";
+  const int rows = (f.height + f.patch_h - 1) / f.patch_h + 3;
+  if (k1_smem_bytes(c.max_masks, f.width, f.patch_w, rows) > 227 * 1024)
+    return "frame too large for the mask-pass tile (S * Wp)";
+  (void)host;
+  return "";
+}
+
+FrameDesc make_desc(const disc_frame& f) {
+  FrameDesc d{};
+  d.depth = f.depth;
+  d.masks = f.masks;
+  d.conf = f.mask_conf;
+  d.feats = f.patch_feats;
+  d.gemb = f.global_embed;
+  d.track = f.track_feats;
+  for (int i = 0; i < 12; ++i) d.pose[i] = f.pose[i];
+  d.fx = f.fx; d.fy = f.fy; d.cx = f.cx; d.cy = f.cy;
+  d.frame_id = f.frame_id;
+  d.H = f.height; d.W = f.width; d.S = f.num_masks; d.Hp = f.patch_h; d.Wp = f.patch_w;
+  d.vec16 = (((int64_t)f.height * f.width) % 16 == 0) && (((uintptr_t)f.masks & 15) == 0);
+  return d;
+}
+
+cudaEvent_t ev_get(disc_map* m) {
+  cudaEvent_t e;
+  if (!m->ev_pool.empty()) {
+    e = m->ev_pool.back();
+    m->ev_pool.pop_back();
+  } else {
+    cudaEventCreate(&e);
+  }
+  return e;
+}
+
+void collect_events(disc_map* m) {
+  for (auto& p : m->ev_pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    if (p.kind == 0) { m->stats.k1_ms += ms; m->stats.k1_launches++; }
+    else if (p.kind == 1) m->stats.stage1_ms += ms;
+    else m->stats.stage2_ms += ms;
+    m->ev_pool.push_back(p.a);
+    m->ev_pool.push_back(p.b);
+  }
+  m->ev_pending.clear();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* disc_version(void) { return VERSION; }
+
+disc_status disc_config_init(disc_config* c) {
+  if (!c) return DISC_ERR_INVALID;
+  std::memset(c, 0, sizeof(*c));
+  c->voxel_size = 0.02f;
+  c->tau_geo = 0.3f;
+  c->tau_vis = 0.8f;
+  c->depth_min = 0.1f;
+  c->depth_max = 10.0f;
+  c->mask_min_conf = 0.5f;
+  c->mask_max_aspect = 10.0f;
+  c->mask_min_area = 400;
+  c->cover_min = 0.25f;
+  c->lambda_size = 3.3f;
+  c->eps_distinct = 1e-6f;
+  c->feat_dim = 1024;
+  c->track_dim = 384;
+  c->max_memberships = 1ll << 22;
+  c->max_instances = 1 << 16;
+  c->max_masks = 64;
+  c->max_pixels = 1280 * 720;
+  c->max_patches = 8192;
+  c->max_pairs_per_frame = 1 << 17;
+  c->window = 16;
+  c->device = 0;
+  c->world_size = 1;
+  c->rank = 0;
+  c->nccl_unique_id = nullptr;
+  return DISC_OK;
+}
+
+static std::string validate_config(const disc_config* c) {
+  if (!(c->voxel_size > 0.0f) || !std::isfinite(c->voxel_size)) return "voxel_size must be > 0";
+  if (!(c->tau_geo > 0.0f && c->tau_geo <= 1.0f)) return "tau_geo must be in (0,1]";
+  if (!(c->tau_vis >= -1.0f && c->tau_vis <= 1.0f)) return "tau_vis must be in [-1,1]";
+  if (!(c->depth_min >= 0.0f && c->depth_min < c->depth_max)) return "bad depth window";
+  if (!(c->mask_min_conf >= 0.0f && c->mask_min_conf <= 1.0f)) return "mask_min_conf in [0,1]";
+  if (!(c->mask_max_aspect >= 1.0f) || c->mask_min_area < 0) return "bad mask filter";
+  if (!(c->cover_min >= 0.0f && c->cover_min <= 1.0f)) return "cover_min in [0,1]";
+  if (!(c->lambda_size > 0.0f) || !(c->eps_distinct >= 0.0f)) return "bad lambda/eps";
+  if (c->feat_dim <= 0 || c->feat_dim % 4 != 0) return "feat_dim must be a positive multiple of 4";
+  if (c->track_dim < 0) return "track_dim must be >= 0";
+  if (c->max_masks < 1 || c->max_masks > 255) return "max_masks in [1,255]";
+  if (c->max_pixels < 1 || c->max_patches < 1) return "bad max_pixels / max_patches";
+  if (c->max_pairs_per_frame < 1 || c->max_pairs_per_frame > (1 << 22)) return "max_pairs_per_frame in [1, 2^22]";
+  if (c->window < 1 || c->window > MAXWIN) return "window in [1,32]";
+  if (c->max_instances < 1 || c->max_instances > (1 << 30)) return "bad max_instances";
+  if (c->max_memberships < 1 || c->max_memberships > (1ll << 31)) return "bad max_memberships";
+  if (c->world_size != 1 || c->rank != 0) return "sharded maps are not supported by this build";
+  return "";
+}
+
+disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
+  if (!cfg || !out) return DISC_ERR_INVALID;
+  *out = nullptr;
+  const std::string v = validate_config(cfg);
+  if (!v.empty()) {
+    std::fprintf(stderr, "disc_map_create: %s\n", v.c_str());
+    return DISC_ERR_INVALID;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev) {
+    cudaGetLastError();
+    std::fprintf(stderr, "disc_map_create: no CUDA device %d\n", cfg->device);
+    return DISC_ERR_CUDA;
+  }
+  cudaSetDevice(cfg->device);
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, cfg->device);
+  if (prop.major != 10) {
+    std::fprintf(stderr, "disc_map_create: libdisc is built for sm_100a (found sm_%d%d)\n", prop.major, prop.minor);
+    return DISC_ERR_UNSUPPORTED;
+  }
+  disc_map* m = new disc_map();
+  m->cfg = *cfg;
+  m->dev = cfg->device;
+  m->nsm = prop.multiProcessorCount;
+  Params& P = m->P;
+  P.r = cfg->voxel_size; P.tau_geo = cfg->tau_geo; P.tau_vis = cfg->tau_vis;
+  P.dmin = cfg->depth_min; P.dmax = cfg->depth_max; P.min_conf = cfg->mask_min_conf;
+  P.max_aspect = cfg->mask_max_aspect; P.cover_min = cfg->cover_min; P.lambda = cfg->lambda_size;
+  P.eps = cfg->eps_distinct; P.min_area = cfg->mask_min_area; P.Df = cfg->feat_dim; P.Dt = cfg->track_dim;
+
+  const int win = cfg->window, SM = cfg->max_masks, Df = cfg->feat_dim, Dt = cfg->track_dim;
+  const int64_t PMAX = cfg->max_pairs_per_frame, PMP = cfg->max_patches;
+  const int64_t PC = (int64_t)next_pow2(std::max<int64_t>(2 * PMAX, 1024));
+  bool ok = true;
+  auto chk = [&](void* p) { ok = ok && p; };
+  // ---- window buffers ----
+  WinBufs& W = m->W;
+  W.PC = (int32_t)PC; W.PMAX = (int32_t)PMAX; W.SMAX = SM; W.PMAXP = (int32_t)PMP;
+  W.FCHUNKS = (int32_t)((PMP + 63) / 64);
+  chk(W.ktab = dalloc<unsigned long long>(m, (size_t)win * PC, 0xFF));
+  chk(W.ptab = dalloc<uint32_t>(m, (size_t)win * PC, 0xFF));
+  chk(W.nsum = dalloc<float>(m, (size_t)win * PC * 3, 0));
+  chk(W.plist = dalloc<uint32_t>(m, (size_t)win * PMAX));
+  chk(W.npairs = dalloc<uint32_t>(m, win));
+  chk(W.cnt = dalloc<uint32_t>(m, (size_t)win * SM * PMP));
+  chk(W.area = dalloc<uint32_t>(m, (size_t)win * SM));
+  chk(W.bbox = dalloc<int32_t>(m, (size_t)win * SM * 4));
+  chk(W.vs = dalloc<uint32_t>(m, (size_t)win * SM));
+  chk(W.daabb = dalloc<int32_t>(m, (size_t)win * SM * 6));
+  chk(W.ang_sum = dalloc<float>(m, (size_t)win * SM));
+  chk(W.ang_cnt = dalloc<uint32_t>(m, (size_t)win * SM));
+  chk(W.oor = dalloc<unsigned long long>(m, win));
+  chk(W.pkey = dalloc<unsigned long long>(m, (size_t)win * PMAX));
+  chk(W.pinfo = dalloc<uint32_t>(m, (size_t)win * PMAX));
+  chk(W.pfk = dalloc<uint32_t>(m, (size_t)win * PMAX));
+  chk(W.pms = dalloc<uint32_t>(m, (size_t)win * PMAX));
+  chk(W.fpart = dalloc<double>(m, (size_t)win * W.FCHUNKS * Df));
+  chk(W.fbar = dalloc<float>(m, (size_t)win * Df));
+  chk(W.rp = dalloc<float>(m, (size_t)win * PMP));
+  chk(W.status = dalloc<int32_t>(m, (size_t)win * SM));
+  chk(W.qf = dalloc<float>(m, (size_t)win * SM * 6));
+  chk(W.emb = dalloc<float>(m, (size_t)win * SM * Df));
+  chk(W.trk = dalloc<double>(m, (size_t)win * SM * std::max(Dt, 1)));
+  chk(W.tok = dalloc<uint8_t>(m, (size_t)win * SM));
+  // ---- map ----
+  MapState& M = m->M;
+  const int64_t IM = cfg->max_instances;
+  M.MC = next_pow2(std::max<int64_t>(2 * cfg->max_memberships, 1024));
+  M.OVFCAP = (uint32_t)std::max<int64_t>(4096, cfg->max_memberships / 8);
+  M.ARENA = (unsigned long long)(8 * cfg->max_memberships + (1 << 20));
+  M.IMAX = (int32_t)IM;
+  chk(M.slots = dalloc<KeySlot>(m, M.MC, 0xFF));
+  chk(M.ovf = dalloc<OvfChunk>(m, M.OVFCAP, 0xFF));
+  chk(M.ovf_top = dalloc<uint32_t>(m, 1));
+  chk(M.alive = dalloc<uint8_t>(m, IM));
+  chk(M.phys_of = dalloc<uint32_t>(m, IM, 0xFF));
+  chk(M.id_of = dalloc<uint32_t>(m, IM, 0xFF));
+  chk(M.vcount = dalloc<int64_t>(m, IM));
+  chk(M.obs = dalloc<int32_t>(m, IM));
+  chk(M.last_seen = dalloc<int64_t>(m, IM));
+  chk(M.aabb = dalloc<int32_t>(m, IM * 6));
+  chk(M.q = dalloc<float>(m, IM));
+  chk(M.E = dalloc<float>(m, (size_t)IM * Df));
+  chk(M.T = dalloc<double>(m, (size_t)IM * std::max(Dt, 1)));
+  chk(M.lst_off = dalloc<unsigned long long>(m, IM));
+  chk(M.lst_len = dalloc<uint32_t>(m, IM));
+  chk(M.lst_cap = dalloc<uint32_t>(m, IM));
+  chk(M.arena = dalloc<uint32_t>(m, M.ARENA));
+  chk(M.arena_top = dalloc<unsigned long long>(m, 1));
+  chk(M.stamp = dalloc<uint32_t>(m, IM));
+  chk(M.local = dalloc<int32_t>(m, IM));
+  chk(M.counters = dalloc<int64_t>(m, 8));
+  chk(m->d_err = dalloc<int>(m, 1));
+  M.err = m->d_err;
+  // ---- per-frame scratch ----
+  FrameScratch& X = m->X;
+  X.CC = 16384;
+  X.TCAP = 4096;
+  X.STCAP = (uint32_t)std::min<int64_t>(cfg->max_memberships + PMAX, 0xFFFFFFF0ll);
+  chk(X.ctab_key = dalloc<unsigned long long>(m, X.CC, 0xFF));
+  chk(X.ctab_cnt = dalloc<uint32_t>(m, X.CC));
+  chk(X.ctab_idx = dalloc<uint32_t>(m, X.TCAP));
+  chk(X.ntrip = dalloc<uint32_t>(m, 1));
+  chk(X.trip_s = dalloc<uint32_t>(m, X.TCAP));
+  chk(X.trip_j = dalloc<uint32_t>(m, X.TCAP));
+  chk(X.trip_c = dalloc<uint32_t>(m, X.TCAP));
+  chk(X.trip_edge = dalloc<uint8_t>(m, X.TCAP));
+  chk(X.det_target = dalloc<int32_t>(m, SM));
+  chk(X.det_id = dalloc<int64_t>(m, SM));
+  chk(X.tgt_phys = dalloc<uint32_t>(m, SM));
+  chk(X.tgt_root = dalloc<uint32_t>(m, SM));
+  chk(X.tgt_stage = dalloc<uint32_t>(m, SM));
+  chk(X.tgt_fill = dalloc<uint32_t>(m, SM));
+  chk(X.tgt_base = dalloc<uint32_t>(m, SM));
+  chk(X.ntgt = dalloc<int32_t>(m, 1));
+  chk(X.seg_phys = dalloc<uint32_t>(m, X.TCAP));
+  chk(X.seg_tgt = dalloc<int32_t>(m, X.TCAP));
+  chk(X.seg_off = dalloc<uint32_t>(m, X.TCAP + 1));
+  chk(X.seg_base = dalloc<unsigned long long>(m, X.TCAP));
+  chk(X.nseg = dalloc<int32_t>(m, 1));
+  chk(X.nrel = dalloc<uint32_t>(m, 1));
+  chk(X.stage_slot = dalloc<uint32_t>(m, X.STCAP));
+  chk(X.stage_tgt = dalloc<uint32_t>(m, X.STCAP));
+  chk(X.nstage = dalloc<uint32_t>(m, 1));
+  chk(X.rep = dalloc<disc_frame_report>(m, MAXWIN));
+  chk(X.live_before = dalloc<int64_t>(m, 1));
+  chk(X.ntrip_last = dalloc<uint32_t>(m, 1));
+  if (cudaMallocHost(&m->h_err, sizeof(int)) != cudaSuccess) ok = false;
+  if (cudaMallocHost(&m->h_rep, sizeof(disc_frame_report) * MAXWIN) != cudaSuccess) ok = false;
+  if (ok && k6_smem_bytes(SM, X.TCAP) > 227 * 1024) ok = false;
+  cudaDeviceSynchronize();
+  if (!ok || cudaGetLastError() != cudaSuccess) {
+    std::fprintf(stderr, "disc_map_create: device allocation failed\n");
+    disc_map_destroy(m);
+    return DISC_ERR_CAPACITY;
+  }
+  *m->h_err = 0;
+  *out = m;
+  return DISC_OK;
+}
+
+void disc_map_destroy(disc_map* m) {
+  if (!m) return;
+  cudaSetDevice(m->dev);
+  cudaDeviceSynchronize();
+  for (void* p : m->allocs) cudaFree(p);
+  if (m->h_err) cudaFreeHost(m->h_err);
+  if (m->h_rep) cudaFreeHost(m->h_rep);
+  if (m->stage) cudaFree(m->stage);
+  if (m->scratch) cudaFree(m->scratch);
+  for (auto& p : m->ev_pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+  for (auto e : m->ev_pool) cudaEventDestroy(e);
+  delete m;
+}
+
+static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t n, void* stream,
+                                  disc_frame_report* reports, bool host_inputs) {
+  if (!m || (!frames && n > 0) || n < 0) return DISC_ERR_INVALID;
+  if (m->sticky != DISC_OK) return m->sticky;
+  cudaSetDevice(m->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  m->last_stream = st;
+  // O0: validate every frame before any mutation
+  for (int i = 0; i < n; ++i) {
+    const std::string v = validate_frame(m, frames[i], host_inputs);
+    if (!v.empty()) return fail(m, DISC_ERR_INVALID, "frame " + std::to_string(i) + ": " + v);
+  }
+  const disc_config& c = m->cfg;
+  const int win = c.window;
+  const int Df = c.feat_dim, Dt = c.track_dim;
+  if (host_inputs && !m->stage) {
+    m->stage_bytes = (size_t)win * ((size_t)c.max_pixels * (4 + c.max_masks) + (size_t)c.max_masks * 4 + 256 +
+                                    (size_t)c.max_patches * ((size_t)Df * 4 + (size_t)Dt * 2) + (size_t)Df * 4 + 4096);
+    if (cudaMalloc((void**)&m->stage, m->stage_bytes) != cudaSuccess) {
+      cudaGetLastError();
+      m->stage = nullptr;
+      return fail(m, DISC_ERR_CAPACITY, "cannot allocate host-input staging buffers");
+    }
+  }
+  for (int w0 = 0; w0 < n; w0 += win) {
+    const int nw = std::min(win, n - w0);
+    WinDesc wd{};
+    wd.n = nw;
+    int maxS = 1, maxHp = 1, maxW = 1, maxWp = 1, maxP = 1, rows = 4;
+    bool sem = false;
+    size_t so = 0;
+    for (int i = 0; i < nw; ++i) {
+      disc_frame f = frames[w0 + i];
+      if (host_inputs) {   // copy this frame's inputs to device staging (stream-ordered)
+        auto put = [&](const void* src, size_t bytes) -> const void* {
+          if (!src || !bytes) return nullptr;
+          so = (so + 255) & ~(size_t)255;
+          void* dst = m->stage + so;
+          cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+          so += bytes;
+          return dst;
+        };
+        const size_t HW = (size_t)f.height * f.width, Pn = (size_t)f.patch_h * f.patch_w;
+        f.depth = (const float*)put(f.depth, HW * 4);
+        f.masks = (const uint8_t*)put(f.masks, HW * f.num_masks);
+        f.mask_conf = (const float*)put(f.mask_conf, (size_t)f.num_masks * 4);
+        f.patch_feats = (const float*)put(f.patch_feats, Pn * Df * 4);
+        f.global_embed = (const float*)put(f.global_embed, (size_t)Df * 4);
+        f.track_feats = (const uint16_t*)put(f.track_feats, Dt > 0 ? Pn * Dt * 2 : 0);
+      }
+      wd.f[i] = make_desc(f);
+      maxS = std::max(maxS, f.num_masks);
+      maxHp = std::max(maxHp, f.patch_h);
+      maxW = std::max(maxW, f.width);
+      maxWp = std::max(maxWp, f.patch_w);
+      maxP = std::max(maxP, f.patch_h * f.patch_w);
+      rows = std::max(rows, (f.height + f.patch_h - 1) / f.patch_h + 3);
+      sem = sem || f.patch_feats != nullptr;
+      m->stats.mask_bytes += (int64_t)f.height * f.width * f.num_masks;
+      m->stats.depth_bytes += (int64_t)f.height * f.width * 4;
+      m->stats.track_bytes += (int64_t)f.patch_h * f.patch_w * Dt * 2;
+      if (f.patch_feats) m->stats.feat_bytes += (int64_t)f.patch_h * f.patch_w * Df * 4;
+    }
+    cudaEvent_t e0 = nullptr, e1 = nullptr, s0 = nullptr, s1 = nullptr, s1b = nullptr, s2 = nullptr;
+    if (m->timing) {
+      e0 = ev_get(m); e1 = ev_get(m); s0 = ev_get(m); s1 = ev_get(m); s1b = ev_get(m); s2 = ev_get(m);
+      cudaEventRecord(s0, st);
+    }
+    launch_stage1(wd, m->W, m->P, m->d_err, sem, maxS, maxHp, maxW, maxWp, maxP, rows, st, e0, e1);
+    if (m->timing) {
+      cudaEventRecord(s1, st);
+      cudaEventRecord(s1b, st);
+    }
+    for (int i = 0; i < nw; ++i) launch_stage2_frame(i, wd.f[i], m->W, m->M, m->X, m->P, sem, m->nsm, st);
+    if (m->timing) {
+      cudaEventRecord(s2, st);
+      m->ev_pending.push_back({e0, e1, 0});
+      m->ev_pending.push_back({s0, s1, 1});
+      m->ev_pending.push_back({s1b, s2, 2});
+    }
+    m->stats.frames += nw;
+    disc_status cs = cuda_check(m, "integrate launch");
+    if (cs != DISC_OK) return cs;
+    if (reports) {
+      cudaMemcpyAsync(m->h_rep, m->X.rep, sizeof(disc_frame_report) * nw, cudaMemcpyDeviceToHost, st);
+      disc_status ss = sync_check(m, st);
+      if (ss != DISC_OK) return ss;
+      std::memcpy(reports + w0, m->h_rep, sizeof(disc_frame_report) * nw);
+    }
+    m->have_last = true;
+    m->last_f = nw - 1;
+    m->last_fd = wd.f[nw - 1];
+    m->last_sem = sem;
+  }
+  if (host_inputs) {   // staging is reused by the next call: keep ordering simple
+    disc_status ss = sync_check(m, st);
+    if (ss != DISC_OK) return ss;
+  }
+  return DISC_OK;
+}
+
+disc_status disc_integrate_frame(disc_map* m, const disc_frame* f, void* stream, disc_frame_report* report) {
+  return integrate_impl(m, f, 1, stream, report, false);
+}
+
+disc_status disc_integrate_frames(disc_map* m, const disc_frame* f, int32_t n, void* stream,
+                                  disc_frame_report* report) {
+  return integrate_impl(m, f, n, stream, report, false);
+}
+
+disc_status disc_integrate_frames_host(disc_map* m, const disc_frame* f, int32_t n, void* stream,
+                                       disc_frame_report* report) {
+  if (!m) return DISC_ERR_INVALID;
+  // the staging buffer holds one window: process window by window
+  const int win = m->cfg.window;
+  for (int w0 = 0; w0 < n; w0 += win) {
+    const int nw = std::min(win, n - w0);
+    disc_status s = integrate_impl(m, f + w0, nw, stream, report ? report + w0 : nullptr, true);
+    if (s != DISC_OK) return s;
+  }
+  return DISC_OK;
+}
+
+static disc_status ensure_scratch(disc_map* m, size_t bytes) {
+  if (m->scratch_bytes >= bytes) return DISC_OK;
+  if (m->scratch) cudaFree(m->scratch);
+  m->scratch = nullptr;
+  m->scratch_bytes = 0;
+  if (cudaMalloc(&m->scratch, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(m, DISC_ERR_CAPACITY, "cannot allocate export scratch");
+  }
+  m->scratch_bytes = bytes;
+  return DISC_OK;
+}
+
+static int64_t host_next_id(disc_map* m) {
+  int64_t nid = 0;
+  cudaMemcpy(&nid, m->M.counters, sizeof(int64_t), cudaMemcpyDeviceToHost);
+  return nid;
+}
+
+disc_status disc_sync(disc_map* m) {
+  if (!m) return DISC_ERR_INVALID;
+  if (m->sticky != DISC_OK) return m->sticky;
+  cudaSetDevice(m->dev);
+  return sync_check(m, m->last_stream);
+}
+
+disc_status disc_query(disc_map* m, const float* q, int32_t k, int64_t* ids, float* scores, int32_t* n_out) {
+  if (!m || !q || k < 0 || (k > 0 && (!ids || !scores)) || !n_out) return DISC_ERR_INVALID;
+  disc_status s = disc_sync(m);
+  if (s != DISC_OK) return s;
+  const int64_t nid = host_next_id(m);
+  const size_t need = (size_t)(nid + 16) * 24 + (size_t)m->cfg.feat_dim * 4 + (16 << 20);
+  if ((s = ensure_scratch(m, need)) != DISC_OK) return s;
+  const int32_t r = run_query(m->M, m->cfg.feat_dim, nid, q, k, ids, scores, m->last_stream, m->scratch, m->scratch_bytes);
+  if (r < 0) return fail(m, DISC_ERR_INTERNAL, "query scratch too small");
+  *n_out = r;
+  return cuda_check(m, "disc_query");
+}
+
+disc_status disc_get_instances(disc_map* m, disc_instance* out, float* embeds, double* track, int32_t cap,
+                               int32_t* n_out) {
+  if (!m || !n_out) return DISC_ERR_INVALID;
+  disc_status s = disc_sync(m);
+  if (s != DISC_OK) return s;
+  const int64_t nid = host_next_id(m);
+  const int Df = m->cfg.feat_dim, Dt = m->cfg.track_dim;
+  const size_t per = sizeof(disc_instance) + (size_t)Df * 4 + (size_t)std::max(Dt, 1) * 8 + 16;
+  const size_t need = (size_t)(nid + 16) * (8 + per) + (16 << 20);
+  if ((s = ensure_scratch(m, need)) != DISC_OK) return s;
+  const int64_t n = export_instances(m->M, Df, Dt, nid, out, embeds, track, out ? cap : 0, m->last_stream,
+                                     m->scratch, m->scratch_bytes);
+  if (n < 0) return fail(m, DISC_ERR_INTERNAL, "export scratch too small");
+  *n_out = (int32_t)n;
+  if (out && n > cap) return fail(m, DISC_ERR_INVALID, "cap too small");
+  return cuda_check(m, "disc_get_instances");
+}
+
+disc_status disc_get_memberships(disc_map* m, uint64_t* keys, int64_t* ids, int64_t cap, int64_t* n_out) {
+  if (!m || !n_out || (keys && !ids)) return DISC_ERR_INVALID;
+  disc_status s = disc_sync(m);
+  if (s != DISC_OK) return s;
+  const size_t need = (size_t)(keys ? cap : 0) * 16 + (1 << 20);
+  if ((s = ensure_scratch(m, need)) != DISC_OK) return s;
+  const int64_t n = export_memberships(m->M, keys, ids, keys ? cap : 0, m->last_stream, m->scratch, m->scratch_bytes);
+  if (n < 0) return fail(m, DISC_ERR_INTERNAL, "export scratch too small");
+  *n_out = n;
+  if (keys && n > cap) return fail(m, DISC_ERR_INVALID, "cap too small");
+  return cuda_check(m, "disc_get_memberships");
+}
+
+disc_status disc_debug_last_frame(disc_map* m, disc_frame_debug* d) {
+  if (!m || !d) return DISC_ERR_INVALID;
+  disc_status s = disc_sync(m);
+  if (s != DISC_OK) return s;
+  if (!m->have_last) return fail(m, DISC_ERR_INVALID, "no frame integrated yet");
+  const int S = m->last_fd.S, f = m->last_f, SM = m->cfg.max_masks, Df = m->cfg.feat_dim, Dt = m->cfg.track_dim;
+  const WinBufs& W = m->W;
+  d->num_masks = S;
+  const size_t fo = (size_t)f * SM;
+  std::vector<int32_t> status(S);
+  cudaMemcpy(status.data(), W.status + fo, 4 * S, cudaMemcpyDeviceToHost);
+  if (d->status) std::memcpy(d->status, status.data(), 4 * S);
+  if (d->area) {
+    std::vector<uint32_t> a(S);
+    cudaMemcpy(a.data(), W.area + fo, 4 * S, cudaMemcpyDeviceToHost);
+    for (int i = 0; i < S; ++i) d->area[i] = a[i];
+  }
+  if (d->bbox) cudaMemcpy(d->bbox, W.bbox + 4 * fo, 16 * S, cudaMemcpyDeviceToHost);
+  if (d->vs) {
+    std::vector<uint32_t> a(S);
+    cudaMemcpy(a.data(), W.vs + fo, 4 * S, cudaMemcpyDeviceToHost);
+    for (int i = 0; i < S; ++i) d->vs[i] = a[i];
+  }
+  if (d->target) cudaMemcpy(d->target, m->X.det_id, 8 * S, cudaMemcpyDeviceToHost);
+  if (d->factors) cudaMemcpy(d->factors, W.qf + 6 * fo, 24 * S, cudaMemcpyDeviceToHost);
+  if (d->embed) cudaMemcpy(d->embed, W.emb + fo * Df, (size_t)4 * S * Df, cudaMemcpyDeviceToHost);
+  if (d->track && Dt > 0) cudaMemcpy(d->track, W.trk + fo * Dt, (size_t)8 * S * Dt, cudaMemcpyDeviceToHost);
+  // pairs of kept detections
+  uint32_t np = 0;
+  cudaMemcpy(&np, W.npairs + f, 4, cudaMemcpyDeviceToHost);
+  np = std::min<uint32_t>(np, (uint32_t)W.PMAX);
+  std::vector<unsigned long long> pk(np);
+  std::vector<uint32_t> ps(np);
+  cudaMemcpy(pk.data(), W.pkey + (size_t)f * W.PMAX, 8ull * np, cudaMemcpyDeviceToHost);
+  cudaMemcpy(ps.data(), W.pinfo + (size_t)f * W.PMAX, 4ull * np, cudaMemcpyDeviceToHost);
+  int64_t k = 0;
+  for (uint32_t i = 0; i < np; ++i) {
+    if (ps[i] >= (uint32_t)S || status[ps[i]] != 0) continue;
+    if (d->pair_s && k < d->pair_cap) {
+      d->pair_s[k] = (int32_t)ps[i];
+      d->pair_key[k] = pk[i];
+    }
+    k++;
+  }
+  d->n_pairs = k;
+  uint32_t nt = 0;
+  cudaMemcpy(&nt, m->X.ntrip_last, 4, cudaMemcpyDeviceToHost);
+  nt = std::min<uint32_t>(nt, (uint32_t)m->X.TCAP);
+  std::vector<uint32_t> ts(nt), tj(nt), tc(nt);
+  std::vector<uint8_t> te(nt);
+  cudaMemcpy(ts.data(), m->X.trip_s, 4ull * nt, cudaMemcpyDeviceToHost);
+  cudaMemcpy(tj.data(), m->X.trip_j, 4ull * nt, cudaMemcpyDeviceToHost);
+  cudaMemcpy(tc.data(), m->X.trip_c, 4ull * nt, cudaMemcpyDeviceToHost);
+  cudaMemcpy(te.data(), m->X.trip_edge, 1ull * nt, cudaMemcpyDeviceToHost);
+  if (d->trip_s)
+    for (uint32_t i = 0; i < nt && i < (uint32_t)d->trip_cap; ++i) {
+      d->trip_s[i] = (int32_t)ts[i];
+      d->trip_j[i] = tj[i];
+      d->trip_c[i] = tc[i];
+      d->trip_edge[i] = te[i];
+    }
+  d->n_trip = nt;
+  return cuda_check(m, "disc_debug_last_frame");
+}
+
+disc_status disc_set_timing(disc_map* m, int32_t on) {
+  if (!m) return DISC_ERR_INVALID;
+  m->timing = on != 0;
+  return DISC_OK;
+}
+
+disc_status disc_get_stats(disc_map* m, disc_stats* s) {
+  if (!m || !s) return DISC_ERR_INVALID;
+  disc_status st = disc_sync(m);
+  if (st != DISC_OK) return st;
+  collect_events(m);
+  *s = m->stats;
+  return DISC_OK;
+}
+
+const char* disc_last_error(const disc_map* m) { return m ? m->err.c_str() : "null map"; }
+
+}  // extern "C"

@@ -1,0 +1,206 @@
+// disc_common.cuh -- device-side types and helpers shared by libdisc's kernels.
+//
+// Product code of the CUDA path.  Shares nothing with oracle/ (the CPU checker).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include "../../include/disc.h"
+
+namespace disc {
+
+constexpr int MAXWIN = 32;
+constexpr uint64_t KEY_EMPTY = ~0ull;       // valid packed keys have bit 63 clear (R6)
+constexpr uint32_t U32_EMPTY = 0xFFFFFFFFu;
+constexpr uint32_t LAB_TOMB = 0xFFFFFFFEu;  // membership label removed by a relabel
+constexpr int KEY_BIAS = 1 << 20;           // R6
+constexpr int INLINE_LABELS = 5;
+constexpr int CHUNK_LABELS = 7;
+
+// error codes raised on the device (sticky; surfaced at synchronising calls)
+enum DevErr : int {
+  DERR_NONE = 0,
+  DERR_FRAME_PAIRS = 1,     // per-frame (s,key) table full
+  DERR_MAP_KEYS = 2,        // voxel hash full
+  DERR_OVF_POOL = 3,        // overflow label chunks exhausted
+  DERR_ARENA = 4,           // per-instance key list arena exhausted
+  DERR_TRIPLES = 5,         // per-frame (s,j) count table full
+  DERR_INSTANCES = 6,       // max_instances exceeded
+  DERR_STAGE = 7,           // per-frame staging list full
+};
+
+// ---- voxel map (stage 2) -------------------------------------------------------------
+// One 32-byte slot per voxel key: the key plus the labels (physical instance labels) of
+// every instance containing it (the membership relation bucketed by key, R12: instances
+// may share voxels).  More than 5 labels spill into 32-byte overflow chunks.
+struct __align__(32) KeySlot {
+  unsigned long long key;
+  uint32_t lab[INLINE_LABELS];
+  uint32_t ovf;
+};
+struct __align__(32) OvfChunk {
+  uint32_t lab[CHUNK_LABELS];
+  uint32_t next;
+};
+
+struct FrameDesc {                // one frame's inputs, passed by value to kernels
+  const float* depth;
+  const uint8_t* masks;
+  const float* conf;
+  const float* feats;
+  const float* gemb;
+  const uint16_t* track;
+  float pose[12];                 // rows 0..2 of the camera->world matrix
+  float fx, fy, cx, cy;
+  int64_t frame_id;
+  int32_t H, W, S, Hp, Wp;
+  int32_t vec16;                  // masks 16-byte vectorisable (H*W % 16 == 0, aligned)
+};
+
+struct WinDesc {
+  FrameDesc f[MAXWIN];
+  int32_t n;
+};
+
+struct Params {                   // method constants
+  float r, tau_geo, tau_vis, dmin, dmax, min_conf, max_aspect, cover_min, lambda, eps;
+  int32_t min_area, Df, Dt;
+};
+
+// ---- per-window stage-1 buffers (device pointers, strides per frame) -----------------
+struct WinBufs {
+  unsigned long long* ktab;   // [win][PC] frame key table (packed key)
+  uint32_t* ptab;             // [win][PC] frame (s,kslot) pair table (code = s<<24 | kslot)
+  float* nsum;                // [win][PC][3] per-pair normal sums (semantic mode)
+  uint32_t* plist;            // [win][PMAX] pair slots in insertion order
+  uint32_t* npairs;           // [win]
+  uint32_t* cnt;              // [win][SMAX][PMAXP] mask pixels per patch
+  uint32_t* area;             // [win][SMAX]
+  int32_t* bbox;              // [win][SMAX][4] umin, vmin, umax, vmax
+  uint32_t* vs;               // [win][SMAX] |V_s|
+  int32_t* daabb;             // [win][SMAX][6] key-space aabb of V_s
+  float* ang_sum;             // [win][SMAX]
+  uint32_t* ang_cnt;          // [win][SMAX]
+  unsigned long long* oor;    // [win] key_out_of_range
+  // pair records for stage 2
+  unsigned long long* pkey;   // [win][PMAX] key
+  uint32_t* pinfo;            // [win][PMAX] mask index s
+  uint32_t* pfk;              // [win][PMAX] frame key-table slot
+  uint32_t* pms;              // [win][PMAX] map slot found by K5 (or U32_EMPTY)
+  // semantic
+  double* fpart;              // [win][FCHUNKS][Df] partial column sums
+  float* fbar;                // [win][Df]
+  float* rp;                  // [win][PMAXP] residual norms r_p
+  int32_t* status;            // [win][SMAX]
+  float* qf;                  // [win][SMAX][6] s_size, s_angle, s_sem, s_dist, q, dbar
+  float* emb;                 // [win][SMAX][Df]
+  double* trk;                // [win][SMAX][Dt]  t_s
+  uint8_t* tok;               // [win][SMAX] t_s defined (nonzero norm)
+  int32_t PC;                 // frame table capacity (power of 2)
+  int32_t PMAX, SMAX, PMAXP, FCHUNKS;
+};
+
+// ---- map state ---------------------------------------------------------------------------
+struct MapState {
+  KeySlot* slots;             // [MC]
+  OvfChunk* ovf;              // [OVFCAP]
+  uint32_t* ovf_top;
+  uint32_t OVFCAP;
+  uint64_t MC;                // power of two
+  // instance table, indexed by id (ids and physical labels share the id space)
+  uint8_t* alive;
+  uint32_t* phys_of;          // id -> physical label of its memberships
+  uint32_t* id_of;            // physical label -> live id
+  int64_t* vcount;
+  int32_t* obs;
+  int64_t* last_seen;
+  int32_t* aabb;              // [6]
+  float* q;
+  float* E;                   // [Df]
+  double* T;                  // [Dt]
+  // per physical label key-slot lists (for relabel enumeration)
+  unsigned long long* lst_off;
+  uint32_t* lst_len;
+  uint32_t* lst_cap;
+  uint32_t* arena;
+  unsigned long long* arena_top;
+  unsigned long long ARENA;
+  int32_t IMAX;
+  uint32_t* stamp;            // [IMAX] K6 generation stamps (instance -> local node id)
+  int32_t* local;             // [IMAX]
+  int64_t* counters;          // [8]: 0 next_id, 1 live_instances, 2 live_memberships, 3 frame gen
+  int* err;
+};
+
+// per-frame stage-2 scratch
+struct FrameScratch {
+  unsigned long long* ctab_key;  // [CC] (s<<32 | j) count table
+  uint32_t* ctab_cnt;            // [CC]
+  uint32_t* ctab_idx;            // [CC] triple index
+  uint32_t* ntrip;               // [1]
+  uint32_t* trip_s;              // [TCAP]
+  uint32_t* trip_j;
+  uint32_t* trip_c;
+  uint8_t* trip_edge;
+  int32_t CC, TCAP;
+  // targets
+  int32_t* det_target;           // [SMAX]  target index or -1
+  int64_t* det_id;               // [SMAX]  instance id fused into (debug)
+  uint32_t* tgt_phys;            // [SMAX]
+  uint32_t* tgt_root;            // [SMAX]
+  uint32_t* tgt_stage;           // [SMAX] staged new entries
+  uint32_t* tgt_fill;            // [SMAX]
+  uint32_t* tgt_base;            // [SMAX]
+  int32_t* ntgt;                 // [1]
+  // relabel segments
+  uint32_t* seg_phys;            // [TCAP] old physical label
+  int32_t* seg_tgt;              // [TCAP]
+  uint32_t* seg_off;             // [TCAP+1] prefix offsets into the relabel item space
+  unsigned long long* seg_base;  // [TCAP] arena offset of the old list
+  int32_t* nseg;                 // [1]
+  uint32_t* nrel;                // [1] total relabel items
+  // staging of new list entries
+  uint32_t* stage_slot;          // [STCAP]
+  uint32_t* stage_tgt;
+  uint32_t* nstage;              // [1]
+  uint32_t STCAP;
+  disc_frame_report* rep;        // [MAXWIN] device reports
+  int64_t* live_before;          // [1]
+  uint32_t* ntrip_last;          // [1] (debug export)
+};
+
+// ---- helpers -------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 30;
+  x *= 0xbf58476d1ce4e5b9ull;
+  x ^= x >> 27;
+  x *= 0x94d049bb133111ebull;
+  x ^= x >> 31;
+  return x;
+}
+__host__ __device__ __forceinline__ uint32_t mix32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+__device__ __forceinline__ uint64_t pack_key(int ix, int iy, int iz) {
+  return ((uint64_t)(uint32_t)(ix + KEY_BIAS) << 42) | ((uint64_t)(uint32_t)(iy + KEY_BIAS) << 21) |
+         (uint64_t)(uint32_t)(iz + KEY_BIAS);
+}
+__device__ __forceinline__ void unpack_key(uint64_t k, int& ix, int& iy, int& iz) {
+  ix = (int)(k >> 42) - KEY_BIAS;
+  iy = (int)((k >> 21) & 0x1FFFFF) - KEY_BIAS;
+  iz = (int)(k & 0x1FFFFF) - KEY_BIAS;
+}
+__device__ __forceinline__ void raise_err(int* err, int code) { atomicMax(err, code); }
+
+template <typename T>
+__device__ __forceinline__ T vload(const T* p) {
+  return *(const volatile T*)p;
+}
+
+}  // namespace disc

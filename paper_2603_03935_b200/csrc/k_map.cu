@@ -1,0 +1,684 @@
+// k_map.cu -- stage 2 of the DISC hot path: the per-frame sequential map update
+// (DESIGN.md §5).  Frame f+1's lookups depend on frame f's merges,
+// so these kernels run per frame, stream-ordered.
+//
+//  K5  k_lookup   every unique (s, key) of the frame probes the voxel hash; each label of
+//                 the key's bucket is one voxel of V_j, so c_sj += 1 (exact |V_s ∩ V_j|,
+//                 P:71), warp-aggregated into a small (s, j) count table
+//  K6  k_assoc    one CTA: exact fp64 threshold (R10) + pinned fp64 visual gate (R15),
+//                 connected components over detections ∪ touched instances (union by
+//                 min-label propagation), survivor = min id (R13), small-to-large physical
+//                 label choice, pinned-order T sums and Q-gated embedding replacement
+//  K7a k_apply    relabel the smaller merged sets in place (insert-if-absent root label,
+//                 tombstone the old one) and insert the frame's detection voxels
+//  K7b k_grow     per target: exact |V| update, grow its key-slot list
+//  K7c k_fill     append new key slots to the lists
+#include "disc_common.cuh"
+#include "disc_launch.h"
+
+namespace disc {
+
+// ------------------------------------------------------------------------------------------
+// voxel hash primitives
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t map_find(const MapState& M, uint64_t key) {
+  uint64_t h = mix64(key) & (M.MC - 1);
+  for (uint64_t probe = 0; probe < M.MC; ++probe) {
+    const unsigned long long k = __ldcg(&M.slots[h].key);
+    if (k == key) return (uint32_t)h;
+    if (k == KEY_EMPTY) return U32_EMPTY;
+    h = (h + 1) & (M.MC - 1);
+  }
+  return U32_EMPTY;
+}
+
+__device__ __forceinline__ uint32_t map_insert_key(const MapState& M, uint64_t key) {
+  uint64_t h = mix64(key) & (M.MC - 1);
+  for (uint64_t probe = 0; probe < M.MC; ++probe) {
+    unsigned long long k = __ldcg(&M.slots[h].key);
+    if (k == key) return (uint32_t)h;
+    if (k == KEY_EMPTY) {
+      k = atomicCAS(&M.slots[h].key, KEY_EMPTY, (unsigned long long)key);
+      if (k == KEY_EMPTY || k == key) return (uint32_t)h;
+    }
+    h = (h + 1) & (M.MC - 1);
+  }
+  raise_err(M.err, DERR_MAP_KEYS);
+  return U32_EMPTY;
+}
+
+// Insert label L into the key's label list unless present.  Linearisable because labels
+// only occupy a prefix of the list (EMPTY is a suffix, never re-created) and L is only ever
+// written by this routine: concurrent inserters of the same L meet at the same first EMPTY
+// cell, where exactly one CAS succeeds.  Returns true iff this call inserted L.
+__device__ bool label_insert(const MapState& M, uint32_t slot, uint32_t L) {
+  uint32_t* labs = M.slots[slot].lab;
+  int n = INLINE_LABELS;
+  uint32_t* next = &M.slots[slot].ovf;
+  while (true) {
+    for (int i = 0; i < n; ++i) {
+      const uint32_t v = __ldcg(&labs[i]);
+      if (v == L) return false;
+      if (v == U32_EMPTY) {
+        const uint32_t old = atomicCAS(&labs[i], U32_EMPTY, L);
+        if (old == U32_EMPTY) return true;
+        if (old == L) return false;
+      }
+    }
+    uint32_t nx = __ldcg(next);
+    if (nx == U32_EMPTY) {
+      const uint32_t c = atomicAdd(M.ovf_top, 1u);
+      if (c >= M.OVFCAP) {
+        raise_err(M.err, DERR_OVF_POOL);
+        return false;
+      }
+      const uint32_t old = atomicCAS(next, U32_EMPTY, c);
+      nx = (old == U32_EMPTY) ? c : old;   // a losing chunk is leaked (rare)
+    }
+    labs = M.ovf[nx].lab;
+    n = CHUNK_LABELS;
+    next = &M.ovf[nx].next;
+  }
+}
+
+// Replace label L of the key by a tombstone (only the relabel of L's owner touches L).
+__device__ bool label_tomb(const MapState& M, uint32_t slot, uint32_t L) {
+  uint32_t* labs = M.slots[slot].lab;
+  int n = INLINE_LABELS;
+  uint32_t nx = __ldcg(&M.slots[slot].ovf);
+  while (true) {
+    for (int i = 0; i < n; ++i) {
+      const uint32_t v = __ldcg(&labs[i]);
+      if (v == L) {
+        atomicExch(&labs[i], LAB_TOMB);
+        return true;
+      }
+      if (v == U32_EMPTY) return false;
+    }
+    if (nx == U32_EMPTY) return false;
+    labs = M.ovf[nx].lab;
+    n = CHUNK_LABELS;
+    nx = __ldcg(&M.ovf[nx].next);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// K5: lookup + overlap counts
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void count_add(const FrameScratch& X, uint64_t code, uint32_t add, int* err) {
+  uint32_t h = (uint32_t)mix64(code) & (uint32_t)(X.CC - 1);
+  for (int probe = 0; probe < X.CC; ++probe) {
+    unsigned long long k = __ldcg(&X.ctab_key[h]);
+    if (k == KEY_EMPTY) {
+      k = atomicCAS(&X.ctab_key[h], KEY_EMPTY, (unsigned long long)code);
+      if (k == KEY_EMPTY) {
+        const uint32_t t = atomicAdd(X.ntrip, 1u);
+        if (t < (uint32_t)X.TCAP) {
+          X.trip_s[t] = (uint32_t)(code >> 32);
+          X.trip_j[t] = (uint32_t)code;
+          X.ctab_idx[t] = h;   // slot of triple t
+        } else {
+          raise_err(err, DERR_TRIPLES);
+        }
+        k = code;
+      }
+    }
+    if (k == code) {
+      atomicAdd(&X.ctab_cnt[h], add);
+      return;
+    }
+    h = (h + 1) & (uint32_t)(X.CC - 1);
+  }
+  raise_err(err, DERR_TRIPLES);
+}
+
+__global__ void __launch_bounds__(256) k_lookup(int f, WinBufs wb, MapState M, FrameScratch X) {
+  const uint32_t np = min(wb.npairs[f], (uint32_t)wb.PMAX);
+  const size_t fo = (size_t)f * wb.PMAX;
+  const int lane = threadIdx.x & 31;
+  unsigned long long* ktab = wb.ktab + (size_t)f * wb.PC;
+  const int32_t* status = wb.status + (size_t)f * wb.SMAX;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < np; base += stride) {
+    const uint32_t idx = base + lane;
+    uint64_t code = KEY_EMPTY;   // first label's (s, j)
+    uint32_t s = 0, slot = U32_EMPTY;
+    if (idx < np) {
+      s = wb.pinfo[fo + idx];
+      ktab[wb.pfk[fo + idx]] = KEY_EMPTY;   // release the frame key-table cell
+      if (status[s] == 0) {
+        slot = map_find(M, wb.pkey[fo + idx]);
+        if (slot != U32_EMPTY) {
+          const KeySlot& ks = M.slots[slot];
+          int nl = 0;
+          for (int i = 0; i < INLINE_LABELS; ++i) {
+            const uint32_t L = ks.lab[i];
+            if (L == U32_EMPTY) break;
+            if (L == LAB_TOMB) continue;
+            const uint64_t c = ((uint64_t)s << 32) | M.id_of[L];
+            if (nl == 0) code = c;
+            else count_add(X, c, 1, M.err);
+            nl++;
+          }
+          uint32_t nx = ks.ovf;
+          while (nx != U32_EMPTY) {
+            const OvfChunk& oc = M.ovf[nx];
+            for (int i = 0; i < CHUNK_LABELS; ++i) {
+              const uint32_t L = oc.lab[i];
+              if (L == U32_EMPTY) break;
+              if (L == LAB_TOMB) continue;
+              const uint64_t c = ((uint64_t)s << 32) | M.id_of[L];
+              if (nl == 0) code = c;
+              else count_add(X, c, 1, M.err);
+              nl++;
+            }
+            nx = oc.next;
+          }
+        }
+      }
+      wb.pms[fo + idx] = slot;
+    }
+    // warp aggregation of the first label's count (most keys carry one label)
+    const unsigned peers = __match_any_sync(0xffffffffu, code);
+    if (code != KEY_EMPTY && lane == __ffs(peers) - 1) count_add(X, code, __popc(peers), M.err);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// K6: association (single CTA)
+// ------------------------------------------------------------------------------------------
+constexpr int K6_THREADS = 1024;
+
+__device__ __forceinline__ double dot_pin_w(const double* a, const double* b, int n) {
+  const int lane = threadIdx.x & 31;
+  double acc = 0.0;
+  for (int d = lane; d < n; d += 32) acc = __fma_rn(a[d], b[d], acc);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+  return acc;
+}
+
+struct K6Smem {   // offsets into dynamic shared memory
+  size_t t_s, t_j, t_c, t_e, t_jl, lab, jnode, comp_root, comp_best, comp_tgt, has_edge, total;
+  __host__ __device__ K6Smem(int S, int TC) {
+    size_t o = 0;
+    auto take = [&](size_t bytes) { const size_t r = o; o = (o + bytes + 15) & ~(size_t)15; return r; };
+    const size_t NN = (size_t)S + TC;
+    t_s = take(4 * (size_t)TC); t_j = take(4 * (size_t)TC); t_c = take(4 * (size_t)TC);
+    t_e = take((size_t)TC); t_jl = take(4 * (size_t)TC); lab = take(4 * NN); jnode = take(4 * (size_t)TC);
+    comp_root = take(4 * NN); comp_best = take(8 * NN); comp_tgt = take(4 * NN); has_edge = take((size_t)S + 1);
+    total = o;
+  }
+};
+
+__global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBufs wb, MapState M,
+                                                      FrameScratch X, Params P, int sem) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int TC = X.TCAP;
+  const int S = F.S;
+  const K6Smem L6(S, TC);
+  uint32_t* t_s = (uint32_t*)(smem_raw + L6.t_s);          // triple s
+  uint32_t* t_j = (uint32_t*)(smem_raw + L6.t_j);          // triple j (instance id)
+  uint32_t* t_c = (uint32_t*)(smem_raw + L6.t_c);          // c_sj
+  uint8_t* t_e = (uint8_t*)(smem_raw + L6.t_e);            // edge flag
+  int32_t* t_jl = (int32_t*)(smem_raw + L6.t_jl);          // local instance index
+  int32_t* lab = (int32_t*)(smem_raw + L6.lab);            // [S + nJ] component label
+  uint32_t* jnode = (uint32_t*)(smem_raw + L6.jnode);      // local index -> id
+  uint32_t* comp_root = (uint32_t*)(smem_raw + L6.comp_root);
+  unsigned long long* comp_best = (unsigned long long*)(smem_raw + L6.comp_best);
+  int32_t* comp_tgt = (int32_t*)(smem_raw + L6.comp_tgt);
+  uint8_t* has_edge = (uint8_t*)(smem_raw + L6.has_edge);
+  __shared__ uint32_t n_tr, n_j, n_tgt, n_seg;
+  __shared__ int changed;
+  __shared__ unsigned long long rel_s, merged_s, edges_s;
+  __shared__ uint32_t gen;
+
+  const size_t fo = (size_t)f * wb.SMAX;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+  if (tid == 0) {
+    n_tr = min(*X.ntrip, (uint32_t)TC);
+    if (*X.ntrip > (uint32_t)TC) raise_err(M.err, DERR_TRIPLES);
+    n_j = 0; n_tgt = 0; n_seg = 0; rel_s = 0; merged_s = 0; edges_s = 0;
+    gen = (uint32_t)(++M.counters[3]);
+    *X.nstage = 0;
+    *X.nrel = 0;
+  }
+  for (int i = tid; i < S + TC; i += blockDim.x) {
+    lab[i] = i;
+    comp_root[i] = U32_EMPTY;
+    comp_best[i] = 0;
+    comp_tgt[i] = -1;
+  }
+  for (int i = tid; i < S; i += blockDim.x) {
+    has_edge[i] = 0;
+    X.det_target[i] = -1;
+    X.det_id[i] = -1;
+    X.tgt_stage[i] = 0;
+  }
+  __syncthreads();
+  const uint32_t ntr = n_tr;
+  // ---- triples: load and release the count table ----
+  for (uint32_t t = tid; t < ntr; t += blockDim.x) {
+    const uint32_t h = X.ctab_idx[t];
+    t_s[t] = X.trip_s[t];
+    t_j[t] = X.trip_j[t];
+    t_c[t] = X.ctab_cnt[h];
+    X.ctab_cnt[h] = 0;
+    X.ctab_key[h] = KEY_EMPTY;
+  }
+  __syncthreads();
+  // ---- O10 edges: exact fp64 geometric test (R10) + pinned fp64 visual gate (R15) ----
+  const double* trk = wb.trk + fo * P.Dt;
+  for (uint32_t t = warp; t < ntr; t += nwarp) {
+    const uint32_t s = t_s[t], j = t_j[t], c = t_c[t];
+    const int64_t vs = wb.vs[fo + s], vj = M.vcount[j];
+    const int64_t mn = vs < vj ? vs : vj;
+    bool e = c >= 1 && (double)c >= (double)P.tau_geo * (double)mn;
+    if (e && P.Dt > 0) {
+      const double* Tj = M.T + (size_t)j * P.Dt;
+      const double TT = dot_pin_w(Tj, Tj, P.Dt);
+      const double dt = dot_pin_w(trk + (size_t)s * P.Dt, Tj, P.Dt);
+      double cosv = -2.0;
+      if (wb.tok[fo + s] && TT > 0.0) cosv = __ddiv_rn(dt, __dsqrt_rn(TT));
+      e = cosv >= (double)P.tau_vis;
+    }
+    if (lane == 0) t_e[t] = e ? 1 : 0;
+  }
+  __syncthreads();
+  // ---- distinct instances among the edges -> local node S + l (generation stamps) ----
+  for (uint32_t t = tid; t < ntr; t += blockDim.x) {
+    if (!t_e[t]) continue;
+    has_edge[t_s[t]] = 1;
+    const uint32_t j = t_j[t];
+    if (atomicExch(&M.stamp[j], gen) != gen) {
+      const uint32_t l = atomicAdd(&n_j, 1u);
+      M.local[j] = (int32_t)l;
+      jnode[l] = j;
+    }
+  }
+  __syncthreads();
+  for (uint32_t t = tid; t < ntr; t += blockDim.x) t_jl[t] = t_e[t] ? M.local[t_j[t]] : -1;
+  __syncthreads();
+  const int nJ = (int)n_j;
+  const int NN = S + nJ;
+  // ---- O11 components: min-label propagation with pointer jumping ----
+  while (true) {
+    if (tid == 0) changed = 0;
+    __syncthreads();
+    for (uint32_t t = tid; t < ntr; t += blockDim.x) {
+      if (!t_e[t]) continue;
+      const int a = (int)t_s[t], b = S + t_jl[t];
+      const int la = lab[a], lb = lab[b];
+      if (la != lb) {
+        const int m = la < lb ? la : lb;
+        atomicMin(&lab[a], m);
+        atomicMin(&lab[b], m);
+        atomicMin(&lab[la], m);
+        atomicMin(&lab[lb], m);
+        changed = 1;
+      }
+    }
+    __syncthreads();
+    for (int x = tid; x < NN; x += blockDim.x) {
+      int l = lab[x];
+      while (lab[l] != l) l = lab[l];
+      lab[x] = l;
+    }
+    __syncthreads();
+    if (!changed) break;
+    __syncthreads();
+  }
+  // ---- per component: root = min id (R13), physical owner = max |V| (ties: min id) ----
+  for (int l = tid; l < nJ; l += blockDim.x) {
+    const int Lb = lab[S + l];
+    const uint32_t j = jnode[l];
+    atomicMin(&comp_root[Lb], j);
+    const unsigned long long key = ((unsigned long long)(uint64_t)M.vcount[j] << 32) | (0x7FFFFFFFu - j);
+    atomicMax(&comp_best[Lb], key);
+  }
+  __syncthreads();
+  for (int x = tid; x < NN; x += blockDim.x) {
+    if (lab[x] == x && comp_root[x] != U32_EMPTY) {
+      const int t = (int)atomicAdd(&n_tgt, 1u);
+      comp_tgt[x] = t;
+      const uint32_t owner = 0x7FFFFFFFu - (uint32_t)(comp_best[x] & 0xFFFFFFFFull);
+      X.tgt_root[t] = comp_root[x];
+      X.tgt_phys[t] = M.phys_of[owner];
+    }
+  }
+  __syncthreads();
+  // ---- detections: component members, isolated kept ones -> new ids ascending s (R13) ----
+  if (tid == 0) {
+    int64_t nid = M.counters[0];
+    int64_t created = 0;
+    for (int s = 0; s < S; ++s) {
+      if (wb.status[fo + s] != 0) continue;
+      if (has_edge[s]) {
+        const int t = comp_tgt[lab[s]];
+        X.det_target[s] = t;
+        X.det_id[s] = X.tgt_root[t];
+      } else {
+        if (nid >= M.IMAX) {
+          raise_err(M.err, DERR_INSTANCES);
+          break;
+        }
+        const int t = (int)n_tgt++;
+        X.det_target[s] = t;
+        X.det_id[s] = nid;
+        X.tgt_root[t] = (uint32_t)nid;
+        X.tgt_phys[t] = (uint32_t)nid;
+        nid++;
+        created++;
+      }
+    }
+    M.counters[0] = nid;
+    M.counters[1] += created;
+    X.rep[f].created = created;
+  }
+  __syncthreads();
+  // ---- O12 apply, one warp per component ----
+  for (int x = warp; x < NN; x += nwarp) {
+    if (lab[x] != x || comp_tgt[x] < 0) continue;
+    const int t = comp_tgt[x];
+    const uint32_t root = X.tgt_root[t];
+    const uint32_t Pl = X.tgt_phys[t];
+    const uint32_t owner = M.id_of[Pl];
+    int32_t obs = M.obs[root];
+    int32_t ab[6];
+    for (int k = 0; k < 6; ++k) ab[k] = M.aabb[(size_t)root * 6 + k];
+    float qcur = M.q[root];
+    int src_kind = 0;      // 0 keep, 1 instance src_id, 2 detection src_id
+    uint32_t src_id = root;
+    uint32_t prev = root;
+    unsigned long long rel = 0;
+    int nmerged = 0;
+    double* Tr = M.T + (size_t)root * P.Dt;
+    // other members J ascending: obs, aabb, T (pinned order), (e,Q) strict >
+    while (true) {
+      uint32_t best = U32_EMPTY;
+      for (int l = lane; l < nJ; l += 32)
+        if (lab[S + l] == x && jnode[l] > prev && jnode[l] < best) best = jnode[l];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+      if (best == U32_EMPTY) break;
+      prev = best;
+      const uint32_t m = best;
+      obs += M.obs[m];
+      for (int k = 0; k < 3; ++k) {
+        ab[k] = min(ab[k], M.aabb[(size_t)m * 6 + k]);
+        ab[3 + k] = max(ab[3 + k], M.aabb[(size_t)m * 6 + 3 + k]);
+      }
+      if (M.q[m] > qcur) { qcur = M.q[m]; src_kind = 1; src_id = m; }
+      const double* Tm = M.T + (size_t)m * P.Dt;
+      for (int d = lane; d < P.Dt; d += 32) Tr[d] = __dadd_rn(Tr[d], Tm[d]);
+      rel += (unsigned long long)M.vcount[m];
+      nmerged++;
+    }
+    // detections Sd ascending
+    for (int s = 0; s < S; ++s) {
+      if (X.det_target[s] != t) continue;
+      obs += 1;
+      for (int k = 0; k < 3; ++k) {
+        ab[k] = min(ab[k], wb.daabb[(fo + s) * 6 + k]);
+        ab[3 + k] = max(ab[3 + k], wb.daabb[(fo + s) * 6 + 3 + k]);
+      }
+      const float qs = wb.qf[(fo + s) * 6 + 4];
+      if (qs > qcur) { qcur = qs; src_kind = 2; src_id = (uint32_t)s; }
+      const double* ts = trk + (size_t)s * P.Dt;
+      for (int d = lane; d < P.Dt; d += 32) Tr[d] = __dadd_rn(Tr[d], ts[d]);
+    }
+    if (src_kind != 0) {
+      const float* src = src_kind == 1 ? M.E + (size_t)src_id * P.Df : wb.emb + (fo + src_id) * P.Df;
+      for (int d = lane; d < P.Df; d += 32) M.E[(size_t)root * P.Df + d] = src[d];
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const int64_t vbase = M.vcount[owner];
+      for (int l = 0; l < nJ; ++l) {
+        if (lab[S + l] != x) continue;
+        const uint32_t m = jnode[l];
+        const uint32_t pm = M.phys_of[m];
+        if (pm != Pl) {   // the smaller sets: relabel into the owner's physical label
+          const uint32_t sg = atomicAdd(&n_seg, 1u);
+          if (sg < (uint32_t)TC) {
+            X.seg_phys[sg] = pm;
+            X.seg_tgt[sg] = t;
+            X.seg_base[sg] = M.lst_off[pm];
+            X.seg_off[sg] = M.lst_len[pm];
+          } else {
+            raise_err(M.err, DERR_TRIPLES);
+          }
+          M.lst_len[pm] = 0;
+          M.lst_cap[pm] = 0;
+        }
+        if (m != root) {
+          M.alive[m] = 0;
+          M.phys_of[m] = U32_EMPTY;
+        }
+      }
+      M.obs[root] = obs;
+      M.last_seen[root] = F.frame_id;
+      for (int k = 0; k < 6; ++k) M.aabb[(size_t)root * 6 + k] = ab[k];
+      M.q[root] = qcur;
+      M.vcount[root] = vbase;
+      M.phys_of[root] = Pl;
+      M.id_of[Pl] = root;
+      atomicAdd(&rel_s, rel);
+      atomicAdd(&merged_s, (unsigned long long)nmerged);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  // ---- new instances (isolated kept detections) ----
+  for (int s = warp; s < S; s += nwarp) {
+    const int t = X.det_target[s];
+    if (t < 0 || has_edge[s]) continue;
+    const uint32_t id = X.tgt_root[t];
+    if (lane == 0) {
+      M.alive[id] = 1;
+      M.phys_of[id] = id;
+      M.id_of[id] = id;
+      M.vcount[id] = 0;
+      M.obs[id] = 1;
+      M.last_seen[id] = F.frame_id;
+      for (int k = 0; k < 6; ++k) M.aabb[(size_t)id * 6 + k] = wb.daabb[(fo + s) * 6 + k];
+      M.q[id] = wb.qf[(fo + s) * 6 + 4];
+      M.lst_len[id] = 0;
+      M.lst_cap[id] = 0;
+    }
+    for (int d = lane; d < P.Dt; d += 32) M.T[(size_t)id * P.Dt + d] = trk[(size_t)s * P.Dt + d];
+    const bool has_e = sem && wb.qf[(fo + s) * 6 + 4] >= 0.f;
+    for (int d = lane; d < P.Df; d += 32) M.E[(size_t)id * P.Df + d] = has_e ? wb.emb[(fo + s) * P.Df + d] : 0.f;
+  }
+  // ---- debug copies of the triples, edge count ----
+  for (uint32_t t = tid; t < ntr; t += blockDim.x) {
+    X.trip_c[t] = t_c[t];
+    X.trip_edge[t] = t_e[t];
+    if (t_e[t]) atomicAdd(&edges_s, 1ull);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const uint32_t ns = min(n_seg, (uint32_t)TC);
+    uint32_t acc = 0;
+    for (uint32_t g = 0; g < ns; ++g) {
+      const uint32_t len = X.seg_off[g];
+      X.seg_off[g] = acc;
+      acc += len;
+    }
+    X.seg_off[ns] = acc;
+    *X.nseg = (int)ns;
+    *X.nrel = acc;
+    *X.ntgt = (int)n_tgt;
+    disc_frame_report& R = X.rep[f];
+    int kept = 0, da = 0, dc = 0, dasp = 0, dnd = 0, dnf = 0;
+    int64_t U = 0;
+    for (int s = 0; s < S; ++s) {
+      switch (wb.status[fo + s]) {
+        case 0: kept++; U += wb.vs[fo + s]; break;
+        case 1: da++; break;
+        case 2: dc++; break;
+        case 3: dasp++; break;
+        case 4: dnd++; break;
+        default: dnf++; break;
+      }
+    }
+    R.kept = kept; R.drop_area = da; R.drop_conf = dc; R.drop_aspect = dasp;
+    R.drop_nodepth = dnd; R.drop_nofeat = dnf;
+    R.key_out_of_range = (int64_t)wb.oor[f];
+    R.unique_pairs = U;
+    R.edges = (int64_t)edges_s;
+    R.merged_away = (int64_t)merged_s;
+    R.relabeled = (int64_t)rel_s;
+    M.counters[1] -= (int64_t)merged_s;
+    R.live_instances = M.counters[1];
+    *X.live_before = M.counters[2];
+    *X.ntrip_last = ntr;
+    *X.ntrip = 0;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// K7a: apply — detection inserts + relabel of the smaller sets (small-to-large)
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_apply(int f, WinBufs wb, MapState M, FrameScratch X) {
+  const uint32_t np = min(wb.npairs[f], (uint32_t)wb.PMAX);
+  const uint32_t nrel = *X.nrel;
+  const uint32_t total = np + nrel;
+  const size_t fo = (size_t)f * wb.PMAX;
+  const int nseg = *X.nseg;
+  const int lane = threadIdx.x & 31;
+  __shared__ int delta_s;
+  if (threadIdx.x == 0) delta_s = 0;
+  __syncthreads();
+  int delta = 0;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < total; base += stride) {
+    const uint32_t it = base + lane;
+    int tnew = -1;
+    uint32_t snew = 0;
+    if (it < np) {
+      const uint32_t s = wb.pinfo[fo + it];
+      const int t = X.det_target[s];
+      if (t >= 0) {
+        const uint32_t L = X.tgt_phys[t];
+        uint32_t slot = wb.pms[fo + it];
+        if (slot == U32_EMPTY) slot = map_insert_key(M, wb.pkey[fo + it]);
+        if (slot != U32_EMPTY && label_insert(M, slot, L)) { tnew = t; snew = slot; delta++; }
+      }
+    } else if (it < total) {
+      const uint32_t r = it - np;
+      int lo = 0, hi = nseg - 1;   // last segment with seg_off <= r
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (X.seg_off[mid] <= r) lo = mid;
+        else hi = mid - 1;
+      }
+      const int t = X.seg_tgt[lo];
+      const uint32_t L = X.tgt_phys[t];
+      const uint32_t slot = M.arena[X.seg_base[lo] + (r - X.seg_off[lo])];
+      if (label_insert(M, slot, L)) { tnew = t; snew = slot; delta++; }
+      if (label_tomb(M, slot, X.seg_phys[lo])) delta--;
+    }
+    // warp-aggregated staging of the new (target, slot) entries
+    const unsigned peers = __match_any_sync(0xffffffffu, tnew);
+    if (tnew >= 0 && lane == __ffs(peers) - 1) atomicAdd(&X.tgt_stage[tnew], (uint32_t)__popc(peers));
+    const unsigned b = __ballot_sync(0xffffffffu, tnew >= 0);
+    if (b) {
+      uint32_t sb = 0;
+      if (lane == 0) sb = atomicAdd(X.nstage, (uint32_t)__popc(b));
+      sb = __shfl_sync(0xffffffffu, sb, 0);
+      if (tnew >= 0) {
+        const uint32_t i = sb + __popc(b & ((1u << lane) - 1u));
+        if (i < X.STCAP) {
+          X.stage_slot[i] = snew;
+          X.stage_tgt[i] = (uint32_t)tnew;
+        } else {
+          raise_err(M.err, DERR_STAGE);
+        }
+      }
+    }
+  }
+  if (delta) atomicAdd(&delta_s, delta);
+  __syncthreads();
+  if (threadIdx.x == 0 && delta_s) atomicAdd((unsigned long long*)&M.counters[2], (unsigned long long)(int64_t)delta_s);
+}
+
+// K7b: per target — |V| update and list growth
+__global__ void __launch_bounds__(256) k_grow(int f, MapState M, FrameScratch X) {
+  const int ntgt = *X.ntgt;
+  const int t = blockIdx.x;
+  if (t == 0 && threadIdx.x == 0) {
+    disc_frame_report& R = X.rep[f];
+    R.live_memberships = M.counters[2];
+    R.new_memberships = M.counters[2] - *X.live_before;
+  }
+  if (t >= ntgt) return;
+  const uint32_t L = X.tgt_phys[t];
+  const uint32_t root = X.tgt_root[t];
+  const uint32_t add = X.tgt_stage[t];
+  __shared__ unsigned long long newoff;
+  __shared__ uint32_t oldlen, grow;
+  if (threadIdx.x == 0) {
+    M.vcount[root] += add;
+    oldlen = M.lst_len[L];
+    const uint32_t need = oldlen + add;
+    grow = 0;
+    if (need > M.lst_cap[L]) {
+      const uint32_t nc = max(max(2 * M.lst_cap[L], need), 64u);
+      const unsigned long long off = atomicAdd(M.arena_top, (unsigned long long)nc);
+      if (off + nc > M.ARENA) {
+        raise_err(M.err, DERR_ARENA);
+      } else {
+        newoff = off;
+        grow = 1;
+        M.lst_cap[L] = nc;
+      }
+    }
+    X.tgt_base[t] = oldlen;
+    X.tgt_fill[t] = 0;
+  }
+  __syncthreads();
+  if (grow) {
+    const unsigned long long src = M.lst_off[L];
+    for (uint32_t i = threadIdx.x; i < oldlen; i += blockDim.x) M.arena[newoff + i] = M.arena[src + i];
+    __syncthreads();
+    if (threadIdx.x == 0) M.lst_off[L] = newoff;
+  }
+  if (threadIdx.x == 0) M.lst_len[L] = oldlen + add;
+}
+
+// K7c: fill the appended list cells (warp-aggregated positions)
+__global__ void __launch_bounds__(256) k_fill(MapState M, FrameScratch X) {
+  const uint32_t n = min(*X.nstage, X.STCAP);
+  const int lane = threadIdx.x & 31;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
+    const uint32_t i = base + lane;
+    const int t = i < n ? (int)X.stage_tgt[i] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, t);
+    const int leader = __ffs(peers) - 1;
+    uint32_t pb = 0;
+    if (t >= 0 && lane == leader) pb = atomicAdd(&X.tgt_fill[t], (uint32_t)__popc(peers));
+    pb = __shfl_sync(0xffffffffu, pb, leader);
+    if (t >= 0) {
+      const uint32_t L = X.tgt_phys[t];
+      const uint32_t pos = X.tgt_base[t] + pb + __popc(peers & ((1u << lane) - 1u));
+      M.arena[M.lst_off[L] + pos] = X.stage_slot[i];
+    }
+  }
+}
+
+size_t k6_smem_bytes(int S, int TC) { return K6Smem(S, TC).total; }
+
+void launch_stage2_frame(int f, const FrameDesc& F, const WinBufs& wb, const MapState& M, const FrameScratch& X,
+                         const Params& P, bool sem, int nsm, cudaStream_t st) {
+  k_lookup<<<2 * nsm, 256, 0, st>>>(f, wb, M, X);
+  const size_t sm6 = k6_smem_bytes(wb.SMAX, X.TCAP);
+  cudaFuncSetAttribute(k_assoc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm6);
+  k_assoc<<<1, K6_THREADS, sm6, st>>>(f, F, wb, M, X, P, sem ? 1 : 0);
+  k_apply<<<2 * nsm, 256, 0, st>>>(f, wb, M, X);
+  k_grow<<<wb.SMAX, 256, 0, st>>>(f, M, X);
+  k_fill<<<nsm, 256, 0, st>>>(M, X);
+}
+
+}  // namespace disc

@@ -87,6 +87,8 @@ class SceneConfig:
     min_area: int = 400
     overlap_masks: bool = False         # X: SAM-"everything" hierarchical masks
     traj: str = "orbit"
+    pieces: tuple = (2, 4)              # Voronoi pieces per large room surface per frame
+    split_frac: float = 0.04            # objects covering more of the image are split 1-3x
     extra: dict = field(default_factory=dict)
 
 
@@ -98,12 +100,14 @@ CONFIGS = {
     "T": SceneConfig("T", 48, 64, 32.0, 32.0, 32.0, 24.0, 0.05, 4, 16, 16, 64, 32, 3,
                      scene="tiny", n_objects=3, min_area=8, traj="tiny"),
     "R": SceneConfig("R", 680, 1200, 600.0, 600.0, 599.5, 339.5, 0.02, 40, _hp(680), _hp(1200),
-                     1024, 384, 2000, room=(6.5, 5.0, 3.0), n_objects=60, traj="orbit"),
+                     1024, 384, 2000, room=(6.5, 5.0, 3.0), n_objects=140, traj="orbit", pieces=(4, 8),
+                     split_frac=0.02),
     "N": SceneConfig("N", 480, 640, 577.6, 578.7, 318.9, 242.7, 0.05, 30, _hp(480), _hp(640),
-                     1024, 384, 5000, room=(7.0, 6.0, 3.0), n_objects=40, noise=True,
-                     valid_max=4.5, traj="handheld"),
+                     1024, 384, 5000, room=(7.0, 6.0, 3.0), n_objects=90, noise=True,
+                     valid_max=4.5, traj="handheld", pieces=(3, 6), split_frac=0.03),
     "H": SceneConfig("H", 480, 640, 320.0, 320.0, 320.0, 240.0, 0.02, 60, _hp(480), _hp(640),
-                     1024, 384, 20000, scene="building", n_objects=2400, traj="tour"),
+                     1024, 384, 20000, scene="building", n_objects=2400, traj="tour", pieces=(3, 6),
+                     split_frac=0.02),
     "X": SceneConfig("X", 480, 640, 577.6, 578.7, 318.9, 242.7, 0.05, 50, _hp(480), _hp(640),
                      1024, 384, 300, room=(7.0, 6.0, 3.0), n_objects=40, overlap_masks=True,
                      traj="handheld"),
@@ -400,9 +404,9 @@ class Generator:
             obj = ax * 2 + side
         # boxes, culled to those near the camera
         lo, hi, bobj = self.lo, self.hi, self.box_obj
-        if lo.shape[0] > 64:
-            ctr = 0.5 * (lo + hi)
-            near = ((ctr - o).norm(dim=1) < cfg.valid_max + 3.0) & (lo[:, 2] < o[2] + 2.5) & (hi[:, 2] > o[2] - 2.5)
+        if lo.shape[0] > 64:   # cull boxes farther than the valid depth range (closest point)
+            closest = torch.minimum(torch.maximum(o, lo), hi)
+            near = ((closest - o).norm(dim=1) < cfg.valid_max + 0.5)
             lo, hi, bobj = lo[near], hi[near], bobj[near]
         B = lo.shape[0]
         chunk = max(1, (1 << 24) // max(B, 1))
@@ -442,10 +446,14 @@ class Generator:
         seg = obj * 8
         vis = torch.unique(obj[obj >= 0])
         rng = np_rng(self.seed, 3_000_000 + f)
+        npix_obj = torch.bincount(obj[obj >= 0], minlength=sc.n_obj)
         for oi in vis.tolist():
-            if not sc.splittable[oi]:
+            big = int(npix_obj[oi]) > cfg.split_frac * HW
+            if not (sc.splittable[oi] or big):
                 continue
-            k = int(rng.integers(2, 5))
+            k = int(rng.integers(cfg.pieces[0], cfg.pieces[1] + 1)) if sc.splittable[oi] else int(rng.integers(1, 4))
+            if k <= 1:
+                continue
             sel = obj == oi
             p = pts[sel]
             lo_, hi_ = p.min(0).values, p.max(0).values

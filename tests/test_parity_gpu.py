@@ -1,0 +1,238 @@
+"""GPU parity: libdisc (CUDA, through the C ABI) vs the CPU oracle on identical seeded inputs.
+
+Sizes: T (3 frames, several tiles + ragged tails), T0 hand fixture, and prefixes of the full
+Replica-, ScanNet- and HM3D-shaped streams at their BASELINE.json resolutions, run through
+the same windowed launch configuration bench.py times.  Rules in tests/parity_util.py.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.oracle import OracleMap  # noqa: E402
+from synth import Generator, disc_config_kwargs, frame_to_numpy, t0_frame  # noqa: E402
+from tests.parity_util import compare_frame_debug, compare_reports, compare_state, gpu_config  # noqa: E402
+
+
+def _dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda:0")
+
+
+def _to_dev(fr: dict, dev):
+    out = {}
+    for k, v in fr.items():
+        if isinstance(v, np.ndarray) and k != "pose":
+            t = torch.from_numpy(np.ascontiguousarray(v))
+            if v.dtype == np.uint16:
+                t = t.view(torch.int16)
+            out[k] = t.to(dev)
+        else:
+            out[k] = v
+    return out
+
+
+def _disc_map(kw, H, W, Hp, Wp, **extra):
+    from paper_2603_03935_b200 import DiscMap
+    return DiscMap(**gpu_config(kw, H, W, Hp, Wp, **extra))
+
+
+# ---------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("tau", [0.3, 0.48])
+def test_t0_hand_fixture(tau):
+    """T0 (golden): both implementations reach 3120 / 2304 and R25 idempotence."""
+    dev = _dev()
+    kw = dict(voxel_size=0.05, tau_geo=tau, feat_dim=16, track_dim=0)
+    gm = _disc_map(kw, 48, 64, 16, 16)
+    om = OracleMap(selfcheck=True, **kw)
+    for i in range(3):
+        fr = t0_frame(i)
+        rg = gm.integrate_frame(_to_dev(fr, dev))
+        ro = om.integrate(fr)
+        compare_reports(rg, ro)
+        compare_frame_debug(gm.last_frame(), om.last_frame(), False, 0)
+        compare_state(gm, om, False, 0)
+    want = [3120] if tau == 0.3 else [1536, 2304]
+    assert list(gm.instances()["vcount"]) == want
+
+
+@pytest.mark.parametrize("semantic", [False, True])
+def test_t0_with_tokens_and_gate(semantic):
+    dev = _dev()
+    kw = dict(voxel_size=0.05, tau_geo=0.3, feat_dim=16, track_dim=8)
+    gm = _disc_map(kw, 48, 64, 16, 16)
+    om = OracleMap(selfcheck=True, **kw)
+    for i in range(3):
+        fr = t0_frame(i, with_tokens=semantic, Df=16, Dt=8)
+        compare_reports(gm.integrate_frame(_to_dev(fr, dev)), om.integrate(fr))
+        compare_frame_debug(gm.last_frame(), om.last_frame(), semantic, 8)
+        compare_state(gm, om, semantic, 8)
+
+
+@pytest.mark.parametrize("semantic", [False, True])
+def test_tiny_config_every_frame(semantic):
+    """T config: every frame, full debug + state parity (M1 and M2)."""
+    dev = _dev()
+    g = Generator("T", device=dev)
+    kw = disc_config_kwargs(g.cfg)
+    c = g.cfg
+    gm = _disc_map(kw, c.H, c.W, c.Hp, c.Wp)
+    om = OracleMap(selfcheck=True, **kw)
+    for f in range(c.frames):
+        fr = g.frame(f, with_feats=semantic)
+        fr["mask_conf"] = torch.clamp(fr["mask_conf"], min=0.45)
+        compare_reports(gm.integrate_frame(fr), om.integrate(frame_to_numpy(fr)))
+        compare_frame_debug(gm.last_frame(), om.last_frame(), semantic, c.Dt)
+        compare_state(gm, om, semantic, c.Dt)
+
+
+def _stream_parity(name, nframes, semantic, window, every=1, **over):
+    dev = _dev()
+    g = Generator(name, device=dev, **over)
+    c = g.cfg
+    kw = disc_config_kwargs(c)
+    gm = _disc_map(kw, c.H, c.W, c.Hp, c.Wp, window=window, S=max(64, c.n_masks))
+    om = OracleMap(**kw)
+    frames = [g.frame(f, with_feats=semantic) for f in range(nframes)]
+    # windowed GPU integration (the launch configuration bench.py times)
+    reps_g = []
+    for w0 in range(0, nframes, window):
+        reps_g += gm.integrate_frames(frames[w0:w0 + window], report=True)
+    reps_o = [om.integrate(frame_to_numpy(fr)) for fr in frames]
+    for rg, ro in zip(reps_g, reps_o):
+        compare_reports(rg, ro)
+    compare_frame_debug(gm.last_frame(), om.last_frame(), semantic, c.Dt)
+    compare_state(gm, om, semantic, c.Dt)
+    return reps_o
+
+
+@pytest.mark.parametrize("semantic", [False, True])
+def test_replica_prefix(semantic):
+    reps = _stream_parity("R", 8, semantic, window=4)
+    assert sum(r["unique_pairs"] for r in reps) > 10000
+
+
+@pytest.mark.parametrize("semantic", [False, True])
+def test_scannet_prefix(semantic):
+    _stream_parity("N", 8, semantic, window=8)
+
+
+def test_hm3d_prefix():
+    _stream_parity("H", 8, True, window=8)
+
+
+def test_stress_overlapping_masks():
+    """X-style SAM 'everything' masks (overlapping, hierarchical), Df 512, 10 cm voxels."""
+    _stream_parity("X", 6, True, window=6, n_masks=120, Df=512, voxel=0.1)
+
+
+def test_ragged_image_scalar_path():
+    """W*H not a multiple of 16: the byte-wise mask path; odd patch grid."""
+    _stream_parity("N", 4, True, window=2, H=239, W=317, Hp=17, Wp=22, fx=290.0, fy=290.0, cx=158.0, cy=119.0)
+
+
+def test_window_batching_equals_single_frames():
+    dev = _dev()
+    g = Generator("N", device=dev)
+    c = g.cfg
+    kw = disc_config_kwargs(c)
+    frames = [g.frame(f) for f in range(10)]
+    a = _disc_map(kw, c.H, c.W, c.Hp, c.Wp, window=8)
+    b = _disc_map(kw, c.H, c.W, c.Hp, c.Wp, window=1)
+    ra = a.integrate_frames(frames, report=True)
+    rb = [b.integrate_frame(fr) for fr in frames]
+    assert ra == rb
+    ka, ia = a.memberships()
+    kb, ib = b.memberships()
+    assert np.array_equal(ka, kb) and np.array_equal(ia, ib)
+    A, B = a.instances(), b.instances()
+    for k in ["id", "vcount", "obs", "aabb", "T"]:
+        assert np.array_equal(A[k], B[k])
+
+
+def test_host_input_path_equals_device_path():
+    dev = _dev()
+    g = Generator("T", device=dev)
+    c = g.cfg
+    kw = disc_config_kwargs(c)
+    frames = [g.frame(f) for f in range(3)]
+    a = _disc_map(kw, c.H, c.W, c.Hp, c.Wp)
+    b = _disc_map(kw, c.H, c.W, c.Hp, c.Wp)
+    ra = a.integrate_frames(frames, report=True)
+    host = [{k: (v.cpu().pin_memory() if isinstance(v, torch.Tensor) else v) for k, v in fr.items()} for fr in frames]
+    rb = b.integrate_frames_host(host, report=True)
+    assert ra == rb
+    assert np.array_equal(a.memberships()[0], b.memberships()[0])
+
+
+def test_query_parity():
+    dev = _dev()
+    g = Generator("N", device=dev)
+    c = g.cfg
+    kw = disc_config_kwargs(c)
+    gm = _disc_map(kw, c.H, c.W, c.Hp, c.Wp)
+    om = OracleMap(**kw)
+    for f in range(4):
+        fr = g.frame(f)
+        gm.integrate_frame(fr)
+        om.integrate(frame_to_numpy(fr))
+    q = g.proto[7].cpu().numpy()
+    ig, sg = gm.query(q, 5)
+    io, so = om.query(q, 5)
+    np.testing.assert_allclose(sg, so, atol=2e-5)
+    # ids equal except where scores tie within 1e-6
+    for a, b, s in zip(ig, io, so):
+        if a != b:
+            assert np.sum(np.abs(so - s) < 1e-6) > 1
+
+
+def test_invalid_frame_is_rejected_before_mutation():
+    from paper_2603_03935_b200 import DiscError
+    dev = _dev()
+    kw = dict(voxel_size=0.05, feat_dim=16, track_dim=0)
+    gm = _disc_map(kw, 48, 64, 16, 16)
+    gm.integrate_frame(_to_dev(t0_frame(0), dev))
+    k0, i0 = gm.memberships()
+    bad = t0_frame(1)
+    bad["pose"] = bad["pose"].copy()
+    bad["pose"][0, 0] = 1.5
+    with pytest.raises(DiscError) as e:
+        gm.integrate_frame(_to_dev(bad, dev))
+    assert e.value.code == 2
+    k1, i1 = gm.memberships()
+    assert np.array_equal(k0, k1) and np.array_equal(i0, i1)
+
+
+def test_empty_and_degenerate_frames():
+    """S = 0; all-invalid depth (every mask 'nodepth'); then a normal frame."""
+    dev = _dev()
+    kw = dict(voxel_size=0.05, feat_dim=16, track_dim=0)
+    gm = _disc_map(kw, 48, 64, 16, 16)
+    om = OracleMap(selfcheck=True, **kw)
+    fr0 = t0_frame(0)
+    e = dict(fr0, masks=np.zeros((0, 48, 64), np.uint8))
+    nod = dict(fr0, frame_id=1, depth=np.zeros((48, 64), np.float32))
+    for fr in [e, nod, dict(fr0, frame_id=2)]:
+        compare_reports(gm.integrate_frame(_to_dev(fr, dev)), om.integrate(fr))
+        compare_state(gm, om, False, 0)
+
+
+def test_gpu_determinism():
+    dev = _dev()
+    g = Generator("R", device=dev)
+    c = g.cfg
+    kw = disc_config_kwargs(c)
+    frames = [g.frame(f) for f in range(6)]
+    outs = []
+    for _ in range(2):
+        gm = _disc_map(kw, c.H, c.W, c.Hp, c.Wp, window=6)
+        gm.integrate_frames(frames)
+        outs.append((gm.memberships(), gm.instances()))
+    (ka, ia), A = outs[0]
+    (kb, ib), B = outs[1]
+    assert np.array_equal(ka, kb) and np.array_equal(ia, ib)
+    for k in ["id", "vcount", "obs", "aabb", "T"]:
+        assert np.array_equal(A[k], B[k])
