@@ -6,6 +6,7 @@
 // validates, sizes, launches and copies.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -95,7 +96,14 @@ const char* dev_err_text(int code) {
     case DERR_TRIPLES: return "per-frame (segment, instance) count table full";
     case DERR_INSTANCES: return "max_instances exceeded";
     case DERR_STAGE: return "per-frame staging list full: raise max_memberships";
-    default: return "device error";
+    default: {
+      static thread_local char buf[96];
+      if (code >= 1000) {
+        std::snprintf(buf, sizeof(buf), "internal invariant violated (device check at source line %d)", code - 1000);
+        return buf;
+      }
+      return "device error";
+    }
   }
 }
 
@@ -104,7 +112,7 @@ disc_status sync_check(disc_map* m, cudaStream_t st) {
   if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_check(m, "cudaStreamSynchronize");
   if (cudaMemcpy(m->h_err, m->d_err, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
     return cuda_check(m, "error flag");
-  if (*m->h_err) return fail(m, DISC_ERR_CAPACITY, dev_err_text(*m->h_err));
+  if (*m->h_err) return fail(m, *m->h_err >= 1000 ? DISC_ERR_INTERNAL : DISC_ERR_CAPACITY, dev_err_text(*m->h_err));
   return DISC_OK;
 }
 
@@ -189,6 +197,19 @@ void collect_events(disc_map* m) {
 }
 
 }  // namespace
+
+namespace disc {
+void debug_check(cudaStream_t st, const char* kernel, int frame) {
+  static int on = -1;
+  if (on < 0) on = getenv("DISC_DEBUG_SYNC") ? 1 : 0;
+  if (!on) return;
+  const cudaError_t e1 = cudaGetLastError();
+  const cudaError_t e2 = cudaStreamSynchronize(st);
+  if (e1 != cudaSuccess || e2 != cudaSuccess)
+    std::fprintf(stderr, "DISC_DEBUG_SYNC: %s (frame %d): %s / %s\n", kernel, frame, cudaGetErrorString(e1),
+                 cudaGetErrorString(e2));
+}
+}  // namespace disc
 
 extern "C" {
 

@@ -197,6 +197,11 @@ __device__ __forceinline__ void unpack_key(uint64_t k, int& ix, int& iy, int& iz
   iz = (int)(k & 0x1FFFFF) - KEY_BIAS;
 }
 __device__ __forceinline__ void raise_err(int* err, int code) { atomicMax(err, code); }
+// internal invariant check: records 1000 + source line in the sticky error flag
+#define DISC_CHECK(err, cond)                       \
+  do {                                              \
+    if (!(cond)) atomicCAS((err), 0, 1000 + __LINE__); \
+  } while (0)
 
 template <typename T>
 __device__ __forceinline__ T vload(const T* p) {

@@ -3,6 +3,9 @@
 #include "disc_common.cuh"
 
 namespace disc {
+// DISC_DEBUG_SYNC=1: synchronise and check after every launch, naming the kernel (debugging
+// aid for device faults; off by default).
+void debug_check(cudaStream_t st, const char* kernel, int frame);
 size_t k1_smem_bytes(int S, int W, int Wp, int rows_cap);
 size_t k6_smem_bytes(int S, int TC);
 void launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* err, bool sem, int maxS,

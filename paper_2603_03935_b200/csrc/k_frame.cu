@@ -304,6 +304,8 @@ __global__ void __launch_bounds__(K1_THREADS) k_mask_pass(WinDesc wd, WinBufs wb
               run_pslot = kslot == U32_EMPTY ? U32_EMPTY
                                              : ptab_insert(ptab, tmask, ((uint32_t)s << 24) | kslot, &fresh, err);
               if (fresh) {
+                DISC_CHECK(err, __ldcg(&ptab[run_pslot]) == (((uint32_t)s << 24) | kslot));
+                DISC_CHECK(err, __ldcg(&ktab[kslot]) == kj);
                 atomicAdd(&vs_s[s], 1u);
                 const uint32_t li = atomicAdd(&npl_s, 1u);
                 if (li < K1_PLIST) {
@@ -370,7 +372,10 @@ __global__ void __launch_bounds__(K1_THREADS) k_mask_pass(WinDesc wd, WinBufs wb
     if (threadIdx.x == 0) raise_err(err, DERR_FRAME_PAIRS);
     return;
   }
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) wb.plist[(size_t)f * wb.PMAX + base_s + i] = pl_s[i];
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    DISC_CHECK(err, pl_s[i] < (uint32_t)wb.PC && __ldcg(&ptab[pl_s[i]]) != U32_EMPTY);
+    wb.plist[(size_t)f * wb.PMAX + base_s + i] = pl_s[i];
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -380,7 +385,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_mask_pass(WinDesc wd, WinBufs wb
 constexpr int K2_THREADS = 256;
 
 template <bool SEM>
-__global__ void __launch_bounds__(K2_THREADS) k_pairs(WinDesc wd, WinBufs wb, Params P) {
+__global__ void __launch_bounds__(K2_THREADS) k_pairs(WinDesc wd, WinBufs wb, Params P, int* err) {
   const int f = blockIdx.y;
   if (f >= wd.n) return;
   const FrameDesc& F = wd.f[f];
@@ -402,13 +407,25 @@ __global__ void __launch_bounds__(K2_THREADS) k_pairs(WinDesc wd, WinBufs wb, Pa
   float* nsum = wb.nsum + (size_t)f * wb.PC * 3;
   for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < np; idx += gridDim.x * blockDim.x) {
     const uint32_t ps = wb.plist[fo + idx];
+    if (ps >= (uint32_t)wb.PC) {
+      atomicCAS(err, 0, 1000 + __LINE__);
+      continue;
+    }
     const uint32_t code = ptab[ps];
     const uint32_t s = code >> 24, ks = code & 0xFFFFFFu;
+    if (code == U32_EMPTY) {
+      atomicCAS(err, 0, 1000 + __LINE__);
+      continue;
+    }
+    if (s >= (uint32_t)S || ks >= (uint32_t)wb.PC) {
+      atomicCAS(err, 0, 1000 + __LINE__);
+      continue;
+    }
     const uint64_t key = ktab[ks];
     wb.pkey[fo + idx] = key;
     wb.pinfo[fo + idx] = s;
     wb.pfk[fo + idx] = ks;
-    ptab[ps] = U32_EMPTY;
+    DISC_CHECK(err, atomicExch(&ptab[ps], U32_EMPTY) == code);
     int k3[3];
     unpack_key(key, k3[0], k3[1], k3[2]);
     for (int a = 0; a < 3; ++a) {
@@ -716,6 +733,7 @@ void launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* e
                    cudaEvent_t ev0, cudaEvent_t ev1) {
   const int n = wd.n;
   k_win_init<<<dim3(1, n), 256, 0, st>>>(wd, wb);
+  debug_check(st, "k_win_init", -1);
   const size_t sm1 = k1_smem_bytes(maxS, maxW, maxWp, rows_cap);
   if (ev0) cudaEventRecord(ev0, st);
   if (sem) {
@@ -725,20 +743,24 @@ void launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* e
     cudaFuncSetAttribute(k_mask_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
     k_mask_pass<false><<<dim3(maxHp, n), K1_THREADS, sm1, st>>>(wd, wb, P, err, rows_cap);
   }
+  debug_check(st, "k_mask_pass", -1);
   if (ev1) cudaEventRecord(ev1, st);
   const size_t sm2 = (size_t)maxS * (6 * 4 + 4 + 4);
   const int g2 = 64;
-  if (sem) k_pairs<true><<<dim3(g2, n), K2_THREADS, sm2, st>>>(wd, wb, P);
-  else k_pairs<false><<<dim3(g2, n), K2_THREADS, sm2, st>>>(wd, wb, P);
+  if (sem) k_pairs<true><<<dim3(g2, n), K2_THREADS, sm2, st>>>(wd, wb, P, err);
+  else k_pairs<false><<<dim3(g2, n), K2_THREADS, sm2, st>>>(wd, wb, P, err);
+  debug_check(st, "k_pairs", -1);
   if (sem) {
     const int nch = (maxP + K3_ROWS - 1) / K3_ROWS;
     k_fbar_part<<<dim3(nch, n), 256, 0, st>>>(wd, wb, P.Df);
     k_fbar<<<dim3((P.Df + 255) / 256, n), 256, 0, st>>>(wd, wb, P.Df);
     k_resid<<<dim3((maxP + 7) / 8, n), 256, 0, st>>>(wd, wb, P.Df);
+    debug_check(st, "k_fbar/k_resid", -1);
   }
   const size_t sm4 = 40 * 8 + (size_t)P.Dt * 8 + 64;
   if (sem) k_detect<true><<<dim3(maxS, n), K4_THREADS, sm4, st>>>(wd, wb, P);
   else k_detect<false><<<dim3(maxS, n), K4_THREADS, sm4, st>>>(wd, wb, P);
+  debug_check(st, "k_detect", -1);
 }
 
 }  // namespace disc

@@ -673,12 +673,17 @@ size_t k6_smem_bytes(int S, int TC) { return K6Smem(S, TC).total; }
 void launch_stage2_frame(int f, const FrameDesc& F, const WinBufs& wb, const MapState& M, const FrameScratch& X,
                          const Params& P, bool sem, int nsm, cudaStream_t st) {
   k_lookup<<<2 * nsm, 256, 0, st>>>(f, wb, M, X);
+  debug_check(st, "k_lookup", f);
   const size_t sm6 = k6_smem_bytes(wb.SMAX, X.TCAP);
   cudaFuncSetAttribute(k_assoc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm6);
   k_assoc<<<1, K6_THREADS, sm6, st>>>(f, F, wb, M, X, P, sem ? 1 : 0);
+  debug_check(st, "k_assoc", f);
   k_apply<<<2 * nsm, 256, 0, st>>>(f, wb, M, X);
+  debug_check(st, "k_apply", f);
   k_grow<<<wb.SMAX, 256, 0, st>>>(f, M, X);
+  debug_check(st, "k_grow", f);
   k_fill<<<nsm, 256, 0, st>>>(M, X);
+  debug_check(st, "k_fill", f);
 }
 
 }  // namespace disc
