@@ -62,8 +62,8 @@ typedef struct {
   float cover_min;         /* 0.25 (patch coverage threshold, inclusive)   R17, R18  */
   float lambda_size;       /* 3.3            */
   float eps_distinct;      /* 1e-6                                          Eq.1, R16        */
-  int32_t feat_dim;        /* Df > 0, multiple of 4 (CLIP token width)                       */
-  int32_t track_dim;       /* Dt >= 0; 0 = no visual gate (DINO tracking width)              */
+  int32_t feat_dim;        /* Df in [4,1024], multiple of 4 (CLIP token width)               */
+  int32_t track_dim;       /* Dt in [0,512]; 0 = no visual gate (DINO tracking width)        */
   /* capacities (device memory is sized from these at create time) */
   int64_t max_memberships; /* live (key, instance) pairs; voxel hash sized 2x               */
   int32_t max_instances;   /* instance ids ever created (ids are never reused, R13)          */
@@ -141,7 +141,9 @@ typedef struct {                       /* timing of the dominant kernels (disc_s
   int64_t k1_launches;
   double stage1_ms, stage2_ms;         /* whole stage-1 batch / sum of stage-2 frame loops  */
   int64_t mask_bytes, depth_bytes, track_bytes, feat_bytes; /* algorithmic input bytes      */
-  int64_t pairs, map_inserts, relabels; /* U, new memberships written, relabel probes        */
+  int64_t pairs, map_inserts, relabels; /* sum U, labels inserted, relabel items processed    */
+  int64_t edges;                       /* sum of qualifying (s, j) edges                     */
+  int64_t launches;                    /* kernels launched by integrate calls                */
 } disc_stats;
 
 /* Fill *c with the defaults named above (capacities sized for a Replica-shaped stream). */

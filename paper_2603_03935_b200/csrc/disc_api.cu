@@ -149,9 +149,8 @@ std::string validate_frame(const disc_map* m, const disc_frame& f, bool host) {
       !std::isfinite(f.cy))
     return "bad intrinsics";
   if (!pose_rigid(f.pose)) return "non-rigid pose";
-  const int rows = (f.height + f.patch_h - 1) / f.patch_h + 3;
-  if (k1_smem_bytes(c.max_masks, f.width, f.patch_w, rows) > 227 * 1024)
-    return "frame too large for the mask-pass tile (S * Wp)";
+  if (k1_smem_bytes(c.max_masks, f.width, k1_rows_cap(f.width)) > 227 * 1024)
+    return "frame too wide for the mask-pass tile";
   (void)host;
   return "";
 }
@@ -168,7 +167,9 @@ FrameDesc make_desc(const disc_frame& f) {
   d.fx = f.fx; d.fy = f.fy; d.cx = f.cx; d.cy = f.cy;
   d.frame_id = f.frame_id;
   d.H = f.height; d.W = f.width; d.S = f.num_masks; d.Hp = f.patch_h; d.Wp = f.patch_w;
-  d.vec16 = (((int64_t)f.height * f.width) % 16 == 0) && (((uintptr_t)f.masks & 15) == 0);
+  // K1 reads mask planes with 32-byte loads and depth with 16-byte loads
+  d.vec16 = (((int64_t)f.height * f.width) % 32 == 0) && (((uintptr_t)f.masks & 31) == 0) &&
+            (((uintptr_t)f.depth & 15) == 0);
   return d;
 }
 
@@ -254,8 +255,9 @@ static std::string validate_config(const disc_config* c) {
   if (!(c->mask_max_aspect >= 1.0f) || c->mask_min_area < 0) return "bad mask filter";
   if (!(c->cover_min >= 0.0f && c->cover_min <= 1.0f)) return "cover_min in [0,1]";
   if (!(c->lambda_size > 0.0f) || !(c->eps_distinct >= 0.0f)) return "bad lambda/eps";
-  if (c->feat_dim <= 0 || c->feat_dim % 4 != 0) return "feat_dim must be a positive multiple of 4";
-  if (c->track_dim < 0) return "track_dim must be >= 0";
+  if (c->feat_dim <= 0 || c->feat_dim % 4 != 0 || c->feat_dim > 1024)
+    return "feat_dim must be a multiple of 4 in [4, 1024]";
+  if (c->track_dim < 0 || c->track_dim > 512) return "track_dim must be in [0, 512]";
   if (c->max_masks < 1 || c->max_masks > 255) return "max_masks in [1,255]";
   if (c->max_pixels < 1 || c->max_patches < 1) return "bad max_pixels / max_patches";
   if (c->max_pairs_per_frame < 1 || c->max_pairs_per_frame > (1 << 22)) return "max_pairs_per_frame in [1, 2^22]";
@@ -478,7 +480,7 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
       maxW = std::max(maxW, f.width);
       maxWp = std::max(maxWp, f.patch_w);
       maxP = std::max(maxP, f.patch_h * f.patch_w);
-      rows = std::max(rows, (f.height + f.patch_h - 1) / f.patch_h + 3);
+      rows = std::max(rows, k1_rows_cap(f.width));
       sem = sem || f.patch_feats != nullptr;
       m->stats.mask_bytes += (int64_t)f.height * f.width * f.num_masks;
       m->stats.depth_bytes += (int64_t)f.height * f.width * 4;
@@ -490,12 +492,13 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
       e0 = ev_get(m); e1 = ev_get(m); s0 = ev_get(m); s1 = ev_get(m); s1b = ev_get(m); s2 = ev_get(m);
       cudaEventRecord(s0, st);
     }
-    launch_stage1(wd, m->W, m->P, m->d_err, sem, maxS, maxHp, maxW, maxWp, maxP, rows, st, e0, e1);
+    m->stats.launches += launch_stage1(wd, m->W, m->P, m->d_err, sem, maxS, maxHp, maxW, maxWp, maxP, rows, st, e0, e1);
     if (m->timing) {
       cudaEventRecord(s1, st);
       cudaEventRecord(s1b, st);
     }
-    for (int i = 0; i < nw; ++i) launch_stage2_frame(i, wd.f[i], m->W, m->M, m->X, m->P, sem, m->nsm, st);
+    for (int i = 0; i < nw; ++i)
+      m->stats.launches += launch_stage2_frame(i, wd.f[i], m->W, m->M, m->X, m->P, sem, m->nsm, st);
     if (m->timing) {
       cudaEventRecord(s2, st);
       m->ev_pending.push_back({e0, e1, 0});
@@ -691,8 +694,14 @@ disc_status disc_get_stats(disc_map* m, disc_stats* s) {
   disc_status st = disc_sync(m);
   if (st != DISC_OK) return st;
   collect_events(m);
+  int64_t ctr[8];
+  cudaMemcpy(ctr, m->M.counters, sizeof(ctr), cudaMemcpyDeviceToHost);
+  m->stats.pairs = ctr[4];
+  m->stats.map_inserts = ctr[5];
+  m->stats.relabels = ctr[6];
+  m->stats.edges = ctr[7];
   *s = m->stats;
-  return DISC_OK;
+  return cuda_check(m, "disc_get_stats");
 }
 
 const char* disc_last_error(const disc_map* m) { return m ? m->err.c_str() : "null map"; }

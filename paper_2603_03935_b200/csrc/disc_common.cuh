@@ -55,7 +55,7 @@ struct FrameDesc {                // one frame's inputs, passed by value to kern
   float fx, fy, cx, cy;
   int64_t frame_id;
   int32_t H, W, S, Hp, Wp;
-  int32_t vec16;                  // masks 16-byte vectorisable (H*W % 16 == 0, aligned)
+  int32_t vec16;                  // vector path: H*W % 32 == 0, masks 32-B and depth 16-B aligned
 };
 
 struct WinDesc {

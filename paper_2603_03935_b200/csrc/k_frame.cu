@@ -12,6 +12,8 @@
 #include "disc_common.cuh"
 #include "disc_launch.h"
 
+#include <algorithm>
+
 namespace disc {
 
 // ------------------------------------------------------------------------------------------
@@ -98,7 +100,6 @@ __global__ void k_win_init(WinDesc wd, WinBufs wb) {
   const int S = wd.f[f].S;
   for (int s = threadIdx.x + blockIdx.x * blockDim.x; s < S; s += blockDim.x * gridDim.x) {
     const size_t i = (size_t)f * wb.SMAX + s;
-    wb.area[i] = 0;
     wb.vs[i] = 0;
     wb.ang_sum[i] = 0.f;
     wb.ang_cnt[i] = 0;
@@ -115,54 +116,115 @@ __global__ void k_win_init(WinDesc wd, WinBufs wb) {
     wb.npairs[f] = 0;
     wb.oor[f] = 0;
   }
+  // per-patch pixel counts are accumulated with atomics by K1: zero the rows this frame uses
+  const int P = wd.f[f].Hp * wd.f[f].Wp;
+  uint32_t* cnt = wb.cnt + (size_t)f * wb.SMAX * wb.PMAXP;
+  for (int s = 0; s < S; ++s)
+    for (int p = threadIdx.x + blockIdx.x * blockDim.x; p < P; p += blockDim.x * gridDim.x)
+      cnt[(size_t)s * wb.PMAXP + p] = 0;
 }
 
 // ------------------------------------------------------------------------------------------
-// K1: one CTA per (patch row, frame).  The CTA's pixels are the image rows that map to patch
-// row `band` (R17 floor mapping), so it owns cnt[s][band][*] outright (no global atomics
-// for per-patch counts).  A thread handles 16 consecutive pixels: keys once, then one
-// 16-byte streaming load per mask plane.
+// K1: mask pass.  Grid = (ceil(H*W / K1_TILE), frames); a CTA owns K1_TILE consecutive
+// pixels (row-major), a warp 1024 consecutive pixels per step, a lane a 32-pixel chunk.
+// Pixel pass (once per chunk): pinned keys (R5) of the 32 pixels, reduced to three bit masks:
+// ok (key valid), kstart (a new voxel key begins), pstart (a new patch begins).  Mask pass:
+// per plane one 256-bit streaming load per lane (evict-first in L2, two planes in flight);
+// per-patch counts = popc over patch segments, bbox from ffs/clz, (s, key-run) items into a
+// per-warp queue that all 32 lanes then process: pixel normals pixel-parallel (R21), frame
+// key / pair table inserts item-parallel.
 // ------------------------------------------------------------------------------------------
-constexpr int K1_THREADS = 256;
-constexpr int K1_PLIST = 2048;
+constexpr int K1_THREADS = 128;
+constexpr int K1_WARPS = K1_THREADS / 32;
+constexpr int K1_PPL = 32;                                // pixels per lane (chunk)
+constexpr int K1_CPL = 2;                                 // chunks per lane
+constexpr int K1_TILE = K1_THREADS * K1_PPL * K1_CPL;     // pixels per CTA
+constexpr int K1_QCAP = 64;                               // per-warp item queue
+constexpr int K1_PLIST = 1024;
+
+struct K1Item {
+  unsigned long long key;
+  uint32_t pix;       // linear index of the chunk's first pixel
+  uint32_t bits;      // pixels of this (s, key) run within the chunk
+};
+
+struct K1Smem {
+  size_t bb, vs, pl, q, qs, qp, qn, xa, pc, rows, total;
+  __host__ __device__ K1Smem(int S, int W, int rows_cap) {
+    size_t o = 0;
+    auto take = [&](size_t b) { const size_t r = o; o = (o + b + 15) & ~(size_t)15; return r; };
+    bb = take((size_t)S * 16);
+    vs = take((size_t)S * 4);
+    pl = take((size_t)K1_PLIST * 4);
+    q = take((size_t)K1_WARPS * K1_QCAP * sizeof(K1Item));
+    qs = take((size_t)K1_WARPS * K1_QCAP * 2);               // item mask index s
+    qp = take((size_t)K1_WARPS * (K1_QCAP + 1) * 4);         // item pixel prefix
+    qn = take((size_t)K1_WARPS * K1_QCAP * 12);              // item normal sums
+    xa = take((size_t)W * 4);
+    pc = take((size_t)W * 2);
+    rows = take((size_t)rows_cap * 8);
+    total = o;
+  }
+};
+
+__device__ __forceinline__ void ld_stream32(const uint8_t* p, uint32_t r[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+}
+
+__device__ __forceinline__ uint32_t nz_bits4(uint32_t w) {   // bit b set iff byte b of w != 0
+  const uint32_t nz = __vcmpne4(w, 0u) & 0x01010101u;
+  return (nz & 1u) | ((nz >> 7) & 2u) | ((nz >> 14) & 4u) | ((nz >> 21) & 8u);
+}
+
+__device__ __forceinline__ uint32_t range_bits(int a, int b) {   // bits [a, b), 0 <= a < b <= 32
+  return (b >= 32 ? 0xFFFFFFFFu : ((1u << b) - 1u)) & ~((1u << a) - 1u);
+}
 
 template <bool SEM>
-__global__ void __launch_bounds__(K1_THREADS) k_mask_pass(WinDesc wd, WinBufs wb, Params P, int* err, int rows_cap) {
+__global__ void __launch_bounds__(K1_THREADS, 8) k_mask_pass(WinDesc wd, WinBufs wb, Params P, int* err,
+                                                             int rows_cap) {
   const int f = blockIdx.y;
   if (f >= wd.n) return;
   const FrameDesc& F = wd.f[f];
-  const int band = blockIdx.x;
-  if (band >= F.Hp) return;
   const int H = F.H, W = F.W, S = F.S, Hp = F.Hp, Wp = F.Wp;
   const int64_t HW = (int64_t)H * W;
-  const int v0 = (int)(((int64_t)band * H + Hp - 1) / Hp);
-  const int v1 = (int)(((int64_t)(band + 1) * H + Hp - 1) / Hp);
-  const int64_t i0 = (int64_t)v0 * W, i1 = (int64_t)v1 * W;
+  const int64_t tile0 = (int64_t)blockIdx.x * K1_TILE;
+  if (tile0 >= HW) return;
+  const int64_t tile1 = min(HW, tile0 + (int64_t)K1_TILE);
+  const int vt0 = (int)(tile0 / W), vt1 = (int)((tile1 - 1) / W);
+  const int r0 = vt0 - 1;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* cnt_s = (uint32_t*)smem_raw;                       // [S][Wp]
-  int32_t* bb_s = (int32_t*)(cnt_s + (size_t)S * Wp);         // [S][4]
-  uint32_t* vs_s = (uint32_t*)(bb_s + 4 * S);                  // [S]
-  uint32_t* pl_s = vs_s + S;                                   // [K1_PLIST]
-  float* xa_s = (float*)(pl_s + K1_PLIST);                     // [W]  ((float)u - cx) / fx
-  uint16_t* pc_s = (uint16_t*)(xa_s + W);                      // [W]  patch column of u
-  float* yb_s = (float*)(pc_s + ((W + 1) & ~1));               // rows v0-1 .. v1: ((float)v - cy)/fy
-  unsigned long long* ks_all = (unsigned long long*)(((uintptr_t)(yb_s + rows_cap) + 15) & ~(uintptr_t)15);
-  unsigned long long* ks = ks_all + threadIdx.x;               // ks[j * K1_THREADS]: packed key
+  const K1Smem L(S, W, rows_cap);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t* bb_s = (int32_t*)(smem_raw + L.bb);
+  uint32_t* vs_s = (uint32_t*)(smem_raw + L.vs);
+  uint32_t* pl_s = (uint32_t*)(smem_raw + L.pl);
+  K1Item* q_s = (K1Item*)(smem_raw + L.q) + warp * K1_QCAP;
+  uint16_t* qs_s = (uint16_t*)(smem_raw + L.qs) + warp * K1_QCAP;
+  uint32_t* qp_s = (uint32_t*)(smem_raw + L.qp) + warp * (K1_QCAP + 1);
+  float* qn_s = (float*)(smem_raw + L.qn) + warp * K1_QCAP * 3;
+  float* xa_s = (float*)(smem_raw + L.xa);
+  uint16_t* pc_s = (uint16_t*)(smem_raw + L.pc);
+  float* yb_s = (float*)(smem_raw + L.rows);
+  int32_t* pr_s = (int32_t*)(yb_s + rows_cap);
   __shared__ uint32_t npl_s, oor_s;
 
-  for (int i = threadIdx.x; i < S * Wp; i += blockDim.x) cnt_s[i] = 0;
   for (int i = threadIdx.x; i < S; i += blockDim.x) {
     bb_s[4 * i + 0] = INT32_MAX; bb_s[4 * i + 1] = INT32_MAX;
     bb_s[4 * i + 2] = -1; bb_s[4 * i + 3] = -1;
     vs_s[i] = 0;
   }
   for (int u = threadIdx.x; u < W; u += blockDim.x) {
-    xa_s[u] = __fdiv_rn(__fsub_rn((float)u, F.cx), F.fx);
-    pc_s[u] = (uint16_t)(((int64_t)u * Wp) / W);
+    xa_s[u] = __fdiv_rn(__fsub_rn((float)u, F.cx), F.fx);   // R5: ((float)u - cx) / fx
+    pc_s[u] = (uint16_t)(((int64_t)u * Wp) / W);             // R17 floor mapping
   }
-  for (int v = v0 - 1 + (int)threadIdx.x; v <= v1; v += blockDim.x)
-    yb_s[v - (v0 - 1)] = __fdiv_rn(__fsub_rn((float)v, F.cy), F.fy);
+  for (int v = r0 + (int)threadIdx.x; v <= vt1 + 1; v += blockDim.x) {
+    yb_s[v - r0] = __fdiv_rn(__fsub_rn((float)v, F.cy), F.fy);
+    pr_s[v - r0] = (int32_t)(((int64_t)v * Hp) / H);
+  }
   if (threadIdx.x == 0) { npl_s = 0; oor_s = 0; }
   __syncthreads();
 
@@ -170,21 +232,31 @@ __global__ void __launch_bounds__(K1_THREADS) k_mask_pass(WinDesc wd, WinBufs wb
   unsigned long long* ktab = wb.ktab + (size_t)f * wb.PC;
   uint32_t* ptab = wb.ptab + (size_t)f * wb.PC;
   float* nsum = wb.nsum + (size_t)f * wb.PC * 3;
+  uint32_t* cnt_g = wb.cnt + (size_t)f * wb.SMAX * wb.PMAXP;
   const float r = P.r;
 
-  auto ybv = [&](int v) { return yb_s[v - (v0 - 1)]; };
-  // world point of an arbitrary pixel (normals need neighbours outside the band)
-  auto wp_at = [&](int u, int v, float p[3]) -> bool {
+  auto key_at = [&](int u, int v, uint64_t& key) -> bool {
     const float d = F.depth[(int64_t)v * W + u];
     if (!depth_valid(d, P)) return false;
-    world_point(F, xa_s[u], (v >= v0 - 1 && v <= v1) ? ybv(v) : __fdiv_rn(__fsub_rn((float)v, F.cy), F.fy), d, p);
-    return true;
+    float p[3];
+    world_point(F, xa_s[u], yb_s[v - r0], d, p);
+    return point_key(p, r, key);
   };
-  // R21 pixel normal (fp32): (P(u+1,v)-P(u-1,v)) x (P(u,v+1)-P(u,v-1)), oriented to the camera
-  auto pixel_normal = [&](int u, int v, const float pc[3], float n[3]) -> bool {
+  // R21 pixel normal (fp32): (P(u+1,v)-P(u-1,v)) x (P(u,v+1)-P(u,v-1)), oriented to the camera.
+  // All five depths are loaded before any test (independent loads in flight).
+  auto pixel_normal = [&](int u, int v, float n[3]) -> bool {
     if (u < 1 || u + 1 >= W || v < 1 || v + 1 >= H) return false;
-    float pl[3], pr[3], pu[3], pd[3];
-    if (!wp_at(u - 1, v, pl) || !wp_at(u + 1, v, pr) || !wp_at(u, v - 1, pu) || !wp_at(u, v + 1, pd)) return false;
+    const float* dp = F.depth + (int64_t)v * W + u;
+    const float dc = dp[0], dl = dp[-1], dr = dp[1], du = dp[-W], dd = dp[W];
+    if (!(depth_valid(dc, P) && depth_valid(dl, P) && depth_valid(dr, P) && depth_valid(du, P) &&
+          depth_valid(dd, P)))
+      return false;
+    float pc[3], pl[3], pr[3], pu[3], pd[3];
+    world_point(F, xa_s[u], yb_s[v - r0], dc, pc);
+    world_point(F, xa_s[u - 1], yb_s[v - r0], dl, pl);
+    world_point(F, xa_s[u + 1], yb_s[v - r0], dr, pr);
+    world_point(F, xa_s[u], yb_s[v - 1 - r0], du, pu);
+    world_point(F, xa_s[u], yb_s[v + 1 - r0], dd, pd);
     const float a0 = pr[0] - pl[0], a1 = pr[1] - pl[1], a2 = pr[2] - pl[2];
     const float b0 = pd[0] - pu[0], b1 = pd[1] - pu[1], b2 = pd[2] - pu[2];
     n[0] = a1 * b2 - a2 * b1;
@@ -195,171 +267,248 @@ __global__ void __launch_bounds__(K1_THREADS) k_mask_pass(WinDesc wd, WinBufs wb
     if (o < 0.f) { n[0] = -n[0]; n[1] = -n[1]; n[2] = -n[2]; }
     return true;
   };
+  auto pix_uv = [&](int64_t i, int& u, int& v) { v = (int)(i / W); u = (int)(i - (int64_t)v * W); };
 
-  const int64_t c0 = i0 >> 4, c1 = (i1 + 15) >> 4;
   uint32_t my_oor = 0;
-  for (int64_t ch = c0 + threadIdx.x; ch < c1; ch += blockDim.x) {
-    const int64_t ib = ch << 4;
-    int u_start = (int)(ib % W), v_start = (int)(ib / W);
-    // ---- pixel pass: keys of the 16 pixels ----
-    uint32_t okbits = 0, inband = 0;
-    {
+  for (int c = 0; c < K1_CPL; ++c) {
+    const int64_t seg0 = tile0 + (int64_t)(c * K1_WARPS + warp) * (32 * K1_PPL);   // warp-uniform
+    if (seg0 >= tile1) break;
+    const int64_t ib = seg0 + (int64_t)lane * K1_PPL;
+    const bool lane_on = ib < tile1;
+    int u_start = 0, v_start = 0;
+    if (lane_on) pix_uv(ib, u_start, v_start);
+    const bool wraps = u_start + K1_PPL > W;            // chunk crosses a row end
+    uint32_t inb = 0, okb = 0, kst = 0, pst = 0;
+    // ---- pixel pass ----
+    if (lane_on) {
+      const int nin = (int)min((int64_t)K1_PPL, tile1 - ib);
+      inb = nin >= 32 ? 0xFFFFFFFFu : ((1u << nin) - 1u);
+      uint64_t prevk = KEY_EMPTY;
+      int prevp = -1;
       int u = u_start, v = v_start;
-      for (int j = 0; j < 16; ++j) {
-        const int64_t i = ib + j;
-        if (i >= i0 && i < i1) {
-          inband |= 1u << j;
-          const float d = F.depth[i];
-          if (depth_valid(d, P)) {
-            float p[3];
-            world_point(F, xa_s[u], ybv(v), d, p);
-            uint64_t key;
-            if (point_key(p, r, key)) {
-              ks[j * K1_THREADS] = key;
-              okbits |= 1u << j;
-            } else {
-              my_oor++;
-            }
-          }
+      const bool vec = F.vec16 && nin == 32;
+#pragma unroll 4
+      for (int j4 = 0; j4 < 8; ++j4) {
+        float dv[4];
+        if (vec) {
+          const float4 x = __ldg((const float4*)(F.depth + ib) + j4);
+          dv[0] = x.x; dv[1] = x.y; dv[2] = x.z; dv[3] = x.w;
+        } else {
+          for (int t = 0; t < 4; ++t) dv[t] = (4 * j4 + t < nin) ? F.depth[ib + 4 * j4 + t] : 0.f;
         }
-        if (++u == W) { u = 0; ++v; }
-      }
-    }
-    if (!inband) continue;
-    // ---- mask pass ----
-    for (int s = 0; s < S; ++s) {
-      uint32_t w[4];
-      if (F.vec16) {
-        const uint4 m = ld_stream16(F.masks + (size_t)s * HW + ib);
-        w[0] = m.x; w[1] = m.y; w[2] = m.z; w[3] = m.w;
-      } else {
-        for (int q = 0; q < 4; ++q) {
-          uint32_t x = 0;
-          for (int b = 0; b < 4; ++b) {
-            const int64_t i = ib + 4 * q + b;
-            if (i < HW) x |= (uint32_t)(F.masks[(size_t)s * HW + i] != 0) << (8 * b);
-          }
-          w[q] = x;
-        }
-      }
-      if ((w[0] | w[1] | w[2] | w[3]) == 0) continue;
-      uint32_t set = 0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t nz = __vcmpne4(w[q], 0u) & 0x01010101u;
-        set |= ((nz & 1u) | ((nz >> 7) & 2u) | ((nz >> 14) & 4u) | ((nz >> 21) & 8u)) << (4 * q);
-      }
-      set &= inband;
-      if (!set) continue;
-      // per-patch pixel counts (regardless of depth) and bbox
-      int umin = INT32_MAX, umax = -1, vmin = INT32_MAX, vmax = -1;
-      {
-        int u = u_start, v = v_start;
-        int run_pc = -1;
-        uint32_t run_n = 0;
-        for (int j = 0; j < 16; ++j) {
-          if (set & (1u << j)) {
-            umin = min(umin, u); umax = max(umax, u);
-            vmin = min(vmin, v); vmax = max(vmax, v);
-            const int pc = pc_s[u];
-            if (pc != run_pc) {
-              if (run_n) atomicAdd(&cnt_s[s * Wp + run_pc], run_n);
-              run_pc = pc;
-              run_n = 0;
+        for (int t = 0; t < 4; ++t) {
+          const int j = 4 * j4 + t;
+          if (j < nin) {
+            const int p = pr_s[v - r0] * Wp + pc_s[u];
+            if (p != prevp) { pst |= 1u << j; prevp = p; }
+            if (depth_valid(dv[t], P)) {
+              float pw[3];
+              world_point(F, xa_s[u], yb_s[v - r0], dv[t], pw);
+              uint64_t key;
+              if (point_key(pw, r, key)) {
+                okb |= 1u << j;
+                if (key != prevk) { kst |= 1u << j; prevk = key; }
+              } else {
+                my_oor++;
+              }
             }
-            run_n++;
           }
           if (++u == W) { u = 0; ++v; }
         }
-        if (run_n) atomicAdd(&cnt_s[s * Wp + run_pc], run_n);
       }
-      atomicMin(&bb_s[4 * s + 0], umin);
-      atomicMin(&bb_s[4 * s + 1], vmin);
-      atomicMax(&bb_s[4 * s + 2], umax);
-      atomicMax(&bb_s[4 * s + 3], vmax);
-      // unique (s, key) pairs, run-compressed along the chunk
-      uint32_t pk = set & okbits;
-      if (!pk) continue;
-      {
-        int u = u_start, v = v_start;
-        uint64_t run_key = KEY_EMPTY;
-        uint32_t run_pslot = U32_EMPTY;
-        float ns0 = 0.f, ns1 = 0.f, ns2 = 0.f;
-        bool have_n = false;
-        for (int j = 0; j < 16; ++j) {
-          if (pk & (1u << j)) {
-            const uint64_t kj = ks[j * K1_THREADS];
-            if (kj != run_key) {
-              if (SEM && have_n && run_pslot != U32_EMPTY) {
-                atomicAdd(&nsum[3 * run_pslot + 0], ns0);
-                atomicAdd(&nsum[3 * run_pslot + 1], ns1);
-                atomicAdd(&nsum[3 * run_pslot + 2], ns2);
+    }
+    // ---- mask pass: two planes in flight per lane ----
+    for (int s0 = 0; s0 < S; s0 += 2) {
+      uint32_t w[2][8];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) w[k][t] = 0u;
+        if (lane_on && s0 + k < S) {
+          const uint8_t* mp = F.masks + (size_t)(s0 + k) * HW + ib;
+          if (F.vec16 && inb == 0xFFFFFFFFu) {
+            ld_stream32(mp, w[k]);
+          } else {
+            for (int t = 0; t < 8; ++t) {
+              uint32_t x = 0;
+              for (int b = 0; b < 4; ++b)
+                if (inb & (1u << (4 * t + b))) x |= (uint32_t)(mp[4 * t + b] != 0) << (8 * b);
+              w[k][t] = x;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int s = s0 + k;
+        if (s >= S) break;
+        uint32_t set = 0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) set |= nz_bits4(w[k][t]) << (4 * t);
+        set &= inb;
+        if (!__any_sync(0xffffffffu, set != 0)) continue;
+        const uint32_t pk = set & okb;
+        int nit = 0;
+        if (set) {
+          // per-patch pixel counts: popc over patch segments (O5, regardless of depth)
+          for (uint32_t g = pst; g;) {
+            const int a = __ffs(g) - 1;
+            g &= g - 1;
+            const int b = g ? __ffs(g) - 1 : 32;
+            const int cnum = __popc(set & range_bits(a, b));
+            if (cnum) {
+              int u, v;
+              pix_uv(ib + a, u, v);
+              atomicAdd(&cnt_g[(size_t)s * wb.PMAXP + pr_s[v - r0] * Wp + pc_s[u]], (uint32_t)cnum);
+            }
+          }
+          // bbox
+          const int j0 = __ffs(set) - 1, j1 = 31 - __clz(set);
+          if (!wraps) {
+            atomicMin(&bb_s[4 * s + 0], u_start + j0);
+            atomicMax(&bb_s[4 * s + 2], u_start + j1);
+            atomicMin(&bb_s[4 * s + 1], v_start);
+            atomicMax(&bb_s[4 * s + 3], v_start);
+          } else {
+            for (uint32_t g = set; g;) {
+              const int j = __ffs(g) - 1;
+              g &= g - 1;
+              int u, v;
+              pix_uv(ib + j, u, v);
+              atomicMin(&bb_s[4 * s + 0], u);
+              atomicMax(&bb_s[4 * s + 2], u);
+              atomicMin(&bb_s[4 * s + 1], v);
+              atomicMax(&bb_s[4 * s + 3], v);
+            }
+          }
+          // (s, key-run) items: key runs (kstart groups) intersecting pk
+          for (uint32_t g = kst; g;) {
+            const int a = __ffs(g) - 1;
+            g &= g - 1;
+            const int b = g ? __ffs(g) - 1 : 32;
+            if (pk & range_bits(a, b)) nit++;
+          }
+        }
+        int off = nit;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, off, o);
+          if (lane >= o) off += t;
+        }
+        const int total = __shfl_sync(0xffffffffu, off, 31);
+        off -= nit;
+        for (int base = 0; base < total; base += K1_QCAP) {
+          if (nit && off + nit > base && off < base + K1_QCAP) {
+            int idx = off;
+            for (uint32_t g = kst; g;) {
+              const int a = __ffs(g) - 1;
+              g &= g - 1;
+              const int b = g ? __ffs(g) - 1 : 32;
+              const uint32_t bits = pk & range_bits(a, b);
+              if (!bits) continue;
+              if (idx >= base && idx < base + K1_QCAP) {
+                int u, v;
+                pix_uv(ib + (__ffs(bits) - 1), u, v);
+                uint64_t key = KEY_EMPTY;
+                key_at(u, v, key);          // the run's key (recomputed, pinned R5)
+                K1Item it;
+                it.key = key;
+                it.pix = (uint32_t)ib;
+                it.bits = bits;
+                q_s[idx - base] = it;
+                qs_s[idx - base] = (uint16_t)s;
               }
-              ns0 = ns1 = ns2 = 0.f;
-              have_n = false;
-              run_key = kj;
-              // frame key table: only keys of mask pixels enter it (K5 releases every cell)
-              const uint32_t kslot = ktab_insert(ktab, tmask, kj, err);
-              bool fresh = false;
-              run_pslot = kslot == U32_EMPTY ? U32_EMPTY
-                                             : ptab_insert(ptab, tmask, ((uint32_t)s << 24) | kslot, &fresh, err);
-              if (fresh) {
-                DISC_CHECK(err, __ldcg(&ptab[run_pslot]) == (((uint32_t)s << 24) | kslot));
-                DISC_CHECK(err, __ldcg(&ktab[kslot]) == kj);
-                atomicAdd(&vs_s[s], 1u);
-                const uint32_t li = atomicAdd(&npl_s, 1u);
-                if (li < K1_PLIST) {
-                  pl_s[li] = run_pslot;
-                } else {
-                  const uint32_t gi = atomicAdd(&wb.npairs[f], 1u);
-                  if (gi < (uint32_t)wb.PMAX) wb.plist[(size_t)f * wb.PMAX + gi] = run_pslot;
-                  else raise_err(err, DERR_FRAME_PAIRS);
-                }
+              idx++;
+            }
+          }
+          __syncwarp();
+          const int nq = min(total - base, K1_QCAP);
+          if (SEM) {
+            // pixel-parallel normals: prefix of pixel counts over the queued items
+            for (int t0 = 0; t0 < nq; t0 += 32) {
+              const int t = t0 + lane;
+              int pc = t < nq ? __popc(q_s[t].bits) : 0;
+              int ex = pc;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, ex, o);
+                if (lane >= o) ex += y;
+              }
+              const int carry = t0 ? (int)qp_s[t0] : 0;
+              if (t < nq) qp_s[t + 1] = (uint32_t)(carry + ex);
+              if (t0 == 0 && lane == 0) qp_s[0] = 0;
+              if (t < nq) { qn_s[3 * t] = 0.f; qn_s[3 * t + 1] = 0.f; qn_s[3 * t + 2] = 0.f; }
+              __syncwarp();
+            }
+            const int npx = (int)qp_s[nq];
+            for (int x = lane; x < npx; x += 32) {
+              int lo = 0, hi = nq - 1;      // item with qp[i] <= x < qp[i+1]
+              while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if ((int)qp_s[mid] <= x) lo = mid;
+                else hi = mid - 1;
+              }
+              uint32_t bits = q_s[lo].bits;
+              for (int k2 = x - (int)qp_s[lo]; k2 > 0; --k2) bits &= bits - 1;
+              int u, v;
+              pix_uv((int64_t)q_s[lo].pix + (__ffs(bits) - 1), u, v);
+              float n[3];
+              if (pixel_normal(u, v, n)) {
+                atomicAdd(&qn_s[3 * lo + 0], n[0]);
+                atomicAdd(&qn_s[3 * lo + 1], n[1]);
+                atomicAdd(&qn_s[3 * lo + 2], n[2]);
+              }
+            }
+            __syncwarp();
+          }
+          for (int t = lane; t < nq; t += 32) {
+            const K1Item it = q_s[t];
+            const uint32_t s_it = qs_s[t];
+            const uint32_t kslot = ktab_insert(ktab, tmask, it.key, err);
+            if (kslot == U32_EMPTY) continue;
+            bool fresh = false;
+            const uint32_t pslot = ptab_insert(ptab, tmask, (s_it << 24) | kslot, &fresh, err);
+            if (pslot == U32_EMPTY) continue;
+            if (fresh) {
+              atomicAdd(&vs_s[s_it], 1u);
+              const uint32_t li = atomicAdd(&npl_s, 1u);
+              if (li < K1_PLIST) {
+                pl_s[li] = pslot;
+              } else {
+                const uint32_t gi = atomicAdd(&wb.npairs[f], 1u);
+                if (gi < (uint32_t)wb.PMAX) wb.plist[(size_t)f * wb.PMAX + gi] = pslot;
+                else raise_err(err, DERR_FRAME_PAIRS);
               }
             }
             if (SEM) {
-              float p[3], n[3];
-              world_point(F, xa_s[u], ybv(v), F.depth[ib + j], p);
-              if (pixel_normal(u, v, p, n)) {
-                ns0 += n[0]; ns1 += n[1]; ns2 += n[2];
-                have_n = true;
+              const float n0 = qn_s[3 * t], n1 = qn_s[3 * t + 1], n2 = qn_s[3 * t + 2];
+              if (n0 != 0.f || n1 != 0.f || n2 != 0.f) {
+                atomicAdd(&nsum[3 * pslot + 0], n0);
+                atomicAdd(&nsum[3 * pslot + 1], n1);
+                atomicAdd(&nsum[3 * pslot + 2], n2);
               }
             }
           }
-          if (++u == W) { u = 0; ++v; }
-        }
-        if (SEM && have_n && run_pslot != U32_EMPTY) {
-          atomicAdd(&nsum[3 * run_pslot + 0], ns0);
-          atomicAdd(&nsum[3 * run_pslot + 1], ns1);
-          atomicAdd(&nsum[3 * run_pslot + 2], ns2);
+          __syncwarp();
         }
       }
     }
   }
-  if (my_oor) atomicAdd(&oor_s, my_oor);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) my_oor += __shfl_xor_sync(0xffffffffu, my_oor, o);
+  if (lane == 0 && my_oor) atomicAdd(&oor_s, my_oor);
   __syncthreads();
 
-  // ---- flush ----
-  uint32_t* cnt_g = wb.cnt + (size_t)f * wb.SMAX * wb.PMAXP;
-  for (int i = threadIdx.x; i < S * Wp; i += blockDim.x) {
-    const int s = i / Wp, pc = i - s * Wp;
-    cnt_g[(size_t)s * wb.PMAXP + (size_t)band * Wp + pc] = cnt_s[i];
-  }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int s = warp; s < S; s += blockDim.x >> 5) {
-    uint32_t a = 0;
-    for (int pc = lane; pc < Wp; pc += 32) a += cnt_s[s * Wp + pc];
-#pragma unroll
-    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (lane == 0 && a) {
-      const size_t gi = (size_t)f * wb.SMAX + s;
-      atomicAdd(&wb.area[gi], a);
-      atomicMin(&wb.bbox[4 * gi + 0], bb_s[4 * s + 0]);
-      atomicMin(&wb.bbox[4 * gi + 1], bb_s[4 * s + 1]);
-      atomicMax(&wb.bbox[4 * gi + 2], bb_s[4 * s + 2]);
-      atomicMax(&wb.bbox[4 * gi + 3], bb_s[4 * s + 3]);
-      if (vs_s[s]) atomicAdd(&wb.vs[gi], vs_s[s]);
-    }
+  // ---- flush per-mask accumulators ----
+  for (int s = threadIdx.x; s < S; s += blockDim.x) {
+    if (bb_s[4 * s + 2] < 0) continue;   // mask absent from this tile
+    const size_t gi = (size_t)f * wb.SMAX + s;
+    atomicMin(&wb.bbox[4 * gi + 0], bb_s[4 * s + 0]);
+    atomicMin(&wb.bbox[4 * gi + 1], bb_s[4 * s + 1]);
+    atomicMax(&wb.bbox[4 * gi + 2], bb_s[4 * s + 2]);
+    atomicMax(&wb.bbox[4 * gi + 3], bb_s[4 * s + 3]);
+    if (vs_s[s]) atomicAdd(&wb.vs[gi], vs_s[s]);
   }
   __shared__ uint32_t base_s;
   const uint32_t n = min(npl_s, (uint32_t)K1_PLIST);
@@ -372,10 +521,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_mask_pass(WinDesc wd, WinBufs wb
     if (threadIdx.x == 0) raise_err(err, DERR_FRAME_PAIRS);
     return;
   }
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-    DISC_CHECK(err, pl_s[i] < (uint32_t)wb.PC && __ldcg(&ptab[pl_s[i]]) != U32_EMPTY);
-    wb.plist[(size_t)f * wb.PMAX + base_s + i] = pl_s[i];
-  }
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) wb.plist[(size_t)f * wb.PMAX + base_s + i] = pl_s[i];
 }
 
 // ------------------------------------------------------------------------------------------
@@ -468,7 +614,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_pairs(WinDesc wd, WinBufs wb, Pa
 // ------------------------------------------------------------------------------------------
 // K3: Eq.1 inputs.  fbar = mean_p f_p (fp64 partial sums, fixed-order reduction) and
 // r_p = |f_p - fbar| (fp32, one warp per patch).  rbar and D_p = r_p / (rbar + eps) are
-// formed in K4 (fixed-order reduction, per detection CTA).
+// formed by k_dmap (fixed-order reduction, one CTA per frame).
 // ------------------------------------------------------------------------------------------
 constexpr int K3_ROWS = 64;
 
@@ -532,9 +678,40 @@ __global__ void __launch_bounds__(256) k_resid(WinDesc wd, WinBufs wb, int Df) {
 }
 
 // ------------------------------------------------------------------------------------------
-// K4: one CTA per (mask, frame).
+// K3d: D_p = r_p / (rbar + eps) in place (Eq.1), one CTA per frame, fixed-order reduction.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_dmap(WinDesc wd, WinBufs wb, Params P) {
+  const int f = blockIdx.x;
+  if (f >= wd.n) return;
+  const FrameDesc& F = wd.f[f];
+  if (!F.feats) return;
+  const int Pn = F.Hp * F.Wp;
+  float* rp = wb.rp + (size_t)f * wb.PMAXP;
+  __shared__ double red[40];
+  double a = 0;
+  for (int p = threadIdx.x; p < Pn; p += blockDim.x) a += (double)rp[p];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if (lane == 0) red[warp] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    red[32] = t / (double)Pn;   // rbar
+  }
+  __syncthreads();
+  const double inv = 1.0 / (red[32] + (double)P.eps);
+  for (int p = threadIdx.x; p < Pn; p += blockDim.x) rp[p] = (float)((double)rp[p] * inv);
+}
+
+// ------------------------------------------------------------------------------------------
+// K4: one CTA per (mask, frame): mask filter (A1), D-weighted pooling (R18), D̄ (R19),
+// Q (Eq.2-3), tracking feature t_s (R15).  Patches of the mask's bbox are split across the
+// 8 warps; per-warp partial sums are combined in fixed warp order (deterministic).
 // ------------------------------------------------------------------------------------------
 constexpr int K4_THREADS = 256;
+constexpr int K4_WARPS = K4_THREADS / 32;
 
 __device__ __forceinline__ double block_sum_d(double x, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -563,6 +740,10 @@ __device__ __forceinline__ double dot_pin_warp(const double* a, const double* b,
   return acc;
 }
 
+size_t k4_smem_bytes(int Df, int Dt) {
+  return 40 * 8 + (size_t)K4_WARPS * Df * 4 + (size_t)K4_WARPS * (Dt > 0 ? Dt : 1) * 8 + (size_t)(Dt > 0 ? Dt : 1) * 8 + 64;
+}
+
 template <bool SEM>
 __global__ void __launch_bounds__(K4_THREADS) k_detect(WinDesc wd, WinBufs wb, Params P) {
   const int f = blockIdx.y;
@@ -571,15 +752,36 @@ __global__ void __launch_bounds__(K4_THREADS) k_detect(WinDesc wd, WinBufs wb, P
   const int s = blockIdx.x;
   if (s >= F.S) return;
   const int H = F.H, W = F.W, Hp = F.Hp, Wp = F.Wp, Df = P.Df, Dt = P.Dt;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const size_t gi = (size_t)f * wb.SMAX + s;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* red = (double*)smem_raw;                 // [33]
-  double* u_s = red + 40;                          // [Dt]
+  double* red = (double*)smem_raw;                         // [40]
+  float* ypart = (float*)(red + 40);                       // [K4_WARPS][Df]
+  double* upart = (double*)(ypart + (size_t)K4_WARPS * Df); // [K4_WARPS][Dt]
+  double* u_s = upart + (size_t)K4_WARPS * (Dt > 0 ? Dt : 1);  // [Dt]
 
-  // ---- A1: mask filter (R8), first failing reason wins: area==0, conf, aspect, area ----
-  const uint32_t area = wb.area[gi];
   const int umin = wb.bbox[4 * gi + 0], vmin = wb.bbox[4 * gi + 1];
   const int umax = wb.bbox[4 * gi + 2], vmax = wb.bbox[4 * gi + 3];
+  const uint32_t* cnt = wb.cnt + (size_t)f * wb.SMAX * wb.PMAXP + (size_t)s * wb.PMAXP;
+  // patch range of the bbox (all patches with cnt > 0 lie inside it)
+  int pr0 = 0, pr1 = -1, pc0 = 0, pc1 = -1;
+  if (umax >= 0) {
+    pr0 = (int)((int64_t)vmin * Hp / H); pr1 = (int)((int64_t)vmax * Hp / H);
+    pc0 = (int)((int64_t)umin * Wp / W); pc1 = (int)((int64_t)umax * Wp / W);
+  }
+  const int npc = pc1 - pc0 + 1, npr = pr1 - pr0 + 1, nbox = npr > 0 ? npr * npc : 0;
+  auto patch_of = [&](int k) { return (pr0 + k / npc) * Wp + pc0 + k % npc; };
+  auto npix_of = [&](int k) {   // pixels of patch k under the floor mapping (R17)
+    const int i = pr0 + k / npc, j = pc0 + k % npc;
+    const int64_t rows = ((int64_t)(i + 1) * H + Hp - 1) / Hp - ((int64_t)i * H + Hp - 1) / Hp;
+    const int64_t cols = ((int64_t)(j + 1) * W + Wp - 1) / Wp - ((int64_t)j * W + Wp - 1) / Wp;
+    return (double)(rows * cols);
+  };
+  double asum = 0;
+  for (int k = threadIdx.x; k < nbox; k += blockDim.x) asum += (double)cnt[patch_of(k)];
+  const uint32_t area = (uint32_t)block_sum_d(asum, red);
+
+  // ---- A1 mask filter (R8): first failing reason wins: area==0, conf, aspect, area ----
   const float conf = F.conf ? F.conf[s] : 1.0f;
   int status = 0;
   if (area == 0) status = 1;
@@ -592,6 +794,7 @@ __global__ void __launch_bounds__(K4_THREADS) k_detect(WinDesc wd, WinBufs wb, P
     else if (wb.vs[gi] == 0) status = 4;            // O3 no valid depth
   }
   float* qf = wb.qf + 6 * gi;
+  if (threadIdx.x == 0) wb.area[gi] = area;
   if (status != 0) {
     if (threadIdx.x == 0) {
       wb.status[gi] = status;
@@ -600,61 +803,67 @@ __global__ void __launch_bounds__(K4_THREADS) k_detect(WinDesc wd, WinBufs wb, P
     }
     return;
   }
-  const int pr0 = (int)((int64_t)vmin * Hp / H), pr1 = (int)((int64_t)vmax * Hp / H);
-  const int pc0 = (int)((int64_t)umin * Wp / W), pc1 = (int)((int64_t)umax * Wp / W);
-  const uint32_t* cnt = wb.cnt + (size_t)f * wb.SMAX * wb.PMAXP + (size_t)s * wb.PMAXP;
-  auto rows_of = [&](int i) { return (int)(((int64_t)(i + 1) * H + Hp - 1) / Hp - ((int64_t)i * H + Hp - 1) / Hp); };
-  auto cols_of = [&](int j) { return (int)(((int64_t)(j + 1) * W + Wp - 1) / Wp - ((int64_t)j * W + Wp - 1) / Wp); };
 
   if (SEM && F.feats) {
-    // rbar: fixed-order reduction of r_p over all P patches (Eq.1 denominator)
-    const int Pn = Hp * Wp;
-    const float* rp = wb.rp + (size_t)f * wb.PMAXP;
-    double a = 0;
-    for (int p = threadIdx.x; p < Pn; p += blockDim.x) a += (double)rp[p];
-    const double rbar = block_sum_d(a, red) / (double)Pn;
-    const double inv = 1.0 / (rbar + (double)P.eps);
-    // weights: w = D cnt/npix if cnt >= cover_min npix (exact), pass 1 = sums
+    const float* D = wb.rp + (size_t)f * wb.PMAXP;   // D_p (k_dmap)
+    // weight sums (O7): w = D cnt/npix if cnt >= cover_min npix (exact); D̄ over cnt > 0
     double wsum = 0, dnum = 0, dden = 0;
-    const int npr = pr1 - pr0 + 1, npc = pc1 - pc0 + 1;
-    for (int k = threadIdx.x; k < npr * npc; k += blockDim.x) {
-      const int i = pr0 + k / npc, j = pc0 + k % npc;
-      const uint32_t c = cnt[i * Wp + j];
+    for (int k = threadIdx.x; k < nbox; k += blockDim.x) {
+      const int p = patch_of(k);
+      const uint32_t c = cnt[p];
       if (!c) continue;
-      const double npix = (double)rows_of(i) * (double)cols_of(j);
-      const double D = (double)rp[i * Wp + j] * inv;
+      const double npix = npix_of(k);
       const double cov = (double)c / npix;
-      dnum += cov * D;
+      const double Dp = (double)D[p];
+      dnum += cov * Dp;
       dden += cov;
-      if ((double)c >= (double)P.cover_min * npix) wsum += D * cov;
+      if ((double)c >= (double)P.cover_min * npix) wsum += Dp * cov;
     }
     wsum = block_sum_d(wsum, red);
     dnum = block_sum_d(dnum, red);
     dden = block_sum_d(dden, red);
     const bool fallback = !(wsum > 0.0);
     const double dbar = dden > 0 ? dnum / dden : 0.0;
-    // pooling y = sum_p w_p f_p, ascending p; each thread owns 4 columns per step
+    // y = sum_p w_p f_p: warp w takes patches k = w, w + 8, ...; lane holds Df/32 columns
+    const int D4 = Df / 4;
+    const int nq4 = (D4 + 31) / 32;    // float4 per lane (Df <= 1024)
+    float4 acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = warp; k < nbox; k += K4_WARPS) {
+      const int p = patch_of(k);
+      const uint32_t c = cnt[p];
+      if (!c) continue;
+      float w;
+      if (fallback) {
+        w = 1.0f;
+      } else {
+        const double npix = npix_of(k);
+        if (!((double)c >= (double)P.cover_min * npix)) continue;
+        w = (float)((double)D[p] * ((double)c / npix));
+      }
+      const float4* row = (const float4*)(F.feats + (size_t)p * Df);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (i < nq4 && lane + 32 * i < D4) {
+          const float4 x = __ldg(row + lane + 32 * i);
+          acc[i].x = fmaf(w, x.x, acc[i].x); acc[i].y = fmaf(w, x.y, acc[i].y);
+          acc[i].z = fmaf(w, x.z, acc[i].z); acc[i].w = fmaf(w, x.w, acc[i].w);
+        }
+      }
+    }
+    float4* yp = (float4*)(ypart + (size_t)warp * Df);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i < nq4 && lane + 32 * i < D4) yp[lane + 32 * i] = acc[i];
+    __syncthreads();
     float* emb = wb.emb + gi * Df;
     double yy = 0;
-    for (int d4 = threadIdx.x; d4 < Df / 4; d4 += blockDim.x) {
-      float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int i = pr0; i <= pr1; ++i)
-        for (int j = pc0; j <= pc1; ++j) {
-          const uint32_t c = cnt[i * Wp + j];
-          if (!c) continue;
-          float w;
-          if (fallback) {
-            w = 1.0f;
-          } else {
-            const double npix = (double)rows_of(i) * (double)cols_of(j);
-            if (!((double)c >= (double)P.cover_min * npix)) continue;
-            w = (float)((double)rp[i * Wp + j] * inv * ((double)c / npix));
-          }
-          const float4 x = __ldg((const float4*)(F.feats + ((size_t)i * Wp + j) * Df) + d4);
-          y.x = fmaf(w, x.x, y.x); y.y = fmaf(w, x.y, y.y); y.z = fmaf(w, x.z, y.z); y.w = fmaf(w, x.w, y.w);
-        }
-      ((float4*)emb)[d4] = y;
-      yy += (double)y.x * y.x + (double)y.y * y.y + (double)y.z * y.z + (double)y.w * y.w;
+    for (int d = threadIdx.x; d < Df; d += blockDim.x) {
+      float y = 0.f;
+      for (int w2 = 0; w2 < K4_WARPS; ++w2) y += ypart[(size_t)w2 * Df + d];
+      emb[d] = y;
+      yy += (double)y * y;
     }
     yy = block_sum_d(yy, red);
     if (!(yy > 0.0)) {
@@ -693,19 +902,35 @@ __global__ void __launch_bounds__(K4_THREADS) k_detect(WinDesc wd, WinBufs wb, P
     for (int k = 0; k < 6; ++k) qf[k] = k == 4 ? -1.f : 0.f;   // geometry-only: no embedding
   }
 
-  // ---- A5b tracking feature (R15): u = sum_p cnt_sp g_p in fp64, ascending p ----
+  // ---- A5b tracking feature (R15): u = sum_p cnt_sp g_p in fp64 (exact for snapped inputs,
+  // so the warp-split order gives the oracle's bits), t = u / sqrt(dot_pin(u, u)) ----
   if (Dt > 0) {
+    const int nd = (Dt + 31) / 32;   // dims per lane (<= 16 on the register path)
+    double ua[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) ua[i] = 0.0;
+    for (int k = warp; k < nbox; k += K4_WARPS) {
+      const int p = patch_of(k);
+      const uint32_t c = cnt[p];
+      if (!c) continue;
+      const uint16_t* g = F.track + (size_t)p * Dt;
+      const double cd = (double)c;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int d = lane + 32 * i;
+        if (i < nd && d < Dt) ua[i] = __dadd_rn(ua[i], __dmul_rn(cd, (double)__uint_as_float((uint32_t)g[d] << 16)));
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int d = lane + 32 * i;
+      if (i < nd && d < Dt) upart[(size_t)warp * Dt + d] = ua[i];
+    }
+    __syncthreads();
     for (int d = threadIdx.x; d < Dt; d += blockDim.x) {
-      double acc = 0.0;
-      for (int i = pr0; i <= pr1; ++i)
-        for (int j = pc0; j <= pc1; ++j) {
-          const uint32_t c = cnt[i * Wp + j];
-          if (!c) continue;
-          const uint16_t b = F.track[((size_t)i * Wp + j) * Dt + d];
-          const float g = __uint_as_float((uint32_t)b << 16);
-          acc = __dadd_rn(acc, __dmul_rn((double)c, (double)g));
-        }
-      u_s[d] = acc;
+      double a = 0.0;
+      for (int w2 = 0; w2 < K4_WARPS; ++w2) a = __dadd_rn(a, upart[(size_t)w2 * Dt + d]);
+      u_s[d] = a;
     }
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -723,25 +948,29 @@ __global__ void __launch_bounds__(K4_THREADS) k_detect(WinDesc wd, WinBufs wb, P
 // ------------------------------------------------------------------------------------------
 // launchers
 // ------------------------------------------------------------------------------------------
-size_t k1_smem_bytes(int S, int W, int Wp, int rows_cap) {
-  return (size_t)S * Wp * 4 + (size_t)S * 16 + (size_t)S * 4 + (size_t)K1_PLIST * 4 + (size_t)W * 4 +
-         (size_t)((W + 1) & ~1) * 2 + (size_t)rows_cap * 4 + 16 + (size_t)16 * K1_THREADS * 8 + 16;
-}
+size_t k1_smem_bytes(int S, int W, int rows_cap) { return K1Smem(S, W, rows_cap).total; }
 
-void launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* err, bool sem, int maxS,
-                   int maxHp, int maxW, int maxWp, int maxP, int rows_cap, cudaStream_t st,
-                   cudaEvent_t ev0, cudaEvent_t ev1) {
+int k1_rows_cap(int W) { return K1_TILE / (W > 0 ? W : 1) + 4; }
+
+int k1_tiles(int64_t HW) { return (int)((HW + K1_TILE - 1) / K1_TILE); }
+
+int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* err, bool sem, int maxS,
+                  int maxHp, int maxW, int maxWp, int maxP, int rows_cap, cudaStream_t st,
+                  cudaEvent_t ev0, cudaEvent_t ev1) {
   const int n = wd.n;
-  k_win_init<<<dim3(1, n), 256, 0, st>>>(wd, wb);
+  int k1_grid = 1;
+  for (int i = 0; i < n; ++i) k1_grid = std::max(k1_grid, k1_tiles((int64_t)wd.f[i].H * wd.f[i].W));
+  (void)maxHp; (void)maxWp;
+  k_win_init<<<dim3(8, n), 256, 0, st>>>(wd, wb);
   debug_check(st, "k_win_init", -1);
-  const size_t sm1 = k1_smem_bytes(maxS, maxW, maxWp, rows_cap);
+  const size_t sm1 = k1_smem_bytes(maxS, maxW, rows_cap);
   if (ev0) cudaEventRecord(ev0, st);
   if (sem) {
     cudaFuncSetAttribute(k_mask_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
-    k_mask_pass<true><<<dim3(maxHp, n), K1_THREADS, sm1, st>>>(wd, wb, P, err, rows_cap);
+    k_mask_pass<true><<<dim3(k1_grid, n), K1_THREADS, sm1, st>>>(wd, wb, P, err, rows_cap);
   } else {
     cudaFuncSetAttribute(k_mask_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
-    k_mask_pass<false><<<dim3(maxHp, n), K1_THREADS, sm1, st>>>(wd, wb, P, err, rows_cap);
+    k_mask_pass<false><<<dim3(k1_grid, n), K1_THREADS, sm1, st>>>(wd, wb, P, err, rows_cap);
   }
   debug_check(st, "k_mask_pass", -1);
   if (ev1) cudaEventRecord(ev1, st);
@@ -755,12 +984,16 @@ void launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* e
     k_fbar_part<<<dim3(nch, n), 256, 0, st>>>(wd, wb, P.Df);
     k_fbar<<<dim3((P.Df + 255) / 256, n), 256, 0, st>>>(wd, wb, P.Df);
     k_resid<<<dim3((maxP + 7) / 8, n), 256, 0, st>>>(wd, wb, P.Df);
-    debug_check(st, "k_fbar/k_resid", -1);
+    k_dmap<<<n, 1024, 0, st>>>(wd, wb, P);
+    debug_check(st, "k_fbar/k_resid/k_dmap", -1);
   }
-  const size_t sm4 = 40 * 8 + (size_t)P.Dt * 8 + 64;
+  const size_t sm4 = k4_smem_bytes(P.Df, P.Dt);
+  cudaFuncSetAttribute(k_detect<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
+  cudaFuncSetAttribute(k_detect<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
   if (sem) k_detect<true><<<dim3(maxS, n), K4_THREADS, sm4, st>>>(wd, wb, P);
   else k_detect<false><<<dim3(maxS, n), K4_THREADS, sm4, st>>>(wd, wb, P);
   debug_check(st, "k_detect", -1);
+  return sem ? 8 : 4;
 }
 
 }  // namespace disc

@@ -192,14 +192,24 @@ constexpr int K6_THREADS = 1024;
 __device__ __forceinline__ double dot_pin_w(const double* a, const double* b, int n) {
   const int lane = threadIdx.x & 31;
   double acc = 0.0;
-  for (int d = lane; d < n; d += 32) acc = __fma_rn(a[d], b[d], acc);
+  int d = lane;
+  for (; d + 96 < n; d += 128) {   // loads of four steps in flight; fma order unchanged (R15)
+    const double a0 = a[d], b0 = b[d], a1 = a[d + 32], b1 = b[d + 32];
+    const double a2 = a[d + 64], b2 = b[d + 64], a3 = a[d + 96], b3 = b[d + 96];
+    acc = __fma_rn(a0, b0, acc);
+    acc = __fma_rn(a1, b1, acc);
+    acc = __fma_rn(a2, b2, acc);
+    acc = __fma_rn(a3, b3, acc);
+  }
+  for (; d < n; d += 32) acc = __fma_rn(a[d], b[d], acc);
 #pragma unroll
   for (int o = 16; o; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
   return acc;
 }
 
 struct K6Smem {   // offsets into dynamic shared memory
-  size_t t_s, t_j, t_c, t_e, t_jl, lab, jnode, comp_root, comp_best, comp_tgt, has_edge, total;
+  size_t t_s, t_j, t_c, t_e, t_jl, lab, jnode, comp_root, comp_best, comp_tgt, has_edge, d_st, d_vs, d_tgt, d_q,
+      total;
   __host__ __device__ K6Smem(int S, int TC) {
     size_t o = 0;
     auto take = [&](size_t bytes) { const size_t r = o; o = (o + bytes + 15) & ~(size_t)15; return r; };
@@ -207,6 +217,8 @@ struct K6Smem {   // offsets into dynamic shared memory
     t_s = take(4 * (size_t)TC); t_j = take(4 * (size_t)TC); t_c = take(4 * (size_t)TC);
     t_e = take((size_t)TC); t_jl = take(4 * (size_t)TC); lab = take(4 * NN); jnode = take(4 * (size_t)TC);
     comp_root = take(4 * NN); comp_best = take(8 * NN); comp_tgt = take(4 * NN); has_edge = take((size_t)S + 1);
+    d_st = take(4 * (size_t)S + 4); d_vs = take(4 * (size_t)S + 4); d_tgt = take(4 * (size_t)S + 4);
+    d_q = take(4 * (size_t)S + 4);
     total = o;
   }
 };
@@ -228,6 +240,10 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
   unsigned long long* comp_best = (unsigned long long*)(smem_raw + L6.comp_best);
   int32_t* comp_tgt = (int32_t*)(smem_raw + L6.comp_tgt);
   uint8_t* has_edge = (uint8_t*)(smem_raw + L6.has_edge);
+  int32_t* d_st = (int32_t*)(smem_raw + L6.d_st);     // per-detection status (staged from global)
+  uint32_t* d_vs = (uint32_t*)(smem_raw + L6.d_vs);   // |V_s|
+  int32_t* d_tgt = (int32_t*)(smem_raw + L6.d_tgt);   // target index (written back at the end)
+  float* d_q = (float*)(smem_raw + L6.d_q);           // Q_s
   __shared__ uint32_t n_tr, n_j, n_tgt, n_seg;
   __shared__ int changed;
   __shared__ unsigned long long rel_s, merged_s, edges_s;
@@ -251,7 +267,10 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
   }
   for (int i = tid; i < S; i += blockDim.x) {
     has_edge[i] = 0;
-    X.det_target[i] = -1;
+    d_tgt[i] = -1;
+    d_st[i] = wb.status[fo + i];
+    d_vs[i] = wb.vs[fo + i];
+    d_q[i] = wb.qf[(fo + i) * 6 + 4];
     X.det_id[i] = -1;
     X.tgt_stage[i] = 0;
   }
@@ -271,7 +290,7 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
   const double* trk = wb.trk + fo * P.Dt;
   for (uint32_t t = warp; t < ntr; t += nwarp) {
     const uint32_t s = t_s[t], j = t_j[t], c = t_c[t];
-    const int64_t vs = wb.vs[fo + s], vj = M.vcount[j];
+    const int64_t vs = d_vs[s], vj = M.vcount[j];
     const int64_t mn = vs < vj ? vs : vj;
     bool e = c >= 1 && (double)c >= (double)P.tau_geo * (double)mn;
     if (e && P.Dt > 0) {
@@ -352,10 +371,10 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
     int64_t nid = M.counters[0];
     int64_t created = 0;
     for (int s = 0; s < S; ++s) {
-      if (wb.status[fo + s] != 0) continue;
+      if (d_st[s] != 0) continue;
       if (has_edge[s]) {
         const int t = comp_tgt[lab[s]];
-        X.det_target[s] = t;
+        d_tgt[s] = t;
         X.det_id[s] = X.tgt_root[t];
       } else {
         if (nid >= M.IMAX) {
@@ -363,7 +382,7 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
           break;
         }
         const int t = (int)n_tgt++;
-        X.det_target[s] = t;
+        d_tgt[s] = t;
         X.det_id[s] = nid;
         X.tgt_root[t] = (uint32_t)nid;
         X.tgt_phys[t] = (uint32_t)nid;
@@ -416,13 +435,13 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
     }
     // detections Sd ascending
     for (int s = 0; s < S; ++s) {
-      if (X.det_target[s] != t) continue;
+      if (d_tgt[s] != t) continue;
       obs += 1;
       for (int k = 0; k < 3; ++k) {
         ab[k] = min(ab[k], wb.daabb[(fo + s) * 6 + k]);
         ab[3 + k] = max(ab[3 + k], wb.daabb[(fo + s) * 6 + 3 + k]);
       }
-      const float qs = wb.qf[(fo + s) * 6 + 4];
+      const float qs = d_q[s];
       if (qs > qcur) { qcur = qs; src_kind = 2; src_id = (uint32_t)s; }
       const double* ts = trk + (size_t)s * P.Dt;
       for (int d = lane; d < P.Dt; d += 32) Tr[d] = __dadd_rn(Tr[d], ts[d]);
@@ -470,8 +489,9 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
   }
   __syncthreads();
   // ---- new instances (isolated kept detections) ----
+  for (int s = tid; s < S; s += blockDim.x) X.det_target[s] = d_tgt[s];
   for (int s = warp; s < S; s += nwarp) {
-    const int t = X.det_target[s];
+    const int t = d_tgt[s];
     if (t < 0 || has_edge[s]) continue;
     const uint32_t id = X.tgt_root[t];
     if (lane == 0) {
@@ -482,12 +502,12 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
       M.obs[id] = 1;
       M.last_seen[id] = F.frame_id;
       for (int k = 0; k < 6; ++k) M.aabb[(size_t)id * 6 + k] = wb.daabb[(fo + s) * 6 + k];
-      M.q[id] = wb.qf[(fo + s) * 6 + 4];
+      M.q[id] = d_q[s];
       M.lst_len[id] = 0;
       M.lst_cap[id] = 0;
     }
     for (int d = lane; d < P.Dt; d += 32) M.T[(size_t)id * P.Dt + d] = trk[(size_t)s * P.Dt + d];
-    const bool has_e = sem && wb.qf[(fo + s) * 6 + 4] >= 0.f;
+    const bool has_e = sem && d_q[s] >= 0.f;
     for (int d = lane; d < P.Df; d += 32) M.E[(size_t)id * P.Df + d] = has_e ? wb.emb[(fo + s) * P.Df + d] : 0.f;
   }
   // ---- debug copies of the triples, edge count ----
@@ -513,8 +533,8 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
     int kept = 0, da = 0, dc = 0, dasp = 0, dnd = 0, dnf = 0;
     int64_t U = 0;
     for (int s = 0; s < S; ++s) {
-      switch (wb.status[fo + s]) {
-        case 0: kept++; U += wb.vs[fo + s]; break;
+      switch (d_st[s]) {
+        case 0: kept++; U += d_vs[s]; break;
         case 1: da++; break;
         case 2: dc++; break;
         case 3: dasp++; break;
@@ -527,6 +547,9 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
     R.key_out_of_range = (int64_t)wb.oor[f];
     R.unique_pairs = U;
     R.edges = (int64_t)edges_s;
+    M.counters[4] += U;
+    M.counters[7] += (int64_t)edges_s;
+    M.counters[6] += (int64_t)acc;
     R.merged_away = (int64_t)merged_s;
     R.relabeled = (int64_t)rel_s;
     M.counters[1] -= (int64_t)merged_s;
@@ -644,7 +667,10 @@ __global__ void __launch_bounds__(256) k_grow(int f, MapState M, FrameScratch X)
     __syncthreads();
     if (threadIdx.x == 0) M.lst_off[L] = newoff;
   }
-  if (threadIdx.x == 0) M.lst_len[L] = oldlen + add;
+  if (threadIdx.x == 0) {
+    M.lst_len[L] = oldlen + add;
+    atomicAdd((unsigned long long*)&M.counters[5], (unsigned long long)add);
+  }
 }
 
 // K7c: fill the appended list cells (warp-aggregated positions)
@@ -670,8 +696,8 @@ __global__ void __launch_bounds__(256) k_fill(MapState M, FrameScratch X) {
 
 size_t k6_smem_bytes(int S, int TC) { return K6Smem(S, TC).total; }
 
-void launch_stage2_frame(int f, const FrameDesc& F, const WinBufs& wb, const MapState& M, const FrameScratch& X,
-                         const Params& P, bool sem, int nsm, cudaStream_t st) {
+int launch_stage2_frame(int f, const FrameDesc& F, const WinBufs& wb, const MapState& M, const FrameScratch& X,
+                        const Params& P, bool sem, int nsm, cudaStream_t st) {
   k_lookup<<<2 * nsm, 256, 0, st>>>(f, wb, M, X);
   debug_check(st, "k_lookup", f);
   const size_t sm6 = k6_smem_bytes(wb.SMAX, X.TCAP);
@@ -684,6 +710,7 @@ void launch_stage2_frame(int f, const FrameDesc& F, const WinBufs& wb, const Map
   debug_check(st, "k_grow", f);
   k_fill<<<nsm, 256, 0, st>>>(M, X);
   debug_check(st, "k_fill", f);
+  return 5;
 }
 
 }  // namespace disc

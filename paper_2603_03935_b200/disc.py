@@ -86,7 +86,8 @@ class disc_stats(C.Structure):
     _fields_ = [("frames", C.c_int64), ("k1_ms", C.c_double), ("k1_launches", C.c_int64),
                 ("stage1_ms", C.c_double), ("stage2_ms", C.c_double), ("mask_bytes", C.c_int64),
                 ("depth_bytes", C.c_int64), ("track_bytes", C.c_int64), ("feat_bytes", C.c_int64),
-                ("pairs", C.c_int64), ("map_inserts", C.c_int64), ("relabels", C.c_int64)]
+                ("pairs", C.c_int64), ("map_inserts", C.c_int64), ("relabels", C.c_int64),
+                ("edges", C.c_int64), ("launches", C.c_int64)]
 
 
 EXPORTS = {
