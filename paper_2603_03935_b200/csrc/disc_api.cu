@@ -136,7 +136,7 @@ bool pose_rigid(const float* P) {   // A0, S:116-118 (same decision rule as docu
 
 std::string validate_frame(const disc_map* m, const disc_frame& f, bool host) {
   const disc_config& c = m->cfg;
-  if (f.height <= 0 || f.width <= 0) return "bad image dims";
+  if (f.height <= 0 || f.width <= 0 || f.height > 65535 || f.width > 65535) return "bad image dims";
   if ((int64_t)f.height * f.width > c.max_pixels) return "H*W exceeds max_pixels";
   if (!f.depth) return "null depth";
   if (f.num_masks < 0 || f.num_masks > c.max_masks) return "num_masks outside [0, max_masks]";
@@ -353,6 +353,7 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(M.q = dalloc<float>(m, IM));
   chk(M.E = dalloc<float>(m, (size_t)IM * Df));
   chk(M.T = dalloc<double>(m, (size_t)IM * std::max(Dt, 1)));
+  chk(M.TT = dalloc<double>(m, IM));
   chk(M.lst_off = dalloc<unsigned long long>(m, IM));
   chk(M.lst_len = dalloc<uint32_t>(m, IM));
   chk(M.lst_cap = dalloc<uint32_t>(m, IM));
@@ -366,7 +367,7 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   // ---- per-frame scratch ----
   FrameScratch& X = m->X;
   X.CC = 16384;
-  X.TCAP = 4096;
+  X.TCAP = 3072;
   X.STCAP = (uint32_t)std::min<int64_t>(cfg->max_memberships + PMAX, 0xFFFFFFF0ll);
   chk(X.ctab_key = dalloc<unsigned long long>(m, X.CC, 0xFF));
   chk(X.ctab_cnt = dalloc<uint32_t>(m, X.CC));
@@ -384,6 +385,14 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(X.tgt_fill = dalloc<uint32_t>(m, SM));
   chk(X.tgt_base = dalloc<uint32_t>(m, SM));
   chk(X.ntgt = dalloc<int32_t>(m, 1));
+  chk(X.tg_kind = dalloc<int32_t>(m, SM));
+  chk(X.tg_vbase = dalloc<int64_t>(m, SM));
+  chk(X.tg_moff = dalloc<uint32_t>(m, SM));
+  chk(X.tg_mcnt = dalloc<uint32_t>(m, SM));
+  chk(X.tg_doff = dalloc<uint32_t>(m, SM));
+  chk(X.tg_dcnt = dalloc<uint32_t>(m, SM));
+  chk(X.tg_mem = dalloc<uint32_t>(m, X.TCAP));
+  chk(X.tg_dets = dalloc<uint32_t>(m, SM));
   chk(X.seg_phys = dalloc<uint32_t>(m, X.TCAP));
   chk(X.seg_tgt = dalloc<int32_t>(m, X.TCAP));
   chk(X.seg_off = dalloc<uint32_t>(m, X.TCAP + 1));
@@ -694,6 +703,7 @@ disc_status disc_get_stats(disc_map* m, disc_stats* s) {
   disc_status st = disc_sync(m);
   if (st != DISC_OK) return st;
   collect_events(m);
+  if (getenv("DISC_K6PROF")) k6_prof_dump();
   int64_t ctr[8];
   cudaMemcpy(ctr, m->M.counters, sizeof(ctr), cudaMemcpyDeviceToHost);
   m->stats.pairs = ctr[4];

@@ -119,6 +119,7 @@ struct MapState {
   float* q;
   float* E;                   // [Df]
   double* T;                  // [Dt]
+  double* TT;                 // dot_pin(T_j, T_j) (R15), refreshed whenever T_j changes
   // per physical label key-slot lists (for relabel enumeration)
   unsigned long long* lst_off;
   uint32_t* lst_len;
@@ -153,6 +154,15 @@ struct FrameScratch {
   uint32_t* tgt_fill;            // [SMAX]
   uint32_t* tgt_base;            // [SMAX]
   int32_t* ntgt;                 // [1]
+  // per-target O12 work lists (written by K6, executed by K7a)
+  int32_t* tg_kind;              // [SMAX] 0 = component with instances, 1 = new instance
+  int64_t* tg_vbase;             // [SMAX] |V| of the physical owner
+  uint32_t* tg_moff;             // [SMAX] offset into tg_mem (member ids ascending)
+  uint32_t* tg_mcnt;
+  uint32_t* tg_doff;             // [SMAX] offset into tg_dets (detections ascending)
+  uint32_t* tg_dcnt;
+  uint32_t* tg_mem;              // [TCAP]
+  uint32_t* tg_dets;             // [SMAX]
   // relabel segments
   uint32_t* seg_phys;            // [TCAP] old physical label
   int32_t* seg_tgt;              // [TCAP]

@@ -13,6 +13,7 @@
 #include "disc_launch.h"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace disc {
 
@@ -125,105 +126,171 @@ __global__ void k_win_init(WinDesc wd, WinBufs wb) {
 }
 
 // ------------------------------------------------------------------------------------------
-// K1: mask pass.  Grid = (ceil(H*W / K1_TILE), frames); a CTA owns K1_TILE consecutive
-// pixels (row-major), a warp 1024 consecutive pixels per step, a lane a 32-pixel chunk.
-// Pixel pass (once per chunk): pinned keys (R5) of the 32 pixels, reduced to three bit masks:
-// ok (key valid), kstart (a new voxel key begins), pstart (a new patch begins).  Mask pass:
-// per plane one 256-bit streaming load per lane (evict-first in L2, two planes in flight);
-// per-patch counts = popc over patch segments, bbox from ffs/clz, (s, key-run) items into a
-// per-warp queue that all 32 lanes then process: pixel normals pixel-parallel (R21), frame
-// key / pair table inserts item-parallel.
+// K1: mask pass.  2-D tiles: a CTA owns 32 rows x 128 columns of one frame, a warp 32 rows x 32
+// columns (lane = row, 32 consecutive pixels per lane).  Depth (+1-pixel halo) is staged in
+// shared memory; mask planes stream into a shared-memory ring with cp.async.  Uniform phases:
+//  1 keys: pinned keys (R5) of the lane's pixels -> ok / kstart (voxel-key runs) / pstart
+//    (patches); each run's key enters the CTA key table (local key index per run).
+//  2 masks: per plane, branch-free byte SIMD records each pixel's first mask (m0) and flags
+//    pixels covered by a second mask; per-patch counts by popc over patch segments; bbox.
+//  3 pairs: one walk over the lane's pixels forms (m0, key-run) items, sums their pixel normals
+//    (R21, semantic mode) and inserts the 32-bit code (m0, local key) into the CTA pair table;
+//    the first inserter of a code inserts (s, key) into the frame's global tables.
+//  4 overlap: pixels in more than one mask (R9) re-read their other planes (slow path).
+//  Normal sums are accumulated per pair-table slot and flushed once per CTA.
 // ------------------------------------------------------------------------------------------
 constexpr int K1_THREADS = 128;
 constexpr int K1_WARPS = K1_THREADS / 32;
-constexpr int K1_PPL = 32;                                // pixels per lane (chunk)
-constexpr int K1_CPL = 2;                                 // chunks per lane
-constexpr int K1_TILE = K1_THREADS * K1_PPL * K1_CPL;     // pixels per CTA
-constexpr int K1_QCAP = 64;                               // per-warp item queue
+constexpr int K1_TW = 32;                                 // tile columns per warp (pixels per lane)
+constexpr int K1_TILE_W = K1_WARPS * K1_TW;               // CTA tile: 32 rows x 128 columns
+constexpr int K1_TILE_H = 32;
+constexpr int K1_KT = 1024;                               // CTA key table slots
+constexpr int K1_PT = 1024;                               // CTA pair table slots
 constexpr int K1_PLIST = 1024;
-
-struct K1Item {
-  unsigned long long key;
-  uint32_t pix;       // linear index of the chunk's first pixel
-  uint32_t bits;      // pixels of this (s, key) run within the chunk
-};
+constexpr int K1_DS = 131;                                // depth tile row stride (130 columns + pad)
+constexpr int K1_MS = 144;                                // mask tile row stride in bytes
+constexpr int K1_NG = 3;                                  // ring slots (plane pairs)
+constexpr uint16_t K1_NOKEY = 0xFFFF;
 
 struct K1Smem {
-  size_t bb, vs, pl, q, qs, qp, qn, xa, pc, rows, total;
-  __host__ __device__ K1Smem(int S, int W, int rows_cap) {
+  size_t bb, vs, pl, kt, gl, m0, pt, pp, pn, xa, pc, dep, msk, total;
+  __host__ __device__ K1Smem(int S, bool sem) {
     size_t o = 0;
     auto take = [&](size_t b) { const size_t r = o; o = (o + b + 15) & ~(size_t)15; return r; };
     bb = take((size_t)S * 16);
     vs = take((size_t)S * 4);
     pl = take((size_t)K1_PLIST * 4);
-    q = take((size_t)K1_WARPS * K1_QCAP * sizeof(K1Item));
-    qs = take((size_t)K1_WARPS * K1_QCAP * 2);               // item mask index s
-    qp = take((size_t)K1_WARPS * (K1_QCAP + 1) * 4);         // item pixel prefix
-    qn = take((size_t)K1_WARPS * K1_QCAP * 12);              // item normal sums
-    xa = take((size_t)W * 4);
-    pc = take((size_t)W * 2);
-    rows = take((size_t)rows_cap * 8);
+    kt = take((size_t)K1_KT * 8);
+    gl = take((size_t)32 * K1_THREADS * 2);              // local key index per run
+    m0 = take((size_t)8 * K1_THREADS * 4);               // first mask per pixel, 4 per word
+    pt = take((size_t)K1_PT * 4);
+    pp = take((size_t)K1_PT * 4);
+    pn = take(sem ? (size_t)K1_PT * 12 : 16);
+    xa = take((size_t)(K1_TILE_W + 2) * 4);
+    pc = take((size_t)(K1_TILE_W + 2) * 2);
+    dep = take((size_t)(K1_TILE_H + 2) * K1_DS * 4);
+    msk = take((size_t)K1_NG * 2 * K1_TILE_H * K1_MS);
     total = o;
   }
 };
 
-__device__ __forceinline__ void ld_stream32(const uint8_t* p, uint32_t r[8]) {
-  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "l"(p));
-}
-
 __device__ __forceinline__ uint32_t nz_bits4(uint32_t w) {   // bit b set iff byte b of w != 0
-  const uint32_t nz = __vcmpne4(w, 0u) & 0x01010101u;
-  return (nz & 1u) | ((nz >> 7) & 2u) | ((nz >> 14) & 4u) | ((nz >> 21) & 8u);
+  return ((__vcmpne4(w, 0u) & 0x08040201u) * 0x01010101u) >> 24;
 }
 
 __device__ __forceinline__ uint32_t range_bits(int a, int b) {   // bits [a, b), 0 <= a < b <= 32
   return (b >= 32 ? 0xFFFFFFFFu : ((1u << b) - 1u)) & ~((1u << a) - 1u);
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, uint32_t src_bytes) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// R21: n = (P(u+1,v) - P(u-1,v)) x (P(u,v+1) - P(u,v-1)), oriented so n . (cam - P) >= 0.
+__device__ __forceinline__ bool normal_from(const FrameDesc& F, const float pc[3], const float pl[3],
+                                            const float pr[3], const float pu[3], const float pd[3], float n[3]) {
+  const float a0 = pr[0] - pl[0], a1 = pr[1] - pl[1], a2 = pr[2] - pl[2];
+  const float b0 = pd[0] - pu[0], b1 = pd[1] - pu[1], b2 = pd[2] - pu[2];
+  n[0] = a1 * b2 - a2 * b1;
+  n[1] = a2 * b0 - a0 * b2;
+  n[2] = a0 * b1 - a1 * b0;
+  if (n[0] == 0.f && n[1] == 0.f && n[2] == 0.f) return false;
+  const float o = n[0] * (F.pose[3] - pc[0]) + n[1] * (F.pose[7] - pc[1]) + n[2] * (F.pose[11] - pc[2]);
+  if (o < 0.f) { n[0] = -n[0]; n[1] = -n[1]; n[2] = -n[2]; }
+  return true;
+}
+
 template <bool SEM>
-__global__ void __launch_bounds__(K1_THREADS, 8) k_mask_pass(WinDesc wd, WinBufs wb, Params P, int* err,
-                                                             int rows_cap) {
+__global__ void __launch_bounds__(K1_THREADS, 2) k_mask_pass(WinDesc wd, WinBufs wb, Params P, int* err,
+                                                             int rows_cap, int ablate) {
+  (void)rows_cap;
   const int f = blockIdx.y;
   if (f >= wd.n) return;
   const FrameDesc& F = wd.f[f];
   const int H = F.H, W = F.W, S = F.S, Hp = F.Hp, Wp = F.Wp;
   const int64_t HW = (int64_t)H * W;
-  const int64_t tile0 = (int64_t)blockIdx.x * K1_TILE;
-  if (tile0 >= HW) return;
-  const int64_t tile1 = min(HW, tile0 + (int64_t)K1_TILE);
-  const int vt0 = (int)(tile0 / W), vt1 = (int)((tile1 - 1) / W);
-  const int r0 = vt0 - 1;
+  const int ntx = (W + K1_TILE_W - 1) / K1_TILE_W, nty = (H + K1_TILE_H - 1) / K1_TILE_H;
+  if ((int)blockIdx.x >= ntx * nty) return;
+  const int ty = blockIdx.x / ntx, tx = blockIdx.x - ty * ntx;
+  const int ut0 = tx * K1_TILE_W, vt0 = ty * K1_TILE_H;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int v = vt0 + lane;                                 // this lane's row
+  const int u0 = ut0 + warp * K1_TW;                        // first column of the lane's chunk
+  const int c0 = warp * K1_TW + 1;                          // its column in the staged tiles
+  const bool lane_on = v < H && u0 < W;
+  const int nin = lane_on ? min(K1_TW, W - u0) : 0;
+  const uint32_t inb = nin >= 32 ? 0xFFFFFFFFu : ((1u << nin) - 1u);
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const K1Smem L(S, W, rows_cap);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const K1Smem L(S, SEM);
   int32_t* bb_s = (int32_t*)(smem_raw + L.bb);
   uint32_t* vs_s = (uint32_t*)(smem_raw + L.vs);
   uint32_t* pl_s = (uint32_t*)(smem_raw + L.pl);
-  K1Item* q_s = (K1Item*)(smem_raw + L.q) + warp * K1_QCAP;
-  uint16_t* qs_s = (uint16_t*)(smem_raw + L.qs) + warp * K1_QCAP;
-  uint32_t* qp_s = (uint32_t*)(smem_raw + L.qp) + warp * (K1_QCAP + 1);
-  float* qn_s = (float*)(smem_raw + L.qn) + warp * K1_QCAP * 3;
-  float* xa_s = (float*)(smem_raw + L.xa);
+  unsigned long long* kt = (unsigned long long*)(smem_raw + L.kt);   // CTA key table
+  uint16_t* gl = (uint16_t*)(smem_raw + L.gl) + threadIdx.x;         // gl[run * K1_THREADS]
+  uint32_t* m0w = (uint32_t*)(smem_raw + L.m0) + threadIdx.x;        // m0w[word * K1_THREADS]
+  uint32_t* pt = (uint32_t*)(smem_raw + L.pt);                       // CTA pair table: (s << 16 | local key)
+  uint32_t* ptp = (uint32_t*)(smem_raw + L.pp);                      // -> global pair slot
+  float* ptn = (float*)(smem_raw + L.pn);                            // -> normal sums
+  float* xa_s = (float*)(smem_raw + L.xa);            // column c <-> u = ut0 - 1 + c
   uint16_t* pc_s = (uint16_t*)(smem_raw + L.pc);
-  float* yb_s = (float*)(smem_raw + L.rows);
-  int32_t* pr_s = (int32_t*)(yb_s + rows_cap);
+  float* dep = (float*)(smem_raw + L.dep);            // [34][K1_DS], row r <-> v = vt0 - 1 + r
+  uint8_t* msk = (uint8_t*)(smem_raw + L.msk);        // [K1_NG][2][32][K1_MS]
   __shared__ uint32_t npl_s, oor_s;
+
+  // ---- mask stream: plane pairs into the ring with cp.async ----
+  const int ngroups = (S + 1) / 2;
+  const bool async_ok = F.vec16 && (W & 15) == 0;     // 16-byte aligned rows
+  auto issue = [&](int g) {
+    if (g < ngroups && !(ablate & 1)) {
+      uint8_t* slot = msk + (size_t)(g % K1_NG) * 2 * K1_TILE_H * K1_MS;
+      for (int k = 0; k < 2; ++k) {
+        const int s = 2 * g + k;
+        uint8_t* dst = slot + (size_t)k * K1_TILE_H * K1_MS;
+        for (int idx = threadIdx.x; idx < K1_TILE_H * 8; idx += K1_THREADS) {
+          const int row = idx >> 3, c16 = idx & 7;
+          const int vv = vt0 + row, uu = ut0 + 16 * c16;
+          const bool in = s < S && vv < H && uu < W;
+          const uint8_t* src = in ? F.masks + (size_t)s * HW + (int64_t)vv * W + uu : F.masks;
+          uint8_t* d = dst + row * K1_MS + 16 * c16;
+          if (async_ok) {
+            cp_async16(d, src, in ? (uint32_t)min(16, W - uu) : 0u);
+          } else {
+            for (int b = 0; b < 16; ++b) d[b] = (in && uu + b < W) ? src[b] : 0;
+          }
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  for (int g = 0; g < K1_NG - 1; ++g) issue(g);
 
   for (int i = threadIdx.x; i < S; i += blockDim.x) {
     bb_s[4 * i + 0] = INT32_MAX; bb_s[4 * i + 1] = INT32_MAX;
     bb_s[4 * i + 2] = -1; bb_s[4 * i + 3] = -1;
     vs_s[i] = 0;
   }
-  for (int u = threadIdx.x; u < W; u += blockDim.x) {
-    xa_s[u] = __fdiv_rn(__fsub_rn((float)u, F.cx), F.fx);   // R5: ((float)u - cx) / fx
-    pc_s[u] = (uint16_t)(((int64_t)u * Wp) / W);             // R17 floor mapping
+  for (int i = threadIdx.x; i < K1_KT; i += blockDim.x) kt[i] = KEY_EMPTY;
+  for (int i = threadIdx.x; i < K1_PT; i += blockDim.x) {
+    pt[i] = U32_EMPTY;
+    ptp[i] = U32_EMPTY;
+    if (SEM) { ptn[3 * i] = 0.f; ptn[3 * i + 1] = 0.f; ptn[3 * i + 2] = 0.f; }
   }
-  for (int v = r0 + (int)threadIdx.x; v <= vt1 + 1; v += blockDim.x) {
-    yb_s[v - r0] = __fdiv_rn(__fsub_rn((float)v, F.cy), F.fy);
-    pr_s[v - r0] = (int32_t)(((int64_t)v * Hp) / H);
+  for (int t = 0; t < 8; ++t) m0w[t * K1_THREADS] = 0xFFFFFFFFu;   // no mask yet
+  for (int c = threadIdx.x; c < K1_TILE_W + 2; c += blockDim.x) {
+    const int u = ut0 - 1 + c;
+    xa_s[c] = (u >= 0 && u < W) ? __fdiv_rn(__fsub_rn((float)u, F.cx), F.fx) : 0.f;   // R5
+    pc_s[c] = (u >= 0 && u < W) ? (uint16_t)(((int64_t)u * Wp) / W) : 0;            // R17
+  }
+  for (int idx = threadIdx.x; idx < (K1_TILE_H + 2) * (K1_TILE_W + 2); idx += blockDim.x) {
+    const int r = idx / (K1_TILE_W + 2), c = idx - r * (K1_TILE_W + 2);
+    const int vv = vt0 - 1 + r, uu = ut0 - 1 + c;
+    dep[r * K1_DS + c] =
+        (vv >= 0 && vv < H && uu >= 0 && uu < W) ? __ldg(F.depth + (int64_t)vv * W + uu) : __int_as_float(0x7fc00000);
   }
   if (threadIdx.x == 0) { npl_s = 0; oor_s = 0; }
   __syncthreads();
@@ -234,271 +301,229 @@ __global__ void __launch_bounds__(K1_THREADS, 8) k_mask_pass(WinDesc wd, WinBufs
   float* nsum = wb.nsum + (size_t)f * wb.PC * 3;
   uint32_t* cnt_g = wb.cnt + (size_t)f * wb.SMAX * wb.PMAXP;
   const float r = P.r;
+  const float ybv = __fdiv_rn(__fsub_rn((float)v, F.cy), F.fy);        // R5 per row
+  const float ybu = __fdiv_rn(__fsub_rn((float)(v - 1), F.cy), F.fy);
+  const float ybd = __fdiv_rn(__fsub_rn((float)(v + 1), F.cy), F.fy);
+  const int prow = lane_on ? (int)(((int64_t)v * Hp) / H) * Wp : 0;
 
-  auto key_at = [&](int u, int v, uint64_t& key) -> bool {
-    const float d = F.depth[(int64_t)v * W + u];
+  auto wp_tile = [&](int dr, int c, float p[3]) -> bool {   // staged pixel (row v + dr, column c)
+    const float d = dep[(lane + 1 + dr) * K1_DS + c];
     if (!depth_valid(d, P)) return false;
-    float p[3];
-    world_point(F, xa_s[u], yb_s[v - r0], d, p);
-    return point_key(p, r, key);
-  };
-  // R21 pixel normal (fp32): (P(u+1,v)-P(u-1,v)) x (P(u,v+1)-P(u,v-1)), oriented to the camera.
-  // All five depths are loaded before any test (independent loads in flight).
-  auto pixel_normal = [&](int u, int v, float n[3]) -> bool {
-    if (u < 1 || u + 1 >= W || v < 1 || v + 1 >= H) return false;
-    const float* dp = F.depth + (int64_t)v * W + u;
-    const float dc = dp[0], dl = dp[-1], dr = dp[1], du = dp[-W], dd = dp[W];
-    if (!(depth_valid(dc, P) && depth_valid(dl, P) && depth_valid(dr, P) && depth_valid(du, P) &&
-          depth_valid(dd, P)))
-      return false;
-    float pc[3], pl[3], pr[3], pu[3], pd[3];
-    world_point(F, xa_s[u], yb_s[v - r0], dc, pc);
-    world_point(F, xa_s[u - 1], yb_s[v - r0], dl, pl);
-    world_point(F, xa_s[u + 1], yb_s[v - r0], dr, pr);
-    world_point(F, xa_s[u], yb_s[v - 1 - r0], du, pu);
-    world_point(F, xa_s[u], yb_s[v + 1 - r0], dd, pd);
-    const float a0 = pr[0] - pl[0], a1 = pr[1] - pl[1], a2 = pr[2] - pl[2];
-    const float b0 = pd[0] - pu[0], b1 = pd[1] - pu[1], b2 = pd[2] - pu[2];
-    n[0] = a1 * b2 - a2 * b1;
-    n[1] = a2 * b0 - a0 * b2;
-    n[2] = a0 * b1 - a1 * b0;
-    if (n[0] == 0.f && n[1] == 0.f && n[2] == 0.f) return false;
-    const float o = n[0] * (F.pose[3] - pc[0]) + n[1] * (F.pose[7] - pc[1]) + n[2] * (F.pose[11] - pc[2]);
-    if (o < 0.f) { n[0] = -n[0]; n[1] = -n[1]; n[2] = -n[2]; }
+    world_point(F, xa_s[c], dr < 0 ? ybu : (dr > 0 ? ybd : ybv), d, p);
     return true;
   };
-  auto pix_uv = [&](int64_t i, int& u, int& v) { v = (int)(i / W); u = (int)(i - (int64_t)v * W); };
-
-  uint32_t my_oor = 0;
-  for (int c = 0; c < K1_CPL; ++c) {
-    const int64_t seg0 = tile0 + (int64_t)(c * K1_WARPS + warp) * (32 * K1_PPL);   // warp-uniform
-    if (seg0 >= tile1) break;
-    const int64_t ib = seg0 + (int64_t)lane * K1_PPL;
-    const bool lane_on = ib < tile1;
-    int u_start = 0, v_start = 0;
-    if (lane_on) pix_uv(ib, u_start, v_start);
-    const bool wraps = u_start + K1_PPL > W;            // chunk crosses a row end
-    uint32_t inb = 0, okb = 0, kst = 0, pst = 0;
-    // ---- pixel pass ----
-    if (lane_on) {
-      const int nin = (int)min((int64_t)K1_PPL, tile1 - ib);
-      inb = nin >= 32 ? 0xFFFFFFFFu : ((1u << nin) - 1u);
-      uint64_t prevk = KEY_EMPTY;
-      int prevp = -1;
-      int u = u_start, v = v_start;
-      const bool vec = F.vec16 && nin == 32;
-#pragma unroll 4
-      for (int j4 = 0; j4 < 8; ++j4) {
-        float dv[4];
-        if (vec) {
-          const float4 x = __ldg((const float4*)(F.depth + ib) + j4);
-          dv[0] = x.x; dv[1] = x.y; dv[2] = x.z; dv[3] = x.w;
-        } else {
-          for (int t = 0; t < 4; ++t) dv[t] = (4 * j4 + t < nin) ? F.depth[ib + 4 * j4 + t] : 0.f;
-        }
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int j = 4 * j4 + t;
-          if (j < nin) {
-            const int p = pr_s[v - r0] * Wp + pc_s[u];
-            if (p != prevp) { pst |= 1u << j; prevp = p; }
-            if (depth_valid(dv[t], P)) {
-              float pw[3];
-              world_point(F, xa_s[u], yb_s[v - r0], dv[t], pw);
-              uint64_t key;
-              if (point_key(pw, r, key)) {
-                okb |= 1u << j;
-                if (key != prevk) { kst |= 1u << j; prevk = key; }
-              } else {
-                my_oor++;
-              }
-            }
-          }
-          if (++u == W) { u = 0; ++v; }
-        }
+  auto pixel_normal = [&](int c, float n[3]) -> bool {   // R21 for pixel (v, ut0 - 1 + c)
+    const int u = ut0 - 1 + c;
+    if (u < 1 || u + 1 >= W || v < 1 || v + 1 >= H) return false;
+    float pc[3], pl[3], pr[3], pu[3], pd[3];
+    if (!wp_tile(0, c, pc) || !wp_tile(0, c - 1, pl) || !wp_tile(0, c + 1, pr) || !wp_tile(-1, c, pu) ||
+        !wp_tile(1, c, pd))
+      return false;
+    return normal_from(F, pc, pl, pr, pu, pd, n);
+  };
+  auto kt_insert = [&](uint64_t key) -> uint16_t {   // CTA key table -> local key index
+    uint32_t h = (uint32_t)mix64(key) & (K1_KT - 1);
+    for (int probe = 0; probe < K1_KT; ++probe) {
+      const unsigned long long cur = kt[h];
+      if (cur == key) return (uint16_t)h;
+      if (cur == KEY_EMPTY) {
+        const unsigned long long old = atomicCAS(&kt[h], KEY_EMPTY, (unsigned long long)key);
+        if (old == KEY_EMPTY || old == key) return (uint16_t)h;
+      }
+      h = (h + 1) & (K1_KT - 1);
+    }
+    return K1_NOKEY;
+  };
+  auto global_insert = [&](uint64_t key, uint32_t s) -> uint32_t {
+    const uint32_t kslot = ktab_insert(ktab, tmask, key, err);
+    if (kslot == U32_EMPTY) return U32_EMPTY;
+    bool fresh = false;
+    const uint32_t pslot = ptab_insert(ptab, tmask, (s << 24) | kslot, &fresh, err);
+    if (pslot != U32_EMPTY && fresh) {
+      atomicAdd(&vs_s[s], 1u);
+      const uint32_t li = atomicAdd(&npl_s, 1u);
+      if (li < K1_PLIST) {
+        pl_s[li] = pslot;
+      } else {
+        const uint32_t gi2 = atomicAdd(&wb.npairs[f], 1u);
+        if (gi2 < (uint32_t)wb.PMAX) wb.plist[(size_t)f * wb.PMAX + gi2] = pslot;
+        else raise_err(err, DERR_FRAME_PAIRS);
       }
     }
-    // ---- mask pass: two planes in flight per lane ----
-    for (int s0 = 0; s0 < S; s0 += 2) {
-      uint32_t w[2][8];
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-#pragma unroll
-        for (int t = 0; t < 8; ++t) w[k][t] = 0u;
-        if (lane_on && s0 + k < S) {
-          const uint8_t* mp = F.masks + (size_t)(s0 + k) * HW + ib;
-          if (F.vec16 && inb == 0xFFFFFFFFu) {
-            ld_stream32(mp, w[k]);
-          } else {
-            for (int t = 0; t < 8; ++t) {
-              uint32_t x = 0;
-              for (int b = 0; b < 4; ++b)
-                if (inb & (1u << (4 * t + b))) x |= (uint32_t)(mp[4 * t + b] != 0) << (8 * b);
-              w[k][t] = x;
-            }
-          }
+    return pslot;
+  };
+  // one (s, key-run) item: CTA pair table, first inserter goes global; normals accumulated
+  auto emit = [&](uint32_t s, uint16_t li, int run_first_c, float n0, float n1, float n2) {
+    uint64_t key = KEY_EMPTY;
+    int slot = -1;
+    bool claimed = false;
+    if (li != K1_NOKEY) {
+      key = kt[li];
+      const uint32_t code = (s << 16) | li;
+      uint32_t h = mix32(code) & (K1_PT - 1);
+      for (int probe = 0; probe < K1_PT; ++probe) {
+        const uint32_t cur = pt[h];
+        if (cur == code) { slot = (int)h; break; }
+        if (cur == U32_EMPTY) {
+          const uint32_t old = atomicCAS(&pt[h], U32_EMPTY, code);
+          if (old == U32_EMPTY) { slot = (int)h; claimed = true; break; }
+          if (old == code) { slot = (int)h; break; }
         }
+        h = (h + 1) & (K1_PT - 1);
       }
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const int s = s0 + k;
-        if (s >= S) break;
-        uint32_t set = 0;
-#pragma unroll
-        for (int t = 0; t < 8; ++t) set |= nz_bits4(w[k][t]) << (4 * t);
-        set &= inb;
-        if (!__any_sync(0xffffffffu, set != 0)) continue;
-        const uint32_t pk = set & okb;
-        int nit = 0;
-        if (set) {
-          // per-patch pixel counts: popc over patch segments (O5, regardless of depth)
-          for (uint32_t g = pst; g;) {
-            const int a = __ffs(g) - 1;
-            g &= g - 1;
-            const int b = g ? __ffs(g) - 1 : 32;
-            const int cnum = __popc(set & range_bits(a, b));
-            if (cnum) {
-              int u, v;
-              pix_uv(ib + a, u, v);
-              atomicAdd(&cnt_g[(size_t)s * wb.PMAXP + pr_s[v - r0] * Wp + pc_s[u]], (uint32_t)cnum);
-            }
+    } else {   // CTA key table full: recompute the run key (pinned R5)
+      float pw[3];
+      if (wp_tile(0, run_first_c, pw)) point_key(pw, r, key);
+    }
+    uint32_t pslot = U32_EMPTY;
+    if (slot < 0 || claimed) {
+      pslot = global_insert(key, s);
+      if (claimed) ptp[slot] = pslot;
+    }
+    if (SEM && (n0 != 0.f || n1 != 0.f || n2 != 0.f)) {
+      if (slot >= 0) {
+        atomicAdd(&ptn[3 * slot + 0], n0);
+        atomicAdd(&ptn[3 * slot + 1], n1);
+        atomicAdd(&ptn[3 * slot + 2], n2);
+      } else if (pslot != U32_EMPTY) {
+        atomicAdd(&nsum[3 * pslot + 0], n0);
+        atomicAdd(&nsum[3 * pslot + 1], n1);
+        atomicAdd(&nsum[3 * pslot + 2], n2);
+      }
+    }
+  };
+
+  // ---- 1: keys ----
+  uint32_t okb = 0, kst = 0, pst = 0;
+  uint32_t my_oor = 0;
+  if (lane_on && !(ablate & 4)) {
+    uint64_t prevk = KEY_EMPTY;
+    int prevp = -1, ng = 0;
+#pragma unroll 4
+    for (int j = 0; j < K1_TW; ++j) {
+      if (j >= nin) break;
+      const int c = c0 + j;
+      const int p = prow + pc_s[c];
+      if (p != prevp) { pst |= 1u << j; prevp = p; }
+      float pw[3];
+      if (wp_tile(0, c, pw)) {
+        uint64_t key;
+        if (point_key(pw, r, key)) {
+          okb |= 1u << j;
+          if (key != prevk) {
+            kst |= 1u << j;
+            prevk = key;
+            gl[ng * K1_THREADS] = kt_insert(key);
+            ng++;
           }
-          // bbox
-          const int j0 = __ffs(set) - 1, j1 = 31 - __clz(set);
-          if (!wraps) {
-            atomicMin(&bb_s[4 * s + 0], u_start + j0);
-            atomicMax(&bb_s[4 * s + 2], u_start + j1);
-            atomicMin(&bb_s[4 * s + 1], v_start);
-            atomicMax(&bb_s[4 * s + 3], v_start);
-          } else {
-            for (uint32_t g = set; g;) {
-              const int j = __ffs(g) - 1;
-              g &= g - 1;
-              int u, v;
-              pix_uv(ib + j, u, v);
-              atomicMin(&bb_s[4 * s + 0], u);
-              atomicMax(&bb_s[4 * s + 2], u);
-              atomicMin(&bb_s[4 * s + 1], v);
-              atomicMax(&bb_s[4 * s + 3], v);
-            }
-          }
-          // (s, key-run) items: key runs (kstart groups) intersecting pk
-          for (uint32_t g = kst; g;) {
-            const int a = __ffs(g) - 1;
-            g &= g - 1;
-            const int b = g ? __ffs(g) - 1 : 32;
-            if (pk & range_bits(a, b)) nit++;
-          }
-        }
-        int off = nit;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int t = __shfl_up_sync(0xffffffffu, off, o);
-          if (lane >= o) off += t;
-        }
-        const int total = __shfl_sync(0xffffffffu, off, 31);
-        off -= nit;
-        for (int base = 0; base < total; base += K1_QCAP) {
-          if (nit && off + nit > base && off < base + K1_QCAP) {
-            int idx = off;
-            for (uint32_t g = kst; g;) {
-              const int a = __ffs(g) - 1;
-              g &= g - 1;
-              const int b = g ? __ffs(g) - 1 : 32;
-              const uint32_t bits = pk & range_bits(a, b);
-              if (!bits) continue;
-              if (idx >= base && idx < base + K1_QCAP) {
-                int u, v;
-                pix_uv(ib + (__ffs(bits) - 1), u, v);
-                uint64_t key = KEY_EMPTY;
-                key_at(u, v, key);          // the run's key (recomputed, pinned R5)
-                K1Item it;
-                it.key = key;
-                it.pix = (uint32_t)ib;
-                it.bits = bits;
-                q_s[idx - base] = it;
-                qs_s[idx - base] = (uint16_t)s;
-              }
-              idx++;
-            }
-          }
-          __syncwarp();
-          const int nq = min(total - base, K1_QCAP);
-          if (SEM) {
-            // pixel-parallel normals: prefix of pixel counts over the queued items
-            for (int t0 = 0; t0 < nq; t0 += 32) {
-              const int t = t0 + lane;
-              int pc = t < nq ? __popc(q_s[t].bits) : 0;
-              int ex = pc;
-#pragma unroll
-              for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, ex, o);
-                if (lane >= o) ex += y;
-              }
-              const int carry = t0 ? (int)qp_s[t0] : 0;
-              if (t < nq) qp_s[t + 1] = (uint32_t)(carry + ex);
-              if (t0 == 0 && lane == 0) qp_s[0] = 0;
-              if (t < nq) { qn_s[3 * t] = 0.f; qn_s[3 * t + 1] = 0.f; qn_s[3 * t + 2] = 0.f; }
-              __syncwarp();
-            }
-            const int npx = (int)qp_s[nq];
-            for (int x = lane; x < npx; x += 32) {
-              int lo = 0, hi = nq - 1;      // item with qp[i] <= x < qp[i+1]
-              while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if ((int)qp_s[mid] <= x) lo = mid;
-                else hi = mid - 1;
-              }
-              uint32_t bits = q_s[lo].bits;
-              for (int k2 = x - (int)qp_s[lo]; k2 > 0; --k2) bits &= bits - 1;
-              int u, v;
-              pix_uv((int64_t)q_s[lo].pix + (__ffs(bits) - 1), u, v);
-              float n[3];
-              if (pixel_normal(u, v, n)) {
-                atomicAdd(&qn_s[3 * lo + 0], n[0]);
-                atomicAdd(&qn_s[3 * lo + 1], n[1]);
-                atomicAdd(&qn_s[3 * lo + 2], n[2]);
-              }
-            }
-            __syncwarp();
-          }
-          for (int t = lane; t < nq; t += 32) {
-            const K1Item it = q_s[t];
-            const uint32_t s_it = qs_s[t];
-            const uint32_t kslot = ktab_insert(ktab, tmask, it.key, err);
-            if (kslot == U32_EMPTY) continue;
-            bool fresh = false;
-            const uint32_t pslot = ptab_insert(ptab, tmask, (s_it << 24) | kslot, &fresh, err);
-            if (pslot == U32_EMPTY) continue;
-            if (fresh) {
-              atomicAdd(&vs_s[s_it], 1u);
-              const uint32_t li = atomicAdd(&npl_s, 1u);
-              if (li < K1_PLIST) {
-                pl_s[li] = pslot;
-              } else {
-                const uint32_t gi = atomicAdd(&wb.npairs[f], 1u);
-                if (gi < (uint32_t)wb.PMAX) wb.plist[(size_t)f * wb.PMAX + gi] = pslot;
-                else raise_err(err, DERR_FRAME_PAIRS);
-              }
-            }
-            if (SEM) {
-              const float n0 = qn_s[3 * t], n1 = qn_s[3 * t + 1], n2 = qn_s[3 * t + 2];
-              if (n0 != 0.f || n1 != 0.f || n2 != 0.f) {
-                atomicAdd(&nsum[3 * pslot + 0], n0);
-                atomicAdd(&nsum[3 * pslot + 1], n1);
-                atomicAdd(&nsum[3 * pslot + 2], n2);
-              }
-            }
-          }
-          __syncwarp();
+        } else {
+          my_oor++;
         }
       }
     }
   }
+
+  // ---- 2: masks -> first mask per pixel, overlap flags, per-patch counts, bbox ----
+  uint32_t ovf = 0;
+  for (int g = 0; g < ngroups; ++g) {
+    cp_async_wait<K1_NG - 2>();
+    __syncthreads();
+    const uint8_t* slot_base = msk + (size_t)(g % K1_NG) * 2 * K1_TILE_H * K1_MS;
+    for (int k = 0; k < 2 && lane_on; ++k) {
+      const int s = 2 * g + k;
+      if (s >= S || (ablate & 1)) break;
+      const uint8_t* row = slot_base + (size_t)k * K1_TILE_H * K1_MS + lane * K1_MS + warp * K1_TW;
+      const uint4 a = *(const uint4*)row, b = *(const uint4*)(row + 16);
+      if ((a.x | a.y | a.z | a.w | b.x | b.y | b.z | b.w) == 0) continue;
+      const uint32_t w8[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      uint32_t set = 0;
+      const uint32_t splat = (uint32_t)s * 0x01010101u;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) my_oor += __shfl_xor_sync(0xffffffffu, my_oor, o);
-  if (lane == 0 && my_oor) atomicAdd(&oor_s, my_oor);
+      for (int t = 0; t < 8; ++t) {
+        const uint32_t sb = __vcmpne4(w8[t], 0u);                 // 0xFF where the pixel is in s
+        set |= (((sb & 0x08040201u) * 0x01010101u) >> 24) << (4 * t);
+        if (sb) {
+          const uint32_t m = m0w[t * K1_THREADS];
+          const uint32_t unset = __vcmpeq4(m, 0xFFFFFFFFu);     // 0xFF where no mask yet
+          const uint32_t fresh = sb & unset, again = sb & ~unset;
+          m0w[t * K1_THREADS] = (m & ~fresh) | (splat & fresh);
+          ovf |= (((again & 0x08040201u) * 0x01010101u) >> 24) << (4 * t);
+        }
+      }
+      set &= inb;
+      if (!set) continue;
+      for (uint32_t gg = pst; gg;) {      // per-patch pixel counts (O5, regardless of depth)
+        const int a0 = __ffs(gg) - 1;
+        gg &= gg - 1;
+        const int b0 = gg ? __ffs(gg) - 1 : 32;
+        const int cnum = __popc(set & range_bits(a0, b0));
+        if (cnum) atomicAdd(&cnt_g[(size_t)s * wb.PMAXP + prow + pc_s[c0 + a0]], (uint32_t)cnum);
+      }
+      atomicMin(&bb_s[4 * s + 0], u0 + __ffs(set) - 1);
+      atomicMax(&bb_s[4 * s + 2], u0 + 31 - __clz(set));
+      atomicMin(&bb_s[4 * s + 1], v);
+      atomicMax(&bb_s[4 * s + 3], v);
+    }
+    __syncthreads();                 // everyone is done with ring slot g % K1_NG
+    issue(g + K1_NG - 1);
+  }
+  cp_async_wait<0>();
+
+  // ---- 3: (first mask, key run) items, normals ----
+  if (lane_on && !(ablate & 2)) {
+    int run = -1, cur_run = -1, first_c = 0;
+    uint32_t cur_m = 0xFF;
+    float n0 = 0.f, n1 = 0.f, n2 = 0.f;
+    for (int j = 0; j < nin; ++j) {
+      if (kst & (1u << j)) run++;
+      if (!(okb & (1u << j))) continue;
+      const uint32_t mj = (m0w[(j >> 2) * K1_THREADS] >> (8 * (j & 3))) & 0xFFu;
+      if (mj == 0xFFu) continue;
+      if (cur_m != 0xFFu && (run != cur_run || mj != cur_m)) {
+        emit(cur_m, gl[cur_run * K1_THREADS], first_c, n0, n1, n2);
+        cur_m = 0xFFu;
+      }
+      if (cur_m == 0xFFu) {
+        cur_m = mj;
+        cur_run = run;
+        first_c = c0 + j;
+        n0 = n1 = n2 = 0.f;
+      }
+      if (SEM && !(ablate & 8)) {
+        float n[3];
+        if (pixel_normal(c0 + j, n)) { n0 += n[0]; n1 += n[1]; n2 += n[2]; }
+      }
+    }
+    if (cur_m != 0xFFu) emit(cur_m, gl[cur_run * K1_THREADS], first_c, n0, n1, n2);
+  }
+
+  // ---- 4: pixels in several masks (overlapping masks, R9): their other planes ----
+  if (lane_on && (ovf & okb) && !(ablate & 2)) {
+    int run = -1;
+    for (int j = 0; j < nin; ++j) {
+      if (kst & (1u << j)) run++;
+      if (!((ovf & okb) & (1u << j))) continue;
+      const uint32_t mj = (m0w[(j >> 2) * K1_THREADS] >> (8 * (j & 3))) & 0xFFu;
+      float n[3] = {0.f, 0.f, 0.f};
+      if (SEM && !(ablate & 8) && !pixel_normal(c0 + j, n)) { n[0] = n[1] = n[2] = 0.f; }
+      const size_t pix = (size_t)v * W + u0 + j;
+      for (int s = (int)mj + 1; s < S; ++s)
+        if (F.masks[(size_t)s * HW + pix]) emit((uint32_t)s, gl[run * K1_THREADS], c0 + j, n[0], n[1], n[2]);
+    }
+  }
+  if (lane_on && my_oor) atomicAdd(&oor_s, my_oor);
   __syncthreads();
+  if (SEM)   // flush normal sums: one global add per distinct (s, key) of the tile
+    for (int i = threadIdx.x; i < K1_PT; i += blockDim.x) {
+      const uint32_t ps = ptp[i];
+      if (pt[i] == U32_EMPTY || ps == U32_EMPTY) continue;
+      const float n0 = ptn[3 * i], n1 = ptn[3 * i + 1], n2 = ptn[3 * i + 2];
+      if (n0 != 0.f || n1 != 0.f || n2 != 0.f) {
+        atomicAdd(&nsum[3 * ps + 0], n0);
+        atomicAdd(&nsum[3 * ps + 1], n1);
+        atomicAdd(&nsum[3 * ps + 2], n2);
+      }
+    }
 
   // ---- flush per-mask accumulators ----
   for (int s = threadIdx.x; s < S; s += blockDim.x) {
@@ -948,18 +973,31 @@ __global__ void __launch_bounds__(K4_THREADS) k_detect(WinDesc wd, WinBufs wb, P
 // ------------------------------------------------------------------------------------------
 // launchers
 // ------------------------------------------------------------------------------------------
-size_t k1_smem_bytes(int S, int W, int rows_cap) { return K1Smem(S, W, rows_cap).total; }
+// DISC_K1_ABLATE (profiling only; results are wrong when set): 1 skip mask planes, 2 skip
+// pair items, 4 skip key computation, 8 skip normals
+static int k1_ablate() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DISC_K1_ABLATE");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
 
-int k1_rows_cap(int W) { return K1_TILE / (W > 0 ? W : 1) + 4; }
+size_t k1_smem_bytes(int S, int W, int rows_cap) { (void)rows_cap; (void)W; return K1Smem(S, true).total; }
 
-int k1_tiles(int64_t HW) { return (int)((HW + K1_TILE - 1) / K1_TILE); }
+int k1_rows_cap(int W) { (void)W; return 4; }
+
+int k1_tiles(int H, int W) {
+  return ((W + K1_TILE_W - 1) / K1_TILE_W) * ((H + K1_TILE_H - 1) / K1_TILE_H);
+}
 
 int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* err, bool sem, int maxS,
                   int maxHp, int maxW, int maxWp, int maxP, int rows_cap, cudaStream_t st,
                   cudaEvent_t ev0, cudaEvent_t ev1) {
   const int n = wd.n;
   int k1_grid = 1;
-  for (int i = 0; i < n; ++i) k1_grid = std::max(k1_grid, k1_tiles((int64_t)wd.f[i].H * wd.f[i].W));
+  for (int i = 0; i < n; ++i) k1_grid = std::max(k1_grid, k1_tiles(wd.f[i].H, wd.f[i].W));
   (void)maxHp; (void)maxWp;
   k_win_init<<<dim3(8, n), 256, 0, st>>>(wd, wb);
   debug_check(st, "k_win_init", -1);
@@ -967,10 +1005,10 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
   if (ev0) cudaEventRecord(ev0, st);
   if (sem) {
     cudaFuncSetAttribute(k_mask_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
-    k_mask_pass<true><<<dim3(k1_grid, n), K1_THREADS, sm1, st>>>(wd, wb, P, err, rows_cap);
+    k_mask_pass<true><<<dim3(k1_grid, n), K1_THREADS, sm1, st>>>(wd, wb, P, err, rows_cap, k1_ablate());
   } else {
     cudaFuncSetAttribute(k_mask_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
-    k_mask_pass<false><<<dim3(k1_grid, n), K1_THREADS, sm1, st>>>(wd, wb, P, err, rows_cap);
+    k_mask_pass<false><<<dim3(k1_grid, n), K1_THREADS, sm1, st>>>(wd, wb, P, err, rows_cap, k1_ablate());
   }
   debug_check(st, "k_mask_pass", -1);
   if (ev1) cudaEventRecord(ev1, st);

@@ -16,6 +16,8 @@
 #include "disc_common.cuh"
 #include "disc_launch.h"
 
+#include <cstdio>
+
 namespace disc {
 
 // ------------------------------------------------------------------------------------------
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(256) k_lookup(int f, WinBufs wb, MapState M, F
 // ------------------------------------------------------------------------------------------
 // K6: association (single CTA)
 // ------------------------------------------------------------------------------------------
-constexpr int K6_THREADS = 1024;
+constexpr int K6_THREADS = 512;
 
 __device__ __forceinline__ double dot_pin_w(const double* a, const double* b, int n) {
   const int lane = threadIdx.x & 31;
@@ -207,9 +209,28 @@ __device__ __forceinline__ double dot_pin_w(const double* a, const double* b, in
   return acc;
 }
 
+// dot_pin with every load of the lane issued before the (unchanged) fma chain
+__device__ __forceinline__ double dot_pin_reg(const double* a, const double* b, int n) {
+  const int lane = threadIdx.x & 31;
+  double x[16], y[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int d = lane + 32 * i;
+    x[i] = d < n ? a[d] : 0.0;
+    y[i] = d < n ? b[d] : 0.0;
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    if (lane + 32 * i < n) acc = __fma_rn(x[i], y[i], acc);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+  return acc;
+}
+
 struct K6Smem {   // offsets into dynamic shared memory
   size_t t_s, t_j, t_c, t_e, t_jl, lab, jnode, comp_root, comp_best, comp_tgt, has_edge, d_st, d_vs, d_tgt, d_q,
-      total;
+      tg_root, tg_phys, j_vc, j_ph, j_obs, j_q, total;
   __host__ __device__ K6Smem(int S, int TC) {
     size_t o = 0;
     auto take = [&](size_t bytes) { const size_t r = o; o = (o + bytes + 15) & ~(size_t)15; return r; };
@@ -219,9 +240,23 @@ struct K6Smem {   // offsets into dynamic shared memory
     comp_root = take(4 * NN); comp_best = take(8 * NN); comp_tgt = take(4 * NN); has_edge = take((size_t)S + 1);
     d_st = take(4 * (size_t)S + 4); d_vs = take(4 * (size_t)S + 4); d_tgt = take(4 * (size_t)S + 4);
     d_q = take(4 * (size_t)S + 4);
+    tg_root = take(4 * (size_t)S + 4); tg_phys = take(4 * (size_t)S + 4);
+    j_vc = take(8 * (size_t)TC); j_ph = take(4 * (size_t)TC); j_obs = take(4 * (size_t)TC); j_q = take(4 * (size_t)TC);
     total = o;
   }
 };
+
+// DISC_K6PROF: phase timestamps of the association kernel (profiling aid)
+__device__ unsigned long long g_k6prof[16];
+#define K6_PROBE(i)                                                                          \
+  do {                                                                                       \
+    if (threadIdx.x == 0) {                                                                  \
+      unsigned long long t_;                                                                 \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                  \
+      atomicAdd(&g_k6prof[(i) + 1], t_ - g_k6prof[0]);                                        \
+      g_k6prof[0] = t_;                                                                      \
+    }                                                                                        \
+  } while (0)
 
 __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBufs wb, MapState M,
                                                       FrameScratch X, Params P, int sem) {
@@ -244,13 +279,26 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
   uint32_t* d_vs = (uint32_t*)(smem_raw + L6.d_vs);   // |V_s|
   int32_t* d_tgt = (int32_t*)(smem_raw + L6.d_tgt);   // target index (written back at the end)
   float* d_q = (float*)(smem_raw + L6.d_q);           // Q_s
-  __shared__ uint32_t n_tr, n_j, n_tgt, n_seg;
+  uint32_t* tg_root = (uint32_t*)(smem_raw + L6.tg_root);   // per target: survivor id
+  uint32_t* tg_phys = (uint32_t*)(smem_raw + L6.tg_phys);   // per target: physical label
+  int64_t* j_vc = (int64_t*)(smem_raw + L6.j_vc);           // per local instance: |V_j|
+  uint32_t* j_ph = (uint32_t*)(smem_raw + L6.j_ph);         //   physical label
+  int32_t* j_obs = (int32_t*)(smem_raw + L6.j_obs);         //   obs count
+  float* j_q = (float*)(smem_raw + L6.j_q);                 //   Q
+  __shared__ uint32_t n_tr, n_j, n_tgt, n_seg, ncomp_s;
+  __shared__ uint32_t mcnt_s[256], dcnt_s[256], moff_s[256], doff_s[256];
+  __shared__ int64_t tg_vb[256];
   __shared__ int changed;
   __shared__ unsigned long long rel_s, merged_s, edges_s;
   __shared__ uint32_t gen;
 
   const size_t fo = (size_t)f * wb.SMAX;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+  if (tid == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    g_k6prof[0] = t_;
+  }
   if (tid == 0) {
     n_tr = min(*X.ntrip, (uint32_t)TC);
     if (*X.ntrip > (uint32_t)TC) raise_err(M.err, DERR_TRIPLES);
@@ -275,6 +323,7 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
     X.tgt_stage[i] = 0;
   }
   __syncthreads();
+  K6_PROBE(0);
   const uint32_t ntr = n_tr;
   // ---- triples: load and release the count table ----
   for (uint32_t t = tid; t < ntr; t += blockDim.x) {
@@ -286,6 +335,7 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
     X.ctab_key[h] = KEY_EMPTY;
   }
   __syncthreads();
+  K6_PROBE(1);
   // ---- O10 edges: exact fp64 geometric test (R10) + pinned fp64 visual gate (R15) ----
   const double* trk = wb.trk + fo * P.Dt;
   for (uint32_t t = warp; t < ntr; t += nwarp) {
@@ -295,8 +345,8 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
     bool e = c >= 1 && (double)c >= (double)P.tau_geo * (double)mn;
     if (e && P.Dt > 0) {
       const double* Tj = M.T + (size_t)j * P.Dt;
-      const double TT = dot_pin_w(Tj, Tj, P.Dt);
-      const double dt = dot_pin_w(trk + (size_t)s * P.Dt, Tj, P.Dt);
+      const double TT = M.TT[j];
+      const double dt = dot_pin_reg(trk + (size_t)s * P.Dt, Tj, P.Dt);
       double cosv = -2.0;
       if (wb.tok[fo + s] && TT > 0.0) cosv = __ddiv_rn(dt, __dsqrt_rn(TT));
       e = cosv >= (double)P.tau_vis;
@@ -304,6 +354,7 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
     if (lane == 0) t_e[t] = e ? 1 : 0;
   }
   __syncthreads();
+  K6_PROBE(2);
   // ---- distinct instances among the edges -> local node S + l (generation stamps) ----
   for (uint32_t t = tid; t < ntr; t += blockDim.x) {
     if (!t_e[t]) continue;
@@ -316,8 +367,17 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
     }
   }
   __syncthreads();
+  K6_PROBE(3);
   for (uint32_t t = tid; t < ntr; t += blockDim.x) t_jl[t] = t_e[t] ? M.local[t_j[t]] : -1;
+  for (int l = tid; l < (int)n_j; l += blockDim.x) {   // one parallel round of attribute loads
+    const uint32_t j = jnode[l];
+    j_vc[l] = M.vcount[j];
+    j_ph[l] = M.phys_of[j];
+    j_obs[l] = M.obs[j];
+    j_q[l] = M.q[j];
+  }
   __syncthreads();
+  K6_PROBE(4);
   const int nJ = (int)n_j;
   const int NN = S + nJ;
   // ---- O11 components: min-label propagation with pointer jumping ----
@@ -352,22 +412,26 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
     const int Lb = lab[S + l];
     const uint32_t j = jnode[l];
     atomicMin(&comp_root[Lb], j);
-    const unsigned long long key = ((unsigned long long)(uint64_t)M.vcount[j] << 32) | (0x7FFFFFFFu - j);
+    const unsigned long long key = ((unsigned long long)(uint64_t)j_vc[l] << 32) | (0x7FFFFFFFu - j);
     atomicMax(&comp_best[Lb], key);
   }
   __syncthreads();
+  K6_PROBE(5);
   for (int x = tid; x < NN; x += blockDim.x) {
     if (lab[x] == x && comp_root[x] != U32_EMPTY) {
       const int t = (int)atomicAdd(&n_tgt, 1u);
       comp_tgt[x] = t;
       const uint32_t owner = 0x7FFFFFFFu - (uint32_t)(comp_best[x] & 0xFFFFFFFFull);
-      X.tgt_root[t] = comp_root[x];
-      X.tgt_phys[t] = M.phys_of[owner];
+      tg_root[t] = comp_root[x];
+      tg_phys[t] = M.phys_of[owner];
+      tg_vb[t] = (int64_t)(comp_best[x] >> 32);   // |V| of the physical owner
     }
   }
   __syncthreads();
+  K6_PROBE(6);
   // ---- detections: component members, isolated kept ones -> new ids ascending s (R13) ----
   if (tid == 0) {
+    ncomp_s = n_tgt;
     int64_t nid = M.counters[0];
     int64_t created = 0;
     for (int s = 0; s < S; ++s) {
@@ -375,7 +439,7 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
       if (has_edge[s]) {
         const int t = comp_tgt[lab[s]];
         d_tgt[s] = t;
-        X.det_id[s] = X.tgt_root[t];
+        X.det_id[s] = tg_root[t];
       } else {
         if (nid >= M.IMAX) {
           raise_err(M.err, DERR_INSTANCES);
@@ -384,8 +448,8 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
         const int t = (int)n_tgt++;
         d_tgt[s] = t;
         X.det_id[s] = nid;
-        X.tgt_root[t] = (uint32_t)nid;
-        X.tgt_phys[t] = (uint32_t)nid;
+        tg_root[t] = (uint32_t)nid;
+        tg_phys[t] = (uint32_t)nid;
         nid++;
         created++;
       }
@@ -395,121 +459,66 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
     X.rep[f].created = created;
   }
   __syncthreads();
-  // ---- O12 apply, one warp per component ----
-  for (int x = warp; x < NN; x += nwarp) {
-    if (lab[x] != x || comp_tgt[x] < 0) continue;
-    const int t = comp_tgt[x];
-    const uint32_t root = X.tgt_root[t];
-    const uint32_t Pl = X.tgt_phys[t];
-    const uint32_t owner = M.id_of[Pl];
-    int32_t obs = M.obs[root];
-    int32_t ab[6];
-    for (int k = 0; k < 6; ++k) ab[k] = M.aabb[(size_t)root * 6 + k];
-    float qcur = M.q[root];
-    int src_kind = 0;      // 0 keep, 1 instance src_id, 2 detection src_id
-    uint32_t src_id = root;
-    uint32_t prev = root;
-    unsigned long long rel = 0;
-    int nmerged = 0;
-    double* Tr = M.T + (size_t)root * P.Dt;
-    // other members J ascending: obs, aabb, T (pinned order), (e,Q) strict >
-    while (true) {
-      uint32_t best = U32_EMPTY;
-      for (int l = lane; l < nJ; l += 32)
-        if (lab[S + l] == x && jnode[l] > prev && jnode[l] < best) best = jnode[l];
-#pragma unroll
-      for (int o = 16; o; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
-      if (best == U32_EMPTY) break;
-      prev = best;
-      const uint32_t m = best;
-      obs += M.obs[m];
-      for (int k = 0; k < 3; ++k) {
-        ab[k] = min(ab[k], M.aabb[(size_t)m * 6 + k]);
-        ab[3 + k] = max(ab[3 + k], M.aabb[(size_t)m * 6 + 3 + k]);
-      }
-      if (M.q[m] > qcur) { qcur = M.q[m]; src_kind = 1; src_id = m; }
-      const double* Tm = M.T + (size_t)m * P.Dt;
-      for (int d = lane; d < P.Dt; d += 32) Tr[d] = __dadd_rn(Tr[d], Tm[d]);
-      rel += (unsigned long long)M.vcount[m];
-      nmerged++;
+  K6_PROBE(7);
+  // ---- O12 work lists for K7a (one CTA per target): member ids ascending, detections
+  // ascending; relabel segments for the smaller sets; report sums ----
+  const int ncomp = (int)ncomp_s;
+  const int ntg = (int)n_tgt;
+  for (int t = tid; t <= S; t += blockDim.x) { mcnt_s[t] = 0; dcnt_s[t] = 0; }
+  __syncthreads();
+  for (int l = tid; l < nJ; l += blockDim.x) atomicAdd(&mcnt_s[comp_tgt[lab[S + l]]], 1u);
+  if (tid == 0) {
+    for (int s2 = 0; s2 < S; ++s2)
+      if (d_tgt[s2] >= 0) dcnt_s[d_tgt[s2]]++;
+    uint32_t mo = 0, dof = 0;
+    for (int t = 0; t < ntg; ++t) {
+      moff_s[t] = mo; mo += mcnt_s[t];
+      doff_s[t] = dof; dof += dcnt_s[t];
+      dcnt_s[t] = 0;
     }
-    // detections Sd ascending
-    for (int s = 0; s < S; ++s) {
-      if (d_tgt[s] != t) continue;
-      obs += 1;
-      for (int k = 0; k < 3; ++k) {
-        ab[k] = min(ab[k], wb.daabb[(fo + s) * 6 + k]);
-        ab[3 + k] = max(ab[3 + k], wb.daabb[(fo + s) * 6 + 3 + k]);
-      }
-      const float qs = d_q[s];
-      if (qs > qcur) { qcur = qs; src_kind = 2; src_id = (uint32_t)s; }
-      const double* ts = trk + (size_t)s * P.Dt;
-      for (int d = lane; d < P.Dt; d += 32) Tr[d] = __dadd_rn(Tr[d], ts[d]);
+    for (int s2 = 0; s2 < S; ++s2) {
+      const int t = d_tgt[s2];
+      if (t >= 0) X.tg_dets[doff_s[t] + dcnt_s[t]++] = (uint32_t)s2;
     }
-    if (src_kind != 0) {
-      const float* src = src_kind == 1 ? M.E + (size_t)src_id * P.Df : wb.emb + (fo + src_id) * P.Df;
-      for (int d = lane; d < P.Df; d += 32) M.E[(size_t)root * P.Df + d] = src[d];
-    }
-    __syncwarp();
-    if (lane == 0) {
-      const int64_t vbase = M.vcount[owner];
-      for (int l = 0; l < nJ; ++l) {
-        if (lab[S + l] != x) continue;
-        const uint32_t m = jnode[l];
-        const uint32_t pm = M.phys_of[m];
-        if (pm != Pl) {   // the smaller sets: relabel into the owner's physical label
-          const uint32_t sg = atomicAdd(&n_seg, 1u);
-          if (sg < (uint32_t)TC) {
-            X.seg_phys[sg] = pm;
-            X.seg_tgt[sg] = t;
-            X.seg_base[sg] = M.lst_off[pm];
-            X.seg_off[sg] = M.lst_len[pm];
-          } else {
-            raise_err(M.err, DERR_TRIPLES);
-          }
-          M.lst_len[pm] = 0;
-          M.lst_cap[pm] = 0;
-        }
-        if (m != root) {
-          M.alive[m] = 0;
-          M.phys_of[m] = U32_EMPTY;
-        }
-      }
-      M.obs[root] = obs;
-      M.last_seen[root] = F.frame_id;
-      for (int k = 0; k < 6; ++k) M.aabb[(size_t)root * 6 + k] = ab[k];
-      M.q[root] = qcur;
-      M.vcount[root] = vbase;
-      M.phys_of[root] = Pl;
-      M.id_of[Pl] = root;
-      atomicAdd(&rel_s, rel);
-      atomicAdd(&merged_s, (unsigned long long)nmerged);
-    }
-    __syncwarp();
   }
   __syncthreads();
-  // ---- new instances (isolated kept detections) ----
-  for (int s = tid; s < S; s += blockDim.x) X.det_target[s] = d_tgt[s];
-  for (int s = warp; s < S; s += nwarp) {
-    const int t = d_tgt[s];
-    if (t < 0 || has_edge[s]) continue;
-    const uint32_t id = X.tgt_root[t];
-    if (lane == 0) {
-      M.alive[id] = 1;
-      M.phys_of[id] = id;
-      M.id_of[id] = id;
-      M.vcount[id] = 0;
-      M.obs[id] = 1;
-      M.last_seen[id] = F.frame_id;
-      for (int k = 0; k < 6; ++k) M.aabb[(size_t)id * 6 + k] = wb.daabb[(fo + s) * 6 + k];
-      M.q[id] = d_q[s];
-      M.lst_len[id] = 0;
-      M.lst_cap[id] = 0;
+  for (int l = tid; l < nJ; l += blockDim.x) {
+    const int t = comp_tgt[lab[S + l]];
+    const uint32_t j = jnode[l];
+    uint32_t rank = 0;
+    for (int l2 = 0; l2 < nJ; ++l2)
+      if (l2 != l && comp_tgt[lab[S + l2]] == t && jnode[l2] < j) rank++;
+    X.tg_mem[moff_s[t] + rank] = j;
+    const uint32_t pm = j_ph[l];
+    if (pm != tg_phys[t]) {   // the smaller sets: relabel into the survivor's physical label
+      const uint32_t sg = atomicAdd(&n_seg, 1u);
+      if (sg < (uint32_t)TC) {
+        X.seg_phys[sg] = pm;
+        X.seg_tgt[sg] = t;
+        X.seg_base[sg] = M.lst_off[pm];
+        X.seg_off[sg] = M.lst_len[pm];
+      } else {
+        raise_err(M.err, DERR_TRIPLES);
+      }
     }
-    for (int d = lane; d < P.Dt; d += 32) M.T[(size_t)id * P.Dt + d] = trk[(size_t)s * P.Dt + d];
-    const bool has_e = sem && d_q[s] >= 0.f;
-    for (int d = lane; d < P.Df; d += 32) M.E[(size_t)id * P.Df + d] = has_e ? wb.emb[(fo + s) * P.Df + d] : 0.f;
+    if (j != tg_root[t]) {
+      atomicAdd(&rel_s, (unsigned long long)j_vc[l]);
+      atomicAdd(&merged_s, 1ull);
+    }
   }
+  for (int t = tid; t < ntg; t += blockDim.x) {
+    X.tgt_root[t] = tg_root[t];
+    X.tgt_phys[t] = tg_phys[t];
+    X.tg_kind[t] = t < ncomp ? 0 : 1;
+    X.tg_vbase[t] = t < ncomp ? tg_vb[t] : 0;
+    X.tg_moff[t] = moff_s[t];
+    X.tg_mcnt[t] = mcnt_s[t];
+    X.tg_doff[t] = doff_s[t];
+    X.tg_dcnt[t] = dcnt_s[t];
+  }
+  for (int s2 = tid; s2 < S; s2 += blockDim.x) X.det_target[s2] = d_tgt[s2];
+  __syncthreads();
+  K6_PROBE(8);
   // ---- debug copies of the triples, edge count ----
   for (uint32_t t = tid; t < ntr; t += blockDim.x) {
     X.trip_c[t] = t_c[t];
@@ -517,6 +526,7 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
     if (t_e[t]) atomicAdd(&edges_s, 1ull);
   }
   __syncthreads();
+  K6_PROBE(9);
   if (tid == 0) {
     const uint32_t ns = min(n_seg, (uint32_t)TC);
     uint32_t acc = 0;
@@ -561,9 +571,139 @@ __global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBuf
 }
 
 // ------------------------------------------------------------------------------------------
-// K7a: apply — detection inserts + relabel of the smaller sets (small-to-large)
+// K7a: apply.  Blocks [0, ntgt) first execute one O12 target each (instance-table update of a
+// merged component / creation of a new instance); then every block joins the grid-stride loop
+// of detection inserts and small-to-large relabels.
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_apply(int f, WinBufs wb, MapState M, FrameScratch X) {
+constexpr int K7_T = 256;
+
+__device__ void apply_target(int t, int f, const FrameDesc& F, const WinBufs& wb, const MapState& M,
+                             const FrameScratch& X, const Params& P, int sem) {
+  __shared__ float q_s[K7_T];
+  __shared__ int32_t ab_s[6];
+  __shared__ int32_t obs_s;
+  __shared__ int src_s;            // -1 keep, i < mcnt member i, mcnt + k detection k
+  const int tid = threadIdx.x, lane = tid & 31;
+  const size_t fo = (size_t)f * wb.SMAX;
+  const double* trk = wb.trk + fo * P.Dt;
+  const int kind = X.tg_kind[t];
+  const uint32_t root = X.tgt_root[t], L = X.tgt_phys[t];
+  const uint32_t moff = X.tg_moff[t], mcnt = X.tg_mcnt[t], doff = X.tg_doff[t], dcnt = X.tg_dcnt[t];
+  const uint32_t* mem = X.tg_mem + moff;
+  const uint32_t* dets = X.tg_dets + doff;
+  if (kind == 1) {   // new instance from its single detection (O12 last paragraph)
+    const uint32_t s = dets[0], id = root;
+    const float qs = wb.qf[(fo + s) * 6 + 4];
+    if (tid == 0) {
+      M.alive[id] = 1;
+      M.phys_of[id] = id;
+      M.id_of[id] = id;
+      M.vcount[id] = 0;
+      M.obs[id] = 1;
+      M.last_seen[id] = F.frame_id;
+      for (int k = 0; k < 6; ++k) M.aabb[(size_t)id * 6 + k] = wb.daabb[(fo + s) * 6 + k];
+      M.q[id] = qs;
+      M.lst_len[id] = 0;
+      M.lst_cap[id] = 0;
+    }
+    for (int d = tid; d < P.Dt; d += blockDim.x) M.T[(size_t)id * P.Dt + d] = trk[(size_t)s * P.Dt + d];
+    const bool has_e = sem && qs >= 0.f;
+    for (int d = tid; d < P.Df; d += blockDim.x) M.E[(size_t)id * P.Df + d] = has_e ? wb.emb[(fo + s) * P.Df + d] : 0.f;
+    if (P.Dt > 0 && tid < 32) {
+      const double tt = dot_pin_reg(trk + (size_t)s * P.Dt, trk + (size_t)s * P.Dt, P.Dt);
+      if (lane == 0) M.TT[id] = tt;
+    }
+    return;
+  }
+  // merged component: root = mem[0] (min id), J = mem[1..], Sd = dets (ascending)
+  if (tid == 0) {
+    obs_s = 0;
+    for (int k = 0; k < 3; ++k) { ab_s[k] = INT32_MAX; ab_s[3 + k] = INT32_MIN; }
+  }
+  __syncthreads();
+  int myobs = 0;
+  for (uint32_t i = tid; i < mcnt + dcnt; i += blockDim.x) {
+    const int32_t* ab;
+    if (i < mcnt) {
+      const uint32_t m = mem[i];
+      myobs += M.obs[m];
+      ab = M.aabb + (size_t)m * 6;
+      if (i < K7_T) q_s[i] = M.q[m];
+    } else {
+      const uint32_t s = dets[i - mcnt];
+      myobs += 1;
+      ab = wb.daabb + (fo + s) * 6;
+      if (i < K7_T) q_s[i] = wb.qf[(fo + s) * 6 + 4];
+    }
+    for (int k = 0; k < 3; ++k) {
+      atomicMin(&ab_s[k], ab[k]);
+      atomicMax(&ab_s[3 + k], ab[3 + k]);
+    }
+  }
+  if (myobs) atomicAdd(&obs_s, myobs);
+  // T_root <- ((T_root + T_j1) + T_j2 ...) + t_s1 ...   elementwise fp64, exactly this order
+  double* Tr = M.T + (size_t)root * P.Dt;
+  for (int d = tid; d < P.Dt; d += blockDim.x) {
+    double acc = Tr[d];
+    for (uint32_t i = 1; i < mcnt; ++i) acc = __dadd_rn(acc, M.T[(size_t)mem[i] * P.Dt + d]);
+    for (uint32_t k = 0; k < dcnt; ++k) acc = __dadd_rn(acc, trk[(size_t)dets[k] * P.Dt + d]);
+    Tr[d] = acc;
+  }
+  __syncthreads();
+  // (e, Q): root's, then J ascending, then Sd ascending, replace iff Q_cand > Q (strict)
+  if (tid == 0) {
+    float qcur = q_s[0];
+    int src = -1;
+    for (uint32_t i = 1; i < mcnt + dcnt; ++i) {
+      const float qi = i < K7_T ? q_s[i] : (i < mcnt ? M.q[mem[i]] : wb.qf[(fo + dets[i - mcnt]) * 6 + 4]);
+      if (qi > qcur) { qcur = qi; src = (int)i; }
+    }
+    src_s = src;
+    q_s[0] = qcur;
+  }
+  if (P.Dt > 0 && tid < 32) {
+    const double tt = dot_pin_reg(Tr, Tr, P.Dt);
+    if (lane == 0) M.TT[root] = tt;
+  }
+  __syncthreads();
+  const int src = src_s;
+  if (src >= 0) {
+    const float* e = (uint32_t)src < mcnt ? M.E + (size_t)mem[src] * P.Df : wb.emb + (fo + dets[src - mcnt]) * P.Df;
+    for (int d = tid; d < P.Df; d += blockDim.x) M.E[(size_t)root * P.Df + d] = e[d];
+  }
+  // members: key lists of physical labels other than the survivor's were captured by K6 as
+  // relabel segments; reset them, kill J
+  for (uint32_t i = tid; i < mcnt; i += blockDim.x) {
+    const uint32_t m = mem[i];
+    const uint32_t pm = M.phys_of[m];
+    if (pm != L) {
+      M.lst_len[pm] = 0;
+      M.lst_cap[pm] = 0;
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = 1 + tid; i < mcnt; i += blockDim.x) {
+    const uint32_t m = mem[i];
+    M.alive[m] = 0;
+    M.phys_of[m] = U32_EMPTY;
+  }
+  if (tid == 0) {
+    M.obs[root] = obs_s;
+    M.last_seen[root] = F.frame_id;
+    for (int k = 0; k < 6; ++k) M.aabb[(size_t)root * 6 + k] = ab_s[k];
+    M.q[root] = q_s[0];
+    M.vcount[root] = X.tg_vbase[t];
+    M.phys_of[root] = L;
+    M.id_of[L] = root;
+  }
+}
+
+__global__ void __launch_bounds__(K7_T) k_apply(int f, FrameDesc F, WinBufs wb, MapState M, FrameScratch X, Params P,
+                                               int sem) {
+  if ((int)blockIdx.x < *X.ntgt) {
+    apply_target(blockIdx.x, f, F, wb, M, X, P, sem);
+    __syncthreads();
+  }
   const uint32_t np = min(wb.npairs[f], (uint32_t)wb.PMAX);
   const uint32_t nrel = *X.nrel;
   const uint32_t total = np + nrel;
@@ -696,6 +836,14 @@ __global__ void __launch_bounds__(256) k_fill(MapState M, FrameScratch X) {
 
 size_t k6_smem_bytes(int S, int TC) { return K6Smem(S, TC).total; }
 
+void k6_prof_dump() {
+  unsigned long long h[16];
+  cudaMemcpyFromSymbol(h, g_k6prof, sizeof(h));
+  fprintf(stderr, "k6 phase ns (cumulative):");
+  for (int i = 1; i < 12; ++i) fprintf(stderr, " %d:%llu", i - 1, h[i]);
+  fprintf(stderr, "\n");
+}
+
 int launch_stage2_frame(int f, const FrameDesc& F, const WinBufs& wb, const MapState& M, const FrameScratch& X,
                         const Params& P, bool sem, int nsm, cudaStream_t st) {
   k_lookup<<<2 * nsm, 256, 0, st>>>(f, wb, M, X);
@@ -704,7 +852,7 @@ int launch_stage2_frame(int f, const FrameDesc& F, const WinBufs& wb, const MapS
   cudaFuncSetAttribute(k_assoc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm6);
   k_assoc<<<1, K6_THREADS, sm6, st>>>(f, F, wb, M, X, P, sem ? 1 : 0);
   debug_check(st, "k_assoc", f);
-  k_apply<<<2 * nsm, 256, 0, st>>>(f, wb, M, X);
+  k_apply<<<2 * nsm, K7_T, 0, st>>>(f, F, wb, M, X, P, sem ? 1 : 0);
   debug_check(st, "k_apply", f);
   k_grow<<<wb.SMAX, 256, 0, st>>>(f, M, X);
   debug_check(st, "k_grow", f);

@@ -1,0 +1,22 @@
+"""Aggregate an ncu --metrics gpu__time_duration.sum --csv launch list per kernel."""
+import collections
+import csv
+import sys
+
+rows = list(csv.reader(open(sys.argv[1])))
+hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+h = rows[hi]
+data = [dict(zip(h, r)) for r in rows[hi + 1:] if len(r) == len(h)]
+scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+agg = collections.OrderedDict()
+for d in data:
+    if d.get("Metric Name") != "gpu__time_duration.sum":
+        continue
+    v = float(d["Metric Value"].replace(",", "")) * scale.get(d["Metric Unit"], 1.0)
+    a = agg.setdefault(d["Kernel Name"], [0, 0.0])
+    a[0] += 1
+    a[1] += v
+tot = sum(a[1] for a in agg.values())
+print(f"total {tot:.1f} us over {sum(a[0] for a in agg.values())} launches")
+for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+    print(f"{t:10.1f} us {n:5d} launches {100 * t / tot:5.1f}%  avg {t / n:9.2f} us  {k[:70]}")
