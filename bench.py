@@ -271,6 +271,7 @@ def main():
             e0.record(stream)
             for s in range(warm_steps, warm_steps + timed_steps):
                 m.integrate_frames(frames_[s * F:(s + 1) * F])
+            m.wait(stream)   # include the last window's stage 2
             e1.record(stream)
             torch.cuda.synchronize()
         barrier(ws)

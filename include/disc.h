@@ -152,7 +152,10 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out);
 void disc_map_destroy(disc_map* m);
 
 /* One frame, device-resident inputs (O0-O13).  report (host) may be NULL; a non-NULL
- * report synchronises the stream. */
+ * report synchronises.  On return `stream` is ordered after the last read of the caller's
+ * inputs; the map update itself may still be running on the library's internal stage-2 stream
+ * (so the next call's per-frame stage 1 overlaps it).  disc_wait orders a stream after all of
+ * the map's work; every reader (query / get / debug / sync) waits for it. */
 disc_status disc_integrate_frame(disc_map* m, const disc_frame* f, void* stream,
                                  disc_frame_report* report);
 /* == n sequential disc_integrate_frame calls; batches stage 1 (per-frame independent work)
@@ -178,6 +181,7 @@ disc_status disc_get_memberships(disc_map* m, uint64_t* keys, int64_t* ids, int6
 disc_status disc_debug_last_frame(disc_map* m, disc_frame_debug* d);
 disc_status disc_set_timing(disc_map* m, int32_t on);
 disc_status disc_get_stats(disc_map* m, disc_stats* s);
+disc_status disc_wait(disc_map* m, void* stream);  /* order `stream` after all queued map work */
 disc_status disc_sync(disc_map* m);    /* wait for the map's work; surfaces device errors */
 const char* disc_last_error(const disc_map* m);
 const char* disc_version(void);

@@ -26,7 +26,13 @@ struct disc_map {
   Params P;
   int dev = 0, nsm = 148;
   MapState M{};
-  WinBufs W{};
+  WinBufs Wb[2]{};               // double-buffered window buffers (stage 1 of window w+1 overlaps
+                                 // stage 2 of window w)
+  int wbuf = 0, last_buf = 0;
+  bool s2_pending[2] = {false, false};
+  cudaStream_t s1 = nullptr, s2 = nullptr;   // internal streams: stage 1, stage 2
+  cudaEvent_t ev_in = nullptr, ev_done = nullptr, ev_s1done = nullptr, ev_s1[2] = {nullptr, nullptr},
+              ev_s2[2] = {nullptr, nullptr};
   FrameScratch X{};
   int* d_err = nullptr;
   int* h_err = nullptr;                 // pinned
@@ -305,7 +311,8 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   bool ok = true;
   auto chk = [&](void* p) { ok = ok && p; };
   // ---- window buffers ----
-  WinBufs& W = m->W;
+  for (int wbi = 0; wbi < 2; ++wbi) {
+  WinBufs& W = m->Wb[wbi];
   W.PC = (int32_t)PC; W.PMAX = (int32_t)PMAX; W.SMAX = SM; W.PMAXP = (int32_t)PMP;
   W.FCHUNKS = (int32_t)((PMP + 63) / 64);
   chk(W.ktab = dalloc<unsigned long long>(m, (size_t)win * PC, 0xFF));
@@ -333,6 +340,7 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(W.emb = dalloc<float>(m, (size_t)win * SM * Df));
   chk(W.trk = dalloc<double>(m, (size_t)win * SM * std::max(Dt, 1)));
   chk(W.tok = dalloc<uint8_t>(m, (size_t)win * SM));
+  }
   // ---- map ----
   MapState& M = m->M;
   const int64_t IM = cfg->max_instances;
@@ -405,6 +413,14 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(X.rep = dalloc<disc_frame_report>(m, MAXWIN));
   chk(X.live_before = dalloc<int64_t>(m, 1));
   chk(X.ntrip_last = dalloc<uint32_t>(m, 1));
+  {
+    int prio_lo = 0, prio_hi = 0;   // stage 2 (latency-bound, few SMs) gets the higher priority
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    if (cudaStreamCreateWithPriority(&m->s1, cudaStreamNonBlocking, prio_lo) != cudaSuccess) ok = false;
+    if (cudaStreamCreateWithPriority(&m->s2, cudaStreamNonBlocking, prio_hi) != cudaSuccess) ok = false;
+  }
+  for (cudaEvent_t* e : {&m->ev_in, &m->ev_done, &m->ev_s1done, &m->ev_s1[0], &m->ev_s1[1], &m->ev_s2[0], &m->ev_s2[1]})
+    if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) ok = false;
   if (cudaMallocHost(&m->h_err, sizeof(int)) != cudaSuccess) ok = false;
   if (cudaMallocHost(&m->h_rep, sizeof(disc_frame_report) * MAXWIN) != cudaSuccess) ok = false;
   if (ok && k6_smem_bytes(SM, X.TCAP) > 227 * 1024) ok = false;
@@ -430,6 +446,10 @@ void disc_map_destroy(disc_map* m) {
   if (m->scratch) cudaFree(m->scratch);
   for (auto& p : m->ev_pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   for (auto e : m->ev_pool) cudaEventDestroy(e);
+  for (cudaEvent_t e : {m->ev_in, m->ev_done, m->ev_s1done, m->ev_s1[0], m->ev_s1[1], m->ev_s2[0], m->ev_s2[1]})
+    if (e) cudaEventDestroy(e);
+  if (m->s1) cudaStreamDestroy(m->s1);
+  if (m->s2) cudaStreamDestroy(m->s2);
   delete m;
 }
 
@@ -457,8 +477,17 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
       return fail(m, DISC_ERR_CAPACITY, "cannot allocate host-input staging buffers");
     }
   }
+  // stream-ordered after the caller's prior work on `st`; stage 1 on s1, stage 2 on s2
+  cudaEventRecord(m->ev_in, st);
+  cudaStreamWaitEvent(m->s1, m->ev_in, 0);
+  cudaStreamWaitEvent(m->s2, m->ev_in, 0);
+  cudaStream_t s1 = m->s1, s2 = m->s2;
   for (int w0 = 0; w0 < n; w0 += win) {
     const int nw = std::min(win, n - w0);
+    const int b = m->wbuf;
+    m->wbuf ^= 1;
+    WinBufs& Wbuf = m->Wb[b];
+    if (m->s2_pending[b]) cudaStreamWaitEvent(s1, m->ev_s2[b], 0);   // stage 2 done with this buffer
     WinDesc wd{};
     wd.n = nw;
     int maxS = 1, maxHp = 1, maxW = 1, maxWp = 1, maxP = 1, rows = 4;
@@ -471,7 +500,7 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
           if (!src || !bytes) return nullptr;
           so = (so + 255) & ~(size_t)255;
           void* dst = m->stage + so;
-          cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+          cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s1);
           so += bytes;
           return dst;
         };
@@ -496,43 +525,51 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
       m->stats.track_bytes += (int64_t)f.patch_h * f.patch_w * Dt * 2;
       if (f.patch_feats) m->stats.feat_bytes += (int64_t)f.patch_h * f.patch_w * Df * 4;
     }
-    cudaEvent_t e0 = nullptr, e1 = nullptr, s0 = nullptr, s1 = nullptr, s1b = nullptr, s2 = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr, t0 = nullptr, t1 = nullptr, t1b = nullptr, t2 = nullptr;
     if (m->timing) {
-      e0 = ev_get(m); e1 = ev_get(m); s0 = ev_get(m); s1 = ev_get(m); s1b = ev_get(m); s2 = ev_get(m);
-      cudaEventRecord(s0, st);
+      e0 = ev_get(m); e1 = ev_get(m); t0 = ev_get(m); t1 = ev_get(m); t1b = ev_get(m); t2 = ev_get(m);
+      cudaEventRecord(t0, s1);
     }
-    m->stats.launches += launch_stage1(wd, m->W, m->P, m->d_err, sem, maxS, maxHp, maxW, maxWp, maxP, rows, st, e0, e1);
-    if (m->timing) {
-      cudaEventRecord(s1, st);
-      cudaEventRecord(s1b, st);
-    }
+    m->stats.launches += launch_stage1(wd, Wbuf, m->P, m->d_err, sem, maxS, maxHp, maxW, maxWp, maxP, rows, s1, e0, e1);
+    if (m->timing) cudaEventRecord(t1, s1);
+    cudaEventRecord(m->ev_s1[b], s1);
+    cudaStreamWaitEvent(s2, m->ev_s1[b], 0);
+    if (m->timing) cudaEventRecord(t1b, s2);
     for (int i = 0; i < nw; ++i)
-      m->stats.launches += launch_stage2_frame(i, wd.f[i], m->W, m->M, m->X, m->P, sem, m->nsm, st);
+      m->stats.launches += launch_stage2_frame(i, wd.f[i], Wbuf, m->M, m->X, m->P, sem, m->nsm, s2);
     if (m->timing) {
-      cudaEventRecord(s2, st);
+      cudaEventRecord(t2, s2);
       m->ev_pending.push_back({e0, e1, 0});
-      m->ev_pending.push_back({s0, s1, 1});
-      m->ev_pending.push_back({s1b, s2, 2});
+      m->ev_pending.push_back({t0, t1, 1});
+      m->ev_pending.push_back({t1b, t2, 2});
     }
+    cudaEventRecord(m->ev_s2[b], s2);
+    m->s2_pending[b] = true;
     m->stats.frames += nw;
     disc_status cs = cuda_check(m, "integrate launch");
     if (cs != DISC_OK) return cs;
     if (reports) {
-      cudaMemcpyAsync(m->h_rep, m->X.rep, sizeof(disc_frame_report) * nw, cudaMemcpyDeviceToHost, st);
-      disc_status ss = sync_check(m, st);
+      cudaMemcpyAsync(m->h_rep, m->X.rep, sizeof(disc_frame_report) * nw, cudaMemcpyDeviceToHost, s2);
+      disc_status ss = sync_check(m, s2);
       if (ss != DISC_OK) return ss;
       std::memcpy(reports + w0, m->h_rep, sizeof(disc_frame_report) * nw);
     }
     m->have_last = true;
+    m->last_buf = b;
     m->last_f = nw - 1;
     m->last_fd = wd.f[nw - 1];
     m->last_sem = sem;
   }
+  // the caller's stream is ordered after stage 1 (the last reader of the caller's inputs);
+  // stage 2 may still run on s2: disc_wait / disc_sync / every reader order after it
+  cudaEventRecord(m->ev_done, s2);
+  cudaEventRecord(m->ev_s1done, s1);
+  cudaStreamWaitEvent(st, m->ev_s1done, 0);
   if (host_inputs) {   // staging is reused by the next call: keep ordering simple
     disc_status ss = sync_check(m, st);
     if (ss != DISC_OK) return ss;
   }
-  return DISC_OK;
+  return cuda_check(m, "integrate launch");
 }
 
 disc_status disc_integrate_frame(disc_map* m, const disc_frame* f, void* stream, disc_frame_report* report) {
@@ -576,10 +613,20 @@ static int64_t host_next_id(disc_map* m) {
   return nid;
 }
 
+disc_status disc_wait(disc_map* m, void* stream) {
+  if (!m) return DISC_ERR_INVALID;
+  if (m->sticky != DISC_OK) return m->sticky;
+  cudaSetDevice(m->dev);
+  cudaStreamWaitEvent((cudaStream_t)stream, m->ev_done, 0);
+  return cuda_check(m, "disc_wait");
+}
+
 disc_status disc_sync(disc_map* m) {
   if (!m) return DISC_ERR_INVALID;
   if (m->sticky != DISC_OK) return m->sticky;
   cudaSetDevice(m->dev);
+  if (m->s1) cudaStreamSynchronize(m->s1);
+  if (m->s2) cudaStreamSynchronize(m->s2);
   return sync_check(m, m->last_stream);
 }
 
@@ -633,7 +680,7 @@ disc_status disc_debug_last_frame(disc_map* m, disc_frame_debug* d) {
   if (s != DISC_OK) return s;
   if (!m->have_last) return fail(m, DISC_ERR_INVALID, "no frame integrated yet");
   const int S = m->last_fd.S, f = m->last_f, SM = m->cfg.max_masks, Df = m->cfg.feat_dim, Dt = m->cfg.track_dim;
-  const WinBufs& W = m->W;
+  const WinBufs& W = m->Wb[m->last_buf];
   d->num_masks = S;
   const size_t fo = (size_t)f * SM;
   std::vector<int32_t> status(S);
@@ -704,6 +751,7 @@ disc_status disc_get_stats(disc_map* m, disc_stats* s) {
   if (st != DISC_OK) return st;
   collect_events(m);
   if (getenv("DISC_K6PROF")) k6_prof_dump();
+  if (getenv("DISC_K1_ABLATE") && (atoi(getenv("DISC_K1_ABLATE")) & 16)) k1_prof_dump();
   int64_t ctr[8];
   cudaMemcpy(ctr, m->M.counters, sizeof(ctr), cudaMemcpyDeviceToHost);
   m->stats.pairs = ctr[4];

@@ -13,6 +13,7 @@
 #include "disc_launch.h"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 namespace disc {
@@ -42,6 +43,31 @@ __device__ __forceinline__ bool point_key(const float p[3], float r, uint64_t& k
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     const float q = floorf(__fdiv_rn(p[i], r));
+    if (!(q >= -1048576.0f && q < 1048576.0f)) return false;
+    k[i] = (int)q;
+  }
+  key = pack_key(k[0], k[1], k[2]);
+  return true;
+}
+
+// Same result as point_key (floor of the correctly rounded quotient, R5) at a fraction of the
+// cost: q = x * fl(1/r) differs from fl(x/r) by at most ~1.8e-7 |q| (two roundings), so whenever
+// no integer lies within |q| * 1e-6 of q, floor(q) == floor(fl(x/r)); otherwise fall back to the
+// IEEE division.
+__device__ __forceinline__ float floor_div_pinned(float x, float r, float rinv) {
+  const float q = x * rinv;
+  const float fq = floorf(q);
+  const float d = q - fq;
+  const float tol = fabsf(q) * 1e-6f + 1e-30f;
+  if (d > tol && d < 1.0f - tol) return fq;
+  return floorf(__fdiv_rn(x, r));
+}
+
+__device__ __forceinline__ bool point_key_fast(const float p[3], float r, float rinv, uint64_t& key) {
+  int k[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const float q = floor_div_pinned(p[i], r, rinv);
     if (!(q >= -1048576.0f && q < 1048576.0f)) return false;
     k[i] = (int)q;
   }
@@ -127,33 +153,34 @@ __global__ void k_win_init(WinDesc wd, WinBufs wb) {
 
 // ------------------------------------------------------------------------------------------
 // K1: mask pass.  2-D tiles: a CTA owns 32 rows x 128 columns of one frame, a warp 32 rows x 32
-// columns (lane = row, 32 consecutive pixels per lane).  Depth (+1-pixel halo) is staged in
-// shared memory; mask planes stream into a shared-memory ring with cp.async.  Uniform phases:
-//  1 keys: pinned keys (R5) of the lane's pixels -> ok / kstart (voxel-key runs) / pstart
-//    (patches); each run's key enters the CTA key table (local key index per run).
-//  2 masks: per plane, branch-free byte SIMD records each pixel's first mask (m0) and flags
-//    pixels covered by a second mask; per-patch counts by popc over patch segments; bbox.
-//  3 pairs: one walk over the lane's pixels forms (m0, key-run) items, sums their pixel normals
-//    (R21, semantic mode) and inserts the 32-bit code (m0, local key) into the CTA pair table;
-//    the first inserter of a code inserts (s, key) into the frame's global tables.
-//  4 overlap: pixels in more than one mask (R9) re-read their other planes (slow path).
-//  Normal sums are accumulated per pair-table slot and flushed once per CTA.
+// columns (lane = row, 32 consecutive pixels per lane).  The tile's depth (+1-pixel halo) is
+// staged in shared memory; uniform phases:
+//  1 patch segments of the lane's chunk (R17).
+//  2 masks: every plane streamed once (32 bytes per lane, evict-first in L2, the next plane pair
+//    in flight); branch-free byte SIMD records each pixel's first mask (m0) and flags pixels in a
+//    second mask; per-patch counts by popc over patch segments; bbox from ffs/clz.
+//  3 one sliding window over the lane's pixels: pinned keys (R5), key runs, (m0, run) items,
+//    pixel normals (R21, semantic mode); each item goes into the CTA pair table (32-bit code
+//    (s, local key index from the CTA key table)).
+//  4 pixels in more than one mask (R9) re-read their other planes (slow path).
+//  5 the tile's distinct (s, key) pairs go to the frame's global key / pair tables (all threads),
+//    with their summed normals.
 // ------------------------------------------------------------------------------------------
 constexpr int K1_THREADS = 128;
 constexpr int K1_WARPS = K1_THREADS / 32;
 constexpr int K1_TW = 32;                                 // tile columns per warp (pixels per lane)
 constexpr int K1_TILE_W = K1_WARPS * K1_TW;               // CTA tile: 32 rows x 128 columns
 constexpr int K1_TILE_H = 32;
-constexpr int K1_KT = 1024;                               // CTA key table slots
-constexpr int K1_PT = 1024;                               // CTA pair table slots
-constexpr int K1_PLIST = 1024;
+constexpr int K1_KT = 512;                                // CTA key table slots
+constexpr int K1_PT = 512;                                // CTA pair table slots
+constexpr int K1_PLIST = 512;
 constexpr int K1_DS = 131;                                // depth tile row stride (130 columns + pad)
 constexpr int K1_MS = 144;                                // mask tile row stride in bytes
 constexpr int K1_NG = 3;                                  // ring slots (plane pairs)
 constexpr uint16_t K1_NOKEY = 0xFFFF;
 
 struct K1Smem {
-  size_t bb, vs, pl, kt, gl, m0, pt, pp, pn, xa, pc, dep, msk, total;
+  size_t bb, vs, pl, kt, m0, pt, pn, xa, pc, dep, total;
   __host__ __device__ K1Smem(int S, bool sem) {
     size_t o = 0;
     auto take = [&](size_t b) { const size_t r = o; o = (o + b + 15) & ~(size_t)15; return r; };
@@ -161,18 +188,21 @@ struct K1Smem {
     vs = take((size_t)S * 4);
     pl = take((size_t)K1_PLIST * 4);
     kt = take((size_t)K1_KT * 8);
-    gl = take((size_t)32 * K1_THREADS * 2);              // local key index per run
     m0 = take((size_t)8 * K1_THREADS * 4);               // first mask per pixel, 4 per word
     pt = take((size_t)K1_PT * 4);
-    pp = take((size_t)K1_PT * 4);
     pn = take(sem ? (size_t)K1_PT * 12 : 16);
     xa = take((size_t)(K1_TILE_W + 2) * 4);
     pc = take((size_t)(K1_TILE_W + 2) * 2);
     dep = take((size_t)(K1_TILE_H + 2) * K1_DS * 4);
-    msk = take((size_t)K1_NG * 2 * K1_TILE_H * K1_MS);
     total = o;
   }
 };
+
+__device__ __forceinline__ void ld_stream32(const uint8_t* p, uint32_t r[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+}
 
 __device__ __forceinline__ uint32_t nz_bits4(uint32_t w) {   // bit b set iff byte b of w != 0
   return ((__vcmpne4(w, 0u) & 0x08040201u) * 0x01010101u) >> 24;
@@ -204,8 +234,19 @@ __device__ __forceinline__ bool normal_from(const FrameDesc& F, const float pc[3
   return true;
 }
 
+__device__ unsigned long long g_k1prof[8];
+#define K1_PROBE(i)                                                  \
+  do {                                                               \
+    if ((ablate & 16) && threadIdx.x == 0) {                         \
+      unsigned long long t_;                                         \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));          \
+      atomicAdd(&g_k1prof[i], t_ - t_prev);                          \
+      t_prev = t_;                                                   \
+    }                                                                \
+  } while (0)
+
 template <bool SEM>
-__global__ void __launch_bounds__(K1_THREADS, 2) k_mask_pass(WinDesc wd, WinBufs wb, Params P, int* err,
+__global__ void __launch_bounds__(K1_THREADS, 4) k_mask_pass(WinDesc wd, WinBufs wb, Params P, int* err,
                                                              int rows_cap, int ablate) {
   (void)rows_cap;
   const int f = blockIdx.y;
@@ -225,49 +266,21 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k_mask_pass(WinDesc wd, WinBufs
   const int nin = lane_on ? min(K1_TW, W - u0) : 0;
   const uint32_t inb = nin >= 32 ? 0xFFFFFFFFu : ((1u << nin) - 1u);
 
+  unsigned long long t_prev = 0;
+  if ((ablate & 16) && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_prev));
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const K1Smem L(S, SEM);
   int32_t* bb_s = (int32_t*)(smem_raw + L.bb);
   uint32_t* vs_s = (uint32_t*)(smem_raw + L.vs);
   uint32_t* pl_s = (uint32_t*)(smem_raw + L.pl);
   unsigned long long* kt = (unsigned long long*)(smem_raw + L.kt);   // CTA key table
-  uint16_t* gl = (uint16_t*)(smem_raw + L.gl) + threadIdx.x;         // gl[run * K1_THREADS]
   uint32_t* m0w = (uint32_t*)(smem_raw + L.m0) + threadIdx.x;        // m0w[word * K1_THREADS]
   uint32_t* pt = (uint32_t*)(smem_raw + L.pt);                       // CTA pair table: (s << 16 | local key)
-  uint32_t* ptp = (uint32_t*)(smem_raw + L.pp);                      // -> global pair slot
   float* ptn = (float*)(smem_raw + L.pn);                            // -> normal sums
   float* xa_s = (float*)(smem_raw + L.xa);            // column c <-> u = ut0 - 1 + c
   uint16_t* pc_s = (uint16_t*)(smem_raw + L.pc);
   float* dep = (float*)(smem_raw + L.dep);            // [34][K1_DS], row r <-> v = vt0 - 1 + r
-  uint8_t* msk = (uint8_t*)(smem_raw + L.msk);        // [K1_NG][2][32][K1_MS]
   __shared__ uint32_t npl_s, oor_s;
-
-  // ---- mask stream: plane pairs into the ring with cp.async ----
-  const int ngroups = (S + 1) / 2;
-  const bool async_ok = F.vec16 && (W & 15) == 0;     // 16-byte aligned rows
-  auto issue = [&](int g) {
-    if (g < ngroups && !(ablate & 1)) {
-      uint8_t* slot = msk + (size_t)(g % K1_NG) * 2 * K1_TILE_H * K1_MS;
-      for (int k = 0; k < 2; ++k) {
-        const int s = 2 * g + k;
-        uint8_t* dst = slot + (size_t)k * K1_TILE_H * K1_MS;
-        for (int idx = threadIdx.x; idx < K1_TILE_H * 8; idx += K1_THREADS) {
-          const int row = idx >> 3, c16 = idx & 7;
-          const int vv = vt0 + row, uu = ut0 + 16 * c16;
-          const bool in = s < S && vv < H && uu < W;
-          const uint8_t* src = in ? F.masks + (size_t)s * HW + (int64_t)vv * W + uu : F.masks;
-          uint8_t* d = dst + row * K1_MS + 16 * c16;
-          if (async_ok) {
-            cp_async16(d, src, in ? (uint32_t)min(16, W - uu) : 0u);
-          } else {
-            for (int b = 0; b < 16; ++b) d[b] = (in && uu + b < W) ? src[b] : 0;
-          }
-        }
-      }
-    }
-    cp_async_commit();
-  };
-  for (int g = 0; g < K1_NG - 1; ++g) issue(g);
 
   for (int i = threadIdx.x; i < S; i += blockDim.x) {
     bb_s[4 * i + 0] = INT32_MAX; bb_s[4 * i + 1] = INT32_MAX;
@@ -277,7 +290,6 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k_mask_pass(WinDesc wd, WinBufs
   for (int i = threadIdx.x; i < K1_KT; i += blockDim.x) kt[i] = KEY_EMPTY;
   for (int i = threadIdx.x; i < K1_PT; i += blockDim.x) {
     pt[i] = U32_EMPTY;
-    ptp[i] = U32_EMPTY;
     if (SEM) { ptn[3 * i] = 0.f; ptn[3 * i + 1] = 0.f; ptn[3 * i + 2] = 0.f; }
   }
   for (int t = 0; t < 8; ++t) m0w[t * K1_THREADS] = 0xFFFFFFFFu;   // no mask yet
@@ -294,6 +306,7 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k_mask_pass(WinDesc wd, WinBufs
   }
   if (threadIdx.x == 0) { npl_s = 0; oor_s = 0; }
   __syncthreads();
+  K1_PROBE(0);
 
   const uint32_t tmask = (uint32_t)wb.PC - 1;
   unsigned long long* ktab = wb.ktab + (size_t)f * wb.PC;
@@ -301,6 +314,7 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k_mask_pass(WinDesc wd, WinBufs
   float* nsum = wb.nsum + (size_t)f * wb.PC * 3;
   uint32_t* cnt_g = wb.cnt + (size_t)f * wb.SMAX * wb.PMAXP;
   const float r = P.r;
+  const float rinv = 1.0f / P.r;   // only used by floor_div_pinned's exact fast path
   const float ybv = __fdiv_rn(__fsub_rn((float)v, F.cy), F.fy);        // R5 per row
   const float ybu = __fdiv_rn(__fsub_rn((float)(v - 1), F.cy), F.fy);
   const float ybd = __fdiv_rn(__fsub_rn((float)(v + 1), F.cy), F.fy);
@@ -352,13 +366,12 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k_mask_pass(WinDesc wd, WinBufs
     }
     return pslot;
   };
-  // one (s, key-run) item: CTA pair table, first inserter goes global; normals accumulated
+  // one (s, key-run) item into the CTA pair table (code = s << 16 | local key); the global
+  // frame tables are filled later from the table's distinct codes (phase 5).  Items whose run key
+  // is not in the CTA key table, or that find the pair table full, go global directly.
   auto emit = [&](uint32_t s, uint16_t li, int run_first_c, float n0, float n1, float n2) {
-    uint64_t key = KEY_EMPTY;
     int slot = -1;
-    bool claimed = false;
     if (li != K1_NOKEY) {
-      key = kt[li];
       const uint32_t code = (s << 16) | li;
       uint32_t h = mix32(code) & (K1_PT - 1);
       for (int probe = 0; probe < K1_PT; ++probe) {
@@ -366,81 +379,92 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k_mask_pass(WinDesc wd, WinBufs
         if (cur == code) { slot = (int)h; break; }
         if (cur == U32_EMPTY) {
           const uint32_t old = atomicCAS(&pt[h], U32_EMPTY, code);
-          if (old == U32_EMPTY) { slot = (int)h; claimed = true; break; }
-          if (old == code) { slot = (int)h; break; }
+          if (old == U32_EMPTY || old == code) { slot = (int)h; break; }
         }
         h = (h + 1) & (K1_PT - 1);
       }
-    } else {   // CTA key table full: recompute the run key (pinned R5)
-      float pw[3];
-      if (wp_tile(0, run_first_c, pw)) point_key(pw, r, key);
     }
-    uint32_t pslot = U32_EMPTY;
-    if (slot < 0 || claimed) {
-      pslot = global_insert(key, s);
-      if (claimed) ptp[slot] = pslot;
-    }
-    if (SEM && (n0 != 0.f || n1 != 0.f || n2 != 0.f)) {
-      if (slot >= 0) {
+    if (slot >= 0) {
+      if (SEM && (n0 != 0.f || n1 != 0.f || n2 != 0.f)) {
         atomicAdd(&ptn[3 * slot + 0], n0);
         atomicAdd(&ptn[3 * slot + 1], n1);
         atomicAdd(&ptn[3 * slot + 2], n2);
-      } else if (pslot != U32_EMPTY) {
-        atomicAdd(&nsum[3 * pslot + 0], n0);
-        atomicAdd(&nsum[3 * pslot + 1], n1);
-        atomicAdd(&nsum[3 * pslot + 2], n2);
       }
+      return;
+    }
+    uint64_t key = KEY_EMPTY;
+    if (li != K1_NOKEY) {
+      key = kt[li];
+    } else {   // CTA key table full: recompute the run key (pinned R5)
+      float pw[3];
+      if (wp_tile(0, run_first_c, pw)) point_key_fast(pw, r, rinv, key);
+    }
+    const uint32_t pslot = global_insert(key, s);
+    if (SEM && pslot != U32_EMPTY && (n0 != 0.f || n1 != 0.f || n2 != 0.f)) {
+      atomicAdd(&nsum[3 * pslot + 0], n0);
+      atomicAdd(&nsum[3 * pslot + 1], n1);
+      atomicAdd(&nsum[3 * pslot + 2], n2);
     }
   };
 
-  // ---- 1: keys ----
-  uint32_t okb = 0, kst = 0, pst = 0;
+  // ---- 1: patch segments of the lane's chunk (R17) ----
+  uint32_t okb = 0, pst = 0;
   uint32_t my_oor = 0;
-  if (lane_on && !(ablate & 4)) {
-    uint64_t prevk = KEY_EMPTY;
-    int prevp = -1, ng = 0;
-#pragma unroll 4
-    for (int j = 0; j < K1_TW; ++j) {
-      if (j >= nin) break;
-      const int c = c0 + j;
-      const int p = prow + pc_s[c];
+  if (lane_on) {
+    int prevp = -1;
+    for (int j = 0; j < nin; ++j) {
+      const int p = prow + pc_s[c0 + j];
       if (p != prevp) { pst |= 1u << j; prevp = p; }
-      float pw[3];
-      if (wp_tile(0, c, pw)) {
-        uint64_t key;
-        if (point_key(pw, r, key)) {
-          okb |= 1u << j;
-          if (key != prevk) {
-            kst |= 1u << j;
-            prevk = key;
-            gl[ng * K1_THREADS] = kt_insert(key);
-            ng++;
-          }
-        } else {
-          my_oor++;
-        }
-      }
     }
   }
 
-  // ---- 2: masks -> first mask per pixel, overlap flags, per-patch counts, bbox ----
+  __syncthreads();
+  K1_PROBE(1);
+  // ---- 2: masks -> first mask per pixel, overlap flags, per-patch counts, bbox.  Each lane
+  // streams its 32 bytes of every plane (evict-first in L2), two planes in flight ----
   uint32_t ovf = 0;
-  for (int g = 0; g < ngroups; ++g) {
-    cp_async_wait<K1_NG - 2>();
-    __syncthreads();
-    const uint8_t* slot_base = msk + (size_t)(g % K1_NG) * 2 * K1_TILE_H * K1_MS;
-    for (int k = 0; k < 2 && lane_on; ++k) {
-      const int s = 2 * g + k;
-      if (s >= S || (ablate & 1)) break;
-      const uint8_t* row = slot_base + (size_t)k * K1_TILE_H * K1_MS + lane * K1_MS + warp * K1_TW;
-      const uint4 a = *(const uint4*)row, b = *(const uint4*)(row + 16);
-      if ((a.x | a.y | a.z | a.w | b.x | b.y | b.z | b.w) == 0) continue;
-      const uint32_t w8[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  const int64_t pix0 = (int64_t)v * W + u0;
+  const bool vec32 = F.vec16 && nin == 32 && (pix0 & 31) == 0;
+  const bool vec16 = F.vec16 && nin == 32 && (pix0 & 15) == 0;
+  auto load_pair = [&](int s0, uint32_t w[2][8]) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) w[k][t] = 0u;
+      if (s0 + k < S) {
+        const uint8_t* mp = F.masks + (size_t)(s0 + k) * HW + pix0;
+        if (vec32) {
+          ld_stream32(mp, w[k]);
+        } else if (vec16) {
+          const uint4 a = ld_stream16(mp), b = ld_stream16(mp + 16);
+          w[k][0] = a.x; w[k][1] = a.y; w[k][2] = a.z; w[k][3] = a.w;
+          w[k][4] = b.x; w[k][5] = b.y; w[k][6] = b.z; w[k][7] = b.w;
+        } else {
+          for (int t = 0; t < 8; ++t) {
+            uint32_t x = 0;
+            for (int bq = 0; bq < 4; ++bq)
+              if (inb & (1u << (4 * t + bq))) x |= (uint32_t)(mp[4 * t + bq] != 0) << (8 * bq);
+            w[k][t] = x;
+          }
+        }
+      }
+    }
+  };
+  const int Sl = (lane_on && !(ablate & 1)) ? S : 0;
+  uint32_t wa[2][8], wn[2][8];
+  if (Sl > 0) load_pair(0, wa);
+  for (int s0 = 0; s0 < Sl; s0 += 2) {
+    if (s0 + 2 < Sl) load_pair(s0 + 2, wn);   // next pair in flight while this one is processed
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int s = s0 + k;
+      if (s >= S) break;
+      if ((wa[k][0] | wa[k][1] | wa[k][2] | wa[k][3] | wa[k][4] | wa[k][5] | wa[k][6] | wa[k][7]) == 0) continue;
       uint32_t set = 0;
       const uint32_t splat = (uint32_t)s * 0x01010101u;
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
-        const uint32_t sb = __vcmpne4(w8[t], 0u);                 // 0xFF where the pixel is in s
+        const uint32_t sb = __vcmpne4(wa[k][t], 0u);                // 0xFF where the pixel is in s
         set |= (((sb & 0x08040201u) * 0x01010101u) >> 24) << (4 * t);
         if (sb) {
           const uint32_t m = m0w[t * K1_THREADS];
@@ -464,66 +488,106 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k_mask_pass(WinDesc wd, WinBufs
       atomicMin(&bb_s[4 * s + 1], v);
       atomicMax(&bb_s[4 * s + 3], v);
     }
-    __syncthreads();                 // everyone is done with ring slot g % K1_NG
-    issue(g + K1_NG - 1);
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int t = 0; t < 8; ++t) wa[k][t] = wn[k][t];
   }
-  cp_async_wait<0>();
+  __syncthreads();
+  K1_PROBE(2);
 
-  // ---- 3: (first mask, key run) items, normals ----
+  // ---- 3: one sliding window over the lane's pixels: pinned keys (R5), key runs, (first mask,
+  // run) items, pixel normals (R21).  Each world point is computed once. ----
   if (lane_on && !(ablate & 2)) {
-    int run = -1, cur_run = -1, first_c = 0;
+    uint64_t run_key = KEY_EMPTY, cur_key = KEY_EMPTY;
+    uint16_t run_li = K1_NOKEY, cur_li = K1_NOKEY;
+    bool run_li_ok = false;
+    int cur_first = 0;
     uint32_t cur_m = 0xFF;
     float n0 = 0.f, n1 = 0.f, n2 = 0.f;
+    const bool inner_v = v >= 1 && v + 1 < H;
+    float pl[3] = {0.f, 0.f, 0.f}, pc[3] = {0.f, 0.f, 0.f};
+    bool vl = SEM ? wp_tile(0, c0 - 1, pl) : false;
+    bool vc = wp_tile(0, c0, pc);
     for (int j = 0; j < nin; ++j) {
-      if (kst & (1u << j)) run++;
-      if (!(okb & (1u << j))) continue;
-      const uint32_t mj = (m0w[(j >> 2) * K1_THREADS] >> (8 * (j & 3))) & 0xFFu;
-      if (mj == 0xFFu) continue;
-      if (cur_m != 0xFFu && (run != cur_run || mj != cur_m)) {
-        emit(cur_m, gl[cur_run * K1_THREADS], first_c, n0, n1, n2);
-        cur_m = 0xFFu;
+      float pr[3] = {0.f, 0.f, 0.f};
+      const bool vr = (j + 1 < nin || SEM) ? wp_tile(0, c0 + j + 1, pr) : false;
+      uint64_t key = KEY_EMPTY;
+      bool ok = false;
+      if (vc) {
+        if (point_key_fast(pc, r, rinv, key)) ok = true;
+        else my_oor++;
       }
-      if (cur_m == 0xFFu) {
-        cur_m = mj;
-        cur_run = run;
-        first_c = c0 + j;
-        n0 = n1 = n2 = 0.f;
+      if (ok) {
+        okb |= 1u << j;
+        if (key != run_key) { run_key = key; run_li_ok = false; }
+        const uint32_t mj = (m0w[(j >> 2) * K1_THREADS] >> (8 * (j & 3))) & 0xFFu;
+        if (mj != 0xFFu) {
+          if (cur_m != 0xFFu && (key != cur_key || mj != cur_m)) {
+            emit(cur_m, cur_li, cur_first, n0, n1, n2);
+            cur_m = 0xFFu;
+          }
+          if (cur_m == 0xFFu) {
+            if (!run_li_ok) { run_li = kt_insert(run_key); run_li_ok = true; }
+            cur_m = mj;
+            cur_key = key;
+            cur_li = run_li;
+            cur_first = c0 + j;
+            n0 = n1 = n2 = 0.f;
+          }
+          const int u = u0 + j;
+          if (SEM && !(ablate & 8) && vl && vr && inner_v && u >= 1 && u + 1 < W) {
+            float pu[3], pd[3], n[3];
+            if (wp_tile(-1, c0 + j, pu) && wp_tile(1, c0 + j, pd) && normal_from(F, pc, pl, pr, pu, pd, n)) {
+              n0 += n[0]; n1 += n[1]; n2 += n[2];
+            }
+          }
+        }
       }
-      if (SEM && !(ablate & 8)) {
-        float n[3];
-        if (pixel_normal(c0 + j, n)) { n0 += n[0]; n1 += n[1]; n2 += n[2]; }
-      }
+      pl[0] = pc[0]; pl[1] = pc[1]; pl[2] = pc[2]; vl = vc;
+      pc[0] = pr[0]; pc[1] = pr[1]; pc[2] = pr[2]; vc = vr;
     }
-    if (cur_m != 0xFFu) emit(cur_m, gl[cur_run * K1_THREADS], first_c, n0, n1, n2);
+    if (cur_m != 0xFFu) emit(cur_m, cur_li, cur_first, n0, n1, n2);
   }
 
   // ---- 4: pixels in several masks (overlapping masks, R9): their other planes ----
   if (lane_on && (ovf & okb) && !(ablate & 2)) {
-    int run = -1;
-    for (int j = 0; j < nin; ++j) {
-      if (kst & (1u << j)) run++;
-      if (!((ovf & okb) & (1u << j))) continue;
+    for (uint32_t bb2 = ovf & okb; bb2;) {
+      const int j = __ffs(bb2) - 1;
+      bb2 &= bb2 - 1;
       const uint32_t mj = (m0w[(j >> 2) * K1_THREADS] >> (8 * (j & 3))) & 0xFFu;
+      float pw[3];
+      uint64_t key = KEY_EMPTY;
+      if (!wp_tile(0, c0 + j, pw) || !point_key_fast(pw, r, rinv, key)) continue;
+      const uint16_t li = kt_insert(key);
       float n[3] = {0.f, 0.f, 0.f};
       if (SEM && !(ablate & 8) && !pixel_normal(c0 + j, n)) { n[0] = n[1] = n[2] = 0.f; }
       const size_t pix = (size_t)v * W + u0 + j;
-      for (int s = (int)mj + 1; s < S; ++s)
-        if (F.masks[(size_t)s * HW + pix]) emit((uint32_t)s, gl[run * K1_THREADS], c0 + j, n[0], n[1], n[2]);
+      for (int s2 = (int)mj + 1; s2 < S; ++s2)
+        if (F.masks[(size_t)s2 * HW + pix]) emit((uint32_t)s2, li, c0 + j, n[0], n[1], n[2]);
     }
   }
   if (lane_on && my_oor) atomicAdd(&oor_s, my_oor);
   __syncthreads();
-  if (SEM)   // flush normal sums: one global add per distinct (s, key) of the tile
-    for (int i = threadIdx.x; i < K1_PT; i += blockDim.x) {
-      const uint32_t ps = ptp[i];
-      if (pt[i] == U32_EMPTY || ps == U32_EMPTY) continue;
+  K1_PROBE(3);
+  // ---- 5: the tile's distinct (s, key) pairs -> global frame tables (all threads, many
+  // independent inserts in flight); normal sums flushed with them ----
+  for (int i = threadIdx.x; i < K1_PT; i += blockDim.x) {
+    const uint32_t code = pt[i];
+    if (code == U32_EMPTY) continue;
+    const uint32_t s = code >> 16;
+    const uint32_t pslot = global_insert(kt[code & 0xFFFFu], s);
+    if (SEM && pslot != U32_EMPTY) {
       const float n0 = ptn[3 * i], n1 = ptn[3 * i + 1], n2 = ptn[3 * i + 2];
       if (n0 != 0.f || n1 != 0.f || n2 != 0.f) {
-        atomicAdd(&nsum[3 * ps + 0], n0);
-        atomicAdd(&nsum[3 * ps + 1], n1);
-        atomicAdd(&nsum[3 * ps + 2], n2);
+        atomicAdd(&nsum[3 * pslot + 0], n0);
+        atomicAdd(&nsum[3 * pslot + 1], n1);
+        atomicAdd(&nsum[3 * pslot + 2], n2);
       }
     }
+  }
+  __syncthreads();
+  K1_PROBE(4);
 
   // ---- flush per-mask accumulators ----
   for (int s = threadIdx.x; s < S; s += blockDim.x) {
@@ -547,6 +611,14 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k_mask_pass(WinDesc wd, WinBufs
     return;
   }
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) wb.plist[(size_t)f * wb.PMAX + base_s + i] = pl_s[i];
+  K1_PROBE(5);
+}
+
+void k1_prof_dump() {
+  unsigned long long h[8];
+  cudaMemcpyFromSymbol(h, g_k1prof, sizeof(h));
+  fprintf(stderr, "k1 phase CTA-ns: setup %llu keys %llu masks %llu items %llu global %llu flush %llu\n", h[0], h[1],
+          h[2], h[3], h[4], h[5]);
 }
 
 // ------------------------------------------------------------------------------------------

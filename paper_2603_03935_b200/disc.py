@@ -103,6 +103,7 @@ EXPORTS = {
     "disc_debug_last_frame": (C.c_int, [C.c_void_p, C.c_void_p]),
     "disc_set_timing": (C.c_int, [C.c_void_p, C.c_int32]),
     "disc_get_stats": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "disc_wait": (C.c_int, [C.c_void_p, C.c_void_p]),
     "disc_sync": (C.c_int, [C.c_void_p]),
     "disc_last_error": (C.c_char_p, [C.c_void_p]),
     "disc_version": (C.c_char_p, []),
@@ -310,3 +311,7 @@ class DiscMap:
 
     def sync(self):
         self._check(lib().disc_sync(self.h))
+
+    def wait(self, stream=None):
+        """Order `stream` (default: torch's current stream) after all queued map work."""
+        self._check(lib().disc_wait(self.h, self._stream(stream)))
