@@ -340,6 +340,7 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(W.emb = dalloc<float>(m, (size_t)win * SM * Df));
   chk(W.trk = dalloc<double>(m, (size_t)win * SM * std::max(Dt, 1)));
   chk(W.tok = dalloc<uint8_t>(m, (size_t)win * SM));
+  chk(W.pmode = dalloc<uint8_t>(m, (size_t)win * SM));
   }
   // ---- map ----
   MapState& M = m->M;
@@ -490,6 +491,8 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
     if (m->s2_pending[b]) cudaStreamWaitEvent(s1, m->ev_s2[b], 0);   // stage 2 done with this buffer
     WinDesc wd{};
     wd.n = nw;
+    wd.Df = Df;
+    wd.Dt = Dt;
     int maxS = 1, maxHp = 1, maxW = 1, maxWp = 1, maxP = 1, rows = 4;
     bool sem = false;
     size_t so = 0;

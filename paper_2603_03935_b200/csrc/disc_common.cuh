@@ -61,6 +61,7 @@ struct FrameDesc {                // one frame's inputs, passed by value to kern
 struct WinDesc {
   FrameDesc f[MAXWIN];
   int32_t n;
+  int32_t Df, Dt;   // feature widths (accumulator zeroing in k_win_init)
 };
 
 struct Params {                   // method constants
@@ -97,6 +98,7 @@ struct WinBufs {
   float* emb;                 // [win][SMAX][Df]
   double* trk;                // [win][SMAX][Dt]  t_s
   uint8_t* tok;               // [win][SMAX] t_s defined (nonzero norm)
+  uint8_t* pmode;             // [win][SMAX] 1: unweighted pooling fallback (R18)
   int32_t PC;                 // frame table capacity (power of 2)
   int32_t PMAX, SMAX, PMAXP, FCHUNKS;
 };

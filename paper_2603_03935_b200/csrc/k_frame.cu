@@ -7,8 +7,8 @@
 //                      pixel counts, unique (s, key) pairs (|V_s|), pixel normal sums (R21)
 //  K2  k_pairs         pair records for stage 2, detection AABBs, S_angle terms (Eq.3)
 //  K3  k_fbar_part / k_fbar / k_resid   distinctiveness map inputs (Eq.1)
-//  K4  k_detect        mask filter (A1), D-weighted pooling, Q (Eq.2-3) and the
-//                      tracking feature t_s (R15)
+//  K4  k_filter / k_pool / k_finalize   mask filter (A1), D-weighted pooling,
+//                      Q (Eq.2-3) and the tracking feature t_s (R15)
 #include "disc_common.cuh"
 #include "disc_launch.h"
 
@@ -139,6 +139,11 @@ __global__ void k_win_init(WinDesc wd, WinBufs wb) {
       wb.daabb[6 * i + 3 + k] = INT32_MIN;
     }
   }
+  // pooling / tracking accumulators of this frame's masks (k_pool reduces into them)
+  for (size_t i = threadIdx.x + blockIdx.x * blockDim.x; i < (size_t)S * wd.Df; i += blockDim.x * gridDim.x)
+    wb.emb[(size_t)f * wb.SMAX * wd.Df + i] = 0.f;
+  for (size_t i = threadIdx.x + blockIdx.x * blockDim.x; i < (size_t)S * wd.Dt; i += blockDim.x * gridDim.x)
+    wb.trk[(size_t)f * wb.SMAX * wd.Dt + i] = 0.0;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     wb.npairs[f] = 0;
     wb.oor[f] = 0;
@@ -803,12 +808,19 @@ __global__ void __launch_bounds__(1024) k_dmap(WinDesc wd, WinBufs wb, Params P)
 }
 
 // ------------------------------------------------------------------------------------------
-// K4: one CTA per (mask, frame): mask filter (A1), D-weighted pooling (R18), D̄ (R19),
-// Q (Eq.2-3), tracking feature t_s (R15).  Patches of the mask's bbox are split across the
-// 8 warps; per-warp partial sums are combined in fixed warp order (deterministic).
+// K4: per-detection features, split for balance (a wall-sized mask no longer serialises ~1000
+// patches in one CTA):
+//  k_filter   (mask, frame): |M_s| from the per-patch counts, mask filter (A1/R8), no-depth
+//             drop; semantic: weight sums -> fallback mode (R18), D̄_s (R19)
+//  k_pool     (CTA group, mask, frame): D-weighted pooling y_s += w_p f_p and tracking
+//             u_s += cnt_sp g_p (R15) over an interleaved share of the bbox patches; per-CTA
+//             fixed-order partials reduced into per-mask accumulators (fp32 / fp64 RED)
+//  k_finalize (mask, frame): e_s = y/|y| ("nofeat" if 0), S_size, S_angle, S_sem, S_dist, Q
+//             (Eq.2-3); t_s = u / sqrt(dot_pin(u, u)) (R15)
 // ------------------------------------------------------------------------------------------
 constexpr int K4_THREADS = 256;
 constexpr int K4_WARPS = K4_THREADS / 32;
+constexpr int K4_CTAS = 8;        // CTAs per mask in k_pool
 
 __device__ __forceinline__ double block_sum_d(double x, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -837,105 +849,125 @@ __device__ __forceinline__ double dot_pin_warp(const double* a, const double* b,
   return acc;
 }
 
-size_t k4_smem_bytes(int Df, int Dt) {
-  return 40 * 8 + (size_t)K4_WARPS * Df * 4 + (size_t)K4_WARPS * (Dt > 0 ? Dt : 1) * 8 + (size_t)(Dt > 0 ? Dt : 1) * 8 + 64;
-}
+struct BoxPatches {   // the patch range of a mask's bbox (every patch with cnt > 0 lies in it)
+  int pr0, pc0, npr, npc, n;
+  __device__ BoxPatches(const WinBufs& wb, size_t gi, int H, int W, int Hp, int Wp) {
+    const int umin = wb.bbox[4 * gi + 0], vmin = wb.bbox[4 * gi + 1];
+    const int umax = wb.bbox[4 * gi + 2], vmax = wb.bbox[4 * gi + 3];
+    pr0 = pc0 = 0; npr = npc = 0;
+    if (umax >= 0) {
+      pr0 = (int)((int64_t)vmin * Hp / H);
+      pc0 = (int)((int64_t)umin * Wp / W);
+      npr = (int)((int64_t)vmax * Hp / H) - pr0 + 1;
+      npc = (int)((int64_t)umax * Wp / W) - pc0 + 1;
+    }
+    n = npr * npc;
+  }
+  __device__ int patch(int k, int Wp) const { return (pr0 + k / npc) * Wp + pc0 + k % npc; }
+  __device__ double npix(int k, int H, int W, int Hp, int Wp) const {   // pixels of patch k (R17)
+    const int i = pr0 + k / npc, j = pc0 + k % npc;
+    const int64_t rows = ((int64_t)(i + 1) * H + Hp - 1) / Hp - ((int64_t)i * H + Hp - 1) / Hp;
+    const int64_t cols = ((int64_t)(j + 1) * W + Wp - 1) / Wp - ((int64_t)j * W + Wp - 1) / Wp;
+    return (double)(rows * cols);
+  }
+};
 
 template <bool SEM>
-__global__ void __launch_bounds__(K4_THREADS) k_detect(WinDesc wd, WinBufs wb, Params P) {
+__global__ void __launch_bounds__(K4_THREADS) k_filter(WinDesc wd, WinBufs wb, Params P) {
   const int f = blockIdx.y;
   if (f >= wd.n) return;
   const FrameDesc& F = wd.f[f];
   const int s = blockIdx.x;
   if (s >= F.S) return;
-  const int H = F.H, W = F.W, Hp = F.Hp, Wp = F.Wp, Df = P.Df, Dt = P.Dt;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int H = F.H, W = F.W, Hp = F.Hp, Wp = F.Wp;
   const size_t gi = (size_t)f * wb.SMAX + s;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* red = (double*)smem_raw;                         // [40]
-  float* ypart = (float*)(red + 40);                       // [K4_WARPS][Df]
-  double* upart = (double*)(ypart + (size_t)K4_WARPS * Df); // [K4_WARPS][Dt]
-  double* u_s = upart + (size_t)K4_WARPS * (Dt > 0 ? Dt : 1);  // [Dt]
-
-  const int umin = wb.bbox[4 * gi + 0], vmin = wb.bbox[4 * gi + 1];
-  const int umax = wb.bbox[4 * gi + 2], vmax = wb.bbox[4 * gi + 3];
+  __shared__ double red[40];
+  const BoxPatches B(wb, gi, H, W, Hp, Wp);
   const uint32_t* cnt = wb.cnt + (size_t)f * wb.SMAX * wb.PMAXP + (size_t)s * wb.PMAXP;
-  // patch range of the bbox (all patches with cnt > 0 lie inside it)
-  int pr0 = 0, pr1 = -1, pc0 = 0, pc1 = -1;
-  if (umax >= 0) {
-    pr0 = (int)((int64_t)vmin * Hp / H); pr1 = (int)((int64_t)vmax * Hp / H);
-    pc0 = (int)((int64_t)umin * Wp / W); pc1 = (int)((int64_t)umax * Wp / W);
-  }
-  const int npc = pc1 - pc0 + 1, npr = pr1 - pr0 + 1, nbox = npr > 0 ? npr * npc : 0;
-  auto patch_of = [&](int k) { return (pr0 + k / npc) * Wp + pc0 + k % npc; };
-  auto npix_of = [&](int k) {   // pixels of patch k under the floor mapping (R17)
-    const int i = pr0 + k / npc, j = pc0 + k % npc;
-    const int64_t rows = ((int64_t)(i + 1) * H + Hp - 1) / Hp - ((int64_t)i * H + Hp - 1) / Hp;
-    const int64_t cols = ((int64_t)(j + 1) * W + Wp - 1) / Wp - ((int64_t)j * W + Wp - 1) / Wp;
-    return (double)(rows * cols);
-  };
   double asum = 0;
-  for (int k = threadIdx.x; k < nbox; k += blockDim.x) asum += (double)cnt[patch_of(k)];
+  for (int k = threadIdx.x; k < B.n; k += blockDim.x) asum += (double)cnt[B.patch(k, Wp)];
   const uint32_t area = (uint32_t)block_sum_d(asum, red);
-
-  // ---- A1 mask filter (R8): first failing reason wins: area==0, conf, aspect, area ----
+  // A1 mask filter (R8, R28): first failing reason wins: area==0, conf, aspect, area
   const float conf = F.conf ? F.conf[s] : 1.0f;
   int status = 0;
   if (area == 0) status = 1;
   else if (conf < P.min_conf) status = 2;
   else {
-    const int64_t bw = umax - umin + 1, bh = vmax - vmin + 1;
+    const int64_t bw = (int64_t)wb.bbox[4 * gi + 2] - wb.bbox[4 * gi + 0] + 1;
+    const int64_t bh = (int64_t)wb.bbox[4 * gi + 3] - wb.bbox[4 * gi + 1] + 1;
     const int64_t lo = min(bw, bh), hi = max(bw, bh);
     if ((double)hi > (double)P.max_aspect * (double)lo) status = 3;
     else if ((int64_t)area < (int64_t)P.min_area) status = 1;
     else if (wb.vs[gi] == 0) status = 4;            // O3 no valid depth
   }
   float* qf = wb.qf + 6 * gi;
-  if (threadIdx.x == 0) wb.area[gi] = area;
-  if (status != 0) {
-    if (threadIdx.x == 0) {
-      wb.status[gi] = status;
+  if (threadIdx.x == 0) {
+    wb.area[gi] = area;
+    wb.status[gi] = status;
+    wb.pmode[gi] = 0;
+    if (status != 0) {
       for (int k = 0; k < 6; ++k) qf[k] = k == 4 ? -1.f : 0.f;
       wb.tok[gi] = 0;
     }
-    return;
   }
+  if (status != 0 || !(SEM && F.feats)) return;
+  // weight sums (O7): w = D cnt/npix if cnt >= cover_min npix (exact); D̄ over cnt > 0 (R19)
+  const float* D = wb.rp + (size_t)f * wb.PMAXP;
+  double wsum = 0, dnum = 0, dden = 0;
+  for (int k = threadIdx.x; k < B.n; k += blockDim.x) {
+    const int p = B.patch(k, Wp);
+    const uint32_t c = cnt[p];
+    if (!c) continue;
+    const double npix = B.npix(k, H, W, Hp, Wp);
+    const double cov = (double)c / npix;
+    const double Dp = (double)D[p];
+    dnum += cov * Dp;
+    dden += cov;
+    if ((double)c >= (double)P.cover_min * npix) wsum += Dp * cov;
+  }
+  wsum = block_sum_d(wsum, red);
+  dnum = block_sum_d(dnum, red);
+  dden = block_sum_d(dden, red);
+  if (threadIdx.x == 0) {
+    wb.pmode[gi] = (wsum > 0.0) ? 0 : 1;   // 1: all-zero weights -> unweighted mean (R18)
+    qf[5] = (float)(dden > 0 ? dnum / dden : 0.0);
+  }
+}
 
+template <bool SEM>
+__global__ void __launch_bounds__(K4_THREADS) k_pool(WinDesc wd, WinBufs wb, Params P) {
+  const int f = blockIdx.z;
+  if (f >= wd.n) return;
+  const FrameDesc& F = wd.f[f];
+  const int s = blockIdx.y;
+  if (s >= F.S) return;
+  const size_t gi = (size_t)f * wb.SMAX + s;
+  if (wb.status[gi] != 0) return;
+  const int H = F.H, W = F.W, Hp = F.Hp, Wp = F.Wp, Df = P.Df, Dt = P.Dt;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const BoxPatches B(wb, gi, H, W, Hp, Wp);
+  const int stride = K4_CTAS * K4_WARPS;
+  const int k0 = blockIdx.x * K4_WARPS + warp;   // interleaved: CTA group x warps
+  if (blockIdx.x * K4_WARPS >= B.n) return;
+  const uint32_t* cnt = wb.cnt + (size_t)f * wb.SMAX * wb.PMAXP + (size_t)s * wb.PMAXP;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   if (SEM && F.feats) {
-    const float* D = wb.rp + (size_t)f * wb.PMAXP;   // D_p (k_dmap)
-    // weight sums (O7): w = D cnt/npix if cnt >= cover_min npix (exact); D̄ over cnt > 0
-    double wsum = 0, dnum = 0, dden = 0;
-    for (int k = threadIdx.x; k < nbox; k += blockDim.x) {
-      const int p = patch_of(k);
-      const uint32_t c = cnt[p];
-      if (!c) continue;
-      const double npix = npix_of(k);
-      const double cov = (double)c / npix;
-      const double Dp = (double)D[p];
-      dnum += cov * Dp;
-      dden += cov;
-      if ((double)c >= (double)P.cover_min * npix) wsum += Dp * cov;
-    }
-    wsum = block_sum_d(wsum, red);
-    dnum = block_sum_d(dnum, red);
-    dden = block_sum_d(dden, red);
-    const bool fallback = !(wsum > 0.0);
-    const double dbar = dden > 0 ? dnum / dden : 0.0;
-    // y = sum_p w_p f_p: warp w takes patches k = w, w + 8, ...; lane holds Df/32 columns
-    const int D4 = Df / 4;
-    const int nq4 = (D4 + 31) / 32;    // float4 per lane (Df <= 1024)
+    float* ypart = (float*)smem_raw;                 // [K4_WARPS][Df]
+    const float* D = wb.rp + (size_t)f * wb.PMAXP;
+    const bool fallback = wb.pmode[gi] != 0;
+    const int D4 = Df / 4, nq4 = (D4 + 31) / 32;
     float4 acc[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int k = warp; k < nbox; k += K4_WARPS) {
-      const int p = patch_of(k);
+    for (int k = k0; k < B.n; k += stride) {
+      const int p = B.patch(k, Wp);
       const uint32_t c = cnt[p];
       if (!c) continue;
       float w;
       if (fallback) {
         w = 1.0f;
       } else {
-        const double npix = npix_of(k);
+        const double npix = B.npix(k, H, W, Hp, Wp);
         if (!((double)c >= (double)P.cover_min * npix)) continue;
         w = (float)((double)D[p] * ((double)c / npix));
       }
@@ -954,14 +986,63 @@ __global__ void __launch_bounds__(K4_THREADS) k_detect(WinDesc wd, WinBufs wb, P
     for (int i = 0; i < 8; ++i)
       if (i < nq4 && lane + 32 * i < D4) yp[lane + 32 * i] = acc[i];
     __syncthreads();
+    float* y = wb.emb + gi * Df;   // per-mask accumulator (zeroed by k_win_init)
+    for (int d = threadIdx.x; d < Df; d += blockDim.x) {
+      float a = 0.f;
+      for (int w2 = 0; w2 < K4_WARPS; ++w2) a += ypart[(size_t)w2 * Df + d];
+      if (a != 0.f) atomicAdd(&y[d], a);
+    }
+    __syncthreads();
+  }
+  if (Dt > 0) {
+    double* upart = (double*)smem_raw;               // [K4_WARPS][Dt] (reuses the pooling scratch)
+    const int nd = (Dt + 31) / 32;
+    double ua[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) ua[i] = 0.0;
+    for (int k = k0; k < B.n; k += stride) {
+      const int p = B.patch(k, Wp);
+      const uint32_t c = cnt[p];
+      if (!c) continue;
+      const uint16_t* g = F.track + (size_t)p * Dt;
+      const double cd = (double)c;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int d = lane + 32 * i;
+        if (i < nd && d < Dt) ua[i] = __dadd_rn(ua[i], __dmul_rn(cd, (double)__uint_as_float((uint32_t)g[d] << 16)));
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int d = lane + 32 * i;
+      if (i < nd && d < Dt) upart[(size_t)warp * Dt + d] = ua[i];
+    }
+    __syncthreads();
+    double* u = wb.trk + gi * Dt;   // per-mask accumulator u_s (exact sums, R15)
+    for (int d = threadIdx.x; d < Dt; d += blockDim.x) {
+      double a = 0.0;
+      for (int w2 = 0; w2 < K4_WARPS; ++w2) a = __dadd_rn(a, upart[(size_t)w2 * Dt + d]);
+      if (a != 0.0) atomicAdd(&u[d], a);
+    }
+  }
+}
+
+template <bool SEM>
+__global__ void __launch_bounds__(K4_THREADS) k_finalize(WinDesc wd, WinBufs wb, Params P) {
+  const int f = blockIdx.y;
+  if (f >= wd.n) return;
+  const FrameDesc& F = wd.f[f];
+  const int s = blockIdx.x;
+  if (s >= F.S) return;
+  const size_t gi = (size_t)f * wb.SMAX + s;
+  if (wb.status[gi] != 0) return;
+  const int H = F.H, W = F.W, Df = P.Df, Dt = P.Dt;
+  __shared__ double red[40];
+  float* qf = wb.qf + 6 * gi;
+  if (SEM && F.feats) {
     float* emb = wb.emb + gi * Df;
     double yy = 0;
-    for (int d = threadIdx.x; d < Df; d += blockDim.x) {
-      float y = 0.f;
-      for (int w2 = 0; w2 < K4_WARPS; ++w2) y += ypart[(size_t)w2 * Df + d];
-      emb[d] = y;
-      yy += (double)y * y;
-    }
+    for (int d = threadIdx.x; d < Df; d += blockDim.x) yy += (double)emb[d] * emb[d];
     yy = block_sum_d(yy, red);
     if (!(yy > 0.0)) {
       if (threadIdx.x == 0) {
@@ -985,61 +1066,27 @@ __global__ void __launch_bounds__(K4_THREADS) k_detect(WinDesc wd, WinBufs wb, P
     eg = block_sum_d(eg, red);
     gg = block_sum_d(gg, red);
     if (threadIdx.x == 0) {
-      const double s_size = fmin((double)P.lambda * (double)area / ((double)H * (double)W), 1.0);
+      const double s_size = fmin((double)P.lambda * (double)wb.area[gi] / ((double)H * (double)W), 1.0);
       const uint32_t ac = wb.ang_cnt[gi];
       const double s_angle = ac ? (double)wb.ang_sum[gi] / (double)ac : 0.0;
       double s_sem = 1.0;
       if (F.gemb) s_sem = gg > 0 ? fmin(fmax(eg / sqrt(gg), 0.0), 1.0) : 0.0;
+      const double dbar = (double)qf[5];
       const double s_dist = 0.5 + 0.5 * dbar;
       qf[0] = (float)s_size; qf[1] = (float)s_angle; qf[2] = (float)s_sem; qf[3] = (float)s_dist;
       qf[4] = (float)(((s_size * s_angle) * s_sem) * s_dist);
-      qf[5] = (float)dbar;
     }
   } else if (threadIdx.x == 0) {
     for (int k = 0; k < 6; ++k) qf[k] = k == 4 ? -1.f : 0.f;   // geometry-only: no embedding
   }
-
-  // ---- A5b tracking feature (R15): u = sum_p cnt_sp g_p in fp64 (exact for snapped inputs,
-  // so the warp-split order gives the oracle's bits), t = u / sqrt(dot_pin(u, u)) ----
-  if (Dt > 0) {
-    const int nd = (Dt + 31) / 32;   // dims per lane (<= 16 on the register path)
-    double ua[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) ua[i] = 0.0;
-    for (int k = warp; k < nbox; k += K4_WARPS) {
-      const int p = patch_of(k);
-      const uint32_t c = cnt[p];
-      if (!c) continue;
-      const uint16_t* g = F.track + (size_t)p * Dt;
-      const double cd = (double)c;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int d = lane + 32 * i;
-        if (i < nd && d < Dt) ua[i] = __dadd_rn(ua[i], __dmul_rn(cd, (double)__uint_as_float((uint32_t)g[d] << 16)));
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int d = lane + 32 * i;
-      if (i < nd && d < Dt) upart[(size_t)warp * Dt + d] = ua[i];
-    }
-    __syncthreads();
-    for (int d = threadIdx.x; d < Dt; d += blockDim.x) {
-      double a = 0.0;
-      for (int w2 = 0; w2 < K4_WARPS; ++w2) a = __dadd_rn(a, upart[(size_t)w2 * Dt + d]);
-      u_s[d] = a;
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      const double nn = dot_pin_warp(u_s, u_s, Dt);
-      double* t = wb.trk + gi * Dt;
-      const bool ok = nn > 0.0;
-      const double n = ok ? sqrt(nn) : 1.0;
-      for (int d = threadIdx.x; d < Dt; d += 32) t[d] = ok ? __ddiv_rn(u_s[d], n) : 0.0;
-      if (threadIdx.x == 0) wb.tok[gi] = ok ? 1 : 0;
-    }
+  if (Dt > 0 && threadIdx.x < 32) {
+    double* t = wb.trk + gi * Dt;   // holds u_s; normalised in place
+    const double nn = dot_pin_warp(t, t, Dt);
+    const bool ok = nn > 0.0;
+    const double n = ok ? sqrt(nn) : 1.0;
+    for (int d = threadIdx.x; d < Dt; d += 32) t[d] = ok ? __ddiv_rn(t[d], n) : 0.0;
+    if (threadIdx.x == 0) wb.tok[gi] = ok ? 1 : 0;
   }
-  if (threadIdx.x == 0) wb.status[gi] = 0;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1097,13 +1144,20 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
     k_dmap<<<n, 1024, 0, st>>>(wd, wb, P);
     debug_check(st, "k_fbar/k_resid/k_dmap", -1);
   }
-  const size_t sm4 = k4_smem_bytes(P.Df, P.Dt);
-  cudaFuncSetAttribute(k_detect<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
-  cudaFuncSetAttribute(k_detect<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
-  if (sem) k_detect<true><<<dim3(maxS, n), K4_THREADS, sm4, st>>>(wd, wb, P);
-  else k_detect<false><<<dim3(maxS, n), K4_THREADS, sm4, st>>>(wd, wb, P);
-  debug_check(st, "k_detect", -1);
-  return sem ? 8 : 4;
+  const size_t smp = std::max((size_t)K4_WARPS * P.Df * 4, (size_t)K4_WARPS * std::max(P.Dt, 1) * 8);
+  cudaFuncSetAttribute(k_pool<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);
+  cudaFuncSetAttribute(k_pool<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);
+  if (sem) {
+    k_filter<true><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
+    k_pool<true><<<dim3(K4_CTAS, maxS, n), K4_THREADS, smp, st>>>(wd, wb, P);
+    k_finalize<true><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
+  } else {
+    k_filter<false><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
+    k_pool<false><<<dim3(K4_CTAS, maxS, n), K4_THREADS, smp, st>>>(wd, wb, P);
+    k_finalize<false><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
+  }
+  debug_check(st, "k_filter/k_pool/k_finalize", -1);
+  return sem ? 10 : 6;
 }
 
 }  // namespace disc
