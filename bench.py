@@ -123,34 +123,23 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
+from paper_2603_03935_b200 import parallel as par  # noqa: E402
+
+
 def setup_dist():
-    import torch
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if ws > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    elif torch.cuda.is_available():
-        torch.cuda.set_device(0)
-    return ws, rank, local
+    r = par.setup()
+    return r.world, r.rank, r.local, r
 
 
 def barrier(ws):
-    if ws > 1:
-        import torch.distributed as dist
-        dist.barrier()
+    par.barrier(RANK)
 
 
 def max_over_ranks(x: float, ws: int) -> float:
-    if ws == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return par.max_over_ranks(x, RANK)
+
+
+RANK = par.Rank(1, 0, 0, None)
 
 
 def frame_bytes(fr) -> int:
@@ -231,8 +220,9 @@ def path_bytes(stats0, stats1, in_bytes, cfg) -> float:
 
 
 def main():
+    global RANK
     args = parse()
-    ws, rank, local = setup_dist()
+    ws, rank, local, RANK = setup_dist()
     if args.impl == "reference":
         run_reference(args, ws, rank)
         return
@@ -245,7 +235,7 @@ def main():
     dev = torch.device("cuda", local)
     F = args.frames_per_step
     # independent scene per rank (weak scaling)
-    g = Generator(args.config, seed=seed_of(args.config) + 7919 * rank, device=dev)
+    g = Generator(args.config, seed=par.stream_seed(seed_of(args.config), rank), device=dev)
     c = g.cfg
     cfg_kw = disc_config_kwargs(c)
     nframes = (args.warmup + args.steps) * F
@@ -376,9 +366,7 @@ def main():
                                 "sample": f"first {n} frames of the same stream (full M2 path), {dt:.1f} s"}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if ws > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
+    par.teardown(RANK)
 
 
 if __name__ == "__main__":

@@ -1,0 +1,71 @@
+"""N > 1 host path on CPU (gloo, world_size 2): rank setup, per-rank scene streams, barrier,
+max-over-ranks timing and the weak-scaling aggregate used by bench.py.  The per-rank workload is
+the CPU oracle on a small generated stream (test infrastructure)."""
+import os
+import socket
+import time
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2603_03935_b200 import parallel as par
+    from synth import Generator, disc_config_kwargs, frame_to_numpy
+    from synth.scenes import seed_of
+    from oracle.oracle import OracleMap
+    r = par.setup("gloo")
+    g = Generator("N", seed=par.stream_seed(seed_of("N"), r.rank), H=60, W=80, Hp=4, Wp=5, fx=72.0, fy=72.0,
+                  cx=40.0, cy=30.0, Df=16, Dt=8)
+    kw = disc_config_kwargs(g.cfg)
+    kw["mask_min_area"] = 10
+    frames = [frame_to_numpy(g.frame(f)) for f in range(3 + r.rank)]   # uneven work per rank
+    om = OracleMap(**kw)
+    par.barrier(r)
+    t0 = time.perf_counter()
+    for fr in frames:
+        om.integrate(fr)
+    dt = time.perf_counter() - t0
+    rate = par.weak_scaling_rate(len(frames), dt, r)
+    mx = par.max_over_ranks(dt, r)
+    keys, ids = om.memberships()
+    q.put((r.rank, rate, mx, dt, len(frames), int(np.bitwise_xor.reduce(keys)) if len(keys) else 0))
+    par.teardown(r)
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_weak_scaling_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=240) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (r0, rate0, mx0, dt0, n0, h0), (r1, rate1, mx1, dt1, n1, h1) = out
+    assert (r0, r1) == (0, 1)
+    assert mx0 == mx1 == max(dt0, dt1)                      # max over ranks
+    assert rate0 == rate1 == pytest.approx((n0 + n1) / max(dt0, dt1))
+    assert h0 != h1                                         # independent scene streams per rank
+
+
+def test_single_rank_defaults():
+    from paper_2603_03935_b200 import parallel as par
+    r = par.Rank(1, 0, 0, None)
+    assert par.max_over_ranks(1.5, r) == 1.5
+    assert par.weak_scaling_rate(10, 2.0, r) == 5.0
+    assert par.stream_seed(100, 0) == 100 and par.stream_seed(100, 3) == 100 + 3 * par.SEED_STRIDE
