@@ -26,7 +26,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -74,42 +73,60 @@ REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_c
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled through NVML DURING the timed region
+    (a polling thread every ~1 ms, plus one sample at entry and one at exit so even a
+    millisecond-long region has readings); nvidia-smi's own polling is too coarse for it."""
 
     def __init__(self, dev: int):
         self.dev = dev
         self.rows = []
-        self.proc = None
+        self.h = None
+        self.stop = threading.Event()
         self.t = None
+
+    def _sample(self):
+        import pynvml
+        sm = pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        try:
+            rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+        self.rows.append((float(sm), float(mx), int(rs)))
+
+    def _loop(self):
+        while not self.stop.wait(0.001):
+            try:
+                self._sample()
+            except Exception:
+                return
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
-                text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            idx = self.dev
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis and vis.split(",")[0].strip().isdigit():
+                idx = int(vis.split(",")[self.dev].strip())
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self._sample()
+            self.t = threading.Thread(target=self._loop, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.h = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 3:
-                try:
-                    self.rows.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
-                except ValueError:
-                    pass
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        if self.h is None:
+            return
+        try:
+            self._sample()
+        except Exception:
+            pass
+        self.stop.set()
+        if self.t:
+            self.t.join(timeout=1)
 
     def summary(self):
         if not self.rows:

@@ -342,6 +342,13 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(W.tok = dalloc<uint8_t>(m, (size_t)win * SM));
   chk(W.pmode = dalloc<uint8_t>(m, (size_t)win * SM));
   }
+  {  // K1 normal-sum scratch, shared by both window buffers (K1 launches are stream-ordered)
+    const int nsmid = k1_nsmid();
+    float4* scr = dalloc<float4>(m, (size_t)nsmid * K1_SLOTS_PER_SM * K1_PT, 0);
+    uint32_t* slot = dalloc<uint32_t>(m, (size_t)nsmid, 0);
+    chk(scr); chk(slot);
+    for (int wbi = 0; wbi < 2; ++wbi) { m->Wb[wbi].k1scr = scr; m->Wb[wbi].k1slot = slot; }
+  }
   // ---- map ----
   MapState& M = m->M;
   const int64_t IM = cfg->max_instances;

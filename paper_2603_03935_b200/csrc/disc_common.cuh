@@ -11,6 +11,8 @@
 namespace disc {
 
 constexpr int MAXWIN = 32;
+constexpr int K1_PT = 512;            // K1 CTA pair-table slots
+constexpr int K1_SLOTS_PER_SM = 16;    // K1 scratch blocks per SM (>= resident K1 CTAs per SM)
 constexpr uint64_t KEY_EMPTY = ~0ull;       // valid packed keys have bit 63 clear (R6)
 constexpr uint32_t U32_EMPTY = 0xFFFFFFFFu;
 constexpr uint32_t LAB_TOMB = 0xFFFFFFFEu;  // membership label removed by a relabel
@@ -99,6 +101,9 @@ struct WinBufs {
   double* trk;                // [win][SMAX][Dt]  t_s
   uint8_t* tok;               // [win][SMAX] t_s defined (nonzero norm)
   uint8_t* pmode;             // [win][SMAX] 1: unweighted pooling fallback (R18)
+  // K1 per-CTA normal-sum scratch: one K1_PT-slot block per resident K1 CTA, acquired per SM
+  float4* k1scr;              // [nsmid][K1_SLOTS_PER_SM][K1_PT], all-zero between CTAs
+  uint32_t* k1slot;           // [nsmid] bitmask of the SM's blocks in use
   int32_t PC;                 // frame table capacity (power of 2)
   int32_t PMAX, SMAX, PMAXP, FCHUNKS;
 };

@@ -8,6 +8,7 @@ namespace disc {
 void debug_check(cudaStream_t st, const char* kernel, int frame);
 void k6_prof_dump();
 void k1_prof_dump();
+int k1_nsmid();   // %nsmid of the current device (upper bound of %smid)
 size_t k1_smem_bytes(int S, int W, int rows_cap);
 int k1_rows_cap(int W);
 size_t k6_smem_bytes(int S, int TC);

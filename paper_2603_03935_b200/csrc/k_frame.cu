@@ -177,15 +177,12 @@ constexpr int K1_TW = 32;                                 // tile columns per wa
 constexpr int K1_TILE_W = K1_WARPS * K1_TW;               // CTA tile: 32 rows x 128 columns
 constexpr int K1_TILE_H = 32;
 constexpr int K1_KT = 512;                                // CTA key table slots
-constexpr int K1_PT = 512;                                // CTA pair table slots
 constexpr int K1_PLIST = 512;
 constexpr int K1_DS = 131;                                // depth tile row stride (130 columns + pad)
-constexpr int K1_MS = 144;                                // mask tile row stride in bytes
-constexpr int K1_NG = 3;                                  // ring slots (plane pairs)
 constexpr uint16_t K1_NOKEY = 0xFFFF;
 
 struct K1Smem {
-  size_t bb, vs, pl, kt, m0, pt, pn, xa, pc, dep, total;
+  size_t bb, vs, pl, kt, m0, pt, xa, pc, dep, total;
   __host__ __device__ K1Smem(int S, bool sem) {
     size_t o = 0;
     auto take = [&](size_t b) { const size_t r = o; o = (o + b + 15) & ~(size_t)15; return r; };
@@ -195,7 +192,6 @@ struct K1Smem {
     kt = take((size_t)K1_KT * 8);
     m0 = take((size_t)8 * K1_THREADS * 4);               // first mask per pixel, 4 per word
     pt = take((size_t)K1_PT * 4);
-    pn = take(sem ? (size_t)K1_PT * 12 : 16);
     xa = take((size_t)(K1_TILE_W + 2) * 4);
     pc = take((size_t)(K1_TILE_W + 2) * 2);
     dep = take((size_t)(K1_TILE_H + 2) * K1_DS * 4);
@@ -220,6 +216,15 @@ __device__ __forceinline__ uint32_t range_bits(int a, int b) {   // bits [a, b),
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, uint32_t src_bytes) {
   const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, uint32_t src_bytes) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes));
+}
+// native vector float reduction at L2 (fire-and-forget; shared-memory float atomics are CAS loops)
+__device__ __forceinline__ void red_add3(float4* p, float a, float b, float c) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(0.f)
+               : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -281,11 +286,10 @@ __global__ void __launch_bounds__(K1_THREADS, 4) k_mask_pass(WinDesc wd, WinBufs
   unsigned long long* kt = (unsigned long long*)(smem_raw + L.kt);   // CTA key table
   uint32_t* m0w = (uint32_t*)(smem_raw + L.m0) + threadIdx.x;        // m0w[word * K1_THREADS]
   uint32_t* pt = (uint32_t*)(smem_raw + L.pt);                       // CTA pair table: (s << 16 | local key)
-  float* ptn = (float*)(smem_raw + L.pn);                            // -> normal sums
   float* xa_s = (float*)(smem_raw + L.xa);            // column c <-> u = ut0 - 1 + c
   uint16_t* pc_s = (uint16_t*)(smem_raw + L.pc);
   float* dep = (float*)(smem_raw + L.dep);            // [34][K1_DS], row r <-> v = vt0 - 1 + r
-  __shared__ uint32_t npl_s, oor_s;
+  __shared__ uint32_t npl_s, oor_s, slot_s;
 
   for (int i = threadIdx.x; i < S; i += blockDim.x) {
     bb_s[4 * i + 0] = INT32_MAX; bb_s[4 * i + 1] = INT32_MAX;
@@ -293,25 +297,41 @@ __global__ void __launch_bounds__(K1_THREADS, 4) k_mask_pass(WinDesc wd, WinBufs
     vs_s[i] = 0;
   }
   for (int i = threadIdx.x; i < K1_KT; i += blockDim.x) kt[i] = KEY_EMPTY;
-  for (int i = threadIdx.x; i < K1_PT; i += blockDim.x) {
-    pt[i] = U32_EMPTY;
-    if (SEM) { ptn[3 * i] = 0.f; ptn[3 * i + 1] = 0.f; ptn[3 * i + 2] = 0.f; }
-  }
+  for (int i = threadIdx.x; i < K1_PT; i += blockDim.x) pt[i] = U32_EMPTY;
   for (int t = 0; t < 8; ++t) m0w[t * K1_THREADS] = 0xFFFFFFFFu;   // no mask yet
   for (int c = threadIdx.x; c < K1_TILE_W + 2; c += blockDim.x) {
     const int u = ut0 - 1 + c;
     xa_s[c] = (u >= 0 && u < W) ? __fdiv_rn(__fsub_rn((float)u, F.cx), F.fx) : 0.f;   // R5
     pc_s[c] = (u >= 0 && u < W) ? (uint16_t)(((int64_t)u * Wp) / W) : 0;            // R17
   }
+  // depth tile (+halo) staged asynchronously; consumed after the mask phase (phase 3).  Outside
+  // the image the tile holds 0, which depth_valid rejects (depth_min >= 0).
   for (int idx = threadIdx.x; idx < (K1_TILE_H + 2) * (K1_TILE_W + 2); idx += blockDim.x) {
     const int r = idx / (K1_TILE_W + 2), c = idx - r * (K1_TILE_W + 2);
     const int vv = vt0 - 1 + r, uu = ut0 - 1 + c;
-    dep[r * K1_DS + c] =
-        (vv >= 0 && vv < H && uu >= 0 && uu < W) ? __ldg(F.depth + (int64_t)vv * W + uu) : __int_as_float(0x7fc00000);
+    const bool in = vv >= 0 && vv < H && uu >= 0 && uu < W;
+    cp_async4(&dep[r * K1_DS + c], in ? (const void*)(F.depth + (int64_t)vv * W + uu) : (const void*)F.depth,
+              in ? 4u : 0u);
   }
-  if (threadIdx.x == 0) { npl_s = 0; oor_s = 0; }
+  cp_async_commit();
+  if (threadIdx.x == 0) {
+    npl_s = 0; oor_s = 0;
+    if (SEM) {   // a scratch block of this SM for the tile's normal sums (released at exit)
+      uint32_t sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      uint32_t* w = wb.k1slot + sm;
+      for (;;) {
+        const uint32_t freeb = ~*(volatile uint32_t*)w & ((1u << K1_SLOTS_PER_SM) - 1u);
+        if (!freeb) continue;
+        const uint32_t b = __ffs(freeb) - 1;
+        if (!(atomicOr(w, 1u << b) & (1u << b))) { slot_s = sm * K1_SLOTS_PER_SM + b; break; }
+      }
+      __threadfence();
+    }
+  }
   __syncthreads();
   K1_PROBE(0);
+  float4* nscr = SEM ? wb.k1scr + (size_t)slot_s * K1_PT : nullptr;
 
   const uint32_t tmask = (uint32_t)wb.PC - 1;
   unsigned long long* ktab = wb.ktab + (size_t)f * wb.PC;
@@ -390,11 +410,7 @@ __global__ void __launch_bounds__(K1_THREADS, 4) k_mask_pass(WinDesc wd, WinBufs
       }
     }
     if (slot >= 0) {
-      if (SEM && (n0 != 0.f || n1 != 0.f || n2 != 0.f)) {
-        atomicAdd(&ptn[3 * slot + 0], n0);
-        atomicAdd(&ptn[3 * slot + 1], n1);
-        atomicAdd(&ptn[3 * slot + 2], n2);
-      }
+      if (SEM && (n0 != 0.f || n1 != 0.f || n2 != 0.f)) red_add3(&nscr[slot], n0, n1, n2);
       return;
     }
     uint64_t key = KEY_EMPTY;
@@ -498,6 +514,7 @@ __global__ void __launch_bounds__(K1_THREADS, 4) k_mask_pass(WinDesc wd, WinBufs
 #pragma unroll
       for (int t = 0; t < 8; ++t) wa[k][t] = wn[k][t];
   }
+  cp_async_wait<0>();
   __syncthreads();
   K1_PROBE(2);
 
@@ -573,6 +590,7 @@ __global__ void __launch_bounds__(K1_THREADS, 4) k_mask_pass(WinDesc wd, WinBufs
     }
   }
   if (lane_on && my_oor) atomicAdd(&oor_s, my_oor);
+  if (SEM) __threadfence();   // this thread's normal reductions before the phase-5 reads
   __syncthreads();
   K1_PROBE(3);
   // ---- 5: the tile's distinct (s, key) pairs -> global frame tables (all threads, many
@@ -582,16 +600,21 @@ __global__ void __launch_bounds__(K1_THREADS, 4) k_mask_pass(WinDesc wd, WinBufs
     if (code == U32_EMPTY) continue;
     const uint32_t s = code >> 16;
     const uint32_t pslot = global_insert(kt[code & 0xFFFFu], s);
-    if (SEM && pslot != U32_EMPTY) {
-      const float n0 = ptn[3 * i], n1 = ptn[3 * i + 1], n2 = ptn[3 * i + 2];
-      if (n0 != 0.f || n1 != 0.f || n2 != 0.f) {
-        atomicAdd(&nsum[3 * pslot + 0], n0);
-        atomicAdd(&nsum[3 * pslot + 1], n1);
-        atomicAdd(&nsum[3 * pslot + 2], n2);
+    if (SEM) {
+      const float4 nn = __ldcg(&nscr[i]);
+      if (nn.x != 0.f || nn.y != 0.f || nn.z != 0.f) {
+        __stcg(&nscr[i], make_float4(0.f, 0.f, 0.f, 0.f));   // leave the block all-zero
+        if (pslot != U32_EMPTY) {
+          atomicAdd(&nsum[3 * pslot + 0], nn.x);
+          atomicAdd(&nsum[3 * pslot + 1], nn.y);
+          atomicAdd(&nsum[3 * pslot + 2], nn.z);
+        }
       }
     }
   }
+  if (SEM) __threadfence();
   __syncthreads();
+  if (SEM && threadIdx.x == 0) atomicAnd(wb.k1slot + slot_s / K1_SLOTS_PER_SM, ~(1u << (slot_s % K1_SLOTS_PER_SM)));
   K1_PROBE(4);
 
   // ---- flush per-mask accumulators ----
@@ -617,6 +640,21 @@ __global__ void __launch_bounds__(K1_THREADS, 4) k_mask_pass(WinDesc wd, WinBufs
   }
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) wb.plist[(size_t)f * wb.PMAX + base_s + i] = pl_s[i];
   K1_PROBE(5);
+}
+
+__global__ void k_nsmid(int* out) {
+  uint32_t n;
+  asm volatile("mov.u32 %0, %%nsmid;" : "=r"(n));
+  *out = (int)n;
+}
+int k1_nsmid() {
+  int* d = nullptr;
+  int h = 0;
+  if (cudaMalloc(&d, sizeof(int)) != cudaSuccess) return 256;
+  k_nsmid<<<1, 1>>>(d);
+  if (cudaMemcpy(&h, d, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess || h <= 0) h = 256;
+  cudaFree(d);
+  return h;
 }
 
 void k1_prof_dump() {
