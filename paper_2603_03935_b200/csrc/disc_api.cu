@@ -25,6 +25,7 @@ struct disc_map {
   disc_config cfg;
   Params P;
   int dev = 0, nsm = 148;
+  int nres = 0;   // SMs reserved for stage 2 (0 = no partition)
   MapState M{};
   WinBufs Wb[2]{};               // double-buffered window buffers (stage 1 of window w+1 overlaps
                                  // stage 2 of window w)
@@ -206,7 +207,36 @@ void collect_events(disc_map* m) {
 }  // namespace
 
 namespace disc {
+// DISC_TIMELINE=1: an event after every launch (profiling aid; nsys is not in this image).
+// tl_dump prints (stream, mark, frame, ms since the first mark) once the work has completed.
+struct TlRec { cudaEvent_t ev; const char* name; int frame; cudaStream_t st; };
+static std::vector<TlRec> g_tl;
+static int tl_on() {
+  static int on = -1;
+  if (on < 0) on = getenv("DISC_TIMELINE") ? 1 : 0;
+  return on;
+}
+void tl_mark(cudaStream_t st, const char* name, int frame) {
+  if (!tl_on()) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, st);
+  g_tl.push_back({e, name, frame, st});
+}
+void tl_dump() {
+  if (!tl_on() || g_tl.empty()) return;
+  cudaDeviceSynchronize();
+  for (const TlRec& r : g_tl) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, g_tl[0].ev, r.ev);
+    std::fprintf(stderr, "TL %p %s %d %.4f\n", (void*)r.st, r.name, r.frame, ms);
+  }
+  for (const TlRec& r : g_tl) cudaEventDestroy(r.ev);
+  g_tl.clear();
+}
+
 void debug_check(cudaStream_t st, const char* kernel, int frame) {
+  tl_mark(st, kernel, frame);
   static int on = -1;
   if (on < 0) on = getenv("DISC_DEBUG_SYNC") ? 1 : 0;
   if (!on) return;
@@ -299,6 +329,11 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   m->cfg = *cfg;
   m->dev = cfg->device;
   m->nsm = prop.multiProcessorCount;
+  {  // stage-2 SM reserve; DISC_S2_SMS overrides it (tuning)
+    const char* e = std::getenv("DISC_S2_SMS");
+    m->nres = e ? std::atoi(e) : 16;
+    m->nres = std::max(0, std::min(m->nres, m->nsm / 2));
+  }
   Params& P = m->P;
   P.r = cfg->voxel_size; P.tau_geo = cfg->tau_geo; P.tau_vis = cfg->tau_vis;
   P.dmin = cfg->depth_min; P.dmax = cfg->depth_max; P.min_conf = cfg->mask_min_conf;
@@ -341,6 +376,8 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(W.trk = dalloc<double>(m, (size_t)win * SM * std::max(Dt, 1)));
   chk(W.tok = dalloc<uint8_t>(m, (size_t)win * SM));
   chk(W.pmode = dalloc<uint8_t>(m, (size_t)win * SM));
+  chk(W.k1ctr = dalloc<uint32_t>(m, 1));
+  chk(W.s2bar = dalloc<uint32_t>(m, 1));
   }
   {  // K1 normal-sum scratch, shared by both window buffers (K1 launches are stream-ordered)
     const int nsmid = k1_nsmid();
@@ -540,13 +577,14 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
       e0 = ev_get(m); e1 = ev_get(m); t0 = ev_get(m); t1 = ev_get(m); t1b = ev_get(m); t2 = ev_get(m);
       cudaEventRecord(t0, s1);
     }
-    m->stats.launches += launch_stage1(wd, Wbuf, m->P, m->d_err, sem, maxS, maxHp, maxW, maxWp, maxP, rows, s1, e0, e1);
+    tl_mark(s1, "s1_begin", -1);
+    m->stats.launches += launch_stage1(wd, Wbuf, m->P, m->d_err, sem, maxS, maxHp, maxW, maxWp, maxP, rows, m->nsm, m->nres, s1, e0, e1);
     if (m->timing) cudaEventRecord(t1, s1);
     cudaEventRecord(m->ev_s1[b], s1);
     cudaStreamWaitEvent(s2, m->ev_s1[b], 0);
     if (m->timing) cudaEventRecord(t1b, s2);
-    for (int i = 0; i < nw; ++i)
-      m->stats.launches += launch_stage2_frame(i, wd.f[i], Wbuf, m->M, m->X, m->P, sem, m->nsm, s2);
+    tl_mark(s2, "s2_begin", -1);
+    m->stats.launches += launch_stage2(wd, Wbuf, m->M, m->X, m->P, sem, m->nsm, m->nres, s2);
     if (m->timing) {
       cudaEventRecord(t2, s2);
       m->ev_pending.push_back({e0, e1, 0});
@@ -637,6 +675,7 @@ disc_status disc_sync(disc_map* m) {
   cudaSetDevice(m->dev);
   if (m->s1) cudaStreamSynchronize(m->s1);
   if (m->s2) cudaStreamSynchronize(m->s2);
+  tl_dump();
   return sync_check(m, m->last_stream);
 }
 
@@ -760,7 +799,7 @@ disc_status disc_get_stats(disc_map* m, disc_stats* s) {
   disc_status st = disc_sync(m);
   if (st != DISC_OK) return st;
   collect_events(m);
-  if (getenv("DISC_K6PROF")) k6_prof_dump();
+  if (getenv("DISC_K6PROF") || getenv("DISC_S2PROF")) k6_prof_dump();
   if (getenv("DISC_K1_ABLATE") && (atoi(getenv("DISC_K1_ABLATE")) & 16)) k1_prof_dump();
   int64_t ctr[8];
   cudaMemcpy(ctr, m->M.counters, sizeof(ctr), cudaMemcpyDeviceToHost);

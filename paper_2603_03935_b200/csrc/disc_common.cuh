@@ -104,6 +104,8 @@ struct WinBufs {
   // K1 per-CTA normal-sum scratch: one K1_PT-slot block per resident K1 CTA, acquired per SM
   float4* k1scr;              // [nsmid][K1_SLOTS_PER_SM][K1_PT], all-zero between CTAs
   uint32_t* k1slot;           // [nsmid] bitmask of the SM's blocks in use
+  uint32_t* k1ctr;            // [1] K1 work-item counter (zeroed by K0)
+  uint32_t* s2bar;            // [1] stage-2 grid barrier counter (zeroed by K0)
   int32_t PC;                 // frame table capacity (power of 2)
   int32_t PMAX, SMAX, PMAXP, FCHUNKS;
 };

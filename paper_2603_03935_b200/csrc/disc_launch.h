@@ -13,10 +13,10 @@ size_t k1_smem_bytes(int S, int W, int rows_cap);
 int k1_rows_cap(int W);
 size_t k6_smem_bytes(int S, int TC);
 int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* err, bool sem, int maxS,
-                  int maxHp, int maxW, int maxWp, int maxP, int rows_cap, cudaStream_t st,
+                  int maxHp, int maxW, int maxWp, int maxP, int rows_cap, int nsm, int nres, cudaStream_t st,
                   cudaEvent_t ev0, cudaEvent_t ev1);
-int launch_stage2_frame(int f, const FrameDesc& F, const WinBufs& wb, const MapState& M,
-                         const FrameScratch& X, const Params& P, bool sem, int nsm, cudaStream_t st);
+int launch_stage2(const WinDesc& wd, const WinBufs& wb, const MapState& M, const FrameScratch& X, const Params& P,
+                  bool sem, int nsm, int nres, cudaStream_t st);
 // export / query
 int64_t export_instances(const MapState& M, int Df, int Dt, int64_t next_id, disc_instance* out,
                          float* embeds, double* track, int32_t cap, cudaStream_t st, void* scratch,

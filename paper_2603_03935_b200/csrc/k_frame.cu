@@ -147,6 +147,7 @@ __global__ void k_win_init(WinDesc wd, WinBufs wb) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     wb.npairs[f] = 0;
     wb.oor[f] = 0;
+    if (f == 0) { *wb.k1ctr = 0; *wb.s2bar = 0; }   // K1's work counter, stage 2's barrier
   }
   // per-patch pixel counts are accumulated with atomics by K1: zero the rows this frame uses
   const int P = wd.f[f].Hp * wd.f[f].Wp;
@@ -171,12 +172,21 @@ __global__ void k_win_init(WinDesc wd, WinBufs wb) {
 //  5 the tile's distinct (s, key) pairs go to the frame's global key / pair tables (all threads),
 //    with their summed normals.
 // ------------------------------------------------------------------------------------------
+#ifndef K1_PERSIST
+#define K1_PERSIST 6   // K1 CTAs per SM (persistent grid)
+#endif
+#ifndef K1_MINB
+#define K1_MINB 6   // resident CTAs per SM the register budget is fitted to
+#endif
 constexpr int K1_THREADS = 128;
 constexpr int K1_WARPS = K1_THREADS / 32;
 constexpr int K1_TW = 32;                                 // tile columns per warp (pixels per lane)
 constexpr int K1_TILE_W = K1_WARPS * K1_TW;               // CTA tile: 32 rows x 128 columns
 constexpr int K1_TILE_H = 32;
-constexpr int K1_KT = 512;                                // CTA key table slots
+#ifndef K1_KT_SLOTS
+#define K1_KT_SLOTS 512
+#endif
+constexpr int K1_KT = K1_KT_SLOTS;                        // CTA key table slots
 constexpr int K1_PLIST = 512;
 constexpr int K1_DS = 131;                                // depth tile row stride (130 columns + pad)
 constexpr uint16_t K1_NOKEY = 0xFFFF;
@@ -255,18 +265,16 @@ __device__ unsigned long long g_k1prof[8];
     }                                                                \
   } while (0)
 
+// one 32 x 128 tile (index `tile`) of frame f; `slot` is the CTA's normal-sum scratch block
 template <bool SEM>
-__global__ void __launch_bounds__(K1_THREADS, 4) k_mask_pass(WinDesc wd, WinBufs wb, Params P, int* err,
-                                                             int rows_cap, int ablate) {
-  (void)rows_cap;
-  const int f = blockIdx.y;
-  if (f >= wd.n) return;
+__device__ __forceinline__ void k1_tile(const WinDesc& wd, const WinBufs& wb, const Params& P, int* err, int f,
+                                        int tile, uint32_t slot, int ablate) {
   const FrameDesc& F = wd.f[f];
   const int H = F.H, W = F.W, S = F.S, Hp = F.Hp, Wp = F.Wp;
   const int64_t HW = (int64_t)H * W;
   const int ntx = (W + K1_TILE_W - 1) / K1_TILE_W, nty = (H + K1_TILE_H - 1) / K1_TILE_H;
-  if ((int)blockIdx.x >= ntx * nty) return;
-  const int ty = blockIdx.x / ntx, tx = blockIdx.x - ty * ntx;
+  if (tile >= ntx * nty) return;
+  const int ty = tile / ntx, tx = tile - ty * ntx;
   const int ut0 = tx * K1_TILE_W, vt0 = ty * K1_TILE_H;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int v = vt0 + lane;                                 // this lane's row
@@ -289,7 +297,7 @@ __global__ void __launch_bounds__(K1_THREADS, 4) k_mask_pass(WinDesc wd, WinBufs
   float* xa_s = (float*)(smem_raw + L.xa);            // column c <-> u = ut0 - 1 + c
   uint16_t* pc_s = (uint16_t*)(smem_raw + L.pc);
   float* dep = (float*)(smem_raw + L.dep);            // [34][K1_DS], row r <-> v = vt0 - 1 + r
-  __shared__ uint32_t npl_s, oor_s, slot_s;
+  __shared__ uint32_t npl_s, oor_s;
 
   for (int i = threadIdx.x; i < S; i += blockDim.x) {
     bb_s[4 * i + 0] = INT32_MAX; bb_s[4 * i + 1] = INT32_MAX;
@@ -314,24 +322,10 @@ __global__ void __launch_bounds__(K1_THREADS, 4) k_mask_pass(WinDesc wd, WinBufs
               in ? 4u : 0u);
   }
   cp_async_commit();
-  if (threadIdx.x == 0) {
-    npl_s = 0; oor_s = 0;
-    if (SEM) {   // a scratch block of this SM for the tile's normal sums (released at exit)
-      uint32_t sm;
-      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-      uint32_t* w = wb.k1slot + sm;
-      for (;;) {
-        const uint32_t freeb = ~*(volatile uint32_t*)w & ((1u << K1_SLOTS_PER_SM) - 1u);
-        if (!freeb) continue;
-        const uint32_t b = __ffs(freeb) - 1;
-        if (!(atomicOr(w, 1u << b) & (1u << b))) { slot_s = sm * K1_SLOTS_PER_SM + b; break; }
-      }
-      __threadfence();
-    }
-  }
+  if (threadIdx.x == 0) { npl_s = 0; oor_s = 0; }
   __syncthreads();
   K1_PROBE(0);
-  float4* nscr = SEM ? wb.k1scr + (size_t)slot_s * K1_PT : nullptr;
+  float4* nscr = SEM ? wb.k1scr + (size_t)slot * K1_PT : nullptr;
 
   const uint32_t tmask = (uint32_t)wb.PC - 1;
   unsigned long long* ktab = wb.ktab + (size_t)f * wb.PC;
@@ -612,9 +606,7 @@ __global__ void __launch_bounds__(K1_THREADS, 4) k_mask_pass(WinDesc wd, WinBufs
       }
     }
   }
-  if (SEM) __threadfence();
   __syncthreads();
-  if (SEM && threadIdx.x == 0) atomicAnd(wb.k1slot + slot_s / K1_SLOTS_PER_SM, ~(1u << (slot_s % K1_SLOTS_PER_SM)));
   K1_PROBE(4);
 
   // ---- flush per-mask accumulators ----
@@ -655,6 +647,41 @@ int k1_nsmid() {
   if (cudaMemcpy(&h, d, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess || h <= 0) h = 256;
   cudaFree(d);
   return h;
+}
+
+// Persistent: K1_PERSIST CTAs per SM pull (frame, tile) items from a counter.  CTAs that land on
+// one of the first `reserve` SMs exit at once, so those SMs stay free for stage 2's per-frame
+// kernels (a latency-bound chain on the map) while K1 streams the masks on the rest.
+template <bool SEM>
+__global__ void __launch_bounds__(K1_THREADS, K1_MINB) k_mask_pass(WinDesc wd, WinBufs wb, Params P, int* err,
+                                                             int tiles_x, int reserve, int ablate) {
+  __shared__ uint32_t slot_s, item_s;
+  uint32_t sm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  if ((int)sm < reserve) return;   // SMs left to stage 2
+  if (SEM && threadIdx.x == 0) {   // a scratch block of this SM for the tiles' normal sums
+    uint32_t* w = wb.k1slot + sm;
+    for (;;) {
+      const uint32_t freeb = ~*(volatile uint32_t*)w & ((1u << K1_SLOTS_PER_SM) - 1u);
+      if (!freeb) continue;
+      const uint32_t b = __ffs(freeb) - 1;
+      if (!(atomicOr(w, 1u << b) & (1u << b))) { slot_s = sm * K1_SLOTS_PER_SM + b; break; }
+    }
+    __threadfence();
+  }
+  const uint32_t total = (uint32_t)tiles_x * (uint32_t)wd.n;
+  for (;;) {
+    if (threadIdx.x == 0) item_s = atomicAdd(wb.k1ctr, 1u);
+    __syncthreads();
+    const uint32_t it = item_s;
+    __syncthreads();
+    if (it >= total) break;
+    k1_tile<SEM>(wd, wb, P, err, (int)(it % (uint32_t)wd.n), (int)(it / (uint32_t)wd.n), slot_s, ablate);
+  }
+  if (SEM && threadIdx.x == 0) {
+    __threadfence();
+    atomicAnd(wb.k1slot + slot_s / K1_SLOTS_PER_SM, ~(1u << (slot_s % K1_SLOTS_PER_SM)));
+  }
 }
 
 void k1_prof_dump() {
@@ -1150,9 +1177,10 @@ int k1_tiles(int H, int W) {
 }
 
 int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* err, bool sem, int maxS,
-                  int maxHp, int maxW, int maxWp, int maxP, int rows_cap, cudaStream_t st,
+                  int maxHp, int maxW, int maxWp, int maxP, int rows_cap, int nsm, int nres, cudaStream_t st,
                   cudaEvent_t ev0, cudaEvent_t ev1) {
   const int n = wd.n;
+  (void)rows_cap;
   int k1_grid = 1;
   for (int i = 0; i < n; ++i) k1_grid = std::max(k1_grid, k1_tiles(wd.f[i].H, wd.f[i].W));
   (void)maxHp; (void)maxWp;
@@ -1162,10 +1190,10 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
   if (ev0) cudaEventRecord(ev0, st);
   if (sem) {
     cudaFuncSetAttribute(k_mask_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
-    k_mask_pass<true><<<dim3(k1_grid, n), K1_THREADS, sm1, st>>>(wd, wb, P, err, rows_cap, k1_ablate());
+    k_mask_pass<true><<<K1_PERSIST * nsm, K1_THREADS, sm1, st>>>(wd, wb, P, err, k1_grid, nres, k1_ablate());
   } else {
     cudaFuncSetAttribute(k_mask_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
-    k_mask_pass<false><<<dim3(k1_grid, n), K1_THREADS, sm1, st>>>(wd, wb, P, err, rows_cap, k1_ablate());
+    k_mask_pass<false><<<K1_PERSIST * nsm, K1_THREADS, sm1, st>>>(wd, wb, P, err, k1_grid, nres, k1_ablate());
   }
   debug_check(st, "k_mask_pass", -1);
   if (ev1) cudaEventRecord(ev1, st);
@@ -1177,24 +1205,32 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
   if (sem) {
     const int nch = (maxP + K3_ROWS - 1) / K3_ROWS;
     k_fbar_part<<<dim3(nch, n), 256, 0, st>>>(wd, wb, P.Df);
+    debug_check(st, "k_fbar_part", -1);
     k_fbar<<<dim3((P.Df + 255) / 256, n), 256, 0, st>>>(wd, wb, P.Df);
+    debug_check(st, "k_fbar", -1);
     k_resid<<<dim3((maxP + 7) / 8, n), 256, 0, st>>>(wd, wb, P.Df);
+    debug_check(st, "k_resid", -1);
     k_dmap<<<n, 1024, 0, st>>>(wd, wb, P);
-    debug_check(st, "k_fbar/k_resid/k_dmap", -1);
+    debug_check(st, "k_dmap", -1);
   }
   const size_t smp = std::max((size_t)K4_WARPS * P.Df * 4, (size_t)K4_WARPS * std::max(P.Dt, 1) * 8);
   cudaFuncSetAttribute(k_pool<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);
   cudaFuncSetAttribute(k_pool<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);
   if (sem) {
     k_filter<true><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
+    debug_check(st, "k_filter", -1);
     k_pool<true><<<dim3(K4_CTAS, maxS, n), K4_THREADS, smp, st>>>(wd, wb, P);
+    debug_check(st, "k_pool", -1);
     k_finalize<true><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
+    debug_check(st, "k_finalize", -1);
   } else {
     k_filter<false><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
+    debug_check(st, "k_filter", -1);
     k_pool<false><<<dim3(K4_CTAS, maxS, n), K4_THREADS, smp, st>>>(wd, wb, P);
+    debug_check(st, "k_pool", -1);
     k_finalize<false><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
+    debug_check(st, "k_finalize", -1);
   }
-  debug_check(st, "k_filter/k_pool/k_finalize", -1);
   return sem ? 10 : 6;
 }
 

@@ -16,7 +16,9 @@
 #include "disc_common.cuh"
 #include "disc_launch.h"
 
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 namespace disc {
 
@@ -134,7 +136,7 @@ __device__ __forceinline__ void count_add(const FrameScratch& X, uint64_t code, 
   raise_err(err, DERR_TRIPLES);
 }
 
-__global__ void __launch_bounds__(256) k_lookup(int f, WinBufs wb, MapState M, FrameScratch X) {
+__device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapState& M, const FrameScratch& X) {
   const uint32_t np = min(wb.npairs[f], (uint32_t)wb.PMAX);
   const size_t fo = (size_t)f * wb.PMAX;
   const int lane = threadIdx.x & 31;
@@ -248,6 +250,7 @@ struct K6Smem {   // offsets into dynamic shared memory
 
 // DISC_K6PROF: phase timestamps of the association kernel (profiling aid)
 __device__ unsigned long long g_k6prof[16];
+__device__ unsigned long long g_s2prof[8];   // DISC_S2PROF phase sums
 #define K6_PROBE(i)                                                                          \
   do {                                                                                       \
     if (threadIdx.x == 0) {                                                                  \
@@ -258,8 +261,8 @@ __device__ unsigned long long g_k6prof[16];
     }                                                                                        \
   } while (0)
 
-__global__ void __launch_bounds__(K6_THREADS) k_assoc(int f, FrameDesc F, WinBufs wb, MapState M,
-                                                      FrameScratch X, Params P, int sem) {
+__device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBufs& wb, const MapState& M,
+                                         const FrameScratch& X, const Params& P, int sem) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int TC = X.TCAP;
   const int S = F.S;
@@ -698,10 +701,10 @@ __device__ void apply_target(int t, int f, const FrameDesc& F, const WinBufs& wb
   }
 }
 
-__global__ void __launch_bounds__(K7_T) k_apply(int f, FrameDesc F, WinBufs wb, MapState M, FrameScratch X, Params P,
-                                               int sem) {
-  if ((int)blockIdx.x < *X.ntgt) {
-    apply_target(blockIdx.x, f, F, wb, M, X, P, sem);
+__device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBufs& wb, const MapState& M,
+                                         const FrameScratch& X, const Params& P, int sem) {
+  for (int t = blockIdx.x; t < *X.ntgt; t += gridDim.x) {
+    apply_target(t, f, F, wb, M, X, P, sem);
     __syncthreads();
   }
   const uint32_t np = min(wb.npairs[f], (uint32_t)wb.PMAX);
@@ -767,15 +770,15 @@ __global__ void __launch_bounds__(K7_T) k_apply(int f, FrameDesc F, WinBufs wb, 
 }
 
 // K7b: per target — |V| update and list growth
-__global__ void __launch_bounds__(256) k_grow(int f, MapState M, FrameScratch X) {
+__device__ __forceinline__ void s2_grow(int f, const MapState& M, const FrameScratch& X) {
   const int ntgt = *X.ntgt;
-  const int t = blockIdx.x;
-  if (t == 0 && threadIdx.x == 0) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     disc_frame_report& R = X.rep[f];
     R.live_memberships = M.counters[2];
     R.new_memberships = M.counters[2] - *X.live_before;
   }
-  if (t >= ntgt) return;
+  for (int t = blockIdx.x; t < ntgt; t += gridDim.x) {
+  __syncthreads();
   const uint32_t L = X.tgt_phys[t];
   const uint32_t root = X.tgt_root[t];
   const uint32_t add = X.tgt_stage[t];
@@ -811,10 +814,11 @@ __global__ void __launch_bounds__(256) k_grow(int f, MapState M, FrameScratch X)
     M.lst_len[L] = oldlen + add;
     atomicAdd((unsigned long long*)&M.counters[5], (unsigned long long)add);
   }
+  }
 }
 
 // K7c: fill the appended list cells (warp-aggregated positions)
-__global__ void __launch_bounds__(256) k_fill(MapState M, FrameScratch X) {
+__device__ __forceinline__ void s2_fill(const MapState& M, const FrameScratch& X) {
   const uint32_t n = min(*X.nstage, X.STCAP);
   const int lane = threadIdx.x & 31;
   const uint32_t stride = gridDim.x * blockDim.x;
@@ -837,6 +841,11 @@ __global__ void __launch_bounds__(256) k_fill(MapState M, FrameScratch X) {
 size_t k6_smem_bytes(int S, int TC) { return K6Smem(S, TC).total; }
 
 void k6_prof_dump() {
+  if (getenv("DISC_S2PROF")) {
+    unsigned long long g[8];
+    cudaMemcpyFromSymbol(g, g_s2prof, sizeof(g));
+    fprintf(stderr, "s2 phase ns: lookup %llu assoc %llu apply %llu grow %llu fill %llu\n", g[0], g[1], g[2], g[3], g[4]);
+  }
   unsigned long long h[16];
   cudaMemcpyFromSymbol(h, g_k6prof, sizeof(h));
   fprintf(stderr, "k6 phase ns (cumulative):");
@@ -844,21 +853,71 @@ void k6_prof_dump() {
   fprintf(stderr, "\n");
 }
 
-int launch_stage2_frame(int f, const FrameDesc& F, const WinBufs& wb, const MapState& M, const FrameScratch& X,
-                        const Params& P, bool sem, int nsm, cudaStream_t st) {
-  k_lookup<<<2 * nsm, 256, 0, st>>>(f, wb, M, X);
-  debug_check(st, "k_lookup", f);
+// Grid-wide barrier of the persistent stage-2 kernel (all CTAs co-resident: the grid is sized to
+// the SMs K1 leaves free, one CTA per SM).  Monotonic counter, zeroed by K0 for the window.
+__device__ __forceinline__ void grid_sync(uint32_t* bar, uint32_t target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    uint32_t v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Stage 2 of a window: the frames' map updates in order, five grid-synchronised phases per frame
+// (K5 lookup, K6 association on CTA 0, K7a apply, K7b grow, K7c fill) in one persistent launch.
+__global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb, MapState M, FrameScratch X,
+                                                        Params P, int sem, int prof) {
+  const uint32_t G = gridDim.x;
+  uint32_t ep = 0;
+  unsigned long long t_prev = 0;
+  auto probe = [&](int i) {   // DISC_S2PROF: phase durations on CTA 0 (profiling aid)
+    if (prof && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      if (i >= 0) atomicAdd(&g_s2prof[i], t_ - t_prev);
+      t_prev = t_;
+    }
+  };
+  probe(-1);
+  for (int f = 0; f < wd.n; ++f) {
+    const FrameDesc& F = wd.f[f];
+    s2_lookup(f, wb, M, X);
+    grid_sync(wb.s2bar, G * ++ep);
+    probe(0);
+    if (blockIdx.x == 0) s2_assoc(f, F, wb, M, X, P, sem);
+    grid_sync(wb.s2bar, G * ++ep);
+    probe(1);
+    s2_apply(f, F, wb, M, X, P, sem);
+    grid_sync(wb.s2bar, G * ++ep);
+    probe(2);
+    s2_grow(f, M, X);
+    grid_sync(wb.s2bar, G * ++ep);
+    probe(3);
+    s2_fill(M, X);
+    grid_sync(wb.s2bar, G * ++ep);
+    probe(4);
+  }
+}
+
+int launch_stage2(const WinDesc& wd, const WinBufs& wb, const MapState& M, const FrameScratch& X, const Params& P,
+                  bool sem, int nsm, int nres, cudaStream_t st) {
   const size_t sm6 = k6_smem_bytes(wb.SMAX, X.TCAP);
-  cudaFuncSetAttribute(k_assoc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm6);
-  k_assoc<<<1, K6_THREADS, sm6, st>>>(f, F, wb, M, X, P, sem ? 1 : 0);
-  debug_check(st, "k_assoc", f);
-  k_apply<<<2 * nsm, K7_T, 0, st>>>(f, F, wb, M, X, P, sem ? 1 : 0);
-  debug_check(st, "k_apply", f);
-  k_grow<<<wb.SMAX, 256, 0, st>>>(f, M, X);
-  debug_check(st, "k_grow", f);
-  k_fill<<<nsm, 256, 0, st>>>(M, X);
-  debug_check(st, "k_fill", f);
-  return 5;
+  static size_t set_for = 0;
+  if (set_for != sm6) {
+    cudaFuncSetAttribute(k_stage2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm6);
+    set_for = sm6;
+  }
+  const int grid = nres > 0 ? nres : std::min(16, nsm);
+  static const int prof = getenv("DISC_S2PROF") ? 1 : 0;
+  k_stage2<<<grid, K6_THREADS, sm6, st>>>(wd, wb, M, X, P, sem ? 1 : 0, prof);
+  debug_check(st, "k_stage2", -1);
+  return 1;
 }
 
 }  // namespace disc

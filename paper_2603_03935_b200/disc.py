@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdisc.so")
+# DISC_LIB_VARIANT: path of an alternative in-tree libdisc build (kernel-tuning experiments)
+LIB_PATH = os.environ.get("DISC_LIB_VARIANT") or os.path.join(_HERE, "libdisc.so")
 
 DISC_OK, DISC_ERR_INVALID, DISC_ERR_INTERNAL, DISC_ERR_CAPACITY, DISC_ERR_CUDA = 0, 2, 4, 5, 6
 STATUS_NAMES = {0: "kept", 1: "area", 2: "conf", 3: "aspect", 4: "nodepth", 5: "nofeat"}
