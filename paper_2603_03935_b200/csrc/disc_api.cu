@@ -156,8 +156,7 @@ std::string validate_frame(const disc_map* m, const disc_frame& f, bool host) {
       !std::isfinite(f.cy))
     return "bad intrinsics";
   if (!pose_rigid(f.pose)) return "non-rigid pose";
-  if (k1_smem_bytes(c.max_masks, f.width, k1_rows_cap(f.width)) > 227 * 1024)
-    return "frame too wide for the mask-pass tile";
+  if (f.height > 16384 || f.width > 16384) return "frame dimension above 16384";
   (void)host;
   return "";
 }
@@ -376,7 +375,11 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(W.trk = dalloc<double>(m, (size_t)win * SM * std::max(Dt, 1)));
   chk(W.tok = dalloc<uint8_t>(m, (size_t)win * SM));
   chk(W.pmode = dalloc<uint8_t>(m, (size_t)win * SM));
-  chk(W.k1ctr = dalloc<uint32_t>(m, 1));
+  chk(W.k1ctr = dalloc<uint32_t>(m, 2));
+  W.MPIX = ((int64_t)cfg->max_pixels + 31) / 32 * 32;   // flat per-frame maps, sector-aligned
+  W.MOVF = W.MPIX / 32;
+  chk(W.m0map = dalloc<uint8_t>(m, (size_t)win * W.MPIX));
+  chk(W.ovfmap = dalloc<uint32_t>(m, (size_t)win * W.MOVF));
   chk(W.s2bar = dalloc<uint32_t>(m, 1));
   }
   {  // K1 normal-sum scratch, shared by both window buffers (K1 launches are stream-ordered)
@@ -565,7 +568,6 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
       maxW = std::max(maxW, f.width);
       maxWp = std::max(maxWp, f.patch_w);
       maxP = std::max(maxP, f.patch_h * f.patch_w);
-      rows = std::max(rows, k1_rows_cap(f.width));
       sem = sem || f.patch_feats != nullptr;
       m->stats.mask_bytes += (int64_t)f.height * f.width * f.num_masks;
       m->stats.depth_bytes += (int64_t)f.height * f.width * 4;
@@ -800,7 +802,6 @@ disc_status disc_get_stats(disc_map* m, disc_stats* s) {
   if (st != DISC_OK) return st;
   collect_events(m);
   if (getenv("DISC_K6PROF") || getenv("DISC_S2PROF")) k6_prof_dump();
-  if (getenv("DISC_K1_ABLATE") && (atoi(getenv("DISC_K1_ABLATE")) & 16)) k1_prof_dump();
   int64_t ctr[8];
   cudaMemcpy(ctr, m->M.counters, sizeof(ctr), cudaMemcpyDeviceToHost);
   m->stats.pairs = ctr[4];

@@ -11,7 +11,7 @@
 namespace disc {
 
 constexpr int MAXWIN = 32;
-constexpr int K1_PT = 512;            // K1 CTA pair-table slots
+constexpr int K1_PT = 1024;           // K1 CTA pair slots (two per CTA key-table slot)
 constexpr int K1_SLOTS_PER_SM = 16;    // K1 scratch blocks per SM (>= resident K1 CTAs per SM)
 constexpr uint64_t KEY_EMPTY = ~0ull;       // valid packed keys have bit 63 clear (R6)
 constexpr uint32_t U32_EMPTY = 0xFFFFFFFFu;
@@ -104,7 +104,10 @@ struct WinBufs {
   // K1 per-CTA normal-sum scratch: one K1_PT-slot block per resident K1 CTA, acquired per SM
   float4* k1scr;              // [nsmid][K1_SLOTS_PER_SM][K1_PT], all-zero between CTAs
   uint32_t* k1slot;           // [nsmid] bitmask of the SM's blocks in use
-  uint32_t* k1ctr;            // [1] K1 work-item counter (zeroed by K0)
+  uint32_t* k1ctr;            // [2] K1a / K1b work-item counters (zeroed by K0)
+  uint8_t* m0map;             // [win][MPIX] first mask per pixel (0xFF none), written by K1a
+  uint32_t* ovfmap;           // [win][MOVF] per row, bit per pixel: in a second mask (R9)
+  int64_t MPIX, MOVF;
   uint32_t* s2bar;            // [1] stage-2 grid barrier counter (zeroed by K0)
   int32_t PC;                 // frame table capacity (power of 2)
   int32_t PMAX, SMAX, PMAXP, FCHUNKS;

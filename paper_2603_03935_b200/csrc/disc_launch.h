@@ -7,10 +7,7 @@ namespace disc {
 // aid for device faults; off by default).
 void debug_check(cudaStream_t st, const char* kernel, int frame);
 void k6_prof_dump();
-void k1_prof_dump();
 int k1_nsmid();   // %nsmid of the current device (upper bound of %smid)
-size_t k1_smem_bytes(int S, int W, int rows_cap);
-int k1_rows_cap(int W);
 size_t k6_smem_bytes(int S, int TC);
 int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* err, bool sem, int maxS,
                   int maxHp, int maxW, int maxWp, int maxP, int rows_cap, int nsm, int nres, cudaStream_t st,

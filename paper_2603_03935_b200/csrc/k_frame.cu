@@ -147,7 +147,7 @@ __global__ void k_win_init(WinDesc wd, WinBufs wb) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     wb.npairs[f] = 0;
     wb.oor[f] = 0;
-    if (f == 0) { *wb.k1ctr = 0; *wb.s2bar = 0; }   // K1's work counter, stage 2's barrier
+    if (f == 0) { wb.k1ctr[0] = 0; wb.k1ctr[1] = 0; *wb.s2bar = 0; }   // K1a/K1b work counters, stage-2 barrier
   }
   // per-patch pixel counts are accumulated with atomics by K1: zero the rows this frame uses
   const int P = wd.f[f].Hp * wd.f[f].Wp;
@@ -158,87 +158,78 @@ __global__ void k_win_init(WinDesc wd, WinBufs wb) {
 }
 
 // ------------------------------------------------------------------------------------------
-// K1: mask pass.  2-D tiles: a CTA owns 32 rows x 128 columns of one frame, a warp 32 rows x 32
-// columns (lane = row, 32 consecutive pixels per lane).  The tile's depth (+1-pixel halo) is
-// staged in shared memory; uniform phases:
-//  1 patch segments of the lane's chunk (R17).
-//  2 masks: every plane streamed once (32 bytes per lane, evict-first in L2, the next plane pair
-//    in flight); branch-free byte SIMD records each pixel's first mask (m0) and flags pixels in a
-//    second mask; per-patch counts by popc over patch segments; bbox from ffs/clz.
-//  3 one sliding window over the lane's pixels: pinned keys (R5), key runs, (m0, run) items,
-//    pixel normals (R21, semantic mode); each item goes into the CTA pair table (32-bit code
-//    (s, local key index from the CTA key table)).
-//  4 pixels in more than one mask (R9) re-read their other planes (slow path).
-//  5 the tile's distinct (s, key) pairs go to the frame's global key / pair tables (all threads),
-//    with their summed normals.
+// K1: the mask pass, in two kernels over the same 32-row x 128-column tiles (persistent grids
+// pulling (frame, tile) items from counters; CTAs that land on one of the first `reserve` SMs
+// exit at once, leaving those SMs to stage 2):
+//  K1a k_masks  streams every mask plane once (a lane owns 32 consecutive pixels of a row; the
+//               four lanes 4r..4r+3 of a warp cover one tile row, so every warp load is whole
+//               128-byte lines; four planes in flight): each pixel's first mask m0 and an "in a
+//               second mask" bit go to HBM maps; per-patch pixel counts (R17) and bboxes.
+//  K1b k_walk   lane = column, one row per step: depth -> pinned world point and key (R5), each
+//               world point computed once (row below computed ahead, row above kept, left/right
+//               from the adjacent lanes); runs of equal (m0, key) along the row are found with a
+//               ballot, their pixel normals (R21) summed by a segmented shuffle scan, and the run's
+//               last lane emits the (s, key) item into the CTA key / pair tables.  Pixels in more
+//               than one mask (R9) emit their other masks per pixel.  The tile's distinct pairs
+//               then go to the frame's key / pair tables.
 // ------------------------------------------------------------------------------------------
-#ifndef K1_PERSIST
-#define K1_PERSIST 6   // K1 CTAs per SM (persistent grid)
+#ifndef K1A_PERSIST
+#define K1A_PERSIST 6
 #endif
-#ifndef K1_MINB
-#define K1_MINB 6   // resident CTAs per SM the register budget is fitted to
+#ifndef K1B_PERSIST
+#define K1B_PERSIST 8
+#endif
+#ifndef K1_NF
+#define K1_NF 4   // mask planes in flight per lane (K1a)
 #endif
 constexpr int K1_THREADS = 128;
 constexpr int K1_WARPS = K1_THREADS / 32;
-constexpr int K1_TW = 32;                                 // tile columns per warp (pixels per lane)
+constexpr int K1_TW = 32;                                 // tile columns per warp
 constexpr int K1_TILE_W = K1_WARPS * K1_TW;               // CTA tile: 32 rows x 128 columns
 constexpr int K1_TILE_H = 32;
-#ifndef K1_KT_SLOTS
-#define K1_KT_SLOTS 512
-#endif
-constexpr int K1_KT = K1_KT_SLOTS;                        // CTA key table slots
+constexpr int K1_KT = K1_PT / 2;                          // CTA key table slots (2 pair slots each)
 constexpr int K1_PLIST = 512;
-constexpr int K1_DS = 131;                                // depth tile row stride (130 columns + pad)
 constexpr uint16_t K1_NOKEY = 0xFFFF;
 
-struct K1Smem {
-  size_t bb, vs, pl, kt, m0, pt, xa, pc, dep, total;
-  __host__ __device__ K1Smem(int S, bool sem) {
-    size_t o = 0;
-    auto take = [&](size_t b) { const size_t r = o; o = (o + b + 15) & ~(size_t)15; return r; };
-    bb = take((size_t)S * 16);
-    vs = take((size_t)S * 4);
-    pl = take((size_t)K1_PLIST * 4);
-    kt = take((size_t)K1_KT * 8);
-    m0 = take((size_t)8 * K1_THREADS * 4);               // first mask per pixel, 4 per word
-    pt = take((size_t)K1_PT * 4);
-    xa = take((size_t)(K1_TILE_W + 2) * 4);
-    pc = take((size_t)(K1_TILE_W + 2) * 2);
-    dep = take((size_t)(K1_TILE_H + 2) * K1_DS * 4);
-    total = o;
-  }
-};
-
+#ifndef K1_MASK_L2
+#define K1_MASK_L2 0   // 0: L2 evict_first, 1: default policy, 2: default + 256-B prefetch
+#endif
 __device__ __forceinline__ void ld_stream32(const uint8_t* p, uint32_t r[8]) {
+#if K1_MASK_L2 == 0
   asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                : "l"(p));
+#elif K1_MASK_L2 == 1
+  asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+#else
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+#endif
 }
-
-__device__ __forceinline__ uint32_t nz_bits4(uint32_t w) {   // bit b set iff byte b of w != 0
-  return ((__vcmpne4(w, 0u) & 0x08040201u) * 0x01010101u) >> 24;
+__device__ __forceinline__ uint4 ld_mask16(const uint8_t* p) {
+  uint4 r;
+#if K1_MASK_L2 == 1
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+#else
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+#endif
+  return r;
 }
 
 __device__ __forceinline__ uint32_t range_bits(int a, int b) {   // bits [a, b), 0 <= a < b <= 32
   return (b >= 32 ? 0xFFFFFFFFu : ((1u << b) - 1u)) & ~((1u << a) - 1u);
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, uint32_t src_bytes) {
-  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, uint32_t src_bytes) {
-  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes));
-}
 // native vector float reduction at L2 (fire-and-forget; shared-memory float atomics are CAS loops)
 __device__ __forceinline__ void red_add3(float4* p, float a, float b, float c) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(0.f)
                : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // R21: n = (P(u+1,v) - P(u-1,v)) x (P(u,v+1) - P(u,v-1)), oriented so n . (cam - P) >= 0.
 __device__ __forceinline__ bool normal_from(const FrameDesc& F, const float pc[3], const float pl[3],
@@ -254,384 +245,423 @@ __device__ __forceinline__ bool normal_from(const FrameDesc& F, const float pc[3
   return true;
 }
 
-__device__ unsigned long long g_k1prof[8];
-#define K1_PROBE(i)                                                  \
-  do {                                                               \
-    if ((ablate & 16) && threadIdx.x == 0) {                         \
-      unsigned long long t_;                                         \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));          \
-      atomicAdd(&g_k1prof[i], t_ - t_prev);                          \
-      t_prev = t_;                                                   \
-    }                                                                \
-  } while (0)
+__device__ __forceinline__ bool on_reserved_sm(int reserve) {
+  uint32_t sm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  return (int)sm < reserve;
+}
 
-// one 32 x 128 tile (index `tile`) of frame f; `slot` is the CTA's normal-sum scratch block
-template <bool SEM>
-__device__ __forceinline__ void k1_tile(const WinDesc& wd, const WinBufs& wb, const Params& P, int* err, int f,
-                                        int tile, uint32_t slot, int ablate) {
-  const FrameDesc& F = wd.f[f];
-  const int H = F.H, W = F.W, S = F.S, Hp = F.Hp, Wp = F.Wp;
-  const int64_t HW = (int64_t)H * W;
-  const int ntx = (W + K1_TILE_W - 1) / K1_TILE_W, nty = (H + K1_TILE_H - 1) / K1_TILE_H;
-  if (tile >= ntx * nty) return;
-  const int ty = tile / ntx, tx = tile - ty * ntx;
-  const int ut0 = tx * K1_TILE_W, vt0 = ty * K1_TILE_H;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int v = vt0 + lane;                                 // this lane's row
-  const int u0 = ut0 + warp * K1_TW;                        // first column of the lane's chunk
-  const int c0 = warp * K1_TW + 1;                          // its column in the staged tiles
-  const bool lane_on = v < H && u0 < W;
-  const int nin = lane_on ? min(K1_TW, W - u0) : 0;
-  const uint32_t inb = nin >= 32 ? 0xFFFFFFFFu : ((1u << nin) - 1u);
-
-  unsigned long long t_prev = 0;
-  if ((ablate & 16) && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_prev));
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const K1Smem L(S, SEM);
-  int32_t* bb_s = (int32_t*)(smem_raw + L.bb);
-  uint32_t* vs_s = (uint32_t*)(smem_raw + L.vs);
-  uint32_t* pl_s = (uint32_t*)(smem_raw + L.pl);
-  unsigned long long* kt = (unsigned long long*)(smem_raw + L.kt);   // CTA key table
-  uint32_t* m0w = (uint32_t*)(smem_raw + L.m0) + threadIdx.x;        // m0w[word * K1_THREADS]
-  uint32_t* pt = (uint32_t*)(smem_raw + L.pt);                       // CTA pair table: (s << 16 | local key)
-  float* xa_s = (float*)(smem_raw + L.xa);            // column c <-> u = ut0 - 1 + c
-  uint16_t* pc_s = (uint16_t*)(smem_raw + L.pc);
-  float* dep = (float*)(smem_raw + L.dep);            // [34][K1_DS], row r <-> v = vt0 - 1 + r
-  __shared__ uint32_t npl_s, oor_s;
-
-  for (int i = threadIdx.x; i < S; i += blockDim.x) {
-    bb_s[4 * i + 0] = INT32_MAX; bb_s[4 * i + 1] = INT32_MAX;
-    bb_s[4 * i + 2] = -1; bb_s[4 * i + 3] = -1;
-    vs_s[i] = 0;
-  }
-  for (int i = threadIdx.x; i < K1_KT; i += blockDim.x) kt[i] = KEY_EMPTY;
-  for (int i = threadIdx.x; i < K1_PT; i += blockDim.x) pt[i] = U32_EMPTY;
-  for (int t = 0; t < 8; ++t) m0w[t * K1_THREADS] = 0xFFFFFFFFu;   // no mask yet
-  for (int c = threadIdx.x; c < K1_TILE_W + 2; c += blockDim.x) {
-    const int u = ut0 - 1 + c;
-    xa_s[c] = (u >= 0 && u < W) ? __fdiv_rn(__fsub_rn((float)u, F.cx), F.fx) : 0.f;   // R5
-    pc_s[c] = (u >= 0 && u < W) ? (uint16_t)(((int64_t)u * Wp) / W) : 0;            // R17
-  }
-  // depth tile (+halo) staged asynchronously; consumed after the mask phase (phase 3).  Outside
-  // the image the tile holds 0, which depth_valid rejects (depth_min >= 0).
-  for (int idx = threadIdx.x; idx < (K1_TILE_H + 2) * (K1_TILE_W + 2); idx += blockDim.x) {
-    const int r = idx / (K1_TILE_W + 2), c = idx - r * (K1_TILE_W + 2);
-    const int vv = vt0 - 1 + r, uu = ut0 - 1 + c;
-    const bool in = vv >= 0 && vv < H && uu >= 0 && uu < W;
-    cp_async4(&dep[r * K1_DS + c], in ? (const void*)(F.depth + (int64_t)vv * W + uu) : (const void*)F.depth,
-              in ? 4u : 0u);
-  }
-  cp_async_commit();
-  if (threadIdx.x == 0) { npl_s = 0; oor_s = 0; }
+// next (frame, tile) item of a persistent K1 grid; CTA-uniform, -1 when done
+__device__ __forceinline__ int next_item(uint32_t* ctr, uint32_t total, uint32_t* item_s) {
+  __syncthreads();   // the previous item's shared state is no longer read
+  if (threadIdx.x == 0) *item_s = atomicAdd(ctr, 1u);
   __syncthreads();
-  K1_PROBE(0);
-  float4* nscr = SEM ? wb.k1scr + (size_t)slot * K1_PT : nullptr;
+  const uint32_t it = *item_s;
+  return it < total ? (int)it : -1;
+}
 
-  const uint32_t tmask = (uint32_t)wb.PC - 1;
-  unsigned long long* ktab = wb.ktab + (size_t)f * wb.PC;
-  uint32_t* ptab = wb.ptab + (size_t)f * wb.PC;
-  float* nsum = wb.nsum + (size_t)f * wb.PC * 3;
-  uint32_t* cnt_g = wb.cnt + (size_t)f * wb.SMAX * wb.PMAXP;
-  const float r = P.r;
-  const float rinv = 1.0f / P.r;   // only used by floor_div_pinned's exact fast path
-  const float ybv = __fdiv_rn(__fsub_rn((float)v, F.cy), F.fy);        // R5 per row
-  const float ybu = __fdiv_rn(__fsub_rn((float)(v - 1), F.cy), F.fy);
-  const float ybd = __fdiv_rn(__fsub_rn((float)(v + 1), F.cy), F.fy);
-  const int prow = lane_on ? (int)(((int64_t)v * Hp) / H) * Wp : 0;
+// ---- K1a ----------------------------------------------------------------------------------
+// The frame is taken as one flat pixel array: lane l of an item owns the 32-byte sector
+// [32 k, 32 k + 32) of every mask plane (k = item * 128 + thread), so a warp load is 1 KB of
+// consecutive, aligned bytes.  A sector may cross row ends; rows and patches are recovered per
+// sector only for the planes that touch it.
+constexpr int K1A_SECT = K1_THREADS;   // sectors per item
 
-  auto wp_tile = [&](int dr, int c, float p[3]) -> bool {   // staged pixel (row v + dr, column c)
-    const float d = dep[(lane + 1 + dr) * K1_DS + c];
-    if (!depth_valid(d, P)) return false;
-    world_point(F, xa_s[c], dr < 0 ? ybu : (dr > 0 ? ybd : ybv), d, p);
-    return true;
-  };
-  auto pixel_normal = [&](int c, float n[3]) -> bool {   // R21 for pixel (v, ut0 - 1 + c)
-    const int u = ut0 - 1 + c;
-    if (u < 1 || u + 1 >= W || v < 1 || v + 1 >= H) return false;
-    float pc[3], pl[3], pr[3], pu[3], pd[3];
-    if (!wp_tile(0, c, pc) || !wp_tile(0, c - 1, pl) || !wp_tile(0, c + 1, pr) || !wp_tile(-1, c, pu) ||
-        !wp_tile(1, c, pd))
-      return false;
-    return normal_from(F, pc, pl, pr, pu, pd, n);
-  };
-  auto kt_insert = [&](uint64_t key) -> uint16_t {   // CTA key table -> local key index
-    uint32_t h = (uint32_t)mix64(key) & (K1_KT - 1);
-    for (int probe = 0; probe < K1_KT; ++probe) {
-      const unsigned long long cur = kt[h];
-      if (cur == key) return (uint16_t)h;
-      if (cur == KEY_EMPTY) {
-        const unsigned long long old = atomicCAS(&kt[h], KEY_EMPTY, (unsigned long long)key);
-        if (old == KEY_EMPTY || old == key) return (uint16_t)h;
-      }
-      h = (h + 1) & (K1_KT - 1);
+template <bool VEC>
+__global__ void __launch_bounds__(K1_THREADS, K1A_PERSIST) k_masks(WinDesc wd, WinBufs wb, int items_f, int reserve,
+                                                                  int ablate) {
+  if (on_reserved_sm(reserve)) return;
+  extern __shared__ int32_t bb_s[];          // [S][4] umin, vmin, umax, vmax
+  __shared__ uint32_t item_s;
+  const uint32_t total = (uint32_t)items_f * (uint32_t)wd.n;
+  for (int it; (it = next_item(wb.k1ctr, total, &item_s)) >= 0;) {
+    const int f = it / items_f, item = it % items_f;   // frame-major
+    const FrameDesc& F = wd.f[f];
+    const int H = F.H, W = F.W, S = F.S, Hp = F.Hp, Wp = F.Wp;
+    const int64_t HW = (int64_t)H * W;
+    if ((int64_t)item * K1A_SECT * 32 >= HW) continue;
+    for (int i = threadIdx.x; i < S; i += blockDim.x) {
+      bb_s[4 * i + 0] = INT32_MAX; bb_s[4 * i + 1] = INT32_MAX;
+      bb_s[4 * i + 2] = -1; bb_s[4 * i + 3] = -1;
     }
-    return K1_NOKEY;
-  };
-  auto global_insert = [&](uint64_t key, uint32_t s) -> uint32_t {
-    const uint32_t kslot = ktab_insert(ktab, tmask, key, err);
-    if (kslot == U32_EMPTY) return U32_EMPTY;
-    bool fresh = false;
-    const uint32_t pslot = ptab_insert(ptab, tmask, (s << 24) | kslot, &fresh, err);
-    if (pslot != U32_EMPTY && fresh) {
-      atomicAdd(&vs_s[s], 1u);
-      const uint32_t li = atomicAdd(&npl_s, 1u);
-      if (li < K1_PLIST) {
-        pl_s[li] = pslot;
+    __syncthreads();
+    const int64_t p0 = ((int64_t)item * K1A_SECT + threadIdx.x) * 32;   // first pixel of the sector
+    const int nv = p0 < HW ? (int)min((int64_t)32, HW - p0) : 0;
+    const uint32_t inb = nv >= 32 ? 0xFFFFFFFFu : ((1u << nv) - 1u);
+    // 32-bit index arithmetic: H, W <= 16384 (validated), so every product below is < 2^31
+    const int v0 = nv ? (int)((uint32_t)p0 / (uint32_t)W) : 0;
+    const int u0 = nv ? (int)p0 - v0 * W : 0;
+    uint32_t* cnt_f = wb.cnt + (size_t)f * wb.SMAX * wb.PMAXP;
+    auto load = [&](int s, uint32_t w[8]) {
+      const uint8_t* mp = F.masks + (size_t)s * HW + p0;
+      if (VEC) {
+        ld_stream32(mp, w);
       } else {
-        const uint32_t gi2 = atomicAdd(&wb.npairs[f], 1u);
-        if (gi2 < (uint32_t)wb.PMAX) wb.plist[(size_t)f * wb.PMAX + gi2] = pslot;
-        else raise_err(err, DERR_FRAME_PAIRS);
-      }
-    }
-    return pslot;
-  };
-  // one (s, key-run) item into the CTA pair table (code = s << 16 | local key); the global
-  // frame tables are filled later from the table's distinct codes (phase 5).  Items whose run key
-  // is not in the CTA key table, or that find the pair table full, go global directly.
-  auto emit = [&](uint32_t s, uint16_t li, int run_first_c, float n0, float n1, float n2) {
-    int slot = -1;
-    if (li != K1_NOKEY) {
-      const uint32_t code = (s << 16) | li;
-      uint32_t h = mix32(code) & (K1_PT - 1);
-      for (int probe = 0; probe < K1_PT; ++probe) {
-        const uint32_t cur = pt[h];
-        if (cur == code) { slot = (int)h; break; }
-        if (cur == U32_EMPTY) {
-          const uint32_t old = atomicCAS(&pt[h], U32_EMPTY, code);
-          if (old == U32_EMPTY || old == code) { slot = (int)h; break; }
-        }
-        h = (h + 1) & (K1_PT - 1);
-      }
-    }
-    if (slot >= 0) {
-      if (SEM && (n0 != 0.f || n1 != 0.f || n2 != 0.f)) red_add3(&nscr[slot], n0, n1, n2);
-      return;
-    }
-    uint64_t key = KEY_EMPTY;
-    if (li != K1_NOKEY) {
-      key = kt[li];
-    } else {   // CTA key table full: recompute the run key (pinned R5)
-      float pw[3];
-      if (wp_tile(0, run_first_c, pw)) point_key_fast(pw, r, rinv, key);
-    }
-    const uint32_t pslot = global_insert(key, s);
-    if (SEM && pslot != U32_EMPTY && (n0 != 0.f || n1 != 0.f || n2 != 0.f)) {
-      atomicAdd(&nsum[3 * pslot + 0], n0);
-      atomicAdd(&nsum[3 * pslot + 1], n1);
-      atomicAdd(&nsum[3 * pslot + 2], n2);
-    }
-  };
-
-  // ---- 1: patch segments of the lane's chunk (R17) ----
-  uint32_t okb = 0, pst = 0;
-  uint32_t my_oor = 0;
-  if (lane_on) {
-    int prevp = -1;
-    for (int j = 0; j < nin; ++j) {
-      const int p = prow + pc_s[c0 + j];
-      if (p != prevp) { pst |= 1u << j; prevp = p; }
-    }
-  }
-
-  __syncthreads();
-  K1_PROBE(1);
-  // ---- 2: masks -> first mask per pixel, overlap flags, per-patch counts, bbox.  Each lane
-  // streams its 32 bytes of every plane (evict-first in L2), two planes in flight ----
-  uint32_t ovf = 0;
-  const int64_t pix0 = (int64_t)v * W + u0;
-  const bool vec32 = F.vec16 && nin == 32 && (pix0 & 31) == 0;
-  const bool vec16 = F.vec16 && nin == 32 && (pix0 & 15) == 0;
-  auto load_pair = [&](int s0, uint32_t w[2][8]) {
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-#pragma unroll
-      for (int t = 0; t < 8; ++t) w[k][t] = 0u;
-      if (s0 + k < S) {
-        const uint8_t* mp = F.masks + (size_t)(s0 + k) * HW + pix0;
-        if (vec32) {
-          ld_stream32(mp, w[k]);
-        } else if (vec16) {
-          const uint4 a = ld_stream16(mp), b = ld_stream16(mp + 16);
-          w[k][0] = a.x; w[k][1] = a.y; w[k][2] = a.z; w[k][3] = a.w;
-          w[k][4] = b.x; w[k][5] = b.y; w[k][6] = b.z; w[k][7] = b.w;
-        } else {
-          for (int t = 0; t < 8; ++t) {
-            uint32_t x = 0;
-            for (int bq = 0; bq < 4; ++bq)
-              if (inb & (1u << (4 * t + bq))) x |= (uint32_t)(mp[4 * t + bq] != 0) << (8 * bq);
-            w[k][t] = x;
-          }
+        for (int t = 0; t < 8; ++t) {
+          uint32_t x = 0;
+          for (int bq = 0; bq < 4; ++bq)
+            if (inb & (1u << (4 * t + bq))) x |= (uint32_t)(mp[4 * t + bq] != 0) << (8 * bq);
+          w[t] = x;
         }
       }
-    }
-  };
-  const int Sl = (lane_on && !(ablate & 1)) ? S : 0;
-  uint32_t wa[2][8], wn[2][8];
-  if (Sl > 0) load_pair(0, wa);
-  for (int s0 = 0; s0 < Sl; s0 += 2) {
-    if (s0 + 2 < Sl) load_pair(s0 + 2, wn);   // next pair in flight while this one is processed
+    };
+    uint32_t m0[8], ovf = 0;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int s = s0 + k;
-      if (s >= S) break;
-      if ((wa[k][0] | wa[k][1] | wa[k][2] | wa[k][3] | wa[k][4] | wa[k][5] | wa[k][6] | wa[k][7]) == 0) continue;
-      uint32_t set = 0;
-      const uint32_t splat = (uint32_t)s * 0x01010101u;
+    for (int t = 0; t < 8; ++t) m0[t] = 0xFFFFFFFFu;   // no mask yet
+    const int Sl = (nv && !(ablate & 1)) ? S : 0;
+    uint32_t buf[K1_NF][8];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const uint32_t sb = __vcmpne4(wa[k][t], 0u);                // 0xFF where the pixel is in s
-        set |= (((sb & 0x08040201u) * 0x01010101u) >> 24) << (4 * t);
-        if (sb) {
-          const uint32_t m = m0w[t * K1_THREADS];
-          const uint32_t unset = __vcmpeq4(m, 0xFFFFFFFFu);     // 0xFF where no mask yet
+    for (int k = 0; k < K1_NF; ++k)
+      if (k < Sl) load(k, buf[k]);
+    for (int s0 = 0; s0 < Sl; s0 += K1_NF) {
+#pragma unroll
+      for (int k = 0; k < K1_NF; ++k) {
+        const int s = s0 + k;
+        if (s >= Sl) break;
+        uint32_t* w = buf[k];
+        if ((w[0] | w[1] | w[2] | w[3] | w[4] | w[5] | w[6] | w[7]) == 0) {
+          if (s + K1_NF < Sl) load(s + K1_NF, buf[k]);   // refill the ring slot
+          continue;
+        }
+        uint32_t set = 0;
+        const uint32_t splat = (uint32_t)s * 0x01010101u;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const uint32_t sb = __vcmpne4(w[t], 0u);                // 0xFF where the pixel is in s
+          set |= (((sb & 0x08040201u) * 0x01010101u) >> 24) << (4 * t);
+          const uint32_t unset = __vcmpeq4(m0[t], 0xFFFFFFFFu);   // 0xFF where no mask yet
           const uint32_t fresh = sb & unset, again = sb & ~unset;
-          m0w[t * K1_THREADS] = (m & ~fresh) | (splat & fresh);
+          m0[t] = (m0[t] & ~fresh) | (splat & fresh);
           ovf |= (((again & 0x08040201u) * 0x01010101u) >> 24) << (4 * t);
         }
+        if (s + K1_NF < Sl) load(s + K1_NF, buf[k]);   // refill the ring slot
+        set &= inb;
+        if (!set) continue;
+        // row segments of the sector, and patch segments inside them: per-patch pixel counts
+        // (O5, regardless of depth, R17) and bbox
+        int j = 0, v = v0, u = u0;
+        while (j < nv) {
+          const int len = min(W - u, nv - j);
+          const uint32_t rowb = set & range_bits(j, j + len);
+          if (rowb) {
+            const int prow = (v * Hp) / H * Wp;
+            int pcol = (u * Wp) / W;
+            int jj = j, uu = u;
+            while (jj < j + len) {
+              const int ub = ((pcol + 1) * W + Wp - 1) / Wp;   // first u of the next patch column
+              const int l2 = min(j + len - jj, ub - uu);
+              const int cn = __popc(set & range_bits(jj, jj + l2));
+              if (cn) atomicAdd(&cnt_f[(size_t)s * wb.PMAXP + prow + pcol], (uint32_t)cn);
+              jj += l2; uu += l2; ++pcol;
+            }
+            atomicMin(&bb_s[4 * s + 0], u + (__ffs(rowb) - 1 - j));
+            atomicMax(&bb_s[4 * s + 2], u + (31 - __clz(rowb) - j));
+            atomicMin(&bb_s[4 * s + 1], v);
+            atomicMax(&bb_s[4 * s + 3], v);
+          }
+          j += len; ++v; u = 0;
+        }
       }
-      set &= inb;
-      if (!set) continue;
-      for (uint32_t gg = pst; gg;) {      // per-patch pixel counts (O5, regardless of depth)
-        const int a0 = __ffs(gg) - 1;
-        gg &= gg - 1;
-        const int b0 = gg ? __ffs(gg) - 1 : 32;
-        const int cnum = __popc(set & range_bits(a0, b0));
-        if (cnum) atomicAdd(&cnt_g[(size_t)s * wb.PMAXP + prow + pc_s[c0 + a0]], (uint32_t)cnum);
-      }
-      atomicMin(&bb_s[4 * s + 0], u0 + __ffs(set) - 1);
-      atomicMax(&bb_s[4 * s + 2], u0 + 31 - __clz(set));
-      atomicMin(&bb_s[4 * s + 1], v);
-      atomicMax(&bb_s[4 * s + 3], v);
     }
-#pragma unroll
-    for (int k = 0; k < 2; ++k)
-#pragma unroll
-      for (int t = 0; t < 8; ++t) wa[k][t] = wn[k][t];
-  }
-  cp_async_wait<0>();
-  __syncthreads();
-  K1_PROBE(2);
-
-  // ---- 3: one sliding window over the lane's pixels: pinned keys (R5), key runs, (first mask,
-  // run) items, pixel normals (R21).  Each world point is computed once. ----
-  if (lane_on && !(ablate & 2)) {
-    uint64_t run_key = KEY_EMPTY, cur_key = KEY_EMPTY;
-    uint16_t run_li = K1_NOKEY, cur_li = K1_NOKEY;
-    bool run_li_ok = false;
-    int cur_first = 0;
-    uint32_t cur_m = 0xFF;
-    float n0 = 0.f, n1 = 0.f, n2 = 0.f;
-    const bool inner_v = v >= 1 && v + 1 < H;
-    float pl[3] = {0.f, 0.f, 0.f}, pc[3] = {0.f, 0.f, 0.f};
-    bool vl = SEM ? wp_tile(0, c0 - 1, pl) : false;
-    bool vc = wp_tile(0, c0, pc);
-    for (int j = 0; j < nin; ++j) {
-      float pr[3] = {0.f, 0.f, 0.f};
-      const bool vr = (j + 1 < nin || SEM) ? wp_tile(0, c0 + j + 1, pr) : false;
-      uint64_t key = KEY_EMPTY;
-      bool ok = false;
-      if (vc) {
-        if (point_key_fast(pc, r, rinv, key)) ok = true;
-        else my_oor++;
+    if (nv) {   // m0 / ovf maps (flat, sector-aligned)
+      uint8_t* mo = wb.m0map + (size_t)f * wb.MPIX + p0;
+      if (VEC) {
+        ((uint4*)mo)[0] = make_uint4(m0[0], m0[1], m0[2], m0[3]);
+        ((uint4*)mo)[1] = make_uint4(m0[4], m0[5], m0[6], m0[7]);
+      } else {
+        for (int j = 0; j < nv; ++j) mo[j] = (uint8_t)(m0[j >> 2] >> (8 * (j & 3)));
       }
-      if (ok) {
-        okb |= 1u << j;
-        if (key != run_key) { run_key = key; run_li_ok = false; }
-        const uint32_t mj = (m0w[(j >> 2) * K1_THREADS] >> (8 * (j & 3))) & 0xFFu;
-        if (mj != 0xFFu) {
-          if (cur_m != 0xFFu && (key != cur_key || mj != cur_m)) {
-            emit(cur_m, cur_li, cur_first, n0, n1, n2);
-            cur_m = 0xFFu;
+      wb.ovfmap[(size_t)f * wb.MOVF + (p0 >> 5)] = ovf & inb;
+    }
+    __syncthreads();
+    for (int s = threadIdx.x; s < S; s += blockDim.x) {
+      if (bb_s[4 * s + 2] < 0) continue;   // mask absent from this item
+      const size_t gi = (size_t)f * wb.SMAX + s;
+      atomicMin(&wb.bbox[4 * gi + 0], bb_s[4 * s + 0]);
+      atomicMin(&wb.bbox[4 * gi + 1], bb_s[4 * s + 1]);
+      atomicMax(&wb.bbox[4 * gi + 2], bb_s[4 * s + 2]);
+      atomicMax(&wb.bbox[4 * gi + 3], bb_s[4 * s + 3]);
+    }
+  }
+}
+
+// ---- K1b ----------------------------------------------------------------------------------
+template <bool SEM>
+__global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, WinBufs wb, Params P, int* err,
+                                                                 int tiles_x, int reserve, int ablate) {
+  if (on_reserved_sm(reserve)) return;
+  extern __shared__ uint32_t vs_s[];                        // [S] |V_s| contributions
+  __shared__ unsigned long long kt[K1_KT];                  // CTA key table
+  __shared__ uint32_t ptc[2 * K1_KT];                       // pair slots 2 li, 2 li + 1: s or EMPTY
+  __shared__ uint32_t pl_s[K1_PLIST];
+  __shared__ float yb_s[K1_TILE_H + 2];                     // row r <-> v = vt0 - 1 + r (R5)
+  __shared__ float4 pose_s[3];                              // pose rows (R5): re-read, not held in registers
+  __shared__ uint32_t item_s, slot_s, npl_s, oor_s, base_s;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (SEM && threadIdx.x == 0) {   // a scratch block of this SM for the tiles' normal sums
+    uint32_t sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    uint32_t* w = wb.k1slot + sm;
+    for (;;) {
+      const uint32_t freeb = ~*(volatile uint32_t*)w & ((1u << K1_SLOTS_PER_SM) - 1u);
+      if (!freeb) continue;
+      const uint32_t b = __ffs(freeb) - 1;
+      if (!(atomicOr(w, 1u << b) & (1u << b))) { slot_s = sm * K1_SLOTS_PER_SM + b; break; }
+    }
+    __threadfence();
+  }
+  const float rv = P.r;
+  const float rinv = 1.0f / P.r;   // only used by floor_div_pinned's exact fast path
+  const uint32_t total = (uint32_t)tiles_x * (uint32_t)wd.n;
+  for (int it; (it = next_item(wb.k1ctr + 1, total, &item_s)) >= 0;) {
+    const int f = it / tiles_x, tile = it % tiles_x;
+    const FrameDesc& F = wd.f[f];
+    const int H = F.H, W = F.W, S = F.S;
+    const int ntx = (W + K1_TILE_W - 1) / K1_TILE_W, nty = (H + K1_TILE_H - 1) / K1_TILE_H;
+    if (tile >= ntx * nty) continue;
+    const int ty = tile / ntx, tx = tile - ty * ntx;
+    const int ut0 = tx * K1_TILE_W, vt0 = ty * K1_TILE_H;
+    float4* nscr = SEM ? wb.k1scr + (size_t)slot_s * K1_PT : nullptr;
+    for (int i = threadIdx.x; i < S; i += blockDim.x) vs_s[i] = 0;
+    for (int i = threadIdx.x; i < K1_KT; i += blockDim.x) kt[i] = KEY_EMPTY;
+    for (int i = threadIdx.x; i < 2 * K1_KT; i += blockDim.x) ptc[i] = U32_EMPTY;
+    for (int r = threadIdx.x; r < K1_TILE_H + 2; r += blockDim.x)
+      yb_s[r] = __fdiv_rn(__fsub_rn((float)(vt0 - 1 + r), F.cy), F.fy);
+    if (threadIdx.x < 3)
+      pose_s[threadIdx.x] = make_float4(F.pose[4 * threadIdx.x], F.pose[4 * threadIdx.x + 1], F.pose[4 * threadIdx.x + 2],
+                                        F.pose[4 * threadIdx.x + 3]);
+    if (threadIdx.x == 0) { npl_s = 0; oor_s = 0; }
+    __syncthreads();
+
+    const uint32_t tmask = (uint32_t)wb.PC - 1;
+    unsigned long long* ktab = wb.ktab + (size_t)f * wb.PC;
+    uint32_t* ptab = wb.ptab + (size_t)f * wb.PC;
+    float* nsum = wb.nsum + (size_t)f * wb.PC * 3;
+    auto kt_insert = [&](uint64_t key) -> uint16_t {   // CTA key table -> local key index
+      uint32_t h = (uint32_t)mix64(key) & (K1_KT - 1);
+      for (int probe = 0; probe < K1_KT; ++probe) {
+        const unsigned long long cur = kt[h];
+        if (cur == key) return (uint16_t)h;
+        if (cur == KEY_EMPTY) {
+          const unsigned long long old = atomicCAS(&kt[h], KEY_EMPTY, (unsigned long long)key);
+          if (old == KEY_EMPTY || old == key) return (uint16_t)h;
+        }
+        h = (h + 1) & (K1_KT - 1);
+      }
+      return K1_NOKEY;
+    };
+    auto global_insert = [&](uint64_t key, uint32_t s) -> uint32_t {
+      const uint32_t kslot = ktab_insert(ktab, tmask, key, err);
+      if (kslot == U32_EMPTY) return U32_EMPTY;
+      bool fresh = false;
+      const uint32_t pslot = ptab_insert(ptab, tmask, (s << 24) | kslot, &fresh, err);
+      if (pslot != U32_EMPTY && fresh) {
+        atomicAdd(&vs_s[s], 1u);
+        const uint32_t li = atomicAdd(&npl_s, 1u);
+        if (li < K1_PLIST) {
+          pl_s[li] = pslot;
+        } else {
+          const uint32_t gi2 = atomicAdd(&wb.npairs[f], 1u);
+          if (gi2 < (uint32_t)wb.PMAX) wb.plist[(size_t)f * wb.PMAX + gi2] = pslot;
+          else raise_err(err, DERR_FRAME_PAIRS);
+        }
+      }
+      return pslot;
+    };
+    // one (s, key) item: CTA key table -> local index li; the pair is slot 2 li or 2 li + 1 (a
+    // voxel rarely meets more than two masks in one tile); otherwise straight to the frame tables
+    auto emit = [&](uint32_t s, uint64_t key, float n0, float n1, float n2) -> int {
+      const uint16_t li = kt_insert(key);
+      int ps = -1;
+      if (li != K1_NOKEY) {
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          uint32_t* c = &ptc[2 * li + jj];
+          uint32_t cur = *c;
+          if (cur == U32_EMPTY) {
+            cur = atomicCAS(c, U32_EMPTY, s);
+            if (cur == U32_EMPTY) cur = s;
           }
-          if (cur_m == 0xFFu) {
-            if (!run_li_ok) { run_li = kt_insert(run_key); run_li_ok = true; }
-            cur_m = mj;
-            cur_key = key;
-            cur_li = run_li;
-            cur_first = c0 + j;
-            n0 = n1 = n2 = 0.f;
+          if (cur == s) { ps = 2 * li + jj; break; }
+        }
+      }
+      const bool hasn = SEM && (n0 != 0.f || n1 != 0.f || n2 != 0.f);
+      if (ps >= 0) {
+        if (hasn) red_add3(&nscr[ps], n0, n1, n2);
+        return ps;
+      }
+      const uint32_t g = global_insert(key, s);
+      if (hasn && g != U32_EMPTY) {
+        atomicAdd(&nsum[3 * g + 0], n0);
+        atomicAdd(&nsum[3 * g + 1], n1);
+        atomicAdd(&nsum[3 * g + 2], n2);
+      }
+      return -1;
+    };
+
+    // ---- walk: lane = column, one row per step ----
+    const int u = ut0 + warp * K1_TW + lane;
+    const int rows = min(K1_TILE_H, H - vt0);
+    uint32_t my_oor = 0;
+    if (!(ablate & 2) && ut0 + warp * K1_TW < W) {
+      const bool col_on = u < W;
+      const bool edge = lane == 0 || lane == 31;
+      const int uh = lane == 0 ? u - 1 : u + 1;   // halo column of the warp's edge lanes
+      const bool h_on = SEM && edge && uh >= 0 && uh < W;
+      const float xa = col_on ? __fdiv_rn(__fsub_rn((float)u, F.cx), F.fx) : 0.f;   // R5
+      const float xh = h_on ? __fdiv_rn(__fsub_rn((float)uh, F.cx), F.fx) : 0.f;
+      const float* dcol = F.depth + (col_on ? u : 0);
+      const float* dhal = F.depth + (h_on ? uh : 0);
+      const uint8_t* mcol = wb.m0map + (size_t)f * wb.MPIX + (col_on ? u : 0);
+      const uint32_t* ovm = wb.ovfmap + (size_t)f * wb.MOVF;   // flat: bit p & 31 of word p >> 5
+      auto wpt = [&](float d, float x, int r, float p[3]) -> bool {   // r = v - vt0 + 1
+        if (!depth_valid(d, P)) return false;
+        const float yb = yb_s[r];
+        const float xc = __fmul_rn(x, d), yc = __fmul_rn(yb, d), zc = d;
+        const float4 a = pose_s[0], b = pose_s[1], c = pose_s[2];
+        p[0] = __fmaf_rn(a.x, xc, __fmaf_rn(a.y, yc, __fmaf_rn(a.z, zc, a.w)));
+        p[1] = __fmaf_rn(b.x, xc, __fmaf_rn(b.y, yc, __fmaf_rn(b.z, zc, b.w)));
+        p[2] = __fmaf_rn(c.x, xc, __fmaf_rn(c.y, yc, __fmaf_rn(c.z, zc, c.w)));
+        return true;
+      };
+      auto drow = [&](const float* base, bool on, int vv) -> float {   // 0 (invalid) off-image
+        return (on && vv >= 0 && vv < H) ? __ldg(base + vv * W) : 0.f;
+      };
+      float pu[3] = {0.f, 0.f, 0.f}, pc[3] = {0.f, 0.f, 0.f};
+      bool vu = SEM ? wpt(drow(dcol, col_on, vt0 - 1), xa, 0, pu) : false;
+      bool vc = wpt(drow(dcol, col_on, vt0), xa, 1, pc);
+      uint64_t kc = KEY_EMPTY;
+      bool kvc = vc && point_key_fast(pc, rv, rinv, kc);
+      float d_dn = drow(dcol, col_on, vt0 + 1);
+      float d_h = drow(dhal, h_on, vt0);
+      uint32_t m_c = col_on ? mcol[vt0 * W] : 0xFFu;
+      auto ovbit = [&](int vv) -> uint32_t {   // pixel (vv, u) is in a second mask
+        const int64_t p = (int64_t)vv * W + u;
+        return col_on ? (ovm[p >> 5] >> (p & 31)) & 1u : 0u;
+      };
+      uint32_t ov_c = ovbit(vt0);
+      uint64_t ck = KEY_EMPTY;   // the lane's last emitted item (rows repeat voxels): key, s, pair slot
+      uint32_t cs = 0xFFFFFFFFu, cps = 0;
+      for (int rr = 0; rr < rows; ++rr) {
+        const int vv = vt0 + rr;
+        // the next row's loads go out before this row's arithmetic
+        const float d_dn2 = drow(dcol, col_on, vv + 2);
+        const float d_h2 = drow(dhal, h_on, vv + 1);
+        const bool more = rr + 1 < rows;
+        const uint32_t m_n = (col_on && more) ? mcol[(vv + 1) * W] : 0xFFu;
+        const uint32_t ov_n = more ? ovbit(vv + 1) : 0u;
+        float pd[3] = {0.f, 0.f, 0.f};
+        const bool vd = wpt(d_dn, xa, rr + 2, pd);
+        const uint32_t m = m_c;
+        if (vc && !kvc) my_oor++;
+        const bool item = m != 0xFFu && kvc;
+        float n0 = 0.f, n1 = 0.f, n2 = 0.f;
+        if (SEM && !(ablate & 8)) {
+          float hx[3] = {0.f, 0.f, 0.f};
+          const bool vh = h_on && wpt(d_h, xh, rr + 1, hx);
+          float pl[3], pr[3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            pl[a] = __shfl_up_sync(0xffffffffu, pc[a], 1);
+            pr[a] = __shfl_down_sync(0xffffffffu, pc[a], 1);
           }
-          const int u = u0 + j;
-          if (SEM && !(ablate & 8) && vl && vr && inner_v && u >= 1 && u + 1 < W) {
-            float pu[3], pd[3], n[3];
-            if (wp_tile(-1, c0 + j, pu) && wp_tile(1, c0 + j, pd) && normal_from(F, pc, pl, pr, pu, pd, n)) {
-              n0 += n[0]; n1 += n[1]; n2 += n[2];
+          const unsigned vb = __ballot_sync(0xffffffffu, vc);
+          bool vl = (vb >> ((lane - 1) & 31)) & 1u, vr = (vb >> ((lane + 1) & 31)) & 1u;
+          if (lane == 0) { pl[0] = hx[0]; pl[1] = hx[1]; pl[2] = hx[2]; vl = vh; }
+          if (lane == 31) { pr[0] = hx[0]; pr[1] = hx[1]; pr[2] = hx[2]; vr = vh; }
+          // R21 with 4 valid neighbours (off-image neighbours read depth 0 = invalid)
+          if (item && vl && vr && vu && vd) {
+            const float a0 = pr[0] - pl[0], a1 = pr[1] - pl[1], a2 = pr[2] - pl[2];
+            const float b0 = pd[0] - pu[0], b1 = pd[1] - pu[1], b2 = pd[2] - pu[2];
+            n0 = a1 * b2 - a2 * b1;
+            n1 = a2 * b0 - a0 * b2;
+            n2 = a0 * b1 - a1 * b0;
+            const float o = n0 * (pose_s[0].w - pc[0]) + n1 * (pose_s[1].w - pc[1]) + n2 * (pose_s[2].w - pc[2]);
+            if (o < 0.f) { n0 = -n0; n1 = -n1; n2 = -n2; }
+          }
+        }
+        // runs of equal (m, key) along the row
+        const uint32_t khi = (uint32_t)(kc >> 32), klo = (uint32_t)kc;
+        const uint32_t mq = item ? m : 0x100u;
+        const uint32_t mp = __shfl_up_sync(0xffffffffu, mq, 1);
+        const uint32_t hp = __shfl_up_sync(0xffffffffu, khi, 1);
+        const uint32_t lp = __shfl_up_sync(0xffffffffu, klo, 1);
+        const bool same_prev = item && lane > 0 && mp == mq && hp == khi && lp == klo;
+        const unsigned items = __ballot_sync(0xffffffffu, item);
+        const unsigned heads = __ballot_sync(0xffffffffu, item && !same_prev);
+        if (items) {
+          const float q0 = n0, q1 = n1, q2 = n2;   // this pixel's own normal
+          if (SEM) {   // segmented inclusive scan over the runs
+            const int start = 31 - __clz(heads & (0xFFFFFFFFu >> (31 - lane)));
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const float a0 = __shfl_up_sync(0xffffffffu, n0, o);
+              const float a1 = __shfl_up_sync(0xffffffffu, n1, o);
+              const float a2 = __shfl_up_sync(0xffffffffu, n2, o);
+              if (lane - o >= start) { n0 += a0; n1 += a1; n2 += a2; }
             }
           }
+          const bool tail = item && !(((items & ~heads) >> 1 >> lane) & 1u);
+          if (tail) {
+            if (kc == ck && m == cs) {   // same voxel and mask as the lane's previous item
+              if (SEM && (n0 != 0.f || n1 != 0.f || n2 != 0.f)) red_add3(&nscr[cps], n0, n1, n2);
+            } else {
+              const int ps = emit(m, kc, n0, n1, n2);
+              if (ps >= 0) { ck = kc; cs = m; cps = (uint32_t)ps; }
+            }
+          }
+          if (item && ov_c) {   // other masks of this pixel (R9), per pixel
+            const size_t pix = (size_t)vv * W + u;
+            for (int s2 = (int)m + 1; s2 < S; ++s2)
+              if (F.masks[(size_t)s2 * H * W + pix]) emit((uint32_t)s2, kc, q0, q1, q2);
+          }
         }
+        pu[0] = pc[0]; pu[1] = pc[1]; pu[2] = pc[2]; vu = vc;
+        pc[0] = pd[0]; pc[1] = pd[1]; pc[2] = pd[2]; vc = vd;
+        kc = KEY_EMPTY;
+        kvc = vc && point_key_fast(pc, rv, rinv, kc);
+        d_dn = d_dn2; d_h = d_h2; m_c = m_n; ov_c = ov_n;
       }
-      pl[0] = pc[0]; pl[1] = pc[1]; pl[2] = pc[2]; vl = vc;
-      pc[0] = pr[0]; pc[1] = pr[1]; pc[2] = pr[2]; vc = vr;
     }
-    if (cur_m != 0xFFu) emit(cur_m, cur_li, cur_first, n0, n1, n2);
-  }
-
-  // ---- 4: pixels in several masks (overlapping masks, R9): their other planes ----
-  if (lane_on && (ovf & okb) && !(ablate & 2)) {
-    for (uint32_t bb2 = ovf & okb; bb2;) {
-      const int j = __ffs(bb2) - 1;
-      bb2 &= bb2 - 1;
-      const uint32_t mj = (m0w[(j >> 2) * K1_THREADS] >> (8 * (j & 3))) & 0xFFu;
-      float pw[3];
-      uint64_t key = KEY_EMPTY;
-      if (!wp_tile(0, c0 + j, pw) || !point_key_fast(pw, r, rinv, key)) continue;
-      const uint16_t li = kt_insert(key);
-      float n[3] = {0.f, 0.f, 0.f};
-      if (SEM && !(ablate & 8) && !pixel_normal(c0 + j, n)) { n[0] = n[1] = n[2] = 0.f; }
-      const size_t pix = (size_t)v * W + u0 + j;
-      for (int s2 = (int)mj + 1; s2 < S; ++s2)
-        if (F.masks[(size_t)s2 * HW + pix]) emit((uint32_t)s2, li, c0 + j, n[0], n[1], n[2]);
-    }
-  }
-  if (lane_on && my_oor) atomicAdd(&oor_s, my_oor);
-  if (SEM) __threadfence();   // this thread's normal reductions before the phase-5 reads
-  __syncthreads();
-  K1_PROBE(3);
-  // ---- 5: the tile's distinct (s, key) pairs -> global frame tables (all threads, many
-  // independent inserts in flight); normal sums flushed with them ----
-  for (int i = threadIdx.x; i < K1_PT; i += blockDim.x) {
-    const uint32_t code = pt[i];
-    if (code == U32_EMPTY) continue;
-    const uint32_t s = code >> 16;
-    const uint32_t pslot = global_insert(kt[code & 0xFFFFu], s);
-    if (SEM) {
-      const float4 nn = __ldcg(&nscr[i]);
-      if (nn.x != 0.f || nn.y != 0.f || nn.z != 0.f) {
-        __stcg(&nscr[i], make_float4(0.f, 0.f, 0.f, 0.f));   // leave the block all-zero
-        if (pslot != U32_EMPTY) {
-          atomicAdd(&nsum[3 * pslot + 0], nn.x);
-          atomicAdd(&nsum[3 * pslot + 1], nn.y);
-          atomicAdd(&nsum[3 * pslot + 2], nn.z);
+    if (my_oor) atomicAdd(&oor_s, my_oor);
+    if (SEM) __threadfence();   // this thread's normal reductions before the reads below
+    __syncthreads();
+    // ---- the tile's distinct (s, key) pairs -> frame tables, normal sums with them ----
+    for (int i = threadIdx.x; i < 2 * K1_KT; i += blockDim.x) {
+      const uint32_t s = ptc[i];
+      if (s == U32_EMPTY) continue;
+      const uint32_t g = global_insert(kt[i >> 1], s);
+      if (SEM) {
+        const float4 nn = __ldcg(&nscr[i]);
+        if (nn.x != 0.f || nn.y != 0.f || nn.z != 0.f) {
+          __stcg(&nscr[i], make_float4(0.f, 0.f, 0.f, 0.f));   // leave the block all-zero
+          if (g != U32_EMPTY) {
+            atomicAdd(&nsum[3 * g + 0], nn.x);
+            atomicAdd(&nsum[3 * g + 1], nn.y);
+            atomicAdd(&nsum[3 * g + 2], nn.z);
+          }
         }
       }
     }
+    __syncthreads();
+    for (int s = threadIdx.x; s < S; s += blockDim.x)
+      if (vs_s[s]) atomicAdd(&wb.vs[(size_t)f * wb.SMAX + s], vs_s[s]);
+    const uint32_t n = min(npl_s, (uint32_t)K1_PLIST);
+    if (threadIdx.x == 0) {
+      base_s = n ? atomicAdd(&wb.npairs[f], n) : 0;
+      if (oor_s) atomicAdd(&wb.oor[f], (unsigned long long)oor_s);
+    }
+    __syncthreads();
+    if (base_s + n > (uint32_t)wb.PMAX) {
+      if (threadIdx.x == 0) raise_err(err, DERR_FRAME_PAIRS);
+    } else {
+      for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) wb.plist[(size_t)f * wb.PMAX + base_s + i] = pl_s[i];
+    }
   }
-  __syncthreads();
-  K1_PROBE(4);
-
-  // ---- flush per-mask accumulators ----
-  for (int s = threadIdx.x; s < S; s += blockDim.x) {
-    if (bb_s[4 * s + 2] < 0) continue;   // mask absent from this tile
-    const size_t gi = (size_t)f * wb.SMAX + s;
-    atomicMin(&wb.bbox[4 * gi + 0], bb_s[4 * s + 0]);
-    atomicMin(&wb.bbox[4 * gi + 1], bb_s[4 * s + 1]);
-    atomicMax(&wb.bbox[4 * gi + 2], bb_s[4 * s + 2]);
-    atomicMax(&wb.bbox[4 * gi + 3], bb_s[4 * s + 3]);
-    if (vs_s[s]) atomicAdd(&wb.vs[gi], vs_s[s]);
+  if (SEM && threadIdx.x == 0) {
+    __threadfence();
+    atomicAnd(wb.k1slot + slot_s / K1_SLOTS_PER_SM, ~(1u << (slot_s % K1_SLOTS_PER_SM)));
   }
-  __shared__ uint32_t base_s;
-  const uint32_t n = min(npl_s, (uint32_t)K1_PLIST);
-  if (threadIdx.x == 0) {
-    base_s = n ? atomicAdd(&wb.npairs[f], n) : 0;
-    if (oor_s) atomicAdd(&wb.oor[f], (unsigned long long)oor_s);
-  }
-  __syncthreads();
-  if (base_s + n > (uint32_t)wb.PMAX) {
-    if (threadIdx.x == 0) raise_err(err, DERR_FRAME_PAIRS);
-    return;
-  }
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) wb.plist[(size_t)f * wb.PMAX + base_s + i] = pl_s[i];
-  K1_PROBE(5);
 }
 
 __global__ void k_nsmid(int* out) {
@@ -647,48 +677,6 @@ int k1_nsmid() {
   if (cudaMemcpy(&h, d, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess || h <= 0) h = 256;
   cudaFree(d);
   return h;
-}
-
-// Persistent: K1_PERSIST CTAs per SM pull (frame, tile) items from a counter.  CTAs that land on
-// one of the first `reserve` SMs exit at once, so those SMs stay free for stage 2's per-frame
-// kernels (a latency-bound chain on the map) while K1 streams the masks on the rest.
-template <bool SEM>
-__global__ void __launch_bounds__(K1_THREADS, K1_MINB) k_mask_pass(WinDesc wd, WinBufs wb, Params P, int* err,
-                                                             int tiles_x, int reserve, int ablate) {
-  __shared__ uint32_t slot_s, item_s;
-  uint32_t sm;
-  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-  if ((int)sm < reserve) return;   // SMs left to stage 2
-  if (SEM && threadIdx.x == 0) {   // a scratch block of this SM for the tiles' normal sums
-    uint32_t* w = wb.k1slot + sm;
-    for (;;) {
-      const uint32_t freeb = ~*(volatile uint32_t*)w & ((1u << K1_SLOTS_PER_SM) - 1u);
-      if (!freeb) continue;
-      const uint32_t b = __ffs(freeb) - 1;
-      if (!(atomicOr(w, 1u << b) & (1u << b))) { slot_s = sm * K1_SLOTS_PER_SM + b; break; }
-    }
-    __threadfence();
-  }
-  const uint32_t total = (uint32_t)tiles_x * (uint32_t)wd.n;
-  for (;;) {
-    if (threadIdx.x == 0) item_s = atomicAdd(wb.k1ctr, 1u);
-    __syncthreads();
-    const uint32_t it = item_s;
-    __syncthreads();
-    if (it >= total) break;
-    k1_tile<SEM>(wd, wb, P, err, (int)(it % (uint32_t)wd.n), (int)(it / (uint32_t)wd.n), slot_s, ablate);
-  }
-  if (SEM && threadIdx.x == 0) {
-    __threadfence();
-    atomicAnd(wb.k1slot + slot_s / K1_SLOTS_PER_SM, ~(1u << (slot_s % K1_SLOTS_PER_SM)));
-  }
-}
-
-void k1_prof_dump() {
-  unsigned long long h[8];
-  cudaMemcpyFromSymbol(h, g_k1prof, sizeof(h));
-  fprintf(stderr, "k1 phase CTA-ns: setup %llu keys %llu masks %llu items %llu global %llu flush %llu\n", h[0], h[1],
-          h[2], h[3], h[4], h[5]);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1158,7 +1146,7 @@ __global__ void __launch_bounds__(K4_THREADS) k_finalize(WinDesc wd, WinBufs wb,
 // launchers
 // ------------------------------------------------------------------------------------------
 // DISC_K1_ABLATE (profiling only; results are wrong when set): 1 skip mask planes, 2 skip
-// pair items, 4 skip key computation, 8 skip normals
+// the walk, 8 skip normals
 static int k1_ablate() {
   static int v = -1;
   if (v < 0) {
@@ -1168,10 +1156,6 @@ static int k1_ablate() {
   return v;
 }
 
-size_t k1_smem_bytes(int S, int W, int rows_cap) { (void)rows_cap; (void)W; return K1Smem(S, true).total; }
-
-int k1_rows_cap(int W) { (void)W; return 4; }
-
 int k1_tiles(int H, int W) {
   return ((W + K1_TILE_W - 1) / K1_TILE_W) * ((H + K1_TILE_H - 1) / K1_TILE_H);
 }
@@ -1180,22 +1164,26 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
                   int maxHp, int maxW, int maxWp, int maxP, int rows_cap, int nsm, int nres, cudaStream_t st,
                   cudaEvent_t ev0, cudaEvent_t ev1) {
   const int n = wd.n;
-  (void)rows_cap;
+  (void)rows_cap; (void)maxW;
   int k1_grid = 1;
   for (int i = 0; i < n; ++i) k1_grid = std::max(k1_grid, k1_tiles(wd.f[i].H, wd.f[i].W));
   (void)maxHp; (void)maxWp;
   k_win_init<<<dim3(8, n), 256, 0, st>>>(wd, wb);
   debug_check(st, "k_win_init", -1);
-  const size_t sm1 = k1_smem_bytes(maxS, maxW, rows_cap);
   if (ev0) cudaEventRecord(ev0, st);
-  if (sem) {
-    cudaFuncSetAttribute(k_mask_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
-    k_mask_pass<true><<<K1_PERSIST * nsm, K1_THREADS, sm1, st>>>(wd, wb, P, err, k1_grid, nres, k1_ablate());
-  } else {
-    cudaFuncSetAttribute(k_mask_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
-    k_mask_pass<false><<<K1_PERSIST * nsm, K1_THREADS, sm1, st>>>(wd, wb, P, err, k1_grid, nres, k1_ablate());
+  int64_t maxHW = 1;
+  bool vec = true;
+  for (int i = 0; i < n; ++i) {
+    maxHW = std::max(maxHW, (int64_t)wd.f[i].H * wd.f[i].W);
+    vec = vec && wd.f[i].vec16;
   }
-  debug_check(st, "k_mask_pass", -1);
+  const int items_a = (int)((maxHW + 32 * K1A_SECT - 1) / (32 * K1A_SECT));
+  if (vec) k_masks<true><<<K1A_PERSIST * nsm, K1_THREADS, (size_t)maxS * 16, st>>>(wd, wb, items_a, nres, k1_ablate());
+  else k_masks<false><<<K1A_PERSIST * nsm, K1_THREADS, (size_t)maxS * 16, st>>>(wd, wb, items_a, nres, k1_ablate());
+  debug_check(st, "k_masks", -1);
+  if (sem) k_walk<true><<<K1B_PERSIST * nsm, K1_THREADS, (size_t)maxS * 4, st>>>(wd, wb, P, err, k1_grid, nres, k1_ablate());
+  else k_walk<false><<<K1B_PERSIST * nsm, K1_THREADS, (size_t)maxS * 4, st>>>(wd, wb, P, err, k1_grid, nres, k1_ablate());
+  debug_check(st, "k_walk", -1);
   if (ev1) cudaEventRecord(ev1, st);
   const size_t sm2 = (size_t)maxS * (6 * 4 + 4 + 4);
   const int g2 = 64;
@@ -1231,7 +1219,7 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
     k_finalize<false><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
     debug_check(st, "k_finalize", -1);
   }
-  return sem ? 10 : 6;
+  return sem ? 11 : 7;
 }
 
 }  // namespace disc

@@ -7,5 +7,5 @@ cd "$(dirname "$0")/../paper_2603_03935_b200/csrc"
 make -s ../libdisc.so
 A="-gencode arch=compute_100a,code=sm_100a"
 /usr/local/cuda/bin/nvcc $A -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr "$@" -c k_frame.cu -o build/k_frame_$tag.o
-/usr/local/cuda/bin/nvcc $A -shared -o build/libdisc_$tag.so build/disc_api.o build/k_frame_$tag.o build/k_map.o build/k_query.o -lcudart_static -lrt -ldl -lpthread
+/usr/local/cuda/bin/nvcc $A -shared -o build/libdisc_$tag.so build/disc_api.o build/k_frame_$tag.o build/k_map.o build/k_query.o -lcudart_static -lrt -ldl -lpthread -Xlinker --no-undefined
 echo "$PWD/build/libdisc_$tag.so"
