@@ -424,7 +424,6 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   FrameScratch& X = m->X;
   X.CC = 16384;
   X.TCAP = 3072;
-  X.STCAP = (uint32_t)std::min<int64_t>(cfg->max_memberships + PMAX, 0xFFFFFFF0ll);
   chk(X.ctab_key = dalloc<unsigned long long>(m, X.CC, 0xFF));
   chk(X.ctab_cnt = dalloc<uint32_t>(m, X.CC));
   chk(X.ctab_idx = dalloc<uint32_t>(m, X.TCAP));
@@ -438,7 +437,9 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(X.tgt_phys = dalloc<uint32_t>(m, SM));
   chk(X.tgt_root = dalloc<uint32_t>(m, SM));
   chk(X.tgt_stage = dalloc<uint32_t>(m, SM));
-  chk(X.tgt_fill = dalloc<uint32_t>(m, SM));
+  chk(X.tg_newoff = dalloc<unsigned long long>(m, SM));
+  chk(X.tg_movesrc = dalloc<unsigned long long>(m, SM));
+  chk(X.tg_mvoff = dalloc<uint32_t>(m, SM + 1));
   chk(X.tgt_base = dalloc<uint32_t>(m, SM));
   chk(X.ntgt = dalloc<int32_t>(m, 1));
   chk(X.tg_kind = dalloc<int32_t>(m, SM));
@@ -455,9 +456,7 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(X.seg_base = dalloc<unsigned long long>(m, X.TCAP));
   chk(X.nseg = dalloc<int32_t>(m, 1));
   chk(X.nrel = dalloc<uint32_t>(m, 1));
-  chk(X.stage_slot = dalloc<uint32_t>(m, X.STCAP));
-  chk(X.stage_tgt = dalloc<uint32_t>(m, X.STCAP));
-  chk(X.nstage = dalloc<uint32_t>(m, 1));
+  chk(X.work = dalloc<uint32_t>(m, 1));
   chk(X.rep = dalloc<disc_frame_report>(m, MAXWIN));
   chk(X.live_before = dalloc<int64_t>(m, 1));
   chk(X.ntrip_last = dalloc<uint32_t>(m, 1));

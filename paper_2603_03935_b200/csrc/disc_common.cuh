@@ -162,9 +162,11 @@ struct FrameScratch {
   int64_t* det_id;               // [SMAX]  instance id fused into (debug)
   uint32_t* tgt_phys;            // [SMAX]
   uint32_t* tgt_root;            // [SMAX]
-  uint32_t* tgt_stage;           // [SMAX] staged new entries
-  uint32_t* tgt_fill;            // [SMAX]
-  uint32_t* tgt_base;            // [SMAX]
+  uint32_t* tgt_stage;           // [SMAX] new list entries appended this frame
+  uint32_t* tgt_base;            // [SMAX] list length before the frame
+  unsigned long long* tg_newoff; // [SMAX] arena offset of the (possibly moved) list
+  unsigned long long* tg_movesrc;// [SMAX] old offset when K6 moved the list to a larger region, else ~0
+  uint32_t* tg_mvoff;            // [SMAX+1] prefix offsets of the moved entries (K7 copy items)
   int32_t* ntgt;                 // [1]
   // per-target O12 work lists (written by K6, executed by K7a)
   int32_t* tg_kind;              // [SMAX] 0 = component with instances, 1 = new instance
@@ -182,11 +184,7 @@ struct FrameScratch {
   unsigned long long* seg_base;  // [TCAP] arena offset of the old list
   int32_t* nseg;                 // [1]
   uint32_t* nrel;                // [1] total relabel items
-  // staging of new list entries
-  uint32_t* stage_slot;          // [STCAP]
-  uint32_t* stage_tgt;
-  uint32_t* nstage;              // [1]
-  uint32_t STCAP;
+  uint32_t* work;                // [1] K7 insert-chunk counter (zeroed by K6)
   disc_frame_report* rep;        // [MAXWIN] device reports
   int64_t* live_before;          // [1]
   uint32_t* ntrip_last;          // [1] (debug export)

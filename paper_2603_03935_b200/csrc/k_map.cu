@@ -136,55 +136,110 @@ __device__ __forceinline__ void count_add(const FrameScratch& X, uint64_t code, 
   raise_err(err, DERR_TRIPLES);
 }
 
+struct SlotV {   // a KeySlot read as two 16-byte L2 loads (key and inline labels together)
+  unsigned long long key;
+  uint32_t lab[INLINE_LABELS];
+  uint32_t ovf;
+};
+__device__ __forceinline__ SlotV slot_load(const MapState& M, uint32_t h) {
+  const uint4* p = reinterpret_cast<const uint4*>(M.slots + h);
+  const uint4 a = __ldcg(p), b = __ldcg(p + 1);
+  SlotV v;
+  v.key = (unsigned long long)a.x | ((unsigned long long)a.y << 32);
+  v.lab[0] = a.z; v.lab[1] = a.w; v.lab[2] = b.x; v.lab[3] = b.y; v.lab[4] = b.z;
+  v.ovf = b.w;
+  return v;
+}
+
+// Two pairs per lane, their hash probes in lockstep, so each lane keeps two independent
+// memory chains in flight (the lookup is a latency chain: attributes -> slot -> labels' ids ->
+// count table).
 __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapState& M, const FrameScratch& X) {
   const uint32_t np = min(wb.npairs[f], (uint32_t)wb.PMAX);
   const size_t fo = (size_t)f * wb.PMAX;
   const int lane = threadIdx.x & 31;
   unsigned long long* ktab = wb.ktab + (size_t)f * wb.PC;
   const int32_t* status = wb.status + (size_t)f * wb.SMAX;
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < np; base += stride) {
-    const uint32_t idx = base + lane;
-    uint64_t code = KEY_EMPTY;   // first label's (s, j)
-    uint32_t s = 0, slot = U32_EMPTY;
-    if (idx < np) {
-      s = wb.pinfo[fo + idx];
-      ktab[wb.pfk[fo + idx]] = KEY_EMPTY;   // release the frame key-table cell
-      if (status[s] == 0) {
-        slot = map_find(M, wb.pkey[fo + idx]);
-        if (slot != U32_EMPTY) {
-          const KeySlot& ks = M.slots[slot];
-          int nl = 0;
-          for (int i = 0; i < INLINE_LABELS; ++i) {
-            const uint32_t L = ks.lab[i];
+  const uint32_t stride = 2 * gridDim.x * blockDim.x;
+  const uint32_t hmask = (uint32_t)(M.MC - 1);
+  for (uint32_t base = 2 * (blockIdx.x * blockDim.x + (threadIdx.x & ~31u)); base < np; base += stride) {
+    uint32_t idx[2], s[2], slot[2], h[2];
+    unsigned long long key[2];
+    bool act[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      idx[q] = base + 32 * q + lane;
+      s[q] = 0; slot[q] = U32_EMPTY; key[q] = KEY_EMPTY; act[q] = false;
+      if (idx[q] < np) {
+        s[q] = wb.pinfo[fo + idx[q]];
+        key[q] = wb.pkey[fo + idx[q]];
+        ktab[wb.pfk[fo + idx[q]]] = KEY_EMPTY;   // release the frame key-table cell
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      act[q] = idx[q] < np && status[s[q]] == 0;
+      h[q] = (uint32_t)mix64(key[q]) & hmask;
+    }
+    SlotV sv[2];
+    for (uint32_t probe = 0; (act[0] || act[1]) && probe <= hmask; ++probe) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        if (act[q]) sv[q] = slot_load(M, h[q]);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (!act[q]) continue;
+        if (sv[q].key == key[q]) { slot[q] = h[q]; act[q] = false; }
+        else if (sv[q].key == KEY_EMPTY) act[q] = false;
+        else h[q] = (h[q] + 1) & hmask;
+      }
+    }
+    uint64_t first[2] = {KEY_EMPTY, KEY_EMPTY};   // each pair's first label (s, j), warp-aggregated
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (idx[q] < np) wb.pms[fo + idx[q]] = slot[q];
+      if (slot[q] == U32_EMPTY) continue;
+      uint32_t id[INLINE_LABELS];
+      bool ok[INLINE_LABELS];
+      bool open = true;   // no EMPTY met yet (labels occupy a prefix)
+#pragma unroll
+      for (int i = 0; i < INLINE_LABELS; ++i) {
+        const uint32_t L = sv[q].lab[i];
+        if (L == U32_EMPTY) open = false;
+        ok[i] = open && L != LAB_TOMB;
+        id[i] = ok[i] ? __ldcg(&M.id_of[L]) : 0u;
+      }
+      int nl = 0;
+#pragma unroll
+      for (int i = 0; i < INLINE_LABELS; ++i) {
+        if (!ok[i]) continue;
+        const uint64_t c = ((uint64_t)s[q] << 32) | id[i];
+        if (nl == 0) first[q] = c;
+        else count_add(X, c, 1, M.err);
+        nl++;
+      }
+      if (open) {   // overflow chunks (more than INLINE_LABELS labels on this key)
+        uint32_t nx = sv[q].ovf;
+        while (nx != U32_EMPTY) {
+          const OvfChunk& oc = M.ovf[nx];
+          for (int i = 0; i < CHUNK_LABELS; ++i) {
+            const uint32_t L = __ldcg(&oc.lab[i]);
             if (L == U32_EMPTY) break;
             if (L == LAB_TOMB) continue;
-            const uint64_t c = ((uint64_t)s << 32) | M.id_of[L];
-            if (nl == 0) code = c;
+            const uint64_t c = ((uint64_t)s[q] << 32) | __ldcg(&M.id_of[L]);
+            if (nl == 0) first[q] = c;
             else count_add(X, c, 1, M.err);
             nl++;
           }
-          uint32_t nx = ks.ovf;
-          while (nx != U32_EMPTY) {
-            const OvfChunk& oc = M.ovf[nx];
-            for (int i = 0; i < CHUNK_LABELS; ++i) {
-              const uint32_t L = oc.lab[i];
-              if (L == U32_EMPTY) break;
-              if (L == LAB_TOMB) continue;
-              const uint64_t c = ((uint64_t)s << 32) | M.id_of[L];
-              if (nl == 0) code = c;
-              else count_add(X, c, 1, M.err);
-              nl++;
-            }
-            nx = oc.next;
-          }
+          nx = __ldcg(&oc.next);
         }
       }
-      wb.pms[fo + idx] = slot;
     }
-    // warp aggregation of the first label's count (most keys carry one label)
-    const unsigned peers = __match_any_sync(0xffffffffu, code);
-    if (code != KEY_EMPTY && lane == __ffs(peers) - 1) count_add(X, code, __popc(peers), M.err);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {   // warp aggregation of the first label's count
+      const unsigned peers = __match_any_sync(0xffffffffu, first[q]);
+      if (first[q] != KEY_EMPTY && lane == __ffs(peers) - 1) count_add(X, first[q], __popc(peers), M.err);
+    }
   }
 }
 
@@ -292,6 +347,7 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
   __shared__ uint32_t mcnt_s[256], dcnt_s[256], moff_s[256], doff_s[256];
   __shared__ int64_t tg_vb[256];
   __shared__ int changed;
+  __shared__ uint32_t wcnt_s[K6_THREADS / 32], wcnt2_s[K6_THREADS / 32], rc_s[8], nrel_s, bound_s[256];
   __shared__ unsigned long long rel_s, merged_s, edges_s;
   __shared__ uint32_t gen;
 
@@ -307,8 +363,8 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
     if (*X.ntrip > (uint32_t)TC) raise_err(M.err, DERR_TRIPLES);
     n_j = 0; n_tgt = 0; n_seg = 0; rel_s = 0; merged_s = 0; edges_s = 0;
     gen = (uint32_t)(++M.counters[3]);
-    *X.nstage = 0;
     *X.nrel = 0;
+    *X.work = 0;
   }
   for (int i = tid; i < S + TC; i += blockDim.x) {
     lab[i] = i;
@@ -432,34 +488,46 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
   }
   __syncthreads();
   K6_PROBE(6);
-  // ---- detections: component members, isolated kept ones -> new ids ascending s (R13) ----
-  if (tid == 0) {
-    ncomp_s = n_tgt;
-    int64_t nid = M.counters[0];
-    int64_t created = 0;
-    for (int s = 0; s < S; ++s) {
-      if (d_st[s] != 0) continue;
-      if (has_edge[s]) {
-        const int t = comp_tgt[lab[s]];
-        d_tgt[s] = t;
-        X.det_id[s] = tg_root[t];
-      } else {
-        if (nid >= M.IMAX) {
-          raise_err(M.err, DERR_INSTANCES);
-          break;
-        }
-        const int t = (int)n_tgt++;
+  // ---- detections: component members, isolated kept ones -> new ids ascending s (R13); the
+  // rank of an isolated detection among them is a block-wide exclusive count ----
+  {
+    const int s = tid;
+    const bool kept = s < S && d_st[s] == 0;
+    const bool iso = kept && !has_edge[s];
+    const unsigned b = __ballot_sync(0xffffffffu, iso);
+    if (lane == 0) wcnt_s[warp] = __popc(b);
+    __syncthreads();
+    int before = __popc(b & ((1u << lane) - 1u)), created = 0;
+    for (int w2 = 0; w2 < nwarp; ++w2) {
+      if (w2 < warp) before += wcnt_s[w2];
+      created += wcnt_s[w2];
+    }
+    const int ncomp = (int)n_tgt;
+    const int64_t nid0 = M.counters[0];
+    if (kept && has_edge[s]) {
+      const int t = comp_tgt[lab[s]];
+      d_tgt[s] = t;
+      X.det_id[s] = tg_root[t];
+    } else if (iso) {
+      const int64_t nid = nid0 + before;
+      if (nid < M.IMAX) {
+        const int t = ncomp + before;
         d_tgt[s] = t;
         X.det_id[s] = nid;
         tg_root[t] = (uint32_t)nid;
         tg_phys[t] = (uint32_t)nid;
-        nid++;
-        created++;
+      } else {
+        raise_err(M.err, DERR_INSTANCES);
       }
     }
-    M.counters[0] = nid;
-    M.counters[1] += created;
-    X.rep[f].created = created;
+    __syncthreads();
+    if (tid == 0) {
+      ncomp_s = ncomp;
+      n_tgt = ncomp + created;
+      M.counters[0] = nid0 + created;
+      M.counters[1] += created;
+      X.rep[f].created = created;
+    }
   }
   __syncthreads();
   K6_PROBE(7);
@@ -467,22 +535,37 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
   // ascending; relabel segments for the smaller sets; report sums ----
   const int ncomp = (int)ncomp_s;
   const int ntg = (int)n_tgt;
-  for (int t = tid; t <= S; t += blockDim.x) { mcnt_s[t] = 0; dcnt_s[t] = 0; }
+  for (int t = tid; t <= S; t += blockDim.x) { mcnt_s[t] = 0; dcnt_s[t] = 0; bound_s[t] = 0; }
   __syncthreads();
   for (int l = tid; l < nJ; l += blockDim.x) atomicAdd(&mcnt_s[comp_tgt[lab[S + l]]], 1u);
-  if (tid == 0) {
-    for (int s2 = 0; s2 < S; ++s2)
-      if (d_tgt[s2] >= 0) dcnt_s[d_tgt[s2]]++;
-    uint32_t mo = 0, dof = 0;
-    for (int t = 0; t < ntg; ++t) {
-      moff_s[t] = mo; mo += mcnt_s[t];
-      doff_s[t] = dof; dof += dcnt_s[t];
-      dcnt_s[t] = 0;
+  for (int s2 = tid; s2 < S; s2 += blockDim.x)
+    if (d_tgt[s2] >= 0) {
+      atomicAdd(&dcnt_s[d_tgt[s2]], 1u);
+      atomicAdd(&bound_s[d_tgt[s2]], d_vs[s2]);   // at most |V_s| new entries per detection
     }
-    for (int s2 = 0; s2 < S; ++s2) {
-      const int t = d_tgt[s2];
-      if (t >= 0) X.tg_dets[doff_s[t] + dcnt_s[t]++] = (uint32_t)s2;
+  __syncthreads();
+  {   // exclusive offsets over the targets (ntg <= S <= 255 < blockDim): warp scans + warp totals
+    const int t = tid;
+    uint32_t mc = t < ntg ? mcnt_s[t] : 0u, dc = t < ntg ? dcnt_s[t] : 0u;
+    uint32_t mi = mc, di = dc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t a = __shfl_up_sync(0xffffffffu, mi, o), b2 = __shfl_up_sync(0xffffffffu, di, o);
+      if (lane >= o) { mi += a; di += b2; }
     }
+    if (lane == 31) { wcnt_s[warp] = mi; wcnt2_s[warp] = di; }
+    __syncthreads();
+    uint32_t mb = 0, db = 0;
+    for (int w2 = 0; w2 < warp; ++w2) { mb += wcnt_s[w2]; db += wcnt2_s[w2]; }
+    if (t < ntg) { moff_s[t] = mb + mi - mc; doff_s[t] = db + di - dc; }
+  }
+  __syncthreads();
+  for (int s2 = tid; s2 < S; s2 += blockDim.x) {   // detections of each target, ascending s
+    const int t = d_tgt[s2];
+    if (t < 0) continue;
+    uint32_t rank = 0;
+    for (int s3 = 0; s3 < s2; ++s3) rank += d_tgt[s3] == t;
+    X.tg_dets[doff_s[t] + rank] = (uint32_t)s2;
   }
   __syncthreads();
   for (int l = tid; l < nJ; l += blockDim.x) {
@@ -499,7 +582,9 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
         X.seg_phys[sg] = pm;
         X.seg_tgt[sg] = t;
         X.seg_base[sg] = M.lst_off[pm];
-        X.seg_off[sg] = M.lst_len[pm];
+        const uint32_t len = M.lst_len[pm];
+        t_jl[sg] = (int32_t)len;   // segment length (t_jl is free after the components)
+        atomicAdd(&bound_s[t], len);
       } else {
         raise_err(M.err, DERR_TRIPLES);
       }
@@ -530,33 +615,100 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
   }
   __syncthreads();
   K6_PROBE(9);
-  if (tid == 0) {
-    const uint32_t ns = min(n_seg, (uint32_t)TC);
-    uint32_t acc = 0;
-    for (uint32_t g = 0; g < ns; ++g) {
-      const uint32_t len = X.seg_off[g];
-      X.seg_off[g] = acc;
-      acc += len;
+  // relabel segment offsets: block-wide exclusive scan of the lengths (chunk per thread)
+  const uint32_t ns = min(n_seg, (uint32_t)TC);
+  {
+    const uint32_t per = (ns + blockDim.x - 1) / blockDim.x;
+    const uint32_t g0 = min(ns, tid * per), g1 = min(ns, g0 + per);
+    uint32_t sum = 0;
+    for (uint32_t g = g0; g < g1; ++g) sum += (uint32_t)t_jl[g];
+    uint32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t a = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += a;
     }
-    X.seg_off[ns] = acc;
+    if (lane == 31) wcnt_s[warp] = inc;
+    __syncthreads();
+    uint32_t base = inc - sum, all = 0;
+    for (int w2 = 0; w2 < nwarp; ++w2) {
+      if (w2 < warp) base += wcnt_s[w2];
+      all += wcnt_s[w2];
+    }
+    for (uint32_t g = g0; g < g1; ++g) {
+      X.seg_off[g] = base;
+      base += (uint32_t)t_jl[g];
+    }
+    if (tid == 0) {
+      X.seg_off[ns] = all;
+      nrel_s = all;
+    }
+  }
+  // list capacity: each target's key list is sized for its worst-case growth this frame (one
+  // entry per frame pair of its detections and per relabel item of its segments), moving it to
+  // a larger arena region when needed, so K7 appends in place
+  for (int t = tid; t < (int)n_tgt; t += blockDim.x) {
+    const uint32_t L = tg_phys[t];
+    const bool fresh = t >= (int)ncomp_s;   // new instance: empty list
+    const uint32_t oldlen = fresh ? 0u : M.lst_len[L], cap = fresh ? 0u : M.lst_cap[L];
+    const unsigned long long off = fresh ? 0ull : M.lst_off[L];
+    const uint32_t need = oldlen + bound_s[t];
+    unsigned long long newoff = off, movesrc = ~0ull;
+    if (need > cap) {
+      const uint32_t nc = max(max(2 * cap, need), 64u);
+      const unsigned long long o = atomicAdd(M.arena_top, (unsigned long long)nc);
+      if (o + nc > M.ARENA) {
+        raise_err(M.err, DERR_ARENA);
+      } else {
+        if (oldlen) movesrc = off;
+        newoff = o;
+        M.lst_off[L] = o;
+        M.lst_cap[L] = nc;
+      }
+    }
+    X.tgt_base[t] = oldlen;
+    X.tg_newoff[t] = newoff;
+    X.tg_movesrc[t] = movesrc;
+    bound_s[t] = movesrc != ~0ull ? oldlen : 0u;   // entries K7 copies to the new region
+  }
+  __syncthreads();
+  {   // prefix offsets of the copy items over the targets (n_tgt <= S < blockDim)
+    const int t = tid;
+    const uint32_t c = t < (int)n_tgt ? bound_s[t] : 0u;
+    uint32_t inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t a = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += a;
+    }
+    if (lane == 31) wcnt2_s[warp] = inc;
+    __syncthreads();
+    uint32_t base = 0, all = 0;
+    for (int w2 = 0; w2 < nwarp; ++w2) {
+      if (w2 < warp) base += wcnt2_s[w2];
+      all += wcnt2_s[w2];
+    }
+    if (t < (int)n_tgt) X.tg_mvoff[t] = base + inc - c;
+    if (t == 0) X.tg_mvoff[n_tgt] = all;
+  }
+  // report counts (O13): statuses and U over the detections
+  if (tid < 8) rc_s[tid] = 0;
+  __syncthreads();
+  for (int s2 = tid; s2 < S; s2 += blockDim.x) {
+    const int st = d_st[s2];
+    atomicAdd(&rc_s[st < 5 ? st : 5], 1u);
+    if (st == 0) atomicAdd(&rc_s[6], d_vs[s2]);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const uint32_t acc = nrel_s;
     *X.nseg = (int)ns;
     *X.nrel = acc;
     *X.ntgt = (int)n_tgt;
     disc_frame_report& R = X.rep[f];
-    int kept = 0, da = 0, dc = 0, dasp = 0, dnd = 0, dnf = 0;
-    int64_t U = 0;
-    for (int s = 0; s < S; ++s) {
-      switch (d_st[s]) {
-        case 0: kept++; U += d_vs[s]; break;
-        case 1: da++; break;
-        case 2: dc++; break;
-        case 3: dasp++; break;
-        case 4: dnd++; break;
-        default: dnf++; break;
-      }
-    }
-    R.kept = kept; R.drop_area = da; R.drop_conf = dc; R.drop_aspect = dasp;
-    R.drop_nodepth = dnd; R.drop_nofeat = dnf;
+    const int64_t U = rc_s[6];
+    R.kept = rc_s[0]; R.drop_area = rc_s[1]; R.drop_conf = rc_s[2]; R.drop_aspect = rc_s[3];
+    R.drop_nodepth = rc_s[4]; R.drop_nofeat = rc_s[5];
     R.key_out_of_range = (int64_t)wb.oor[f];
     R.unique_pairs = U;
     R.edges = (int64_t)edges_s;
@@ -578,15 +730,11 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
 // merged component / creation of a new instance); then every block joins the grid-stride loop
 // of detection inserts and small-to-large relabels.
 // ------------------------------------------------------------------------------------------
-constexpr int K7_T = 256;
-
-__device__ void apply_target(int t, int f, const FrameDesc& F, const WinBufs& wb, const MapState& M,
-                             const FrameScratch& X, const Params& P, int sem) {
-  __shared__ float q_s[K7_T];
-  __shared__ int32_t ab_s[6];
-  __shared__ int32_t obs_s;
-  __shared__ int src_s;            // -1 keep, i < mcnt member i, mcnt + k detection k
-  const int tid = threadIdx.x, lane = tid & 31;
+// One O12 target per warp (a few dozen per frame), so every target runs at once and the warps
+// without one start the inserts immediately.
+__device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc& F, const WinBufs& wb,
+                                                  const MapState& M, const FrameScratch& X, const Params& P, int sem) {
+  const int lane = threadIdx.x & 31;
   const size_t fo = (size_t)f * wb.SMAX;
   const double* trk = wb.trk + fo * P.Dt;
   const int kind = X.tg_kind[t];
@@ -597,128 +745,137 @@ __device__ void apply_target(int t, int f, const FrameDesc& F, const WinBufs& wb
   if (kind == 1) {   // new instance from its single detection (O12 last paragraph)
     const uint32_t s = dets[0], id = root;
     const float qs = wb.qf[(fo + s) * 6 + 4];
-    if (tid == 0) {
+    if (lane == 0) {
       M.alive[id] = 1;
       M.phys_of[id] = id;
       M.id_of[id] = id;
       M.vcount[id] = 0;
       M.obs[id] = 1;
       M.last_seen[id] = F.frame_id;
-      for (int k = 0; k < 6; ++k) M.aabb[(size_t)id * 6 + k] = wb.daabb[(fo + s) * 6 + k];
       M.q[id] = qs;
       M.lst_len[id] = 0;
-      M.lst_cap[id] = 0;
     }
-    for (int d = tid; d < P.Dt; d += blockDim.x) M.T[(size_t)id * P.Dt + d] = trk[(size_t)s * P.Dt + d];
+    if (lane < 6) M.aabb[(size_t)id * 6 + lane] = wb.daabb[(fo + s) * 6 + lane];
+    for (int d = lane; d < P.Dt; d += 32) M.T[(size_t)id * P.Dt + d] = trk[(size_t)s * P.Dt + d];
     const bool has_e = sem && qs >= 0.f;
-    for (int d = tid; d < P.Df; d += blockDim.x) M.E[(size_t)id * P.Df + d] = has_e ? wb.emb[(fo + s) * P.Df + d] : 0.f;
-    if (P.Dt > 0 && tid < 32) {
+    const float4* es = (const float4*)(wb.emb + (fo + s) * P.Df);
+    float4* ed = (float4*)(M.E + (size_t)id * P.Df);
+    for (int d4 = lane; d4 < P.Df / 4; d4 += 32) ed[d4] = has_e ? es[d4] : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (P.Dt > 0) {
       const double tt = dot_pin_reg(trk + (size_t)s * P.Dt, trk + (size_t)s * P.Dt, P.Dt);
       if (lane == 0) M.TT[id] = tt;
     }
     return;
   }
   // merged component: root = mem[0] (min id), J = mem[1..], Sd = dets (ascending)
-  if (tid == 0) {
-    obs_s = 0;
-    for (int k = 0; k < 3; ++k) { ab_s[k] = INT32_MAX; ab_s[3 + k] = INT32_MIN; }
-  }
-  __syncthreads();
-  int myobs = 0;
-  for (uint32_t i = tid; i < mcnt + dcnt; i += blockDim.x) {
-    const int32_t* ab;
-    if (i < mcnt) {
-      const uint32_t m = mem[i];
-      myobs += M.obs[m];
-      ab = M.aabb + (size_t)m * 6;
-      if (i < K7_T) q_s[i] = M.q[m];
-    } else {
-      const uint32_t s = dets[i - mcnt];
-      myobs += 1;
-      ab = wb.daabb + (fo + s) * 6;
-      if (i < K7_T) q_s[i] = wb.qf[(fo + s) * 6 + 4];
+  const uint32_t n = mcnt + dcnt;
+  int obs = 0;
+  int32_t ab[6] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MIN, INT32_MIN, INT32_MIN};
+  float qbest = -INFINITY;   // max Q over candidates 1..n-1, first index attaining it
+  int ibest = -1;
+  float q0 = 0.f;
+  for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    float qi = -INFINITY;
+    if (i < n) {
+      const int32_t* a;
+      if (i < mcnt) {
+        const uint32_t m = mem[i];
+        obs += M.obs[m];
+        a = M.aabb + (size_t)m * 6;
+        qi = M.q[m];
+      } else {
+        const uint32_t s = dets[i - mcnt];
+        obs += 1;
+        a = wb.daabb + (fo + s) * 6;
+        qi = wb.qf[(fo + s) * 6 + 4];
+      }
+      for (int k = 0; k < 3; ++k) { ab[k] = min(ab[k], a[k]); ab[3 + k] = max(ab[3 + k], a[3 + k]); }
     }
+    if (i0 == 0) q0 = __shfl_sync(0xffffffffu, qi, 0);
+    const bool cand = i >= 1 && i < n;
+    float qm = cand ? qi : -INFINITY;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) qm = fmaxf(qm, __shfl_xor_sync(0xffffffffu, qm, o));
+    const unsigned hit = __ballot_sync(0xffffffffu, cand && qi == qm);
+    if (qm > qbest && hit) { qbest = qm; ibest = (int)i0 + __ffs(hit) - 1; }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    obs += __shfl_xor_sync(0xffffffffu, obs, o);
+#pragma unroll
     for (int k = 0; k < 3; ++k) {
-      atomicMin(&ab_s[k], ab[k]);
-      atomicMax(&ab_s[3 + k], ab[3 + k]);
+      ab[k] = min(ab[k], __shfl_xor_sync(0xffffffffu, ab[k], o));
+      ab[3 + k] = max(ab[3 + k], __shfl_xor_sync(0xffffffffu, ab[3 + k], o));
     }
   }
-  if (myobs) atomicAdd(&obs_s, myobs);
+  // (e, Q): root's, then J ascending, then Sd ascending, replace iff Q_cand > Q (strict): the
+  // first candidate attaining the maximum, if that maximum exceeds the root's Q
+  const int src = qbest > q0 ? ibest : -1;
   // T_root <- ((T_root + T_j1) + T_j2 ...) + t_s1 ...   elementwise fp64, exactly this order
   double* Tr = M.T + (size_t)root * P.Dt;
-  for (int d = tid; d < P.Dt; d += blockDim.x) {
+  for (int d = lane; d < P.Dt; d += 32) {
     double acc = Tr[d];
     for (uint32_t i = 1; i < mcnt; ++i) acc = __dadd_rn(acc, M.T[(size_t)mem[i] * P.Dt + d]);
     for (uint32_t k = 0; k < dcnt; ++k) acc = __dadd_rn(acc, trk[(size_t)dets[k] * P.Dt + d]);
     Tr[d] = acc;
   }
-  __syncthreads();
-  // (e, Q): root's, then J ascending, then Sd ascending, replace iff Q_cand > Q (strict)
-  if (tid == 0) {
-    float qcur = q_s[0];
-    int src = -1;
-    for (uint32_t i = 1; i < mcnt + dcnt; ++i) {
-      const float qi = i < K7_T ? q_s[i] : (i < mcnt ? M.q[mem[i]] : wb.qf[(fo + dets[i - mcnt]) * 6 + 4]);
-      if (qi > qcur) { qcur = qi; src = (int)i; }
-    }
-    src_s = src;
-    q_s[0] = qcur;
-  }
-  if (P.Dt > 0 && tid < 32) {
+  __syncwarp();
+  if (P.Dt > 0) {
     const double tt = dot_pin_reg(Tr, Tr, P.Dt);
     if (lane == 0) M.TT[root] = tt;
   }
-  __syncthreads();
-  const int src = src_s;
   if (src >= 0) {
-    const float* e = (uint32_t)src < mcnt ? M.E + (size_t)mem[src] * P.Df : wb.emb + (fo + dets[src - mcnt]) * P.Df;
-    for (int d = tid; d < P.Df; d += blockDim.x) M.E[(size_t)root * P.Df + d] = e[d];
+    const float4* e = (const float4*)((uint32_t)src < mcnt ? M.E + (size_t)mem[src] * P.Df
+                                                           : wb.emb + (fo + dets[src - mcnt]) * P.Df);
+    float4* ed = (float4*)(M.E + (size_t)root * P.Df);
+    for (int d4 = lane; d4 < P.Df / 4; d4 += 32) ed[d4] = e[d4];
   }
   // members: key lists of physical labels other than the survivor's were captured by K6 as
-  // relabel segments; reset them, kill J
-  for (uint32_t i = tid; i < mcnt; i += blockDim.x) {
+  // relabel segments; reset them, kill J (same lane per member: read before the kill)
+  for (uint32_t i = lane; i < mcnt; i += 32) {
     const uint32_t m = mem[i];
     const uint32_t pm = M.phys_of[m];
     if (pm != L) {
       M.lst_len[pm] = 0;
       M.lst_cap[pm] = 0;
     }
+    if (i >= 1) {
+      M.alive[m] = 0;
+      M.phys_of[m] = U32_EMPTY;
+    }
   }
-  __syncthreads();
-  for (uint32_t i = 1 + tid; i < mcnt; i += blockDim.x) {
-    const uint32_t m = mem[i];
-    M.alive[m] = 0;
-    M.phys_of[m] = U32_EMPTY;
-  }
-  if (tid == 0) {
-    M.obs[root] = obs_s;
+  if (lane == 0) {
+    M.obs[root] = obs;
     M.last_seen[root] = F.frame_id;
-    for (int k = 0; k < 6; ++k) M.aabb[(size_t)root * 6 + k] = ab_s[k];
-    M.q[root] = q_s[0];
+    M.q[root] = src >= 0 ? qbest : q0;
     M.vcount[root] = X.tg_vbase[t];
     M.phys_of[root] = L;
     M.id_of[L] = root;
   }
+  if (lane < 6) M.aabb[(size_t)root * 6 + lane] = ab[lane];
 }
 
 __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBufs& wb, const MapState& M,
                                          const FrameScratch& X, const Params& P, int sem) {
-  for (int t = blockIdx.x; t < *X.ntgt; t += gridDim.x) {
-    apply_target(t, f, F, wb, M, X, P, sem);
-    __syncthreads();
-  }
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), nw = gridDim.x * (blockDim.x >> 5);
+  const int ntgt = *X.ntgt;
+  for (int t = gw; t < ntgt; t += nw) apply_target_warp(t, f, F, wb, M, X, P, sem);
   const uint32_t np = min(wb.npairs[f], (uint32_t)wb.PMAX);
   const uint32_t nrel = *X.nrel;
-  const uint32_t total = np + nrel;
+  const uint32_t nmove = X.tg_mvoff[ntgt];
+  const uint32_t total = np + nrel + nmove;
   const size_t fo = (size_t)f * wb.PMAX;
   const int nseg = *X.nseg;
-  const int lane = threadIdx.x & 31;
-  __shared__ int delta_s;
-  if (threadIdx.x == 0) delta_s = 0;
-  __syncthreads();
   int delta = 0;
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < total; base += stride) {
+  // items: frame pairs (inserts), relabel items, entries of lists K6 moved (copies); 32-item
+  // chunks from a counter (the target warps take fewer)
+  for (;;) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(X.work, 32u);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= total) break;
     const uint32_t it = base + lane;
     int tnew = -1;
     uint32_t snew = 0;
@@ -731,7 +888,7 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
         if (slot == U32_EMPTY) slot = map_insert_key(M, wb.pkey[fo + it]);
         if (slot != U32_EMPTY && label_insert(M, slot, L)) { tnew = t; snew = slot; delta++; }
       }
-    } else if (it < total) {
+    } else if (it < np + nrel) {
       const uint32_t r = it - np;
       int lo = 0, hi = nseg - 1;   // last segment with seg_off <= r
       while (lo < hi) {
@@ -744,97 +901,48 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
       const uint32_t slot = M.arena[X.seg_base[lo] + (r - X.seg_off[lo])];
       if (label_insert(M, slot, L)) { tnew = t; snew = slot; delta++; }
       if (label_tomb(M, slot, X.seg_phys[lo])) delta--;
-    }
-    // warp-aggregated staging of the new (target, slot) entries
-    const unsigned peers = __match_any_sync(0xffffffffu, tnew);
-    if (tnew >= 0 && lane == __ffs(peers) - 1) atomicAdd(&X.tgt_stage[tnew], (uint32_t)__popc(peers));
-    const unsigned b = __ballot_sync(0xffffffffu, tnew >= 0);
-    if (b) {
-      uint32_t sb = 0;
-      if (lane == 0) sb = atomicAdd(X.nstage, (uint32_t)__popc(b));
-      sb = __shfl_sync(0xffffffffu, sb, 0);
-      if (tnew >= 0) {
-        const uint32_t i = sb + __popc(b & ((1u << lane) - 1u));
-        if (i < X.STCAP) {
-          X.stage_slot[i] = snew;
-          X.stage_tgt[i] = (uint32_t)tnew;
-        } else {
-          raise_err(M.err, DERR_STAGE);
-        }
+    } else if (it < total) {
+      const uint32_t r = it - np - nrel;
+      int lo = 0, hi = ntgt - 1;   // last target with tg_mvoff <= r
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (X.tg_mvoff[mid] <= r) lo = mid;
+        else hi = mid - 1;
       }
+      const uint32_t i = r - X.tg_mvoff[lo];
+      M.arena[X.tg_newoff[lo] + i] = M.arena[X.tg_movesrc[lo] + i];
+    }
+    // append the new (target, slot) entries to the targets' lists (warp-aggregated positions;
+    // K6 reserved the room)
+    const unsigned peers = __match_any_sync(0xffffffffu, tnew);
+    const int leader = __ffs(peers) - 1;
+    uint32_t pb = 0;
+    if (tnew >= 0 && lane == leader) pb = atomicAdd(&X.tgt_stage[tnew], (uint32_t)__popc(peers));
+    pb = __shfl_sync(0xffffffffu, pb, leader);
+    if (tnew >= 0) {
+      const uint32_t pos = X.tgt_base[tnew] + pb + __popc(peers & ((1u << lane) - 1u));
+      M.arena[X.tg_newoff[tnew] + pos] = snew;
     }
   }
-  if (delta) atomicAdd(&delta_s, delta);
-  __syncthreads();
-  if (threadIdx.x == 0 && delta_s) atomicAdd((unsigned long long*)&M.counters[2], (unsigned long long)(int64_t)delta_s);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) delta += __shfl_xor_sync(0xffffffffu, delta, o);
+  if (lane == 0 && delta) atomicAdd((unsigned long long*)&M.counters[2], (unsigned long long)(int64_t)delta);
 }
 
-// K7b: per target — |V| update and list growth
-__device__ __forceinline__ void s2_grow(int f, const MapState& M, const FrameScratch& X) {
+// K7 tail, run in the next phase: list lengths and exact |V| of the frame's targets, insert counter,
+// membership report fields
+__device__ __forceinline__ void s2_finalize(int f, const MapState& M, const FrameScratch& X) {
   const int ntgt = *X.ntgt;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     disc_frame_report& R = X.rep[f];
     R.live_memberships = M.counters[2];
     R.new_memberships = M.counters[2] - *X.live_before;
   }
-  for (int t = blockIdx.x; t < ntgt; t += gridDim.x) {
-  __syncthreads();
-  const uint32_t L = X.tgt_phys[t];
-  const uint32_t root = X.tgt_root[t];
-  const uint32_t add = X.tgt_stage[t];
-  __shared__ unsigned long long newoff;
-  __shared__ uint32_t oldlen, grow;
-  if (threadIdx.x == 0) {
-    M.vcount[root] += add;
-    oldlen = M.lst_len[L];
-    const uint32_t need = oldlen + add;
-    grow = 0;
-    if (need > M.lst_cap[L]) {
-      const uint32_t nc = max(max(2 * M.lst_cap[L], need), 64u);
-      const unsigned long long off = atomicAdd(M.arena_top, (unsigned long long)nc);
-      if (off + nc > M.ARENA) {
-        raise_err(M.err, DERR_ARENA);
-      } else {
-        newoff = off;
-        grow = 1;
-        M.lst_cap[L] = nc;
-      }
-    }
-    X.tgt_base[t] = oldlen;
-    X.tgt_fill[t] = 0;
-  }
-  __syncthreads();
-  if (grow) {
-    const unsigned long long src = M.lst_off[L];
-    for (uint32_t i = threadIdx.x; i < oldlen; i += blockDim.x) M.arena[newoff + i] = M.arena[src + i];
-    __syncthreads();
-    if (threadIdx.x == 0) M.lst_off[L] = newoff;
-  }
-  if (threadIdx.x == 0) {
-    M.lst_len[L] = oldlen + add;
-    atomicAdd((unsigned long long*)&M.counters[5], (unsigned long long)add);
-  }
-  }
-}
-
-// K7c: fill the appended list cells (warp-aggregated positions)
-__device__ __forceinline__ void s2_fill(const MapState& M, const FrameScratch& X) {
-  const uint32_t n = min(*X.nstage, X.STCAP);
-  const int lane = threadIdx.x & 31;
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
-    const uint32_t i = base + lane;
-    const int t = i < n ? (int)X.stage_tgt[i] : -1;
-    const unsigned peers = __match_any_sync(0xffffffffu, t);
-    const int leader = __ffs(peers) - 1;
-    uint32_t pb = 0;
-    if (t >= 0 && lane == leader) pb = atomicAdd(&X.tgt_fill[t], (uint32_t)__popc(peers));
-    pb = __shfl_sync(0xffffffffu, pb, leader);
-    if (t >= 0) {
-      const uint32_t L = X.tgt_phys[t];
-      const uint32_t pos = X.tgt_base[t] + pb + __popc(peers & ((1u << lane) - 1u));
-      M.arena[M.lst_off[L] + pos] = X.stage_slot[i];
-    }
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntgt; t += gridDim.x * blockDim.x) {
+    const uint32_t add = X.tgt_stage[t];
+    M.lst_len[X.tgt_phys[t]] = X.tgt_base[t] + add;
+    M.vcount[X.tgt_root[t]] += add;
+    if (add) atomicAdd((unsigned long long*)&M.counters[5], (unsigned long long)add);
   }
 }
 
@@ -844,7 +952,7 @@ void k6_prof_dump() {
   if (getenv("DISC_S2PROF")) {
     unsigned long long g[8];
     cudaMemcpyFromSymbol(g, g_s2prof, sizeof(g));
-    fprintf(stderr, "s2 phase ns: lookup %llu assoc %llu apply %llu grow %llu fill %llu\n", g[0], g[1], g[2], g[3], g[4]);
+    fprintf(stderr, "s2 phase ns: lookup %llu assoc %llu apply %llu\n", g[0], g[1], g[2]);
   }
   unsigned long long h[16];
   cudaMemcpyFromSymbol(h, g_k6prof, sizeof(h));
@@ -869,8 +977,9 @@ __device__ __forceinline__ void grid_sync(uint32_t* bar, uint32_t target) {
   __syncthreads();
 }
 
-// Stage 2 of a window: the frames' map updates in order, five grid-synchronised phases per frame
-// (K5 lookup, K6 association on CTA 0, K7a apply, K7b grow, K7c fill) in one persistent launch.
+// Stage 2 of a window: the frames' map updates in order, three grid-synchronised phases per frame
+// (K5 lookup with the previous frame's K7 tail, K6 association on CTA 0, K7 apply) in one
+// persistent launch.
 __global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb, MapState M, FrameScratch X,
                                                         Params P, int sem, int prof) {
   const uint32_t G = gridDim.x;
@@ -888,6 +997,7 @@ __global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb
   for (int f = 0; f < wd.n; ++f) {
     const FrameDesc& F = wd.f[f];
     s2_lookup(f, wb, M, X);
+    if (f > 0) s2_finalize(f - 1, M, X);
     grid_sync(wb.s2bar, G * ++ep);
     probe(0);
     if (blockIdx.x == 0) s2_assoc(f, F, wb, M, X, P, sem);
@@ -896,13 +1006,8 @@ __global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb
     s2_apply(f, F, wb, M, X, P, sem);
     grid_sync(wb.s2bar, G * ++ep);
     probe(2);
-    s2_grow(f, M, X);
-    grid_sync(wb.s2bar, G * ++ep);
-    probe(3);
-    s2_fill(M, X);
-    grid_sync(wb.s2bar, G * ++ep);
-    probe(4);
   }
+  if (wd.n > 0) s2_finalize(wd.n - 1, M, X);
 }
 
 int launch_stage2(const WinDesc& wd, const WinBufs& wb, const MapState& M, const FrameScratch& X, const Params& P,
