@@ -351,7 +351,7 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   W.FCHUNKS = (int32_t)((PMP + 63) / 64);
   chk(W.ktab = dalloc<unsigned long long>(m, (size_t)win * PC, 0xFF));
   chk(W.ptab = dalloc<uint32_t>(m, (size_t)win * PC, 0xFF));
-  chk(W.nsum = dalloc<float>(m, (size_t)win * PC * 3, 0));
+  chk(W.nsum = dalloc<float4>(m, (size_t)win * PC, 0));
   chk(W.plist = dalloc<uint32_t>(m, (size_t)win * PMAX));
   chk(W.npairs = dalloc<uint32_t>(m, win));
   chk(W.cnt = dalloc<uint32_t>(m, (size_t)win * SM * PMP));

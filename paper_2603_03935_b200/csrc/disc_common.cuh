@@ -75,7 +75,7 @@ struct Params {                   // method constants
 struct WinBufs {
   unsigned long long* ktab;   // [win][PC] frame key table (packed key)
   uint32_t* ptab;             // [win][PC] frame (s,kslot) pair table (code = s<<24 | kslot)
-  float* nsum;                // [win][PC][3] per-pair normal sums (semantic mode)
+  float4* nsum;               // [win][PC] per-pair normal sums (semantic mode; w unused)
   uint32_t* plist;            // [win][PMAX] pair slots in insertion order
   uint32_t* npairs;           // [win]
   uint32_t* cnt;              // [win][SMAX][PMAXP] mask pixels per patch

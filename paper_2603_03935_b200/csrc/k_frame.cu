@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
     const uint32_t tmask = (uint32_t)wb.PC - 1;
     unsigned long long* ktab = wb.ktab + (size_t)f * wb.PC;
     uint32_t* ptab = wb.ptab + (size_t)f * wb.PC;
-    float* nsum = wb.nsum + (size_t)f * wb.PC * 3;
+    float4* nsum = wb.nsum + (size_t)f * wb.PC;
     auto kt_insert = [&](uint64_t key) -> uint16_t {   // CTA key table -> local key index
       uint32_t h = (uint32_t)mix64(key) & (K1_KT - 1);
       for (int probe = 0; probe < K1_KT; ++probe) {
@@ -492,9 +492,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
       }
       const uint32_t g = global_insert(key, s);
       if (hasn && g != U32_EMPTY) {
-        atomicAdd(&nsum[3 * g + 0], n0);
-        atomicAdd(&nsum[3 * g + 1], n1);
-        atomicAdd(&nsum[3 * g + 2], n2);
+        red_add3(&nsum[g], n0, n1, n2);
       }
       return -1;
     };
@@ -634,11 +632,9 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
       if (SEM) {
         const float4 nn = __ldcg(&nscr[i]);
         if (nn.x != 0.f || nn.y != 0.f || nn.z != 0.f) {
-          __stcg(&nscr[i], make_float4(0.f, 0.f, 0.f, 0.f));   // leave the block all-zero
+          if (!(ablate & 32)) __stcg(&nscr[i], make_float4(0.f, 0.f, 0.f, 0.f));   // leave the block all-zero
           if (g != U32_EMPTY) {
-            atomicAdd(&nsum[3 * g + 0], nn.x);
-            atomicAdd(&nsum[3 * g + 1], nn.y);
-            atomicAdd(&nsum[3 * g + 2], nn.z);
+            red_add3(&nsum[g], nn.x, nn.y, nn.z);
           }
         }
       }
@@ -686,82 +682,91 @@ int k1_nsmid() {
 constexpr int K2_THREADS = 256;
 
 template <bool SEM>
-__global__ void __launch_bounds__(K2_THREADS) k_pairs(WinDesc wd, WinBufs wb, Params P, int* err) {
+__global__ void __launch_bounds__(K2_THREADS) k_pairs(WinDesc wd, WinBufs wb, Params P, int* err, int abl) {
   const int f = blockIdx.y;
   if (f >= wd.n) return;
   const FrameDesc& F = wd.f[f];
   const int S = F.S;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int32_t* ab_s = (int32_t*)smem_raw;            // [S][6]
-  float* as_s = (float*)(ab_s + 6 * S);          // [S]
-  uint32_t* ac_s = (uint32_t*)(as_s + S);        // [S]
-  for (int s = threadIdx.x; s < S; s += blockDim.x) {
+  for (int s = threadIdx.x; s < S; s += blockDim.x)
     for (int k = 0; k < 3; ++k) { ab_s[6 * s + k] = INT32_MAX; ab_s[6 * s + 3 + k] = INT32_MIN; }
-    as_s[s] = 0.f;
-    ac_s[s] = 0;
-  }
   __syncthreads();
   const uint32_t np = min(wb.npairs[f], (uint32_t)wb.PMAX);
   const size_t fo = (size_t)f * wb.PMAX;
   uint32_t* ptab = wb.ptab + (size_t)f * wb.PC;
   const unsigned long long* ktab = wb.ktab + (size_t)f * wb.PC;
-  float* nsum = wb.nsum + (size_t)f * wb.PC * 3;
-  for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < np; idx += gridDim.x * blockDim.x) {
-    const uint32_t ps = wb.plist[fo + idx];
-    if (ps >= (uint32_t)wb.PC) {
-      atomicCAS(err, 0, 1000 + __LINE__);
-      continue;
-    }
-    const uint32_t code = ptab[ps];
-    const uint32_t s = code >> 24, ks = code & 0xFFFFFFu;
-    if (code == U32_EMPTY) {
-      atomicCAS(err, 0, 1000 + __LINE__);
-      continue;
-    }
-    if (s >= (uint32_t)S || ks >= (uint32_t)wb.PC) {
-      atomicCAS(err, 0, 1000 + __LINE__);
-      continue;
-    }
-    const uint64_t key = ktab[ks];
-    wb.pkey[fo + idx] = key;
-    wb.pinfo[fo + idx] = s;
-    wb.pfk[fo + idx] = ks;
-    DISC_CHECK(err, atomicExch(&ptab[ps], U32_EMPTY) == code);
-    int k3[3];
-    unpack_key(key, k3[0], k3[1], k3[2]);
-    for (int a = 0; a < 3; ++a) {
-      atomicMin(&ab_s[6 * s + a], k3[a]);
-      atomicMax(&ab_s[6 * s + 3 + a], k3[a]);
-    }
-    if (SEM) {
-      const float n0 = nsum[3 * ps], n1 = nsum[3 * ps + 1], n2 = nsum[3 * ps + 2];
-      nsum[3 * ps] = 0.f; nsum[3 * ps + 1] = 0.f; nsum[3 * ps + 2] = 0.f;
-      const float nl = sqrtf(n0 * n0 + n1 * n1 + n2 * n2);
-      if (nl > 0.f) {
-        const float r0 = ((float)k3[0] + 0.5f) * P.r - F.pose[3];
-        const float r1 = ((float)k3[1] + 0.5f) * P.r - F.pose[7];
-        const float r2 = ((float)k3[2] + 0.5f) * P.r - F.pose[11];
-        const float rl = sqrtf(r0 * r0 + r1 * r1 + r2 * r2);
-        if (rl > 0.f) {
-          const float dot = (r0 * n0 + r1 * n1 + r2 * n2) / (rl * nl);
-          atomicAdd(&as_s[s], fmaxf(0.f, -dot));
-          atomicAdd(&ac_s[s], 1u);
+  float4* nsum = wb.nsum + (size_t)f * wb.PC;
+  const int lane = threadIdx.x & 31;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < np; base += stride) {
+    const uint32_t idx = base + lane;
+    uint32_t sv = 0xFFFFFFFFu;   // this lane's detection when it has an S_angle term
+    float term = 0.f;
+    if (idx < np) {
+      const uint32_t ps = wb.plist[fo + idx];
+      const uint32_t code = ps < (uint32_t)wb.PC ? ptab[ps] : U32_EMPTY;
+      const uint32_t s = code >> 24, ks = code & 0xFFFFFFu;
+      if (code == U32_EMPTY || s >= (uint32_t)S || ks >= (uint32_t)wb.PC) {
+        atomicCAS(err, 0, 1000 + __LINE__);
+      } else {
+        const uint64_t key = ktab[ks];
+        wb.pkey[fo + idx] = key;
+        wb.pinfo[fo + idx] = s;
+        wb.pfk[fo + idx] = ks;
+        ptab[ps] = U32_EMPTY;   // release the pair-table cell for the next window
+        int k3[3];
+        unpack_key(key, k3[0], k3[1], k3[2]);
+        if (!(abl & 2))
+          for (int a = 0; a < 3; ++a) {
+            atomicMin(&ab_s[6 * s + a], k3[a]);
+            atomicMax(&ab_s[6 * s + 3 + a], k3[a]);
+          }
+        if (SEM && !(abl & 1)) {
+          const float4 nv = __ldcg(&nsum[ps]);
+          const float n0 = nv.x, n1 = nv.y, n2 = nv.z;
+          const float nl = sqrtf(n0 * n0 + n1 * n1 + n2 * n2);
+          if (nl > 0.f) {
+            const float r0 = ((float)k3[0] + 0.5f) * P.r - F.pose[3];
+            const float r1 = ((float)k3[1] + 0.5f) * P.r - F.pose[7];
+            const float r2 = ((float)k3[2] + 0.5f) * P.r - F.pose[11];
+            const float rl = sqrtf(r0 * r0 + r1 * r1 + r2 * r2);
+            if (rl > 0.f) {
+              const float dot = (r0 * n0 + r1 * n1 + r2 * n2) / (rl * nl);
+              term = fmaxf(0.f, -dot);
+              sv = s;
+            }
+          }
         }
+      }
+    }
+    if (SEM && !(abl & 16)) {   // S_angle sums: warp sums per distinct detection, one native RED each
+      unsigned pending = __ballot_sync(0xffffffffu, sv != 0xFFFFFFFFu);
+      while (pending) {
+        const int leader = __ffs(pending) - 1;
+        const uint32_t s0 = __shfl_sync(0xffffffffu, sv, leader);
+        const bool in = sv == s0;
+        float v = in ? term : 0.f;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        const unsigned inb = __ballot_sync(0xffffffffu, in);
+        if (lane == leader) {
+          const size_t gi = (size_t)f * wb.SMAX + s0;
+          atomicAdd(&wb.ang_sum[gi], v);
+          atomicAdd(&wb.ang_cnt[gi], (uint32_t)__popc(inb));
+        }
+        pending &= ~inb;
       }
     }
   }
   __syncthreads();
-  for (int s = threadIdx.x; s < S; s += blockDim.x) {
+  for (int s = threadIdx.x; s < S && !(abl & 4); s += blockDim.x) {
     const size_t gi = (size_t)f * wb.SMAX + s;
     if (ab_s[6 * s] != INT32_MAX) {
       for (int a = 0; a < 3; ++a) {
         atomicMin(&wb.daabb[6 * gi + a], ab_s[6 * s + a]);
         atomicMax(&wb.daabb[6 * gi + 3 + a], ab_s[6 * s + 3 + a]);
       }
-    }
-    if (SEM && ac_s[s]) {
-      atomicAdd(&wb.ang_sum[gi], as_s[s]);
-      atomicAdd(&wb.ang_cnt[gi], ac_s[s]);
     }
   }
 }
@@ -1004,36 +1009,82 @@ __global__ void __launch_bounds__(K4_THREADS) k_pool(WinDesc wd, WinBufs wb, Par
   if (blockIdx.x * K4_WARPS >= B.n) return;
   const uint32_t* cnt = wb.cnt + (size_t)f * wb.SMAX * wb.PMAXP + (size_t)s * wb.PMAXP;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  if (SEM && F.feats) {
-    float* ypart = (float*)smem_raw;                 // [K4_WARPS][Df]
-    const float* D = wb.rp + (size_t)f * wb.PMAXP;
-    const bool fallback = wb.pmode[gi] != 0;
-    const int D4 = Df / 4, nq4 = (D4 + 31) / 32;
-    float4 acc[8];
+  const bool pool = SEM && F.feats;
+  const float* D = wb.rp + (size_t)f * wb.PMAXP;
+  const bool fallback = wb.pmode[gi] != 0;
+  const int D4 = Df / 4, nq4 = (D4 + 31) / 32;
+  const bool tvec = (Dt & 3) == 0;               // tracking rows as 4 x bf16 loads
+  const int nt = tvec ? (Dt / 4 + 31) / 32 : (Dt + 31) / 32;
+  float4 acc[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int k = k0; k < B.n; k += stride) {
-      const int p = B.patch(k, Wp);
-      const uint32_t c = cnt[p];
-      if (!c) continue;
-      float w;
-      if (fallback) {
-        w = 1.0f;
-      } else {
+  for (int i = 0; i < 8; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  double ua[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) ua[i] = 0.0;
+  // one pass over the interleaved bbox patches: D-weighted pooling y_s += w_p f_p (P:128,
+  // R18) and tracking u_s += cnt_sp g_p (R15); the next patch's count and D are fetched ahead
+  int p_n = 0;
+  uint32_t c_n = 0;
+  float d_n = 0.f;
+  auto fetch = [&](int kk) {
+    p_n = B.patch(kk, Wp);
+    c_n = cnt[p_n];
+    d_n = pool ? D[p_n] : 0.f;
+  };
+  if (k0 < B.n) fetch(k0);
+  for (int k = k0; k < B.n; k += stride) {
+    const int p = p_n;
+    const uint32_t c = c_n;
+    const float Dp = d_n;
+    if (k + stride < B.n) fetch(k + stride);
+    if (!c) continue;
+    if (pool) {
+      float w = 1.0f;
+      bool use = true;
+      if (!fallback) {
         const double npix = B.npix(k, H, W, Hp, Wp);
-        if (!((double)c >= (double)P.cover_min * npix)) continue;
-        w = (float)((double)D[p] * ((double)c / npix));
+        use = (double)c >= (double)P.cover_min * npix;
+        w = (float)((double)Dp * ((double)c / npix));
       }
-      const float4* row = (const float4*)(F.feats + (size_t)p * Df);
+      if (use) {
+        const float4* row = (const float4*)(F.feats + (size_t)p * Df);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        if (i < nq4 && lane + 32 * i < D4) {
-          const float4 x = __ldg(row + lane + 32 * i);
-          acc[i].x = fmaf(w, x.x, acc[i].x); acc[i].y = fmaf(w, x.y, acc[i].y);
-          acc[i].z = fmaf(w, x.z, acc[i].z); acc[i].w = fmaf(w, x.w, acc[i].w);
+        for (int i = 0; i < 8; ++i) {
+          if (i < nq4 && lane + 32 * i < D4) {
+            const float4 x = __ldg(row + lane + 32 * i);
+            acc[i].x = fmaf(w, x.x, acc[i].x); acc[i].y = fmaf(w, x.y, acc[i].y);
+            acc[i].z = fmaf(w, x.z, acc[i].z); acc[i].w = fmaf(w, x.w, acc[i].w);
+          }
         }
       }
     }
+    if (Dt > 0) {
+      const double cd = (double)c;
+      if (tvec) {
+        const uint2* g = (const uint2*)(F.track + (size_t)p * Dt);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int j = lane + 32 * i;
+          if (i < nt && j < Dt / 4) {
+            const uint2 v = __ldg(g + j);
+            ua[4 * i + 0] = __dadd_rn(ua[4 * i + 0], __dmul_rn(cd, (double)__uint_as_float(v.x << 16)));
+            ua[4 * i + 1] = __dadd_rn(ua[4 * i + 1], __dmul_rn(cd, (double)__uint_as_float(v.x & 0xFFFF0000u)));
+            ua[4 * i + 2] = __dadd_rn(ua[4 * i + 2], __dmul_rn(cd, (double)__uint_as_float(v.y << 16)));
+            ua[4 * i + 3] = __dadd_rn(ua[4 * i + 3], __dmul_rn(cd, (double)__uint_as_float(v.y & 0xFFFF0000u)));
+          }
+        }
+      } else {
+        const uint16_t* g = F.track + (size_t)p * Dt;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int d = lane + 32 * i;
+          if (i < nt && d < Dt) ua[i] = __dadd_rn(ua[i], __dmul_rn(cd, (double)__uint_as_float((uint32_t)g[d] << 16)));
+        }
+      }
+    }
+  }
+  if (pool) {   // fixed-order reduction over the CTA's warps, then one RED per element
+    float* ypart = (float*)smem_raw;                 // [K4_WARPS][Df]
     float4* yp = (float4*)(ypart + (size_t)warp * Df);
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -1049,26 +1100,19 @@ __global__ void __launch_bounds__(K4_THREADS) k_pool(WinDesc wd, WinBufs wb, Par
   }
   if (Dt > 0) {
     double* upart = (double*)smem_raw;               // [K4_WARPS][Dt] (reuses the pooling scratch)
-    const int nd = (Dt + 31) / 32;
-    double ua[16];
+    if (tvec) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) ua[i] = 0.0;
-    for (int k = k0; k < B.n; k += stride) {
-      const int p = B.patch(k, Wp);
-      const uint32_t c = cnt[p];
-      if (!c) continue;
-      const uint16_t* g = F.track + (size_t)p * Dt;
-      const double cd = (double)c;
+      for (int i = 0; i < 4; ++i) {
+        const int j = lane + 32 * i;
+        if (i < nt && j < Dt / 4)
+          for (int e = 0; e < 4; ++e) upart[(size_t)warp * Dt + 4 * j + e] = ua[4 * i + e];
+      }
+    } else {
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int d = lane + 32 * i;
-        if (i < nd && d < Dt) ua[i] = __dadd_rn(ua[i], __dmul_rn(cd, (double)__uint_as_float((uint32_t)g[d] << 16)));
+        if (i < nt && d < Dt) upart[(size_t)warp * Dt + d] = ua[i];
       }
-    }
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int d = lane + 32 * i;
-      if (i < nd && d < Dt) upart[(size_t)warp * Dt + d] = ua[i];
     }
     __syncthreads();
     double* u = wb.trk + gi * Dt;   // per-mask accumulator u_s (exact sums, R15)
@@ -1170,6 +1214,9 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
   (void)maxHp; (void)maxWp;
   k_win_init<<<dim3(8, n), 256, 0, st>>>(wd, wb);
   debug_check(st, "k_win_init", -1);
+  // per-pair normal sums start from zero: one coalesced memset per window (zeroing the slots
+  // one by one after use costs far more: scattered partial-line writes)
+  if (sem) cudaMemsetAsync(wb.nsum, 0, (size_t)n * wb.PC * sizeof(float4), st);
   if (ev0) cudaEventRecord(ev0, st);
   int64_t maxHW = 1;
   bool vec = true;
@@ -1185,10 +1232,11 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
   else k_walk<false><<<K1B_PERSIST * nsm, K1_THREADS, (size_t)maxS * 4, st>>>(wd, wb, P, err, k1_grid, nres, k1_ablate());
   debug_check(st, "k_walk", -1);
   if (ev1) cudaEventRecord(ev1, st);
-  const size_t sm2 = (size_t)maxS * (6 * 4 + 4 + 4);
+  const size_t sm2 = (size_t)maxS * 6 * 4;
   const int g2 = 64;
-  if (sem) k_pairs<true><<<dim3(g2, n), K2_THREADS, sm2, st>>>(wd, wb, P, err);
-  else k_pairs<false><<<dim3(g2, n), K2_THREADS, sm2, st>>>(wd, wb, P, err);
+  static const int k2abl = getenv("DISC_K2_ABLATE") ? atoi(getenv("DISC_K2_ABLATE")) : 0;   // profiling only
+  if (sem) k_pairs<true><<<dim3(g2, n), K2_THREADS, sm2, st>>>(wd, wb, P, err, k2abl);
+  else k_pairs<false><<<dim3(g2, n), K2_THREADS, sm2, st>>>(wd, wb, P, err, k2abl);
   debug_check(st, "k_pairs", -1);
   if (sem) {
     const int nch = (maxP + K3_ROWS - 1) / K3_ROWS;
