@@ -369,6 +369,8 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(W.fpart = dalloc<double>(m, (size_t)win * W.FCHUNKS * Df));
   chk(W.fbar = dalloc<float>(m, (size_t)win * Df));
   chk(W.rp = dalloc<float>(m, (size_t)win * PMP));
+  chk(W.rbar = dalloc<double>(m, (size_t)win));
+  chk(W.psum = dalloc<double>(m, (size_t)win * SM * 3));
   chk(W.status = dalloc<int32_t>(m, (size_t)win * SM));
   chk(W.qf = dalloc<float>(m, (size_t)win * SM * 6));
   chk(W.emb = dalloc<float>(m, (size_t)win * SM * Df));

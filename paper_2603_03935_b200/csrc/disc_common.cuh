@@ -94,7 +94,9 @@ struct WinBufs {
   // semantic
   double* fpart;              // [win][FCHUNKS][Df] partial column sums
   float* fbar;                // [win][Df]
-  float* rp;                  // [win][PMAXP] residual norms r_p
+  float* rp;                  // [win][PMAXP] residual norms r_p (D_p after k_dmap)
+  double* rbar;               // [win] mean r_p (Eq.1)
+  double* psum;               // [win][SMAX][3] R18 / R19 sums with r_p for D_p: weight sum, sum cover r, sum cover
   int32_t* status;            // [win][SMAX]
   float* qf;                  // [win][SMAX][6] s_size, s_angle, s_sem, s_dist, q, dbar
   float* emb;                 // [win][SMAX][Df]

@@ -130,6 +130,7 @@ __global__ void k_win_init(WinDesc wd, WinBufs wb) {
     wb.vs[i] = 0;
     wb.ang_sum[i] = 0.f;
     wb.ang_cnt[i] = 0;
+    wb.psum[3 * i] = 0.0; wb.psum[3 * i + 1] = 0.0; wb.psum[3 * i + 2] = 0.0;
     wb.bbox[4 * i + 0] = INT32_MAX;
     wb.bbox[4 * i + 1] = INT32_MAX;
     wb.bbox[4 * i + 2] = -1;
@@ -813,30 +814,6 @@ __global__ void __launch_bounds__(256) k_fbar(WinDesc wd, WinBufs wb, int Df) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_resid(WinDesc wd, WinBufs wb, int Df) {
-  const int f = blockIdx.y;
-  if (f >= wd.n) return;
-  const FrameDesc& F = wd.f[f];
-  if (!F.feats) return;
-  const int P = F.Hp * F.Wp;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  const float4* fb = (const float4*)(wb.fbar + (size_t)f * Df);
-  for (int p = warp; p < P; p += nw) {
-    const float4* row = (const float4*)(F.feats + (size_t)p * Df);
-    float acc = 0.f;
-    for (int d4 = lane; d4 < Df / 4; d4 += 32) {
-      const float4 x = __ldg(row + d4);
-      const float4 m = fb[d4];
-      const float a = x.x - m.x, b = x.y - m.y, c = x.z - m.z, e = x.w - m.w;
-      acc = fmaf(a, a, acc); acc = fmaf(b, b, acc); acc = fmaf(c, c, acc); acc = fmaf(e, e, acc);
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) wb.rp[(size_t)f * wb.PMAXP + p] = sqrtf(acc);
-  }
-}
-
 // ------------------------------------------------------------------------------------------
 // K3d: D_p = r_p / (rbar + eps) in place (Eq.1), one CTA per frame, fixed-order reduction.
 // ------------------------------------------------------------------------------------------
@@ -859,6 +836,7 @@ __global__ void __launch_bounds__(1024) k_dmap(WinDesc wd, WinBufs wb, Params P)
     double t = 0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
     red[32] = t / (double)Pn;   // rbar
+    wb.rbar[f] = red[32];
   }
   __syncthreads();
   const double inv = 1.0 / (red[32] + (double)P.eps);
@@ -968,159 +946,201 @@ __global__ void __launch_bounds__(K4_THREADS) k_filter(WinDesc wd, WinBufs wb, P
       wb.tok[gi] = 0;
     }
   }
-  if (status != 0 || !(SEM && F.feats)) return;
-  // weight sums (O7): w = D cnt/npix if cnt >= cover_min npix (exact); D̄ over cnt > 0 (R19)
-  const float* D = wb.rp + (size_t)f * wb.PMAXP;
-  double wsum = 0, dnum = 0, dden = 0;
-  for (int k = threadIdx.x; k < B.n; k += blockDim.x) {
-    const int p = B.patch(k, Wp);
-    const uint32_t c = cnt[p];
-    if (!c) continue;
-    const double npix = B.npix(k, H, W, Hp, Wp);
-    const double cov = (double)c / npix;
-    const double Dp = (double)D[p];
-    dnum += cov * Dp;
-    dden += cov;
-    if ((double)c >= (double)P.cover_min * npix) wsum += Dp * cov;
-  }
-  wsum = block_sum_d(wsum, red);
-  dnum = block_sum_d(dnum, red);
-  dden = block_sum_d(dden, red);
-  if (threadIdx.x == 0) {
-    wb.pmode[gi] = (wsum > 0.0) ? 0 : 1;   // 1: all-zero weights -> unweighted mean (R18)
-    qf[5] = (float)(dden > 0 ? dnum / dden : 0.0);
-  }
+
+}
+
+// ------------------------------------------------------------------------------------------
+// K4b k_poolr: one pass over the frame's patch tokens.  A warp owns a segment of up to
+// K4R_SEG patches of one patch row; for each patch it reads the CLIP row once, forms
+// r_p = |f_p - fbar| (Eq.1 numerator, written for k_dmap) and, for every kept mask covering the
+// patch, adds r_p cover f_p to the mask's pooled sum (P:128 with D_p = r_p / (rbar + eps): the
+// common factor 1 / (rbar + eps) cancels in e_s = y / |y| and in the all-zero test of R18) and
+// cnt g_p to the tracking sum u_s (R15), plus the scalar sums of R18 / R19.  The warp keeps one
+// mask's running sums in its shared-memory slice and flushes them with native REDs when the
+// segment moves on to another mask; the other masks of a boundary patch are reduced directly.
+// ------------------------------------------------------------------------------------------
+constexpr int K4R_SEG = 8;        // patches per warp segment
+constexpr int K4R_WARPS = 4;
+
+__device__ __forceinline__ void red_add4(float4* p, float4 v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+size_t k4r_smem_bytes(int Df, int Dt) {
+  return (size_t)(1 + K4R_WARPS) * Df * 4 + (size_t)K4R_WARPS * Dt * 8;
 }
 
 template <bool SEM>
-__global__ void __launch_bounds__(K4_THREADS) k_pool(WinDesc wd, WinBufs wb, Params P) {
-  const int f = blockIdx.z;
+__global__ void __launch_bounds__(K4R_WARPS * 32) k_poolr(WinDesc wd, WinBufs wb, Params P) {
+  const int f = blockIdx.y;
   if (f >= wd.n) return;
   const FrameDesc& F = wd.f[f];
+  const int H = F.H, W = F.W, Hp = F.Hp, Wp = F.Wp, S = F.S, Df = P.Df, Dt = P.Dt;
+  const bool pool = SEM && F.feats;
+  if (!pool && Dt == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int segs_row = (Wp + K4R_SEG - 1) / K4R_SEG;
+  const int seg = blockIdx.x * K4R_WARPS + warp;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* fb_s = (float*)smem_raw;                                       // [Df] fbar
+  float* ya = fb_s + Df + (size_t)warp * Df;                            // [Df] running pooled sum
+  double* ua = (double*)(fb_s + (size_t)(1 + K4R_WARPS) * Df) + (size_t)warp * Dt;   // [Dt]
+  if (pool)
+    for (int d = threadIdx.x; d < Df; d += blockDim.x) fb_s[d] = wb.fbar[(size_t)f * Df + d];
+  for (int d = lane; d < Df; d += 32) ya[d] = 0.f;
+  for (int d = lane; d < Dt; d += 32) ua[d] = 0.0;
+  __syncthreads();
+  if (seg >= Hp * segs_row) return;
+  const int pr = seg / segs_row, pc0 = (seg - pr * segs_row) * K4R_SEG, pc1 = min(Wp, pc0 + K4R_SEG);
+  const size_t gbase = (size_t)f * wb.SMAX;
+  const uint32_t* cnt = wb.cnt + gbase * wb.PMAXP;
+  const int D4 = Df / 4, nq4 = (D4 + 31) / 32;
+  const int nch = (S + 31) >> 5;   // <= 8 (S <= 255)
+  // this lane's kept flags (status 0) for masks lane, lane + 32, ... (S <= 255)
+  uint32_t keptl = 0;
+  for (int q = 0; q < nch; ++q)
+    if (32 * q + lane < S && wb.status[gbase + 32 * q + lane] == 0) keptl |= 1u << q;
+  const int64_t rows = ((int64_t)(pr + 1) * H + Hp - 1) / Hp - ((int64_t)pr * H + Hp - 1) / Hp;
+  int cur = -1;                     // mask whose sums the warp's slice holds
+  double sc0 = 0, sc1 = 0, sc2 = 0; // its R18 / R19 scalar sums
+  auto flush = [&]() {
+    if (cur < 0) return;
+    const size_t gi = gbase + cur;
+    if (pool) {
+      float4* y = (float4*)(wb.emb + gi * Df);
+      for (int d4 = lane; d4 < D4; d4 += 32) {
+        red_add4(&y[d4], ((float4*)ya)[d4]);
+        ((float4*)ya)[d4] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if (lane == 0) {
+        double* ps = wb.psum + gi * 3;
+        atomicAdd(&ps[0], sc0);
+        atomicAdd(&ps[1], sc1);
+        atomicAdd(&ps[2], sc2);
+      }
+    }
+    double* u = wb.trk + gi * Dt;
+    for (int d = lane; d < Dt; d += 32) {
+      if (ua[d] != 0.0) atomicAdd(&u[d], ua[d]);
+      ua[d] = 0.0;
+    }
+    sc0 = sc1 = sc2 = 0;
+    cur = -1;
+    __syncwarp();
+  };
+  auto prefetch = [&](int pp) {   // the next patch's rows into L2 (one 128-byte line per lane)
+    if (pool && lane * 32 < Df) asm volatile("prefetch.global.L2 [%0];" ::"l"(F.feats + (size_t)pp * Df + lane * 32));
+    if (Dt > 0 && lane * 64 < Dt) asm volatile("prefetch.global.L2 [%0];" ::"l"(F.track + (size_t)pp * Dt + lane * 64));
+  };
+  prefetch(pr * Wp + pc0);
+  for (int pcx = pc0; pcx < pc1; ++pcx) {
+    const int p = pr * Wp + pcx;
+    if (pcx + 1 < pc1) prefetch(p + 1);
+    float4 x[8];
+    float r = 0.f;
+    if (pool) {   // the patch's CLIP row and r_p (k_resid's arithmetic: per-lane fmaf, xor butterfly)
+      const float4* row = (const float4*)(F.feats + (size_t)p * Df);
+      float acc = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        x[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < nq4 && lane + 32 * i < D4) {
+          x[i] = __ldg(row + lane + 32 * i);
+          const float4 m = ((const float4*)fb_s)[lane + 32 * i];
+          const float a = x[i].x - m.x, b = x[i].y - m.y, c = x[i].z - m.z, e = x[i].w - m.w;
+          acc = fmaf(a, a, acc); acc = fmaf(b, b, acc); acc = fmaf(c, c, acc); acc = fmaf(e, e, acc);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      r = sqrtf(acc);
+      if (lane == 0) wb.rp[(size_t)f * wb.PMAXP + p] = r;
+    }
+    // keep the slice's mask if it covers p, else flush it: p's first mask takes the slice
+    if (cur >= 0 && cnt[(size_t)cur * wb.PMAXP + p] == 0) flush();
+    const int64_t cols = ((int64_t)(pcx + 1) * W + Wp - 1) / Wp - ((int64_t)pcx * W + Wp - 1) / Wp;
+    const double npix = (double)(rows * cols);
+    for (int q = 0; q < nch; ++q) {   // the kept masks covering p, 32 per ballot
+      const uint32_t c_l = ((keptl >> q) & 1u) ? cnt[(size_t)(32 * q + lane) * wb.PMAXP + p] : 0u;
+      for (uint32_t todo = __ballot_sync(0xffffffffu, c_l != 0); todo;) {
+        const int b = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int s = 32 * q + b;
+        const uint32_t c = __shfl_sync(0xffffffffu, c_l, b);
+        if (cur < 0) cur = s;
+        const double cov = (double)c / npix;
+        const bool use = (double)c >= (double)P.cover_min * npix;   // R17, exact
+        const float w = (float)((double)r * cov);
+        const uint16_t* g = F.track + (size_t)p * Dt;
+        if (s == cur) {
+          if (pool) {
+            if (use) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                if (i < nq4 && lane + 32 * i < D4) {
+                  float4 a = ((float4*)ya)[lane + 32 * i];
+                  a.x = fmaf(w, x[i].x, a.x); a.y = fmaf(w, x[i].y, a.y);
+                  a.z = fmaf(w, x[i].z, a.z); a.w = fmaf(w, x[i].w, a.w);
+                  ((float4*)ya)[lane + 32 * i] = a;
+                }
+              }
+              sc0 += (double)r * cov;
+            }
+            sc1 += cov * (double)r;
+            sc2 += cov;
+          }
+          for (int d = lane; d < Dt; d += 32)
+            ua[d] = __dadd_rn(ua[d], __dmul_rn((double)c, (double)__uint_as_float((uint32_t)g[d] << 16)));
+        } else {   // another mask of a boundary patch: reduce straight into its sums
+          const size_t gi = gbase + s;
+          if (pool) {
+            if (use) {
+              float4* y = (float4*)(wb.emb + gi * Df);
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (i < nq4 && lane + 32 * i < D4)
+                  red_add4(&y[lane + 32 * i], make_float4(w * x[i].x, w * x[i].y, w * x[i].z, w * x[i].w));
+            }
+            if (lane == 0) {
+              double* ps = wb.psum + gi * 3;
+              if (use) atomicAdd(&ps[0], (double)r * cov);
+              atomicAdd(&ps[1], cov * (double)r);
+              atomicAdd(&ps[2], cov);
+            }
+          }
+          double* u = wb.trk + gi * Dt;
+          for (int d = lane; d < Dt; d += 32)
+            atomicAdd(&u[d], __dmul_rn((double)c, (double)__uint_as_float((uint32_t)g[d] << 16)));
+        }
+      }
+    }
+  }
+  flush();
+}
+
+// R18 fallback: a kept mask whose weights are all zero is pooled unweighted over its patches
+// with cnt > 0 (its weighted sum is exactly zero).  Rare; CTAs of other masks exit at once.
+template <bool SEM>
+__global__ void __launch_bounds__(K4_THREADS) k_fallback(WinDesc wd, WinBufs wb, Params P) {
+  const int f = blockIdx.z;
+  if (!SEM || f >= wd.n) return;
+  const FrameDesc& F = wd.f[f];
   const int s = blockIdx.y;
-  if (s >= F.S) return;
+  if (s >= F.S || !F.feats) return;
   const size_t gi = (size_t)f * wb.SMAX + s;
-  if (wb.status[gi] != 0) return;
-  const int H = F.H, W = F.W, Hp = F.Hp, Wp = F.Wp, Df = P.Df, Dt = P.Dt;
+  if (wb.status[gi] != 0 || wb.psum[gi * 3] > 0.0) return;
+  const int H = F.H, W = F.W, Hp = F.Hp, Wp = F.Wp, Df = P.Df;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const BoxPatches B(wb, gi, H, W, Hp, Wp);
   const int stride = K4_CTAS * K4_WARPS;
-  const int k0 = blockIdx.x * K4_WARPS + warp;   // interleaved: CTA group x warps
-  if (blockIdx.x * K4_WARPS >= B.n) return;
   const uint32_t* cnt = wb.cnt + (size_t)f * wb.SMAX * wb.PMAXP + (size_t)s * wb.PMAXP;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const bool pool = SEM && F.feats;
-  const float* D = wb.rp + (size_t)f * wb.PMAXP;
-  const bool fallback = wb.pmode[gi] != 0;
-  const int D4 = Df / 4, nq4 = (D4 + 31) / 32;
-  const bool tvec = (Dt & 3) == 0;               // tracking rows as 4 x bf16 loads
-  const int nt = tvec ? (Dt / 4 + 31) / 32 : (Dt + 31) / 32;
-  float4 acc[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  double ua[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) ua[i] = 0.0;
-  // one pass over the interleaved bbox patches: D-weighted pooling y_s += w_p f_p (P:128,
-  // R18) and tracking u_s += cnt_sp g_p (R15); the next patch's count and D are fetched ahead
-  int p_n = 0;
-  uint32_t c_n = 0;
-  float d_n = 0.f;
-  auto fetch = [&](int kk) {
-    p_n = B.patch(kk, Wp);
-    c_n = cnt[p_n];
-    d_n = pool ? D[p_n] : 0.f;
-  };
-  if (k0 < B.n) fetch(k0);
-  for (int k = k0; k < B.n; k += stride) {
-    const int p = p_n;
-    const uint32_t c = c_n;
-    const float Dp = d_n;
-    if (k + stride < B.n) fetch(k + stride);
-    if (!c) continue;
-    if (pool) {
-      float w = 1.0f;
-      bool use = true;
-      if (!fallback) {
-        const double npix = B.npix(k, H, W, Hp, Wp);
-        use = (double)c >= (double)P.cover_min * npix;
-        w = (float)((double)Dp * ((double)c / npix));
-      }
-      if (use) {
-        const float4* row = (const float4*)(F.feats + (size_t)p * Df);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if (i < nq4 && lane + 32 * i < D4) {
-            const float4 x = __ldg(row + lane + 32 * i);
-            acc[i].x = fmaf(w, x.x, acc[i].x); acc[i].y = fmaf(w, x.y, acc[i].y);
-            acc[i].z = fmaf(w, x.z, acc[i].z); acc[i].w = fmaf(w, x.w, acc[i].w);
-          }
-        }
-      }
-    }
-    if (Dt > 0) {
-      const double cd = (double)c;
-      if (tvec) {
-        const uint2* g = (const uint2*)(F.track + (size_t)p * Dt);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int j = lane + 32 * i;
-          if (i < nt && j < Dt / 4) {
-            const uint2 v = __ldg(g + j);
-            ua[4 * i + 0] = __dadd_rn(ua[4 * i + 0], __dmul_rn(cd, (double)__uint_as_float(v.x << 16)));
-            ua[4 * i + 1] = __dadd_rn(ua[4 * i + 1], __dmul_rn(cd, (double)__uint_as_float(v.x & 0xFFFF0000u)));
-            ua[4 * i + 2] = __dadd_rn(ua[4 * i + 2], __dmul_rn(cd, (double)__uint_as_float(v.y << 16)));
-            ua[4 * i + 3] = __dadd_rn(ua[4 * i + 3], __dmul_rn(cd, (double)__uint_as_float(v.y & 0xFFFF0000u)));
-          }
-        }
-      } else {
-        const uint16_t* g = F.track + (size_t)p * Dt;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int d = lane + 32 * i;
-          if (i < nt && d < Dt) ua[i] = __dadd_rn(ua[i], __dmul_rn(cd, (double)__uint_as_float((uint32_t)g[d] << 16)));
-        }
-      }
-    }
-  }
-  if (pool) {   // fixed-order reduction over the CTA's warps, then one RED per element
-    float* ypart = (float*)smem_raw;                 // [K4_WARPS][Df]
-    float4* yp = (float4*)(ypart + (size_t)warp * Df);
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (i < nq4 && lane + 32 * i < D4) yp[lane + 32 * i] = acc[i];
-    __syncthreads();
-    float* y = wb.emb + gi * Df;   // per-mask accumulator (zeroed by k_win_init)
-    for (int d = threadIdx.x; d < Df; d += blockDim.x) {
-      float a = 0.f;
-      for (int w2 = 0; w2 < K4_WARPS; ++w2) a += ypart[(size_t)w2 * Df + d];
-      if (a != 0.f) atomicAdd(&y[d], a);
-    }
-    __syncthreads();
-  }
-  if (Dt > 0) {
-    double* upart = (double*)smem_raw;               // [K4_WARPS][Dt] (reuses the pooling scratch)
-    if (tvec) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int j = lane + 32 * i;
-        if (i < nt && j < Dt / 4)
-          for (int e = 0; e < 4; ++e) upart[(size_t)warp * Dt + 4 * j + e] = ua[4 * i + e];
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int d = lane + 32 * i;
-        if (i < nt && d < Dt) upart[(size_t)warp * Dt + d] = ua[i];
-      }
-    }
-    __syncthreads();
-    double* u = wb.trk + gi * Dt;   // per-mask accumulator u_s (exact sums, R15)
-    for (int d = threadIdx.x; d < Dt; d += blockDim.x) {
-      double a = 0.0;
-      for (int w2 = 0; w2 < K4_WARPS; ++w2) a = __dadd_rn(a, upart[(size_t)w2 * Dt + d]);
-      if (a != 0.0) atomicAdd(&u[d], a);
-    }
+  float* y = wb.emb + gi * Df;
+  for (int k = blockIdx.x * K4_WARPS + warp; k < B.n; k += stride) {
+    const int p = B.patch(k, Wp);
+    if (!cnt[p]) continue;
+    const float* row = F.feats + (size_t)p * Df;
+    for (int d = lane; d < Df; d += 32) atomicAdd(&y[d], row[d]);
   }
 }
 
@@ -1168,7 +1188,11 @@ __global__ void __launch_bounds__(K4_THREADS) k_finalize(WinDesc wd, WinBufs wb,
       const double s_angle = ac ? (double)wb.ang_sum[gi] / (double)ac : 0.0;
       double s_sem = 1.0;
       if (F.gemb) s_sem = gg > 0 ? fmin(fmax(eg / sqrt(gg), 0.0), 1.0) : 0.0;
-      const double dbar = (double)qf[5];
+      // R19: D-bar = sum(cover D) / sum(cover) with D = r / (rbar + eps)
+      const double* ps = wb.psum + gi * 3;
+      const double dbar = ps[2] > 0.0 ? ps[1] / ps[2] / (wb.rbar[f] + (double)P.eps) : 0.0;
+      qf[5] = (float)dbar;
+      wb.pmode[gi] = ps[0] > 0.0 ? 0 : 1;   // 1: all-zero weights -> unweighted pooling (R18)
       const double s_dist = 0.5 + 0.5 * dbar;
       qf[0] = (float)s_size; qf[1] = (float)s_angle; qf[2] = (float)s_sem; qf[3] = (float)s_dist;
       qf[4] = (float)(((s_size * s_angle) * s_sem) * s_dist);
@@ -1244,30 +1268,38 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
     debug_check(st, "k_fbar_part", -1);
     k_fbar<<<dim3((P.Df + 255) / 256, n), 256, 0, st>>>(wd, wb, P.Df);
     debug_check(st, "k_fbar", -1);
-    k_resid<<<dim3((maxP + 7) / 8, n), 256, 0, st>>>(wd, wb, P.Df);
-    debug_check(st, "k_resid", -1);
-    k_dmap<<<n, 1024, 0, st>>>(wd, wb, P);
-    debug_check(st, "k_dmap", -1);
   }
-  const size_t smp = std::max((size_t)K4_WARPS * P.Df * 4, (size_t)K4_WARPS * std::max(P.Dt, 1) * 8);
-  cudaFuncSetAttribute(k_pool<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);
-  cudaFuncSetAttribute(k_pool<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);
+  int segs = 1;
+  for (int i = 0; i < n; ++i)
+    segs = std::max(segs, wd.f[i].Hp * ((wd.f[i].Wp + K4R_SEG - 1) / K4R_SEG));
+  const dim3 gpr((segs + K4R_WARPS - 1) / K4R_WARPS, n);
+  const size_t smr = k4r_smem_bytes(P.Df, P.Dt);
+  static size_t smr_set = 0;
+  if (smr != smr_set) {
+    cudaFuncSetAttribute(k_poolr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
+    cudaFuncSetAttribute(k_poolr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
+    smr_set = smr;
+  }
   if (sem) {
     k_filter<true><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
     debug_check(st, "k_filter", -1);
-    k_pool<true><<<dim3(K4_CTAS, maxS, n), K4_THREADS, smp, st>>>(wd, wb, P);
-    debug_check(st, "k_pool", -1);
+    k_poolr<true><<<gpr, K4R_WARPS * 32, smr, st>>>(wd, wb, P);
+    debug_check(st, "k_poolr", -1);
+    k_dmap<<<n, 1024, 0, st>>>(wd, wb, P);
+    debug_check(st, "k_dmap", -1);
+    k_fallback<true><<<dim3(K4_CTAS, maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
+    debug_check(st, "k_fallback", -1);
     k_finalize<true><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
     debug_check(st, "k_finalize", -1);
   } else {
     k_filter<false><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
     debug_check(st, "k_filter", -1);
-    k_pool<false><<<dim3(K4_CTAS, maxS, n), K4_THREADS, smp, st>>>(wd, wb, P);
-    debug_check(st, "k_pool", -1);
+    k_poolr<false><<<gpr, K4R_WARPS * 32, smr, st>>>(wd, wb, P);
+    debug_check(st, "k_poolr", -1);
     k_finalize<false><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
     debug_check(st, "k_finalize", -1);
   }
-  return sem ? 11 : 7;
+  return sem ? 12 : 7;
 }
 
 }  // namespace disc
