@@ -1020,7 +1020,11 @@ int launch_stage2(const WinDesc& wd, const WinBufs& wb, const MapState& M, const
   }
   const int grid = nres > 0 ? nres : std::min(16, nsm);
   static const int prof = getenv("DISC_S2PROF") ? 1 : 0;
-  k_stage2<<<grid, K6_THREADS, sm6, st>>>(wd, wb, M, X, P, sem ? 1 : 0, prof);
+  // cooperative launch: its CTAs wait on one another at the grid barriers, so co-residency must
+  // be guaranteed, not assumed
+  int semi = sem ? 1 : 0;
+  void* args[] = {(void*)&wd, (void*)&wb, (void*)&M, (void*)&X, (void*)&P, (void*)&semi, (void*)&prof};
+  cudaLaunchCooperativeKernel((const void*)k_stage2, dim3(grid), dim3(K6_THREADS), args, sm6, st);
   debug_check(st, "k_stage2", -1);
   return 1;
 }
