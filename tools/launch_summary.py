@@ -7,7 +7,7 @@ rows = list(csv.reader(open(sys.argv[1])))
 hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
 h = rows[hi]
 data = [dict(zip(h, r)) for r in rows[hi + 1:] if len(r) == len(h)]
-scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
 agg = collections.OrderedDict()
 for d in data:
     if d.get("Metric Name") != "gpu__time_duration.sum":

@@ -9,8 +9,13 @@ WANT = ["Duration", "DRAM Throughput", "Memory Throughput", "Compute (SM) Throug
         "Dynamic Shared Memory Per Block", "Grid Size", "Theoretical Occupancy"]
 
 
-def details(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
+def _k(kernel):
+    return ["-k", f"regex:{kernel}"] if kernel else []
+
+
+def details(rep, kernel=None):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"] + _k(kernel), capture_output=True,
+                         text=True).stdout
     r = list(csv.reader(out.splitlines()))
     h = r[0]
     res = {}
@@ -21,8 +26,9 @@ def details(rep):
     return res
 
 
-def raw(rep, names):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+def raw(rep, names, kernel=None):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"] + _k(kernel), capture_output=True,
+                         text=True).stdout
     r = list(csv.reader(out.splitlines()))
     h, u = r[0], r[1]
     res = {}
@@ -34,8 +40,8 @@ def raw(rep, names):
     return res
 
 
-def hot_lines(rep, top=20):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+def hot_lines(rep, top=20, kernel=None):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"] + _k(kernel),
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     def f(x):
