@@ -379,9 +379,7 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(W.pmode = dalloc<uint8_t>(m, (size_t)win * SM));
   chk(W.k1ctr = dalloc<uint32_t>(m, 2));
   W.MPIX = ((int64_t)cfg->max_pixels + 31) / 32 * 32;   // flat per-frame maps, sector-aligned
-  W.MOVF = W.MPIX / 32;
-  chk(W.m0map = dalloc<uint8_t>(m, (size_t)win * W.MPIX));
-  chk(W.ovfmap = dalloc<uint32_t>(m, (size_t)win * W.MOVF));
+  chk(W.m0map = dalloc<uint16_t>(m, (size_t)win * W.MPIX));
   chk(W.s2bar = dalloc<uint32_t>(m, 1));
   }
   {  // K1 normal-sum scratch, shared by both window buffers (K1 launches are stream-ordered)

@@ -107,9 +107,9 @@ struct WinBufs {
   float4* k1scr;              // [nsmid][K1_SLOTS_PER_SM][K1_PT], all-zero between CTAs
   uint32_t* k1slot;           // [nsmid] bitmask of the SM's blocks in use
   uint32_t* k1ctr;            // [2] K1a / K1b work-item counters (zeroed by K0)
-  uint8_t* m0map;             // [win][MPIX] first mask per pixel (0xFF none), written by K1a
-  uint32_t* ovfmap;           // [win][MOVF] per row, bit per pixel: in a second mask (R9)
-  int64_t MPIX, MOVF;
+  uint16_t* m0map;            // [win][MPIX] per pixel: first mask (low byte, 0xFF none), bit 8 = in a
+                              // second mask (R9); written by K1a
+  int64_t MPIX;
   uint32_t* s2bar;            // [1] stage-2 grid barrier counter (zeroed by K0)
   int32_t PC;                 // frame table capacity (power of 2)
   int32_t PMAX, SMAX, PMAXP, FCHUNKS;

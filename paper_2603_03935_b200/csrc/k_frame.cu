@@ -364,15 +364,24 @@ __global__ void __launch_bounds__(K1_THREADS, K1A_PERSIST) k_masks(WinDesc wd, W
         }
       }
     }
-    if (nv) {   // m0 / ovf maps (flat, sector-aligned)
-      uint8_t* mo = wb.m0map + (size_t)f * wb.MPIX + p0;
+    if (nv) {   // first-mask map, u16 per pixel: m0 | (in a second mask) << 8 (flat, 64-B aligned)
+      uint16_t* mo = wb.m0map + (size_t)f * wb.MPIX + p0;
       if (VEC) {
-        ((uint4*)mo)[0] = make_uint4(m0[0], m0[1], m0[2], m0[3]);
-        ((uint4*)mo)[1] = make_uint4(m0[4], m0[5], m0[6], m0[7]);
+#pragma unroll
+        for (int t = 0; t < 8; t += 2) {
+          uint32_t q[4];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t w = m0[t + h], ob = ovf >> (4 * (t + h));
+            q[2 * h] = __byte_perm(w, 0, 0x4140) | ((ob & 1u) << 8) | (((ob >> 1) & 1u) << 24);
+            q[2 * h + 1] = __byte_perm(w, 0, 0x4342) | (((ob >> 2) & 1u) << 8) | (((ob >> 3) & 1u) << 24);
+          }
+          ((uint4*)mo)[t / 2] = make_uint4(q[0], q[1], q[2], q[3]);
+        }
       } else {
-        for (int j = 0; j < nv; ++j) mo[j] = (uint8_t)(m0[j >> 2] >> (8 * (j & 3)));
+        for (int j = 0; j < nv; ++j)
+          mo[j] = (uint16_t)(((m0[j >> 2] >> (8 * (j & 3))) & 0xFFu) | (((ovf >> j) & 1u) << 8));
       }
-      wb.ovfmap[(size_t)f * wb.MOVF + (p0 >> 5)] = ovf & inb;
     }
     __syncthreads();
     for (int s = threadIdx.x; s < S; s += blockDim.x) {
@@ -511,11 +520,9 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
       const float xh = h_on ? __fdiv_rn(__fsub_rn((float)uh, F.cx), F.fx) : 0.f;
       const float* dcol = F.depth + (col_on ? u : 0);
       const float* dhal = F.depth + (h_on ? uh : 0);
-      const uint8_t* mcol = wb.m0map + (size_t)f * wb.MPIX + (col_on ? u : 0);
-      const uint32_t* ovm = wb.ovfmap + (size_t)f * wb.MOVF;   // flat: bit p & 31 of word p >> 5
-      auto wpt = [&](float d, float x, int r, float p[3]) -> bool {   // r = v - vt0 + 1
+      const uint16_t* mcol = wb.m0map + (size_t)f * wb.MPIX + (col_on ? u : 0);
+      auto wpt = [&](float d, float x, float yb, float p[3]) -> bool {
         if (!depth_valid(d, P)) return false;
-        const float yb = yb_s[r];
         const float xc = __fmul_rn(x, d), yc = __fmul_rn(yb, d), zc = d;
         const float4 a = pose_s[0], b = pose_s[1], c = pose_s[2];
         p[0] = __fmaf_rn(a.x, xc, __fmaf_rn(a.y, yc, __fmaf_rn(a.z, zc, a.w)));
@@ -524,40 +531,56 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
         return true;
       };
       auto drow = [&](const float* base, bool on, int vv) -> float {   // 0 (invalid) off-image
-        return (on && vv >= 0 && vv < H) ? __ldg(base + vv * W) : 0.f;
+        const float d = __ldg(base + min(max(vv, 0), H - 1) * W);   // in-bounds address, no branch
+        return (on && (unsigned)vv < (unsigned)H) ? d : 0.f;
+      };
+      // R6 range test alone, for pixels in no mask (only key_out_of_range needs them): exact
+      // fast accept when |x| <= 2^19 r, else the pinned key
+      auto in_range = [&](const float p[3]) -> bool {
+        const float lim = 524288.0f * rv;
+        if (fabsf(p[0]) <= lim && fabsf(p[1]) <= lim && fabsf(p[2]) <= lim) return true;
+        uint64_t k;
+        return point_key_fast(p, rv, rinv, k);
       };
       float pu[3] = {0.f, 0.f, 0.f}, pc[3] = {0.f, 0.f, 0.f};
-      bool vu = SEM ? wpt(drow(dcol, col_on, vt0 - 1), xa, 0, pu) : false;
-      bool vc = wpt(drow(dcol, col_on, vt0), xa, 1, pc);
+      float ybc = yb_s[1];   // the centre row's yb (halo pixels)
+      bool vu = SEM ? wpt(drow(dcol, col_on, vt0 - 1), xa, yb_s[0], pu) : false;
+      bool vc = wpt(drow(dcol, col_on, vt0), xa, ybc, pc);
+      uint32_t mv_c = col_on ? mcol[vt0 * W] : 0xFFu;   // m0 | overlap << 8
       uint64_t kc = KEY_EMPTY;
-      bool kvc = vc && point_key_fast(pc, rv, rinv, kc);
+      bool kvc = vc && ((mv_c & 0xFFu) != 0xFFu ? point_key_fast(pc, rv, rinv, kc) : in_range(pc));
       float d_dn = drow(dcol, col_on, vt0 + 1);
       float d_h = drow(dhal, h_on, vt0);
-      uint32_t m_c = col_on ? mcol[vt0 * W] : 0xFFu;
-      auto ovbit = [&](int vv) -> uint32_t {   // pixel (vv, u) is in a second mask
-        const int64_t p = (int64_t)vv * W + u;
-        return col_on ? (ovm[p >> 5] >> (p & 31)) & 1u : 0u;
-      };
-      uint32_t ov_c = ovbit(vt0);
-      uint64_t ck = KEY_EMPTY;   // the lane's last emitted item (rows repeat voxels): key, s, pair slot
-      uint32_t cs = 0xFFFFFFFFu, cps = 0;
+      // the lane's pending item (rows repeat voxels): while its run tails keep the same (s, key)
+      // the normals are summed in registers; the item is emitted once, when it changes
+      uint64_t ck = KEY_EMPTY;
+      uint32_t cs = 0xFFFFFFFFu;
+      float pn0 = 0.f, pn1 = 0.f, pn2 = 0.f;
+      // running row pointers (no per-row index arithmetic): depth two rows ahead, halo depth and
+      // first-mask entry one row ahead; a pointer past the image is never dereferenced
+      const float* dp = dcol + (int64_t)(vt0 + 2) * W;
+      const float* hp = dhal + (int64_t)(vt0 + 1) * W;
+      const uint16_t* mp = mcol + (int64_t)(vt0 + 1) * W;
+      const int lim2 = col_on ? H - vt0 - 2 : -1;   // rr < lim2: row vv + 2 exists (and the column)
+      const int limh = h_on ? H - vt0 - 1 : -1;
       for (int rr = 0; rr < rows; ++rr) {
         const int vv = vt0 + rr;
         // the next row's loads go out before this row's arithmetic
-        const float d_dn2 = drow(dcol, col_on, vv + 2);
-        const float d_h2 = drow(dhal, h_on, vv + 1);
+        const float d_dn2 = rr < lim2 ? __ldg(dp) : 0.f;
+        const float d_h2 = rr < limh ? __ldg(hp) : 0.f;
         const bool more = rr + 1 < rows;
-        const uint32_t m_n = (col_on && more) ? mcol[(vv + 1) * W] : 0xFFu;
-        const uint32_t ov_n = more ? ovbit(vv + 1) : 0u;
+        const uint32_t mv_n = (col_on && more) ? (uint32_t)*mp : 0xFFu;
+        dp += W; hp += W; mp += W;
+        const float ybn = yb_s[rr + 2];
         float pd[3] = {0.f, 0.f, 0.f};
-        const bool vd = wpt(d_dn, xa, rr + 2, pd);
-        const uint32_t m = m_c;
+        const bool vd = wpt(d_dn, xa, ybn, pd);
+        const uint32_t m = mv_c & 0xFFu;
         if (vc && !kvc) my_oor++;
         const bool item = m != 0xFFu && kvc;
         float n0 = 0.f, n1 = 0.f, n2 = 0.f;
         if (SEM && !(ablate & 8)) {
           float hx[3] = {0.f, 0.f, 0.f};
-          const bool vh = h_on && wpt(d_h, xh, rr + 1, hx);
+          const bool vh = h_on && wpt(d_h, xh, ybc, hx);
           float pl[3], pr[3];
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
@@ -590,10 +613,10 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
         const unsigned heads = __ballot_sync(0xffffffffu, item && !same_prev);
         if (items) {
           const float q0 = n0, q1 = n1, q2 = n2;   // this pixel's own normal
-          if (SEM) {   // segmented inclusive scan over the runs
+          if (SEM) {   // segmented inclusive scan over the runs (only as many steps as the longest run)
             const int start = 31 - __clz(heads & (0xFFFFFFFFu >> (31 - lane)));
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
+            const int maxd = (int)__reduce_max_sync(0xffffffffu, item ? (uint32_t)(lane - start) : 0u);
+            for (int o = 1; o <= maxd; o <<= 1) {
               const float a0 = __shfl_up_sync(0xffffffffu, n0, o);
               const float a1 = __shfl_up_sync(0xffffffffu, n1, o);
               const float a2 = __shfl_up_sync(0xffffffffu, n2, o);
@@ -602,14 +625,14 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
           }
           const bool tail = item && !(((items & ~heads) >> 1 >> lane) & 1u);
           if (tail) {
-            if (kc == ck && m == cs) {   // same voxel and mask as the lane's previous item
-              if (SEM && (n0 != 0.f || n1 != 0.f || n2 != 0.f)) red_add3(&nscr[cps], n0, n1, n2);
+            if (kc == ck && m == cs) {
+              pn0 += n0; pn1 += n1; pn2 += n2;
             } else {
-              const int ps = emit(m, kc, n0, n1, n2);
-              if (ps >= 0) { ck = kc; cs = m; cps = (uint32_t)ps; }
+              if (cs != 0xFFFFFFFFu) emit(cs, ck, pn0, pn1, pn2);
+              ck = kc; cs = m; pn0 = n0; pn1 = n1; pn2 = n2;
             }
           }
-          if (item && ov_c) {   // other masks of this pixel (R9), per pixel
+          if (item && (mv_c >> 8)) {   // other masks of this pixel (R9), per pixel
             const size_t pix = (size_t)vv * W + u;
             for (int s2 = (int)m + 1; s2 < S; ++s2)
               if (F.masks[(size_t)s2 * H * W + pix]) emit((uint32_t)s2, kc, q0, q1, q2);
@@ -618,9 +641,10 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
         pu[0] = pc[0]; pu[1] = pc[1]; pu[2] = pc[2]; vu = vc;
         pc[0] = pd[0]; pc[1] = pd[1]; pc[2] = pd[2]; vc = vd;
         kc = KEY_EMPTY;
-        kvc = vc && point_key_fast(pc, rv, rinv, kc);
-        d_dn = d_dn2; d_h = d_h2; m_c = m_n; ov_c = ov_n;
+        kvc = vc && ((mv_n & 0xFFu) != 0xFFu ? point_key_fast(pc, rv, rinv, kc) : in_range(pc));
+        d_dn = d_dn2; d_h = d_h2; mv_c = mv_n; ybc = ybn;
       }
+      if (cs != 0xFFFFFFFFu) emit(cs, ck, pn0, pn1, pn2);
     }
     if (my_oor) atomicAdd(&oor_s, my_oor);
     if (SEM) __threadfence();   // this thread's normal reductions before the reads below
