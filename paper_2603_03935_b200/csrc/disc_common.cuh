@@ -11,7 +11,10 @@
 namespace disc {
 
 constexpr int MAXWIN = 32;
-constexpr int K1_PT = 1024;           // K1 CTA pair slots (two per CTA key-table slot)
+#ifndef K1_PT_SLOTS
+#define K1_PT_SLOTS 2048   // a far wall puts ~1000 distinct voxels in one 32x128 tile
+#endif
+constexpr int K1_PT = K1_PT_SLOTS;         // K1 CTA pair slots (two per CTA key-table slot)
 constexpr int K1_SLOTS_PER_SM = 16;    // K1 scratch blocks per SM (>= resident K1 CTAs per SM)
 constexpr uint64_t KEY_EMPTY = ~0ull;       // valid packed keys have bit 63 clear (R6)
 constexpr uint32_t U32_EMPTY = 0xFFFFFFFFu;

@@ -4,8 +4,13 @@
 set -e
 tag=$1; shift
 cd "$(dirname "$0")/../paper_2603_03935_b200/csrc"
-make -s ../libdisc.so
+mkdir -p build/var_$tag
 A="-gencode arch=compute_100a,code=sm_100a"
-/usr/local/cuda/bin/nvcc $A -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr "$@" -c k_frame.cu -o build/k_frame_$tag.o
-/usr/local/cuda/bin/nvcc $A -shared -o build/libdisc_$tag.so build/disc_api.o build/k_frame_$tag.o build/k_map.o build/k_query.o -lcudart_static -lrt -ldl -lpthread -Xlinker --no-undefined
+objs=""
+for src in disc_api k_frame k_map k_query; do
+  /usr/local/cuda/bin/nvcc $A -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr "$@" -c $src.cu -o build/var_$tag/$src.o &
+  objs="$objs build/var_$tag/$src.o"
+done
+wait
+/usr/local/cuda/bin/nvcc $A -shared -o build/libdisc_$tag.so $objs -lcudart_static -lrt -ldl -lpthread -Xlinker --no-undefined
 echo "$PWD/build/libdisc_$tag.so"

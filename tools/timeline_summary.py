@@ -35,3 +35,15 @@ for k, v in sorted(dur.items(), key=lambda kv: -kv[1]):
 t0 = recs[0][3]
 t1 = recs[-1][3]
 print(f"span {(t1 - t0) / max(nwin - 1, 1):.3f} ms/window (first mark to last mark / (windows-1))")
+
+# per-stream busy/idle: gaps between a stream's consecutive marks that follow a stage-begin mark
+streams = collections.defaultdict(list)
+for st, name, fr, ms in recs:
+    streams[st].append((ms, name))
+for st, ev in streams.items():
+    ev.sort()
+    names = [n for _, n in ev]
+    kind = "s2" if "k_stage2" in names else "s1"
+    gaps = [(ev[i][0] - ev[i - 1][0], ev[i - 1][1], ev[i][1]) for i in range(1, len(ev)) if ev[i][1] in ("s1_begin", "s2_begin")]
+    tot_gap = sum(g for g, _, _ in gaps)
+    print(f"{kind}: {len(ev)} marks, waits before stage begins: {tot_gap / max(nwin, 1):.3f} ms/window")
