@@ -343,13 +343,14 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
   uint32_t* j_ph = (uint32_t*)(smem_raw + L6.j_ph);         //   physical label
   int32_t* j_obs = (int32_t*)(smem_raw + L6.j_obs);         //   obs count
   float* j_q = (float*)(smem_raw + L6.j_q);                 //   Q
-  __shared__ uint32_t n_tr, n_j, n_tgt, n_seg, ncomp_s;
+  __shared__ uint32_t n_j, n_tgt, n_seg, ncomp_s, n_cand;
   __shared__ uint32_t mcnt_s[256], dcnt_s[256], moff_s[256], doff_s[256];
   __shared__ int64_t tg_vb[256];
   __shared__ int changed;
   __shared__ uint32_t wcnt_s[K6_THREADS / 32], wcnt2_s[K6_THREADS / 32], rc_s[8], nrel_s, bound_s[256];
   __shared__ unsigned long long rel_s, merged_s, edges_s;
   __shared__ uint32_t gen;
+  __shared__ int64_t cnt_s[3];
 
   const size_t fo = (size_t)f * wb.SMAX;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
@@ -358,11 +359,16 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
     g_k6prof[0] = t_;
   }
+  const uint32_t ntr = min(__ldcg(X.ntrip), (uint32_t)TC);
   if (tid == 0) {
-    n_tr = min(*X.ntrip, (uint32_t)TC);
-    if (*X.ntrip > (uint32_t)TC) raise_err(M.err, DERR_TRIPLES);
-    n_j = 0; n_tgt = 0; n_seg = 0; rel_s = 0; merged_s = 0; edges_s = 0;
-    gen = (uint32_t)(++M.counters[3]);
+    if (__ldcg(X.ntrip) > (uint32_t)TC) raise_err(M.err, DERR_TRIPLES);
+    n_j = 0; n_tgt = 0; n_seg = 0; rel_s = 0; merged_s = 0; edges_s = 0; n_cand = 0;
+    // the map counters this step reads, all in one round trip (only this thread writes 0, 1, 3,
+    // 4, 6, 7; counter 2 is K7's)
+    const int64_t c0 = M.counters[0], c1 = M.counters[1], c2 = M.counters[2], c3 = M.counters[3];
+    cnt_s[0] = c0; cnt_s[1] = c1; cnt_s[2] = c2;
+    gen = (uint32_t)(c3 + 1);
+    M.counters[3] = c3 + 1;
     *X.nrel = 0;
     *X.work = 0;
   }
@@ -372,7 +378,8 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
     comp_best[i] = 0;
     comp_tgt[i] = -1;
   }
-  for (int i = tid; i < S; i += blockDim.x) {
+  __syncthreads();   // counters above
+  for (int i = tid; i < S; i += blockDim.x) {   // (loads in flight with the triples' below)
     has_edge[i] = 0;
     d_tgt[i] = -1;
     d_st[i] = wb.status[fo + i];
@@ -381,36 +388,42 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
     X.det_id[i] = -1;
     X.tgt_stage[i] = 0;
   }
-  __syncthreads();
   K6_PROBE(0);
-  const uint32_t ntr = n_tr;
-  // ---- triples: load and release the count table ----
+  // ---- triples (count table released) + O10 exact fp64 geometric test (R10), thread per
+  // triple; candidates for the visual gate are compacted ----
   for (uint32_t t = tid; t < ntr; t += blockDim.x) {
     const uint32_t h = X.ctab_idx[t];
-    t_s[t] = X.trip_s[t];
-    t_j[t] = X.trip_j[t];
-    t_c[t] = X.ctab_cnt[h];
+    const uint32_t s = X.trip_s[t], j = X.trip_j[t];
+    const uint32_t c = X.ctab_cnt[h];
+    const int64_t vj = M.vcount[j];
     X.ctab_cnt[h] = 0;
     X.ctab_key[h] = KEY_EMPTY;
+    t_s[t] = s;
+    t_j[t] = j;
+    t_c[t] = c;
+    const int64_t vs = wb.vs[fo + s];
+    const int64_t mn = vs < vj ? vs : vj;
+    const bool e = c >= 1 && (double)c >= (double)P.tau_geo * (double)mn;
+    t_e[t] = e ? 1 : 0;
+    if (e && P.Dt > 0) t_jl[atomicAdd(&n_cand, 1u)] = (int32_t)t;   // t_jl: candidate list for now
   }
   __syncthreads();
   K6_PROBE(1);
-  // ---- O10 edges: exact fp64 geometric test (R10) + pinned fp64 visual gate (R15) ----
+  // ---- pinned fp64 visual gate (R15) on the candidates, warp per candidate ----
   const double* trk = wb.trk + fo * P.Dt;
-  for (uint32_t t = warp; t < ntr; t += nwarp) {
-    const uint32_t s = t_s[t], j = t_j[t], c = t_c[t];
-    const int64_t vs = d_vs[s], vj = M.vcount[j];
-    const int64_t mn = vs < vj ? vs : vj;
-    bool e = c >= 1 && (double)c >= (double)P.tau_geo * (double)mn;
-    if (e && P.Dt > 0) {
+  if (P.Dt > 0) {
+    const uint32_t nc = n_cand;
+    for (uint32_t k = warp; k < nc; k += nwarp) {
+      const uint32_t t = (uint32_t)t_jl[k];
+      const uint32_t s = t_s[t], j = t_j[t];
       const double* Tj = M.T + (size_t)j * P.Dt;
       const double TT = M.TT[j];
+      const uint8_t tok = wb.tok[fo + s];
       const double dt = dot_pin_reg(trk + (size_t)s * P.Dt, Tj, P.Dt);
       double cosv = -2.0;
-      if (wb.tok[fo + s] && TT > 0.0) cosv = __ddiv_rn(dt, __dsqrt_rn(TT));
-      e = cosv >= (double)P.tau_vis;
+      if (tok && TT > 0.0) cosv = __ddiv_rn(dt, __dsqrt_rn(TT));
+      if (lane == 0 && !(cosv >= (double)P.tau_vis)) t_e[t] = 0;
     }
-    if (lane == 0) t_e[t] = e ? 1 : 0;
   }
   __syncthreads();
   K6_PROBE(2);
@@ -419,22 +432,19 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
     if (!t_e[t]) continue;
     has_edge[t_s[t]] = 1;
     const uint32_t j = t_j[t];
-    if (atomicExch(&M.stamp[j], gen) != gen) {
+    if (atomicExch(&M.stamp[j], gen) != gen) {   // first sight: local index + attributes
       const uint32_t l = atomicAdd(&n_j, 1u);
       M.local[j] = (int32_t)l;
       jnode[l] = j;
+      j_vc[l] = M.vcount[j];
+      j_ph[l] = M.phys_of[j];
+      j_obs[l] = M.obs[j];
+      j_q[l] = M.q[j];
     }
   }
   __syncthreads();
   K6_PROBE(3);
-  for (uint32_t t = tid; t < ntr; t += blockDim.x) t_jl[t] = t_e[t] ? M.local[t_j[t]] : -1;
-  for (int l = tid; l < (int)n_j; l += blockDim.x) {   // one parallel round of attribute loads
-    const uint32_t j = jnode[l];
-    j_vc[l] = M.vcount[j];
-    j_ph[l] = M.phys_of[j];
-    j_obs[l] = M.obs[j];
-    j_q[l] = M.q[j];
-  }
+  for (uint32_t t = tid; t < ntr; t += blockDim.x) t_jl[t] = t_e[t] ? __ldcg(&M.local[t_j[t]]) : -1;
   __syncthreads();
   K6_PROBE(4);
   const int nJ = (int)n_j;
@@ -503,7 +513,7 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
       created += wcnt_s[w2];
     }
     const int ncomp = (int)n_tgt;
-    const int64_t nid0 = M.counters[0];
+    const int64_t nid0 = cnt_s[0];
     if (kept && has_edge[s]) {
       const int t = comp_tgt[lab[s]];
       d_tgt[s] = t;
@@ -525,7 +535,7 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
       ncomp_s = ncomp;
       n_tgt = ncomp + created;
       M.counters[0] = nid0 + created;
-      M.counters[1] += created;
+      cnt_s[1] += created;
       X.rep[f].created = created;
     }
   }
@@ -644,6 +654,8 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
       nrel_s = all;
     }
   }
+  __syncthreads();
+  K6_PROBE(10);
   // list capacity: each target's key list is sized for its worst-case growth this frame (one
   // entry per frame pair of its detections and per relabel item of its segments), moving it to
   // a larger arena region when needed, so K7 appends in place
@@ -691,6 +703,8 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
     if (t < (int)n_tgt) X.tg_mvoff[t] = base + inc - c;
     if (t == 0) X.tg_mvoff[n_tgt] = all;
   }
+  __syncthreads();
+  K6_PROBE(11);
   // report counts (O13): statuses and U over the detections
   if (tid < 8) rc_s[tid] = 0;
   __syncthreads();
@@ -712,17 +726,20 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
     R.key_out_of_range = (int64_t)wb.oor[f];
     R.unique_pairs = U;
     R.edges = (int64_t)edges_s;
-    M.counters[4] += U;
-    M.counters[7] += (int64_t)edges_s;
-    M.counters[6] += (int64_t)acc;
+    atomicAdd((unsigned long long*)&M.counters[4], (unsigned long long)U);
+    atomicAdd((unsigned long long*)&M.counters[7], (unsigned long long)edges_s);
+    atomicAdd((unsigned long long*)&M.counters[6], (unsigned long long)acc);
     R.merged_away = (int64_t)merged_s;
     R.relabeled = (int64_t)rel_s;
-    M.counters[1] -= (int64_t)merged_s;
-    R.live_instances = M.counters[1];
-    *X.live_before = M.counters[2];
+    const int64_t live = cnt_s[1] - (int64_t)merged_s;
+    M.counters[1] = live;
+    R.live_instances = live;
+    *X.live_before = cnt_s[2];
     *X.ntrip_last = ntr;
     *X.ntrip = 0;
   }
+  __syncthreads();
+  K6_PROBE(12);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -957,7 +974,7 @@ void k6_prof_dump() {
   unsigned long long h[16];
   cudaMemcpyFromSymbol(h, g_k6prof, sizeof(h));
   fprintf(stderr, "k6 phase ns (cumulative):");
-  for (int i = 1; i < 12; ++i) fprintf(stderr, " %d:%llu", i - 1, h[i]);
+  for (int i = 1; i < 14; ++i) fprintf(stderr, " %d:%llu", i - 1, h[i]);
   fprintf(stderr, "\n");
 }
 
