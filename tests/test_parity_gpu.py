@@ -129,6 +129,13 @@ def test_stress_overlapping_masks():
     _stream_parity("X", 6, True, window=6, n_masks=120, Df=512, voxel=0.1)
 
 
+def test_tiny_voxels_overflow_tile_tables():
+    """2 mm voxels: nearly every pixel is its own voxel, so the mask pass's per-tile key / pair
+    tables overflow and items take the direct path into the frame tables."""
+    reps = _stream_parity("N", 3, True, window=3, voxel=0.002)
+    assert max(r["unique_pairs"] for r in reps) > 100000
+
+
 def test_ragged_image_scalar_path():
     """W*H not a multiple of 16: the byte-wise mask path; odd patch grid."""
     _stream_parity("N", 4, True, window=2, H=239, W=317, Hp=17, Wp=22, fx=290.0, fy=290.0, cx=158.0, cy=119.0)
