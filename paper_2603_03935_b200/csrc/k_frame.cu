@@ -1265,6 +1265,8 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
   // per-pair normal sums start from zero: one coalesced memset per window (zeroing the slots
   // one by one after use costs far more: scattered partial-line writes)
   if (sem) cudaMemsetAsync(wb.nsum, 0, (size_t)n * wb.PC * sizeof(float4), st);
+  // the frames' key tables start empty (one memset per window; no per-pair release in stage 2)
+  cudaMemsetAsync(wb.ktab, 0xFF, (size_t)n * wb.PC * sizeof(unsigned long long), st);
   if (ev0) cudaEventRecord(ev0, st);
   int64_t maxHW = 1;
   bool vec = true;

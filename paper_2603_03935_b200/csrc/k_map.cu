@@ -51,11 +51,40 @@ __device__ __forceinline__ uint32_t map_insert_key(const MapState& M, uint64_t k
   return U32_EMPTY;
 }
 
+struct SlotV {   // a KeySlot read as two 16-byte L2 loads (key and inline labels together)
+  unsigned long long key;
+  uint32_t lab[INLINE_LABELS];
+  uint32_t ovf;
+};
+__device__ __forceinline__ SlotV slot_load(const MapState& M, uint32_t h) {
+  const uint4* p = reinterpret_cast<const uint4*>(M.slots + h);
+  const uint4 a = __ldcg(p), b = __ldcg(p + 1);
+  SlotV v;
+  v.key = (unsigned long long)a.x | ((unsigned long long)a.y << 32);
+  v.lab[0] = a.z; v.lab[1] = a.w; v.lab[2] = b.x; v.lab[3] = b.y; v.lab[4] = b.z;
+  v.ovf = b.w;
+  return v;
+}
+
 // Insert label L into the key's label list unless present.  Linearisable because labels
 // only occupy a prefix of the list (EMPTY is a suffix, never re-created) and L is only ever
 // written by this routine: concurrent inserters of the same L meet at the same first EMPTY
 // cell, where exactly one CAS succeeds.  Returns true iff this call inserted L.
 __device__ bool label_insert(const MapState& M, uint32_t slot, uint32_t L) {
+  for (;;) {   // inline labels: one 32-byte read, then a CAS on the first EMPTY cell
+    const SlotV v = slot_load(M, slot);
+    int e = -1;
+#pragma unroll
+    for (int i = 0; i < INLINE_LABELS; ++i) {
+      if (e >= 0) continue;
+      if (v.lab[i] == L) return false;
+      if (v.lab[i] == U32_EMPTY) e = i;
+    }
+    if (e < 0) break;   // inline cells full: overflow chunks
+    const uint32_t old = atomicCAS(&M.slots[slot].lab[e], U32_EMPTY, L);
+    if (old == U32_EMPTY) return true;
+    if (old == L) return false;
+  }
   uint32_t* labs = M.slots[slot].lab;
   int n = INLINE_LABELS;
   uint32_t* next = &M.slots[slot].ovf;
@@ -136,67 +165,101 @@ __device__ __forceinline__ void count_add(const FrameScratch& X, uint64_t code, 
   raise_err(err, DERR_TRIPLES);
 }
 
-struct SlotV {   // a KeySlot read as two 16-byte L2 loads (key and inline labels together)
-  unsigned long long key;
-  uint32_t lab[INLINE_LABELS];
-  uint32_t ovf;
-};
-__device__ __forceinline__ SlotV slot_load(const MapState& M, uint32_t h) {
-  const uint4* p = reinterpret_cast<const uint4*>(M.slots + h);
-  const uint4 a = __ldcg(p), b = __ldcg(p + 1);
-  SlotV v;
-  v.key = (unsigned long long)a.x | ((unsigned long long)a.y << 32);
-  v.lab[0] = a.z; v.lab[1] = a.w; v.lab[2] = b.x; v.lab[3] = b.y; v.lab[4] = b.z;
-  v.ovf = b.w;
-  return v;
-}
-
-// Two pairs per lane, their hash probes in lockstep, so each lane keeps two independent
+// LK_Q pairs per lane, their hash probes in lockstep, so each lane keeps LK_Q independent
 // memory chains in flight (the lookup is a latency chain: attributes -> slot -> labels' ids ->
 // count table).
+#ifndef LK_Q
+#define LK_Q 4   // unique (s, key) pairs per lane in flight (lookup)
+#endif
+__device__ unsigned long long g_lkprof[4];   // DISC_S2PROF: lookup sub-phases on CTA 0 (init, loop, flush)
+__device__ __forceinline__ void lk_probe(int i, unsigned long long& tp) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    if (i >= 0) atomicAdd(&g_lkprof[i], t_ - tp);
+    tp = t_;
+  }
+}
+constexpr int LK_CT = 2048;   // per-CTA (s, j) count table slots (in the dynamic shared memory)
+
 __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapState& M, const FrameScratch& X) {
   const uint32_t np = min(wb.npairs[f], (uint32_t)wb.PMAX);
   const size_t fo = (size_t)f * wb.PMAX;
   const int lane = threadIdx.x & 31;
-  unsigned long long* ktab = wb.ktab + (size_t)f * wb.PC;
-  const int32_t* status = wb.status + (size_t)f * wb.SMAX;
-  const uint32_t stride = 2 * gridDim.x * blockDim.x;
+  // the association's shared memory is free during this phase: the frame's statuses and a CTA
+  // table of (s, j) counts (flushed to the frame's count table at the end)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned long long* ck = (unsigned long long*)smem_raw;                 // [LK_CT] codes
+  uint32_t* cc = (uint32_t*)(ck + LK_CT);                                 // [LK_CT] counts
+  int32_t* status = (int32_t*)(cc + LK_CT);                               // [SMAX]
+  unsigned long long tp = 0;
+  lk_probe(-1, tp);
+  for (int i = threadIdx.x; i < LK_CT; i += blockDim.x) { ck[i] = KEY_EMPTY; cc[i] = 0; }
+  for (int i = threadIdx.x; i < wb.SMAX; i += blockDim.x) status[i] = wb.status[(size_t)f * wb.SMAX + i];
+  __syncthreads();
+  lk_probe(0, tp);
+  auto cta_add = [&](uint64_t code, uint32_t add) {   // CTA table, else straight to the frame's
+    uint32_t h = (uint32_t)mix64(code) & (LK_CT - 1);
+    for (int probe = 0; probe < 64; ++probe) {
+      unsigned long long k = ck[h];
+      if (k == KEY_EMPTY) {
+        k = atomicCAS(&ck[h], KEY_EMPTY, (unsigned long long)code);
+        if (k == KEY_EMPTY) k = code;
+      }
+      if (k == code) {
+        atomicAdd(&cc[h], add);
+        return;
+      }
+      h = (h + 1) & (LK_CT - 1);
+    }
+    count_add(X, code, add, M.err);
+  };
+  const uint32_t stride = LK_Q * gridDim.x * blockDim.x;
   const uint32_t hmask = (uint32_t)(M.MC - 1);
-  for (uint32_t base = 2 * (blockIdx.x * blockDim.x + (threadIdx.x & ~31u)); base < np; base += stride) {
-    uint32_t idx[2], s[2], slot[2], h[2];
-    unsigned long long key[2];
-    bool act[2];
+  const uint32_t gthreads = gridDim.x * blockDim.x;
+  // pair q of a lane: base + q * (grid threads), so every CTA gets an equal share
+  for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < np; base += stride) {
+    uint32_t idx[LK_Q], s[LK_Q], slot[LK_Q], h[LK_Q];
+    unsigned long long key[LK_Q];
+    bool act[LK_Q];
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      idx[q] = base + 32 * q + lane;
+    for (int q = 0; q < LK_Q; ++q) {
+      idx[q] = base + q * gthreads + lane;
       s[q] = 0; slot[q] = U32_EMPTY; key[q] = KEY_EMPTY; act[q] = false;
       if (idx[q] < np) {
         s[q] = wb.pinfo[fo + idx[q]];
         key[q] = wb.pkey[fo + idx[q]];
-        ktab[wb.pfk[fo + idx[q]]] = KEY_EMPTY;   // release the frame key-table cell
       }
     }
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < LK_Q; ++q) {
       act[q] = idx[q] < np && status[s[q]] == 0;
       h[q] = (uint32_t)mix64(key[q]) & hmask;
     }
-    SlotV sv[2];
-    for (uint32_t probe = 0; (act[0] || act[1]) && probe <= hmask; ++probe) {
+    SlotV sv[LK_Q];
+    auto any_act = [&]() {
+      bool a = false;
 #pragma unroll
-      for (int q = 0; q < 2; ++q)
+      for (int q = 0; q < LK_Q; ++q) a = a || act[q];
+      return a;
+    };
+    for (uint32_t probe = 0; any_act() && probe <= hmask; ++probe) {
+#pragma unroll
+      for (int q = 0; q < LK_Q; ++q)
         if (act[q]) sv[q] = slot_load(M, h[q]);
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
+      for (int q = 0; q < LK_Q; ++q) {
         if (!act[q]) continue;
         if (sv[q].key == key[q]) { slot[q] = h[q]; act[q] = false; }
         else if (sv[q].key == KEY_EMPTY) act[q] = false;
         else h[q] = (h[q] + 1) & hmask;
       }
     }
-    uint64_t first[2] = {KEY_EMPTY, KEY_EMPTY};   // each pair's first label (s, j), warp-aggregated
+    uint64_t first[LK_Q];
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < LK_Q; ++q) first[q] = KEY_EMPTY;   // each pair's first label (s, j), warp-aggregated
+#pragma unroll
+    for (int q = 0; q < LK_Q; ++q) {
       if (idx[q] < np) wb.pms[fo + idx[q]] = slot[q];
       if (slot[q] == U32_EMPTY) continue;
       uint32_t id[INLINE_LABELS];
@@ -215,7 +278,7 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
         if (!ok[i]) continue;
         const uint64_t c = ((uint64_t)s[q] << 32) | id[i];
         if (nl == 0) first[q] = c;
-        else count_add(X, c, 1, M.err);
+        else cta_add(c, 1);
         nl++;
       }
       if (open) {   // overflow chunks (more than INLINE_LABELS labels on this key)
@@ -228,7 +291,7 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
             if (L == LAB_TOMB) continue;
             const uint64_t c = ((uint64_t)s[q] << 32) | __ldcg(&M.id_of[L]);
             if (nl == 0) first[q] = c;
-            else count_add(X, c, 1, M.err);
+            else cta_add(c, 1);
             nl++;
           }
           nx = __ldcg(&oc.next);
@@ -236,11 +299,17 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
       }
     }
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {   // warp aggregation of the first label's count
+    for (int q = 0; q < LK_Q; ++q) {   // warp aggregation of the first label's count
       const unsigned peers = __match_any_sync(0xffffffffu, first[q]);
-      if (first[q] != KEY_EMPTY && lane == __ffs(peers) - 1) count_add(X, first[q], __popc(peers), M.err);
+      if (first[q] != KEY_EMPTY && lane == __ffs(peers) - 1) cta_add(first[q], __popc(peers));
     }
   }
+  __syncthreads();
+  lk_probe(1, tp);
+  for (int i = threadIdx.x; i < LK_CT; i += blockDim.x)   // flush the CTA's counts
+    if (cc[i]) count_add(X, ck[i], cc[i], M.err);
+  __syncthreads();
+  lk_probe(2, tp);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -306,6 +375,8 @@ struct K6Smem {   // offsets into dynamic shared memory
 // DISC_K6PROF: phase timestamps of the association kernel (profiling aid)
 __device__ unsigned long long g_k6prof[16];
 __device__ unsigned long long g_s2prof[8];   // DISC_S2PROF phase sums
+__device__ unsigned long long g_s2cta[8];
+__device__ unsigned long long g_s2items[4];   // DISC_S2PROF: K7 items: pairs, relabels, list-move copies, targets
 #define K6_PROBE(i)                                                                          \
   do {                                                                                       \
     if (threadIdx.x == 0) {                                                                  \
@@ -878,11 +949,30 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
   const int lane = threadIdx.x & 31;
   const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), nw = gridDim.x * (blockDim.x >> 5);
   const int ntgt = *X.ntgt;
+  // per-detection / per-target routing in shared memory (the association's bytes are free now)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned long long* to_s = (unsigned long long*)smem_raw;   // [SMAX] list offsets
+  int32_t* dt_s = (int32_t*)(to_s + wb.SMAX);                  // [SMAX] detection -> target
+  uint32_t* tp_s = (uint32_t*)(dt_s + wb.SMAX);                // [SMAX] target -> physical label
+  uint32_t* tb_s = tp_s + wb.SMAX;                             // [SMAX] target -> list length before
+  for (int i = threadIdx.x; i < F.S; i += blockDim.x) dt_s[i] = X.det_target[i];
+  for (int t = threadIdx.x; t < ntgt; t += blockDim.x) {
+    tp_s[t] = X.tgt_phys[t];
+    tb_s[t] = X.tgt_base[t];
+    to_s[t] = X.tg_newoff[t];
+  }
+  __syncthreads();
   for (int t = gw; t < ntgt; t += nw) apply_target_warp(t, f, F, wb, M, X, P, sem);
   const uint32_t np = min(wb.npairs[f], (uint32_t)wb.PMAX);
   const uint32_t nrel = *X.nrel;
   const uint32_t nmove = X.tg_mvoff[ntgt];
   const uint32_t total = np + nrel + nmove;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {   // (cheap; counted always, printed under DISC_S2PROF)
+    atomicAdd(&g_s2items[0], (unsigned long long)np);
+    atomicAdd(&g_s2items[1], (unsigned long long)nrel);
+    atomicAdd(&g_s2items[2], (unsigned long long)nmove);
+    atomicAdd(&g_s2items[3], (unsigned long long)ntgt);
+  }
   const size_t fo = (size_t)f * wb.PMAX;
   const int nseg = *X.nseg;
   int delta = 0;
@@ -898,9 +988,9 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
     uint32_t snew = 0;
     if (it < np) {
       const uint32_t s = wb.pinfo[fo + it];
-      const int t = X.det_target[s];
+      const int t = dt_s[s];
       if (t >= 0) {
-        const uint32_t L = X.tgt_phys[t];
+        const uint32_t L = tp_s[t];
         uint32_t slot = wb.pms[fo + it];
         if (slot == U32_EMPTY) slot = map_insert_key(M, wb.pkey[fo + it]);
         if (slot != U32_EMPTY && label_insert(M, slot, L)) { tnew = t; snew = slot; delta++; }
@@ -914,7 +1004,7 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
         else hi = mid - 1;
       }
       const int t = X.seg_tgt[lo];
-      const uint32_t L = X.tgt_phys[t];
+      const uint32_t L = tp_s[t];
       const uint32_t slot = M.arena[X.seg_base[lo] + (r - X.seg_off[lo])];
       if (label_insert(M, slot, L)) { tnew = t; snew = slot; delta++; }
       if (label_tomb(M, slot, X.seg_phys[lo])) delta--;
@@ -937,13 +1027,32 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
     if (tnew >= 0 && lane == leader) pb = atomicAdd(&X.tgt_stage[tnew], (uint32_t)__popc(peers));
     pb = __shfl_sync(0xffffffffu, pb, leader);
     if (tnew >= 0) {
-      const uint32_t pos = X.tgt_base[tnew] + pb + __popc(peers & ((1u << lane) - 1u));
-      M.arena[X.tg_newoff[tnew] + pos] = snew;
+      const uint32_t pos = tb_s[tnew] + pb + __popc(peers & ((1u << lane) - 1u));
+      M.arena[to_s[tnew] + pos] = snew;
     }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) delta += __shfl_xor_sync(0xffffffffu, delta, o);
   if (lane == 0 && delta) atomicAdd((unsigned long long*)&M.counters[2], (unsigned long long)(int64_t)delta);
+}
+
+// While CTA 0 runs the association of frame f, the other CTAs pull frame f+1's lookup working
+// set into L2: its pair records and the hash slots its keys start probing at (a hint only: the
+// slots are read again, after frame f's update, by the lookup).
+__device__ __forceinline__ void s2_prefetch(int f, const WinBufs& wb, const MapState& M) {
+  const uint32_t np = min(__ldcg(&wb.npairs[f]), (uint32_t)wb.PMAX);
+  const size_t fo = (size_t)f * wb.PMAX;
+  const uint32_t hmask = (uint32_t)(M.MC - 1);
+  const uint32_t n = gridDim.x - 1, b = blockIdx.x - 1;   // CTAs 1..G-1
+  for (uint32_t i = b * blockDim.x + threadIdx.x; i < np; i += n * blockDim.x) {
+    if ((i & 31) == 0) {   // one line of each record array per 32 pairs
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(wb.pinfo + fo + i));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(wb.pms + fo + i));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(wb.pkey + fo + i + 16));
+    }
+    const unsigned long long key = __ldcg(&wb.pkey[fo + i]);
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(M.slots + ((uint32_t)mix64(key) & hmask)));
+  }
 }
 
 // K7 tail, run in the next phase: list lengths and exact |V| of the frame's targets, insert counter,
@@ -963,13 +1072,23 @@ __device__ __forceinline__ void s2_finalize(int f, const MapState& M, const Fram
   }
 }
 
-size_t k6_smem_bytes(int S, int TC) { return K6Smem(S, TC).total; }
+size_t k6_smem_bytes(int S, int TC) {
+  // the association's layout; the lookup / apply phases reuse the same bytes
+  return std::max(K6Smem(S, TC).total, (size_t)LK_CT * 12 + (size_t)S * 32 + 64);
+}
 
 void k6_prof_dump() {
   if (getenv("DISC_S2PROF")) {
     unsigned long long g[8];
     cudaMemcpyFromSymbol(g, g_s2prof, sizeof(g));
     fprintf(stderr, "s2 phase ns: lookup %llu assoc %llu apply %llu\n", g[0], g[1], g[2]);
+    unsigned long long c[8];
+    cudaMemcpyFromSymbol(c, g_s2cta, sizeof(c));
+    fprintf(stderr, "s2 per-CTA work: lookup sum %llu max %llu, apply sum %llu max %llu\n", c[0], c[1], c[4], c[5]);
+    cudaMemcpyFromSymbol(c, g_s2items, 4 * sizeof(unsigned long long));
+    fprintf(stderr, "s2 K7 items: pairs %llu relabels %llu moves %llu targets %llu\n", c[0], c[1], c[2], c[3]);
+    cudaMemcpyFromSymbol(c, g_lkprof, 3 * sizeof(unsigned long long));
+    fprintf(stderr, "s2 lookup CTA0: init %llu loop %llu flush %llu\n", c[0], c[1], c[2]);
   }
   unsigned long long h[16];
   cudaMemcpyFromSymbol(h, g_k6prof, sizeof(h));
@@ -1011,16 +1130,31 @@ __global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb
     }
   };
   probe(-1);
+  unsigned long long c0 = 0;
+  auto cta_t = [&](int i) {   // this CTA's own work time in phase i (before its barrier wait)
+    if (prof) __syncthreads();   // (prof is grid-uniform)
+    if (prof && threadIdx.x == 0) {
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      if (i >= 0) { atomicAdd(&g_s2cta[2 * i], t_ - c0); atomicMax(&g_s2cta[2 * i + 1], t_ - c0); }
+      c0 = t_;
+    }
+  };
   for (int f = 0; f < wd.n; ++f) {
     const FrameDesc& F = wd.f[f];
+    cta_t(-1);
     s2_lookup(f, wb, M, X);
     if (f > 0) s2_finalize(f - 1, M, X);
+    cta_t(0);
     grid_sync(wb.s2bar, G * ++ep);
     probe(0);
     if (blockIdx.x == 0) s2_assoc(f, F, wb, M, X, P, sem);
+    else if (f + 1 < wd.n) s2_prefetch(f + 1, wb, M);
     grid_sync(wb.s2bar, G * ++ep);
     probe(1);
+    cta_t(-1);
     s2_apply(f, F, wb, M, X, P, sem);
+    cta_t(2);
     grid_sync(wb.s2bar, G * ++ep);
     probe(2);
   }
