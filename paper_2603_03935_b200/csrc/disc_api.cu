@@ -366,6 +366,7 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(W.pinfo = dalloc<uint32_t>(m, (size_t)win * PMAX));
   chk(W.pfk = dalloc<uint32_t>(m, (size_t)win * PMAX));
   chk(W.pms = dalloc<uint32_t>(m, (size_t)win * PMAX));
+  chk(W.plab = dalloc<uint2>(m, (size_t)win * PMAX));
   chk(W.fpart = dalloc<double>(m, (size_t)win * W.FCHUNKS * Df));
   chk(W.fbar = dalloc<float>(m, (size_t)win * Df));
   chk(W.rp = dalloc<float>(m, (size_t)win * PMP));

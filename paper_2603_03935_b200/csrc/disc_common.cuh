@@ -94,6 +94,7 @@ struct WinBufs {
   uint32_t* pinfo;            // [win][PMAX] mask index s
   uint32_t* pfk;              // [win][PMAX] frame key-table slot
   uint32_t* pms;              // [win][PMAX] map slot found by K5 (or U32_EMPTY)
+  uint2* plab;                // [win][PMAX] the slot's first two labels seen by K5 (K7 skips inserts of a present label)
   // semantic
   double* fpart;              // [win][FCHUNKS][Df] partial column sums
   float* fbar;                // [win][Df]

@@ -260,7 +260,13 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
     for (int q = 0; q < LK_Q; ++q) first[q] = KEY_EMPTY;   // each pair's first label (s, j), warp-aggregated
 #pragma unroll
     for (int q = 0; q < LK_Q; ++q) {
-      if (idx[q] < np) wb.pms[fo + idx[q]] = slot[q];
+      if (idx[q] < np) {
+        wb.pms[fo + idx[q]] = slot[q];
+        // labels only ever gain entries, except the tombstones of merged-away sets, never the
+        // survivor's: a label present now is present when K7 would insert it
+        wb.plab[fo + idx[q]] = slot[q] == U32_EMPTY ? make_uint2(U32_EMPTY, U32_EMPTY)
+                                                    : make_uint2(sv[q].lab[0], sv[q].lab[1]);
+      }
       if (slot[q] == U32_EMPTY) continue;
       uint32_t id[INLINE_LABELS];
       bool ok[INLINE_LABELS];
@@ -820,7 +826,7 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
 // ------------------------------------------------------------------------------------------
 // One O12 target per warp (a few dozen per frame), so every target runs at once and the warps
 // without one start the inserts immediately.
-__device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc& F, const WinBufs& wb,
+__device__ void apply_target_warp_general(int t, int f, const FrameDesc& F, const WinBufs& wb,
                                                   const MapState& M, const FrameScratch& X, const Params& P, int sem) {
   const int lane = threadIdx.x & 31;
   const size_t fo = (size_t)f * wb.SMAX;
@@ -944,6 +950,142 @@ __device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc&
   if (lane < 6) M.aabb[(size_t)root * 6 + lane] = ab[lane];
 }
 
+// Fast path (up to 32 members + detections, Dt <= 512): a few dependent memory round trips —
+// descriptors; member / detection ids; their attributes and T / t rows together; the embedding
+// copy — with T_root's sums and dot_pin(T, T) kept in registers (same lane / element order as
+// dot_pin_reg: lane l holds d = l, l + 32, ... ascending).
+__device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc& F, const WinBufs& wb,
+                                                  const MapState& M, const FrameScratch& X, const Params& P, int sem) {
+  const int lane = threadIdx.x & 31;
+  const size_t fo = (size_t)f * wb.SMAX;
+  const double* trk = wb.trk + fo * P.Dt;
+  const int kind = X.tg_kind[t];
+  const uint32_t root = X.tgt_root[t], L = X.tgt_phys[t];
+  const uint32_t moff = X.tg_moff[t], mcnt = X.tg_mcnt[t], doff = X.tg_doff[t], dcnt = X.tg_dcnt[t];
+  const int64_t vbase = X.tg_vbase[t];
+  const int Dt = P.Dt, Df = P.Df;
+  if (mcnt + dcnt > 32 || Dt > 512) {
+    apply_target_warp_general(t, f, F, wb, M, X, P, sem);
+    return;
+  }
+  const uint32_t n = mcnt + dcnt;
+  // candidate of this lane: members (ids ascending) then detections (s ascending)
+  const bool is_mem = (uint32_t)lane < mcnt, is_det = !is_mem && (uint32_t)lane < n;
+  const uint32_t cid = is_mem ? X.tg_mem[moff + lane] : (is_det ? X.tg_dets[doff + lane - mcnt] : 0u);
+  // attributes of the candidate
+  int obs = 0;
+  float qi = -INFINITY;
+  uint32_t pm = U32_EMPTY;
+  int32_t ab[6] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MIN, INT32_MIN, INT32_MIN};
+  if (is_mem) {
+    obs = M.obs[cid];
+    qi = M.q[cid];
+    pm = M.phys_of[cid];
+    for (int k = 0; k < 6; ++k) ab[k] = M.aabb[(size_t)cid * 6 + k];
+  } else if (is_det) {
+    obs = 1;
+    qi = wb.qf[(fo + cid) * 6 + 4];
+    for (int k = 0; k < 6; ++k) ab[k] = wb.daabb[(fo + cid) * 6 + k];
+  }
+  // T sums, pinned order: T_root (new instance: t_s1) then J ascending then Sd ascending
+  double acc[16];
+  const int nt = (Dt + 31) / 32;
+  const uint32_t cid0 = __shfl_sync(0xffffffffu, cid, 0);   // (outside the lane-dependent branches)
+  const uint32_t first = 1;   // candidate 0 is the base: T_root (= mem[0], the min id) or t_s1
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const int d = lane + 32 * k;
+    acc[k] = 0.0;
+    if (k < nt && d < Dt) {
+      if (kind == 1) acc[k] = trk[(size_t)cid0 * Dt + d];
+      else acc[k] = M.T[(size_t)root * Dt + d];
+    }
+  }
+  for (uint32_t i = first; i < n; ++i) {
+    const uint32_t id = __shfl_sync(0xffffffffu, cid, i);
+    const double* row = i < mcnt ? M.T + (size_t)id * Dt : trk + (size_t)id * Dt;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int d = lane + 32 * k;
+      if (k < nt && d < Dt) acc[k] = __dadd_rn(acc[k], row[d]);
+    }
+  }
+  double tt = 0.0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const int d = lane + 32 * k;
+    if (k < nt && d < Dt) {
+      M.T[(size_t)root * Dt + d] = acc[k];
+      tt = __fma_rn(acc[k], acc[k], tt);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) tt = __dadd_rn(tt, __shfl_xor_sync(0xffffffffu, tt, o));
+  // obs, aabb: warp reductions; (e, Q): the first candidate after the base with the maximum Q,
+  // if it beats the base's (strict replacement in the pinned order)
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    obs += __shfl_xor_sync(0xffffffffu, obs, o);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      ab[k] = min(ab[k], __shfl_xor_sync(0xffffffffu, ab[k], o));
+      ab[3 + k] = max(ab[3 + k], __shfl_xor_sync(0xffffffffu, ab[3 + k], o));
+    }
+  }
+  const float q0 = __shfl_sync(0xffffffffu, qi, 0);
+  int src = -1;
+  float qnew = q0;
+  if (kind == 0) {
+    const bool cand = (uint32_t)lane >= 1 && (uint32_t)lane < n;
+    float qm = cand ? qi : -INFINITY;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) qm = fmaxf(qm, __shfl_xor_sync(0xffffffffu, qm, o));
+    const unsigned hit = __ballot_sync(0xffffffffu, cand && qi == qm);
+    if (hit && qm > q0) { src = __ffs(hit) - 1; qnew = qm; }
+  }
+  const bool has_e = kind == 1 ? (sem && q0 >= 0.f) : src >= 0;
+  const uint32_t sid = __shfl_sync(0xffffffffu, cid, src >= 0 ? src : 0);
+  const float4* es = kind == 1 ? (const float4*)(wb.emb + (fo + sid) * Df)
+                               : ((uint32_t)src < mcnt ? (const float4*)(M.E + (size_t)sid * Df)
+                                                       : (const float4*)(wb.emb + (fo + sid) * Df));
+  float4* ed = (float4*)(M.E + (size_t)root * Df);
+  if (kind == 1) {
+    for (int d4 = lane; d4 < Df / 4; d4 += 32) ed[d4] = has_e ? es[d4] : make_float4(0.f, 0.f, 0.f, 0.f);
+  } else if (has_e) {
+    for (int d4 = lane; d4 < Df / 4; d4 += 32) ed[d4] = es[d4];
+  }
+  if (kind == 0 && is_mem) {   // members: lists of other physical labels reset, J killed
+    if (pm != L) {
+      M.lst_len[pm] = 0;
+      M.lst_cap[pm] = 0;
+    }
+    if (lane >= 1) {
+      M.alive[cid] = 0;
+      M.phys_of[cid] = U32_EMPTY;
+    }
+  }
+  if (lane == 0) {
+    if (kind == 1) {
+      M.alive[root] = 1;
+      M.phys_of[root] = root;
+      M.id_of[root] = root;
+      M.vcount[root] = 0;
+      M.obs[root] = 1;
+      M.q[root] = q0;
+      M.lst_len[root] = 0;
+    } else {
+      M.obs[root] = obs;
+      M.q[root] = qnew;
+      M.vcount[root] = vbase;
+      M.phys_of[root] = L;
+      M.id_of[L] = root;
+    }
+    M.last_seen[root] = F.frame_id;
+    if (Dt > 0) M.TT[root] = tt;
+  }
+  if (lane < 6) M.aabb[(size_t)root * 6 + lane] = ab[lane];
+}
+
 __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBufs& wb, const MapState& M,
                                          const FrameScratch& X, const Params& P, int sem) {
   const int lane = threadIdx.x & 31;
@@ -992,8 +1134,11 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
       if (t >= 0) {
         const uint32_t L = tp_s[t];
         uint32_t slot = wb.pms[fo + it];
-        if (slot == U32_EMPTY) slot = map_insert_key(M, wb.pkey[fo + it]);
-        if (slot != U32_EMPTY && label_insert(M, slot, L)) { tnew = t; snew = slot; delta++; }
+        const uint2 pl = wb.plab[fo + it];
+        if (!(slot != U32_EMPTY && (pl.x == L || pl.y == L))) {   // else: already a member
+          if (slot == U32_EMPTY) slot = map_insert_key(M, wb.pkey[fo + it]);
+          if (slot != U32_EMPTY && label_insert(M, slot, L)) { tnew = t; snew = slot; delta++; }
+        }
       }
     } else if (it < np + nrel) {
       const uint32_t r = it - np;
