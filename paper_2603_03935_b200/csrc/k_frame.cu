@@ -996,7 +996,10 @@ size_t k4r_smem_bytes(int Df, int Dt) {
 }
 
 template <bool SEM>
-__global__ void __launch_bounds__(K4R_WARPS * 32) k_poolr(WinDesc wd, WinBufs wb, Params P) {
+#ifndef K4R_MINB
+#define K4R_MINB 4
+#endif
+__global__ void __launch_bounds__(K4R_WARPS * 32, K4R_MINB) k_poolr(WinDesc wd, WinBufs wb, Params P) {
   const int f = blockIdx.y;
   if (f >= wd.n) return;
   const FrameDesc& F = wd.f[f];
@@ -1021,6 +1024,7 @@ __global__ void __launch_bounds__(K4R_WARPS * 32) k_poolr(WinDesc wd, WinBufs wb
   const uint32_t* cnt = wb.cnt + gbase * wb.PMAXP;
   const int D4 = Df / 4, nq4 = (D4 + 31) / 32;
   const int nch = (S + 31) >> 5;   // <= 8 (S <= 255)
+  const bool tvec = (Dt & 3) == 0;   // tracking rows as uint2 (4 bf16) per lane (Dt <= 512)
   // this lane's kept flags (status 0) for masks lane, lane + 32, ... (S <= 255)
   uint32_t keptl = 0;
   for (int q = 0; q < nch; ++q)
@@ -1081,6 +1085,13 @@ __global__ void __launch_bounds__(K4R_WARPS * 32) k_poolr(WinDesc wd, WinBufs wb
       r = sqrtf(acc);
       if (lane == 0) wb.rp[(size_t)f * wb.PMAXP + p] = r;
     }
+    // the patch's tracking row, once: lane l holds elements 4 l + j + 128 k (uint2 = 4 bf16)
+    uint2 gv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      gv[k] = make_uint2(0u, 0u);
+      if (tvec && 4 * lane + 128 * k < Dt) gv[k] = __ldg((const uint2*)(F.track + (size_t)p * Dt) + lane + 32 * k);
+    }
     // keep the slice's mask if it covers p, else flush it: p's first mask takes the slice
     if (cur >= 0 && cnt[(size_t)cur * wb.PMAXP + p] == 0) flush();
     const int64_t cols = ((int64_t)(pcx + 1) * W + Wp - 1) / Wp - ((int64_t)pcx * W + Wp - 1) / Wp;
@@ -1114,8 +1125,21 @@ __global__ void __launch_bounds__(K4R_WARPS * 32) k_poolr(WinDesc wd, WinBufs wb
             sc1 += cov * (double)r;
             sc2 += cov;
           }
-          for (int d = lane; d < Dt; d += 32)
-            ua[d] = __dadd_rn(ua[d], __dmul_rn((double)c, (double)__uint_as_float((uint32_t)g[d] << 16)));
+          if (tvec) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int d0 = 4 * lane + 128 * k;
+              if (d0 < Dt) {
+                const uint32_t e[4] = {gv[k].x << 16, gv[k].x & 0xFFFF0000u, gv[k].y << 16, gv[k].y & 0xFFFF0000u};
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj)
+                  ua[d0 + jj] = __dadd_rn(ua[d0 + jj], __dmul_rn((double)c, (double)__uint_as_float(e[jj])));
+              }
+            }
+          } else {
+            for (int d = lane; d < Dt; d += 32)
+              ua[d] = __dadd_rn(ua[d], __dmul_rn((double)c, (double)__uint_as_float((uint32_t)g[d] << 16)));
+          }
         } else {   // another mask of a boundary patch: reduce straight into its sums
           const size_t gi = gbase + s;
           if (pool) {
@@ -1134,8 +1158,21 @@ __global__ void __launch_bounds__(K4R_WARPS * 32) k_poolr(WinDesc wd, WinBufs wb
             }
           }
           double* u = wb.trk + gi * Dt;
-          for (int d = lane; d < Dt; d += 32)
-            atomicAdd(&u[d], __dmul_rn((double)c, (double)__uint_as_float((uint32_t)g[d] << 16)));
+          if (tvec) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int d0 = 4 * lane + 128 * k;
+              if (d0 < Dt) {
+                const uint32_t e[4] = {gv[k].x << 16, gv[k].x & 0xFFFF0000u, gv[k].y << 16, gv[k].y & 0xFFFF0000u};
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj)
+                  atomicAdd(&u[d0 + jj], __dmul_rn((double)c, (double)__uint_as_float(e[jj])));
+              }
+            }
+          } else {
+            for (int d = lane; d < Dt; d += 32)
+              atomicAdd(&u[d], __dmul_rn((double)c, (double)__uint_as_float((uint32_t)g[d] << 16)));
+          }
         }
       }
     }
