@@ -362,18 +362,19 @@ __device__ __forceinline__ double dot_pin_reg(const double* a, const double* b, 
 
 struct K6Smem {   // offsets into dynamic shared memory
   size_t t_s, t_j, t_c, t_e, t_jl, lab, jnode, comp_root, comp_best, comp_tgt, has_edge, d_st, d_vs, d_tgt, d_q,
-      tg_root, tg_phys, j_vc, j_ph, j_obs, j_q, total;
+      tg_root, tg_phys, j_vc, j_ph, j_obs, j_q, j_lo, j_ll, j_lc, total;
   __host__ __device__ K6Smem(int S, int TC) {
     size_t o = 0;
     auto take = [&](size_t bytes) { const size_t r = o; o = (o + bytes + 15) & ~(size_t)15; return r; };
     const size_t NN = (size_t)S + TC;
-    t_s = take(4 * (size_t)TC); t_j = take(4 * (size_t)TC); t_c = take(4 * (size_t)TC);
+    t_s = take((size_t)TC); t_j = take(4 * (size_t)TC); t_c = take(4 * (size_t)TC);
     t_e = take((size_t)TC); t_jl = take(4 * (size_t)TC); lab = take(4 * NN); jnode = take(4 * (size_t)TC);
     comp_root = take(4 * NN); comp_best = take(8 * NN); comp_tgt = take(4 * NN); has_edge = take((size_t)S + 1);
     d_st = take(4 * (size_t)S + 4); d_vs = take(4 * (size_t)S + 4); d_tgt = take(4 * (size_t)S + 4);
     d_q = take(4 * (size_t)S + 4);
     tg_root = take(4 * (size_t)S + 4); tg_phys = take(4 * (size_t)S + 4);
-    j_vc = take(8 * (size_t)TC); j_ph = take(4 * (size_t)TC); j_obs = take(4 * (size_t)TC); j_q = take(4 * (size_t)TC);
+    j_vc = take(4 * (size_t)TC); j_ph = take(4 * (size_t)TC); j_obs = take(4 * (size_t)TC); j_q = take(4 * (size_t)TC);
+    j_lo = take(4 * (size_t)TC); j_ll = take(4 * (size_t)TC); j_lc = take(4 * (size_t)TC);   // list of the phys label
     total = o;
   }
 };
@@ -399,7 +400,7 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
   const int TC = X.TCAP;
   const int S = F.S;
   const K6Smem L6(S, TC);
-  uint32_t* t_s = (uint32_t*)(smem_raw + L6.t_s);          // triple s
+  uint8_t* t_s = (uint8_t*)(smem_raw + L6.t_s);            // triple s (S <= 255)
   uint32_t* t_j = (uint32_t*)(smem_raw + L6.t_j);          // triple j (instance id)
   uint32_t* t_c = (uint32_t*)(smem_raw + L6.t_c);          // c_sj
   uint8_t* t_e = (uint8_t*)(smem_raw + L6.t_e);            // edge flag
@@ -416,13 +417,17 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
   float* d_q = (float*)(smem_raw + L6.d_q);           // Q_s
   uint32_t* tg_root = (uint32_t*)(smem_raw + L6.tg_root);   // per target: survivor id
   uint32_t* tg_phys = (uint32_t*)(smem_raw + L6.tg_phys);   // per target: physical label
-  int64_t* j_vc = (int64_t*)(smem_raw + L6.j_vc);           // per local instance: |V_j|
+  uint32_t* j_vc = (uint32_t*)(smem_raw + L6.j_vc);         // per local instance: |V_j|
+  uint32_t* j_lo = (uint32_t*)(smem_raw + L6.j_lo);         //   key list of its physical label: offset,
+  uint32_t* j_ll = (uint32_t*)(smem_raw + L6.j_ll);         //   length,
+  uint32_t* j_lc = (uint32_t*)(smem_raw + L6.j_lc);         //   capacity
   uint32_t* j_ph = (uint32_t*)(smem_raw + L6.j_ph);         //   physical label
   int32_t* j_obs = (int32_t*)(smem_raw + L6.j_obs);         //   obs count
   float* j_q = (float*)(smem_raw + L6.j_q);                 //   Q
   __shared__ uint32_t n_j, n_tgt, n_seg, ncomp_s, n_cand;
   __shared__ uint32_t mcnt_s[256], dcnt_s[256], moff_s[256], doff_s[256];
   __shared__ int64_t tg_vb[256];
+  __shared__ int32_t tg_own[256];   // component target -> local index of its physical owner
   __shared__ int changed;
   __shared__ uint32_t wcnt_s[K6_THREADS / 32], wcnt2_s[K6_THREADS / 32], rc_s[8], nrel_s, bound_s[256];
   __shared__ unsigned long long rel_s, merged_s, edges_s;
@@ -475,7 +480,7 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
     const int64_t vj = M.vcount[j];
     X.ctab_cnt[h] = 0;
     X.ctab_key[h] = KEY_EMPTY;
-    t_s[t] = s;
+    t_s[t] = (uint8_t)s;
     t_j[t] = j;
     t_c[t] = c;
     const int64_t vs = wb.vs[fo + s];
@@ -513,7 +518,7 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
       const uint32_t l = atomicAdd(&n_j, 1u);
       M.local[j] = (int32_t)l;
       jnode[l] = j;
-      j_vc[l] = M.vcount[j];
+      j_vc[l] = (uint32_t)M.vcount[j];
       j_ph[l] = M.phys_of[j];
       j_obs[l] = M.obs[j];
       j_q[l] = M.q[j];
@@ -522,6 +527,12 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
   __syncthreads();
   K6_PROBE(3);
   for (uint32_t t = tid; t < ntr; t += blockDim.x) t_jl[t] = t_e[t] ? __ldcg(&M.local[t_j[t]]) : -1;
+  for (int l = tid; l < (int)n_j; l += blockDim.x) {   // the key list of each instance's physical label
+    const uint32_t pm = j_ph[l];
+    j_lo[l] = (uint32_t)M.lst_off[pm];
+    j_ll[l] = M.lst_len[pm];
+    j_lc[l] = M.lst_cap[pm];
+  }
   __syncthreads();
   K6_PROBE(4);
   const int nJ = (int)n_j;
@@ -567,10 +578,16 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
     if (lab[x] == x && comp_root[x] != U32_EMPTY) {
       const int t = (int)atomicAdd(&n_tgt, 1u);
       comp_tgt[x] = t;
-      const uint32_t owner = 0x7FFFFFFFu - (uint32_t)(comp_best[x] & 0xFFFFFFFFull);
       tg_root[t] = comp_root[x];
-      tg_phys[t] = M.phys_of[owner];
       tg_vb[t] = (int64_t)(comp_best[x] >> 32);   // |V| of the physical owner
+    }
+  }
+  __syncthreads();
+  for (int l = tid; l < nJ; l += blockDim.x) {   // the physical owner's local index -> its label
+    const int Lb = lab[S + l];
+    if (jnode[l] == 0x7FFFFFFFu - (uint32_t)(comp_best[Lb] & 0xFFFFFFFFull)) {
+      tg_phys[comp_tgt[Lb]] = j_ph[l];
+      tg_own[comp_tgt[Lb]] = l;
     }
   }
   __syncthreads();
@@ -647,20 +664,23 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
     if (t < ntg) { moff_s[t] = mb + mi - mc; doff_s[t] = db + di - dc; }
   }
   __syncthreads();
+  int32_t* tl_s = (int32_t*)comp_root;   // (comp_root is dead after the targets were formed)
+  for (int l = tid; l < nJ; l += blockDim.x) tl_s[l] = comp_tgt[lab[S + l]];   // member -> target
   for (int s2 = tid; s2 < S; s2 += blockDim.x) {   // detections of each target, ascending s
     const int t = d_tgt[s2];
     if (t < 0) continue;
     uint32_t rank = 0;
+#pragma unroll 8
     for (int s3 = 0; s3 < s2; ++s3) rank += d_tgt[s3] == t;
     X.tg_dets[doff_s[t] + rank] = (uint32_t)s2;
   }
   __syncthreads();
   for (int l = tid; l < nJ; l += blockDim.x) {
-    const int t = comp_tgt[lab[S + l]];
+    const int t = tl_s[l];
     const uint32_t j = jnode[l];
     uint32_t rank = 0;
-    for (int l2 = 0; l2 < nJ; ++l2)
-      if (l2 != l && comp_tgt[lab[S + l2]] == t && jnode[l2] < j) rank++;
+#pragma unroll 8
+    for (int l2 = 0; l2 < nJ; ++l2) rank += (tl_s[l2] == t) & (jnode[l2] < j);   // ids are distinct
     X.tg_mem[moff_s[t] + rank] = j;
     const uint32_t pm = j_ph[l];
     if (pm != tg_phys[t]) {   // the smaller sets: relabel into the survivor's physical label
@@ -668,8 +688,8 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
       if (sg < (uint32_t)TC) {
         X.seg_phys[sg] = pm;
         X.seg_tgt[sg] = t;
-        X.seg_base[sg] = M.lst_off[pm];
-        const uint32_t len = M.lst_len[pm];
+        X.seg_base[sg] = j_lo[l];
+        const uint32_t len = j_ll[l];
         t_jl[sg] = (int32_t)len;   // segment length (t_jl is free after the components)
         atomicAdd(&bound_s[t], len);
       } else {
@@ -739,8 +759,9 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
   for (int t = tid; t < (int)n_tgt; t += blockDim.x) {
     const uint32_t L = tg_phys[t];
     const bool fresh = t >= (int)ncomp_s;   // new instance: empty list
-    const uint32_t oldlen = fresh ? 0u : M.lst_len[L], cap = fresh ? 0u : M.lst_cap[L];
-    const unsigned long long off = fresh ? 0ull : M.lst_off[L];
+    const int lo = fresh ? 0 : tg_own[t];
+    const uint32_t oldlen = fresh ? 0u : j_ll[lo], cap = fresh ? 0u : j_lc[lo];
+    const unsigned long long off = fresh ? 0ull : j_lo[lo];
     const uint32_t need = oldlen + bound_s[t];
     unsigned long long newoff = off, movesrc = ~0ull;
     if (need > cap) {
