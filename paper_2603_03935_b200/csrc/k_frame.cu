@@ -991,14 +991,40 @@ __device__ __forceinline__ void red_add4(float4* p, float4 v) {
                : "memory");
 }
 
-size_t k4r_smem_bytes(int Df, int Dt) {
-  return (size_t)(1 + K4R_WARPS) * Df * 4 + (size_t)K4R_WARPS * Dt * 8;
+// bulk asynchronous copies (TMA engine, 1-D) into shared memory, completion on an mbarrier
+__device__ __forceinline__ uint32_t sm_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   sm_addr(dst)),
+               "l"(src), "r"(bytes), "r"(sm_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+          sm_addr(bar)),
+      "r"(parity)
+      : "memory");
 }
 
-template <bool SEM>
+// shared bytes of k_poolr: fbar, the warps' running sums, and (bulk path) two row stages per warp
+size_t k4r_smem_bytes(int Df, int Dt, bool bulk) {
+  return (size_t)(1 + K4R_WARPS) * Df * 4 + (size_t)K4R_WARPS * Dt * 8 +
+         (bulk ? (size_t)K4R_WARPS * 2 * ((size_t)Df * 4 + (size_t)Dt * 2) : 0);
+}
+
 #ifndef K4R_MINB
 #define K4R_MINB 4
 #endif
+// BULK: a warp's patch rows (CLIP row + tracking row) arrive by bulk async copies into a
+// two-stage shared-memory ring, the next patch in flight while this one is reduced.
+template <bool SEM, bool BULK>
 __global__ void __launch_bounds__(K4R_WARPS * 32, K4R_MINB) k_poolr(WinDesc wd, WinBufs wb, Params P) {
   const int f = blockIdx.y;
   if (f >= wd.n) return;
@@ -1013,6 +1039,10 @@ __global__ void __launch_bounds__(K4R_WARPS * 32, K4R_MINB) k_poolr(WinDesc wd, 
   float* fb_s = (float*)smem_raw;                                       // [Df] fbar
   float* ya = fb_s + Df + (size_t)warp * Df;                            // [Df] running pooled sum
   double* ua = (double*)(fb_s + (size_t)(1 + K4R_WARPS) * Df) + (size_t)warp * Dt;   // [Dt]
+  // (BULK) the warp's two stages: CLIP row [Df] floats, then tracking row [Dt] bf16
+  unsigned char* stg = (unsigned char*)((double*)(fb_s + (size_t)(1 + K4R_WARPS) * Df) + (size_t)K4R_WARPS * Dt) +
+                       (size_t)warp * 2 * ((size_t)Df * 4 + (size_t)Dt * 2);
+  __shared__ __align__(8) uint64_t bar_s[K4R_WARPS][2];
   if (pool)
     for (int d = threadIdx.x; d < Df; d += blockDim.x) fb_s[d] = wb.fbar[(size_t)f * Df + d];
   for (int d = lane; d < Df; d += 32) ya[d] = 0.f;
@@ -1061,20 +1091,44 @@ __global__ void __launch_bounds__(K4R_WARPS * 32, K4R_MINB) k_poolr(WinDesc wd, 
     if (pool && lane * 32 < Df) asm volatile("prefetch.global.L2 [%0];" ::"l"(F.feats + (size_t)pp * Df + lane * 32));
     if (Dt > 0 && lane * 64 < Dt) asm volatile("prefetch.global.L2 [%0];" ::"l"(F.track + (size_t)pp * Dt + lane * 64));
   };
-  prefetch(pr * Wp + pc0);
+  const uint32_t stage_bytes = (uint32_t)Df * 4 + (uint32_t)Dt * 2;
+  auto issue = [&](int pcx) {   // lane 0: the rows of patch pcx into stage (pcx - pc0) & 1
+    const int st = (pcx - pc0) & 1, pp = pr * Wp + pcx;
+    unsigned char* b = stg + (size_t)st * stage_bytes;
+    const uint32_t fb = pool ? (uint32_t)Df * 4 : 0u, tb = (uint32_t)Dt * 2;
+    mbar_expect_tx(&bar_s[warp][st], fb + tb);
+    if (fb) bulk_g2s(b, F.feats + (size_t)pp * Df, fb, &bar_s[warp][st]);
+    if (tb) bulk_g2s(b + (size_t)Df * 4, F.track + (size_t)pp * Dt, tb, &bar_s[warp][st]);
+  };
+  if (BULK) {
+    if (lane == 0) {
+      mbar_init(&bar_s[warp][0], 1);
+      mbar_init(&bar_s[warp][1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      issue(pc0);
+      if (pc0 + 1 < pc1) issue(pc0 + 1);
+    }
+    __syncwarp();
+  } else {
+    prefetch(pr * Wp + pc0);
+  }
   for (int pcx = pc0; pcx < pc1; ++pcx) {
     const int p = pr * Wp + pcx;
-    if (pcx + 1 < pc1) prefetch(p + 1);
+    const int st = (pcx - pc0) & 1;
+    if (BULK) mbar_wait(&bar_s[warp][st], ((pcx - pc0) >> 1) & 1);
+    else if (pcx + 1 < pc1) prefetch(p + 1);
+    const float4* srow = (const float4*)(stg + (size_t)st * stage_bytes);
+    const uint2* strk = (const uint2*)(stg + (size_t)st * stage_bytes + (size_t)Df * 4);
     float4 x[8];
     float r = 0.f;
     if (pool) {   // the patch's CLIP row and r_p (k_resid's arithmetic: per-lane fmaf, xor butterfly)
-      const float4* row = (const float4*)(F.feats + (size_t)p * Df);
+      const float4* row = BULK ? srow : (const float4*)(F.feats + (size_t)p * Df);
       float acc = 0.f;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         x[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (i < nq4 && lane + 32 * i < D4) {
-          x[i] = __ldg(row + lane + 32 * i);
+          x[i] = BULK ? row[lane + 32 * i] : __ldg(row + lane + 32 * i);
           const float4 m = ((const float4*)fb_s)[lane + 32 * i];
           const float a = x[i].x - m.x, b = x[i].y - m.y, c = x[i].z - m.z, e = x[i].w - m.w;
           acc = fmaf(a, a, acc); acc = fmaf(b, b, acc); acc = fmaf(c, c, acc); acc = fmaf(e, e, acc);
@@ -1090,7 +1144,8 @@ __global__ void __launch_bounds__(K4R_WARPS * 32, K4R_MINB) k_poolr(WinDesc wd, 
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       gv[k] = make_uint2(0u, 0u);
-      if (tvec && 4 * lane + 128 * k < Dt) gv[k] = __ldg((const uint2*)(F.track + (size_t)p * Dt) + lane + 32 * k);
+      if (tvec && 4 * lane + 128 * k < Dt)
+        gv[k] = BULK ? strk[lane + 32 * k] : __ldg((const uint2*)(F.track + (size_t)p * Dt) + lane + 32 * k);
     }
     // keep the slice's mask if it covers p, else flush it: p's first mask takes the slice
     if (cur >= 0 && cnt[(size_t)cur * wb.PMAXP + p] == 0) flush();
@@ -1175,6 +1230,10 @@ __global__ void __launch_bounds__(K4R_WARPS * 32, K4R_MINB) k_poolr(WinDesc wd, 
           }
         }
       }
+    }
+    if (BULK) {   // the stage is free again: the patch after next goes into it
+      __syncwarp();
+      if (lane == 0 && pcx + 2 < pc1) issue(pcx + 2);
     }
   }
   flush();
@@ -1336,17 +1395,29 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
   for (int i = 0; i < n; ++i)
     segs = std::max(segs, wd.f[i].Hp * ((wd.f[i].Wp + K4R_SEG - 1) / K4R_SEG));
   const dim3 gpr((segs + K4R_WARPS - 1) / K4R_WARPS, n);
-  const size_t smr = k4r_smem_bytes(P.Df, P.Dt);
-  static size_t smr_set = 0;
-  if (smr != smr_set) {
-    cudaFuncSetAttribute(k_poolr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
-    cudaFuncSetAttribute(k_poolr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
-    smr_set = smr;
+  // bulk path: 16-byte rows (Df % 4 == 0 holds; Dt % 8 == 0) and 16-byte aligned token arrays
+  // the bulk-copy variant measured slower (fewer resident warps for its staging rings): opt-in
+  static const bool bulk_ok = getenv("DISC_POOLR_BULK") != nullptr;
+  bool bulk = bulk_ok && (P.Dt % 8) == 0 && P.Dt <= 512;
+  for (int i = 0; i < n && bulk; ++i)
+    bulk = (((uintptr_t)wd.f[i].feats | (uintptr_t)wd.f[i].track) & 15) == 0;
+  const size_t smr = k4r_smem_bytes(P.Df, P.Dt, bulk);
+  static size_t smr_set[2] = {0, 0};
+  if (smr != smr_set[bulk]) {
+    if (bulk) {
+      cudaFuncSetAttribute(k_poolr<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
+      cudaFuncSetAttribute(k_poolr<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
+    } else {
+      cudaFuncSetAttribute(k_poolr<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
+      cudaFuncSetAttribute(k_poolr<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr);
+    }
+    smr_set[bulk] = smr;
   }
   if (sem) {
     k_filter<true><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
     debug_check(st, "k_filter", -1);
-    k_poolr<true><<<gpr, K4R_WARPS * 32, smr, st>>>(wd, wb, P);
+    if (bulk) k_poolr<true, true><<<gpr, K4R_WARPS * 32, smr, st>>>(wd, wb, P);
+    else k_poolr<true, false><<<gpr, K4R_WARPS * 32, smr, st>>>(wd, wb, P);
     debug_check(st, "k_poolr", -1);
     k_dmap<<<n, 1024, 0, st>>>(wd, wb, P);
     debug_check(st, "k_dmap", -1);
@@ -1357,7 +1428,8 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
   } else {
     k_filter<false><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
     debug_check(st, "k_filter", -1);
-    k_poolr<false><<<gpr, K4R_WARPS * 32, smr, st>>>(wd, wb, P);
+    if (bulk) k_poolr<false, true><<<gpr, K4R_WARPS * 32, smr, st>>>(wd, wb, P);
+    else k_poolr<false, false><<<gpr, K4R_WARPS * 32, smr, st>>>(wd, wb, P);
     debug_check(st, "k_poolr", -1);
     k_finalize<false><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
     debug_check(st, "k_finalize", -1);
