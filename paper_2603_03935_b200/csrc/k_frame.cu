@@ -118,6 +118,27 @@ __device__ __forceinline__ uint4 ld_stream16(const uint8_t* p) {
   return r;
 }
 
+// Streaming reads (each byte used once per window): L2 evict-first through a cache policy, so
+// the window's token / depth streams do not push the map's working set out of L2 while the
+// stage-2 kernel runs beside stage 1.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ float4 ld_f4_ef(const float4* p, uint64_t pol) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ float ld_f_ef(const float* p, uint64_t pol) {
+  float r;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
+  return r;
+}
+
 // ------------------------------------------------------------------------------------------
 // K0
 // ------------------------------------------------------------------------------------------
@@ -514,6 +535,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
     if (!(ablate & 2) && ut0 + warp * K1_TW < W) {
       const bool col_on = u < W;
       const bool edge = lane == 0 || lane == 31;
+      const uint64_t pol = policy_evict_first();
       const int uh = lane == 0 ? u - 1 : u + 1;   // halo column of the warp's edge lanes
       const bool h_on = SEM && edge && uh >= 0 && uh < W;
       const float xa = col_on ? __fdiv_rn(__fsub_rn((float)u, F.cx), F.fx) : 0.f;   // R5
@@ -566,8 +588,8 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
       for (int rr = 0; rr < rows; ++rr) {
         const int vv = vt0 + rr;
         // the next row's loads go out before this row's arithmetic
-        const float d_dn2 = rr < lim2 ? __ldg(dp) : 0.f;
-        const float d_h2 = rr < limh ? __ldg(hp) : 0.f;
+        const float d_dn2 = rr < lim2 ? ld_f_ef(dp, pol) : 0.f;
+        const float d_h2 = rr < limh ? ld_f_ef(hp, pol) : 0.f;
         const bool more = rr + 1 < rows;
         const uint32_t mv_n = (col_on && more) ? (uint32_t)*mp : 0xFFu;
         dp += W; hp += W; mp += W;
@@ -814,10 +836,11 @@ __global__ void __launch_bounds__(256) k_fbar_part(WinDesc wd, WinBufs wb, int D
   if (p0 >= P) return;
   const int p1 = min(P, p0 + K3_ROWS);
   double* part = wb.fpart + ((size_t)f * wb.FCHUNKS + ch) * Df;
+  const uint64_t pol = policy_evict_first();
   for (int d4 = threadIdx.x; d4 < Df / 4; d4 += blockDim.x) {
     double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
     for (int p = p0; p < p1; ++p) {
-      const float4 x = __ldg((const float4*)(F.feats + (size_t)p * Df) + d4);
+      const float4 x = ld_f4_ef((const float4*)(F.feats + (size_t)p * Df) + d4, pol);
       a0 += x.x; a1 += x.y; a2 += x.z; a3 += x.w;
     }
     part[4 * d4 + 0] = a0; part[4 * d4 + 1] = a1; part[4 * d4 + 2] = a2; part[4 * d4 + 3] = a3;
@@ -1032,6 +1055,7 @@ __global__ void __launch_bounds__(K4R_WARPS * 32, K4R_MINB) k_poolr(WinDesc wd, 
   const int H = F.H, W = F.W, Hp = F.Hp, Wp = F.Wp, S = F.S, Df = P.Df, Dt = P.Dt;
   const bool pool = SEM && F.feats;
   if (!pool && Dt == 0) return;
+  const uint64_t pol = policy_evict_first();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int segs_row = (Wp + K4R_SEG - 1) / K4R_SEG;
   const int seg = blockIdx.x * K4R_WARPS + warp;
@@ -1128,7 +1152,7 @@ __global__ void __launch_bounds__(K4R_WARPS * 32, K4R_MINB) k_poolr(WinDesc wd, 
       for (int i = 0; i < 8; ++i) {
         x[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (i < nq4 && lane + 32 * i < D4) {
-          x[i] = BULK ? row[lane + 32 * i] : __ldg(row + lane + 32 * i);
+          x[i] = BULK ? row[lane + 32 * i] : ld_f4_ef(row + lane + 32 * i, pol);
           const float4 m = ((const float4*)fb_s)[lane + 32 * i];
           const float a = x[i].x - m.x, b = x[i].y - m.y, c = x[i].z - m.z, e = x[i].w - m.w;
           acc = fmaf(a, a, acc); acc = fmaf(b, b, acc); acc = fmaf(c, c, acc); acc = fmaf(e, e, acc);
