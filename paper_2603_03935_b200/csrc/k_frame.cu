@@ -119,7 +119,7 @@ __device__ __forceinline__ uint4 ld_stream16(const uint8_t* p) {
 }
 
 // Streaming reads (each byte used once per window): L2 evict-first through a cache policy, so
-// the window's token / depth streams do not push the map's working set out of L2 while the
+// the window's token streams do not push the map's working set out of L2 while the
 // stage-2 kernel runs beside stage 1.
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;
@@ -131,11 +131,6 @@ __device__ __forceinline__ float4 ld_f4_ef(const float4* p, uint64_t pol) {
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
                : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
                : "l"(p), "l"(pol));
-  return r;
-}
-__device__ __forceinline__ float ld_f_ef(const float* p, uint64_t pol) {
-  float r;
-  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
   return r;
 }
 
@@ -535,7 +530,6 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
     if (!(ablate & 2) && ut0 + warp * K1_TW < W) {
       const bool col_on = u < W;
       const bool edge = lane == 0 || lane == 31;
-      const uint64_t pol = policy_evict_first();
       const int uh = lane == 0 ? u - 1 : u + 1;   // halo column of the warp's edge lanes
       const bool h_on = SEM && edge && uh >= 0 && uh < W;
       const float xa = col_on ? __fdiv_rn(__fsub_rn((float)u, F.cx), F.fx) : 0.f;   // R5
@@ -588,8 +582,8 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
       for (int rr = 0; rr < rows; ++rr) {
         const int vv = vt0 + rr;
         // the next row's loads go out before this row's arithmetic
-        const float d_dn2 = rr < lim2 ? ld_f_ef(dp, pol) : 0.f;
-        const float d_h2 = rr < limh ? ld_f_ef(hp, pol) : 0.f;
+        const float d_dn2 = rr < lim2 ? __ldg(dp) : 0.f;
+        const float d_h2 = rr < limh ? __ldg(hp) : 0.f;
         const bool more = rr + 1 < rows;
         const uint32_t mv_n = (col_on && more) ? (uint32_t)*mp : 0xFFu;
         dp += W; hp += W; mp += W;
@@ -635,10 +629,10 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
         const unsigned heads = __ballot_sync(0xffffffffu, item && !same_prev);
         if (items) {
           const float q0 = n0, q1 = n1, q2 = n2;   // this pixel's own normal
-          if (SEM) {   // segmented inclusive scan over the runs (only as many steps as the longest run)
+          if (SEM) {   // segmented inclusive scan over the runs
             const int start = 31 - __clz(heads & (0xFFFFFFFFu >> (31 - lane)));
-            const int maxd = (int)__reduce_max_sync(0xffffffffu, item ? (uint32_t)(lane - start) : 0u);
-            for (int o = 1; o <= maxd; o <<= 1) {
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
               const float a0 = __shfl_up_sync(0xffffffffu, n0, o);
               const float a1 = __shfl_up_sync(0xffffffffu, n1, o);
               const float a2 = __shfl_up_sync(0xffffffffu, n2, o);
