@@ -322,6 +322,36 @@ __global__ void __launch_bounds__(K1_THREADS, K1A_PERSIST) k_masks(WinDesc wd, W
         }
       }
     };
+    // the sector's row / patch segmentation, once for all planes: segment starts (bit j), their
+    // patch indices (up to K1A_NSEG), and the row break jb (W >= 32: at most two rows)
+    constexpr int K1A_NSEG = 8;
+    uint32_t segbits = 0;
+    int pidx[K1A_NSEG];
+    int nseg = 0;
+    bool fast = W >= 32;
+    {
+      int j = 0, v = v0, u = u0;
+      while (j < nv) {
+        const int len = min(W - u, nv - j);
+        const int prow = (v * Hp) / H * Wp;
+        int pcol = (u * Wp) / W;
+        int jj = j, uu = u;
+        while (jj < j + len) {
+          const int ub = ((pcol + 1) * W + Wp - 1) / Wp;   // first u of the next patch column
+          const int l2 = min(j + len - jj, ub - uu);
+          segbits |= 1u << jj;
+#pragma unroll
+          for (int k = 0; k < K1A_NSEG; ++k)
+            if (k == nseg) pidx[k] = prow + pcol;
+          ++nseg;
+          jj += l2; uu += l2; ++pcol;
+        }
+        j += len; ++v; u = 0;
+      }
+      if (nseg > K1A_NSEG) fast = false;
+    }
+    const int jb = u0 + nv > W ? W - u0 : 32;   // first pixel of the second row
+    const uint32_t rowA = jb >= 32 ? 0xFFFFFFFFu : ((1u << jb) - 1u);
     uint32_t m0[8], ovf = 0;
 #pragma unroll
     for (int t = 0; t < 8; ++t) m0[t] = 0xFFFFFFFFu;   // no mask yet
@@ -354,8 +384,33 @@ __global__ void __launch_bounds__(K1_THREADS, K1A_PERSIST) k_masks(WinDesc wd, W
         if (s + K1_NF < Sl) load(s + K1_NF, buf[k]);   // refill the ring slot
         set &= inb;
         if (!set) continue;
-        // row segments of the sector, and patch segments inside them: per-patch pixel counts
-        // (O5, regardless of depth, R17) and bbox
+        if (fast) {   // per-patch pixel counts (O5, regardless of depth, R17) and bbox
+          uint32_t sb = segbits;
+#pragma unroll
+          for (int k = 0; k < K1A_NSEG; ++k) {
+            if (k >= nseg) break;
+            const int a0 = __ffs(sb) - 1;
+            sb &= sb - 1;
+            const int b0 = sb ? __ffs(sb) - 1 : 32;
+            const int cn = __popc(set & range_bits(a0, b0));
+            if (cn) atomicAdd(&cnt_f[(size_t)s * wb.PMAXP + pidx[k]], (uint32_t)cn);
+          }
+          const uint32_t sa = set & rowA, sb2 = set & ~rowA;
+          if (sa) {
+            atomicMin(&bb_s[4 * s + 0], u0 + __ffs(sa) - 1);
+            atomicMax(&bb_s[4 * s + 2], u0 + 31 - __clz(sa));
+            atomicMin(&bb_s[4 * s + 1], v0);
+            atomicMax(&bb_s[4 * s + 3], v0);
+          }
+          if (sb2) {
+            atomicMin(&bb_s[4 * s + 0], __ffs(sb2) - 1 - jb);
+            atomicMax(&bb_s[4 * s + 2], 31 - __clz(sb2) - jb);
+            atomicMin(&bb_s[4 * s + 1], v0 + 1);
+            atomicMax(&bb_s[4 * s + 3], v0 + 1);
+          }
+          continue;
+        }
+        // general: row segments of the sector, and patch segments inside them
         int j = 0, v = v0, u = u0;
         while (j < nv) {
           const int len = min(W - u, nv - j);
