@@ -262,7 +262,8 @@ def main():
     t_gen = time.perf_counter() - t_gen
     maxS = max(fr["masks"].shape[0] for fr in frames)
     caps = dict(max_pixels=c.H * c.W, max_patches=c.Hp * c.Wp, max_masks=max(64, maxS), window=F,
-                max_memberships=1 << 23, max_instances=1 << 17, max_pairs_per_frame=1 << 17, device=local)
+                max_memberships=1 << 23, max_instances=1 << 17,
+                max_pairs_per_frame=int(os.environ.get("BENCH_PMAX", 1 << 17)), device=local)
 
     def run(frames_, timed_steps, warm_steps, m):
         for s in range(warm_steps):
