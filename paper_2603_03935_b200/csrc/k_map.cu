@@ -1247,7 +1247,7 @@ void k6_prof_dump() {
   if (getenv("DISC_S2PROF")) {
     unsigned long long g[8];
     cudaMemcpyFromSymbol(g, g_s2prof, sizeof(g));
-    fprintf(stderr, "s2 phase ns: lookup %llu assoc %llu apply %llu\n", g[0], g[1], g[2]);
+    fprintf(stderr, "s2 phase ns: lookup %llu assoc %llu apply %llu (64 barriers x launches: %llu)\n", g[0], g[1], g[2], g[7]);
     unsigned long long c[8];
     cudaMemcpyFromSymbol(c, g_s2cta, sizeof(c));
     fprintf(stderr, "s2 per-CTA work: lookup sum %llu max %llu, apply sum %llu max %llu\n", c[0], c[1], c[4], c[5]);
@@ -1266,15 +1266,13 @@ void k6_prof_dump() {
 // Grid-wide barrier of the persistent stage-2 kernel (all CTAs co-resident: the grid is sized to
 // the SMs K1 leaves free, one CTA per SM).  Monotonic counter, zeroed by K0 for the window.
 __device__ __forceinline__ void grid_sync(uint32_t* bar, uint32_t target) {
-  __syncthreads();
+  __syncthreads();   // the CTA's writes are ordered before thread 0's release (causality is cumulative)
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1u);
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
     uint32_t v;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
     } while (v < target);
-    __threadfence();
   }
   __syncthreads();
 }
@@ -1296,6 +1294,10 @@ __global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb
     }
   };
   probe(-1);
+  if (prof == 2) {   // DISC_S2PROF=2: cost of 64 empty grid barriers (profiling aid)
+    for (int i = 0; i < 64; ++i) grid_sync(wb.s2bar, G * ++ep);
+    probe(7);
+  }
   unsigned long long c0 = 0;
   auto cta_t = [&](int i) {   // this CTA's own work time in phase i (before its barrier wait)
     if (prof) __syncthreads();   // (prof is grid-uniform)
@@ -1336,7 +1338,7 @@ int launch_stage2(const WinDesc& wd, const WinBufs& wb, const MapState& M, const
     set_for = sm6;
   }
   const int grid = nres > 0 ? nres : std::min(16, nsm);
-  static const int prof = getenv("DISC_S2PROF") ? 1 : 0;
+  static const int prof = getenv("DISC_S2PROF") ? atoi(getenv("DISC_S2PROF")) : 0;
   // cooperative launch: its CTAs wait on one another at the grid barriers, so co-residency must
   // be guaranteed, not assumed
   int semi = sem ? 1 : 0;
