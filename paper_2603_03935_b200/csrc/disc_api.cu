@@ -330,7 +330,7 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   m->nsm = prop.multiProcessorCount;
   {  // stage-2 SM reserve; DISC_S2_SMS overrides it (tuning)
     const char* e = std::getenv("DISC_S2_SMS");
-    m->nres = e ? std::atoi(e) : 16;
+    m->nres = e ? std::atoi(e) : 20;
     m->nres = std::max(0, std::min(m->nres, m->nsm / 2));
   }
   Params& P = m->P;
