@@ -134,6 +134,14 @@ __device__ __forceinline__ float4 ld_f4_ef(const float4* p, uint64_t pol) {
   return r;
 }
 
+// Table fills with streaming (evict-first) stores: the window's frame tables are cleared without
+// displacing the map's working set in L2.
+__global__ void k_fill_cs(uint4* p, size_t n16, uint32_t v) {
+  const uint4 w = make_uint4(v, v, v, v);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
+    __stcs(p + i, w);
+}
+
 // ------------------------------------------------------------------------------------------
 // K0
 // ------------------------------------------------------------------------------------------
@@ -1433,9 +1441,9 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
   debug_check(st, "k_win_init", -1);
   // per-pair normal sums start from zero: one coalesced memset per window (zeroing the slots
   // one by one after use costs far more: scattered partial-line writes)
-  if (sem) cudaMemsetAsync(wb.nsum, 0, (size_t)n * wb.PC * sizeof(float4), st);
+  if (sem) k_fill_cs<<<4 * nsm, 256, 0, st>>>((uint4*)wb.nsum, (size_t)n * wb.PC, 0u);
   // the frames' key tables start empty (one memset per window; no per-pair release in stage 2)
-  cudaMemsetAsync(wb.ktab, 0xFF, (size_t)n * wb.PC * sizeof(unsigned long long), st);
+  k_fill_cs<<<4 * nsm, 256, 0, st>>>((uint4*)wb.ktab, (size_t)n * wb.PC / 2, 0xFFFFFFFFu);
   if (ev0) cudaEventRecord(ev0, st);
   int64_t maxHW = 1;
   bool vec = true;
@@ -1507,7 +1515,7 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
     k_finalize<false><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
     debug_check(st, "k_finalize", -1);
   }
-  return sem ? 12 : 7;
+  return sem ? 14 : 8;
 }
 
 }  // namespace disc
