@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1A_PERSIST) k_masks(WinDesc wd, W
             q[2 * h] = __byte_perm(w, 0, 0x4140) | ((ob & 1u) << 8) | (((ob >> 1) & 1u) << 24);
             q[2 * h + 1] = __byte_perm(w, 0, 0x4342) | (((ob >> 2) & 1u) << 8) | (((ob >> 3) & 1u) << 24);
           }
-          ((uint4*)mo)[t / 2] = make_uint4(q[0], q[1], q[2], q[3]);
+          __stcs((uint4*)mo + t / 2, make_uint4(q[0], q[1], q[2], q[3]));   // streaming: read once by K1b
         }
       } else {
         for (int j = 0; j < nv; ++j)
@@ -645,10 +645,10 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
       for (int rr = 0; rr < rows; ++rr) {
         const int vv = vt0 + rr;
         // the next row's loads go out before this row's arithmetic
-        const float d_dn2 = rr < lim2 ? __ldg(dp) : 0.f;
-        const float d_h2 = rr < limh ? __ldg(hp) : 0.f;
+        const float d_dn2 = rr < lim2 ? __ldcs(dp) : 0.f;   // streaming (evict-first) reads
+        const float d_h2 = rr < limh ? __ldcs(hp) : 0.f;
         const bool more = rr + 1 < rows;
-        const uint32_t mv_n = (col_on && more) ? (uint32_t)*mp : 0xFFu;
+        const uint32_t mv_n = (col_on && more) ? (uint32_t)__ldcs(mp) : 0xFFu;
         dp += W; hp += W; mp += W;
         const float ybn = yb_s[rr + 2];
         float pd[3] = {0.f, 0.f, 0.f};
@@ -1226,7 +1226,7 @@ __global__ void __launch_bounds__(K4R_WARPS * 32, K4R_MINB) k_poolr(WinDesc wd, 
     for (int k = 0; k < 4; ++k) {
       gv[k] = make_uint2(0u, 0u);
       if (tvec && 4 * lane + 128 * k < Dt)
-        gv[k] = BULK ? strk[lane + 32 * k] : __ldg((const uint2*)(F.track + (size_t)p * Dt) + lane + 32 * k);
+        gv[k] = BULK ? strk[lane + 32 * k] : __ldcs((const uint2*)(F.track + (size_t)p * Dt) + lane + 32 * k);
     }
     // keep the slice's mask if it covers p, else flush it: p's first mask takes the slice
     if (cur >= 0 && cnt[(size_t)cur * wb.PMAXP + p] == 0) flush();
