@@ -182,7 +182,8 @@ __device__ __forceinline__ void lk_probe(int i, unsigned long long& tp) {
 }
 constexpr int LK_CT = 2048;   // per-CTA (s, j) count table slots (in the dynamic shared memory)
 
-__device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapState& M, const FrameScratch& X) {
+__device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapState& M, const FrameScratch& X,
+                                          int Dt) {
   const uint32_t np = min(wb.npairs[f], (uint32_t)wb.PMAX);
   const size_t fo = (size_t)f * wb.PMAX;
   const int lane = threadIdx.x & 31;
@@ -313,7 +314,12 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
   __syncthreads();
   lk_probe(1, tp);
   for (int i = threadIdx.x; i < LK_CT; i += blockDim.x)   // flush the CTA's counts
-    if (cc[i]) count_add(X, ck[i], cc[i], M.err);
+    if (cc[i]) {
+      count_add(X, ck[i], cc[i], M.err);
+      // warm L2 with the instance's tracking sum T_j for the association's visual gate
+      const double* Tj = M.T + (size_t)(uint32_t)ck[i] * Dt;
+      for (int d = 0; d < Dt; d += 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(Tj + d));
+    }
   __syncthreads();
   lk_probe(2, tp);
 }
@@ -1311,7 +1317,7 @@ __global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb
   for (int f = 0; f < wd.n; ++f) {
     const FrameDesc& F = wd.f[f];
     cta_t(-1);
-    s2_lookup(f, wb, M, X);
+    s2_lookup(f, wb, M, X, P.Dt);
     if (f > 0) s2_finalize(f - 1, M, X);
     cta_t(0);
     grid_sync(wb.s2bar, G * ++ep);
