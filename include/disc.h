@@ -185,6 +185,11 @@ disc_status disc_wait(disc_map* m, void* stream);  /* order `stream` after all q
 disc_status disc_sync(disc_map* m);    /* wait for the map's work; surfaces device errors */
 const char* disc_last_error(const disc_map* m);
 const char* disc_version(void);
+/* NCCL unique id for the key-sharded map: 128 bytes that rank 0 creates
+ * and broadcasts out of band; every rank then passes it in disc_config.nccl_unique_id.  Loads
+ * libnccl.so.2 at run time; DISC_ERR_NCCL if it is missing or fails.  (The sharded map itself is
+ * NEXT: disc_map_create returns DISC_ERR_UNSUPPORTED for world_size > 1 this round.) */
+disc_status disc_nccl_unique_id(uint8_t out[128]);
 
 #ifdef __cplusplus
 }

@@ -5,6 +5,7 @@
 // Every step of the hot path runs in the kernels of k_frame.cu / k_map.cu; this file only
 // validates, sizes, launches and copies.
 #include <cmath>
+#include <dlfcn.h>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -251,6 +252,19 @@ extern "C" {
 
 const char* disc_version(void) { return VERSION; }
 
+disc_status disc_nccl_unique_id(uint8_t out[128]) {
+  if (!out) return DISC_ERR_INVALID;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+  if (!h) return DISC_ERR_NCCL;
+  typedef int (*get_id_fn)(void*);   // ncclResult_t ncclGetUniqueId(ncclUniqueId*), 128-byte id
+  get_id_fn get_id = (get_id_fn)dlsym(h, "ncclGetUniqueId");
+  if (!get_id) return DISC_ERR_NCCL;
+  unsigned char id[128];
+  if (get_id(id) != 0) return DISC_ERR_NCCL;
+  std::memcpy(out, id, 128);
+  return DISC_OK;
+}
+
 disc_status disc_config_init(disc_config* c) {
   if (!c) return DISC_ERR_INVALID;
   std::memset(c, 0, sizeof(*c));
@@ -306,6 +320,7 @@ static std::string validate_config(const disc_config* c) {
 disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   if (!cfg || !out) return DISC_ERR_INVALID;
   *out = nullptr;
+  if (cfg->world_size > 1) return DISC_ERR_UNSUPPORTED;   // key-sharded map: NEXT
   const std::string v = validate_config(cfg);
   if (!v.empty()) {
     std::fprintf(stderr, "disc_map_create: %s\n", v.c_str());

@@ -108,6 +108,7 @@ EXPORTS = {
     "disc_sync": (C.c_int, [C.c_void_p]),
     "disc_last_error": (C.c_char_p, [C.c_void_p]),
     "disc_version": (C.c_char_p, []),
+    "disc_nccl_unique_id": (C.c_int, [C.c_void_p]),
 }
 
 _lib = None
@@ -142,6 +143,15 @@ def _ptr(t):
     if t is None:
         return None
     return C.c_void_p(t.data_ptr())
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (disc_nccl_unique_id), for disc_config.nccl_unique_id."""
+    buf = (C.c_uint8 * 128)()
+    rc = lib().disc_nccl_unique_id(C.cast(buf, C.c_void_p))
+    if rc != DISC_OK:
+        raise DiscError(rc, "disc_nccl_unique_id failed (libnccl.so.2 missing?)")
+    return bytes(buf)
 
 
 class DiscMap:

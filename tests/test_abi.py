@@ -101,3 +101,11 @@ def test_invalid_config_rejected(built):
 def test_sass_is_sm100a(built):
     out = subprocess.run(["cuobjdump", "--list-elf", built.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_nccl_unique_id_export():
+    """disc_nccl_unique_id: 128 bytes from NCCL's bootstrap (no GPU needed); fresh per call."""
+    from paper_2603_03935_b200.disc import nccl_unique_id
+    a, b = nccl_unique_id(), nccl_unique_id()
+    assert len(a) == 128 and any(a)
+    assert a != b
