@@ -466,6 +466,7 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(X.tg_dcnt = dalloc<uint32_t>(m, SM));
   chk(X.tg_mem = dalloc<uint32_t>(m, X.TCAP));
   chk(X.tg_dets = dalloc<uint32_t>(m, SM));
+  chk(X.tg_cand = dalloc<uint32_t>(m, (size_t)SM * 32));
   chk(X.seg_phys = dalloc<uint32_t>(m, X.TCAP));
   chk(X.seg_tgt = dalloc<int32_t>(m, X.TCAP));
   chk(X.seg_off = dalloc<uint32_t>(m, X.TCAP + 1));

@@ -183,6 +183,7 @@ struct FrameScratch {
   uint32_t* tg_dcnt;
   uint32_t* tg_mem;              // [TCAP]
   uint32_t* tg_dets;             // [SMAX]
+  uint32_t* tg_cand;             // [SMAX][32] per target: members then detections (first 32), for K7's fast path
   // relabel segments
   uint32_t* seg_phys;            // [TCAP] old physical label
   int32_t* seg_tgt;              // [TCAP]

@@ -389,7 +389,8 @@ struct K6Smem {   // offsets into dynamic shared memory
 __device__ unsigned long long g_k6prof[16];
 __device__ unsigned long long g_s2prof[8];   // DISC_S2PROF phase sums
 __device__ unsigned long long g_s2cta[8];
-__device__ unsigned long long g_s2items[4];   // DISC_S2PROF: K7 items: pairs, relabels, list-move copies, targets
+__device__ unsigned long long g_s2items[4];
+__device__ unsigned long long g_tgprof[4];   // DISC_S2PROF: target-update warp time sum / max, count, item-loop time sum   // DISC_S2PROF: K7 items: pairs, relabels, list-move copies, targets
 #define K6_PROBE(i)                                                                          \
   do {                                                                                       \
     if (threadIdx.x == 0) {                                                                  \
@@ -679,6 +680,7 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
 #pragma unroll 8
     for (int s3 = 0; s3 < s2; ++s3) rank += d_tgt[s3] == t;
     X.tg_dets[doff_s[t] + rank] = (uint32_t)s2;
+    if (mcnt_s[t] + rank < 32) X.tg_cand[t * 32 + mcnt_s[t] + rank] = (uint32_t)s2;
   }
   __syncthreads();
   for (int l = tid; l < nJ; l += blockDim.x) {
@@ -688,6 +690,7 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
 #pragma unroll 8
     for (int l2 = 0; l2 < nJ; ++l2) rank += (tl_s[l2] == t) & (jnode[l2] < j);   // ids are distinct
     X.tg_mem[moff_s[t] + rank] = j;
+    if (rank < 32) X.tg_cand[t * 32 + rank] = j;
     const uint32_t pm = j_ph[l];
     if (pm != tg_phys[t]) {   // the smaller sets: relabel into the survivor's physical label
       const uint32_t sg = atomicAdd(&n_seg, 1u);
@@ -996,9 +999,11 @@ __device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc&
     return;
   }
   const uint32_t n = mcnt + dcnt;
-  // candidate of this lane: members (ids ascending) then detections (s ascending)
+  // candidate of this lane: members (ids ascending) then detections (s ascending); K6 wrote them
+  // side by side (tg_cand), one read with the descriptors
   const bool is_mem = (uint32_t)lane < mcnt, is_det = !is_mem && (uint32_t)lane < n;
-  const uint32_t cid = is_mem ? X.tg_mem[moff + lane] : (is_det ? X.tg_dets[doff + lane - mcnt] : 0u);
+  const uint32_t cid = (is_mem || is_det) ? X.tg_cand[t * 32 + lane] : 0u;
+
   // attributes of the candidate
   int obs = 0;
   float qi = -INFINITY;
@@ -1018,6 +1023,15 @@ __device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc&
   double acc[16];
   const int nt = (Dt + 31) / 32;
   const uint32_t cid0 = __shfl_sync(0xffffffffu, cid, 0);   // (outside the lane-dependent branches)
+  // new instance: its embedding row is read now, in flight with the tracking row below
+  const int D4 = Df / 4, nq4 = (D4 + 31) / 32;
+  float4 ev[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    ev[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (kind == 1 && sem && i < nq4 && lane + 32 * i < D4)
+      ev[i] = ((const float4*)(wb.emb + (fo + cid0) * Df))[lane + 32 * i];
+  }
   const uint32_t first = 1;   // candidate 0 is the base: T_root (= mem[0], the min id) or t_s1
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
@@ -1077,7 +1091,9 @@ __device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc&
                                                        : (const float4*)(wb.emb + (fo + sid) * Df));
   float4* ed = (float4*)(M.E + (size_t)root * Df);
   if (kind == 1) {
-    for (int d4 = lane; d4 < Df / 4; d4 += 32) ed[d4] = has_e ? es[d4] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i < nq4 && lane + 32 * i < D4) ed[lane + 32 * i] = has_e ? ev[i] : make_float4(0.f, 0.f, 0.f, 0.f);
   } else if (has_e) {
     for (int d4 = lane; d4 < Df / 4; d4 += 32) ed[d4] = es[d4];
   }
@@ -1116,7 +1132,9 @@ __device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc&
 __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBufs& wb, const MapState& M,
                                          const FrameScratch& X, const Params& P, int sem) {
   const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), nw = gridDim.x * (blockDim.x >> 5);
+  // targets spread over the CTAs first (warp w of CTA b takes target w * G + b), so no CTA holds
+  // them all and the items are shared out evenly
+  const int gw = (threadIdx.x >> 5) * gridDim.x + blockIdx.x, nw = gridDim.x * (blockDim.x >> 5);
   const int ntgt = *X.ntgt;
   // per-detection / per-target routing in shared memory (the association's bytes are free now)
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1131,7 +1149,17 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
     to_s[t] = X.tg_newoff[t];
   }
   __syncthreads();
-  for (int t = gw; t < ntgt; t += nw) apply_target_warp(t, f, F, wb, M, X, P, sem);
+  for (int t = gw; t < ntgt; t += nw) {
+    unsigned long long t0_, t1_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0_));
+    apply_target_warp(t, f, F, wb, M, X, P, sem);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1_));
+    if (lane == 0) {
+      atomicAdd(&g_tgprof[0], t1_ - t0_);
+      atomicMax(&g_tgprof[1], t1_ - t0_);
+      atomicAdd(&g_tgprof[2], 1ull);
+    }
+  }
   const uint32_t np = min(wb.npairs[f], (uint32_t)wb.PMAX);
   const uint32_t nrel = *X.nrel;
   const uint32_t nmove = X.tg_mvoff[ntgt];
@@ -1145,62 +1173,76 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
   const size_t fo = (size_t)f * wb.PMAX;
   const int nseg = *X.nseg;
   int delta = 0;
-  // items: frame pairs (inserts), relabel items, entries of lists K6 moved (copies); 32-item
-  // chunks from a counter (the target warps take fewer)
+  // items: frame pairs (inserts), relabel items, entries of lists K6 moved (copies); 64-item
+  // chunks from a counter (the target warps take fewer), two items per lane with their record
+  // loads issued together
   for (;;) {
     uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(X.work, 32u);
+    if (lane == 0) base = atomicAdd(X.work, 64u);
     base = __shfl_sync(0xffffffffu, base, 0);
     if (base >= total) break;
-    const uint32_t it = base + lane;
-    int tnew = -1;
-    uint32_t snew = 0;
-    if (it < np) {
-      const uint32_t s = wb.pinfo[fo + it];
-      const int t = dt_s[s];
-      if (t >= 0) {
-        const uint32_t L = tp_s[t];
-        uint32_t slot = wb.pms[fo + it];
-        const uint2 pl = wb.plab[fo + it];
-        if (!(slot != U32_EMPTY && (pl.x == L || pl.y == L))) {   // else: already a member
-          if (slot == U32_EMPTY) slot = map_insert_key(M, wb.pkey[fo + it]);
-          if (slot != U32_EMPTY && label_insert(M, slot, L)) { tnew = t; snew = slot; delta++; }
-        }
+    uint32_t itq[2], sq[2], slotq[2];
+    uint2 plq[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {   // the pair records of both items first
+      itq[q] = base + 32 * q + lane;
+      sq[q] = 0; slotq[q] = U32_EMPTY; plq[q] = make_uint2(U32_EMPTY, U32_EMPTY);
+      if (itq[q] < np) {
+        sq[q] = wb.pinfo[fo + itq[q]];
+        slotq[q] = wb.pms[fo + itq[q]];
+        plq[q] = wb.plab[fo + itq[q]];
       }
-    } else if (it < np + nrel) {
-      const uint32_t r = it - np;
-      int lo = 0, hi = nseg - 1;   // last segment with seg_off <= r
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (X.seg_off[mid] <= r) lo = mid;
-        else hi = mid - 1;
-      }
-      const int t = X.seg_tgt[lo];
-      const uint32_t L = tp_s[t];
-      const uint32_t slot = M.arena[X.seg_base[lo] + (r - X.seg_off[lo])];
-      if (label_insert(M, slot, L)) { tnew = t; snew = slot; delta++; }
-      if (label_tomb(M, slot, X.seg_phys[lo])) delta--;
-    } else if (it < total) {
-      const uint32_t r = it - np - nrel;
-      int lo = 0, hi = ntgt - 1;   // last target with tg_mvoff <= r
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (X.tg_mvoff[mid] <= r) lo = mid;
-        else hi = mid - 1;
-      }
-      const uint32_t i = r - X.tg_mvoff[lo];
-      M.arena[X.tg_newoff[lo] + i] = M.arena[X.tg_movesrc[lo] + i];
     }
-    // append the new (target, slot) entries to the targets' lists (warp-aggregated positions;
-    // K6 reserved the room)
-    const unsigned peers = __match_any_sync(0xffffffffu, tnew);
-    const int leader = __ffs(peers) - 1;
-    uint32_t pb = 0;
-    if (tnew >= 0 && lane == leader) pb = atomicAdd(&X.tgt_stage[tnew], (uint32_t)__popc(peers));
-    pb = __shfl_sync(0xffffffffu, pb, leader);
-    if (tnew >= 0) {
-      const uint32_t pos = tb_s[tnew] + pb + __popc(peers & ((1u << lane) - 1u));
-      M.arena[to_s[tnew] + pos] = snew;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const uint32_t it = itq[q];
+      int tnew = -1;
+      uint32_t snew = 0;
+      if (it < np) {
+        const int t = dt_s[sq[q]];
+        if (t >= 0) {
+          const uint32_t L = tp_s[t];
+          uint32_t slot = slotq[q];
+          if (!(slot != U32_EMPTY && (plq[q].x == L || plq[q].y == L))) {   // else: already a member
+            if (slot == U32_EMPTY) slot = map_insert_key(M, wb.pkey[fo + it]);
+            if (slot != U32_EMPTY && label_insert(M, slot, L)) { tnew = t; snew = slot; delta++; }
+          }
+        }
+      } else if (it < np + nrel) {
+        const uint32_t r = it - np;
+        int lo = 0, hi = nseg - 1;   // last segment with seg_off <= r
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (X.seg_off[mid] <= r) lo = mid;
+          else hi = mid - 1;
+        }
+        const int t = X.seg_tgt[lo];
+        const uint32_t L = tp_s[t];
+        const uint32_t slot = M.arena[X.seg_base[lo] + (r - X.seg_off[lo])];
+        if (label_insert(M, slot, L)) { tnew = t; snew = slot; delta++; }
+        if (label_tomb(M, slot, X.seg_phys[lo])) delta--;
+      } else if (it < total) {
+        const uint32_t r = it - np - nrel;
+        int lo = 0, hi = ntgt - 1;   // last target with tg_mvoff <= r
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (X.tg_mvoff[mid] <= r) lo = mid;
+          else hi = mid - 1;
+        }
+        const uint32_t i = r - X.tg_mvoff[lo];
+        M.arena[X.tg_newoff[lo] + i] = M.arena[X.tg_movesrc[lo] + i];
+      }
+      // append the new (target, slot) entries to the targets' lists (warp-aggregated positions;
+      // K6 reserved the room)
+      const unsigned peers = __match_any_sync(0xffffffffu, tnew);
+      const int leader = __ffs(peers) - 1;
+      uint32_t pb = 0;
+      if (tnew >= 0 && lane == leader) pb = atomicAdd(&X.tgt_stage[tnew], (uint32_t)__popc(peers));
+      pb = __shfl_sync(0xffffffffu, pb, leader);
+      if (tnew >= 0) {
+        const uint32_t pos = tb_s[tnew] + pb + __popc(peers & ((1u << lane) - 1u));
+        M.arena[to_s[tnew] + pos] = snew;
+      }
     }
   }
 #pragma unroll
@@ -1261,6 +1303,8 @@ void k6_prof_dump() {
     fprintf(stderr, "s2 K7 items: pairs %llu relabels %llu moves %llu targets %llu\n", c[0], c[1], c[2], c[3]);
     cudaMemcpyFromSymbol(c, g_lkprof, 3 * sizeof(unsigned long long));
     fprintf(stderr, "s2 lookup CTA0: init %llu loop %llu flush %llu\n", c[0], c[1], c[2]);
+    cudaMemcpyFromSymbol(c, g_tgprof, 3 * sizeof(unsigned long long));
+    fprintf(stderr, "s2 target warps: sum %llu max %llu count %llu\n", c[0], c[1], c[2]);
   }
   unsigned long long h[16];
   cudaMemcpyFromSymbol(h, g_k6prof, sizeof(h));
