@@ -26,7 +26,8 @@ struct disc_map {
   disc_config cfg;
   Params P;
   int dev = 0, nsm = 148;
-  int nres = 0;   // SMs reserved for stage 2 (0 = no partition)
+  int nres = 0;       // SMs reserved for stage 2 (0 = no partition), windows with CLIP tokens
+  int nres_geo = 0;   // the same for geometry-only windows (lighter stage 1: more SMs to stage 2)
   MapState M{};
   WinBufs Wb[2]{};               // double-buffered window buffers (stage 1 of window w+1 overlaps
                                  // stage 2 of window w)
@@ -347,6 +348,9 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
     const char* e = std::getenv("DISC_S2_SMS");
     m->nres = e ? std::atoi(e) : 20;
     m->nres = std::max(0, std::min(m->nres, m->nsm / 2));
+    const char* eg = std::getenv("DISC_S2_SMS_GEO");
+    m->nres_geo = eg ? std::atoi(eg) : 40;
+    m->nres_geo = std::max(0, std::min(m->nres_geo, m->nsm / 2));
   }
   Params& P = m->P;
   P.r = cfg->voxel_size; P.tau_geo = cfg->tau_geo; P.tau_vis = cfg->tau_vis;
@@ -596,13 +600,13 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
       cudaEventRecord(t0, s1);
     }
     tl_mark(s1, "s1_begin", -1);
-    m->stats.launches += launch_stage1(wd, Wbuf, m->P, m->d_err, sem, maxS, maxHp, maxW, maxWp, maxP, rows, m->nsm, m->nres, s1, e0, e1);
+    m->stats.launches += launch_stage1(wd, Wbuf, m->P, m->d_err, sem, maxS, maxHp, maxW, maxWp, maxP, rows, m->nsm, sem ? m->nres : m->nres_geo, s1, e0, e1);
     if (m->timing) cudaEventRecord(t1, s1);
     cudaEventRecord(m->ev_s1[b], s1);
     cudaStreamWaitEvent(s2, m->ev_s1[b], 0);
     if (m->timing) cudaEventRecord(t1b, s2);
     tl_mark(s2, "s2_begin", -1);
-    m->stats.launches += launch_stage2(wd, Wbuf, m->M, m->X, m->P, sem, m->nsm, m->nres, s2);
+    m->stats.launches += launch_stage2(wd, Wbuf, m->M, m->X, m->P, sem, m->nsm, sem ? m->nres : m->nres_geo, s2);
     if (m->timing) {
       cudaEventRecord(t2, s2);
       m->ev_pending.push_back({e0, e1, 0});
