@@ -1140,7 +1140,7 @@ __global__ void __launch_bounds__(K4R_WARPS * 32, K4R_MINB) k_poolr(WinDesc wd, 
   uint32_t keptl = 0;
   for (int q = 0; q < nch; ++q)
     if (32 * q + lane < S && wb.status[gbase + 32 * q + lane] == 0) keptl |= 1u << q;
-  const int64_t rows = ((int64_t)(pr + 1) * H + Hp - 1) / Hp - ((int64_t)pr * H + Hp - 1) / Hp;
+  const int rows = ((pr + 1) * H + Hp - 1) / Hp - (pr * H + Hp - 1) / Hp;
   int cur = -1;                     // mask whose sums the warp's slice holds
   double sc0 = 0, sc1 = 0, sc2 = 0; // its R18 / R19 scalar sums
   auto flush = [&]() {
@@ -1230,7 +1230,8 @@ __global__ void __launch_bounds__(K4R_WARPS * 32, K4R_MINB) k_poolr(WinDesc wd, 
     }
     // keep the slice's mask if it covers p, else flush it: p's first mask takes the slice
     if (cur >= 0 && cnt[(size_t)cur * wb.PMAXP + p] == 0) flush();
-    const int64_t cols = ((int64_t)(pcx + 1) * W + Wp - 1) / Wp - ((int64_t)pcx * W + Wp - 1) / Wp;
+    // patch pixel count (R17), 32-bit: W, H <= 16384
+    const int cols = ((pcx + 1) * W + Wp - 1) / Wp - (pcx * W + Wp - 1) / Wp;
     const double npix = (double)(rows * cols);
     for (int q = 0; q < nch; ++q) {   // the kept masks covering p, 32 per ballot
       const uint32_t c_l = ((keptl >> q) & 1u) ? cnt[(size_t)(32 * q + lane) * wb.PMAXP + p] : 0u;
