@@ -327,7 +327,10 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
 // ------------------------------------------------------------------------------------------
 // K6: association (single CTA)
 // ------------------------------------------------------------------------------------------
-constexpr int K6_THREADS = 512;
+#ifndef K6_T
+#define K6_T 512
+#endif
+constexpr int K6_THREADS = K6_T;
 
 __device__ __forceinline__ double dot_pin_w(const double* a, const double* b, int n) {
   const int lane = threadIdx.x & 31;
