@@ -322,7 +322,7 @@ def main():
                    "frames_timed_per_rank": args.steps * F, "masks_per_frame_mean":
                        round(sum(fr["masks"].shape[0] for fr in timed) / len(timed), 1),
                    "parallelism": f"{ws} independent maps (one scene stream per rank)" if ws > 1 else "1 GPU"},
-        "roofline": {"bound": "hbm", "kernel": "K1 mask pass (k_masks + k_walk)", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": "K1 mask pass (k_masks + k_walk + k_dedup)", "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
                      "traffic": traffic, "algorithmic_bytes_per_launch": k1_bytes / max(k1_launches, 1),
                      "avg_launch_ms": k1_ms / max(k1_launches, 1), "launches": k1_launches,

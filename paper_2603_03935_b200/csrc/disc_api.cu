@@ -367,12 +367,18 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   for (int wbi = 0; wbi < 2; ++wbi) {
   WinBufs& W = m->Wb[wbi];
   W.PC = (int32_t)PC; W.PMAX = (int32_t)PMAX; W.SMAX = SM; W.PMAXP = (int32_t)PMP;
+  W.RCAP = (int32_t)PMAX;
+  if (const char* e = getenv("DISC_K1_RCAP")) W.RCAP = (int32_t)std::max<int64_t>(0, std::min<int64_t>(PMAX, atoll(e)));   // tests
   W.FCHUNKS = (int32_t)((PMP + 63) / 64);
   chk(W.ktab = dalloc<unsigned long long>(m, (size_t)win * PC, 0xFF));
   chk(W.ptab = dalloc<uint32_t>(m, (size_t)win * PC, 0xFF));
   chk(W.nsum = dalloc<float4>(m, (size_t)win * PC, 0));
   chk(W.plist = dalloc<uint32_t>(m, (size_t)win * PMAX));
   chk(W.npairs = dalloc<uint32_t>(m, win));
+  chk(W.rkey = dalloc<unsigned long long>(m, (size_t)win * PMAX));
+  chk(W.rs = dalloc<uint32_t>(m, (size_t)win * PMAX));
+  chk(W.rn = dalloc<float4>(m, (size_t)win * PMAX));
+  chk(W.rcount = dalloc<uint32_t>(m, win));
   chk(W.cnt = dalloc<uint32_t>(m, (size_t)win * SM * PMP));
   chk(W.area = dalloc<uint32_t>(m, (size_t)win * SM));
   chk(W.bbox = dalloc<int32_t>(m, (size_t)win * SM * 4));

@@ -81,6 +81,12 @@ struct WinBufs {
   float4* nsum;               // [win][PC] per-pair normal sums (semantic mode; w unused)
   uint32_t* plist;            // [win][PMAX] pair slots in insertion order
   uint32_t* npairs;           // [win]
+  // K1b -> K1c: each tile's distinct (s, key) items with their normal sums
+  unsigned long long* rkey;   // [win][PMAX] key
+  uint32_t* rs;               // [win][PMAX] mask index s
+  float4* rn;                 // [win][PMAX] normal sum (semantic mode)
+  uint32_t* rcount;           // [win] records reserved; a tile whose block passes RCAP inserts its
+                              // items itself and writes KEY_EMPTY into its records below RCAP
   uint32_t* cnt;              // [win][SMAX][PMAXP] mask pixels per patch
   uint32_t* area;             // [win][SMAX]
   int32_t* bbox;              // [win][SMAX][4] umin, vmin, umax, vmax
@@ -117,6 +123,7 @@ struct WinBufs {
   uint32_t* s2bar;            // [1] stage-2 grid barrier counter (zeroed by K0)
   int32_t PC;                 // frame table capacity (power of 2)
   int32_t PMAX, SMAX, PMAXP, FCHUNKS;
+  int32_t RCAP;               // record list capacity per frame (PMAX; DISC_K1_RCAP lowers it in tests)
 };
 
 // ---- map state ---------------------------------------------------------------------------

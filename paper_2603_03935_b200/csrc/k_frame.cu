@@ -171,6 +171,7 @@ __global__ void k_win_init(WinDesc wd, WinBufs wb) {
     wb.trk[(size_t)f * wb.SMAX * wd.Dt + i] = 0.0;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     wb.npairs[f] = 0;
+    wb.rcount[f] = 0;
     wb.oor[f] = 0;
     if (f == 0) { wb.k1ctr[0] = 0; wb.k1ctr[1] = 0; *wb.s2bar = 0; }   // K1a/K1b work counters, stage-2 barrier
   }
@@ -192,11 +193,12 @@ __global__ void k_win_init(WinDesc wd, WinBufs wb) {
 //               second mask" bit go to HBM maps; per-patch pixel counts (R17) and bboxes.
 //  K1b k_walk   lane = column, one row per step: depth -> pinned world point and key (R5), each
 //               world point computed once (row below computed ahead, row above kept, left/right
-//               from the adjacent lanes); runs of equal (m0, key) along the row are found with a
-//               ballot, their pixel normals (R21) summed by a segmented shuffle scan, and the run's
-//               last lane emits the (s, key) item into the CTA key / pair tables.  Pixels in more
-//               than one mask (R9) emit their other masks per pixel.  The tile's distinct pairs
-//               then go to the frame's key / pair tables.
+//               from the adjacent lanes); a lane sums its pixel normals (R21) in registers while
+//               its (m0, key) repeats down the column, and a finished run goes to the warp's
+//               shared-memory queue (one ballot), drained 32 at a time into the CTA key / pair
+//               tables.  Pixels in more than one mask (R9) emit their other masks per pixel.  The
+//               tile's distinct pairs go to the frame's record list.
+//  K1c k_dedup  one record per thread into the frame's key / pair tables (|V_s|, pair list).
 // ------------------------------------------------------------------------------------------
 #ifndef K1A_PERSIST
 #define K1A_PERSIST 6
@@ -214,6 +216,10 @@ constexpr int K1_TILE_W = K1_WARPS * K1_TW;               // CTA tile: 32 rows x
 constexpr int K1_TILE_H = 32;
 constexpr int K1_KT = K1_PT / 2;                          // CTA key table slots (2 pair slots each)
 constexpr int K1_PLIST = 512;
+constexpr uint32_t K1_Q = 64;
+#ifndef K1C_BLOCKS
+#define K1C_BLOCKS 64   // K1c blocks per frame
+#endif                             // k_walk per-warp run queue
 constexpr uint16_t K1_NOKEY = 0xFFFF;
 
 #ifndef K1_MASK_L2
@@ -485,7 +491,10 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
   __shared__ uint32_t pl_s[K1_PLIST];
   __shared__ float yb_s[K1_TILE_H + 2];                     // row r <-> v = vt0 - 1 + r (R5)
   __shared__ float4 pose_s[3];                              // pose rows (R5): re-read, not held in registers
-  __shared__ uint32_t item_s, slot_s, npl_s, oor_s, base_s;
+  __shared__ unsigned long long qk[K1_WARPS][K1_Q];          // per-warp queue of finished runs: key,
+  __shared__ uint32_t qs[K1_WARPS][K1_Q];                    //   mask index,
+  __shared__ float qv[K1_WARPS][SEM ? K1_Q : 1][3];          //   normal sum
+  __shared__ uint32_t item_s, slot_s, npl_s, oor_s, base_s, rc_s, rb_s;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (SEM && threadIdx.x == 0) {   // a scratch block of this SM for the tiles' normal sums
     uint32_t sm;
@@ -519,7 +528,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
     if (threadIdx.x < 3)
       pose_s[threadIdx.x] = make_float4(F.pose[4 * threadIdx.x], F.pose[4 * threadIdx.x + 1], F.pose[4 * threadIdx.x + 2],
                                         F.pose[4 * threadIdx.x + 3]);
-    if (threadIdx.x == 0) { npl_s = 0; oor_s = 0; }
+    if (threadIdx.x == 0) { npl_s = 0; oor_s = 0; rc_s = 0; }
     __syncthreads();
 
     const uint32_t tmask = (uint32_t)wb.PC - 1;
@@ -630,8 +639,16 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
       bool kvc = vc && ((mv_c & 0xFFu) != 0xFFu ? point_key_fast(pc, rv, rinv, kc) : in_range(pc));
       float d_dn = drow(dcol, col_on, vt0 + 1);
       float d_h = drow(dhal, h_on, vt0);
-      // the lane's pending item (rows repeat voxels): while its run tails keep the same (s, key)
-      // the normals are summed in registers; the item is emitted once, when it changes
+      // the lane's pending item (rows repeat voxels)
+      uint32_t qn = 0;   // records in the warp's queue (warp-uniform)
+      auto drain = [&]() {
+        __syncwarp();
+        for (uint32_t i = lane; i < qn; i += 32)
+          emit(qs[warp][i], qk[warp][i], SEM ? qv[warp][i][0] : 0.f, SEM ? qv[warp][i][1] : 0.f,
+               SEM ? qv[warp][i][2] : 0.f);
+        __syncwarp();
+        qn = 0;
+      };
       uint64_t ck = KEY_EMPTY;
       uint32_t cs = 0xFFFFFFFFu;
       float pn0 = 0.f, pn1 = 0.f, pn2 = 0.f;
@@ -681,40 +698,29 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
             if (o < 0.f) { n0 = -n0; n1 = -n1; n2 = -n2; }
           }
         }
-        // runs of equal (m, key) along the row
-        const uint32_t khi = (uint32_t)(kc >> 32), klo = (uint32_t)kc;
-        const uint32_t mq = item ? m : 0x100u;
-        const uint32_t mp = __shfl_up_sync(0xffffffffu, mq, 1);
-        const uint32_t hp = __shfl_up_sync(0xffffffffu, khi, 1);
-        const uint32_t lp = __shfl_up_sync(0xffffffffu, klo, 1);
-        const bool same_prev = item && lane > 0 && mp == mq && hp == khi && lp == klo;
-        const unsigned items = __ballot_sync(0xffffffffu, item);
-        const unsigned heads = __ballot_sync(0xffffffffu, item && !same_prev);
-        if (items) {
-          const float q0 = n0, q1 = n1, q2 = n2;   // this pixel's own normal
-          if (SEM) {   // segmented inclusive scan over the runs
-            const int start = 31 - __clz(heads & (0xFFFFFFFFu >> (31 - lane)));
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const float a0 = __shfl_up_sync(0xffffffffu, n0, o);
-              const float a1 = __shfl_up_sync(0xffffffffu, n1, o);
-              const float a2 = __shfl_up_sync(0xffffffffu, n2, o);
-              if (lane - o >= start) { n0 += a0; n1 += a1; n2 += a2; }
-            }
+        // vertical runs: a lane's item accumulates in registers while it repeats the same (s, key)
+        // down the rows; a finished run is appended to the warp's queue (one ballot, no divergent
+        // table work per row) and the queue is drained into the CTA tables 32 records at a time
+        const bool same = item && kc == ck && m == cs;
+        const bool push = item && !same && cs != 0xFFFFFFFFu;
+        const unsigned pm = __ballot_sync(0xffffffffu, push);
+        if (pm) {
+          if (push) {
+            const uint32_t pos = qn + __popc(pm & ((1u << lane) - 1u));
+            qk[warp][pos] = ck;
+            qs[warp][pos] = cs;
+            if (SEM) { qv[warp][pos][0] = pn0; qv[warp][pos][1] = pn1; qv[warp][pos][2] = pn2; }
           }
-          const bool tail = item && !(((items & ~heads) >> 1 >> lane) & 1u);
-          if (tail) {
-            if (kc == ck && m == cs) {
-              pn0 += n0; pn1 += n1; pn2 += n2;
-            } else {
-              if (cs != 0xFFFFFFFFu) emit(cs, ck, pn0, pn1, pn2);
-              ck = kc; cs = m; pn0 = n0; pn1 = n1; pn2 = n2;
-            }
-          }
-          if (item && (mv_c >> 8)) {   // other masks of this pixel (R9), per pixel
+          qn += __popc(pm);
+          if (qn > K1_Q - 32) { drain(); }
+        }
+        if (item) {
+          if (same) { pn0 += n0; pn1 += n1; pn2 += n2; }
+          else { ck = kc; cs = m; pn0 = n0; pn1 = n1; pn2 = n2; }
+          if (mv_c >> 8) {   // other masks of this pixel (R9), per pixel
             const size_t pix = (size_t)vv * W + u;
             for (int s2 = (int)m + 1; s2 < S; ++s2)
-              if (F.masks[(size_t)s2 * H * W + pix]) emit((uint32_t)s2, kc, q0, q1, q2);
+              if (F.masks[(size_t)s2 * H * W + pix]) emit((uint32_t)s2, kc, n0, n1, n2);
           }
         }
         pu[0] = pc[0]; pu[1] = pc[1]; pu[2] = pc[2]; vu = vc;
@@ -723,24 +729,51 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
         kvc = vc && ((mv_n & 0xFFu) != 0xFFu ? point_key_fast(pc, rv, rinv, kc) : in_range(pc));
         d_dn = d_dn2; d_h = d_h2; mv_c = mv_n; ybc = ybn;
       }
-      if (cs != 0xFFFFFFFFu) emit(cs, ck, pn0, pn1, pn2);
+      {
+        const bool push = cs != 0xFFFFFFFFu;
+        const unsigned pm = __ballot_sync(0xffffffffu, push);
+        if (push) {
+          const uint32_t pos = qn + __popc(pm & ((1u << lane) - 1u));
+          qk[warp][pos] = ck;
+          qs[warp][pos] = cs;
+          if (SEM) { qv[warp][pos][0] = pn0; qv[warp][pos][1] = pn1; qv[warp][pos][2] = pn2; }
+        }
+        qn += __popc(pm);
+        drain();
+      }
     }
     if (my_oor) atomicAdd(&oor_s, my_oor);
     if (SEM) __threadfence();   // this thread's normal reductions before the reads below
     __syncthreads();
-    // ---- the tile's distinct (s, key) pairs -> frame tables, normal sums with them ----
+    // ---- the tile's distinct (s, key) items -> the frame's record list (K1c inserts them into
+    // the frame tables with many inserts in flight); a full list sends the tile to the tables here
+    uint32_t mine = 0;
+    for (int i = threadIdx.x; i < 2 * K1_KT; i += blockDim.x) mine += ptc[i] != U32_EMPTY;
+    const uint32_t roff = mine ? atomicAdd(&rc_s, mine) : 0;
+    __syncthreads();
+    if (threadIdx.x == 0) rb_s = rc_s ? atomicAdd(&wb.rcount[f], rc_s) : 0;
+    __syncthreads();
+    // past RCAP: this tile inserts its items itself and blanks its reserved records below RCAP
+    const bool direct = rb_s + rc_s > (uint32_t)wb.RCAP;
+    uint32_t r = rb_s + roff;
     for (int i = threadIdx.x; i < 2 * K1_KT; i += blockDim.x) {
       const uint32_t s = ptc[i];
       if (s == U32_EMPTY) continue;
-      const uint32_t g = global_insert(kt[i >> 1], s);
+      float4 nn = make_float4(0.f, 0.f, 0.f, 0.f);
       if (SEM) {
-        const float4 nn = __ldcg(&nscr[i]);
-        if (nn.x != 0.f || nn.y != 0.f || nn.z != 0.f) {
-          if (!(ablate & 32)) __stcg(&nscr[i], make_float4(0.f, 0.f, 0.f, 0.f));   // leave the block all-zero
-          if (g != U32_EMPTY) {
-            red_add3(&nsum[g], nn.x, nn.y, nn.z);
-          }
-        }
+        nn = __ldcg(&nscr[i]);
+        if (nn.x != 0.f || nn.y != 0.f || nn.z != 0.f) __stcg(&nscr[i], make_float4(0.f, 0.f, 0.f, 0.f));
+      }
+      if (!direct) {
+        const size_t o = (size_t)f * wb.PMAX + r++;
+        __stcg(&wb.rkey[o], kt[i >> 1]);
+        __stcg(&wb.rs[o], s);
+        if (SEM) __stcg(&wb.rn[o], nn);
+      } else {
+        if (r < (uint32_t)wb.RCAP) __stcg(&wb.rkey[(size_t)f * wb.PMAX + r], (unsigned long long)KEY_EMPTY);
+        ++r;
+        const uint32_t g = global_insert(kt[i >> 1], s);
+        if (SEM && g != U32_EMPTY && (nn.x != 0.f || nn.y != 0.f || nn.z != 0.f)) red_add3(&nsum[g], nn.x, nn.y, nn.z);
       }
     }
     __syncthreads();
@@ -762,6 +795,57 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
     __threadfence();
     atomicAnd(wb.k1slot + slot_s / K1_SLOTS_PER_SM, ~(1u << (slot_s % K1_SLOTS_PER_SM)));
   }
+}
+
+// ---- K1c ----------------------------------------------------------------------------------
+// The tiles' (s, key) records -> the frame's key / pair tables (A3): one record per thread, so
+// thousands of the dependent L2 compare-and-swap chains are in flight at once (inside K1b they
+// stalled the whole CTA at the end of every tile).  Fresh pairs count into |V_s| and the pair list.
+template <bool SEM>
+__global__ void __launch_bounds__(256) k_dedup(WinDesc wd, WinBufs wb, int* err) {
+  extern __shared__ uint32_t vsd_s[];   // [S] fresh pairs per mask
+  const int f = blockIdx.y;
+  if (f >= wd.n) return;
+  const int S = wd.f[f].S;
+  for (int i = threadIdx.x; i < S; i += blockDim.x) vsd_s[i] = 0;
+  __syncthreads();
+  const uint32_t n = min(wb.rcount[f], (uint32_t)wb.RCAP);
+  const uint32_t tmask = (uint32_t)wb.PC - 1;
+  unsigned long long* ktab = wb.ktab + (size_t)f * wb.PC;
+  uint32_t* ptab = wb.ptab + (size_t)f * wb.PC;
+  float4* nsum = wb.nsum + (size_t)f * wb.PC;
+  const int lane = threadIdx.x & 31;
+  for (uint32_t b = blockIdx.x * blockDim.x; b < n; b += gridDim.x * blockDim.x) {
+    const uint32_t i = b + threadIdx.x;
+    bool fresh = false;
+    uint32_t pslot = U32_EMPTY;
+    if (i < n) {
+      const size_t o = (size_t)f * wb.PMAX + i;
+      const unsigned long long key = __ldcs(&wb.rkey[o]);
+      const uint32_t s = __ldcs(&wb.rs[o]);
+      const uint32_t kslot = key == KEY_EMPTY ? U32_EMPTY : ktab_insert(ktab, tmask, key, err);
+      if (kslot != U32_EMPTY) pslot = ptab_insert(ptab, tmask, (s << 24) | kslot, &fresh, err);
+      if (SEM && pslot != U32_EMPTY) {
+        const float4 nn = __ldcs(&wb.rn[o]);
+        if (nn.x != 0.f || nn.y != 0.f || nn.z != 0.f) red_add3(&nsum[pslot], nn.x, nn.y, nn.z);
+      }
+      if (fresh) atomicAdd(&vsd_s[s], 1u);
+    }
+    const unsigned fm = __ballot_sync(0xffffffffu, fresh);
+    if (fm) {   // warp-aggregated append to the frame's pair list
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&wb.npairs[f], (uint32_t)__popc(fm));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (fresh) {
+        const uint32_t gi = base + __popc(fm & ((1u << lane) - 1u));
+        if (gi < (uint32_t)wb.PMAX) wb.plist[(size_t)f * wb.PMAX + gi] = pslot;
+        else raise_err(err, DERR_FRAME_PAIRS);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < S; i += blockDim.x)
+    if (vsd_s[i]) atomicAdd(&wb.vs[(size_t)f * wb.SMAX + i], vsd_s[i]);
 }
 
 __global__ void k_nsmid(int* out) {
@@ -1459,6 +1543,9 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
   if (sem) k_walk<true><<<K1B_PERSIST * nsm, K1_THREADS, (size_t)maxS * 4, st>>>(wd, wb, P, err, k1_grid, nres, k1_ablate());
   else k_walk<false><<<K1B_PERSIST * nsm, K1_THREADS, (size_t)maxS * 4, st>>>(wd, wb, P, err, k1_grid, nres, k1_ablate());
   debug_check(st, "k_walk", -1);
+  if (sem) k_dedup<true><<<dim3(K1C_BLOCKS, n), 256, (size_t)maxS * 4, st>>>(wd, wb, err);
+  else k_dedup<false><<<dim3(K1C_BLOCKS, n), 256, (size_t)maxS * 4, st>>>(wd, wb, err);
+  debug_check(st, "k_dedup", -1);
   if (ev1) cudaEventRecord(ev1, st);
   const size_t sm2 = (size_t)maxS * 6 * 4;
   const int g2 = 64;
@@ -1516,7 +1603,7 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
     k_finalize<false><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
     debug_check(st, "k_finalize", -1);
   }
-  return sem ? 14 : 8;
+  return sem ? 15 : 9;
 }
 
 }  // namespace disc

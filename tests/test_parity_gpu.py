@@ -136,6 +136,16 @@ def test_tiny_voxels_overflow_tile_tables():
     assert max(r["unique_pairs"] for r in reps) > 100000
 
 
+@pytest.mark.parametrize("rcap", [0, 3000])
+def test_record_list_overflow_direct_path(rcap, monkeypatch):
+    """K1b hands each tile's distinct (s, key) items to K1c through a per-frame record list; a
+    tile whose records would pass the list's capacity inserts them into the frame tables itself
+    (and blanks its reserved records).  A lowered capacity (test knob DISC_K1_RCAP, read at map
+    creation) mixes both paths inside one frame (3000) or sends every tile direct (0)."""
+    monkeypatch.setenv("DISC_K1_RCAP", str(rcap))
+    _stream_parity("R", 4, True, window=4)
+
+
 def test_ragged_image_scalar_path():
     """W*H not a multiple of 16: the byte-wise mask path; odd patch grid."""
     _stream_parity("N", 4, True, window=2, H=239, W=317, Hp=17, Wp=22, fx=290.0, fy=290.0, cx=158.0, cy=119.0)
