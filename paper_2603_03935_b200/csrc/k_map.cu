@@ -987,8 +987,24 @@ __device__ void apply_target_warp_general(int t, int f, const FrameDesc& F, cons
 // descriptors; member / detection ids; their attributes and T / t rows together; the embedding
 // copy — with T_root's sums and dot_pin(T, T) kept in registers (same lane / element order as
 // dot_pin_reg: lane l holds d = l, l + 32, ... ascending).
+#ifndef K7_STG_ROWS
+#define K7_STG_ROWS 8    // tracking rows per staged batch of a target warp
+#endif
+#ifndef K7_STG_WARPS
+#define K7_STG_WARPS 2   // warps per CTA with a staging area (targets go to warp w of CTA b as w * G + b)
+#endif
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+// stg: this warp's shared staging area for K7_STG_ROWS tracking rows (nullptr: register path)
 __device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc& F, const WinBufs& wb,
-                                                  const MapState& M, const FrameScratch& X, const Params& P, int sem) {
+                                                  const MapState& M, const FrameScratch& X, const Params& P, int sem,
+                                                  double* stg) {
   const int lane = threadIdx.x & 31;
   const size_t fo = (size_t)f * wb.SMAX;
   const double* trk = wb.trk + fo * P.Dt;
@@ -1035,23 +1051,51 @@ __device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc&
     if (kind == 1 && sem && i < nq4 && lane + 32 * i < D4)
       ev[i] = ((const float4*)(wb.emb + (fo + cid0) * Df))[lane + 32 * i];
   }
-  const uint32_t first = 1;   // candidate 0 is the base: T_root (= mem[0], the min id) or t_s1
+  if (stg) {
+    // the candidates' rows (candidate 0 = the base: T_root = T of mem[0], the min id, or t_s1)
+    // staged K7_STG_ROWS at a time with async copies, so a batch costs one memory round trip;
+    // summed in the pinned order from shared memory
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const int d = lane + 32 * k;
-    acc[k] = 0.0;
-    if (k < nt && d < Dt) {
-      if (kind == 1) acc[k] = trk[(size_t)cid0 * Dt + d];
-      else acc[k] = M.T[(size_t)root * Dt + d];
+    for (int k = 0; k < 16; ++k) acc[k] = 0.0;
+    const int c16 = Dt / 2;   // 16-byte chunks per row
+    for (uint32_t i0 = 0; i0 < n; i0 += K7_STG_ROWS) {
+      const uint32_t nb = min((uint32_t)K7_STG_ROWS, n - i0);
+      for (uint32_t b = 0; b < nb; ++b) {
+        const uint32_t i = i0 + b;
+        const uint32_t id = __shfl_sync(0xffffffffu, cid, i);
+        const double* row = (kind == 0 && i < mcnt) ? M.T + (size_t)id * Dt : trk + (size_t)id * Dt;
+        for (int c = lane; c < c16; c += 32) cp_async16(stg + (size_t)b * Dt + 2 * c, row + 2 * c);
+      }
+      cp_async_wait_all();
+      __syncwarp();
+      for (uint32_t b = 0; b < nb; ++b) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int d = lane + 32 * k;
+          if (k < nt && d < Dt) acc[k] = (i0 + b == 0) ? stg[d] : __dadd_rn(acc[k], stg[(size_t)b * Dt + d]);
+        }
+      }
+      __syncwarp();
     }
-  }
-  for (uint32_t i = first; i < n; ++i) {
-    const uint32_t id = __shfl_sync(0xffffffffu, cid, i);
-    const double* row = i < mcnt ? M.T + (size_t)id * Dt : trk + (size_t)id * Dt;
+  } else {
+    const uint32_t first = 1;   // candidate 0 is the base: T_root (= mem[0], the min id) or t_s1
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
       const int d = lane + 32 * k;
-      if (k < nt && d < Dt) acc[k] = __dadd_rn(acc[k], row[d]);
+      acc[k] = 0.0;
+      if (k < nt && d < Dt) {
+        if (kind == 1) acc[k] = trk[(size_t)cid0 * Dt + d];
+        else acc[k] = M.T[(size_t)root * Dt + d];
+      }
+    }
+    for (uint32_t i = first; i < n; ++i) {
+      const uint32_t id = __shfl_sync(0xffffffffu, cid, i);
+      const double* row = i < mcnt ? M.T + (size_t)id * Dt : trk + (size_t)id * Dt;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int d = lane + 32 * k;
+        if (k < nt && d < Dt) acc[k] = __dadd_rn(acc[k], row[d]);
+      }
     }
   }
   double tt = 0.0;
@@ -1152,10 +1196,21 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
     to_s[t] = X.tg_newoff[t];
   }
   __syncthreads();
+  // shared staging for the target warps' tracking rows (warps 0 .. K7_STG_WARPS-1, if it fits)
+  double* stg = nullptr;
+  {
+    uint32_t dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    const size_t base = ((size_t)wb.SMAX * 20 + 127) & ~(size_t)127;
+    const size_t per = (size_t)K7_STG_ROWS * P.Dt * 8;
+    const int w = threadIdx.x >> 5;
+    if (P.Dt > 0 && (P.Dt & 1) == 0 && w < K7_STG_WARPS && base + (size_t)K7_STG_WARPS * per <= dyn)
+      stg = (double*)(smem_raw + base + (size_t)w * per);
+  }
   for (int t = gw; t < ntgt; t += nw) {
     unsigned long long t0_, t1_;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0_));
-    apply_target_warp(t, f, F, wb, M, X, P, sem);
+    apply_target_warp(t, f, F, wb, M, X, P, sem, stg);
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1_));
     if (lane == 0) {
       atomicAdd(&g_tgprof[0], t1_ - t0_);
