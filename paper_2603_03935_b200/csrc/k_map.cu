@@ -51,6 +51,27 @@ __device__ __forceinline__ uint32_t map_insert_key(const MapState& M, uint64_t k
   return U32_EMPTY;
 }
 
+// As map_insert_key, with the home slot tried by a CAS first (no read when it is free);
+// *created = this call claimed the slot (its label cells are all EMPTY).
+__device__ __forceinline__ uint32_t map_insert_key_c(const MapState& M, uint64_t key, bool* created) {
+  uint64_t h = mix64(key) & (M.MC - 1);
+  unsigned long long k = atomicCAS(&M.slots[h].key, KEY_EMPTY, (unsigned long long)key);
+  if (k == KEY_EMPTY) { *created = true; return (uint32_t)h; }
+  if (k == key) return (uint32_t)h;
+  for (uint64_t probe = 1; probe < M.MC; ++probe) {
+    h = (h + 1) & (M.MC - 1);
+    k = __ldcg(&M.slots[h].key);
+    if (k == key) return (uint32_t)h;
+    if (k == KEY_EMPTY) {
+      k = atomicCAS(&M.slots[h].key, KEY_EMPTY, (unsigned long long)key);
+      if (k == KEY_EMPTY) { *created = true; return (uint32_t)h; }
+      if (k == key) return (uint32_t)h;
+    }
+  }
+  raise_err(M.err, DERR_MAP_KEYS);
+  return U32_EMPTY;
+}
+
 struct SlotV {   // a KeySlot read as two 16-byte L2 loads (key and inline labels together)
   unsigned long long key;
   uint32_t lab[INLINE_LABELS];
@@ -1262,8 +1283,27 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
           const uint32_t L = tp_s[t];
           uint32_t slot = slotq[q];
           if (!(slot != U32_EMPTY && (plq[q].x == L || plq[q].y == L))) {   // else: already a member
-            if (slot == U32_EMPTY) slot = map_insert_key(M, wb.pkey[fo + it]);
-            if (slot != U32_EMPTY && label_insert(M, slot, L)) { tnew = t; snew = slot; delta++; }
+            // first EMPTY cell as the lookup saw it, when it saw the whole inline list (at most one
+            // label): a CAS there, without reading the slot again; any other outcome than EMPTY or
+            // L takes the general insert
+            int e = -1;
+            if (slot == U32_EMPTY) {
+              bool created = false;
+              slot = map_insert_key_c(M, wb.pkey[fo + it], &created);
+              if (created) e = 0;
+            } else if (plq[q].y == U32_EMPTY) {
+              e = plq[q].x == U32_EMPTY ? 0 : 1;
+            }
+            if (slot != U32_EMPTY) {
+              bool ins;
+              if (e >= 0) {
+                const uint32_t old = atomicCAS(&M.slots[slot].lab[e], U32_EMPTY, L);
+                ins = old == U32_EMPTY ? true : (old == L ? false : label_insert(M, slot, L));
+              } else {
+                ins = label_insert(M, slot, L);
+              }
+              if (ins) { tnew = t; snew = slot; delta++; }
+            }
           }
         }
       } else if (it < np + nrel) {
