@@ -217,6 +217,7 @@ constexpr int K1_TILE_H = 32;
 constexpr int K1_KT = K1_PT / 2;                          // CTA key table slots (2 pair slots each)
 constexpr int K1_PLIST = 512;
 constexpr uint32_t K1_Q = 64;
+constexpr uint32_t K1C_PL = 1024;                        // k_dedup per-block pair list
 #ifndef K1C_BLOCKS
 #define K1C_BLOCKS 64   // K1c blocks per frame
 #endif                             // k_walk per-warp run queue
@@ -804,17 +805,19 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
 template <bool SEM>
 __global__ void __launch_bounds__(256) k_dedup(WinDesc wd, WinBufs wb, int* err) {
   extern __shared__ uint32_t vsd_s[];   // [S] fresh pairs per mask
+  __shared__ uint32_t pl_s[K1C_PL];     // the block's fresh pair slots
+  __shared__ uint32_t npl_s, base_s;
   const int f = blockIdx.y;
   if (f >= wd.n) return;
   const int S = wd.f[f].S;
   for (int i = threadIdx.x; i < S; i += blockDim.x) vsd_s[i] = 0;
+  if (threadIdx.x == 0) npl_s = 0;
   __syncthreads();
   const uint32_t n = min(wb.rcount[f], (uint32_t)wb.RCAP);
   const uint32_t tmask = (uint32_t)wb.PC - 1;
   unsigned long long* ktab = wb.ktab + (size_t)f * wb.PC;
   uint32_t* ptab = wb.ptab + (size_t)f * wb.PC;
   float4* nsum = wb.nsum + (size_t)f * wb.PC;
-  const int lane = threadIdx.x & 31;
   for (uint32_t b = blockIdx.x * blockDim.x; b < n; b += gridDim.x * blockDim.x) {
     const uint32_t i = b + threadIdx.x;
     bool fresh = false;
@@ -831,13 +834,12 @@ __global__ void __launch_bounds__(256) k_dedup(WinDesc wd, WinBufs wb, int* err)
       }
       if (fresh) atomicAdd(&vsd_s[s], 1u);
     }
-    const unsigned fm = __ballot_sync(0xffffffffu, fresh);
-    if (fm) {   // warp-aggregated append to the frame's pair list
-      uint32_t base = 0;
-      if (lane == 0) base = atomicAdd(&wb.npairs[f], (uint32_t)__popc(fm));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (fresh) {
-        const uint32_t gi = base + __popc(fm & ((1u << lane) - 1u));
+    if (fresh) {   // the block's list first (one global reservation per block), else the frame's
+      const uint32_t li = atomicAdd(&npl_s, 1u);
+      if (li < K1C_PL) {
+        pl_s[li] = pslot;
+      } else {
+        const uint32_t gi = atomicAdd(&wb.npairs[f], 1u);
         if (gi < (uint32_t)wb.PMAX) wb.plist[(size_t)f * wb.PMAX + gi] = pslot;
         else raise_err(err, DERR_FRAME_PAIRS);
       }
@@ -846,6 +848,14 @@ __global__ void __launch_bounds__(256) k_dedup(WinDesc wd, WinBufs wb, int* err)
   __syncthreads();
   for (int i = threadIdx.x; i < S; i += blockDim.x)
     if (vsd_s[i]) atomicAdd(&wb.vs[(size_t)f * wb.SMAX + i], vsd_s[i]);
+  const uint32_t m = min(npl_s, K1C_PL);
+  if (threadIdx.x == 0) base_s = m ? atomicAdd(&wb.npairs[f], m) : 0u;
+  __syncthreads();
+  if (base_s + m > (uint32_t)wb.PMAX) {
+    if (threadIdx.x == 0) raise_err(err, DERR_FRAME_PAIRS);
+  } else {
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) wb.plist[(size_t)f * wb.PMAX + base_s + i] = pl_s[i];
+  }
 }
 
 __global__ void k_nsmid(int* out) {

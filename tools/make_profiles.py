@@ -34,14 +34,15 @@ def summarize(rep, kernel, out, title):
 
 if __name__ == "__main__":
     # usage: make_profiles.py <report> <round tag> <frames per launch> kernel [kernel ...]
-    # K1 = k_masks + k_walk: their summed DRAM bytes per frame feed bench.py's roofline.traffic
+    # K1 = k_masks + k_walk + k_dedup: their summed DRAM bytes per frame feed bench.py's roofline.traffic
     rep, tag, fpl, kernels = sys.argv[1], sys.argv[2], int(sys.argv[3]), sys.argv[4:]
     per = {}
     for k in kernels:
         per[k] = summarize(rep, k, os.path.join(ROOT, "profiles", f"{tag}_{k}_ncu_summary.txt"), f"{tag} {k}") / fpl
         print(k, "dram bytes per frame", per[k])
     if "k_masks" in per and "k_walk" in per:
-        json.dump({"dram_bytes_per_frame": per["k_masks"] + per["k_walk"], "source": os.path.basename(rep),
+        k1 = [k for k in ("k_masks", "k_walk", "k_dedup") if k in per]
+        json.dump({"dram_bytes_per_frame": sum(per[k] for k in k1), "source": os.path.basename(rep),
                    "per_kernel": per,
-                   "note": "dram__bytes_read.sum + dram__bytes_write.sum of the K1 pass (k_masks + k_walk) per frame"},
+                   "note": "dram__bytes_read.sum + dram__bytes_write.sum of the K1 pass (%s) per frame" % " + ".join(k1)},
                   open(os.path.join(ROOT, "profiles", "k1_dram_bytes_per_frame.json"), "w"), indent=1)
