@@ -263,7 +263,9 @@ def main():
     maxS = max(fr["masks"].shape[0] for fr in frames)
     caps = dict(max_pixels=c.H * c.W, max_patches=c.Hp * c.Wp, max_masks=max(64, maxS), window=F,
                 max_memberships=1 << 23, max_instances=1 << 17,
-                max_pairs_per_frame=int(os.environ.get("BENCH_PMAX", 1 << 17)), device=local)
+                # per-frame (mask, voxel) pair capacity: the R stream's frames stay below ~32k unique
+                # pairs; 2^16 leaves a 2x margin, a frame past it fails loudly
+                max_pairs_per_frame=int(os.environ.get("BENCH_PMAX", 1 << 16)), device=local)
 
     def run(frames_, timed_steps, warm_steps, m):
         for s in range(warm_steps):
@@ -364,15 +366,18 @@ def main():
     barrier(ws)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    max_u = 0
     for s in range(1, E + 1):
-        me.integrate_frames_host(host[s * F:(s + 1) * F], report=True)
+        reps = me.integrate_frames_host(host[s * F:(s + 1) * F], report=True)
+        max_u = max([max_u] + [r["unique_pairs"] for r in reps])
     torch.cuda.synchronize()
     te = max_over_ranks(time.perf_counter() - t0, ws)
     from paper_2603_03935_b200.disc import disc_frame_report
     import ctypes
     line["e2e"] = {"value": ws * E * F / te, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
                    "d2h_bytes_per_step": F * ctypes.sizeof(disc_frame_report), "steps": E,
-                   "api": "disc_integrate_frames_host (pinned host buffers)"}
+                   "api": "disc_integrate_frames_host (pinned host buffers)", "max_unique_pairs_per_frame": int(max_u),
+                   "max_pairs_per_frame": caps["max_pairs_per_frame"]}
     del me, host
 
     # ---- CPU baseline: the oracle as it stands, 1 thread, bounded prefix of the stream ----

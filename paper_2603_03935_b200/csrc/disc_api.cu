@@ -454,6 +454,8 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(X.ctab_cnt = dalloc<uint32_t>(m, X.CC));
   chk(X.ctab_idx = dalloc<uint32_t>(m, X.TCAP));
   chk(X.ntrip = dalloc<uint32_t>(m, 1));
+  chk(X.trip_gate = dalloc<uint8_t>(m, X.TCAP));
+  chk(X.gate_done = dalloc<uint32_t>(m, 1, 0));
   chk(X.trip_s = dalloc<uint32_t>(m, X.TCAP));
   chk(X.trip_j = dalloc<uint32_t>(m, X.TCAP));
   chk(X.trip_c = dalloc<uint32_t>(m, X.TCAP));

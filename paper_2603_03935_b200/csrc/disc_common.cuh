@@ -165,6 +165,8 @@ struct FrameScratch {
   uint32_t* ctab_cnt;            // [CC]
   uint32_t* ctab_idx;            // [CC] triple index
   uint32_t* ntrip;               // [1]
+  uint8_t* trip_gate;            // [TCAP] visual gate of each triple (R15), computed by CTAs 1.. of stage 2
+  uint32_t* gate_done;           // [1] triples gated so far this frame (reset by the association)
   uint32_t* trip_s;              // [TCAP]
   uint32_t* trip_j;
   uint32_t* trip_c;

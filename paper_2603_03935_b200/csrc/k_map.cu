@@ -522,9 +522,21 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
   }
   __syncthreads();
   K6_PROBE(1);
-  // ---- pinned fp64 visual gate (R15) on the candidates, warp per candidate ----
+  // ---- pinned fp64 visual gate (R15): computed for every triple by CTAs 1.. (s2_gate) while
+  // this CTA ran the steps above; a single-CTA grid gates its candidates itself ----
   const double* trk = wb.trk + fo * P.Dt;
-  if (P.Dt > 0) {
+  if (P.Dt > 0 && gridDim.x > 1) {
+    if (tid == 0) {
+      uint32_t v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(X.gate_done) : "memory");
+      } while (v < ntr);
+    }
+    __syncthreads();
+    for (uint32_t t = tid; t < ntr; t += blockDim.x)
+      if (t_e[t] && !__ldcg(&X.trip_gate[t])) t_e[t] = 0;
+    if (tid == 0) *X.gate_done = 0;   // every gate of this frame is in
+  } else if (P.Dt > 0) {
     const uint32_t nc = n_cand;
     for (uint32_t k = warp; k < nc; k += nwarp) {
       const uint32_t t = (uint32_t)t_jl[k];
@@ -1348,6 +1360,34 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
   if (lane == 0 && delta) atomicAdd((unsigned long long*)&M.counters[2], (unsigned long long)(int64_t)delta);
 }
 
+// While CTA 0 starts the association of frame f, CTAs 1.. evaluate the pinned fp64 visual gate
+// (R15) of every (s, j) triple of the frame, warp per triple (the association keeps the geometric
+// edges whose gate passed).  Same dot_pin_reg as the single-CTA path: the same bits.
+__device__ __forceinline__ void s2_gate(int f, const WinBufs& wb, const MapState& M, const FrameScratch& X,
+                                     const Params& P) {
+  const uint32_t ntr = min(__ldcg(X.ntrip), (uint32_t)X.TCAP);
+  const size_t fo = (size_t)f * wb.SMAX;
+  const double* trk = wb.trk + fo * P.Dt;
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwc = blockDim.x >> 5;
+  const uint32_t w = (blockIdx.x - 1) * nwc + (threadIdx.x >> 5), nw = (gridDim.x - 1) * nwc;
+  uint32_t done = 0;
+  for (uint32_t t = w; t < ntr; t += nw) {
+    const uint32_t s = __ldcg(&X.trip_s[t]), j = __ldcg(&X.trip_j[t]);
+    const double TT = __ldcg(&M.TT[j]);
+    const uint8_t tok = wb.tok[fo + s];
+    const double dt = dot_pin_reg(trk + (size_t)s * P.Dt, M.T + (size_t)j * P.Dt, P.Dt);
+    double cosv = -2.0;
+    if (tok && TT > 0.0) cosv = __ddiv_rn(dt, __dsqrt_rn(TT));
+    if (lane == 0) X.trip_gate[t] = cosv >= (double)P.tau_vis ? 1 : 0;
+    ++done;
+  }
+  if (lane == 0 && done) {
+    __threadfence();
+    atomicAdd(X.gate_done, done);
+  }
+}
+
 // While CTA 0 runs the association of frame f, the other CTAs pull frame f+1's lookup working
 // set into L2: its pair records and the hash slots its keys start probing at (a hint only: the
 // slots are read again, after frame f's update, by the lookup).
@@ -1464,8 +1504,12 @@ __global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb
     cta_t(0);
     grid_sync(wb.s2bar, G * ++ep);
     probe(0);
-    if (blockIdx.x == 0) s2_assoc(f, F, wb, M, X, P, sem);
-    else if (f + 1 < wd.n) s2_prefetch(f + 1, wb, M);
+    if (blockIdx.x == 0) {
+      s2_assoc(f, F, wb, M, X, P, sem);
+    } else {
+      if (P.Dt > 0) s2_gate(f, wb, M, X, P);
+      if (f + 1 < wd.n) s2_prefetch(f + 1, wb, M);
+    }
     grid_sync(wb.s2bar, G * ++ep);
     probe(1);
     cta_t(-1);
