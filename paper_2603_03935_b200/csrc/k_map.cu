@@ -187,7 +187,7 @@ __device__ __forceinline__ void count_add(const FrameScratch& X, uint64_t code, 
 }
 
 // LK_Q pairs per lane, their hash probes in lockstep, so each lane keeps LK_Q independent
-// memory chains in flight (the lookup is a latency chain: attributes -> slot -> labels' ids ->
+// memory chains in flight (the lookup is a latency chain: attributes -> slot -> labels ->
 // count table).
 #ifndef LK_Q
 #define LK_Q 4   // unique (s, key) pairs per lane in flight (lookup)
@@ -298,7 +298,7 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
         const uint32_t L = sv[q].lab[i];
         if (L == U32_EMPTY) open = false;
         ok[i] = open && L != LAB_TOMB;
-        id[i] = ok[i] ? __ldcg(&M.id_of[L]) : 0u;
+        id[i] = ok[i] ? L : 0u;   // counted by physical label (one-to-one with the live ids here)
       }
       int nl = 0;
 #pragma unroll
@@ -317,7 +317,7 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
             const uint32_t L = __ldcg(&oc.lab[i]);
             if (L == U32_EMPTY) break;
             if (L == LAB_TOMB) continue;
-            const uint64_t c = ((uint64_t)s[q] << 32) | __ldcg(&M.id_of[L]);
+            const uint64_t c = ((uint64_t)s[q] << 32) | L;
             if (nl == 0) first[q] = c;
             else cta_add(c, 1);
             nl++;
@@ -335,12 +335,7 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
   __syncthreads();
   lk_probe(1, tp);
   for (int i = threadIdx.x; i < LK_CT; i += blockDim.x)   // flush the CTA's counts
-    if (cc[i]) {
-      count_add(X, ck[i], cc[i], M.err);
-      // warm L2 with the instance's tracking sum T_j for the association's visual gate
-      const double* Tj = M.T + (size_t)(uint32_t)ck[i] * Dt;
-      for (int d = 0; d < Dt; d += 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(Tj + d));
-    }
+    if (cc[i]) count_add(X, ck[i], cc[i], M.err);
   __syncthreads();
   lk_probe(2, tp);
 }
@@ -506,7 +501,9 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
   // triple; candidates for the visual gate are compacted ----
   for (uint32_t t = tid; t < ntr; t += blockDim.x) {
     const uint32_t h = X.ctab_idx[t];
-    const uint32_t s = X.trip_s[t], j = X.trip_j[t];
+    // the lookup counted by physical label: its live id (after the previous frame's update every
+    // label in the map is a live instance's physical label)
+    const uint32_t s = X.trip_s[t], j = __ldcg(&M.id_of[X.trip_j[t]]);
     const uint32_t c = X.ctab_cnt[h];
     const int64_t vj = M.vcount[j];
     X.ctab_cnt[h] = 0;
@@ -762,6 +759,7 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
   // ---- debug copies of the triples, edge count ----
   for (uint32_t t = tid; t < ntr; t += blockDim.x) {
     X.trip_c[t] = t_c[t];
+    X.trip_j[t] = t_j[t];   // (ids, for the debug export; the gate CTAs are done with the labels)
     X.trip_edge[t] = t_e[t];
     if (t_e[t]) atomicAdd(&edges_s, 1ull);
   }
@@ -1373,7 +1371,7 @@ __device__ __forceinline__ void s2_gate(int f, const WinBufs& wb, const MapState
   const uint32_t w = (blockIdx.x - 1) * nwc + (threadIdx.x >> 5), nw = (gridDim.x - 1) * nwc;
   uint32_t done = 0;
   for (uint32_t t = w; t < ntr; t += nw) {
-    const uint32_t s = __ldcg(&X.trip_s[t]), j = __ldcg(&X.trip_j[t]);
+    const uint32_t s = __ldcg(&X.trip_s[t]), j = __ldcg(&M.id_of[__ldcg(&X.trip_j[t])]);
     const double TT = __ldcg(&M.TT[j]);
     const uint8_t tok = wb.tok[fo + s];
     const double dt = dot_pin_reg(trk + (size_t)s * P.Dt, M.T + (size_t)j * P.Dt, P.Dt);

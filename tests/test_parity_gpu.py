@@ -146,6 +146,15 @@ def test_record_list_overflow_direct_path(rcap, monkeypatch):
     _stream_parity("R", 4, True, window=4)
 
 
+@pytest.mark.parametrize("semantic", [False, True])
+def test_single_cta_stage2(semantic, monkeypatch):
+    """A one-CTA stage-2 grid (DISC_S2_SMS=1, read at map creation): no helper CTAs, so the
+    association gates its candidates itself and nothing prefetches; same results."""
+    monkeypatch.setenv("DISC_S2_SMS", "1")
+    monkeypatch.setenv("DISC_S2_SMS_GEO", "1")
+    _stream_parity("R", 4, semantic, window=4)
+
+
 def test_ragged_image_scalar_path():
     """W*H not a multiple of 16: the byte-wise mask path; odd patch grid."""
     _stream_parity("N", 4, True, window=2, H=239, W=317, Hp=17, Wp=22, fx=290.0, fy=290.0, cx=158.0, cy=119.0)
