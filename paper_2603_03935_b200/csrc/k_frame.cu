@@ -184,7 +184,7 @@ __global__ void k_win_init(WinDesc wd, WinBufs wb) {
 }
 
 // ------------------------------------------------------------------------------------------
-// K1: the mask pass, in two kernels over the same 32-row x 128-column tiles (persistent grids
+// K1: the mask pass, in three kernels (K1a/K1b persistent grids
 // pulling (frame, tile) items from counters; CTAs that land on one of the first `reserve` SMs
 // exit at once, leaving those SMs to stage 2):
 //  K1a k_masks  streams every mask plane once (a lane owns 32 consecutive pixels of a row; the
@@ -212,7 +212,8 @@ __global__ void k_win_init(WinDesc wd, WinBufs wb) {
 constexpr int K1_THREADS = 128;
 constexpr int K1_WARPS = K1_THREADS / 32;
 constexpr int K1_TW = 32;                                 // tile columns per warp
-constexpr int K1_TILE_W = K1_WARPS * K1_TW;               // CTA tile: 32 rows x 128 columns
+// output columns per warp: 30 with normals (lanes 0 and 31 compute the neighbour columns), else 32
+__host__ __device__ constexpr int k1_cols_out(bool sem) { return sem ? K1_TW - 2 : K1_TW; }
 constexpr int K1_TILE_H = 32;
 constexpr int K1_KT = K1_PT / 2;                          // CTA key table slots (2 pair slots each)
 constexpr int K1_PLIST = 512;
@@ -516,10 +517,11 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
     const int f = it / tiles_x, tile = it % tiles_x;
     const FrameDesc& F = wd.f[f];
     const int H = F.H, W = F.W, S = F.S;
-    const int ntx = (W + K1_TILE_W - 1) / K1_TILE_W, nty = (H + K1_TILE_H - 1) / K1_TILE_H;
+    constexpr int TWO = k1_cols_out(SEM), TILE_W = K1_WARPS * TWO;
+    const int ntx = (W + TILE_W - 1) / TILE_W, nty = (H + K1_TILE_H - 1) / K1_TILE_H;
     if (tile >= ntx * nty) continue;
     const int ty = tile / ntx, tx = tile - ty * ntx;
-    const int ut0 = tx * K1_TILE_W, vt0 = ty * K1_TILE_H;
+    const int ut0 = tx * TILE_W, vt0 = ty * K1_TILE_H;
     float4* nscr = SEM ? wb.k1scr + (size_t)slot_s * K1_PT : nullptr;
     for (int i = threadIdx.x; i < S; i += blockDim.x) vs_s[i] = 0;
     for (int i = threadIdx.x; i < K1_KT; i += blockDim.x) kt[i] = KEY_EMPTY;
@@ -596,20 +598,18 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
       return -1;
     };
 
-    // ---- walk: lane = column, one row per step ----
-    const int u = ut0 + warp * K1_TW + lane;
+    // ---- walk: lane = column, one row per step; with normals (SEM) a warp's 32 lanes cover 30
+    // output columns, lanes 0 and 31 being the left / right neighbour columns (no items) ----
+    const int u = ut0 + warp * TWO + lane - (SEM ? 1 : 0);
+    const bool out_lane = !SEM || (lane >= 1 && lane <= 30);
     const int rows = min(K1_TILE_H, H - vt0);
     uint32_t my_oor = 0;
-    if (!(ablate & 2) && ut0 + warp * K1_TW < W) {
-      const bool col_on = u < W;
-      const bool edge = lane == 0 || lane == 31;
-      const int uh = lane == 0 ? u - 1 : u + 1;   // halo column of the warp's edge lanes
-      const bool h_on = SEM && edge && uh >= 0 && uh < W;
+    if (!(ablate & 2) && ut0 + warp * TWO < W) {
+      const bool col_on = u >= 0 && u < W;
       const float xa = col_on ? __fdiv_rn(__fsub_rn((float)u, F.cx), F.fx) : 0.f;   // R5
-      const float xh = h_on ? __fdiv_rn(__fsub_rn((float)uh, F.cx), F.fx) : 0.f;
       const float* dcol = F.depth + (col_on ? u : 0);
-      const float* dhal = F.depth + (h_on ? uh : 0);
       const uint16_t* mcol = wb.m0map + (size_t)f * wb.MPIX + (col_on ? u : 0);
+      const bool m_on = col_on && out_lane;   // first-mask entries of the output columns only
       auto wpt = [&](float d, float x, float yb, float p[3]) -> bool {
         if (!depth_valid(d, P)) return false;
         const float xc = __fmul_rn(x, d), yc = __fmul_rn(yb, d), zc = d;
@@ -632,14 +632,12 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
         return point_key_fast(p, rv, rinv, k);
       };
       float pu[3] = {0.f, 0.f, 0.f}, pc[3] = {0.f, 0.f, 0.f};
-      float ybc = yb_s[1];   // the centre row's yb (halo pixels)
       bool vu = SEM ? wpt(drow(dcol, col_on, vt0 - 1), xa, yb_s[0], pu) : false;
-      bool vc = wpt(drow(dcol, col_on, vt0), xa, ybc, pc);
-      uint32_t mv_c = col_on ? mcol[vt0 * W] : 0xFFu;   // m0 | overlap << 8
+      bool vc = wpt(drow(dcol, col_on, vt0), xa, yb_s[1], pc);
+      uint32_t mv_c = m_on ? mcol[vt0 * W] : 0xFFu;   // m0 | overlap << 8
       uint64_t kc = KEY_EMPTY;
       bool kvc = vc && ((mv_c & 0xFFu) != 0xFFu ? point_key_fast(pc, rv, rinv, kc) : in_range(pc));
       float d_dn = drow(dcol, col_on, vt0 + 1);
-      float d_h = drow(dhal, h_on, vt0);
       // the lane's pending item (rows repeat voxels)
       uint32_t qn = 0;   // records in the warp's queue (warp-uniform)
       auto drain = [&]() {
@@ -653,31 +651,26 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
       uint64_t ck = KEY_EMPTY;
       uint32_t cs = 0xFFFFFFFFu;
       float pn0 = 0.f, pn1 = 0.f, pn2 = 0.f;
-      // running row pointers (no per-row index arithmetic): depth two rows ahead, halo depth and
-      // first-mask entry one row ahead; a pointer past the image is never dereferenced
+      // running row pointers (no per-row index arithmetic): depth two rows ahead, first-mask
+      // entry one row ahead; a pointer past the image is never dereferenced
       const float* dp = dcol + (int64_t)(vt0 + 2) * W;
-      const float* hp = dhal + (int64_t)(vt0 + 1) * W;
       const uint16_t* mp = mcol + (int64_t)(vt0 + 1) * W;
       const int lim2 = col_on ? H - vt0 - 2 : -1;   // rr < lim2: row vv + 2 exists (and the column)
-      const int limh = h_on ? H - vt0 - 1 : -1;
       for (int rr = 0; rr < rows; ++rr) {
         const int vv = vt0 + rr;
         // the next row's loads go out before this row's arithmetic
         const float d_dn2 = rr < lim2 ? __ldcs(dp) : 0.f;   // streaming (evict-first) reads
-        const float d_h2 = rr < limh ? __ldcs(hp) : 0.f;
         const bool more = rr + 1 < rows;
-        const uint32_t mv_n = (col_on && more) ? (uint32_t)__ldcs(mp) : 0xFFu;
-        dp += W; hp += W; mp += W;
+        const uint32_t mv_n = (m_on && more) ? (uint32_t)__ldcs(mp) : 0xFFu;
+        dp += W; mp += W;
         const float ybn = yb_s[rr + 2];
         float pd[3] = {0.f, 0.f, 0.f};
         const bool vd = wpt(d_dn, xa, ybn, pd);
         const uint32_t m = mv_c & 0xFFu;
-        if (vc && !kvc) my_oor++;
-        const bool item = m != 0xFFu && kvc;
+        if (out_lane && vc && !kvc) my_oor++;
+        const bool item = m != 0xFFu && kvc;   // (m is 0xFF in the neighbour lanes)
         float n0 = 0.f, n1 = 0.f, n2 = 0.f;
-        if (SEM && !(ablate & 8)) {
-          float hx[3] = {0.f, 0.f, 0.f};
-          const bool vh = h_on && wpt(d_h, xh, ybc, hx);
+        if (SEM) {
           float pl[3], pr[3];
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
@@ -685,9 +678,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
             pr[a] = __shfl_down_sync(0xffffffffu, pc[a], 1);
           }
           const unsigned vb = __ballot_sync(0xffffffffu, vc);
-          bool vl = (vb >> ((lane - 1) & 31)) & 1u, vr = (vb >> ((lane + 1) & 31)) & 1u;
-          if (lane == 0) { pl[0] = hx[0]; pl[1] = hx[1]; pl[2] = hx[2]; vl = vh; }
-          if (lane == 31) { pr[0] = hx[0]; pr[1] = hx[1]; pr[2] = hx[2]; vr = vh; }
+          const bool vl = (vb >> ((lane - 1) & 31)) & 1u, vr = (vb >> ((lane + 1) & 31)) & 1u;
           // R21 with 4 valid neighbours (off-image neighbours read depth 0 = invalid)
           if (item && vl && vr && vu && vd) {
             const float a0 = pr[0] - pl[0], a1 = pr[1] - pl[1], a2 = pr[2] - pl[2];
@@ -728,7 +719,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
         pc[0] = pd[0]; pc[1] = pd[1]; pc[2] = pd[2]; vc = vd;
         kc = KEY_EMPTY;
         kvc = vc && ((mv_n & 0xFFu) != 0xFFu ? point_key_fast(pc, rv, rinv, kc) : in_range(pc));
-        d_dn = d_dn2; d_h = d_h2; mv_c = mv_n; ybc = ybn;
+        d_dn = d_dn2; mv_c = mv_n;
       }
       {
         const bool push = cs != 0xFFFFFFFFu;
@@ -1520,8 +1511,9 @@ static int k1_ablate() {
   return v;
 }
 
-int k1_tiles(int H, int W) {
-  return ((W + K1_TILE_W - 1) / K1_TILE_W) * ((H + K1_TILE_H - 1) / K1_TILE_H);
+int k1_tiles(int H, int W, bool sem) {
+  const int tw = K1_WARPS * k1_cols_out(sem);
+  return ((W + tw - 1) / tw) * ((H + K1_TILE_H - 1) / K1_TILE_H);
 }
 
 int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* err, bool sem, int maxS,
@@ -1530,7 +1522,7 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
   const int n = wd.n;
   (void)rows_cap; (void)maxW;
   int k1_grid = 1;
-  for (int i = 0; i < n; ++i) k1_grid = std::max(k1_grid, k1_tiles(wd.f[i].H, wd.f[i].W));
+  for (int i = 0; i < n; ++i) k1_grid = std::max(k1_grid, k1_tiles(wd.f[i].H, wd.f[i].W, sem));
   (void)maxHp; (void)maxWp;
   k_win_init<<<dim3(8, n), 256, 0, st>>>(wd, wb);
   debug_check(st, "k_win_init", -1);
