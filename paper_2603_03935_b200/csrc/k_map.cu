@@ -1431,7 +1431,7 @@ void k6_prof_dump() {
   if (getenv("DISC_S2PROF")) {
     unsigned long long g[8];
     cudaMemcpyFromSymbol(g, g_s2prof, sizeof(g));
-    fprintf(stderr, "s2 phase ns: lookup %llu assoc %llu apply %llu (64 barriers x launches: %llu)\n", g[0], g[1], g[2], g[7]);
+    fprintf(stderr, "s2 phase ns: lookup %llu assoc %llu apply %llu kernel span %llu (64 barriers x launches: %llu)\n", g[0], g[1], g[2], g[6], g[7]);
     unsigned long long c[8];
     cudaMemcpyFromSymbol(c, g_s2cta, sizeof(c));
     fprintf(stderr, "s2 per-CTA work: lookup sum %llu max %llu, apply sum %llu max %llu\n", c[0], c[1], c[4], c[5]);
@@ -1480,6 +1480,8 @@ __global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb
     }
   };
   probe(-1);
+  unsigned long long t_k0 = 0;
+  if (prof && blockIdx.x == 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_k0));
   if (prof == 2) {   // DISC_S2PROF=2: cost of 64 empty grid barriers (profiling aid)
     for (int i = 0; i < 64; ++i) grid_sync(wb.s2bar, G * ++ep);
     probe(7);
@@ -1517,6 +1519,11 @@ __global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb
     probe(2);
   }
   if (wd.n > 0) s2_finalize(wd.n - 1, M, X);
+  if (prof && blockIdx.x == 0 && threadIdx.x == 0) {   // the kernel's own span (CTA 0)
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    atomicAdd(&g_s2prof[6], t_ - t_k0);
+  }
 }
 
 int launch_stage2(const WinDesc& wd, const WinBufs& wb, const MapState& M, const FrameScratch& X, const Params& P,
