@@ -155,6 +155,12 @@ def test_single_cta_stage2(semantic, monkeypatch):
     _stream_parity("R", 4, semantic, window=4)
 
 
+def test_odd_tracking_dim_register_path():
+    """Odd Dt: tracking rows are not 16-byte multiples, so the K7 target warps sum them from
+    registers instead of the async-copy staging; the fp64 sums stay bit-exact."""
+    _stream_parity("N", 6, True, window=3, Dt=37)
+
+
 def test_ragged_image_scalar_path():
     """W*H not a multiple of 16: the byte-wise mask path; odd patch grid."""
     _stream_parity("N", 4, True, window=2, H=239, W=317, Hp=17, Wp=22, fx=290.0, fy=290.0, cx=158.0, cy=119.0)
