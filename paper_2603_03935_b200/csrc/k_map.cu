@@ -1041,7 +1041,7 @@ __device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc&
   const double* trk = wb.trk + fo * P.Dt;
   const int kind = X.tg_kind[t];
   const uint32_t root = X.tgt_root[t], L = X.tgt_phys[t];
-  const uint32_t moff = X.tg_moff[t], mcnt = X.tg_mcnt[t], doff = X.tg_doff[t], dcnt = X.tg_dcnt[t];
+  const uint32_t mcnt = X.tg_mcnt[t], dcnt = X.tg_dcnt[t];
   const int64_t vbase = X.tg_vbase[t];
   const int Dt = P.Dt, Df = P.Df;
   if (mcnt + dcnt > 32 || Dt > 512) {

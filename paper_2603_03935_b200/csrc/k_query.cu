@@ -3,6 +3,7 @@
 #include <vector>
 
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include "disc_common.cuh"
 #include "disc_launch.h"
@@ -59,7 +60,7 @@ static int32_t select_ids(const MapState& M, int64_t n, int want_embed, int32_t*
   if (!flags) return -1;
   k_alive_flags<<<256, 256, 0, st>>>(M, n, flags, want_embed);
   size_t tb = 0;
-  cub::CountingInputIterator<int32_t> it(0);
+  thrust::counting_iterator<int32_t> it(0);
   cub::DeviceSelect::Flagged(nullptr, tb, it, flags, ids, nsel, (int)n, st);
   void* tmp = sc.take<char>(tb);
   if (!tmp) return -1;
