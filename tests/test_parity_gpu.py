@@ -89,18 +89,20 @@ def test_tiny_config_every_frame(semantic):
         compare_state(gm, om, semantic, c.Dt)
 
 
-def _stream_parity(name, nframes, semantic, window, every=1, **over):
+def _stream_parity(name, nframes, semantic, window, every=1, caps=None, reports=True, **over):
     dev = _dev()
     g = Generator(name, device=dev, **over)
     c = g.cfg
     kw = disc_config_kwargs(c)
-    gm = _disc_map(kw, c.H, c.W, c.Hp, c.Wp, window=window, S=max(64, c.n_masks))
+    gm = _disc_map(kw, c.H, c.W, c.Hp, c.Wp, window=window, S=max(64, c.n_masks), **(caps or {}))
     om = OracleMap(**kw)
     frames = [g.frame(f, with_feats=semantic) for f in range(nframes)]
     # windowed GPU integration (the launch configuration bench.py times)
+    # (without reports no call waits for its window: window w+1's stage 1 overlaps w's stage 2)
     reps_g = []
     for w0 in range(0, nframes, window):
-        reps_g += gm.integrate_frames(frames[w0:w0 + window], report=True)
+        r = gm.integrate_frames(frames[w0:w0 + window], report=reports)
+        reps_g += r if reports else []
     reps_o = [om.integrate(frame_to_numpy(fr)) for fr in frames]
     for rg, ro in zip(reps_g, reps_o):
         compare_reports(rg, ro)
@@ -113,6 +115,17 @@ def _stream_parity(name, nframes, semantic, window, every=1, **over):
 def test_replica_prefix(semantic):
     reps = _stream_parity("R", 8, semantic, window=4)
     assert sum(r["unique_pairs"] for r in reps) > 10000
+
+
+@pytest.mark.parametrize("semantic", [False, True])
+@pytest.mark.parametrize("reports", [True, False])
+def test_replica_bench_launch_configuration(semantic, reports):
+    """The bench's launch configuration on its workload: Replica-shaped frames, 16-frame windows,
+    bench.py's capacities (pairs 2^16 per frame, 2^23 memberships, 2^17 instances), three windows
+    -- per-frame reports, the last frame's debug export and the whole map compared with the oracle;
+    without reports the windows run as in bench.py (stage 1 of window w+1 beside stage 2 of w)."""
+    _stream_parity("R", 48, semantic, window=16, reports=reports,
+                   caps=dict(max_pairs=1 << 16, max_memberships=1 << 23, max_instances=1 << 17))
 
 
 @pytest.mark.parametrize("semantic", [False, True])
