@@ -208,16 +208,15 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
   const uint32_t np = min(wb.npairs[f], (uint32_t)wb.PMAX);
   const size_t fo = (size_t)f * wb.PMAX;
   const int lane = threadIdx.x & 31;
-  // the association's shared memory is free during this phase: the frame's statuses and a CTA
-  // table of (s, j) counts (flushed to the frame's count table at the end)
+  // the association's shared memory is free during this phase: a CTA table of (s, j) counts
+  // (flushed to the frame's count table at the end)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned long long* ck = (unsigned long long*)smem_raw;                 // [LK_CT] codes
   uint32_t* cc = (uint32_t*)(ck + LK_CT);                                 // [LK_CT] counts
-  int32_t* status = (int32_t*)(cc + LK_CT);                               // [SMAX]
+  const int32_t* stf = wb.status + (size_t)f * wb.SMAX;                   // the frame's statuses
   unsigned long long tp = 0;
   lk_probe(-1, tp);
   for (int i = threadIdx.x; i < LK_CT; i += blockDim.x) { ck[i] = KEY_EMPTY; cc[i] = 0; }
-  for (int i = threadIdx.x; i < wb.SMAX; i += blockDim.x) status[i] = wb.status[(size_t)f * wb.SMAX + i];
   __syncthreads();
   lk_probe(0, tp);
   auto cta_add = [&](uint64_t code, uint32_t add) {   // CTA table, else straight to the frame's
@@ -255,7 +254,7 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
     }
 #pragma unroll
     for (int q = 0; q < LK_Q; ++q) {
-      act[q] = idx[q] < np && status[s[q]] == 0;
+      act[q] = idx[q] < np && stf[s[q]] == 0;   // (a few L1 lines: no staging round trip)
       h[q] = (uint32_t)mix64(key[q]) & hmask;
     }
     SlotV sv[LK_Q];
