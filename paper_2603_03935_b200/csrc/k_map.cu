@@ -1072,15 +1072,12 @@ __device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc&
   double acc[16];
   const int nt = (Dt + 31) / 32;
   const uint32_t cid0 = __shfl_sync(0xffffffffu, cid, 0);   // (outside the lane-dependent branches)
-  // new instance: its embedding row is read now, in flight with the tracking row below
-  const int D4 = Df / 4, nq4 = (D4 + 31) / 32;
-  float4 ev[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    ev[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (kind == 1 && sem && i < nq4 && lane + 32 * i < D4)
-      ev[i] = ((const float4*)(wb.emb + (fo + cid0) * Df))[lane + 32 * i];
-  }
+  // new instance: its embedding row goes to shared memory with the tracking rows' first batch
+  // (staged path; no registers held across the sums), else it is copied at the end
+  const int D4 = Df / 4;
+  float4* stg_e = stg ? (float4*)(stg + (size_t)K7_STG_ROWS * Dt) : nullptr;
+  if (stg && kind == 1 && sem)
+    for (int d4 = lane; d4 < D4; d4 += 32) cp_async16(stg_e + d4, (const float4*)(wb.emb + (fo + cid0) * Df) + d4);
   if (stg) {
     // the candidates' rows (candidate 0 = the base: T_root = T of mem[0], the min id, or t_s1)
     // staged K7_STG_ROWS at a time with async copies, so a batch costs one memory round trip;
@@ -1168,9 +1165,8 @@ __device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc&
                                                        : (const float4*)(wb.emb + (fo + sid) * Df));
   float4* ed = (float4*)(M.E + (size_t)root * Df);
   if (kind == 1) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (i < nq4 && lane + 32 * i < D4) ed[lane + 32 * i] = has_e ? ev[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4* src = stg_e ? stg_e : (const float4*)(wb.emb + (fo + cid0) * Df);
+    for (int d4 = lane; d4 < D4; d4 += 32) ed[d4] = has_e ? src[d4] : make_float4(0.f, 0.f, 0.f, 0.f);
   } else if (has_e) {
     for (int d4 = lane; d4 < Df / 4; d4 += 32) ed[d4] = es[d4];
   }
@@ -1232,7 +1228,7 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
     uint32_t dyn;
     asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
     const size_t base = ((size_t)wb.SMAX * 20 + 127) & ~(size_t)127;
-    const size_t per = (size_t)K7_STG_ROWS * P.Dt * 8;
+    const size_t per = ((size_t)K7_STG_ROWS * P.Dt * 8 + (size_t)P.Df * 4 + 15) & ~(size_t)15;   // rows + e
     const int w = threadIdx.x >> 5;
     if (P.Dt > 0 && (P.Dt & 1) == 0 && w < K7_STG_WARPS && base + (size_t)K7_STG_WARPS * per <= dyn)
       stg = (double*)(smem_raw + base + (size_t)w * per);
