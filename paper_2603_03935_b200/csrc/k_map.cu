@@ -190,7 +190,7 @@ __device__ __forceinline__ void count_add(const FrameScratch& X, uint64_t code, 
 // memory chains in flight (the lookup is a latency chain: attributes -> slot -> labels ->
 // count table).
 #ifndef LK_Q
-#define LK_Q 4   // unique (s, key) pairs per lane in flight (lookup)
+#define LK_Q 3   // unique (s, key) pairs per lane in flight (lookup; 4 held more registers than it hid latency)
 #endif
 __device__ unsigned long long g_lkprof[4];   // DISC_S2PROF: lookup sub-phases on CTA 0 (init, loop, flush)
 __device__ __forceinline__ void lk_probe(int i, unsigned long long& tp) {
