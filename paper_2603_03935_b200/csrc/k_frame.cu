@@ -1605,7 +1605,7 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
     k_finalize<false><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
     debug_check(st, "k_finalize", -1);
   }
-  return sem ? 15 : 9;
+  return sem ? 14 : 9;   // the launches above on s1, counted exactly (bench.py reports them)
 }
 
 }  // namespace disc
