@@ -263,9 +263,12 @@ def main():
     maxS = max(fr["masks"].shape[0] for fr in frames)
     caps = dict(max_pixels=c.H * c.W, max_patches=c.Hp * c.Wp, max_masks=max(64, maxS), window=F,
                 max_memberships=1 << 23, max_instances=1 << 17,
-                # per-frame (mask, voxel) pair capacity: the R stream's frames stay below ~32k unique
-                # pairs; 2^16 leaves a 2x margin, a frame past it fails loudly
-                max_pairs_per_frame=int(os.environ.get("BENCH_PMAX", 1 << 16)), device=local)
+                # per-frame (mask, voxel) pair capacity: R and N frames stay below ~32k unique pairs
+                # (e2e records the maximum seen), so 2^16 leaves a 2x margin; H's far
+                # views reach ~1 pair per pixel (2 cm voxels, 480x640): 2^19.  A frame past it fails
+                # loudly (CAPACITY)
+                max_pairs_per_frame=int(os.environ.get("BENCH_PMAX", 1 << 19 if args.config == "H" else 1 << 16)),
+                device=local)
 
     def run(frames_, timed_steps, warm_steps, m):
         for s in range(warm_steps):

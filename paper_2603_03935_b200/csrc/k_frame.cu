@@ -217,6 +217,7 @@ __host__ __device__ constexpr int k1_cols_out(bool sem) { return sem ? K1_TW - 2
 constexpr int K1_TILE_H = 32;
 constexpr int K1_KT = K1_PT / 2;                          // CTA key table slots (2 pair slots each)
 constexpr int K1_PLIST = 512;
+constexpr int K1_KT_PROBES = 16;                           // CTA key-table probe bound
 constexpr uint32_t K1_Q = 64;
 constexpr uint32_t K1C_PL = 1024;                        // k_dedup per-block pair list
 #ifndef K1C_BLOCKS
@@ -538,9 +539,11 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
     unsigned long long* ktab = wb.ktab + (size_t)f * wb.PC;
     uint32_t* ptab = wb.ptab + (size_t)f * wb.PC;
     float4* nsum = wb.nsum + (size_t)f * wb.PC;
-    auto kt_insert = [&](uint64_t key) -> uint16_t {   // CTA key table -> local key index
+    // CTA key table -> local key index; at most K1_KT_PROBES probes, so a table that far views
+    // (up to a voxel per pixel) fill up fails fast and the item takes the record list
+    auto kt_insert = [&](uint64_t key) -> uint16_t {
       uint32_t h = (uint32_t)mix64(key) & (K1_KT - 1);
-      for (int probe = 0; probe < K1_KT; ++probe) {
+      for (int probe = 0; probe < K1_KT_PROBES; ++probe) {
         const unsigned long long cur = kt[h];
         if (cur == key) return (uint16_t)h;
         if (cur == KEY_EMPTY) {
@@ -571,6 +574,26 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
     };
     // one (s, key) item: CTA key table -> local index li; the pair is slot 2 li or 2 li + 1 (a
     // voxel rarely meets more than two masks in one tile); otherwise straight to the frame tables
+    // one (s, key) item into the CTA tables; false when they are full (the caller spills it)
+    auto emit_cta = [&](uint32_t s, uint64_t key, float n0, float n1, float n2) -> bool {
+      const uint16_t li = kt_insert(key);
+      int ps = -1;
+      if (li != K1_NOKEY) {
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          uint32_t* c = &ptc[2 * li + jj];
+          uint32_t cur = *c;
+          if (cur == U32_EMPTY) {
+            cur = atomicCAS(c, U32_EMPTY, s);
+            if (cur == U32_EMPTY) cur = s;
+          }
+          if (cur == s) { ps = 2 * li + jj; break; }
+        }
+      }
+      if (ps < 0) return false;
+      if (SEM && (n0 != 0.f || n1 != 0.f || n2 != 0.f)) red_add3(&nscr[ps], n0, n1, n2);
+      return true;
+    };
     auto emit = [&](uint32_t s, uint64_t key, float n0, float n1, float n2) -> int {
       const uint16_t li = kt_insert(key);
       int ps = -1;
@@ -640,11 +663,43 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
       float d_dn = drow(dcol, col_on, vt0 + 1);
       // the lane's pending item (rows repeat voxels)
       uint32_t qn = 0;   // records in the warp's queue (warp-uniform)
+      // the queue into the CTA tables; items they cannot hold (far views: up to a voxel per pixel)
+      // go to the frame's record list for K1c (one reservation per warp), and only past its
+      // capacity into the frame tables from here
       auto drain = [&]() {
         __syncwarp();
-        for (uint32_t i = lane; i < qn; i += 32)
-          emit(qs[warp][i], qk[warp][i], SEM ? qv[warp][i][0] : 0.f, SEM ? qv[warp][i][1] : 0.f,
-               SEM ? qv[warp][i][2] : 0.f);
+        for (uint32_t i0 = 0; i0 < qn; i0 += 32) {
+          const uint32_t i = i0 + lane;
+          uint32_t s = 0;
+          unsigned long long key = 0;
+          float a = 0.f, b = 0.f, c = 0.f;
+          bool spill = false;
+          if (i < qn) {
+            s = qs[warp][i];
+            key = qk[warp][i];
+            if (SEM) { a = qv[warp][i][0]; b = qv[warp][i][1]; c = qv[warp][i][2]; }
+            spill = !emit_cta(s, key, a, b, c);
+          }
+          const unsigned sm = __ballot_sync(0xffffffffu, spill);
+          if (sm) {
+            const int ld = __ffs(sm) - 1;
+            uint32_t rb = 0;
+            if (lane == ld) rb = atomicAdd(&wb.rcount[f], (uint32_t)__popc(sm));
+            rb = __shfl_sync(0xffffffffu, rb, ld);
+            if (spill) {
+              const uint32_t r = rb + __popc(sm & ((1u << lane) - 1u));
+              if (r < (uint32_t)wb.RCAP) {
+                const size_t o = (size_t)f * wb.PMAX + r;
+                __stcg(&wb.rkey[o], key);
+                __stcg(&wb.rs[o], s);
+                if (SEM) __stcg(&wb.rn[o], make_float4(a, b, c, 0.f));
+              } else {
+                const uint32_t g = global_insert(key, s);
+                if (SEM && g != U32_EMPTY && (a != 0.f || b != 0.f || c != 0.f)) red_add3(&nsum[g], a, b, c);
+              }
+            }
+          }
+        }
         __syncwarp();
         qn = 0;
       };
