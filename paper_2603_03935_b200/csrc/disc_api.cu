@@ -40,6 +40,13 @@ struct disc_map {
   int* d_err = nullptr;
   int* h_err = nullptr;                 // pinned
   disc_frame_report* h_rep = nullptr;   // pinned [MAXWIN]
+  // adaptive stage-2 reserve: each window's pair counts come back (pinned, no sync); a finished
+  // copy sets the running pairs-per-frame level the next windows' SM split follows
+  uint32_t* h_np = nullptr;             // pinned [2][MAXWIN]
+  cudaEvent_t ev_np[2] = {nullptr, nullptr};
+  int np_pending[2] = {0, 0};
+  double np_avg = -1.0;
+  bool adapt = true;
   std::vector<void*> allocs;
   disc_status sticky = DISC_OK;
   std::string err;
@@ -351,6 +358,8 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
     const char* eg = std::getenv("DISC_S2_SMS_GEO");
     m->nres_geo = eg ? std::atoi(eg) : 40;
     m->nres_geo = std::max(0, std::min(m->nres_geo, m->nsm / 2));
+    const char* ea = std::getenv("DISC_S2_ADAPT");   // 0: fixed split (tuning)
+    m->adapt = !(ea && std::atoi(ea) == 0);
   }
   Params& P = m->P;
   P.r = cfg->voxel_size; P.tau_geo = cfg->tau_geo; P.tau_vis = cfg->tau_vis;
@@ -495,8 +504,10 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
     if (cudaStreamCreateWithPriority(&m->s1, cudaStreamNonBlocking, prio_lo) != cudaSuccess) ok = false;
     if (cudaStreamCreateWithPriority(&m->s2, cudaStreamNonBlocking, prio_hi) != cudaSuccess) ok = false;
   }
-  for (cudaEvent_t* e : {&m->ev_in, &m->ev_done, &m->ev_s1done, &m->ev_s1[0], &m->ev_s1[1], &m->ev_s2[0], &m->ev_s2[1]})
+  for (cudaEvent_t* e : {&m->ev_in, &m->ev_done, &m->ev_s1done, &m->ev_s1[0], &m->ev_s1[1], &m->ev_s2[0], &m->ev_s2[1],
+                         &m->ev_np[0], &m->ev_np[1]})
     if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) ok = false;
+  if (cudaMallocHost(&m->h_np, sizeof(uint32_t) * 2 * MAXWIN) != cudaSuccess) ok = false;
   if (cudaMallocHost(&m->h_err, sizeof(int)) != cudaSuccess) ok = false;
   if (cudaMallocHost(&m->h_rep, sizeof(disc_frame_report) * MAXWIN) != cudaSuccess) ok = false;
   if (ok && k6_smem_bytes(SM, X.TCAP) > 227 * 1024) ok = false;
@@ -518,15 +529,40 @@ void disc_map_destroy(disc_map* m) {
   for (void* p : m->allocs) cudaFree(p);
   if (m->h_err) cudaFreeHost(m->h_err);
   if (m->h_rep) cudaFreeHost(m->h_rep);
+  if (m->h_np) cudaFreeHost(m->h_np);
   if (m->stage) cudaFree(m->stage);
   if (m->scratch) cudaFree(m->scratch);
   for (auto& p : m->ev_pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   for (auto e : m->ev_pool) cudaEventDestroy(e);
-  for (cudaEvent_t e : {m->ev_in, m->ev_done, m->ev_s1done, m->ev_s1[0], m->ev_s1[1], m->ev_s2[0], m->ev_s2[1]})
+  for (cudaEvent_t e : {m->ev_in, m->ev_done, m->ev_s1done, m->ev_s1[0], m->ev_s1[1], m->ev_s2[0], m->ev_s2[1],
+                        m->ev_np[0], m->ev_np[1]})
     if (e) cudaEventDestroy(e);
   if (m->s1) cudaStreamDestroy(m->s1);
   if (m->s2) cudaStreamDestroy(m->s2);
   delete m;
+}
+
+// SMs for stage 2 in the next window: the base split plus, when the stream's frames carry many
+// (mask, voxel) pairs (far views, H-shaped maps), more SMs for the lookup / apply work that grows
+// with them (measured: H-shaped 108 k pairs per frame, 20 -> 64 SMs: +42 % frames/s; R-shaped 20 k: no
+// gain).  The level comes from pair counts already copied back, never from a wait.
+static int stage2_reserve(disc_map* m, bool sem) {
+  for (int bb = 0; bb < 2; ++bb) {
+    if (!m->np_pending[bb]) continue;
+    const cudaError_t q = cudaEventQuery(m->ev_np[bb]);
+    if (q == cudaSuccess) {
+      uint64_t sum = 0;
+      for (int i = 0; i < m->np_pending[bb]; ++i) sum += m->h_np[(size_t)bb * MAXWIN + i];
+      m->np_avg = (double)sum / m->np_pending[bb];
+      m->np_pending[bb] = 0;
+    } else if (q == cudaErrorNotReady) {
+      (void)cudaGetLastError();   // (not an error)
+    }
+  }
+  const int base = sem ? m->nres : m->nres_geo;
+  int extra = 0;
+  if (m->adapt && base > 0 && m->np_avg > 24000.0) extra = (int)std::min(44.0, (m->np_avg - 24000.0) / 2000.0);
+  return std::min(base + extra, m->nsm / 2);
 }
 
 static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t n, void* stream,
@@ -608,13 +644,17 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
       cudaEventRecord(t0, s1);
     }
     tl_mark(s1, "s1_begin", -1);
-    m->stats.launches += launch_stage1(wd, Wbuf, m->P, m->d_err, sem, maxS, maxHp, maxW, maxWp, maxP, rows, m->nsm, sem ? m->nres : m->nres_geo, s1, e0, e1);
+    const int nres_w = stage2_reserve(m, sem);
+    m->stats.launches += launch_stage1(wd, Wbuf, m->P, m->d_err, sem, maxS, maxHp, maxW, maxWp, maxP, rows, m->nsm, nres_w, s1, e0, e1);
+    cudaMemcpyAsync(m->h_np + (size_t)b * MAXWIN, Wbuf.npairs, sizeof(uint32_t) * nw, cudaMemcpyDeviceToHost, s1);
+    cudaEventRecord(m->ev_np[b], s1);
+    m->np_pending[b] = nw;
     if (m->timing) cudaEventRecord(t1, s1);
     cudaEventRecord(m->ev_s1[b], s1);
     cudaStreamWaitEvent(s2, m->ev_s1[b], 0);
     if (m->timing) cudaEventRecord(t1b, s2);
     tl_mark(s2, "s2_begin", -1);
-    m->stats.launches += launch_stage2(wd, Wbuf, m->M, m->X, m->P, sem, m->nsm, sem ? m->nres : m->nres_geo, s2);
+    m->stats.launches += launch_stage2(wd, Wbuf, m->M, m->X, m->P, sem, m->nsm, nres_w, s2);
     if (m->timing) {
       cudaEventRecord(t2, s2);
       m->ev_pending.push_back({e0, e1, 0});
