@@ -70,7 +70,12 @@ typedef struct {
   int32_t max_masks;       /* S per frame, <= 255                                            */
   int32_t max_pixels;      /* H*W per frame                                                  */
   int32_t max_patches;     /* Hp*Wp per frame                                                */
-  int32_t max_pairs_per_frame; /* unique (mask, voxel) pairs per frame, <= 2^22              */
+  int32_t max_pairs_per_frame; /* unique (mask, voxel) pairs per frame (all masks, dropped  */
+                               /* ones included), <= 2^22; a frame past it fails with the   */
+                               /* sticky DISC_ERR_CAPACITY.  Also sizes the frame hash      */
+                               /* tables (2x, power of two) and the per-frame item list     */
+                               /* between the mask pass and the dedup (an overflowing list  */
+                               /* falls back to direct inserts, never to an error)          */
   int32_t window;          /* frames per stage-1 batch in disc_integrate_frames, 1..32       */
   int32_t device;          /* CUDA ordinal                                                   */
   /* sharding (reserved; must be 1 / 0 / NULL in this version) */
