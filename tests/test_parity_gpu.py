@@ -120,11 +120,11 @@ def test_replica_prefix(semantic):
 @pytest.mark.parametrize("semantic", [False, True])
 @pytest.mark.parametrize("reports", [True, False])
 def test_replica_bench_launch_configuration(semantic, reports):
-    """The bench's launch configuration on its workload: Replica-shaped frames, 16-frame windows,
-    bench.py's capacities (pairs 2^16 per frame, 2^23 memberships, 2^17 instances), three windows
+    """The bench's launch configuration on its workload: Replica-shaped frames, 32-frame windows,
+    bench.py's capacities (pairs 2^16 per frame, 2^23 memberships, 2^17 instances), two windows
     -- per-frame reports, the last frame's debug export and the whole map compared with the oracle;
     without reports the windows run as in bench.py (stage 1 of window w+1 beside stage 2 of w)."""
-    _stream_parity("R", 48, semantic, window=16, reports=reports,
+    _stream_parity("R", 64, semantic, window=32, reports=reports,
                    caps=dict(max_pairs=1 << 16, max_memberships=1 << 23, max_instances=1 << 17))
 
 
