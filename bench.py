@@ -9,7 +9,7 @@ relabel/insert).  Each step integrates NEW frames of the trajectory into the gro
 
 Timing: W untimed warm-up steps, then exactly K steps bracketed by barrier +
 cuda.synchronize, CUDA events on the map's stream; max over ranks.  Inputs per step
-(~0.8 GB) exceed L2 (126 MB), so no flush is needed.  Clocks sampled with nvidia-smi during
+(~1.5 GB per 32-frame step) exceed L2 (126 MB), so no flush is needed.  Clocks sampled with nvidia-smi during
 the timed region.  `e2e`: same metric through disc_integrate_frames_host with pinned HOST
 inputs (H2D copies + report D2H inside the timed region).  `cpu_baseline`: the CPU oracle
 (oracle/, single thread) on a bounded prefix of the same stream.
