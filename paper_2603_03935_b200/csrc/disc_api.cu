@@ -353,7 +353,9 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   m->nsm = prop.multiProcessorCount;
   {  // stage-2 SM reserve; DISC_S2_SMS overrides it (tuning)
     const char* e = std::getenv("DISC_S2_SMS");
-    m->nres = e ? std::atoi(e) : 20;
+    // longer windows amortise stage 1's per-window work, so stage 2 gets a few more SMs (measured
+    // on R: 16-frame windows best at 20, 32-frame windows at 26)
+    m->nres = e ? std::atoi(e) : (cfg->window > 16 ? 26 : 20);
     m->nres = std::max(0, std::min(m->nres, m->nsm / 2));
     const char* eg = std::getenv("DISC_S2_SMS_GEO");
     m->nres_geo = eg ? std::atoi(eg) : 40;
