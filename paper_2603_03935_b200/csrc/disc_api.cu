@@ -358,7 +358,7 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
     m->nres = e ? std::atoi(e) : (cfg->window > 16 ? 26 : 20);
     m->nres = std::max(0, std::min(m->nres, m->nsm / 2));
     const char* eg = std::getenv("DISC_S2_SMS_GEO");
-    m->nres_geo = eg ? std::atoi(eg) : 40;
+    m->nres_geo = eg ? std::atoi(eg) : (cfg->window > 16 ? 48 : 40);
     m->nres_geo = std::max(0, std::min(m->nres_geo, m->nsm / 2));
     const char* ea = std::getenv("DISC_S2_ADAPT");   // 0: fixed split (tuning)
     m->adapt = !(ea && std::atoi(ea) == 0);
