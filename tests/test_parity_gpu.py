@@ -142,6 +142,33 @@ def test_stress_overlapping_masks():
     _stream_parity("X", 6, True, window=6, n_masks=120, Df=512, voxel=0.1)
 
 
+@pytest.mark.parametrize("name,n_masks,Df,voxel", [("X", 10, 768, 0.01), ("X", 150, 1024, 0.05),
+                                                    ("X", 100, 512, 0.02), ("N", 255, 512, 0.02)])
+def test_stress_sweep_points(name, n_masks, Df, voxel):
+    """Points of BASELINE configs[4] (voxel 1-10 cm x masks 10-200 x Df 512/768/1024): X-style
+    hierarchical masks up to S = 150 (frame 1's ~120 kept masks all become instances that frame
+    2's masks overlap: ~1-2k (s, j) triples), and the ABI's maximum S = 255 masks per frame
+    (disc.h max_masks) with partition masks; 4 frames each."""
+    reps = _stream_parity(name, 4, True, window=4, n_masks=n_masks, Df=Df, voxel=voxel)
+    assert max(r["kept"] for r in reps) >= min(8, n_masks // 2) or name == "N"
+
+
+def test_triple_capacity_overflow_is_loud():
+    """X at S = 200 hierarchical masks: frame 2's dense (s, j) overlap set passes the per-frame
+    triple capacity (3072, the single-CTA association's shared-memory tables, DESIGN.md §5 limits):
+    the call fails with the sticky DISC_ERR_CAPACITY instead of dropping counts."""
+    from paper_2603_03935_b200.disc import DiscError
+    dev = _dev()
+    g = Generator("X", device=dev, n_masks=200, Df=512, voxel=0.05)
+    c = g.cfg
+    gm = _disc_map(disc_config_kwargs(c), c.H, c.W, c.Hp, c.Wp, window=4, S=200)
+    with pytest.raises(DiscError) as e:
+        gm.integrate_frames([g.frame(f, with_feats=True) for f in range(4)], report=True)
+    assert e.value.code == 5 and "count table full" in str(e.value)   # DISC_ERR_CAPACITY
+    with pytest.raises(DiscError):    # sticky
+        gm.integrate_frames([g.frame(4, with_feats=True)], report=True)
+
+
 def test_tiny_voxels_overflow_tile_tables():
     """2 mm voxels: nearly every pixel is its own voxel, so the mask pass's per-tile key / pair
     tables overflow and items take the direct path into the frame tables."""
