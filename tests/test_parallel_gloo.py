@@ -69,3 +69,24 @@ def test_single_rank_defaults():
     assert par.max_over_ranks(1.5, r) == 1.5
     assert par.weak_scaling_rate(10, 2.0, r) == 5.0
     assert par.stream_seed(100, 0) == 100 and par.stream_seed(100, 3) == 100 + 3 * par.SEED_STRIDE
+
+
+@pytest.mark.timeout(300)
+def test_reference_arm_under_torchrun_two_ranks():
+    """`bench.py --impl reference` launched the way the driver launches N > 1 (torchrun, gloo on a
+    CPU box): rank 0 alone times the oracle and prints ONE JSON line; rank 1 exits 0 without work."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--impl", "reference",
+           "--gpus", "2", "--steps", "1", "--warmup", "1", "--config", "N"]
+    p = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=280)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["unit"] == "frames/s" and d["value"] > 0 and d["steps"] == 1
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
