@@ -137,6 +137,16 @@ def test_hm3d_prefix():
     _stream_parity("H", 8, True, window=8)
 
 
+@pytest.mark.parametrize("name,pmax", [("H", 1 << 19), ("N", 1 << 16)])
+def test_bench_launch_configuration_h_n(name, pmax):
+    """`bench.py --config H|N`'s launch configuration: 32-frame windows, its capacities (pairs 2^19
+    per frame for H, 2^16 for N), no per-window reports (window 2's stage 1 beside window 1's
+    stage 2), a ragged second window of 8 frames; the last frame's debug export and the whole map
+    compared with the oracle."""
+    _stream_parity(name, 40, True, window=32, reports=False,
+                   caps=dict(max_pairs=pmax, max_memberships=1 << 23, max_instances=1 << 17))
+
+
 def test_stress_overlapping_masks():
     """X-style SAM 'everything' masks (overlapping, hierarchical), Df 512, 10 cm voxels."""
     _stream_parity("X", 6, True, window=6, n_masks=120, Df=512, voxel=0.1)
