@@ -320,7 +320,9 @@ static std::string validate_config(const disc_config* c) {
   if (c->max_pairs_per_frame < 1 || c->max_pairs_per_frame > (1 << 22)) return "max_pairs_per_frame in [1, 2^22]";
   if (c->window < 1 || c->window > MAXWIN) return "window in [1,32]";
   if (c->max_instances < 1 || c->max_instances > (1 << 30)) return "bad max_instances";
-  if (c->max_memberships < 1 || c->max_memberships > (1ll << 31)) return "bad max_memberships";
+  // <= 2^28: the voxel hash (2^29 slots) and the key-list arena (8 * 2^28 + 2^20 entries) stay
+  // indexable by 32-bit slot numbers / list offsets below the U32_EMPTY sentinel
+  if (c->max_memberships < 1 || c->max_memberships > (1ll << 28)) return "max_memberships in [1, 2^28]";
   if (c->world_size != 1 || c->rank != 0) return "sharded maps are not supported by this build";
   return "";
 }
@@ -459,8 +461,15 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   M.err = m->d_err;
   // ---- per-frame scratch ----
   FrameScratch& X = m->X;
-  X.CC = 16384;
-  X.TCAP = 3072;
+  // (s, j) count triples per frame: up to TCS in the association's shared-memory tables, up to
+  // TCAP through its global-memory layout (dense SAM-"everything" frames: ~S^2/10 triples measured
+  // at S = 150); DISC_TCAP / DISC_K6_TCS override them (tests force the global layout with TCS 0)
+  X.TCS = 3072;
+  X.TCAP = (int32_t)std::max<int64_t>(X.TCS, (int64_t)SM * 256);
+  if (const char* e = getenv("DISC_TCAP")) X.TCAP = std::max(1, atoi(e));
+  if (const char* e = getenv("DISC_K6_TCS")) X.TCS = std::max(0, std::min(3072, atoi(e)));
+  X.CC = (int32_t)next_pow2(std::max<int64_t>(16384, 2 * (int64_t)X.TCAP));
+  chk(X.k6g = dalloc<unsigned char>(m, k6_layout_bytes(SM, X.TCAP)));
   chk(X.ctab_key = dalloc<unsigned long long>(m, X.CC, 0xFF));
   chk(X.ctab_cnt = dalloc<uint32_t>(m, X.CC));
   chk(X.ctab_idx = dalloc<uint32_t>(m, X.TCAP));
@@ -512,7 +521,7 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   if (cudaMallocHost(&m->h_np, sizeof(uint32_t) * 2 * MAXWIN) != cudaSuccess) ok = false;
   if (cudaMallocHost(&m->h_err, sizeof(int)) != cudaSuccess) ok = false;
   if (cudaMallocHost(&m->h_rep, sizeof(disc_frame_report) * MAXWIN) != cudaSuccess) ok = false;
-  if (ok && k6_smem_bytes(SM, X.TCAP) > 227 * 1024) ok = false;
+  if (ok && k6_smem_bytes(SM, X.TCS) > 227 * 1024) ok = false;
   cudaDeviceSynchronize();
   if (!ok || cudaGetLastError() != cudaSuccess) {
     std::fprintf(stderr, "disc_map_create: device allocation failed\n");
@@ -703,7 +712,13 @@ disc_status disc_integrate_frames(disc_map* m, const disc_frame* f, int32_t n, v
 
 disc_status disc_integrate_frames_host(disc_map* m, const disc_frame* f, int32_t n, void* stream,
                                        disc_frame_report* report) {
-  if (!m) return DISC_ERR_INVALID;
+  if (!m || (!f && n > 0) || n < 0) return DISC_ERR_INVALID;
+  if (m->sticky != DISC_OK) return m->sticky;
+  // O0 over ALL n frames before the first window mutates the map (disc.h: INVALID = nothing changed)
+  for (int i = 0; i < n; ++i) {
+    const std::string v = validate_frame(m, f[i], true);
+    if (!v.empty()) return fail(m, DISC_ERR_INVALID, "frame " + std::to_string(i) + ": " + v);
+  }
   // the staging buffer holds one window: process window by window
   const int win = m->cfg.window;
   for (int w0 = 0; w0 < n; w0 += win) {

@@ -171,7 +171,9 @@ struct FrameScratch {
   uint32_t* trip_j;
   uint32_t* trip_c;
   uint8_t* trip_edge;
-  int32_t CC, TCAP;
+  int32_t CC, TCAP;               // count-table slots (power of 2, >= 2 TCAP); triple capacity per frame
+  int32_t TCS;                     // triples the association holds in shared memory (denser frames: k6g)
+  unsigned char* k6g;            // global-memory association layout for TCAP triples (K6Smem(SMAX, TCAP))
   // targets
   int32_t* det_target;           // [SMAX]  target index or -1
   int64_t* det_id;               // [SMAX]  instance id fused into (debug)

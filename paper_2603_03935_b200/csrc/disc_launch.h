@@ -9,6 +9,7 @@ void debug_check(cudaStream_t st, const char* kernel, int frame);
 void k6_prof_dump();
 int k1_nsmid();   // %nsmid of the current device (upper bound of %smid)
 size_t k6_smem_bytes(int S, int TC);
+size_t k6_layout_bytes(int S, int TC);   // the association's table layout alone (global-memory mode)
 int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* err, bool sem, int maxS,
                   int maxHp, int maxW, int maxWp, int maxP, int rows_cap, int nsm, int nres, cudaStream_t st,
                   cudaEvent_t ev0, cudaEvent_t ev1);

@@ -422,33 +422,41 @@ __device__ unsigned long long g_tgprof[4];   // DISC_S2PROF: target-update warp 
 __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBufs& wb, const MapState& M,
                                          const FrameScratch& X, const Params& P, int sem) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int TC = X.TCAP;
+  // Layout: the shared-memory tables hold up to X.TCS (s, j) triples; a denser frame (hierarchical
+  // SAM-"everything" masks overlapping many instances, BASELINE configs[4]) runs the same steps on
+  // the same layout in a global-memory scratch sized for X.TCAP triples (block-scope atomics and
+  // __syncthreads order it exactly as in shared memory).  Only a frame past X.TCAP fails (loudly).
+  const uint32_t ntr_all = __ldcg(X.ntrip);
+  const uint32_t ntr = min(ntr_all, (uint32_t)X.TCAP);
+  const bool gmode = ntr > (uint32_t)X.TCS;
+  const int TC = gmode ? X.TCAP : X.TCS;
+  unsigned char* const k6b = gmode ? X.k6g : smem_raw;
   const int S = F.S;
   const K6Smem L6(S, TC);
-  uint8_t* t_s = (uint8_t*)(smem_raw + L6.t_s);            // triple s (S <= 255)
-  uint32_t* t_j = (uint32_t*)(smem_raw + L6.t_j);          // triple j (instance id)
-  uint32_t* t_c = (uint32_t*)(smem_raw + L6.t_c);          // c_sj
-  uint8_t* t_e = (uint8_t*)(smem_raw + L6.t_e);            // edge flag
-  int32_t* t_jl = (int32_t*)(smem_raw + L6.t_jl);          // local instance index
-  int32_t* lab = (int32_t*)(smem_raw + L6.lab);            // [S + nJ] component label
-  uint32_t* jnode = (uint32_t*)(smem_raw + L6.jnode);      // local index -> id
-  uint32_t* comp_root = (uint32_t*)(smem_raw + L6.comp_root);
-  unsigned long long* comp_best = (unsigned long long*)(smem_raw + L6.comp_best);
-  int32_t* comp_tgt = (int32_t*)(smem_raw + L6.comp_tgt);
-  uint8_t* has_edge = (uint8_t*)(smem_raw + L6.has_edge);
-  int32_t* d_st = (int32_t*)(smem_raw + L6.d_st);     // per-detection status (staged from global)
-  uint32_t* d_vs = (uint32_t*)(smem_raw + L6.d_vs);   // |V_s|
-  int32_t* d_tgt = (int32_t*)(smem_raw + L6.d_tgt);   // target index (written back at the end)
-  float* d_q = (float*)(smem_raw + L6.d_q);           // Q_s
-  uint32_t* tg_root = (uint32_t*)(smem_raw + L6.tg_root);   // per target: survivor id
-  uint32_t* tg_phys = (uint32_t*)(smem_raw + L6.tg_phys);   // per target: physical label
-  uint32_t* j_vc = (uint32_t*)(smem_raw + L6.j_vc);         // per local instance: |V_j|
-  uint32_t* j_lo = (uint32_t*)(smem_raw + L6.j_lo);         //   key list of its physical label: offset,
-  uint32_t* j_ll = (uint32_t*)(smem_raw + L6.j_ll);         //   length,
-  uint32_t* j_lc = (uint32_t*)(smem_raw + L6.j_lc);         //   capacity
-  uint32_t* j_ph = (uint32_t*)(smem_raw + L6.j_ph);         //   physical label
-  int32_t* j_obs = (int32_t*)(smem_raw + L6.j_obs);         //   obs count
-  float* j_q = (float*)(smem_raw + L6.j_q);                 //   Q
+  uint8_t* t_s = (uint8_t*)(k6b + L6.t_s);            // triple s (S <= 255)
+  uint32_t* t_j = (uint32_t*)(k6b + L6.t_j);          // triple j (instance id)
+  uint32_t* t_c = (uint32_t*)(k6b + L6.t_c);          // c_sj
+  uint8_t* t_e = (uint8_t*)(k6b + L6.t_e);            // edge flag
+  int32_t* t_jl = (int32_t*)(k6b + L6.t_jl);          // local instance index
+  int32_t* lab = (int32_t*)(k6b + L6.lab);            // [S + nJ] component label
+  uint32_t* jnode = (uint32_t*)(k6b + L6.jnode);      // local index -> id
+  uint32_t* comp_root = (uint32_t*)(k6b + L6.comp_root);
+  unsigned long long* comp_best = (unsigned long long*)(k6b + L6.comp_best);
+  int32_t* comp_tgt = (int32_t*)(k6b + L6.comp_tgt);
+  uint8_t* has_edge = (uint8_t*)(k6b + L6.has_edge);
+  int32_t* d_st = (int32_t*)(k6b + L6.d_st);     // per-detection status (staged from global)
+  uint32_t* d_vs = (uint32_t*)(k6b + L6.d_vs);   // |V_s|
+  int32_t* d_tgt = (int32_t*)(k6b + L6.d_tgt);   // target index (written back at the end)
+  float* d_q = (float*)(k6b + L6.d_q);           // Q_s
+  uint32_t* tg_root = (uint32_t*)(k6b + L6.tg_root);   // per target: survivor id
+  uint32_t* tg_phys = (uint32_t*)(k6b + L6.tg_phys);   // per target: physical label
+  uint32_t* j_vc = (uint32_t*)(k6b + L6.j_vc);         // per local instance: |V_j|
+  uint32_t* j_lo = (uint32_t*)(k6b + L6.j_lo);         //   key list of its physical label: offset,
+  uint32_t* j_ll = (uint32_t*)(k6b + L6.j_ll);         //   length,
+  uint32_t* j_lc = (uint32_t*)(k6b + L6.j_lc);         //   capacity
+  uint32_t* j_ph = (uint32_t*)(k6b + L6.j_ph);         //   physical label
+  int32_t* j_obs = (int32_t*)(k6b + L6.j_obs);         //   obs count
+  float* j_q = (float*)(k6b + L6.j_q);                 //   Q
   __shared__ uint32_t n_j, n_tgt, n_seg, ncomp_s, n_cand;
   __shared__ uint32_t mcnt_s[256], dcnt_s[256], moff_s[256], doff_s[256];
   __shared__ int64_t tg_vb[256];
@@ -466,9 +474,8 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
     g_k6prof[0] = t_;
   }
-  const uint32_t ntr = min(__ldcg(X.ntrip), (uint32_t)TC);
   if (tid == 0) {
-    if (__ldcg(X.ntrip) > (uint32_t)TC) raise_err(M.err, DERR_TRIPLES);
+    if (ntr_all > (uint32_t)X.TCAP) raise_err(M.err, DERR_TRIPLES);
     n_j = 0; n_tgt = 0; n_seg = 0; rel_s = 0; merged_s = 0; edges_s = 0; n_cand = 0;
     // the map counters this step reads, all in one round trip (only this thread writes 0, 1, 3,
     // 4, 6, 7; counter 2 is K7's)
@@ -479,7 +486,7 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
     *X.nrel = 0;
     *X.work = 0;
   }
-  for (int i = tid; i < S + TC; i += blockDim.x) {
+  for (int i = tid; i < S + (int)ntr; i += blockDim.x) {   // nodes: detections + (<= ntr) instances
     lab[i] = i;
     comp_root[i] = U32_EMPTY;
     comp_best[i] = 0;
@@ -1417,6 +1424,8 @@ __device__ __forceinline__ void s2_finalize(int f, const MapState& M, const Fram
   }
 }
 
+size_t k6_layout_bytes(int S, int TC) { return K6Smem(S, TC).total; }
+
 size_t k6_smem_bytes(int S, int TC) {
   // the association's layout; the lookup / apply phases reuse the same bytes
   return std::max(K6Smem(S, TC).total, (size_t)LK_CT * 12 + (size_t)S * 32 + 64);
@@ -1523,7 +1532,7 @@ __global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb
 
 int launch_stage2(const WinDesc& wd, const WinBufs& wb, const MapState& M, const FrameScratch& X, const Params& P,
                   bool sem, int nsm, int nres, cudaStream_t st) {
-  const size_t sm6 = k6_smem_bytes(wb.SMAX, X.TCAP);
+  const size_t sm6 = k6_smem_bytes(wb.SMAX, X.TCS);
   static size_t set_for = 0;
   if (set_for != sm6) {
     cudaFuncSetAttribute(k_stage2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm6);

@@ -285,7 +285,7 @@ class DiscMap:
         o = np.lexsort((ids, keys))
         return keys[o], ids[o]
 
-    def last_frame(self, pair_cap: int = 1 << 22, trip_cap: int = 1 << 14) -> dict:
+    def last_frame(self, pair_cap: int = 1 << 22, trip_cap: int = 1 << 17) -> dict:
         d = disc_frame_debug()
         self._check(lib().disc_debug_last_frame(self.h, C.byref(d)))
         S = d.num_masks
