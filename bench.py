@@ -1,24 +1,29 @@
 #!/usr/bin/env python
 """bench.py -- DISC per-frame mapping hot path on B200 (libdisc, sm_100a).
 
-One STEP = one window of F frames (default 16) of the Replica-shaped stream (BASELINE.json
-configs[1]: 680x1200, ~33 masks/frame, 2 cm voxels, ViT-L/14 1024-d tokens, 384-d tracking)
-through disc_integrate_frames: every §8(a) row (mask pass + back-projection + dedup, D map,
-D-weighted pooling + Q, tracking, lookup + overlap counts, association + union-find,
-relabel/insert).  Each step integrates NEW frames of the trajectory into the growing map.
+Workload (default --config H = BASELINE.json configs[3], the config the 1/2/4/8-GPU numbers are
+quoted on): the HM3D-shaped multi-story building stream, 480x640, ~60 masks/frame (finer SAM-like
+over-segmentation, mean 60 +- 20 %), 2 cm voxels, 34x45 ViT-L/14 tokens (1024-d CLIP, 384-d bf16
+tracking).  Before timing, the map is PREFILLED (untimed, windows generated on the fly) by the first
+frames of the tour until it holds >= 10^7 live (voxel, instance) memberships; every timed frame then
+looks up, merges into and relabels a map of that size.
 
-Timing: W untimed warm-up steps, then exactly K steps bracketed by barrier +
-cuda.synchronize, CUDA events on the map's stream; max over ranks.  Inputs per step
-(~1.5 GB per 32-frame step) exceed L2 (126 MB), so no flush is needed.  Clocks sampled with nvidia-smi during
-the timed region.  `e2e`: same metric through disc_integrate_frames_host with pinned HOST
-inputs (H2D copies + report D2H inside the timed region).  `cpu_baseline`: the CPU oracle
-(oracle/, single thread) on a bounded prefix of the same stream.
+One STEP = one window of F = 32 NEW frames of the stream through disc_integrate_frames.
+  value = M1 frames/s = "voxel association + refinement" (BASELINE.json metric; SURVEY §8(a) rows
+          A0-A3, A5b, A6-A8: patch_feats = NULL), device-timed.
+  m2    = the full path (+ A4 distinctiveness, A5 D-weighted pooling + Q) on the next frames.
+Timing: W untimed warm-up steps, then exactly K steps bracketed by barrier + cuda.synchronize,
+CUDA events on the caller's stream (disc_wait orders it after the map's internal streams); max
+over ranks.  Inputs per step (~0.65 GB M1 / ~0.85 GB M2) exceed the 126 MB L2: no flush needed.
+Clocks sampled through NVML during the timed region.  `e2e`: M1 through the public host-input call
+disc_integrate_frames_host (pinned host buffers: H2D inside the timed region, report D2H).
+`cpu_baseline`: the CPU oracle (oracle/, 1 thread, as it stands) on a bounded prefix of the stream.
 
-N > 1 (torchrun): every rank maps its own independent scene stream (weak scaling, no
-data-path collective: independent problems); value = all frames / max time.
+N > 1 (torchrun): DISC_SHARDED=0 (default until the sharded path is selected) gives every rank
+its own scene stream (weak scaling, independent problems); see DESIGN.md §8.
 
---impl reference: the reference arm is the CPU oracle (this tier has no reference code);
-rank 0 runs it on the host cores, each step a bounded sample of the same workload.
+--impl reference: the reference arm is the CPU oracle (this tier has no reference code); rank 0
+runs it on the host cores, each step a bounded sample (1 frame) of the same workload.
 """
 from __future__ import annotations
 
@@ -42,11 +47,15 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="R", choices=["R", "N", "H"])
-    p.add_argument("--frames-per-step", type=int, default=32)   # = the map's window (32: +3 % over 16)
+    p.add_argument("--config", default="H", choices=["R", "N", "H"])
+    p.add_argument("--frames-per-step", type=int, default=32)   # = the map's window
+    p.add_argument("--prefill-memberships", type=float, default=None,
+                   help="untimed prefill until the map holds this many live memberships (H: 1e7, else 0)")
+    p.add_argument("--prefill-max-frames", type=int, default=8192)
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--oracle-seconds", type=float, default=12.0)
-    p.add_argument("--no-m1", action="store_true")
+    p.add_argument("--no-m2", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     return p.parse_args()
 
@@ -55,16 +64,18 @@ def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             mp = json.load(f)
-        return float(mp["hbm_gbs"]), "measured"
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 WORKLOAD = {
-    "R": "replica-shaped stream (BASELINE configs[1]): 680x1200, ~33 masks/frame, 2 cm voxels, "
+    "R": "replica-shaped stream (BASELINE configs[1]): 680x1200, ~40 masks/frame, 2 cm voxels, "
          "ViT-L/14 48x85x1024 fp32 tokens, 48x85x384 bf16 tracking tokens",
-    "N": "scannet-shaped stream (BASELINE configs[2]): 480x640 noisy depth, ~21 masks/frame, 5 cm voxels",
-    "H": "hm3d multi-story building (BASELINE configs[3]): 480x640, ~35 masks/frame, 2 cm voxels",
+    "N": "scannet-shaped stream (BASELINE configs[2]): 480x640 noisy depth, ~30 masks/frame, 5 cm voxels, "
+         "34x45x1024 fp32 tokens, 34x45x384 bf16 tracking tokens",
+    "H": "hm3d multi-story building (BASELINE configs[3]): 480x640, ~60 masks/frame, 2 cm voxels, "
+         "34x45x1024 fp32 tokens, 34x45x384 bf16 tracking tokens, map prefilled to >= 1e7 live memberships",
 }
 
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
@@ -182,6 +193,11 @@ def run_oracle_frames(frames_np, cfg_kw, budget_s, min_frames=1):
     return n, time.perf_counter() - t0
 
 
+def m1(fr: dict) -> dict:
+    """M1 input of a frame: no CLIP tokens (association + refinement only)."""
+    return dict(fr, patch_feats=None, global_embed=None)
+
+
 # --------------------------------------------------------------------------------------------
 # reference arm (the CPU oracle)
 # --------------------------------------------------------------------------------------------
@@ -195,8 +211,8 @@ def run_reference(args, ws, rank):
     dev = "cuda:0" if torch.cuda.is_available() else "cpu"
     g = Generator(args.config, device=dev)
     cfg_kw = disc_config_kwargs(g.cfg)
-    per_step = 2 if args.config == "R" else 4
-    frames = [frame_to_numpy(g.frame(f)) for f in range((args.warmup + args.steps) * per_step)]
+    per_step = 1 if args.config in ("R", "H") else 2
+    frames = [frame_to_numpy(m1(g.frame(f, with_feats=False))) for f in range((args.warmup + args.steps) * per_step)]
     om = OracleMap(**cfg_kw)
     fi = 0
     for _ in range(args.warmup):
@@ -211,11 +227,12 @@ def run_reference(args, ws, rank):
     value = n / dt
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD[args.config], "frames_per_step": per_step,
-                       "mode": "M2 (all §8(a) rows)", "l2": "n/a (CPU)"},
+                       "mode": "M1 (voxel association + refinement)", "l2": "n/a (CPU)"},
             "cpu_baseline": {"value": value, "unit": "frames/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{n} frames ({per_step}/step) after {args.warmup * per_step} warm-up frames"},
+                             "sample": f"{n} frames ({per_step}/step) after {args.warmup * per_step} warm-up frames, "
+                                       f"map starting empty (the oracle cannot prefill 1e7 memberships in minutes)"},
             "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
     print(json.dumps(line), flush=True)
@@ -225,15 +242,20 @@ def run_reference(args, ws, rank):
 # our arm
 # --------------------------------------------------------------------------------------------
 
-def path_bytes(stats0, stats1, in_bytes, cfg) -> float:
-    """Algorithmic bytes of the whole path over a timed region (SURVEY §8(d) B_f):
-    inputs read once + 16 B per membership probe (U) / insert / relabel item + instance
-    state of touched instances (T reads for the gate, embeddings written)."""
-    d = {k: stats1[k] - stats0[k] for k in ["pairs", "map_inserts", "relabels", "edges"]}
-    b = in_bytes
-    b += 16 * (d["pairs"] + d["map_inserts"] + d["relabels"])
-    b += d["edges"] * cfg.Dt * 8
-    return float(b)
+def stage2_bytes(d: dict, Dt: int) -> float:
+    """SURVEY §8(d) map bytes of stage 2 (A6-A8): 16 B per membership probe (U) / insert / relabel
+    item + the gate's instance tracking rows (Dt fp64 per qualifying edge)."""
+    return 16.0 * (d["pairs"] + d["map_inserts"] + d["relabels"]) + 8.0 * Dt * d["edges"]
+
+
+def load_traffic(config: str, mode: str):
+    """ncu dram bytes per frame of the kernels, captured on THIS config and mode (profiles/)."""
+    f = os.path.join(ROOT, "profiles", f"traffic_{config}.json")
+    try:
+        with open(f) as fh:
+            return json.load(fh)[mode]
+    except Exception:
+        return None
 
 
 def main():
@@ -243,7 +265,6 @@ def main():
     if args.impl == "reference":
         run_reference(args, ws, rank)
         return
-    import numpy as np  # noqa: F401
     import torch
     from synth import Generator, disc_config_kwargs, frame_to_numpy
     from synth.scenes import seed_of
@@ -251,26 +272,44 @@ def main():
 
     dev = torch.device("cuda", local)
     F = args.frames_per_step
-    # independent scene per rank (weak scaling)
     g = Generator(args.config, seed=par.stream_seed(seed_of(args.config), rank), device=dev)
     c = g.cfg
     cfg_kw = disc_config_kwargs(c)
-    nframes = (args.warmup + args.steps) * F
-    t_gen = time.perf_counter()
-    frames = [g.frame(f) for f in range(nframes)]
-    torch.cuda.synchronize()
-    t_gen = time.perf_counter() - t_gen
-    maxS = max(fr["masks"].shape[0] for fr in frames)
-    caps = dict(max_pixels=c.H * c.W, max_patches=c.Hp * c.Wp, max_masks=max(64, maxS), window=F,
-                max_memberships=1 << 23, max_instances=1 << 17,
-                # per-frame (mask, voxel) pair capacity: R and N frames stay below ~32k unique pairs
-                # (e2e records the maximum seen), so 2^16 leaves a 2x margin; H's far
-                # views reach ~1 pair per pixel (2 cm voxels, 480x640): 2^19.  A frame past it fails
-                # loudly (CAPACITY)
-                max_pairs_per_frame=int(os.environ.get("BENCH_PMAX", 1 << 19 if args.config == "H" else 1 << 16)),
+    prefill = args.prefill_memberships if args.prefill_memberships is not None else (1e7 if args.config == "H" else 0)
+    caps = dict(max_pixels=c.H * c.W, max_patches=c.Hp * c.Wp, max_masks=int(c.n_masks * 1.2) + 8, window=F,
+                max_memberships=1 << 25 if prefill > 0 else 1 << 23, max_instances=1 << 20,
+                # per-frame (mask, voxel) pair capacity: R and N frames stay below ~40k unique pairs, H's far
+                # views reach ~1 pair per pixel (2 cm voxels, 480x640): 2^19.  Past it: loud CAPACITY error
+                max_pairs_per_frame=int(os.environ.get("BENCH_PMAX", 1 << 19 if args.config == "H" else 1 << 17)),
                 device=local)
+    m = DiscMap(**cfg_kw, **caps)
+    t_gen = 0.0
+    nxt = 0   # next frame index of the stream
 
-    def run(frames_, timed_steps, warm_steps, m):
+    def gen(n, feats):
+        nonlocal nxt, t_gen
+        t0 = time.perf_counter()
+        out = [g.frame(f, with_feats=feats) for f in range(nxt, nxt + n)]
+        if not feats:
+            out = [m1(fr) for fr in out]
+        torch.cuda.synchronize()
+        t_gen += time.perf_counter() - t0
+        nxt += n
+        return out
+
+    # ---- prefill (untimed): the tour's first frames until the map holds `prefill` memberships ----
+    live = 0
+    t_pf = time.perf_counter()
+    while live < prefill and nxt < args.prefill_max_frames:
+        reps = m.integrate_frames(gen(F, False), report=True)
+        live = reps[-1]["live_memberships"]
+        if rank == 0 and (nxt // F) % 8 == 0:
+            print(f"prefill: {nxt} frames, {live} live memberships, {reps[-1]['live_instances']} instances, "
+                  f"{time.perf_counter() - t_pf:.0f} s", file=sys.stderr, flush=True)
+    prefill_frames = nxt
+    t_pf = time.perf_counter() - t_pf
+
+    def run(frames_, timed_steps, warm_steps):
         for s in range(warm_steps):
             m.integrate_frames(frames_[s * F:(s + 1) * F])
         m.sync()
@@ -280,6 +319,7 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier(ws)
         torch.cuda.synchronize()
+        torch.cuda.nvtx.range_push("timed")
         with ClockSampler(local) as clk:
             e0.record(stream)
             for s in range(warm_steps, warm_steps + timed_steps):
@@ -287,109 +327,123 @@ def main():
             m.wait(stream)   # include the last window's stage 2
             e1.record(stream)
             torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
         barrier(ws)
         ms = e0.elapsed_time(e1)
         m.set_timing(False)
         st1 = m.stats()
-        return ms, st0, st1, clk.summary()
+        return ms, {k: st1[k] - st0[k] for k in st1}, clk.summary()
 
-    # ---- M2: the whole path (headline) ----
-    m2 = DiscMap(**cfg_kw, **caps)
-    ms, st0, st1, clocks = run(frames, args.steps, args.warmup, m2)
-    ms_max = max_over_ranks(ms, ws)
-    timed = frames[args.warmup * F:]
-    value = ws * args.steps * F / (ms_max / 1e3)
     peak, peak_kind = peaks()
-    # dominant kernel: K1 (mask pass + back-projection + dedup).  Algorithmic bytes per frame =
-    # S*H*W mask bytes + 4*H*W depth bytes (every input byte read once).
-    k1_bytes = sum(fr["masks"].numel() + fr["depth"].numel() * 4 for fr in timed)
-    k1_ms = st1["k1_ms"] - st0["k1_ms"]
-    k1_launches = st1["k1_launches"] - st0["k1_launches"]
-    achieved = k1_bytes / (k1_ms / 1e3) / 1e9 if k1_ms > 0 else None
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "k1_dram_bytes_per_frame.json")
-    if os.path.exists(tfile):
-        try:
-            with open(tfile) as f:
-                traffic = json.load(f)["dram_bytes_per_frame"] * F
-        except Exception:
-            traffic = None
-    in_bytes = sum(frame_bytes(fr) for fr in timed)
-    pb = path_bytes(st0, st1, in_bytes, c)
-    launches = st1["launches"] - st0["launches"]
 
+    def measure(mode, feats):
+        frames = gen((args.warmup + args.steps) * F, feats)
+        ms, d, clocks = run(frames, args.steps, args.warmup)
+        ms_max = max_over_ranks(ms, ws)
+        timed = frames[args.warmup * F:]
+        n = len(timed)
+        in_bytes = sum(frame_bytes(fr) for fr in timed)
+        k1_bytes = sum(fr["masks"].numel() + fr["depth"].numel() * 4 for fr in timed)
+        s2_bytes = stage2_bytes(d, c.Dt)
+        k1_ms, s2_ms = d["k1_ms"], d["stage2_ms"]
+        kern = {
+            "K1": {"kernel": "K1 mask pass (k_masks + k_walk + k_dedup)", "bound": "hbm",
+                   "algorithmic_bytes_per_launch": k1_bytes / max(d["k1_launches"], 1),
+                   "bytes_per_unit": "S*H*W mask bytes + 4*H*W depth bytes per frame (every input byte once)",
+                   "avg_launch_ms": k1_ms / max(d["k1_launches"], 1), "launches": d["k1_launches"],
+                   "achieved": k1_bytes / (k1_ms / 1e3) / 1e9 if k1_ms > 0 else None,
+                   "share_of_step": k1_ms / ms if ms > 0 else None},
+            "stage2": {"kernel": "k_stage2 (A6 lookup + overlap counts, A7 association, A8 map update)", "bound": "hbm",
+                       "algorithmic_bytes_per_launch": s2_bytes / max(args.steps, 1),
+                       "bytes_per_unit": "16 B per (s,key) probe / insert / relabel item + 8*Dt B per edge (SURVEY §8(d))",
+                       "avg_launch_ms": s2_ms / max(args.steps, 1), "launches": args.steps,
+                       "achieved": s2_bytes / (s2_ms / 1e3) / 1e9 if s2_ms > 0 else None,
+                       "share_of_step": s2_ms / ms if ms > 0 else None},
+        }
+        tr = load_traffic(args.config, mode) or {}
+        for k, v in kern.items():
+            v["peak"], v["unit"] = peak, "GB/s"
+            v["frac"] = v["achieved"] / peak if v["achieved"] else None
+            t = tr.get(k)
+            v["traffic"] = t * n / v["launches"] if t is not None and v["launches"] else None
+        dom = max(kern, key=lambda k: kern[k]["share_of_step"] or 0.0)
+        pb = in_bytes + s2_bytes
+        return {"value": ws * args.steps * F / (ms_max / 1e3), "ms": ms_max, "clocks": clocks, "kernels": kern,
+                "dominant": dom, "frames": timed, "d": d,
+                "path": {"bound": "hbm", "algorithmic_bytes_per_frame": pb / n, "achieved": pb / (ms / 1e3) / 1e9,
+                         "peak": peak, "unit": "GB/s", "frac": pb / (ms / 1e3) / 1e9 / peak,
+                         "stage1_ms": d["stage1_ms"], "stage2_ms": s2_ms}}
+
+    r1 = measure("M1", False)
+    dom = r1["kernels"][r1["dominant"]]
+    timed = r1["frames"]
     line = {
-        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "metric": METRIC, "value": r1["value"], "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": r1["ms"] / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD[args.config], "frames_per_step": F, "mode": "M2 (all §8(a) rows)",
-                   "l2": f"no flush: inputs per step {in_bytes / args.steps / 1e9:.2f} GB > 126 MB L2",
-                   "frames_timed_per_rank": args.steps * F, "masks_per_frame_mean":
-                       round(sum(fr["masks"].shape[0] for fr in timed) / len(timed), 1),
+        "config": {"workload": WORKLOAD[args.config], "frames_per_step": F,
+                   "mode": "M1 = voxel association + refinement (A0-A3, A5b, A6-A8; no CLIP tokens)",
+                   "l2": f"no flush: inputs per step {sum(frame_bytes(fr) for fr in timed) / args.steps / 1e9:.2f} GB > 126 MB L2",
+                   "frames_timed_per_rank": args.steps * F,
+                   "masks_per_frame_mean": round(sum(fr["masks"].shape[0] for fr in timed) / len(timed), 1),
+                   "prefill_frames": prefill_frames, "prefill_seconds": round(t_pf, 1),
+                   "live_memberships_before_timing": int(live),
                    "parallelism": f"{ws} independent maps (one scene stream per rank)" if ws > 1 else "1 GPU"},
-        "roofline": {"bound": "hbm", "kernel": "K1 mask pass (k_masks + k_walk + k_dedup)", "achieved": achieved, "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
-                     "traffic": traffic, "algorithmic_bytes_per_launch": k1_bytes / max(k1_launches, 1),
-                     "avg_launch_ms": k1_ms / max(k1_launches, 1), "launches": k1_launches,
-                     "share_of_step": k1_ms / ms if ms > 0 else None},
-        "path_roofline": {"bound": "hbm", "algorithmic_bytes_per_frame": pb / len(timed),
-                          "achieved": pb / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
-                          "frac": pb / (ms / 1e3) / 1e9 / peak,
-                          "stage1_ms": st1["stage1_ms"] - st0["stage1_ms"],
-                          "stage2_ms": st1["stage2_ms"] - st0["stage2_ms"]},
-        "clocks": clocks,
-        "gpu_launches": launches,
-        "counters": {k: st1[k] - st0[k] for k in ["pairs", "map_inserts", "relabels", "edges"]},
-        "gen_seconds": round(t_gen, 1),
+        "roofline": {"bound": dom["bound"], "kernel": dom["kernel"], "achieved": dom["achieved"], "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": dom["frac"], "traffic": dom["traffic"],
+                     "algorithmic_bytes_per_launch": dom["algorithmic_bytes_per_launch"],
+                     "bytes_per_unit": dom["bytes_per_unit"], "avg_launch_ms": dom["avg_launch_ms"],
+                     "launches": dom["launches"], "share_of_step": dom["share_of_step"]},
+        "roofline_kernels": r1["kernels"],
+        "path_roofline": r1["path"],
+        "clocks": r1["clocks"],
+        "gpu_launches": r1["d"]["launches"],
+        "counters": {k: r1["d"][k] for k in ["pairs", "map_inserts", "relabels", "edges"]},
     }
-    del m2
+    del r1, timed
 
-    # ---- M1: association + refinement only (no CLIP tokens) ----
-    if not args.no_m1:
-        frames_m1 = [dict(fr, patch_feats=None, global_embed=None) for fr in frames]
-        m1 = DiscMap(**cfg_kw, **caps)
-        ms1, a0, a1, _ = run(frames_m1, args.steps, args.warmup, m1)
-        ms1 = max_over_ranks(ms1, ws)
-        in1 = sum(frame_bytes(fr) for fr in frames_m1[args.warmup * F:])
-        pb1 = path_bytes(a0, a1, in1, c)
-        line["m1"] = {"value": ws * args.steps * F / (ms1 / 1e3), "unit": "frames/s", "ms_per_step": ms1 / args.steps,
-                      "path_frac": pb1 / (ms1 / 1e3) / 1e9 / peak,
-                      "k1_frac": (sum(fr["masks"].numel() + fr["depth"].numel() * 4 for fr in frames_m1[args.warmup * F:])
-                                  / ((a1["k1_ms"] - a0["k1_ms"]) / 1e3) / 1e9 / peak)}
-        del m1
+    # ---- M2: the whole path (CLIP distinctiveness + pooling + Q as well), next frames ----
+    if not args.no_m2:
+        r2 = measure("M2", True)
+        line["m2"] = {"value": r2["value"], "unit": "frames/s", "ms_per_step": r2["ms"] / args.steps,
+                      "mode": "M2 = all §8(a) rows", "path_roofline": r2["path"], "roofline_kernels": r2["kernels"],
+                      "dominant": r2["dominant"], "clocks": r2["clocks"], "gpu_launches": r2["d"]["launches"]}
+        del r2
 
-    # ---- e2e: the public API with pinned HOST inputs, copies inside the timed region ----
-    E = max(1, min(args.e2e_steps, args.steps))
-    host = []
-    for fr in frames[: (E + 1) * F]:
-        host.append({k: (v.cpu().pin_memory() if isinstance(v, torch.Tensor) else v) for k, v in fr.items()})
-    me = DiscMap(**cfg_kw, **caps)
-    me.integrate_frames_host(host[:F], report=True)   # warm-up step
-    h2d = sum(frame_bytes(fr) for fr in host[F:]) / E
-    barrier(ws)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    max_u = 0
-    for s in range(1, E + 1):
-        reps = me.integrate_frames_host(host[s * F:(s + 1) * F], report=True)
-        max_u = max([max_u] + [r["unique_pairs"] for r in reps])
-    torch.cuda.synchronize()
-    te = max_over_ranks(time.perf_counter() - t0, ws)
-    from paper_2603_03935_b200.disc import disc_frame_report
-    import ctypes
-    line["e2e"] = {"value": ws * E * F / te, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
-                   "d2h_bytes_per_step": F * ctypes.sizeof(disc_frame_report), "steps": E,
-                   "api": "disc_integrate_frames_host (pinned host buffers)", "max_unique_pairs_per_frame": int(max_u),
-                   "max_pairs_per_frame": caps["max_pairs_per_frame"]}
-    del me, host
+    # ---- e2e: the public API with pinned HOST inputs (M1), copies inside the timed region ----
+    if not args.no_e2e:
+        E = max(1, min(args.e2e_steps, args.steps))
+        host = [{k: (v.cpu().pin_memory() if isinstance(v, torch.Tensor) else v) for k, v in fr.items()}
+                for fr in gen((E + 1) * F, False)]
+        m.integrate_frames_host(host[:F], report=True)   # warm-up step
+        h2d = sum(frame_bytes(fr) for fr in host[F:]) / E
+        barrier(ws)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        max_u = 0
+        for s in range(1, E + 1):
+            reps = m.integrate_frames_host(host[s * F:(s + 1) * F], report=True)
+            max_u = max([max_u] + [r["unique_pairs"] for r in reps])
+        torch.cuda.synchronize()
+        te = max_over_ranks(time.perf_counter() - t0, ws)
+        from paper_2603_03935_b200.disc import disc_frame_report
+        import ctypes
+        line["e2e"] = {"value": ws * E * F / te, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
+                       "d2h_bytes_per_step": F * ctypes.sizeof(disc_frame_report), "steps": E, "mode": "M1",
+                       "api": "disc_integrate_frames_host (pinned host buffers)",
+                       "max_unique_pairs_per_frame": int(max_u), "max_pairs_per_frame": caps["max_pairs_per_frame"],
+                       "live_memberships_after": int(reps[-1]["live_memberships"])}
+        del host
+    line["gen_seconds"] = round(t_gen, 1)
 
-    # ---- CPU baseline: the oracle as it stands, 1 thread, bounded prefix of the stream ----
+    # ---- CPU baseline: the oracle as it stands, 1 thread, bounded prefix of the stream (M1) ----
     if rank == 0 and ws == 1 and not args.no_cpu:
-        frames_np = (frame_to_numpy(fr) for fr in frames)
+        g0 = Generator(args.config, seed=par.stream_seed(seed_of(args.config), rank), device=dev)
+        frames_np = (frame_to_numpy(m1(g0.frame(f, with_feats=False))) for f in range(10 ** 6))
         n, dt = run_oracle_frames(frames_np, cfg_kw, args.oracle_seconds)
         line["cpu_baseline"] = {"value": n / dt, "unit": "frames/s", "cores": 1, "host_cores": os.cpu_count(),
                                 "kind": "oracle",
-                                "sample": f"first {n} frames of the same stream (full M2 path), {dt:.1f} s"}
+                                "sample": f"first {n} frames of the same stream (M1 path), map starting empty, {dt:.1f} s"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     par.teardown(RANK)

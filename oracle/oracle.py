@@ -14,7 +14,8 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libdisc_oracle.so")
+# DISC_ORACLE_LIB: an alternative build of the same source (the ASan/UBSan build, tools/sanitize_oracle.sh)
+_LIB_PATH = os.environ.get("DISC_ORACLE_LIB") or os.path.join(_HERE, "libdisc_oracle.so")
 
 KEPT, DROP_AREA, DROP_CONF, DROP_ASPECT, DROP_NODEPTH, DROP_NOFEAT = range(6)
 
@@ -67,8 +68,8 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(
-                os.path.join(_HERE, "disc_oracle.cpp")):
+        if not os.environ.get("DISC_ORACLE_LIB") and (not os.path.exists(_LIB_PATH) or os.path.getmtime(
+                _LIB_PATH) < os.path.getmtime(os.path.join(_HERE, "disc_oracle.cpp"))):
             build()
         L = C.CDLL(_LIB_PATH)
         P, I32, I64, U64, D, F = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_double, C.c_float

@@ -20,6 +20,7 @@ import numpy as np
 import torch
 
 MASK32 = 0xFFFFFFFF
+PIECES = 64   # segment id = object id * PIECES + piece
 
 
 # ----------------------------------------------------------------------------------------
@@ -89,6 +90,7 @@ class SceneConfig:
     traj: str = "orbit"
     pieces: tuple = (2, 4)              # Voronoi pieces per large room surface per frame
     split_frac: float = 0.04            # objects covering more of the image are split 1-3x
+    fill_masks: bool = False            # refine segments up to ~n_masks per frame (mean n_masks, +-20 %)
     extra: dict = field(default_factory=dict)
 
 
@@ -101,13 +103,14 @@ CONFIGS = {
                      scene="tiny", n_objects=3, min_area=8, traj="tiny"),
     "R": SceneConfig("R", 680, 1200, 600.0, 600.0, 599.5, 339.5, 0.02, 40, _hp(680), _hp(1200),
                      1024, 384, 2000, room=(6.5, 5.0, 3.0), n_objects=140, traj="orbit", pieces=(4, 8),
-                     split_frac=0.02),
+                     split_frac=0.02, fill_masks=True),
     "N": SceneConfig("N", 480, 640, 577.6, 578.7, 318.9, 242.7, 0.05, 30, _hp(480), _hp(640),
                      1024, 384, 5000, room=(7.0, 6.0, 3.0), n_objects=90, noise=True,
-                     valid_max=4.5, traj="handheld", pieces=(3, 6), split_frac=0.03),
+                     valid_max=4.5, traj="handheld", pieces=(3, 6), split_frac=0.03,
+                     fill_masks=True),
     "H": SceneConfig("H", 480, 640, 320.0, 320.0, 320.0, 240.0, 0.02, 60, _hp(480), _hp(640),
                      1024, 384, 20000, scene="building", n_objects=2400, traj="tour", pieces=(3, 6),
-                     split_frac=0.02),
+                     split_frac=0.02, fill_masks=True),
     "X": SceneConfig("X", 480, 640, 577.6, 578.7, 318.9, 242.7, 0.05, 50, _hp(480), _hp(640),
                      1024, 384, 300, room=(7.0, 6.0, 3.0), n_objects=40, overlap_masks=True,
                      traj="handheld"),
@@ -443,7 +446,7 @@ class Generator:
         depth = torch.where(depth > cfg.valid_max, torch.zeros_like(depth), depth)
         obj = torch.where(hitmask, obj, torch.full_like(obj, -1))
         # SAM-like segments: split large surfaces into 2-4 frame-varying Voronoi pieces
-        seg = obj * 8
+        seg = obj * PIECES
         vis = torch.unique(obj[obj >= 0])
         rng = np_rng(self.seed, 3_000_000 + f)
         npix_obj = torch.bincount(obj[obj >= 0], minlength=sc.n_obj)
@@ -459,11 +462,15 @@ class Generator:
             lo_, hi_ = p.min(0).values, p.max(0).values
             seeds = lo_ + (hi_ - lo_) * torch.tensor(rng.uniform(0, 1, (k, 3)), dtype=torch.float32, device=dev)
             piece = torch.cdist(p, seeds).argmin(1)
-            seg[sel] = oi * 8 + piece
+            seg[sel] = oi * PIECES + piece
         seg = torch.where(obj >= 0, seg, torch.full_like(seg, -1))
+        n_target = cfg.n_masks
+        if cfg.fill_masks:   # finer SAM-like over-segmentation up to this frame's mask count
+            n_target = int(round(cfg.n_masks * rng.uniform(0.8, 1.2)))
+            seg = self._refine(seg, pts, rng, n_target)
         ids, counts = torch.unique(seg[seg >= 0], return_counts=True)
         order = torch.argsort(counts, descending=True, stable=True)
-        ids = ids[order][: cfg.n_masks]
+        ids = ids[order][: n_target]
         S_part = ids.shape[0]
         masks = (seg[None, :] == ids[:, None]).to(torch.uint8)
         if cfg.overlap_masks and S_part < cfg.n_masks:
@@ -496,15 +503,48 @@ class Generator:
             out["track_feats"] = snap_bf16(tr).reshape(cfg.Hp, cfg.Wp, cfg.Dt).contiguous()
         return out
 
+    def _refine(self, seg, pts, rng, n_target):
+        """R/N/H: SAM-like over-segmentation finer than the per-surface split -- while the frame has
+        fewer than n_target segments, the largest segment (at least 4 x min_area pixels) is cut in
+        two along the Voronoi boundary of two of its own 3-D points (a partition: masks stay
+        disjoint, every pixel keeps one segment)."""
+        cfg = self.cfg
+        ids, counts = torch.unique(seg[seg >= 0], return_counts=True)
+        cnt = dict(zip(ids.tolist(), counts.tolist()))
+        used = {}
+        for i in cnt:
+            used[i // PIECES] = max(used.get(i // PIECES, -1), i % PIECES)
+        while len(cnt) < n_target:
+            L = max(cnt, key=lambda k: (cnt[k], -k))
+            o = L // PIECES
+            if cnt[L] < 4 * cfg.min_area or used[o] + 1 >= PIECES:
+                break
+            sel = seg == L
+            p = pts[sel]
+            a, b = rng.integers(0, p.shape[0], 2)
+            if a == b:
+                b = (a + p.shape[0] // 2) % p.shape[0]
+            second = (p - p[int(b)]).square().sum(1) < (p - p[int(a)]).square().sum(1)
+            n2 = int(second.sum())
+            if n2 == 0 or n2 == p.shape[0]:
+                break
+            new = o * PIECES + used[o] + 1
+            used[o] += 1
+            idx = sel.nonzero()[:, 0]
+            seg[idx[second]] = new
+            cnt[new] = n2
+            cnt[L] -= n2
+        return seg
+
     def _hierarchical(self, masks, obj, ids, n_target):
         """X: add overlapping whole-object and half-segment masks (SAM 'everything')."""
         cfg = self.cfg
         extra = []
-        objs = torch.unique(ids // 8)
+        objs = torch.unique(ids // PIECES)
         for oi in objs.tolist():          # whole-object masks (unions of pieces)
             if len(extra) + masks.shape[0] >= n_target:
                 break
-            if int((ids // 8 == oi).sum()) > 1:
+            if int((ids // PIECES == oi).sum()) > 1:
                 extra.append((obj == oi).to(torch.uint8))
         level = 0
         while len(extra) + masks.shape[0] < n_target and level < 4:
