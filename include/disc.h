@@ -78,7 +78,18 @@ typedef struct {
                                /* falls back to direct inserts, never to an error)          */
   int32_t window;          /* frames per stage-1 batch in disc_integrate_frames, 1..32       */
   int32_t device;          /* CUDA ordinal                                                   */
-  /* sharding (reserved; must be 1 / 0 / NULL in this version) */
+  /* key-hash sharding: world_size = G shards; shard g owns the    */
+  /* voxel keys with (mix64(key) >> 40) mod G == g (memberships, hash slots, key lists) and a   */
+  /* replica of the instance table.  G = 1: unsharded (rank 0, nccl_unique_id NULL).            */
+  /* G > 1, nccl_unique_id == NULL: all G shards in this process on `device` (exchanges =       */
+  /*   device copies; rank must be 0; G <= 16); the caller passes the whole frame stream.       */
+  /* G > 1, nccl_unique_id = the 128 bytes of disc_nccl_unique_id() created by rank 0 and       */
+  /*   broadcast out of band: this process is shard `rank` of G (one GPU each, NCCL exchanges   */
+  /*   on the caller's stream).  Every rank calls the same sequence of integrate calls, each    */
+  /*   with the SAME number of its own frames: rank r's j-th frame is frame r + G j of the      */
+  /*   stream (windows of floor(window / G) frames per rank).  Reports are returned for the     */
+  /*   caller's own frames; the instance table is replicated and bit-identical to G = 1;       */
+  /*   disc_get_memberships returns this process's shards' keys.                                */
   int32_t world_size, rank;
   const void* nccl_unique_id;
 } disc_config;
@@ -149,6 +160,8 @@ typedef struct {                       /* timing of the dominant kernels (disc_s
   int64_t pairs, map_inserts, relabels; /* sum U, labels inserted, relabel items processed    */
   int64_t edges;                       /* sum of qualifying (s, j) edges                     */
   int64_t launches;                    /* kernels launched by integrate calls                */
+  int64_t shard_memberships[16];       /* live memberships held by each shard of this process */
+                                       /* (sharded map: the keys it owns; unsharded: [0] all) */
 } disc_stats;
 
 /* Fill *c with the defaults named above (capacities sized for a Replica-shaped stream). */
@@ -192,8 +205,7 @@ const char* disc_last_error(const disc_map* m);
 const char* disc_version(void);
 /* NCCL unique id for the key-sharded map: 128 bytes that rank 0 creates
  * and broadcasts out of band; every rank then passes it in disc_config.nccl_unique_id.  Loads
- * libnccl.so.2 at run time; DISC_ERR_NCCL if it is missing or fails.  (The sharded map itself is
- * NEXT: disc_map_create returns DISC_ERR_UNSUPPORTED for world_size > 1 this round.) */
+ * libnccl.so.2 at run time; DISC_ERR_NCCL if it is missing or fails. */
 disc_status disc_nccl_unique_id(uint8_t out[128]);
 
 #ifdef __cplusplus

@@ -67,6 +67,8 @@ struct disc_map {
   // export scratch
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
+  // key-hash-sharded map (world_size > 1): this handle drives the local shards (sub-maps)
+  struct ShardGroup* grp = nullptr;
 };
 
 namespace {
@@ -323,14 +325,17 @@ static std::string validate_config(const disc_config* c) {
   // <= 2^28: the voxel hash (2^29 slots) and the key-list arena (8 * 2^28 + 2^20 entries) stay
   // indexable by 32-bit slot numbers / list offsets below the U32_EMPTY sentinel
   if (c->max_memberships < 1 || c->max_memberships > (1ll << 28)) return "max_memberships in [1, 2^28]";
-  if (c->world_size != 1 || c->rank != 0) return "sharded maps are not supported by this build";
+  if (c->world_size != 1 || c->rank != 0) return "world_size / rank";   // (> 1: group_create)
   return "";
 }
+
+static disc_status group_create(const disc_config* cfg, disc_map** out);
+static void group_destroy(disc_map* m);
 
 disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   if (!cfg || !out) return DISC_ERR_INVALID;
   *out = nullptr;
-  if (cfg->world_size > 1) return DISC_ERR_UNSUPPORTED;   // key-sharded map: NEXT
+  if (cfg->world_size > 1) return group_create(cfg, out);   // key-hash-sharded map
   const std::string v = validate_config(cfg);
   if (!v.empty()) {
     std::fprintf(stderr, "disc_map_create: %s\n", v.c_str());
@@ -537,6 +542,7 @@ void disc_map_destroy(disc_map* m) {
   if (!m) return;
   cudaSetDevice(m->dev);
   cudaDeviceSynchronize();
+  group_destroy(m);
   for (void* p : m->allocs) cudaFree(p);
   if (m->h_err) cudaFreeHost(m->h_err);
   if (m->h_rep) cudaFreeHost(m->h_rep);
@@ -551,6 +557,363 @@ void disc_map_destroy(disc_map* m) {
   if (m->s1) cudaStreamDestroy(m->s1);
   if (m->s2) cudaStreamDestroy(m->s2);
   delete m;
+}
+
+// ==========================================================================================
+// Key-hash-sharded map.  G shards; shard g owns the voxel keys with
+// key_owner(key, G) == g (their memberships, hash slots and per-instance key lists) and a replica
+// of the instance table.  Per window: stage 1 frame-parallel (shard g runs window slots g + G j),
+// the detection records all-gathered, every kept (s, key) pair routed to its owner; per frame:
+// lookup on own keys -> X1 all-gather of the partial (s, label, count) triples, each shard adds
+// the others' into its count table (integer sums: identical on every shard) -> the association,
+// replicated (identical decisions) -> apply on own keys, instance updates on every replica ->
+// X2 all-reduce of the new memberships per target -> |V| and the report.
+//  * one process, G shards on one device (nccl_unique_id == NULL): the exchanges are device copies;
+//  * G processes (torchrun, one GPU each), one shard per rank: the exchanges are NCCL collectives
+//    (ncclAllGather / ncclAllReduce / grouped ncclSend + ncclRecv) on the caller's stream.
+// ==========================================================================================
+static disc_status ensure_stage(disc_map* m);
+static void stage_frame(disc_map* m, size_t& so, disc_frame& f, cudaStream_t st);
+
+struct NcclApi {
+  struct UniqueId { char internal[128]; };
+  void* lib = nullptr;
+  int (*init_rank)(void**, int, UniqueId, int) = nullptr;
+  int (*destroy)(void*) = nullptr;
+  int (*all_gather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+  int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*group_start)() = nullptr;
+  int (*group_end)() = nullptr;
+  const char* (*errstr)(int) = nullptr;
+  enum { U8 = 1, U32 = 3, I64 = 4, U64 = 5, SUM = 0 };
+  bool load() {
+    lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!lib) return false;
+    init_rank = (decltype(init_rank))dlsym(lib, "ncclCommInitRank");
+    destroy = (decltype(destroy))dlsym(lib, "ncclCommDestroy");
+    all_gather = (decltype(all_gather))dlsym(lib, "ncclAllGather");
+    all_reduce = (decltype(all_reduce))dlsym(lib, "ncclAllReduce");
+    send = (decltype(send))dlsym(lib, "ncclSend");
+    recv = (decltype(recv))dlsym(lib, "ncclRecv");
+    group_start = (decltype(group_start))dlsym(lib, "ncclGroupStart");
+    group_end = (decltype(group_end))dlsym(lib, "ncclGroupEnd");
+    errstr = (decltype(errstr))dlsym(lib, "ncclGetErrorString");
+    return init_rank && destroy && all_gather && all_reduce && send && recv && group_start && group_end;
+  }
+};
+
+struct ShardGroup {
+  int G = 1;          // shards in total
+  int L = 1;          // shards in this process (one process: G; NCCL: 1)
+  int rank = 0;       // NCCL rank (this process's shard = rank); 0 in one process
+  bool nccl = false;
+  std::vector<disc_map*> sh;   // local shards (complete single maps: state, window buffers, scratch)
+  DetLayout DL{1, 4, 0};
+  int nloc = 1;                // frames per shard per window
+  uint8_t* det_send = nullptr; // [nloc][REC] (NCCL)
+  uint8_t* det_all = nullptr;  // [G][nloc][REC]
+  uint32_t* trip_all = nullptr;
+  size_t trip_stride = 0;      // u32 per shard: 1 + 3 TCAP
+  int64_t* add_all = nullptr;  // [G][SMAX + 2]
+  size_t add_stride = 0;
+  FrameMeta* meta = nullptr;   // [window] (device)
+  FrameMeta* h_meta = nullptr; // pinned [window]
+  RouteDst* route = nullptr;   // device: local shards' stage-2 pair arrays
+  // NCCL pair all-to-all
+  NcclApi nc;
+  void* comm = nullptr;
+  PairRec* psend = nullptr;
+  PairRec* precv = nullptr;
+  size_t pcap = 0;
+  unsigned long long* pcnt = nullptr;   // [G] counts, then scatter cursors
+  unsigned long long* poff = nullptr;   // [G] send offsets
+  unsigned long long* pmat = nullptr;   // [G][G] count matrix (all-gathered)
+  unsigned long long* h_pmat = nullptr; // pinned [G][G]
+  disc_frame_report* h_rep = nullptr;   // pinned [window]
+};
+
+static disc_status group_fail_nccl(disc_map* m, int rc, const char* what) {
+  ShardGroup& Gp = *m->grp;
+  return fail(m, DISC_ERR_NCCL, std::string(what) + ": " + (Gp.nc.errstr ? Gp.nc.errstr(rc) : "nccl error"));
+}
+
+static void group_destroy(disc_map* m) {
+  ShardGroup* g = m->grp;
+  if (!g) return;
+  for (disc_map* s : g->sh) disc_map_destroy(s);
+  if (g->comm && g->nc.destroy) g->nc.destroy(g->comm);
+  if (g->h_meta) cudaFreeHost(g->h_meta);
+  if (g->h_pmat) cudaFreeHost(g->h_pmat);
+  if (g->h_rep) cudaFreeHost(g->h_rep);
+  delete g;
+  m->grp = nullptr;
+}
+
+static disc_status group_create(const disc_config* cfg, disc_map** out) {
+  const int G = cfg->world_size;
+  const bool nccl = cfg->nccl_unique_id != nullptr;
+  if (G < 2 || G > MAX_LOCAL_SHARDS * 64) return DISC_ERR_INVALID;
+  if (nccl ? (cfg->rank < 0 || cfg->rank >= G) : (cfg->rank != 0 || G > MAX_LOCAL_SHARDS)) return DISC_ERR_INVALID;
+  disc_config sc = *cfg;
+  sc.world_size = 1;
+  sc.rank = 0;
+  sc.nccl_unique_id = nullptr;
+  const std::string v = validate_config(&sc);
+  if (!v.empty()) {
+    std::fprintf(stderr, "disc_map_create: %s\n", v.c_str());
+    return DISC_ERR_INVALID;
+  }
+  disc_map* m = new disc_map();
+  m->cfg = *cfg;
+  m->dev = cfg->device;
+  m->grp = new ShardGroup();
+  ShardGroup& Gp = *m->grp;
+  Gp.G = G;
+  Gp.nccl = nccl;
+  Gp.L = nccl ? 1 : G;
+  Gp.rank = nccl ? cfg->rank : 0;
+  for (int l = 0; l < Gp.L; ++l) {
+    disc_map* s = nullptr;
+    const disc_status st = disc_map_create(&sc, &s);
+    if (st != DISC_OK) {
+      disc_map_destroy(m);
+      return st;
+    }
+    Gp.sh.push_back(s);
+  }
+  cudaSetDevice(cfg->device);
+  m->nsm = Gp.sh[0]->nsm;
+  const int SM = cfg->max_masks, Df = cfg->feat_dim, Dt = cfg->track_dim, win = cfg->window;
+  Gp.DL = DetLayout(SM, Df, Dt);
+  Gp.nloc = nccl ? std::max(1, win / G) : (win + G - 1) / G;
+  const size_t rec = Gp.DL.total;
+  bool ok = true;
+  auto chk = [&](void* p) { ok = ok && p; };
+  chk(Gp.det_all = dalloc<uint8_t>(m, (size_t)G * Gp.nloc * rec));
+  if (nccl) chk(Gp.det_send = dalloc<uint8_t>(m, (size_t)Gp.nloc * rec));
+  const int TCAP = Gp.sh[0]->X.TCAP;
+  Gp.trip_stride = 1 + 3 * (size_t)TCAP;
+  chk(Gp.trip_all = dalloc<uint32_t>(m, (size_t)G * Gp.trip_stride));
+  Gp.add_stride = (size_t)SM + 2;
+  chk(Gp.add_all = dalloc<int64_t>(m, (size_t)G * Gp.add_stride));
+  chk(Gp.meta = dalloc<FrameMeta>(m, (size_t)MAXWIN));
+  chk(Gp.route = dalloc<RouteDst>(m, 1));
+  if (cudaMallocHost(&Gp.h_meta, sizeof(FrameMeta) * MAXWIN) != cudaSuccess) ok = false;
+  if (cudaMallocHost(&Gp.h_rep, sizeof(disc_frame_report) * MAXWIN) != cudaSuccess) ok = false;
+  if (ok) {
+    RouteDst rd{};
+    for (int l = 0; l < Gp.L; ++l) {
+      const WinBufs& w = Gp.sh[l]->Wb[1];
+      rd.pkey[l] = w.pkey;
+      rd.pinfo[l] = w.pinfo;
+      rd.npairs[l] = w.npairs;
+    }
+    rd.PMAX = Gp.sh[0]->Wb[1].PMAX;
+    cudaMemcpy(Gp.route, &rd, sizeof(rd), cudaMemcpyHostToDevice);
+  }
+  if (ok && nccl) {
+    // pair all-to-all buffers: a rank's frames of one window hold at most nloc * PMAX pairs
+    Gp.pcap = (size_t)Gp.nloc * cfg->max_pairs_per_frame;
+    chk(Gp.psend = dalloc<PairRec>(m, Gp.pcap));
+    chk(Gp.precv = dalloc<PairRec>(m, Gp.pcap * G));
+    chk(Gp.pcnt = dalloc<unsigned long long>(m, G));
+    chk(Gp.poff = dalloc<unsigned long long>(m, G));
+    chk(Gp.pmat = dalloc<unsigned long long>(m, (size_t)G * G));
+    if (cudaMallocHost(&Gp.h_pmat, sizeof(unsigned long long) * G * G) != cudaSuccess) ok = false;
+    if (ok && !Gp.nc.load()) {
+      std::fprintf(stderr, "disc_map_create: libnccl.so.2 not loadable\n");
+      disc_map_destroy(m);
+      return DISC_ERR_NCCL;
+    }
+    if (ok) {
+      NcclApi::UniqueId id;
+      std::memcpy(id.internal, cfg->nccl_unique_id, 128);
+      const int rc = Gp.nc.init_rank(&Gp.comm, G, id, cfg->rank);
+      if (rc != 0) {
+        std::fprintf(stderr, "disc_map_create: ncclCommInitRank failed (%d)\n", rc);
+        disc_map_destroy(m);
+        return DISC_ERR_NCCL;
+      }
+    }
+  }
+  if (cudaEventCreateWithFlags(&m->ev_done, cudaEventDisableTiming) != cudaSuccess) ok = false;
+  cudaDeviceSynchronize();
+  if (!ok || cudaGetLastError() != cudaSuccess) {
+    std::fprintf(stderr, "disc_map_create: device allocation failed (sharded map)\n");
+    disc_map_destroy(m);
+    return DISC_ERR_CAPACITY;
+  }
+  *out = m;
+  return DISC_OK;
+}
+
+// surface device errors of every local shard (sticky)
+static disc_status group_sync(disc_map* m, cudaStream_t st) {
+  if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_check(m, "cudaStreamSynchronize");
+  for (disc_map* s : m->grp->sh) {
+    const disc_status r = sync_check(s, st);
+    if (r != DISC_OK) return fail(m, r, s->err);
+  }
+  return DISC_OK;
+}
+
+// n = frames of THIS caller (one process: the whole stream, window slot i = frame w0 + i, shard
+// g runs the slots i = g mod G; NCCL: this rank's frames, global slot rank + G j = its frame w0 + j)
+static disc_status group_integrate(disc_map* m, const disc_frame* frames, int32_t n, void* stream,
+                                   disc_frame_report* reports, bool host_inputs) {
+  if (!m || (!frames && n > 0) || n < 0) return DISC_ERR_INVALID;
+  if (m->sticky != DISC_OK) return m->sticky;
+  ShardGroup& Gp = *m->grp;
+  cudaSetDevice(m->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  m->last_stream = st;
+  for (int i = 0; i < n; ++i) {   // O0 over every frame before any mutation
+    const std::string v = validate_frame(m, frames[i], host_inputs);
+    if (!v.empty()) return fail(m, DISC_ERR_INVALID, "frame " + std::to_string(i) + ": " + v);
+  }
+  const int G = Gp.G, L = Gp.L, SM = m->cfg.max_masks, Df = m->cfg.feat_dim, Dt = m->cfg.track_dim;
+  const int per_call = Gp.nccl ? Gp.nloc : m->cfg.window;   // caller frames per window
+  for (int w0 = 0; w0 < n; w0 += per_call) {
+    const int nc = std::min(per_call, n - w0);
+    const int Wn = Gp.nccl ? G * nc : nc;   // window slots
+    bool sem = Gp.nccl;   // NCCL: the other ranks' frames may carry tokens; q = -1 marks those without
+    for (int i = 0; i < nc; ++i) sem = sem || frames[w0 + i].patch_feats != nullptr;
+    // ---- stage 1, frame-parallel: local shard l (global g) runs its window slots ----
+    for (int l = 0; l < L; ++l) {
+      disc_map* s = Gp.sh[l];
+      const int g = Gp.nccl ? Gp.rank : l;
+      if (host_inputs) {
+        const disc_status ss = ensure_stage(s);
+        if (ss != DISC_OK) return fail(m, ss, s->err);
+      }
+      WinDesc wd{};
+      wd.Df = Df;
+      wd.Dt = Dt;
+      int maxS = 1, maxP = 1;
+      size_t so = 0;
+      for (int j = 0;; ++j) {
+        const int ci = Gp.nccl ? j : g + G * j;   // caller frame index within the window
+        if (ci >= nc) break;
+        disc_frame f = frames[w0 + ci];
+        if (host_inputs) stage_frame(s, so, f, st);
+        wd.f[wd.n] = make_desc(f);
+        Gp.h_meta[wd.n] = FrameMeta{f.num_masks, 0, f.frame_id};
+        maxS = std::max(maxS, f.num_masks);
+        maxP = std::max(maxP, f.patch_h * f.patch_w);
+        m->stats.mask_bytes += (int64_t)f.height * f.width * f.num_masks;
+        m->stats.depth_bytes += (int64_t)f.height * f.width * 4;
+        m->stats.track_bytes += (int64_t)f.patch_h * f.patch_w * Dt * 2;
+        if (f.patch_feats) m->stats.feat_bytes += (int64_t)f.patch_h * f.patch_w * Df * 4;
+        wd.n++;
+      }
+      cudaMemsetAsync(s->Wb[1].npairs, 0, sizeof(uint32_t) * MAXWIN, st);
+      if (wd.n > 0) {
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (m->timing && l == 0) { e0 = ev_get(m); e1 = ev_get(m); }
+        m->stats.launches += launch_stage1(wd, s->Wb[0], s->P, s->d_err, sem, maxS, 1, 1, 1, maxP, 4, s->nsm, 0, st,
+                                           e0, e1);
+        if (e0) m->ev_pending.push_back({e0, e1, 0});
+        uint8_t* dst = Gp.nccl ? Gp.det_send : Gp.det_all + (size_t)g * Gp.nloc * Gp.DL.total;
+        launch_det_pack(s->Wb[0], wd.n, Gp.h_meta, dst, Gp.DL, Df, Dt, sem, st);
+      }
+      // (the pinned meta is read at launch: kernel arguments are copied by value)
+    }
+    // ---- stage-1 exchange: detection records to every shard, pairs to their owners ----
+    if (Gp.nccl) {
+      int rc = Gp.nc.all_gather(Gp.det_send, Gp.det_all, (size_t)Gp.nloc * Gp.DL.total, NcclApi::U8, Gp.comm, st);
+      if (rc) return group_fail_nccl(m, rc, "ncclAllGather(detections)");
+      disc_map* s = Gp.sh[0];
+      cudaMemsetAsync(Gp.pcnt, 0, sizeof(unsigned long long) * G, st);
+      launch_pair_route(s->Wb[0], nc, Gp.rank, G, nullptr, Gp.pcnt, nullptr, nullptr, s->d_err, st);
+      rc = Gp.nc.all_gather(Gp.pcnt, Gp.pmat, G, NcclApi::U64, Gp.comm, st);
+      if (rc) return group_fail_nccl(m, rc, "ncclAllGather(pair counts)");
+      cudaMemcpyAsync(Gp.h_pmat, Gp.pmat, sizeof(unsigned long long) * G * G, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);   // the all-to-all sizes (one host round trip per window)
+      std::vector<unsigned long long> off(G), roff(G + 1, 0);
+      unsigned long long o = 0;
+      for (int d = 0; d < G; ++d) { off[d] = o; o += Gp.h_pmat[(size_t)Gp.rank * G + d]; }
+      for (int r = 0; r < G; ++r) roff[r + 1] = roff[r] + Gp.h_pmat[(size_t)r * G + Gp.rank];
+      if (o > Gp.pcap || roff[G] > Gp.pcap * G) return fail(m, DISC_ERR_CAPACITY, "pair exchange buffer full");
+      cudaMemcpyAsync(Gp.poff, off.data(), sizeof(unsigned long long) * G, cudaMemcpyHostToDevice, st);
+      cudaMemsetAsync(Gp.pcnt, 0, sizeof(unsigned long long) * G, st);
+      launch_pair_route(s->Wb[0], nc, Gp.rank, G, nullptr, Gp.pcnt, Gp.poff, Gp.psend, s->d_err, st);
+      Gp.nc.group_start();
+      for (int r = 0; r < G; ++r) {
+        const unsigned long long ns = Gp.h_pmat[(size_t)Gp.rank * G + r], nr = Gp.h_pmat[(size_t)r * G + Gp.rank];
+        if (ns) Gp.nc.send(Gp.psend + off[r], ns * sizeof(PairRec), NcclApi::U8, r, Gp.comm, st);
+        if (nr) Gp.nc.recv(Gp.precv + roff[r], nr * sizeof(PairRec), NcclApi::U8, r, Gp.comm, st);
+      }
+      rc = Gp.nc.group_end();
+      if (rc) return group_fail_nccl(m, rc, "ncclSend/ncclRecv(pairs)");
+      launch_pair_deliver(Gp.precv, roff[G], s->Wb[1], s->d_err, st);
+    } else {
+      for (int l = 0; l < L; ++l) {
+        const int nown = (nc - l + G - 1) / G;
+        launch_pair_route(Gp.sh[l]->Wb[0], nown, l, G, Gp.route, nullptr, nullptr, nullptr, Gp.sh[l]->d_err, st);
+      }
+    }
+    for (int l = 0; l < L; ++l)
+      launch_det_unpack(Gp.det_all, Wn, G, Gp.nloc, Gp.DL, Gp.sh[l]->Wb[1], Gp.meta, Df, Dt, sem, st);
+    // ---- stage 2, frame after frame, with the two exchanges ----
+    cudaEvent_t t1b = nullptr, t2 = nullptr;
+    if (m->timing) { t1b = ev_get(m); t2 = ev_get(m); cudaEventRecord(t1b, st); }
+    const int grid = m->nsm;
+    for (int i = 0; i < Wn; ++i) {
+      for (int l = 0; l < L; ++l) {
+        disc_map* s = Gp.sh[l];
+        launch_stage2_sharded_frame(0, i, Gp.meta, s->Wb[1], s->M, s->X, s->P, sem, grid, st);
+        const int g = Gp.nccl ? Gp.rank : l;
+        launch_trip_pack(s->X, Gp.trip_all + (size_t)g * Gp.trip_stride, s->X.TCAP, s->d_err, st);
+      }
+      if (Gp.nccl) {
+        const int rc = Gp.nc.all_gather(Gp.trip_all + (size_t)Gp.rank * Gp.trip_stride, Gp.trip_all, Gp.trip_stride,
+                                        NcclApi::U32, Gp.comm, st);
+        if (rc) return group_fail_nccl(m, rc, "ncclAllGather(triples)");
+      }
+      for (int l = 0; l < L; ++l) {
+        disc_map* s = Gp.sh[l];
+        launch_trip_merge(s->X, Gp.trip_all, Gp.trip_stride, G, Gp.nccl ? Gp.rank : l, s->d_err, st);
+        launch_stage2_sharded_frame(1, i, Gp.meta, s->Wb[1], s->M, s->X, s->P, sem, grid, st);
+        launch_stage2_sharded_frame(2, i, Gp.meta, s->Wb[1], s->M, s->X, s->P, sem, grid, st);
+        launch_add_pack(s->M, s->X, Gp.add_all + (size_t)(Gp.nccl ? 0 : l) * Gp.add_stride, SM, st);
+      }
+      int parts = G;
+      if (Gp.nccl) {
+        const int rc = Gp.nc.all_reduce(Gp.add_all, Gp.add_all, Gp.add_stride, NcclApi::I64, NcclApi::SUM, Gp.comm, st);
+        if (rc) return group_fail_nccl(m, rc, "ncclAllReduce(new memberships)");
+        parts = 1;
+      }
+      for (int l = 0; l < L; ++l)
+        launch_finalize_sum(i, Gp.sh[l]->M, Gp.sh[l]->X, Gp.add_all, parts, Gp.add_stride, SM, st);
+      m->stats.launches += 5 * L;
+    }
+    if (t2) {
+      cudaEventRecord(t2, st);
+      m->ev_pending.push_back({t1b, t2, 2});
+    }
+    m->stats.frames += Wn;
+    disc_status cs = cuda_check(m, "sharded integrate launch");
+    if (cs != DISC_OK) return cs;
+    // last-frame bookkeeping of every local shard (debug export)
+    cudaMemcpyAsync(Gp.h_meta, Gp.meta, sizeof(FrameMeta) * Wn, cudaMemcpyDeviceToHost, st);
+    if (reports) cudaMemcpyAsync(Gp.h_rep, Gp.sh[0]->X.rep, sizeof(disc_frame_report) * Wn, cudaMemcpyDeviceToHost, st);
+    const disc_status ss = group_sync(m, st);
+    if (ss != DISC_OK) return ss;
+    if (reports)
+      for (int j = 0; j < nc; ++j) reports[w0 + j] = Gp.h_rep[Gp.nccl ? Gp.rank + G * j : j];
+    for (disc_map* s : Gp.sh) {
+      s->have_last = true;
+      s->last_buf = 1;
+      s->last_f = Wn - 1;
+      s->last_fd = FrameDesc{};
+      s->last_fd.S = Gp.h_meta[Wn - 1].S;
+      s->last_stream = st;
+    }
+  }
+  cudaEventRecord(m->ev_done, st);   // disc_wait orders other streams after the map's work
+  return cuda_check(m, "sharded integrate");
 }
 
 // SMs for stage 2 in the next window: the base split plus, when the stream's frames carry many
@@ -576,6 +939,40 @@ static int stage2_reserve(disc_map* m, bool sem) {
   return std::min(base + extra, m->nsm / 2);
 }
 
+// host-input staging: one window of frames' inputs (pinned host -> device, stream-ordered)
+static disc_status ensure_stage(disc_map* m) {
+  if (m->stage) return DISC_OK;
+  const disc_config& c = m->cfg;
+  m->stage_bytes = (size_t)c.window * ((size_t)c.max_pixels * (4 + c.max_masks) + (size_t)c.max_masks * 4 + 256 +
+                                       (size_t)c.max_patches * ((size_t)c.feat_dim * 4 + (size_t)c.track_dim * 2) +
+                                       (size_t)c.feat_dim * 4 + 4096);
+  if (cudaMalloc((void**)&m->stage, m->stage_bytes) != cudaSuccess) {
+    cudaGetLastError();
+    m->stage = nullptr;
+    return fail(m, DISC_ERR_CAPACITY, "cannot allocate host-input staging buffers");
+  }
+  return DISC_OK;
+}
+
+static void stage_frame(disc_map* m, size_t& so, disc_frame& f, cudaStream_t st) {
+  const int Df = m->cfg.feat_dim, Dt = m->cfg.track_dim;
+  auto put = [&](const void* src, size_t bytes) -> const void* {
+    if (!src || !bytes) return nullptr;
+    so = (so + 255) & ~(size_t)255;
+    void* dst = m->stage + so;
+    cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+    so += bytes;
+    return dst;
+  };
+  const size_t HW = (size_t)f.height * f.width, Pn = (size_t)f.patch_h * f.patch_w;
+  f.depth = (const float*)put(f.depth, HW * 4);
+  f.masks = (const uint8_t*)put(f.masks, HW * f.num_masks);
+  f.mask_conf = (const float*)put(f.mask_conf, (size_t)f.num_masks * 4);
+  f.patch_feats = (const float*)put(f.patch_feats, Pn * Df * 4);
+  f.global_embed = (const float*)put(f.global_embed, (size_t)Df * 4);
+  f.track_feats = (const uint16_t*)put(f.track_feats, Dt > 0 ? Pn * Dt * 2 : 0);
+}
+
 static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t n, void* stream,
                                   disc_frame_report* reports, bool host_inputs) {
   if (!m || (!frames && n > 0) || n < 0) return DISC_ERR_INVALID;
@@ -591,14 +988,9 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
   const disc_config& c = m->cfg;
   const int win = c.window;
   const int Df = c.feat_dim, Dt = c.track_dim;
-  if (host_inputs && !m->stage) {
-    m->stage_bytes = (size_t)win * ((size_t)c.max_pixels * (4 + c.max_masks) + (size_t)c.max_masks * 4 + 256 +
-                                    (size_t)c.max_patches * ((size_t)Df * 4 + (size_t)Dt * 2) + (size_t)Df * 4 + 4096);
-    if (cudaMalloc((void**)&m->stage, m->stage_bytes) != cudaSuccess) {
-      cudaGetLastError();
-      m->stage = nullptr;
-      return fail(m, DISC_ERR_CAPACITY, "cannot allocate host-input staging buffers");
-    }
+  if (host_inputs) {
+    const disc_status ss = ensure_stage(m);
+    if (ss != DISC_OK) return ss;
   }
   // stream-ordered after the caller's prior work on `st`; stage 1 on s1, stage 2 on s2
   cudaEventRecord(m->ev_in, st);
@@ -620,23 +1012,7 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
     size_t so = 0;
     for (int i = 0; i < nw; ++i) {
       disc_frame f = frames[w0 + i];
-      if (host_inputs) {   // copy this frame's inputs to device staging (stream-ordered)
-        auto put = [&](const void* src, size_t bytes) -> const void* {
-          if (!src || !bytes) return nullptr;
-          so = (so + 255) & ~(size_t)255;
-          void* dst = m->stage + so;
-          cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s1);
-          so += bytes;
-          return dst;
-        };
-        const size_t HW = (size_t)f.height * f.width, Pn = (size_t)f.patch_h * f.patch_w;
-        f.depth = (const float*)put(f.depth, HW * 4);
-        f.masks = (const uint8_t*)put(f.masks, HW * f.num_masks);
-        f.mask_conf = (const float*)put(f.mask_conf, (size_t)f.num_masks * 4);
-        f.patch_feats = (const float*)put(f.patch_feats, Pn * Df * 4);
-        f.global_embed = (const float*)put(f.global_embed, (size_t)Df * 4);
-        f.track_feats = (const uint16_t*)put(f.track_feats, Dt > 0 ? Pn * Dt * 2 : 0);
-      }
+      if (host_inputs) stage_frame(m, so, f, s1);   // this frame's inputs to device staging
       wd.f[i] = make_desc(f);
       maxS = std::max(maxS, f.num_masks);
       maxHp = std::max(maxHp, f.patch_h);
@@ -702,17 +1078,20 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
 }
 
 disc_status disc_integrate_frame(disc_map* m, const disc_frame* f, void* stream, disc_frame_report* report) {
+  if (m && m->grp) return group_integrate(m, f, 1, stream, report, false);
   return integrate_impl(m, f, 1, stream, report, false);
 }
 
 disc_status disc_integrate_frames(disc_map* m, const disc_frame* f, int32_t n, void* stream,
                                   disc_frame_report* report) {
+  if (m && m->grp) return group_integrate(m, f, n, stream, report, false);
   return integrate_impl(m, f, n, stream, report, false);
 }
 
 disc_status disc_integrate_frames_host(disc_map* m, const disc_frame* f, int32_t n, void* stream,
                                        disc_frame_report* report) {
   if (!m || (!f && n > 0) || n < 0) return DISC_ERR_INVALID;
+  if (m->grp) return group_integrate(m, f, n, stream, report, true);
   if (m->sticky != DISC_OK) return m->sticky;
   // O0 over ALL n frames before the first window mutates the map (disc.h: INVALID = nothing changed)
   for (int i = 0; i < n; ++i) {
@@ -760,6 +1139,7 @@ disc_status disc_sync(disc_map* m) {
   if (!m) return DISC_ERR_INVALID;
   if (m->sticky != DISC_OK) return m->sticky;
   cudaSetDevice(m->dev);
+  if (m->grp) return group_sync(m, m->last_stream);
   if (m->s1) cudaStreamSynchronize(m->s1);
   if (m->s2) cudaStreamSynchronize(m->s2);
   tl_dump();
@@ -768,6 +1148,10 @@ disc_status disc_sync(disc_map* m) {
 
 disc_status disc_query(disc_map* m, const float* q, int32_t k, int64_t* ids, float* scores, int32_t* n_out) {
   if (!m || !q || k < 0 || (k > 0 && (!ids || !scores)) || !n_out) return DISC_ERR_INVALID;
+  if (m->grp) {   // the instance table is replicated: shard 0 answers
+    const disc_status gs = disc_sync(m);
+    return gs != DISC_OK ? gs : disc_query(m->grp->sh[0], q, k, ids, scores, n_out);
+  }
   disc_status s = disc_sync(m);
   if (s != DISC_OK) return s;
   const int64_t nid = host_next_id(m);
@@ -782,6 +1166,10 @@ disc_status disc_query(disc_map* m, const float* q, int32_t k, int64_t* ids, flo
 disc_status disc_get_instances(disc_map* m, disc_instance* out, float* embeds, double* track, int32_t cap,
                                int32_t* n_out) {
   if (!m || !n_out) return DISC_ERR_INVALID;
+  if (m->grp) {   // replicated instance table (|V| summed over the shards' keys every frame)
+    const disc_status gs = disc_sync(m);
+    return gs != DISC_OK ? gs : disc_get_instances(m->grp->sh[0], out, embeds, track, cap, n_out);
+  }
   disc_status s = disc_sync(m);
   if (s != DISC_OK) return s;
   const int64_t nid = host_next_id(m);
@@ -799,6 +1187,20 @@ disc_status disc_get_instances(disc_map* m, disc_instance* out, float* embeds, d
 
 disc_status disc_get_memberships(disc_map* m, uint64_t* keys, int64_t* ids, int64_t cap, int64_t* n_out) {
   if (!m || !n_out || (keys && !ids)) return DISC_ERR_INVALID;
+  if (m->grp) {   // the shards' key sets are disjoint: the union is their concatenation (this process's shards)
+    disc_status gs = disc_sync(m);
+    if (gs != DISC_OK) return gs;
+    int64_t tot = 0;
+    for (disc_map* sh : m->grp->sh) {
+      int64_t k = 0;
+      gs = disc_get_memberships(sh, keys ? keys + tot : nullptr, keys ? ids + tot : nullptr,
+                                keys ? std::max<int64_t>(0, cap - tot) : 0, &k);
+      if (gs != DISC_OK) return fail(m, gs, sh->err);
+      tot += k;
+    }
+    *n_out = tot;
+    return DISC_OK;
+  }
   disc_status s = disc_sync(m);
   if (s != DISC_OK) return s;
   const size_t need = (size_t)(keys ? cap : 0) * 16 + (1 << 20);
@@ -812,6 +1214,26 @@ disc_status disc_get_memberships(disc_map* m, uint64_t* keys, int64_t* ids, int6
 
 disc_status disc_debug_last_frame(disc_map* m, disc_frame_debug* d) {
   if (!m || !d) return DISC_ERR_INVALID;
+  if (m->grp) {   // replicated records and (merged) triples; each shard's share of the pairs
+    disc_status gs = disc_sync(m);
+    if (gs != DISC_OK) return gs;
+    int64_t k = 0;
+    for (disc_map* sh : m->grp->sh) {
+      disc_frame_debug dl = *d;
+      if (d->pair_s) {
+        dl.pair_s = d->pair_s + std::min(k, d->pair_cap);
+        dl.pair_key = d->pair_key + std::min(k, d->pair_cap);
+        dl.pair_cap = std::max<int64_t>(0, d->pair_cap - k);
+      }
+      gs = disc_debug_last_frame(sh, &dl);
+      if (gs != DISC_OK) return fail(m, gs, sh->err);
+      k += dl.n_pairs;
+      d->num_masks = dl.num_masks;
+      d->n_trip = dl.n_trip;
+    }
+    d->n_pairs = k;
+    return DISC_OK;
+  }
   disc_status s = disc_sync(m);
   if (s != DISC_OK) return s;
   if (!m->have_last) return fail(m, DISC_ERR_INVALID, "no frame integrated yet");
@@ -886,6 +1308,19 @@ disc_status disc_get_stats(disc_map* m, disc_stats* s) {
   disc_status st = disc_sync(m);
   if (st != DISC_OK) return st;
   collect_events(m);
+  if (m->grp) {   // U and edges are replicated; inserts / relabel items are per shard (own keys)
+    m->stats.pairs = m->stats.map_inserts = m->stats.relabels = m->stats.edges = 0;
+    for (size_t l = 0; l < m->grp->sh.size(); ++l) {
+      int64_t ctr[8];
+      cudaMemcpy(ctr, m->grp->sh[l]->M.counters, sizeof(ctr), cudaMemcpyDeviceToHost);
+      if (l == 0) { m->stats.pairs = ctr[4]; m->stats.edges = ctr[7]; }
+      m->stats.map_inserts += ctr[5];
+      m->stats.relabels += ctr[6];
+      if (l < 16) m->stats.shard_memberships[l] = ctr[2];   // own keys' live memberships
+    }
+    *s = m->stats;
+    return cuda_check(m, "disc_get_stats");
+  }
   if (getenv("DISC_K6PROF") || getenv("DISC_S2PROF")) k6_prof_dump();
   int64_t ctr[8];
   cudaMemcpy(ctr, m->M.counters, sizeof(ctr), cudaMemcpyDeviceToHost);
@@ -893,6 +1328,7 @@ disc_status disc_get_stats(disc_map* m, disc_stats* s) {
   m->stats.map_inserts = ctr[5];
   m->stats.relabels = ctr[6];
   m->stats.edges = ctr[7];
+  m->stats.shard_memberships[0] = ctr[2];
   *s = m->stats;
   return cuda_check(m, "disc_get_stats");
 }

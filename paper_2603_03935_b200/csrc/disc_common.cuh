@@ -208,6 +208,14 @@ struct FrameScratch {
   uint32_t* ntrip_last;          // [1] (debug export)
 };
 
+// per window slot: the frame's mask count and id (the sharded map's stage-2 kernels read them from
+// device memory: a rank holds the inputs of its own frames only)
+struct FrameMeta {
+  int32_t S;
+  int32_t pad;
+  int64_t frame_id;
+};
+
 // ---- helpers -------------------------------------------------------------------------
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x ^= x >> 30;
@@ -224,6 +232,11 @@ __host__ __device__ __forceinline__ uint32_t mix32(uint32_t x) {
   x *= 0x846ca68bu;
   x ^= x >> 16;
   return x;
+}
+// owning shard of a voxel key in a G-way key-hash-sharded map: high hash bits, so
+// ownership is independent of the slot position (low bits) inside the owner's hash table
+__host__ __device__ __forceinline__ uint32_t key_owner(uint64_t key, uint32_t G) {
+  return (uint32_t)((mix64(key) >> 40) % (uint64_t)G);
 }
 __device__ __forceinline__ uint64_t pack_key(int ix, int iy, int iz) {
   return ((uint64_t)(uint32_t)(ix + KEY_BIAS) << 42) | ((uint64_t)(uint32_t)(iy + KEY_BIAS) << 21) |

@@ -1530,6 +1530,138 @@ __global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// The key-hash-sharded map: the same three phases as k_stage2, one
+// kernel each per frame and shard, so that the shards' partial results can be exchanged between
+// them (kernel boundaries are the barriers; the exchange is NCCL across processes or device copies
+// between the shards of one process).  Shard g holds the memberships of the keys it owns
+// (owner = key_owner(key, G)) and a replica of the instance table, which every shard updates
+// identically from identical (exchanged) inputs.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ FrameDesc meta_desc(const FrameMeta* meta, int f) {
+  FrameDesc F{};
+  F.S = meta[f].S;
+  F.frame_id = meta[f].frame_id;
+  return F;
+}
+
+__global__ void __launch_bounds__(K6_THREADS, 1) k_s2_lookup(int f, WinBufs wb, MapState M, FrameScratch X, Params P) {
+  s2_lookup(f, wb, M, X, P.Dt);
+}
+
+// X1 send side: this shard's partial (s, physical label, count) triples of frame f
+__global__ void __launch_bounds__(512) k_trip_pack(FrameScratch X, uint32_t* out, int cap, int* err) {
+  const uint32_t n = __ldcg(X.ntrip);
+  if (n > (uint32_t)cap) {
+    if (threadIdx.x == 0) { raise_err(err, DERR_TRIPLES); out[0] = 0; }
+    return;
+  }
+  if (threadIdx.x == 0) out[0] = n;
+  for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) {
+    out[1 + 3 * t] = X.trip_s[t];
+    out[2 + 3 * t] = X.trip_j[t];
+    out[3 + 3 * t] = X.ctab_cnt[X.ctab_idx[t]];
+  }
+}
+
+// X1 receive side: the other shards' partial triples added into this shard's count table (integer
+// sums: every shard ends with the same (s, j) -> c_sj set, in any order)
+__global__ void __launch_bounds__(256) k_trip_merge(FrameScratch X, const uint32_t* all, size_t stride, int G, int self,
+                                                    int* err) {
+  for (int g = 0; g < G; ++g) {
+    if (g == self) continue;
+    const uint32_t* b = all + (size_t)g * stride;
+    const uint32_t n = b[0];
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+      count_add(X, ((uint64_t)b[1 + 3 * t] << 32) | b[2 + 3 * t], b[3 + 3 * t], err);
+  }
+}
+
+__global__ void __launch_bounds__(K6_THREADS, 1) k_s2_assoc(int f, const FrameMeta* meta, WinBufs wb, MapState M,
+                                                            FrameScratch X, Params P, int sem) {
+  const FrameDesc F = meta_desc(meta, f);
+  s2_assoc(f, F, wb, M, X, P, sem);   // one CTA: it evaluates the visual gate of its candidates itself
+}
+
+__global__ void __launch_bounds__(K6_THREADS, 1) k_s2_apply(int f, const FrameMeta* meta, WinBufs wb, MapState M,
+                                                            FrameScratch X, Params P, int sem) {
+  const FrameDesc F = meta_desc(meta, f);
+  s2_apply(f, F, wb, M, X, P, sem);
+}
+
+// X2 send side: this shard's new memberships per target (own keys), its live count and the live
+// count the association saw (report fields)
+__global__ void k_add_pack(MapState M, FrameScratch X, int64_t* out, int smax) {
+  const int ntgt = *X.ntgt;
+  for (int t = threadIdx.x; t < smax; t += blockDim.x) out[t] = t < ntgt ? (int64_t)X.tgt_stage[t] : 0;
+  if (threadIdx.x == 0) {
+    out[smax] = M.counters[2];
+    out[smax + 1] = *X.live_before;
+  }
+}
+
+// K7 tail with the SUMMED adds: |V_root| grows by every shard's new memberships; the key lists
+// (own keys) by this shard's
+__global__ void k_s2_finalize_sum(int f, MapState M, FrameScratch X, const int64_t* all, int parts, size_t stride,
+                                  int smax) {
+  const int ntgt = *X.ntgt;
+  auto sum = [&](int k) {   // fixed order over the shards' rows (integers: any order is exact)
+    int64_t v = 0;
+    for (int g = 0; g < parts; ++g) v += all[(size_t)g * stride + k];
+    return v;
+  };
+  if (threadIdx.x == 0) {
+    disc_frame_report& R = X.rep[f];
+    R.live_memberships = sum(smax);
+    R.new_memberships = sum(smax) - sum(smax + 1);
+  }
+  for (int t = threadIdx.x; t < ntgt; t += blockDim.x) {
+    const uint32_t add = X.tgt_stage[t];
+    M.lst_len[X.tgt_phys[t]] = X.tgt_base[t] + add;
+    M.vcount[X.tgt_root[t]] += sum(t);
+    if (add) atomicAdd((unsigned long long*)&M.counters[5], (unsigned long long)add);
+  }
+}
+
+void launch_stage2_sharded_frame(int phase, int f, const FrameMeta* meta, const WinBufs& wb, const MapState& M,
+                                 const FrameScratch& X, const Params& P, bool sem, int grid, cudaStream_t st) {
+  const size_t sm6 = k6_smem_bytes(wb.SMAX, X.TCS);
+  static size_t set_for = 0;
+  if (set_for != sm6) {
+    cudaFuncSetAttribute(k_s2_lookup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm6);
+    cudaFuncSetAttribute(k_s2_assoc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm6);
+    cudaFuncSetAttribute(k_s2_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm6);
+    set_for = sm6;
+  }
+  const int semi = sem ? 1 : 0;
+  if (phase == 0) k_s2_lookup<<<grid, K6_THREADS, sm6, st>>>(f, wb, M, X, P);
+  else if (phase == 1) k_s2_assoc<<<1, K6_THREADS, sm6, st>>>(f, meta, wb, M, X, P, semi);
+  else k_s2_apply<<<grid, K6_THREADS, sm6, st>>>(f, meta, wb, M, X, P, semi);
+  debug_check(st, phase == 0 ? "k_s2_lookup" : phase == 1 ? "k_s2_assoc" : "k_s2_apply", f);
+}
+
+void launch_trip_pack(const FrameScratch& X, uint32_t* out, int cap, int* err, cudaStream_t st) {
+  k_trip_pack<<<1, 512, 0, st>>>(X, out, cap, err);
+  debug_check(st, "k_trip_pack", -1);
+}
+
+void launch_trip_merge(const FrameScratch& X, const uint32_t* all, size_t stride, int G, int self, int* err,
+                       cudaStream_t st) {
+  k_trip_merge<<<16, 256, 0, st>>>(X, all, stride, G, self, err);
+  debug_check(st, "k_trip_merge", -1);
+}
+
+void launch_add_pack(const MapState& M, const FrameScratch& X, int64_t* out, int smax, cudaStream_t st) {
+  k_add_pack<<<1, 256, 0, st>>>(M, X, out, smax);
+  debug_check(st, "k_add_pack", -1);
+}
+
+void launch_finalize_sum(int f, const MapState& M, const FrameScratch& X, const int64_t* all, int parts, size_t stride,
+                         int smax, cudaStream_t st) {
+  k_s2_finalize_sum<<<1, 256, 0, st>>>(f, M, X, all, parts, stride, smax);
+  debug_check(st, "k_s2_finalize_sum", f);
+}
+
 int launch_stage2(const WinDesc& wd, const WinBufs& wb, const MapState& M, const FrameScratch& X, const Params& P,
                   bool sem, int nsm, int nres, cudaStream_t st) {
   const size_t sm6 = k6_smem_bytes(wb.SMAX, X.TCS);

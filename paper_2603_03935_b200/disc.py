@@ -88,7 +88,7 @@ class disc_stats(C.Structure):
                 ("stage1_ms", C.c_double), ("stage2_ms", C.c_double), ("mask_bytes", C.c_int64),
                 ("depth_bytes", C.c_int64), ("track_bytes", C.c_int64), ("feat_bytes", C.c_int64),
                 ("pairs", C.c_int64), ("map_inserts", C.c_int64), ("relabels", C.c_int64),
-                ("edges", C.c_int64), ("launches", C.c_int64)]
+                ("edges", C.c_int64), ("launches", C.c_int64), ("shard_memberships", C.c_int64 * 16)]
 
 
 EXPORTS = {
@@ -158,7 +158,15 @@ class DiscMap:
     """A GPU-resident DISC map (libdisc).  Single writer per map."""
 
     def __init__(self, **cfg):
+        """cfg: disc_config fields.  world_size = G > 1 makes a key-hash-sharded map:
+        with nccl_unique_id = None all G shards live in this process (one device); with the 128-byte
+        id of nccl_unique_id() (rank 0's, broadcast) this process is shard `rank` of G (NCCL)."""
         import torch
+        uid = cfg.pop("nccl_unique_id", None)
+        self._uid = None
+        if uid is not None:
+            self._uid = (C.c_uint8 * 128)(*bytes(uid))
+            cfg["nccl_unique_id"] = C.cast(self._uid, C.c_void_p)
         self.cfg = default_config(**cfg)
         h = C.c_void_p()
         rc = lib().disc_map_create(C.byref(self.cfg), C.byref(h))
@@ -318,7 +326,9 @@ class DiscMap:
     def stats(self) -> dict:
         s = disc_stats()
         self._check(lib().disc_get_stats(self.h, C.byref(s)))
-        return {k: getattr(s, k) for k, _ in disc_stats._fields_}
+        out = {k: getattr(s, k) for k, _ in disc_stats._fields_}
+        out["shard_memberships"] = list(out["shard_memberships"])
+        return out
 
     def sync(self):
         self._check(lib().disc_sync(self.h))
