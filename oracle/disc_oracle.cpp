@@ -728,6 +728,130 @@ extern "C" int32_t ora_integrate(ora_map* m, const ora_frame* f, ora_report* rep
 }
 
 /* ------------------------------------------------------------------------------------ */
+/* finalize (NEXT f1): P:100 [§III-B] "a final, lightweight post-processing step iterates   */
+/* over the map to merge remaining orphaned candidates and filter out residual noisy        */
+/* instances, such as segments containing fewer than a minimum threshold of voxels";        */
+/* S:333-337 "all instance pairs meeting (tau_geo, tau_vis) merged to fixpoint ...; then     */
+/* every instance with |voxels| < min_voxels removed".  Readings:              */
+/*  R35 fixpoint = rounds of the snapshot union-find of R12 over INSTANCE pairs: each round */
+/*      tests every pair against the round-start map, merges each component into its min  */
+/*      id, and the rounds repeat until no pair qualifies;                                  */
+/*  R36 pair test = R10's c >= 1 and c >= tau_geo min(|V_i|, |V_j|) exactly in fp64, with  */
+/*      c = |V_i ∩ V_j|, and (Dt > 0) the gate (dot_pin(T_i,T_j) / sqrt(dot_pin(T_i,T_i)))  */
+/*      / sqrt(dot_pin(T_j,T_j)) >= tau_vis for i < j, a zero norm giving -2 (R15 pinned);  */
+/*  R37 merge = O12 without detections: V union, obs summed, last_seen = max, T summed in   */
+/*      ascending id order, (e, Q) replaced in ascending id order iff Q_j > Q (strict);     */
+/*  R38 the filter runs once, after the fixpoint; removed instances lose their memberships. */
+/* ------------------------------------------------------------------------------------ */
+extern "C" int32_t ora_finalize(ora_map* m, float tau_geo, float tau_vis, int64_t min_voxels,
+                                ora_final_report* rep) {
+  ora_final_report R{};
+  const int32_t Dt = m->cfg.track_dim;
+  while (true) {
+    /* pair counts c_ij = |V_i ∩ V_j| from the membership relation (every key's id set) */
+    std::map<std::pair<Id, Id>, int64_t> C;
+    for (const auto& kv : m->mem) {
+      const std::vector<Id> ids(kv.second.begin(), kv.second.end());  // ascending
+      for (size_t a = 0; a < ids.size(); ++a)
+        for (size_t b = a + 1; b < ids.size(); ++b) C[{ids[a], ids[b]}]++;
+    }
+    if (m->selfcheck) {  // brute force: std::set_intersection over every pair of instances
+      for (auto i = m->inst.begin(); i != m->inst.end(); ++i)
+        for (auto j = std::next(i); j != m->inst.end(); ++j) {
+          std::vector<Key> out;
+          std::set_intersection(i->second.V.begin(), i->second.V.end(), j->second.V.begin(),
+                                j->second.V.end(), std::back_inserter(out));
+          auto it = C.find({i->first, j->first});
+          if ((int64_t)out.size() != (it == C.end() ? 0 : it->second)) {
+            m->err = "selfcheck: finalize pair counts != set_intersection";
+            return ORA_SELFCHECK_FAILED;
+          }
+        }
+    }
+    /* R36 qualifying pairs */
+    std::map<Id, std::vector<Id>> adj;
+    int64_t nedge = 0;
+    for (const auto& kv : C) {
+      const Id i = kv.first.first, j = kv.first.second;
+      const Inst& A = m->inst.at(i);
+      const Inst& B = m->inst.at(j);
+      const int64_t c = kv.second;
+      const int64_t mn = std::min((int64_t)A.V.size(), (int64_t)B.V.size());
+      if (!(c >= 1 && (double)c >= (double)tau_geo * (double)mn)) continue;
+      if (Dt > 0) {
+        const double aa = ora_dot_pin(Dt, A.T.data(), A.T.data());
+        const double bb = ora_dot_pin(Dt, B.T.data(), B.T.data());
+        double cosv = -2.0;
+        if (aa > 0.0 && bb > 0.0) cosv = ora_dot_pin(Dt, A.T.data(), B.T.data()) / std::sqrt(aa) / std::sqrt(bb);
+        if (!(cosv >= (double)tau_vis)) continue;
+      }
+      adj[i].push_back(j);
+      adj[j].push_back(i);
+      nedge++;
+    }
+    if (nedge == 0) break;
+    R.rounds++;
+    R.edges += nedge;
+    /* components (BFS), each merged into its min id (R37) */
+    std::set<Id> seen;
+    std::vector<std::vector<Id>> comps;
+    for (const auto& kv : adj) {
+      if (seen.count(kv.first)) continue;
+      std::vector<Id> comp;
+      std::deque<Id> q{kv.first};
+      seen.insert(kv.first);
+      while (!q.empty()) {
+        const Id x = q.front();
+        q.pop_front();
+        comp.push_back(x);
+        for (Id y : adj[x])
+          if (!seen.count(y)) { seen.insert(y); q.push_back(y); }
+      }
+      std::sort(comp.begin(), comp.end());
+      comps.push_back(comp);
+    }
+    for (const auto& J : comps) {
+      const Id root = J.front();
+      Inst& Rt = m->inst.at(root);
+      for (size_t a = 1; a < J.size(); ++a) {
+        Inst& Ij = m->inst.at(J[a]);
+        R.relabeled += (int64_t)Ij.V.size();
+        Rt.V.insert(Ij.V.begin(), Ij.V.end());
+        Rt.obs += Ij.obs;
+        Rt.last_seen = std::max(Rt.last_seen, Ij.last_seen);
+        for (int32_t k = 0; k < Dt; ++k) Rt.T[k] = Rt.T[k] + Ij.T[k];
+        if (Ij.Q > Rt.Q) { Rt.Q = Ij.Q; Rt.e = Ij.e; }
+        for (Obs& o : Ij.accept) add_accept(Rt, o.q, o.e);
+        for (const Key& k : Ij.V) {
+          auto& ids = m->mem[k];
+          ids.erase(J[a]);
+          ids.insert(root);
+        }
+        m->inst.erase(J[a]);
+        R.merged_away++;
+      }
+    }
+  }
+  /* R38 the minimum-size filter */
+  std::vector<Id> drop;
+  for (const auto& kv : m->inst)
+    if ((int64_t)kv.second.V.size() < min_voxels) drop.push_back(kv.first);
+  for (Id id : drop) {
+    for (const Key& k : m->inst.at(id).V) {
+      auto it = m->mem.find(k);
+      it->second.erase(id);
+      if (it->second.empty()) m->mem.erase(it);
+    }
+    m->inst.erase(id);
+    R.removed++;
+  }
+  R.live_instances = (int64_t)m->inst.size();
+  for (const auto& kv : m->inst) R.live_memberships += (int64_t)kv.second.V.size();
+  if (rep) *rep = R;
+  return ORA_OK;
+}
+
+/* ------------------------------------------------------------------------------------ */
 /* export                                                                                */
 /* ------------------------------------------------------------------------------------ */
 

@@ -80,6 +80,18 @@ void     ora_set_selfcheck(ora_map* m, int32_t on);  /* brute-force cross-checks
 int32_t  ora_integrate(ora_map* m, const ora_frame* f, ora_report* rep);
 const char* ora_last_error(const ora_map* m);
 
+/* finalize (readings R35-R38): orphan merge to a fixpoint, then the minimum-
+   size filter.  Thresholds are explicit (pass the map's own tau_geo / tau_vis for SPEC's op). */
+typedef struct {
+  int64_t rounds;            /* union-find rounds that merged something                         */
+  int64_t edges;             /* qualifying instance pairs, summed over the rounds               */
+  int64_t merged_away;       /* instances erased by merges                                      */
+  int64_t relabeled;         /* sum of |V_j| over merged-away instances                         */
+  int64_t removed;           /* instances below min_voxels                                      */
+  int64_t live_instances, live_memberships;
+} ora_final_report;
+int32_t  ora_finalize(ora_map* m, float tau_geo, float tau_vis, int64_t min_voxels, ora_final_report* rep);
+
 /* ---- map state export ---- */
 int64_t ora_num_instances(const ora_map* m);
 /* ascending id; e [n][Df] (zeros if q == -1), T [n][Dt]; any pointer may be NULL */

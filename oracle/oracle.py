@@ -57,6 +57,14 @@ class OraReport(C.Structure):
         return {k: int(getattr(self, k)) for k, _ in REPORT_FIELDS}
 
 
+class OraFinalReport(C.Structure):
+    _fields_ = [(k, C.c_int64) for k in ["rounds", "edges", "merged_away", "relabeled", "removed", "live_instances",
+                                          "live_memberships"]]
+
+    def as_dict(self):
+        return {k: int(getattr(self, k)) for k, _ in self._fields_}
+
+
 def build() -> str:
     subprocess.run(["make", "-s", "-C", _HERE], check=True)
     return _LIB_PATH
@@ -90,6 +98,7 @@ def lib():
             "ora_s_size": (D, [I64, I32, I32, D]), "ora_s_angle": (D, [I64, P, P]),
             "ora_s_sem": (D, [I32, P, P]), "ora_s_dist": (D, [D]), "ora_quality": (D, [D, D, D, D]),
             "ora_dot_pin": (D, [I32, P, P]), "ora_query": (I64, [P, P, I32, P, P]),
+            "ora_finalize": (I32, [P, F, F, I64, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -224,6 +233,16 @@ class OracleMap:
         lib().ora_last_quality(self.h, _p(f6), _p(e), _p(u) if Dt else None, _p(t) if Dt else None)
         return dict(status=st, area=area, bbox=bbox, vs=vs, target=tgt, pair_s=ps, pair_key=pk,
                     trip_s=ts, trip_j=tj, trip_c=tc, trip_edge=te, factors=f6, e=e, u=u, t=t)
+
+    def finalize(self, tau_geo=None, tau_vis=None, min_voxels=0) -> dict:
+        """Orphan merge to a fixpoint + minimum-size filter (R35-R38)."""
+        rep = OraFinalReport()
+        tg = self.cfg.tau_geo if tau_geo is None else tau_geo
+        tv = self.cfg.tau_vis if tau_vis is None else tau_vis
+        rc = lib().ora_finalize(self.h, tg, tv, int(min_voxels), C.byref(rep))
+        if rc != 0:
+            raise RuntimeError(f"oracle finalize rc={rc}: {lib().ora_last_error(self.h).decode()}")
+        return rep.as_dict()
 
     def query(self, q, k: int):
         q = np.ascontiguousarray(q, np.float32)

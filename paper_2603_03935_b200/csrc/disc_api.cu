@@ -808,7 +808,7 @@ static disc_status group_integrate(disc_map* m, const disc_frame* frames, int32_
         if (f.patch_feats) m->stats.feat_bytes += (int64_t)f.patch_h * f.patch_w * Df * 4;
         wd.n++;
       }
-      cudaMemsetAsync(s->Wb[1].npairs, 0, sizeof(uint32_t) * MAXWIN, st);
+      cudaMemsetAsync(s->Wb[1].npairs, 0, sizeof(uint32_t) * m->cfg.window, st);
       if (wd.n > 0) {
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (m->timing && l == 0) { e0 = ev_get(m); e1 = ev_get(m); }
