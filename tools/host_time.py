@@ -5,7 +5,7 @@ from paper_2603_03935_b200 import DiscMap
 g = Generator("R", device="cuda:0"); c = g.cfg
 fr = [g.frame(f) for f in range(16 * 9)]
 torch.cuda.synchronize()
-m = DiscMap(**disc_config_kwargs(c), max_pixels=c.H*c.W, max_patches=c.Hp*c.Wp, max_masks=64, window=16,
+m = DiscMap(**disc_config_kwargs(c), max_pixels=c.H*c.W, max_patches=c.Hp*c.Wp, max_masks=96, window=16,
             max_memberships=1 << 23, max_instances=1 << 17, max_pairs_per_frame=1 << 17)
 m.integrate_frames(fr[:16]); m.sync()
 ts = []

@@ -13,7 +13,7 @@ c = g.cfg
 nw = int(os.environ.get("WINDOWS", "4"))
 fr = [g.frame(f) for f in range(16 * (nw + 1))]
 torch.cuda.synchronize()
-m = DiscMap(**disc_config_kwargs(c), max_pixels=c.H * c.W, max_patches=c.Hp * c.Wp, max_masks=64, window=16,
+m = DiscMap(**disc_config_kwargs(c), max_pixels=c.H * c.W, max_patches=c.Hp * c.Wp, max_masks=96, window=16,
             max_memberships=1 << 22, max_instances=1 << 16, max_pairs_per_frame=1 << 17)
 m.integrate_frames(fr[:16]); m.sync(); s0 = m.stats(); m.set_timing(True)
 for w in range(1, nw + 1):

@@ -13,7 +13,7 @@ cfg = os.environ.get("CFG", "R")
 nw = int(os.environ.get("WINDOWS", "32"))
 g = Generator(cfg, device="cuda:0")
 c = g.cfg
-m = DiscMap(**disc_config_kwargs(c), max_pixels=c.H * c.W, max_patches=c.Hp * c.Wp, max_masks=64, window=16,
+m = DiscMap(**disc_config_kwargs(c), max_pixels=c.H * c.W, max_patches=c.Hp * c.Wp, max_masks=96, window=16,
             max_memberships=1 << 23, max_instances=1 << 17,
             max_pairs_per_frame=int(os.environ.get("PMAX", 1 << 17)))
 for w in range(nw):

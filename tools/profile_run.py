@@ -19,7 +19,7 @@ g = Generator(a.config, device="cuda:0")
 c = g.cfg
 frames = [g.frame(f, with_feats=not a.m1) for f in range(a.windows * a.window)]
 torch.cuda.synchronize()
-m = DiscMap(**disc_config_kwargs(c), max_pixels=c.H * c.W, max_patches=c.Hp * c.Wp, max_masks=64, window=a.window,
+m = DiscMap(**disc_config_kwargs(c), max_pixels=c.H * c.W, max_patches=c.Hp * c.Wp, max_masks=96, window=a.window,
             max_memberships=1 << 22, max_instances=1 << 16,
             max_pairs_per_frame=a.pmax or (1 << 19 if a.config == "H" else 1 << 17))
 for w in range(a.windows):

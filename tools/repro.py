@@ -12,7 +12,7 @@ g = Generator(name, device="cuda:0")
 c = g.cfg
 frames = [g.frame(f) for f in range(n)]
 torch.cuda.synchronize()
-m = DiscMap(**disc_config_kwargs(c), max_pixels=c.H * c.W, max_patches=c.Hp * c.Wp, max_masks=64, window=win,
+m = DiscMap(**disc_config_kwargs(c), max_pixels=c.H * c.W, max_patches=c.Hp * c.Wp, max_masks=96, window=win,
             max_memberships=1 << 21, max_instances=1 << 14,
             max_pairs_per_frame=min(1 << 22, 2 * c.H * c.W))
 for w0 in range(0, n, win):

@@ -19,7 +19,7 @@ for cfg, nf in [("T", 3), (name, n)]:
     c = g.cfg
     frames = [g.frame(f) for f in range(nf)]
     torch.cuda.synchronize()
-    m = DiscMap(**disc_config_kwargs(c), max_pixels=c.H * c.W, max_patches=c.Hp * c.Wp, max_masks=64, window=win,
+    m = DiscMap(**disc_config_kwargs(c), max_pixels=c.H * c.W, max_patches=c.Hp * c.Wp, max_masks=96, window=win,
                 max_memberships=1 << 21, max_instances=1 << 14, max_pairs_per_frame=min(1 << 22, 2 * c.H * c.W))
     last = None
     for w0 in range(0, nf, win):

@@ -13,7 +13,7 @@ c = g.cfg
 nw = int(os.environ.get("WINDOWS", "6"))
 fr = [g.frame(f) for f in range(16 * nw)]
 torch.cuda.synchronize()
-m = DiscMap(**disc_config_kwargs(c), max_pixels=c.H * c.W, max_patches=c.Hp * c.Wp, max_masks=64, window=16,
+m = DiscMap(**disc_config_kwargs(c), max_pixels=c.H * c.W, max_patches=c.Hp * c.Wp, max_masks=96, window=16,
             max_memberships=1 << 22, max_instances=1 << 16, max_pairs_per_frame=1 << 17)
 for w in range(nw):
     m.integrate_frames(fr[16 * w:16 * (w + 1)])
