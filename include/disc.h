@@ -164,6 +164,15 @@ typedef struct {                       /* timing of the dominant kernels (disc_s
                                        /* (sharded map: the keys it owns; unsharded: [0] all) */
 } disc_stats;
 
+typedef struct {                       /* disc_finalize report                                */
+  int64_t rounds;                      /* union-find rounds that merged something (R35)      */
+  int64_t edges;                       /* qualifying instance pairs, summed over the rounds  */
+  int64_t merged_away;                 /* instances erased by merges                          */
+  int64_t relabeled;                   /* sum of |V_j| over merged-away instances j           */
+  int64_t removed;                     /* instances below min_voxels (R38)                    */
+  int64_t live_instances, live_memberships;
+} disc_final_report;
+
 /* Fill *c with the defaults named above (capacities sized for a Replica-shaped stream). */
 disc_status disc_config_init(disc_config* c);
 disc_status disc_map_create(const disc_config* cfg, disc_map** out);
@@ -197,6 +206,16 @@ disc_status disc_get_instances(disc_map* m, disc_instance* out, float* embeds, d
 disc_status disc_get_memberships(disc_map* m, uint64_t* keys, int64_t* ids, int64_t cap,
                                  int64_t* n_out);
 disc_status disc_debug_last_frame(disc_map* m, disc_frame_debug* d);
+/* End of trajectory (P:100 [§III-B]: "merge remaining orphaned candidates and filter out residual
+ * noisy instances, such as segments containing fewer than a minimum threshold of voxels";
+ * S:333-337; readings R35-R38): every pair of live instances (i < j) with c_ij = |V_i ∩ V_j| >= 1,
+ * c_ij >= tau_geo min(|V_i|, |V_j|) (exact) and, when Dt > 0, (dot_pin(T_i,T_j) / sqrt(dot_pin(T_i,T_i)))
+ * / sqrt(dot_pin(T_j,T_j)) >= tau_vis is an edge; components merge into their min id (T summed in
+ * ascending id order, (e, Q) replaced iff strictly higher in that order, obs summed, last_seen =
+ * max); repeated until no pair qualifies; then every instance with |V| < min_voxels is removed with
+ * its memberships.  Pass the map's own tau_geo / tau_vis for SPEC's finalize.  Synchronises; the
+ * map stays usable (integration may continue).  DISC_ERR_UNSUPPORTED on a sharded map. */
+disc_status disc_finalize(disc_map* m, float tau_geo, float tau_vis, int64_t min_voxels, disc_final_report* rep);
 disc_status disc_set_timing(disc_map* m, int32_t on);
 disc_status disc_get_stats(disc_map* m, disc_stats* s);
 disc_status disc_wait(disc_map* m, void* stream);  /* order `stream` after all queued map work */

@@ -1297,6 +1297,25 @@ disc_status disc_debug_last_frame(disc_map* m, disc_frame_debug* d) {
   return cuda_check(m, "disc_debug_last_frame");
 }
 
+disc_status disc_finalize(disc_map* m, float tau_geo, float tau_vis, int64_t min_voxels, disc_final_report* rep) {
+  if (!m || !(tau_geo > 0.0f && tau_geo <= 1.0f) || !(tau_vis >= -1.0f && tau_vis <= 1.0f) || min_voxels < 0)
+    return DISC_ERR_INVALID;
+  if (m->grp) return fail(m, DISC_ERR_UNSUPPORTED, "disc_finalize: sharded maps are not supported");
+  disc_status s = disc_sync(m);
+  if (s != DISC_OK) return s;
+  int64_t r[7] = {0, 0, 0, 0, 0, 0, 0};
+  if (run_finalize(m->M, m->cfg.feat_dim, m->cfg.track_dim, host_next_id(m), tau_geo, tau_vis, min_voxels, m->d_err,
+                   m->last_stream, r) != 0)
+    return fail(m, DISC_ERR_CAPACITY, "disc_finalize: cannot allocate its temporary buffers");
+  s = sync_check(m, m->last_stream);
+  if (s != DISC_OK) return s;
+  if (rep) {
+    rep->rounds = r[0]; rep->edges = r[1]; rep->merged_away = r[2]; rep->relabeled = r[3]; rep->removed = r[4];
+    rep->live_instances = r[5]; rep->live_memberships = r[6];
+  }
+  return cuda_check(m, "disc_finalize");
+}
+
 disc_status disc_set_timing(disc_map* m, int32_t on) {
   if (!m) return DISC_ERR_INVALID;
   m->timing = on != 0;

@@ -254,6 +254,27 @@ __device__ __forceinline__ void raise_err(int* err, int code) { atomicMax(err, c
     if (!(cond)) atomicCAS((err), 0, 1000 + __LINE__); \
   } while (0)
 
+// dot_pin with every load of the lane issued before the (unchanged) fma chain
+// R15 dot_pin, warp-cooperative (Dt <= 512): lane l accumulates d = l, l + 32, ... ascending with
+// fma, then the xor butterfly 16, 8, 4, 2, 1 -- the oracle's ora_dot_pin order.
+__device__ __forceinline__ double dot_pin_reg(const double* a, const double* b, int n) {
+  const int lane = threadIdx.x & 31;
+  double x[16], y[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int d = lane + 32 * i;
+    x[i] = d < n ? a[d] : 0.0;
+    y[i] = d < n ? b[d] : 0.0;
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    if (lane + 32 * i < n) acc = __fma_rn(x[i], y[i], acc);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+  return acc;
+}
+
 template <typename T>
 __device__ __forceinline__ T vload(const T* p) {
   return *(const volatile T*)p;

@@ -58,6 +58,10 @@ void launch_pair_route(const WinBufs& src, int n, int g, int G, const RouteDst* 
                        const unsigned long long* offsets, PairRec* send, int* err, cudaStream_t st);
 void launch_pair_deliver(const PairRec* recv, unsigned long long n, const WinBufs& dst, int* err, cudaStream_t st);
 
+// disc_finalize (k_final.cu): rep_out = rounds, edges, merged_away, relabeled, removed, live_instances,
+// live_memberships
+int run_finalize(const MapState& M, int Df, int Dt, int64_t next_id, float tau_geo, float tau_vis, int64_t min_voxels,
+                 int* err, cudaStream_t st, int64_t rep_out[7]);
 // export / query
 int64_t export_instances(const MapState& M, int Df, int Dt, int64_t next_id, disc_instance* out,
                          float* embeds, double* track, int32_t cap, cudaStream_t st, void* scratch,

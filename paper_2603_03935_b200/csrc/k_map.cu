@@ -365,25 +365,6 @@ __device__ __forceinline__ double dot_pin_w(const double* a, const double* b, in
   return acc;
 }
 
-// dot_pin with every load of the lane issued before the (unchanged) fma chain
-__device__ __forceinline__ double dot_pin_reg(const double* a, const double* b, int n) {
-  const int lane = threadIdx.x & 31;
-  double x[16], y[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int d = lane + 32 * i;
-    x[i] = d < n ? a[d] : 0.0;
-    y[i] = d < n ? b[d] : 0.0;
-  }
-  double acc = 0.0;
-#pragma unroll
-  for (int i = 0; i < 16; ++i)
-    if (lane + 32 * i < n) acc = __fma_rn(x[i], y[i], acc);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
-  return acc;
-}
-
 struct K6Smem {   // offsets into dynamic shared memory
   size_t t_s, t_j, t_c, t_e, t_jl, lab, jnode, comp_root, comp_best, comp_tgt, has_edge, d_st, d_vs, d_tgt, d_q,
       tg_root, tg_phys, j_vc, j_ph, j_obs, j_q, j_lo, j_ll, j_lc, total;

@@ -91,6 +91,14 @@ class disc_stats(C.Structure):
                 ("edges", C.c_int64), ("launches", C.c_int64), ("shard_memberships", C.c_int64 * 16)]
 
 
+class disc_final_report(C.Structure):
+    _fields_ = [(k, C.c_int64) for k in ["rounds", "edges", "merged_away", "relabeled", "removed", "live_instances",
+                                          "live_memberships"]]
+
+    def as_dict(self):
+        return {k: int(getattr(self, k)) for k, _ in self._fields_}
+
+
 EXPORTS = {
     "disc_config_init": (C.c_int, [C.c_void_p]),
     "disc_map_create": (C.c_int, [C.c_void_p, C.c_void_p]),
@@ -103,6 +111,7 @@ EXPORTS = {
     "disc_get_memberships": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "disc_debug_last_frame": (C.c_int, [C.c_void_p, C.c_void_p]),
     "disc_set_timing": (C.c_int, [C.c_void_p, C.c_int32]),
+    "disc_finalize": (C.c_int, [C.c_void_p, C.c_float, C.c_float, C.c_int64, C.c_void_p]),
     "disc_get_stats": (C.c_int, [C.c_void_p, C.c_void_p]),
     "disc_wait": (C.c_int, [C.c_void_p, C.c_void_p]),
     "disc_sync": (C.c_int, [C.c_void_p]),
@@ -319,6 +328,14 @@ class DiscMap:
         o = np.lexsort((tj[:nt], ts[:nt]))
         out.update(trip_s=ts[:nt][o], trip_j=tj[:nt][o], trip_c=tc[:nt][o], trip_edge=te[:nt][o])
         return out
+
+    def finalize(self, tau_geo=None, tau_vis=None, min_voxels: int = 0) -> dict:
+        """End-of-trajectory orphan merge + minimum-size filter (disc_finalize)."""
+        rep = disc_final_report()
+        tg = self.cfg.tau_geo if tau_geo is None else tau_geo
+        tv = self.cfg.tau_vis if tau_vis is None else tau_vis
+        self._check(lib().disc_finalize(self.h, tg, tv, int(min_voxels), C.byref(rep)))
+        return rep.as_dict()
 
     def set_timing(self, on: bool):
         self._check(lib().disc_set_timing(self.h, 1 if on else 0))
