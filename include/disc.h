@@ -216,6 +216,18 @@ disc_status disc_debug_last_frame(disc_map* m, disc_frame_debug* d);
  * its memberships.  Pass the map's own tau_geo / tau_vis for SPEC's finalize.  Synchronises; the
  * map stays usable (integration may continue).  DISC_ERR_UNSUPPORTED on a sharded map. */
 disc_status disc_finalize(disc_map* m, float tau_geo, float tau_vis, int64_t min_voxels, disc_final_report* rep);
+/* NEXT f4, batched open-vocabulary retrieval (P:195 [§IV-A] "top-k cosine-similarity predictions";
+ * S:398-403; R39): for every live instance with an embedding (ascending id) the k (1..16) best rows
+ * of table (host [C][Df], class text embeddings in the token space, R23) by cos = e_j . t_c / |t_c|,
+ * descending, ties by ascending class index.  ids host [cap], classes / scores host [cap][min(k,C)];
+ * NULL ids: count only.  Synchronises. */
+disc_status disc_classify(disc_map* m, const float* table, int32_t C, int32_t k, int64_t* ids, int32_t* classes,
+                          float* scores, int64_t cap, int64_t* n_out);
+/* NEXT f4, dense transfer (P:201 [§IV-B]; R40): for each point (host [P][3], world metres)
+ * the id of the instance owning the nearest voxel centre (k + 0.5) r (ties: lower id), or -1 when
+ * that centre is farther than d_assign (<= 64 voxels).  out host [P].  DISC_ERR_UNSUPPORTED on a
+ * sharded map.  Synchronises. */
+disc_status disc_dense_transfer(disc_map* m, const float* points, int64_t P, float d_assign, int64_t* out);
 disc_status disc_set_timing(disc_map* m, int32_t on);
 disc_status disc_get_stats(disc_map* m, disc_stats* s);
 disc_status disc_wait(disc_map* m, void* stream);  /* order `stream` after all queued map work */

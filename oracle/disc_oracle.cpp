@@ -998,3 +998,71 @@ extern "C" int64_t ora_query(const ora_map* m, const float* q, int32_t k, int64_
   }
   return n;
 }
+
+/* ------------------------------------------------------------------------------------ */
+/* batched open-vocabulary retrieval (NEXT f4): P:195 [§IV-A] "the correct ground-truth     */
+/* semantic class appearing within the top-k cosine-similarity predictions"      */
+/* classify_topk: "indices of the k largest cosines against table rows, descending, ties by */
+/* ascending index", for every live instance with an embedding (ascending id).  R39: the     */
+/* cosine is e_j . t_c / |t_c| in fp64 (e_j is unit, Eq. of S:391's rank_instances).         */
+/* ------------------------------------------------------------------------------------ */
+extern "C" int64_t ora_classify(const ora_map* m, const float* table, int32_t C, int32_t k, int64_t* ids,
+                                int32_t* classes, double* scores, int64_t cap) {
+  const int32_t Df = m->cfg.feat_dim;
+  std::vector<double> tn(C);
+  for (int32_t c = 0; c < C; ++c) {
+    double t = 0.0;
+    for (int32_t d = 0; d < Df; ++d) t += (double)table[(int64_t)c * Df + d] * (double)table[(int64_t)c * Df + d];
+    tn[c] = std::sqrt(t);
+  }
+  const int32_t kk = std::min(k, C);
+  int64_t n = 0;
+  for (const auto& kv : m->inst) {
+    if (kv.second.Q < 0.0) continue;
+    if (n < cap && ids) {
+      std::vector<std::pair<double, int32_t>> all(C);
+      for (int32_t c = 0; c < C; ++c) {
+        double s = 0.0;
+        for (int32_t d = 0; d < Df; ++d) s += kv.second.e[d] * (double)table[(int64_t)c * Df + d];
+        all[c] = {tn[c] > 0.0 ? s / tn[c] : 0.0, c};
+      }
+      std::sort(all.begin(), all.end(), [](const auto& a, const auto& b) {
+        if (a.first != b.first) return a.first > b.first;
+        return a.second < b.second;
+      });
+      ids[n] = kv.first;
+      for (int32_t i = 0; i < kk; ++i) {
+        classes[n * kk + i] = all[i].second;
+        scores[n * kk + i] = all[i].first;
+      }
+    }
+    n++;
+  }
+  return n;
+}
+
+/* dense transfer (NEXT f4): P:201 [§IV-B] "associating each 3D point in the ground truth to its */
+/* closest CLIP feature vector in our mapped scene"; "each gt point takes the top-1   */
+/* class of the spatially nearest instance (nearest voxel center over all instances); points     */
+/* farther than d_assign from any voxel labeled unassigned".  R40: distance to the voxel centre  */
+/* (k + 0.5) r, squared, in fp64 with r = (double)voxel_size, point coordinates fp32 promoted,   */
+/* summed x, y, z in that order; the minimum (d^2, id) wins (ties: lower id); unassigned  */
+/* iff d^2 > d_assign^2 (fp64).  Brute force over the membership relation.                        */
+extern "C" void ora_dense_transfer(const ora_map* m, const float* pts, int64_t P, float d_assign, int64_t* out) {
+  const double r = (double)m->cfg.voxel_size, dmax = (double)d_assign * (double)d_assign;
+  for (int64_t p = 0; p < P; ++p) {
+    double best = INFINITY;
+    Id bid = -1;
+    for (const auto& kv : m->mem) {
+      double d2 = 0.0;
+      for (int a = 0; a < 3; ++a) {
+        const double c = ((double)kv.first[a] + 0.5) * r;
+        const double x = (double)pts[3 * p + a] - c;
+        d2 = d2 + x * x;
+      }
+      for (Id j : kv.second)
+        if (d2 < best || (d2 == best && j < bid)) { best = d2; bid = j; }
+    }
+    out[p] = (bid >= 0 && best <= dmax) ? bid : -1;
+  }
+}

@@ -92,6 +92,14 @@ typedef struct {
 } ora_final_report;
 int32_t  ora_finalize(ora_map* m, float tau_geo, float tau_vis, int64_t min_voxels, ora_final_report* rep);
 
+/* batched retrieval (R39): top-k classes of every live instance with an
+   embedding, ascending id; classes / scores [n][min(k, C)]; returns n (fills at most cap rows) */
+int64_t ora_classify(const ora_map* m, const float* table, int32_t C, int32_t k, int64_t* ids,
+                     int32_t* classes, double* scores, int64_t cap);
+/* dense transfer (R40): nearest-voxel-centre instance of each point [P][3]
+   (world, metres), -1 if farther than d_assign */
+void    ora_dense_transfer(const ora_map* m, const float* pts, int64_t P, float d_assign, int64_t* out);
+
 /* ---- map state export ---- */
 int64_t ora_num_instances(const ora_map* m);
 /* ascending id; e [n][Df] (zeros if q == -1), T [n][Dt]; any pointer may be NULL */

@@ -99,6 +99,8 @@ def lib():
             "ora_s_sem": (D, [I32, P, P]), "ora_s_dist": (D, [D]), "ora_quality": (D, [D, D, D, D]),
             "ora_dot_pin": (D, [I32, P, P]), "ora_query": (I64, [P, P, I32, P, P]),
             "ora_finalize": (I32, [P, F, F, I64, P]),
+            "ora_classify": (I64, [P, P, I32, I32, P, P, P, I64]),
+            "ora_dense_transfer": (None, [P, P, I64, F, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -243,6 +245,25 @@ class OracleMap:
         if rc != 0:
             raise RuntimeError(f"oracle finalize rc={rc}: {lib().ora_last_error(self.h).decode()}")
         return rep.as_dict()
+
+    def classify(self, table, k: int):
+        """Top-k classes (table rows) of every live instance with an embedding."""
+        table = np.ascontiguousarray(table, np.float32)
+        C = table.shape[0]
+        n = lib().ora_classify(self.h, _p(table), C, k, None, None, None, 0)
+        kk = min(k, C)
+        ids = np.zeros(n, np.int64)
+        cls = np.zeros((n, kk), np.int32)
+        sc = np.zeros((n, kk), np.float64)
+        lib().ora_classify(self.h, _p(table), C, k, _p(ids), _p(cls), _p(sc), n)
+        return ids, cls, sc
+
+    def dense_transfer(self, points, d_assign: float):
+        """Nearest-voxel-centre instance per point, -1 = unassigned."""
+        pts = np.ascontiguousarray(points, np.float32).reshape(-1, 3)
+        out = np.zeros(pts.shape[0], np.int64)
+        lib().ora_dense_transfer(self.h, _p(pts), pts.shape[0], d_assign, _p(out))
+        return out
 
     def query(self, q, k: int):
         q = np.ascontiguousarray(q, np.float32)

@@ -1297,6 +1297,43 @@ disc_status disc_debug_last_frame(disc_map* m, disc_frame_debug* d) {
   return cuda_check(m, "disc_debug_last_frame");
 }
 
+disc_status disc_classify(disc_map* m, const float* table, int32_t C, int32_t k, int64_t* ids, int32_t* classes,
+                          float* scores, int64_t cap, int64_t* n_out) {
+  if (!m || !table || C < 1 || k < 1 || k > 16 || !n_out || cap < 0 || (ids && (!classes || !scores)))
+    return DISC_ERR_INVALID;
+  if (m->grp) {   // the instance table (and its embeddings) is replicated: shard 0 answers
+    const disc_status gs = disc_sync(m);
+    return gs != DISC_OK ? gs : disc_classify(m->grp->sh[0], table, C, k, ids, classes, scores, cap, n_out);
+  }
+  disc_status s = disc_sync(m);
+  if (s != DISC_OK) return s;
+  const int64_t nid = host_next_id(m);
+  const int kk = std::min(k, C);
+  const size_t need = (size_t)(nid + 16) * (16 + 8 * (size_t)kk) + (size_t)C * (m->cfg.feat_dim * 4 + 8) + (16 << 20);
+  if ((s = ensure_scratch(m, need)) != DISC_OK) return s;
+  const int64_t n = run_classify(m->M, m->cfg.feat_dim, nid, table, C, k, ids, classes, scores, ids ? cap : 0,
+                                 m->last_stream, m->scratch, m->scratch_bytes);
+  if (n < 0) return fail(m, DISC_ERR_INTERNAL, "classify scratch too small");
+  *n_out = n;
+  if (ids && n > cap) return fail(m, DISC_ERR_INVALID, "cap too small");
+  return cuda_check(m, "disc_classify");
+}
+
+disc_status disc_dense_transfer(disc_map* m, const float* points, int64_t P, float d_assign, int64_t* out) {
+  if (!m || P < 0 || (P > 0 && (!points || !out)) || !(d_assign >= 0.0f) || !std::isfinite(d_assign))
+    return DISC_ERR_INVALID;
+  if (m->grp) return fail(m, DISC_ERR_UNSUPPORTED, "disc_dense_transfer: sharded maps are not supported");
+  if (d_assign / m->cfg.voxel_size > 64.0f) return fail(m, DISC_ERR_INVALID, "d_assign above 64 voxels");
+  disc_status s = disc_sync(m);
+  if (s != DISC_OK) return s;
+  if (P == 0) return DISC_OK;
+  if ((s = ensure_scratch(m, (size_t)P * 20 + (1 << 20))) != DISC_OK) return s;
+  if (run_dense_transfer(m->M, m->cfg.voxel_size, points, P, d_assign, out, m->last_stream, m->scratch,
+                         m->scratch_bytes) != 0)
+    return fail(m, DISC_ERR_INTERNAL, "dense transfer scratch too small");
+  return cuda_check(m, "disc_dense_transfer");
+}
+
 disc_status disc_finalize(disc_map* m, float tau_geo, float tau_vis, int64_t min_voxels, disc_final_report* rep) {
   if (!m || !(tau_geo > 0.0f && tau_geo <= 1.0f) || !(tau_vis >= -1.0f && tau_vis <= 1.0f) || min_voxels < 0)
     return DISC_ERR_INVALID;

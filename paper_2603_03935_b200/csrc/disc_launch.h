@@ -68,6 +68,11 @@ int64_t export_instances(const MapState& M, int Df, int Dt, int64_t next_id, dis
                          size_t scratch_bytes);
 int64_t export_memberships(const MapState& M, uint64_t* keys, int64_t* ids, int64_t cap, cudaStream_t st,
                            void* scratch, size_t scratch_bytes);
+int64_t run_classify(const MapState& M, int Df, int64_t next_id, const float* table_host, int32_t C, int32_t k,
+                     int64_t* ids_out, int32_t* cls_out, float* sc_out, int64_t cap, cudaStream_t st, void* scratch,
+                     size_t scratch_bytes);
+int run_dense_transfer(const MapState& M, float r, const float* pts_host, int64_t P, float d_assign, int64_t* out_host,
+                       cudaStream_t st, void* scratch, size_t scratch_bytes);
 int32_t run_query(const MapState& M, int Df, int64_t next_id, const float* q_host, int32_t k, int64_t* ids,
                   float* scores, cudaStream_t st, void* scratch, size_t scratch_bytes);
 }  // namespace disc

@@ -190,4 +190,202 @@ int32_t run_query(const MapState& M, int Df, int64_t next_id, const float* q_hos
   return m;
 }
 
+// ------------------------------------------------------------------------------------------
+// NEXT row f4: batched open-vocabulary retrieval.
+//  classify_topk (P:195 [§IV-A], R39): cos(e_j, t_c) = e_j . t_c / |t_c| for every live
+//  instance with an embedding x every class row, the k best per instance (descending, ties by
+//  ascending class index).  A dense contraction E [n x Df] x T^T [Df x C] with a per-row top-k
+//  epilogue fused in: 64 x 64 output tiles from shared-memory K-slices (fp32 FFMA, 4 x 4 outputs
+//  per thread), each tile's scores merged into the rows' running top-k lists in shared memory, so
+//  the n x C score matrix never reaches HBM.
+// ------------------------------------------------------------------------------------------
+constexpr int CL_T = 64, CL_K = 32, CL_KMAX = 16;
+
+__global__ void __launch_bounds__(256) k_classify(MapState M, int Df, const int32_t* ids, int n, const float* tab,
+                                                  const double* tnorm, int C, int k, int32_t* out_c, float* out_s) {
+  __shared__ float As[CL_K][CL_T + 1], Bs[CL_K][CL_T + 1];
+  __shared__ float S[CL_T][CL_T + 1];
+  __shared__ float tk_s[CL_T][CL_KMAX];
+  __shared__ int32_t tk_c[CL_T][CL_KMAX];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int r0 = blockIdx.x * CL_T;
+  for (int i = threadIdx.x; i < CL_T * CL_KMAX; i += blockDim.x) {
+    tk_s[i / CL_KMAX][i % CL_KMAX] = -INFINITY;
+    tk_c[i / CL_KMAX][i % CL_KMAX] = INT32_MAX;
+  }
+  for (int c0 = 0; c0 < C; c0 += CL_T) {
+    float acc[4][4] = {};
+    for (int d0 = 0; d0 < Df; d0 += CL_K) {
+      for (int i = threadIdx.x; i < CL_K * CL_T; i += blockDim.x) {
+        const int row = i / CL_K, dd = i % CL_K;   // consecutive threads: consecutive dims of one row
+        const int r = r0 + row, c = c0 + row, d = d0 + dd;
+        As[dd][row] = (r < n && d < Df) ? M.E[(size_t)ids[r] * Df + d] : 0.f;
+        Bs[dd][row] = (c < C && d < Df) ? tab[(size_t)c * Df + d] : 0.f;
+      }
+      __syncthreads();
+#pragma unroll 8
+      for (int dd = 0; dd < CL_K; ++dd) {
+        float a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) { a[i] = As[dd][ty * 4 + i]; b[i] = Bs[dd][tx * 4 + i]; }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = c0 + tx * 4 + j;
+        S[ty * 4 + i][tx * 4 + j] = c < C ? (tnorm[c] > 0.0 ? (float)((double)acc[i][j] / tnorm[c]) : 0.f) : -INFINITY;
+      }
+    __syncthreads();
+    if (threadIdx.x < CL_T) {   // merge the tile into row threadIdx.x's top-k (classes ascending: ties keep the lower index)
+      const int row = threadIdx.x;
+      for (int j = 0; j < CL_T && c0 + j < C; ++j) {
+        const float v = S[row][j];
+        if (!(v > tk_s[row][k - 1])) continue;
+        int pos = k - 1;
+        while (pos > 0 && v > tk_s[row][pos - 1]) {
+          tk_s[row][pos] = tk_s[row][pos - 1];
+          tk_c[row][pos] = tk_c[row][pos - 1];
+          --pos;
+        }
+        tk_s[row][pos] = v;
+        tk_c[row][pos] = c0 + j;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < CL_T && r0 + threadIdx.x < n)
+    for (int i = 0; i < k; ++i) {
+      out_c[(size_t)(r0 + threadIdx.x) * k + i] = tk_c[threadIdx.x][i];
+      out_s[(size_t)(r0 + threadIdx.x) * k + i] = tk_s[threadIdx.x][i];
+    }
+}
+
+__global__ void k_table_norms(const float* tab, int C, int Df, double* tnorm) {
+  const int lane = threadIdx.x & 31;
+  for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < C; c += (gridDim.x * blockDim.x) >> 5) {
+    double a = 0;
+    for (int d = lane; d < Df; d += 32) a += (double)tab[(size_t)c * Df + d] * tab[(size_t)c * Df + d];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) tnorm[c] = sqrt(a);
+  }
+}
+
+int64_t run_classify(const MapState& M, int Df, int64_t next_id, const float* table_host, int32_t C, int32_t k,
+                     int64_t* ids_out, int32_t* cls_out, float* sc_out, int64_t cap, cudaStream_t st, void* scratch,
+                     size_t scratch_bytes) {
+  Scratch sc{(char*)scratch, scratch_bytes};
+  const int64_t nn = next_id > 0 ? next_id : 1;
+  int32_t* ids = sc.take<int32_t>(nn);
+  int32_t* nsel = sc.take<int32_t>(1);
+  float* tab = sc.take<float>((size_t)C * Df);
+  double* tnorm = sc.take<double>(C);
+  if (!ids || !nsel || !tab || !tnorm) return -1;
+  const int32_t n = select_ids(M, next_id, 1, ids, nsel, sc, st);
+  if (n < 0) return -1;
+  if (!ids_out || n == 0) return n;
+  const int kk = k < C ? k : C;
+  const int m = (int)(n < cap ? n : cap);
+  int32_t* dc = sc.take<int32_t>((size_t)m * kk);
+  float* ds = sc.take<float>((size_t)m * kk);
+  if (!dc || !ds) return -1;
+  cudaMemcpyAsync(tab, table_host, sizeof(float) * C * Df, cudaMemcpyHostToDevice, st);
+  k_table_norms<<<64, 256, 0, st>>>(tab, C, Df, tnorm);
+  k_classify<<<(m + CL_T - 1) / CL_T, 256, 0, st>>>(M, Df, ids, m, tab, tnorm, C, kk, dc, ds);
+  static thread_local std::vector<int32_t> hid;
+  hid.resize(m);
+  cudaMemcpyAsync(hid.data(), ids, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(cls_out, dc, sizeof(int32_t) * m * kk, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(sc_out, ds, sizeof(float) * m * kk, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  for (int i = 0; i < m; ++i) ids_out[i] = hid[i];
+  return n;
+}
+
+// ------------------------------------------------------------------------------------------
+//  dense transfer (P:201 [§IV-B], R40): the nearest voxel centre (k + 0.5) r over all
+//  instances' voxels, searched in the voxel hash over the cube of keys within d_assign of the
+//  point (thread per point); squared distances in fp64, no contraction, x + y + z in that order
+//  (the oracle's arithmetic, so ties and the d_assign cut are decided identically); ties -> lower id.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t q_find(const MapState& M, uint64_t key) {
+  uint64_t h = mix64(key) & (M.MC - 1);
+  for (uint64_t probe = 0; probe < M.MC; ++probe) {
+    const unsigned long long k = __ldcg(&M.slots[h].key);
+    if (k == key) return (uint32_t)h;
+    if (k == KEY_EMPTY) return U32_EMPTY;
+    h = (h + 1) & (M.MC - 1);
+  }
+  return U32_EMPTY;
+}
+
+__global__ void k_dense_transfer(MapState M, const float* pts, int64_t P, double r, int R, double dmax2, int64_t* out) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+    const double x[3] = {(double)pts[3 * p], (double)pts[3 * p + 1], (double)pts[3 * p + 2]};
+    int c[3];
+    for (int a = 0; a < 3; ++a) c[a] = (int)floor(x[a] / r);
+    double best = INFINITY;
+    int64_t bid = -1;
+    for (int dx = -R; dx <= R; ++dx)
+      for (int dy = -R; dy <= R; ++dy)
+        for (int dz = -R; dz <= R; ++dz) {
+          const int k[3] = {c[0] + dx, c[1] + dy, c[2] + dz};
+          bool inr = true;
+          for (int a = 0; a < 3; ++a) inr = inr && k[a] >= -KEY_BIAS && k[a] < KEY_BIAS;
+          if (!inr) continue;
+          double d2 = 0.0;
+          for (int a = 0; a < 3; ++a) {
+            const double ce = __dmul_rn(__dadd_rn((double)k[a], 0.5), r);
+            const double t = __dsub_rn(x[a], ce);
+            d2 = __dadd_rn(d2, __dmul_rn(t, t));
+          }
+          if (d2 > dmax2 || d2 > best) continue;
+          const uint64_t key = ((uint64_t)(uint32_t)(k[0] + KEY_BIAS) << 42) |
+                               ((uint64_t)(uint32_t)(k[1] + KEY_BIAS) << 21) | (uint64_t)(uint32_t)(k[2] + KEY_BIAS);
+          const uint32_t h = q_find(M, key);
+          if (h == U32_EMPTY) continue;
+          const uint32_t* labs = M.slots[h].lab;
+          int nl = INLINE_LABELS;
+          uint32_t nx = M.slots[h].ovf;
+          bool done = false;
+          while (!done) {
+            for (int i = 0; i < nl; ++i) {
+              const uint32_t L = labs[i];
+              if (L == U32_EMPTY) { done = true; break; }
+              if (L == LAB_TOMB) continue;
+              const int64_t id = M.id_of[L];
+              if (d2 < best || (d2 == best && id < bid)) { best = d2; bid = id; }
+            }
+            if (done || nx == U32_EMPTY) break;
+            labs = M.ovf[nx].lab;
+            nl = CHUNK_LABELS;
+            nx = M.ovf[nx].next;
+          }
+        }
+    out[p] = bid;
+  }
+}
+
+int run_dense_transfer(const MapState& M, float r, const float* pts_host, int64_t P, float d_assign, int64_t* out_host,
+                       cudaStream_t st, void* scratch, size_t scratch_bytes) {
+  Scratch sc{(char*)scratch, scratch_bytes};
+  float* pts = sc.take<float>((size_t)P * 3);
+  int64_t* out = sc.take<int64_t>((size_t)P);
+  if (!pts || !out) return -1;
+  const double rd = (double)r, dd = (double)d_assign;
+  const int R = (int)ceil(dd / rd) + 1;
+  cudaMemcpyAsync(pts, pts_host, sizeof(float) * 3 * P, cudaMemcpyHostToDevice, st);
+  k_dense_transfer<<<(int)std::min<int64_t>((P + 127) / 128, 4096), 128, 0, st>>>(M, pts, P, rd, R, dd * dd, out);
+  cudaMemcpyAsync(out_host, out, sizeof(int64_t) * P, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  return 0;
+}
+
 }  // namespace disc

@@ -112,6 +112,9 @@ EXPORTS = {
     "disc_debug_last_frame": (C.c_int, [C.c_void_p, C.c_void_p]),
     "disc_set_timing": (C.c_int, [C.c_void_p, C.c_int32]),
     "disc_finalize": (C.c_int, [C.c_void_p, C.c_float, C.c_float, C.c_int64, C.c_void_p]),
+    "disc_classify": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                C.c_int64, C.c_void_p]),
+    "disc_dense_transfer": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_float, C.c_void_p]),
     "disc_get_stats": (C.c_int, [C.c_void_p, C.c_void_p]),
     "disc_wait": (C.c_int, [C.c_void_p, C.c_void_p]),
     "disc_sync": (C.c_int, [C.c_void_p]),
@@ -328,6 +331,28 @@ class DiscMap:
         o = np.lexsort((tj[:nt], ts[:nt]))
         out.update(trip_s=ts[:nt][o], trip_j=tj[:nt][o], trip_c=tc[:nt][o], trip_edge=te[:nt][o])
         return out
+
+    def classify(self, table, k: int):
+        """Top-k classes (rows of table [C][Df]) of every live instance with an embedding (disc_classify)."""
+        table = np.ascontiguousarray(table, np.float32)
+        C_ = table.shape[0]
+        n = C.c_int64()
+        p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        self._check(lib().disc_classify(self.h, p(table), C_, k, None, None, None, 0, C.byref(n)))
+        kk = min(k, C_)
+        ids = np.zeros(max(n.value, 1), np.int64)
+        cls = np.zeros((max(n.value, 1), kk), np.int32)
+        sc = np.zeros((max(n.value, 1), kk), np.float32)
+        self._check(lib().disc_classify(self.h, p(table), C_, k, p(ids), p(cls), p(sc), n.value, C.byref(n)))
+        return ids[: n.value], cls[: n.value], sc[: n.value]
+
+    def dense_transfer(self, points, d_assign: float):
+        """Nearest-voxel-centre instance per point, -1 = unassigned (disc_dense_transfer)."""
+        pts = np.ascontiguousarray(points, np.float32).reshape(-1, 3)
+        out = np.zeros(max(pts.shape[0], 1), np.int64)
+        self._check(lib().disc_dense_transfer(self.h, pts.ctypes.data_as(C.c_void_p), pts.shape[0], d_assign,
+                                              out.ctypes.data_as(C.c_void_p)))
+        return out[: pts.shape[0]]
 
     def finalize(self, tau_geo=None, tau_vis=None, min_voxels: int = 0) -> dict:
         """End-of-trajectory orphan merge + minimum-size filter (disc_finalize)."""
