@@ -1,17 +1,20 @@
 """Multi-GPU orchestration of the DISC path (one process per GPU, torch.distributed).
 
-This round the path scales as independent maps (SURVEY §8(e) frame-/scene-parallel stage):
-every rank integrates its own scene stream (a rank-specific seed), there is no data-path
-collective, and throughput is all frames processed / the max over ranks of the device time
-(weak scaling).  The key-hash-sharded single map with NCCL all-to-all + allreduce is NEXT
-(DESIGN.md §8).  Backend: NCCL when CUDA is available, gloo otherwise (CPU tests).
+The map is key-hash sharded: rank r is shard r of G; it owns the voxel
+keys with (mix64(key) >> 40) mod G == r and a replica of the instance table, runs stage 1 for the
+stream's frames f = r + G j, and exchanges with the other ranks inside libdisc over NCCL (detection
+records all-gathered and (s, key) pairs routed to their owners per window; partial overlap-count
+triples all-gathered and new-membership counts all-reduced per frame).  This module only does the
+host-side plumbing around it: process-group setup, the NCCL unique-id bootstrap (rank 0 creates it
+with disc_nccl_unique_id, the process group broadcasts it), the frame split, barriers and
+max-over-ranks timing.  Backend: NCCL when CUDA is available, gloo otherwise (CPU tests).
 """
 from __future__ import annotations
 
 import os
 from dataclasses import dataclass
 
-SEED_STRIDE = 7919   # rank r maps the stream with seed  base + SEED_STRIDE * r
+SEED_STRIDE = 7919   # independent-map mode: rank r maps the stream with seed  base + SEED_STRIDE * r
 
 
 @dataclass
@@ -46,6 +49,26 @@ def setup(backend: str | None = None) -> Rank:
         else:
             dist.init_process_group(backend)
     return Rank(ws, rank, local, backend)
+
+
+def sharded_map_kwargs(r: Rank) -> dict:
+    """disc_config fields that make this process shard r.rank of an r.world-way key-sharded map:
+    rank 0 creates the 128-byte NCCL unique id (disc_nccl_unique_id) and the process group
+    broadcasts it, so every rank passes the same id (S:§8(b) bootstrap).  world 1: unsharded."""
+    if not r.distributed:
+        return dict(world_size=1, rank=0)
+    import torch.distributed as dist
+    obj = [None]
+    if r.rank == 0:
+        from .disc import nccl_unique_id
+        obj[0] = nccl_unique_id()
+    dist.broadcast_object_list(obj, src=0)
+    return dict(world_size=r.world, rank=r.rank, nccl_unique_id=obj[0])
+
+
+def own_frames(n: int, r: Rank) -> list:
+    """Indices of the stream's first n frames that rank r integrates: f = r + G j (disc.h sharding)."""
+    return list(range(r.rank, n, r.world))
 
 
 def stream_seed(base: int, rank: int) -> int:
