@@ -19,8 +19,12 @@ Clocks sampled through NVML during the timed region.  `e2e`: M1 through the publ
 disc_integrate_frames_host (pinned host buffers: H2D inside the timed region, report D2H).
 `cpu_baseline`: the CPU oracle (oracle/, 1 thread, as it stands) on a bounded prefix of the stream.
 
-N > 1 (torchrun): DISC_SHARDED=0 (default until the sharded path is selected) gives every rank
-its own scene stream (weak scaling, independent problems); see DESIGN.md §8.
+N > 1 (torchrun): ONE stream into ONE key-hash-sharded map: rank r is
+shard r (owns the voxel keys with mix64(key) >> 40 mod N == r), runs stage 1 for the frames
+f = r + N j, and libdisc exchanges over NCCL (detections all-gathered, (s, key) pairs routed to their
+owners per window; overlap-count triples all-gathered, new-membership counts all-reduced per
+frame).  A step is still 32 frames of the stream (32 / N per rank): strong scaling.  DISC_SHARDED=0
+falls back to N independent maps (one scene stream per rank, weak scaling).
 
 --impl reference: the reference arm is the CPU oracle (this tier has no reference code); rank 0
 runs it on the host cores, each step a bounded sample (1 frame) of the same workload.
@@ -272,7 +276,12 @@ def main():
 
     dev = torch.device("cuda", local)
     F = args.frames_per_step
-    g = Generator(args.config, seed=par.stream_seed(seed_of(args.config), rank), device=dev)
+    sharded = ws > 1 and os.environ.get("DISC_SHARDED", "1") != "0"
+    Fr = F // ws if sharded else F   # frames per rank per step
+    if sharded and F % ws:
+        raise SystemExit(f"--frames-per-step {F} must be a multiple of --gpus {ws} for the sharded map")
+    g = Generator(args.config, seed=seed_of(args.config) if sharded else par.stream_seed(seed_of(args.config), rank),
+                  device=dev)
     c = g.cfg
     cfg_kw = disc_config_kwargs(c)
     prefill = args.prefill_memberships if args.prefill_memberships is not None else (1e7 if args.config == "H" else 0)
@@ -282,14 +291,14 @@ def main():
                 # views reach ~1 pair per pixel (2 cm voxels, 480x640): 2^19.  Past it: loud CAPACITY error
                 max_pairs_per_frame=int(os.environ.get("BENCH_PMAX", 1 << 19 if args.config == "H" else 1 << 17)),
                 device=local)
-    m = DiscMap(**cfg_kw, **caps)
+    m = DiscMap(**cfg_kw, **caps, **(par.sharded_map_kwargs(RANK) if sharded else {}))
     t_gen = 0.0
     nxt = 0   # next frame index of the stream
 
-    def gen(n, feats):
+    def gen(n, feats):   # this rank's frames among the stream's next n
         nonlocal nxt, t_gen
         t0 = time.perf_counter()
-        out = [g.frame(f, with_feats=feats) for f in range(nxt, nxt + n)]
+        out = [g.frame(f, with_feats=feats) for f in range(nxt, nxt + n) if not sharded or f % ws == rank]
         if not feats:
             out = [m1(fr) for fr in out]
         torch.cuda.synchronize()
@@ -311,7 +320,7 @@ def main():
 
     def run(frames_, timed_steps, warm_steps):
         for s in range(warm_steps):
-            m.integrate_frames(frames_[s * F:(s + 1) * F])
+            m.integrate_frames(frames_[s * Fr:(s + 1) * Fr])
         m.sync()
         st0 = m.stats()
         m.set_timing(True)
@@ -323,7 +332,7 @@ def main():
         with ClockSampler(local) as clk:
             e0.record(stream)
             for s in range(warm_steps, warm_steps + timed_steps):
-                m.integrate_frames(frames_[s * F:(s + 1) * F])
+                m.integrate_frames(frames_[s * Fr:(s + 1) * Fr])
             m.wait(stream)   # include the last window's stage 2
             e1.record(stream)
             torch.cuda.synchronize()
@@ -340,7 +349,7 @@ def main():
         frames = gen((args.warmup + args.steps) * F, feats)
         ms, d, clocks = run(frames, args.steps, args.warmup)
         ms_max = max_over_ranks(ms, ws)
-        timed = frames[args.warmup * F:]
+        timed = frames[args.warmup * Fr:]
         n = len(timed)
         in_bytes = sum(frame_bytes(fr) for fr in timed)
         k1_bytes = sum(fr["masks"].numel() + fr["depth"].numel() * 4 for fr in timed)
@@ -368,7 +377,7 @@ def main():
             v["traffic"] = t * n / v["launches"] if t is not None and v["launches"] else None
         dom = max(kern, key=lambda k: kern[k]["share_of_step"] or 0.0)
         pb = in_bytes + s2_bytes
-        return {"value": ws * args.steps * F / (ms_max / 1e3), "ms": ms_max, "clocks": clocks, "kernels": kern,
+        return {"value": (1 if sharded else ws) * args.steps * F / (ms_max / 1e3), "ms": ms_max, "clocks": clocks, "kernels": kern,
                 "dominant": dom, "frames": timed, "d": d,
                 "path": {"bound": "hbm", "algorithmic_bytes_per_frame": pb / n, "achieved": pb / (ms / 1e3) / 1e9,
                          "peak": peak, "unit": "GB/s", "frac": pb / (ms / 1e3) / 1e9 / peak,
@@ -380,15 +389,16 @@ def main():
     line = {
         "metric": METRIC, "value": r1["value"], "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": r1["ms"] / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD[args.config], "frames_per_step": F,
                    "mode": "M1 = voxel association + refinement (A0-A3, A5b, A6-A8; no CLIP tokens)",
                    "l2": f"no flush: inputs per step {sum(frame_bytes(fr) for fr in timed) / args.steps / 1e9:.2f} GB > 126 MB L2",
-                   "frames_timed_per_rank": args.steps * F,
+                   "frames_timed_per_rank": args.steps * Fr,
                    "masks_per_frame_mean": round(sum(fr["masks"].shape[0] for fr in timed) / len(timed), 1),
                    "prefill_frames": prefill_frames, "prefill_seconds": round(t_pf, 1),
                    "live_memberships_before_timing": int(live),
-                   "parallelism": f"{ws} independent maps (one scene stream per rank)" if ws > 1 else "1 GPU"},
+                   "parallelism": (f"one stream, key-hash-sharded map over {ws} GPUs (NCCL)" if sharded else
+                                   f"{ws} independent maps (one scene stream per rank)") if ws > 1 else "1 GPU"},
         "roofline": {"bound": dom["bound"], "kernel": dom["kernel"], "achieved": dom["achieved"], "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": dom["frac"], "traffic": dom["traffic"],
                      "algorithmic_bytes_per_launch": dom["algorithmic_bytes_per_launch"],
@@ -415,21 +425,21 @@ def main():
         E = max(1, min(args.e2e_steps, args.steps))
         host = [{k: (v.cpu().pin_memory() if isinstance(v, torch.Tensor) else v) for k, v in fr.items()}
                 for fr in gen((E + 1) * F, False)]
-        m.integrate_frames_host(host[:F], report=True)   # warm-up step
-        h2d = sum(frame_bytes(fr) for fr in host[F:]) / E
+        m.integrate_frames_host(host[:Fr], report=True)   # warm-up step
+        h2d = sum(frame_bytes(fr) for fr in host[Fr:]) / E
         barrier(ws)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         max_u = 0
         for s in range(1, E + 1):
-            reps = m.integrate_frames_host(host[s * F:(s + 1) * F], report=True)
+            reps = m.integrate_frames_host(host[s * Fr:(s + 1) * Fr], report=True)
             max_u = max([max_u] + [r["unique_pairs"] for r in reps])
         torch.cuda.synchronize()
         te = max_over_ranks(time.perf_counter() - t0, ws)
         from paper_2603_03935_b200.disc import disc_frame_report
         import ctypes
-        line["e2e"] = {"value": ws * E * F / te, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
-                       "d2h_bytes_per_step": F * ctypes.sizeof(disc_frame_report), "steps": E, "mode": "M1",
+        line["e2e"] = {"value": (1 if sharded else ws) * E * F / te, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
+                       "d2h_bytes_per_step": Fr * ctypes.sizeof(disc_frame_report), "steps": E, "mode": "M1",
                        "api": "disc_integrate_frames_host (pinned host buffers)",
                        "max_unique_pairs_per_frame": int(max_u), "max_pairs_per_frame": caps["max_pairs_per_frame"],
                        "live_memberships_after": int(reps[-1]["live_memberships"])}

@@ -778,8 +778,12 @@ static disc_status group_integrate(disc_map* m, const disc_frame* frames, int32_
   for (int w0 = 0; w0 < n; w0 += per_call) {
     const int nc = std::min(per_call, n - w0);
     const int Wn = Gp.nccl ? G * nc : nc;   // window slots
-    bool sem = Gp.nccl;   // NCCL: the other ranks' frames may carry tokens; q = -1 marks those without
-    for (int i = 0; i < nc; ++i) sem = sem || frames[w0 + i].patch_feats != nullptr;
+    // stage 1 and the record packing follow this process's own frames; the replicated stage 2
+    // (and the unpacking) must assume tokens when another rank's frames may carry them (NCCL): a
+    // frame without tokens has q = -1 everywhere, so no embedding is ever taken from it
+    bool sem_own = false;
+    for (int i = 0; i < nc; ++i) sem_own = sem_own || frames[w0 + i].patch_feats != nullptr;
+    const bool sem = Gp.nccl || sem_own;
     // ---- stage 1, frame-parallel: local shard l (global g) runs its window slots ----
     for (int l = 0; l < L; ++l) {
       disc_map* s = Gp.sh[l];
@@ -812,11 +816,11 @@ static disc_status group_integrate(disc_map* m, const disc_frame* frames, int32_
       if (wd.n > 0) {
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (m->timing && l == 0) { e0 = ev_get(m); e1 = ev_get(m); }
-        m->stats.launches += launch_stage1(wd, s->Wb[0], s->P, s->d_err, sem, maxS, 1, 1, 1, maxP, 4, s->nsm, 0, st,
-                                           e0, e1);
+        m->stats.launches += launch_stage1(wd, s->Wb[0], s->P, s->d_err, sem_own, maxS, 1, 1, 1, maxP, 4, s->nsm, 0,
+                                           st, e0, e1);
         if (e0) m->ev_pending.push_back({e0, e1, 0});
         uint8_t* dst = Gp.nccl ? Gp.det_send : Gp.det_all + (size_t)g * Gp.nloc * Gp.DL.total;
-        launch_det_pack(s->Wb[0], wd.n, Gp.h_meta, dst, Gp.DL, Df, Dt, sem, st);
+        launch_det_pack(s->Wb[0], wd.n, Gp.h_meta, dst, Gp.DL, Df, Dt, sem_own, st);
       }
       // (the pinned meta is read at launch: kernel arguments are copied by value)
     }
