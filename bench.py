@@ -341,7 +341,7 @@ def main():
         ms = e0.elapsed_time(e1)
         m.set_timing(False)
         st1 = m.stats()
-        return ms, {k: st1[k] - st0[k] for k in st1}, clk.summary()
+        return ms, {k: st1[k] - st0[k] for k in st1 if not isinstance(st1[k], list)}, clk.summary()
 
     peak, peak_kind = peaks()
 

@@ -203,8 +203,11 @@ __device__ __forceinline__ void lk_probe(int i, unsigned long long& tp) {
 }
 constexpr int LK_CT = 2048;   // per-CTA (s, j) count table slots (in the dynamic shared memory)
 
+// spec: the pair's slot index was found by s2_spec during the previous frame's association (pms,
+// U32_EMPTY = key absent then): keys never move in the open-addressing table, so the probe starts
+// at that slot and matches at once; only keys absent then (new keys) probe from their home slot
 __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapState& M, const FrameScratch& X,
-                                          int Dt) {
+                                          int Dt, bool spec = false) {
   const uint32_t np = min(wb.npairs[f], (uint32_t)wb.PMAX);
   const size_t fo = (size_t)f * wb.PMAX;
   const int lane = threadIdx.x & 31;
@@ -256,6 +259,10 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
     for (int q = 0; q < LK_Q; ++q) {
       act[q] = idx[q] < np && stf[s[q]] == 0;   // (a few L1 lines: no staging round trip)
       h[q] = (uint32_t)mix64(key[q]) & hmask;
+      if (spec && idx[q] < np) {
+        const uint32_t ps = wb.pms[fo + idx[q]];
+        if (ps != U32_EMPTY) h[q] = ps;
+      }
     }
     SlotV sv[LK_Q];
     auto any_act = [&]() {
@@ -1369,16 +1376,56 @@ __device__ __forceinline__ void s2_gate(int f, const WinBufs& wb, const MapState
   }
 }
 
-// While CTA 0 runs the association of frame f, the other CTAs pull frame f+1's lookup working
-// set into L2: its pair records and the hash slots its keys start probing at (a hint only: the
-// slots are read again, after frame f's update, by the lookup).
-__device__ __forceinline__ void s2_prefetch(int f, const WinBufs& wb, const MapState& M) {
+// While CTA 0 runs the association of frame f, the other CTAs look up frame f+1's keys
+// speculatively (against the map before frame f's update): each kept pair's slot index, or
+// U32_EMPTY, into pms.  Frame f+1's lookup re-reads the found slots (their labels may have changed;
+// the slot of a key never does) and probes only the keys absent here.
+__device__ __forceinline__ void s2_spec(int f, const WinBufs& wb, const MapState& M) {
+  const uint32_t np = min(__ldcg(&wb.npairs[f]), (uint32_t)wb.PMAX);
+  const size_t fo = (size_t)f * wb.PMAX;
+  const uint32_t hmask = (uint32_t)(M.MC - 1);
+  const int32_t* stf = wb.status + (size_t)f * wb.SMAX;
+  const uint32_t nth = (gridDim.x - 1) * blockDim.x;   // CTAs 1..G-1
+  constexpr int Q = 4;
+  for (uint32_t b = (blockIdx.x - 1) * blockDim.x + threadIdx.x; b < np; b += Q * nth) {
+    unsigned long long key[Q];
+    uint32_t h[Q], res[Q];
+    bool act[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const uint32_t i = b + q * nth;
+      act[q] = i < np && stf[__ldcg(&wb.pinfo[fo + i])] == 0;
+      key[q] = act[q] ? __ldcg(&wb.pkey[fo + i]) : KEY_EMPTY;
+      h[q] = (uint32_t)mix64(key[q]) & hmask;
+      res[q] = U32_EMPTY;
+    }
+    for (uint32_t probe = 0; probe <= hmask; ++probe) {
+      bool any = false;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        if (!act[q]) continue;
+        const unsigned long long k = __ldcg(&M.slots[h[q]].key);
+        if (k == key[q]) { res[q] = h[q]; act[q] = false; }
+        else if (k == KEY_EMPTY) act[q] = false;
+        else h[q] = (h[q] + 1) & hmask;
+        any = any || act[q];
+      }
+      if (!any) break;
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+      if (b + q * nth < np) wb.pms[fo + b + q * nth] = res[q];
+  }
+}
+
+// (DISC_S2_SPEC=0) the round-1 variant: only pull frame f+1's pair records and home slots into L2
+__device__ __forceinline__ void s2_prefetch_hint(int f, const WinBufs& wb, const MapState& M) {
   const uint32_t np = min(__ldcg(&wb.npairs[f]), (uint32_t)wb.PMAX);
   const size_t fo = (size_t)f * wb.PMAX;
   const uint32_t hmask = (uint32_t)(M.MC - 1);
   const uint32_t n = gridDim.x - 1, b = blockIdx.x - 1;   // CTAs 1..G-1
   for (uint32_t i = b * blockDim.x + threadIdx.x; i < np; i += n * blockDim.x) {
-    if ((i & 31) == 0) {   // one line of each record array per 32 pairs
+    if ((i & 31) == 0) {
       asm volatile("prefetch.global.L2 [%0];" ::"l"(wb.pinfo + fo + i));
       asm volatile("prefetch.global.L2 [%0];" ::"l"(wb.pms + fo + i));
       asm volatile("prefetch.global.L2 [%0];" ::"l"(wb.pkey + fo + i + 16));
@@ -1452,7 +1499,7 @@ __device__ __forceinline__ void grid_sync(uint32_t* bar, uint32_t target) {
 // (K5 lookup with the previous frame's K7 tail, K6 association on CTA 0, K7 apply) in one
 // persistent launch.
 __global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb, MapState M, FrameScratch X,
-                                                        Params P, int sem, int prof) {
+                                                        Params P, int sem, int prof, int spec) {
   const uint32_t G = gridDim.x;
   uint32_t ep = 0;
   unsigned long long t_prev = 0;
@@ -1484,7 +1531,7 @@ __global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb
   for (int f = 0; f < wd.n; ++f) {
     const FrameDesc& F = wd.f[f];
     cta_t(-1);
-    s2_lookup(f, wb, M, X, P.Dt);
+    s2_lookup(f, wb, M, X, P.Dt, spec && f > 0 && G > 1);
     if (f > 0) s2_finalize(f - 1, M, X);
     cta_t(0);
     grid_sync(wb.s2bar, G * ++ep);
@@ -1493,7 +1540,10 @@ __global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb
       s2_assoc(f, F, wb, M, X, P, sem);
     } else {
       if (P.Dt > 0) s2_gate(f, wb, M, X, P);
-      if (f + 1 < wd.n) s2_prefetch(f + 1, wb, M);
+      if (f + 1 < wd.n) {
+        if (spec) s2_spec(f + 1, wb, M);
+        else s2_prefetch_hint(f + 1, wb, M);
+      }
     }
     grid_sync(wb.s2bar, G * ++ep);
     probe(1);
@@ -1656,7 +1706,8 @@ int launch_stage2(const WinDesc& wd, const WinBufs& wb, const MapState& M, const
   // cooperative launch: its CTAs wait on one another at the grid barriers, so co-residency must
   // be guaranteed, not assumed
   int semi = sem ? 1 : 0;
-  void* args[] = {(void*)&wd, (void*)&wb, (void*)&M, (void*)&X, (void*)&P, (void*)&semi, (void*)&prof};
+  static const int spec = getenv("DISC_S2_SPEC") ? atoi(getenv("DISC_S2_SPEC")) : 1;   // speculative lookups
+  void* args[] = {(void*)&wd, (void*)&wb, (void*)&M, (void*)&X, (void*)&P, (void*)&semi, (void*)&prof, (void*)&spec};
   cudaLaunchCooperativeKernel((const void*)k_stage2, dim3(grid), dim3(K6_THREADS), args, sm6, st);
   debug_check(st, "k_stage2", -1);
   return 1;

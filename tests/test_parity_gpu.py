@@ -94,7 +94,7 @@ def _stream_parity(name, nframes, semantic, window, every=1, caps=None, reports=
     g = Generator(name, device=dev, **over)
     c = g.cfg
     kw = disc_config_kwargs(c)
-    gm = _disc_map(kw, c.H, c.W, c.Hp, c.Wp, window=window, S=max(64, int(c.n_masks * 1.2) + 8), **(caps or {}))
+    gm = _disc_map(kw, c.H, c.W, c.Hp, c.Wp, window=window, S=min(255, max(64, int(c.n_masks * 1.2) + 8)), **(caps or {}))
     om = OracleMap(**kw)
     frames = [g.frame(f, with_feats=semantic) for f in range(nframes)]
     # windowed GPU integration (the launch configuration bench.py times)
