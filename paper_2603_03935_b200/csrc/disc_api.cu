@@ -67,6 +67,10 @@ struct disc_map {
   // export scratch
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
+  // frame-table state per window buffer: clean = every slot EMPTY / zero (map creation; after a
+  // window that released its slots); release when the tables are >= tab_ratio x the pairs per frame
+  bool ktab_clean[2] = {true, true}, nsum_clean[2] = {true, true};
+  double tab_ratio = 8.0;
   // key-hash-sharded map (world_size > 1): this handle drives the local shards (sub-maps)
   struct ShardGroup* grp = nullptr;
 };
@@ -369,6 +373,8 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
     m->nres_geo = std::max(0, std::min(m->nres_geo, m->nsm / 2));
     const char* ea = std::getenv("DISC_S2_ADAPT");   // 0: fixed split (tuning)
     m->adapt = !(ea && std::atoi(ea) == 0);
+    const char* er = std::getenv("DISC_TAB_RELEASE_RATIO");   // tuning: 1e30 = always fill
+    if (er) m->tab_ratio = std::atof(er);
   }
   Params& P = m->P;
   P.r = cfg->voxel_size; P.tau_geo = cfg->tau_geo; P.tau_vis = cfg->tau_vis;
@@ -1036,7 +1042,12 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
     }
     tl_mark(s1, "s1_begin", -1);
     const int nres_w = stage2_reserve(m, sem);
-    m->stats.launches += launch_stage1(wd, Wbuf, m->P, m->d_err, sem, maxS, maxHp, maxW, maxWp, maxP, rows, m->nsm, nres_w, s1, e0, e1);
+    // frame tables: fill the dirty ones; release after use when they are much larger than a frame's pairs
+    const bool release = m->np_avg > 0.0 && (double)Wbuf.PC > m->tab_ratio * m->np_avg;
+    m->stats.launches += launch_stage1(wd, Wbuf, m->P, m->d_err, sem, maxS, maxHp, maxW, maxWp, maxP, rows, m->nsm,
+                                       nres_w, s1, e0, e1, !m->ktab_clean[b], !m->nsum_clean[b], release);
+    m->ktab_clean[b] = release;
+    if (sem) m->nsum_clean[b] = release;
     cudaMemcpyAsync(m->h_np + (size_t)b * MAXWIN, Wbuf.npairs, sizeof(uint32_t) * nw, cudaMemcpyDeviceToHost, s1);
     cudaEventRecord(m->ev_np[b], s1);
     m->np_pending[b] = nw;

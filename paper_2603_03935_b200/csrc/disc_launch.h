@@ -12,7 +12,8 @@ size_t k6_smem_bytes(int S, int TC);
 size_t k6_layout_bytes(int S, int TC);   // the association's table layout alone (global-memory mode)
 int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* err, bool sem, int maxS,
                   int maxHp, int maxW, int maxWp, int maxP, int rows_cap, int nsm, int nres, cudaStream_t st,
-                  cudaEvent_t ev0, cudaEvent_t ev1);
+                  cudaEvent_t ev0, cudaEvent_t ev1, bool fill_ktab = true, bool fill_nsum = true,
+                  bool release = false);
 int launch_stage2(const WinDesc& wd, const WinBufs& wb, const MapState& M, const FrameScratch& X, const Params& P,
                   bool sem, int nsm, int nres, cudaStream_t st);
 // the key-hash-sharded map (k_map.cu: stage-2 phases per frame; k_shard.cu: stage-1 exchange)

@@ -1571,9 +1571,27 @@ int k1_tiles(int H, int W, bool sem) {
   return ((W + tw - 1) / tw) * ((H + K1_TILE_H - 1) / K1_TILE_H);
 }
 
+// Release of the frame tables after use (tables much larger than the frames' pair counts, e.g. H's
+// 2^20-slot tables for ~10^5 pairs): the key slot of every pair and (semantic mode) its normal-sum
+// slot return to EMPTY / 0, instead of a streaming fill of the whole tables before the next window.
+__global__ void __launch_bounds__(256) k_release(WinDesc wd, WinBufs wb, int sem) {
+  const int f = blockIdx.y;
+  if (f >= wd.n) return;
+  const uint32_t np = min(wb.npairs[f], (uint32_t)wb.PMAX);
+  const size_t fo = (size_t)f * wb.PMAX, to = (size_t)f * wb.PC;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
+    const uint32_t ks = wb.pfk[fo + i];
+    if (ks < (uint32_t)wb.PC) __stcs(&wb.ktab[to + ks], (unsigned long long)KEY_EMPTY);
+    if (sem) {
+      const uint32_t ps = wb.plist[fo + i];
+      if (ps < (uint32_t)wb.PC) __stcs(&wb.nsum[to + ps], make_float4(0.f, 0.f, 0.f, 0.f));
+    }
+  }
+}
+
 int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* err, bool sem, int maxS,
                   int maxHp, int maxW, int maxWp, int maxP, int rows_cap, int nsm, int nres, cudaStream_t st,
-                  cudaEvent_t ev0, cudaEvent_t ev1) {
+                  cudaEvent_t ev0, cudaEvent_t ev1, bool fill_ktab, bool fill_nsum, bool release) {
   const int n = wd.n;
   (void)rows_cap; (void)maxW;
   int k1_grid = 1;
@@ -1581,11 +1599,12 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
   (void)maxHp; (void)maxWp;
   k_win_init<<<dim3(8, n), 256, 0, st>>>(wd, wb);
   debug_check(st, "k_win_init", -1);
-  // per-pair normal sums start from zero: one coalesced memset per window (zeroing the slots
-  // one by one after use costs far more: scattered partial-line writes)
-  if (sem) k_fill_cs<<<4 * nsm, 256, 0, st>>>((uint4*)wb.nsum, (size_t)n * wb.PC, 0u);
-  // the frames' key tables start empty (one memset per window; no per-pair release in stage 2)
-  k_fill_cs<<<4 * nsm, 256, 0, st>>>((uint4*)wb.ktab, (size_t)n * wb.PC / 2, 0xFFFFFFFFu);
+  // per-pair normal sums start from zero and the key tables empty: either one streaming fill per
+  // window (tables sized close to the frames' pair counts: scattered zeroing of partial lines costs
+  // more) or, when the previous window released its slots (k_release), nothing to do
+  int launches = 0;
+  if (sem && fill_nsum) { k_fill_cs<<<4 * nsm, 256, 0, st>>>((uint4*)wb.nsum, (size_t)n * wb.PC, 0u); ++launches; }
+  if (fill_ktab) { k_fill_cs<<<4 * nsm, 256, 0, st>>>((uint4*)wb.ktab, (size_t)n * wb.PC / 2, 0xFFFFFFFFu); ++launches; }
   if (ev0) cudaEventRecord(ev0, st);
   int64_t maxHW = 1;
   bool vec = true;
@@ -1610,6 +1629,11 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
   if (sem) k_pairs<true><<<dim3(g2, n), K2_THREADS, sm2, st>>>(wd, wb, P, err, k2abl);
   else k_pairs<false><<<dim3(g2, n), K2_THREADS, sm2, st>>>(wd, wb, P, err, k2abl);
   debug_check(st, "k_pairs", -1);
+  if (release) {
+    k_release<<<dim3(32, n), 256, 0, st>>>(wd, wb, sem ? 1 : 0);
+    debug_check(st, "k_release", -1);
+    ++launches;
+  }
   if (sem) {
     const int nch = (maxP + K3_ROWS - 1) / K3_ROWS;
     k_fbar_part<<<dim3(nch, n), 256, 0, st>>>(wd, wb, P.Df);
@@ -1660,7 +1684,7 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
     k_finalize<false><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
     debug_check(st, "k_finalize", -1);
   }
-  return sem ? 14 : 9;   // the launches above on s1, counted exactly (bench.py reports them)
+  return (sem ? 12 : 8) + launches;   // the launches above on s1, counted exactly (bench.py reports them)
 }
 
 }  // namespace disc

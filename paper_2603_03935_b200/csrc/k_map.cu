@@ -1252,14 +1252,25 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
   const size_t fo = (size_t)f * wb.PMAX;
   const int nseg = *X.nseg;
   int delta = 0;
-  // items: frame pairs (inserts), relabel items, entries of lists K6 moved (copies); 64-item
-  // chunks from a counter (the target warps take fewer), two items per lane with their record
-  // loads issued together
+  // items: frame pairs (inserts), relabel items, entries of lists K6 moved (copies), two items per
+  // lane with their record loads issued together.  The pair items (the bulk: every unique (s, key)
+  // of the frame, most already members) are split statically over the warps in 64-item blocks; the
+  // relabel / copy items (uneven) come in 64-item chunks from a counter.  (All chunks from one
+  // counter serialised ~1.5 k atomics per H frame on one L2 address.)
+  const uint32_t npb = (np + 63) / 64;   // pair blocks
+  uint32_t sblk = (uint32_t)gw;
   for (;;) {
     uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(X.work, 64u);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (base >= total) break;
+    const bool stat = sblk < npb;   // a static pair block: its items past np are nobody's
+    if (stat) {
+      base = sblk * 64u;
+      sblk += (uint32_t)nw;
+    } else {
+      if (lane == 0) base = atomicAdd(X.work, 64u);
+      base = __shfl_sync(0xffffffffu, base, 0) + npb * 64u;
+      if (base >= npb * 64u + nrel + nmove) break;
+      base -= (npb * 64u - np);   // -> the item index space: relabel items start at np
+    }
     uint32_t itq[2], sq[2], slotq[2];
     uint2 plq[2];
 #pragma unroll
@@ -1306,7 +1317,7 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
             }
           }
         }
-      } else if (it < np + nrel) {
+      } else if (!stat && it < np + nrel) {
         const uint32_t r = it - np;
         int lo = 0, hi = nseg - 1;   // last segment with seg_off <= r
         while (lo < hi) {
@@ -1319,7 +1330,7 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
         const uint32_t slot = M.arena[X.seg_base[lo] + (r - X.seg_off[lo])];
         if (label_insert(M, slot, L)) { tnew = t; snew = slot; delta++; }
         if (label_tomb(M, slot, X.seg_phys[lo])) delta--;
-      } else if (it < total) {
+      } else if (!stat && it < total) {
         const uint32_t r = it - np - nrel;
         int lo = 0, hi = ntgt - 1;   // last target with tg_mvoff <= r
         while (lo < hi) {
