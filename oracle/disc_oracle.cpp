@@ -266,6 +266,52 @@ extern "C" double ora_dot_pin(int32_t n, const double* a, const double* b) {
   return lane[0];
 }
 
+/* P:92 [§III-A] "filtered using a custom, parallelized CUDA implementation of the DBSCAN algorithm
+ * to remove noise"; "output labels equal those of the classic sequential DBSCAN".  The
+ * classic algorithm (Ester et al. 1996) written out: points visited in index order; an unvisited
+ * point with >= min_pts points within eps (itself included) starts a new cluster, which is expanded
+ * breadth-first through core points; non-core points reached get the cluster (once) -- a border
+ * point thus belongs to the first cluster that reaches it; the rest is noise.  R42: squared fp64
+ * distance of the fp32 points, summed x, y, z, compared with (double)eps^2. */
+extern "C" int32_t ora_dbscan(int64_t n, const float* pts, float eps, int32_t min_pts, int32_t* labels) {
+  const double e2 = (double)eps * (double)eps;
+  auto d2 = [&](int64_t a, int64_t b) {
+    double s = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      const double x = (double)pts[3 * a + k] - (double)pts[3 * b + k];
+      s = s + x * x;
+    }
+    return s;
+  };
+  auto neigh = [&](int64_t a) {
+    std::vector<int64_t> out;
+    for (int64_t b = 0; b < n; ++b)
+      if (d2(a, b) <= e2) out.push_back(b);
+    return out;
+  };
+  constexpr int32_t UNSEEN = -2, NOISE = -1;
+  for (int64_t i = 0; i < n; ++i) labels[i] = UNSEEN;
+  int32_t C = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (labels[i] != UNSEEN) continue;
+    std::vector<int64_t> N = neigh(i);
+    if ((int64_t)N.size() < min_pts) { labels[i] = NOISE; continue; }
+    const int32_t c = C++;
+    labels[i] = c;
+    std::deque<int64_t> q(N.begin(), N.end());
+    while (!q.empty()) {
+      const int64_t j = q.front();
+      q.pop_front();
+      if (labels[j] == NOISE) labels[j] = c;   // border point (or a core point seen as noise earlier: impossible)
+      if (labels[j] != UNSEEN) continue;
+      labels[j] = c;
+      std::vector<int64_t> Nj = neigh(j);
+      if ((int64_t)Nj.size() >= min_pts) q.insert(q.end(), Nj.begin(), Nj.end());
+    }
+  }
+  return C;
+}
+
 /* ------------------------------------------------------------------------------------ */
 /* map                                                                                   */
 /* ------------------------------------------------------------------------------------ */
@@ -280,6 +326,7 @@ static bool valid_config(const ora_config* c) {
   if (!(c->mask_max_aspect >= 1.0f) || c->mask_min_area < 0) return false;
   if (!(c->cover_min >= 0.0f && c->cover_min <= 1.0f)) return false;
   if (!(c->lambda_size > 0.0f) || !(c->eps_distinct >= 0.0f)) return false;
+  if (!(c->dbscan_eps >= 0.0f) || (c->dbscan_eps > 0.0f && c->dbscan_min_pts < 1)) return false;
   if (c->feat_dim <= 0 || c->track_dim < 0) return false;
   return true;
 }
@@ -407,15 +454,39 @@ extern "C" int32_t ora_integrate(ora_map* m, const ora_frame* f, ora_report* rep
     return true;
   };
 
-  /* O3 detection voxel sets V_s, with O4 normal sums per (s, k) */
+  /* O3 detection voxel sets V_s, with O4 normal sums per (s, k).  With DBSCAN on (R42): only
+   * the pixels whose world points form the segment's largest DBSCAN cluster (by point count; ties:
+   * the first cluster created) contribute; a segment left without points is dropped ("nodepth"). */
   for (int32_t s = 0; s < S; ++s) {
     Det& d = det[s];
     if (d.status != ORA_KEPT) continue;
     const uint8_t* M = f->masks + (int64_t)s * HW;
+    std::vector<uint8_t> keep;   // DBSCAN: pixels of the kept cluster
+    if (c.dbscan_eps > 0.0f) {
+      std::vector<int64_t> pix;
+      std::vector<float> P3;
+      for (int64_t i = 0; i < HW; ++i)
+        if (M[i] && kvalid[i]) {
+          pix.push_back(i);
+          P3.insert(P3.end(), pw[i].begin(), pw[i].end());
+        }
+      std::vector<int32_t> lab(pix.size());
+      const int32_t nc = ora_dbscan((int64_t)pix.size(), P3.data(), c.dbscan_eps, c.dbscan_min_pts, lab.data());
+      std::vector<int64_t> size(nc, 0);
+      for (int32_t l : lab)
+        if (l >= 0) size[l]++;
+      int32_t best = -1;
+      for (int32_t k = 0; k < nc; ++k)
+        if (best < 0 || size[k] > size[best]) best = k;
+      keep.assign(HW, 0);
+      for (size_t q = 0; q < pix.size(); ++q)
+        if (best >= 0 && lab[q] == best) keep[pix[q]] = 1;
+    }
     for (int32_t v = 0; v < H; ++v)
       for (int32_t u = 0; u < W; ++u) {
         const int64_t i = (int64_t)v * W + u;
         if (!M[i] || !kvalid[i]) continue;
+        if (!keep.empty() && !keep[i]) continue;
         d.V.insert(key[i]);
         if (semantic) {
           double n[3];

@@ -35,6 +35,8 @@ typedef struct {
   float cover_min;         /* 0.25                               R17, R18  */
   float lambda_size;       /* 3.3     */
   float eps_distinct;      /* 1e-6                               R16       */
+  float dbscan_eps;        /* > 0: DBSCAN denoise (R42), metres; 0 = off (R7) */
+  int32_t dbscan_min_pts;  /* core threshold, neighbours incl. the point itself     */
   int32_t feat_dim;        /* Df > 0                                       */
   int32_t track_dim;       /* Dt >= 0, 0 = no visual gate                  */
 } ora_config;
@@ -99,6 +101,12 @@ int64_t ora_classify(const ora_map* m, const float* table, int32_t C, int32_t k,
 /* dense transfer (R40): nearest-voxel-centre instance of each point [P][3]
    (world, metres), -1 if farther than d_assign */
 void    ora_dense_transfer(const ora_map* m, const float* pts, int64_t P, float d_assign, int64_t* out);
+
+/* P:92 / S:123-131 DBSCAN (R42): the classic sequential algorithm over points [n][3] (fp32, taken
+   in index order), squared distances in fp64 (dx^2 + dy^2 + dz^2, no contraction) against
+   (double)eps^2, a point's neighbourhood including itself; labels[i] = cluster number in creation
+   order (0, 1, ...) or -1 (noise); returns the number of clusters */
+int32_t ora_dbscan(int64_t n, const float* pts, float eps, int32_t min_pts, int32_t* labels);
 
 /* ---- map state export ---- */
 int64_t ora_num_instances(const ora_map* m);

@@ -26,6 +26,7 @@ class OraConfig(C.Structure):
         ("depth_min", C.c_float), ("depth_max", C.c_float),
         ("mask_min_conf", C.c_float), ("mask_max_aspect", C.c_float), ("mask_min_area", C.c_int32),
         ("cover_min", C.c_float), ("lambda_size", C.c_float), ("eps_distinct", C.c_float),
+        ("dbscan_eps", C.c_float), ("dbscan_min_pts", C.c_int32),
         ("feat_dim", C.c_int32), ("track_dim", C.c_int32),
     ]
 
@@ -101,6 +102,7 @@ def lib():
             "ora_finalize": (I32, [P, F, F, I64, P]),
             "ora_classify": (I64, [P, P, I32, I32, P, P, P, I64]),
             "ora_dense_transfer": (None, [P, P, I64, F, P]),
+            "ora_dbscan": (I32, [I64, P, F, I32, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -120,7 +122,7 @@ def _c(a, dtype):
 
 DEFAULTS = dict(voxel_size=0.05, tau_geo=0.3, tau_vis=0.8, depth_min=0.1, depth_max=10.0,
                 mask_min_conf=0.5, mask_max_aspect=10.0, mask_min_area=400, cover_min=0.25,
-                lambda_size=3.3, eps_distinct=1e-6, feat_dim=64, track_dim=0)
+                lambda_size=3.3, eps_distinct=1e-6, dbscan_eps=0.0, dbscan_min_pts=8, feat_dim=64, track_dim=0)
 
 
 def make_config(**kw) -> OraConfig:
@@ -348,3 +350,11 @@ def dot_pin(a, b):
     a = np.ascontiguousarray(a, np.float64)
     b = np.ascontiguousarray(b, np.float64)
     return lib().ora_dot_pin(a.shape[0], _p(a), _p(b))
+
+
+def dbscan(points, eps: float, min_pts: int):
+    """Classic sequential DBSCAN labels (R42): cluster number in creation order or -1."""
+    pts = np.ascontiguousarray(points, np.float32).reshape(-1, 3)
+    lab = np.zeros(pts.shape[0], np.int32)
+    n = lib().ora_dbscan(pts.shape[0], _p(pts), eps, min_pts, _p(lab))
+    return lab, n
