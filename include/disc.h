@@ -62,6 +62,9 @@ typedef struct {
   float cover_min;         /* 0.25 (patch coverage threshold, inclusive)   R17, R18  */
   float lambda_size;       /* 3.3            */
   float eps_distinct;      /* 1e-6                                          Eq.1, R16        */
+  float dbscan_eps;        /* > 0: DBSCAN denoise of each segment's points before voxelisation */
+                           /* (R42): the largest cluster is kept; 0 = off (R7) */
+  int32_t dbscan_min_pts;  /* core threshold (points within eps, the point included), >= 1      */
   int32_t feat_dim;        /* Df in [4,1024], multiple of 4 (CLIP token width)               */
   int32_t track_dim;       /* Dt in [0,512]; 0 = no visual gate (DINO tracking width)        */
   /* capacities (device memory is sized from these at create time) */

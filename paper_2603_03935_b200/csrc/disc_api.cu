@@ -293,6 +293,8 @@ disc_status disc_config_init(disc_config* c) {
   c->cover_min = 0.25f;
   c->lambda_size = 3.3f;
   c->eps_distinct = 1e-6f;
+  c->dbscan_eps = 0.0f;      // R7: off unless asked for
+  c->dbscan_min_pts = 8;
   c->feat_dim = 1024;
   c->track_dim = 384;
   c->max_memberships = 1ll << 22;
@@ -318,6 +320,8 @@ static std::string validate_config(const disc_config* c) {
   if (!(c->mask_max_aspect >= 1.0f) || c->mask_min_area < 0) return "bad mask filter";
   if (!(c->cover_min >= 0.0f && c->cover_min <= 1.0f)) return "cover_min in [0,1]";
   if (!(c->lambda_size > 0.0f) || !(c->eps_distinct >= 0.0f)) return "bad lambda/eps";
+  if (!(c->dbscan_eps >= 0.0f) || !std::isfinite(c->dbscan_eps) || (c->dbscan_eps > 0.0f && c->dbscan_min_pts < 1))
+    return "dbscan_eps >= 0 (min_pts >= 1 when on)";
   if (c->feat_dim <= 0 || c->feat_dim % 4 != 0 || c->feat_dim > 1024)
     return "feat_dim must be a multiple of 4 in [4, 1024]";
   if (c->track_dim < 0 || c->track_dim > 512) return "track_dim must be in [0, 512]";
@@ -381,6 +385,7 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   P.dmin = cfg->depth_min; P.dmax = cfg->depth_max; P.min_conf = cfg->mask_min_conf;
   P.max_aspect = cfg->mask_max_aspect; P.cover_min = cfg->cover_min; P.lambda = cfg->lambda_size;
   P.eps = cfg->eps_distinct; P.min_area = cfg->mask_min_area; P.Df = cfg->feat_dim; P.Dt = cfg->track_dim;
+  P.db_eps = cfg->dbscan_eps; P.db_min = cfg->dbscan_min_pts;
 
   const int win = cfg->window, SM = cfg->max_masks, Df = cfg->feat_dim, Dt = cfg->track_dim;
   const int64_t PMAX = cfg->max_pairs_per_frame, PMP = cfg->max_patches;
@@ -428,6 +433,25 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(W.tok = dalloc<uint8_t>(m, (size_t)win * SM));
   chk(W.pmode = dalloc<uint8_t>(m, (size_t)win * SM));
   chk(W.k1ctr = dalloc<uint32_t>(m, 2));
+  if (cfg->dbscan_eps > 0.0f) {   // NEXT f3: per-frame (mask, point) records of the DBSCAN denoise
+    W.DBP = (int32_t)std::min<int64_t>(1 << 24, std::max<int64_t>(2 * (int64_t)cfg->max_pixels, PMAX));
+    const size_t nd = (size_t)win * W.DBP;
+    chk(W.dbk = dalloc<unsigned long long>(m, nd));
+    chk(W.dbv = dalloc<uint32_t>(m, nd));
+    chk(W.dbk2 = dalloc<unsigned long long>(m, nd));
+    chk(W.dbv2 = dalloc<uint32_t>(m, nd));
+    chk(W.dbx = dalloc<float4>(m, nd));
+    chk(W.dbpar = dalloc<uint32_t>(m, nd));
+    chk(W.dblab = dalloc<uint32_t>(m, nd));
+    chk(W.dbsz = dalloc<uint32_t>(m, nd));
+    chk(W.dbcore = dalloc<uint8_t>(m, nd));
+    chk(W.dbbest = dalloc<unsigned long long>(m, (size_t)win * SM));
+    chk(W.dbn = dalloc<uint32_t>(m, win));
+    chk(W.dbbeg = dalloc<int>(m, win));
+    chk(W.dbend = dalloc<int>(m, win));
+    W.dbtmp_bytes = dbscan_tmp_bytes((int)nd, win);
+    chk(W.dbtmp = dalloc<unsigned char>(m, W.dbtmp_bytes));
+  }
   W.MPIX = ((int64_t)cfg->max_pixels + 31) / 32 * 32;   // flat per-frame maps, sector-aligned
   chk(W.m0map = dalloc<uint16_t>(m, (size_t)win * W.MPIX));
   chk(W.s2bar = dalloc<uint32_t>(m, 1));

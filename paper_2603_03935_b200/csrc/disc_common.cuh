@@ -72,6 +72,8 @@ struct WinDesc {
 struct Params {                   // method constants
   float r, tau_geo, tau_vis, dmin, dmax, min_conf, max_aspect, cover_min, lambda, eps;
   int32_t min_area, Df, Dt;
+  float db_eps;                   // DBSCAN denoise (R42): 0 = off
+  int32_t db_min;
 };
 
 // ---- per-window stage-1 buffers (device pointers, strides per frame) -----------------
@@ -124,6 +126,23 @@ struct WinBufs {
   int32_t PC;                 // frame table capacity (power of 2)
   int32_t PMAX, SMAX, PMAXP, FCHUNKS;
   int32_t RCAP;               // record list capacity per frame (PMAX; DISC_K1_RCAP lowers it in tests)
+  // DBSCAN denoise (R42; allocated when dbscan_eps > 0): each frame's (mask, point) records
+  unsigned long long* dbk;    // [win][DBP] sort key: s << 56 | grid cell (3 x 18 bits)
+  uint32_t* dbv;              // [win][DBP] pixel index
+  unsigned long long* dbk2;   // [win][DBP] sorted keys
+  uint32_t* dbv2;             // [win][DBP] sorted pixel indices
+  float4* dbx;                // [win][DBP] world point of sorted position (w: pixel index bits)
+  uint32_t* dbpar;            // [win][DBP] union-find parent (sorted positions)
+  uint32_t* dblab;            // [win][DBP] cluster root position of a point, U32_EMPTY = noise
+  uint32_t* dbsz;             // [win][DBP] cluster sizes (at root positions)
+  uint8_t* dbcore;            // [win][DBP]
+  unsigned long long* dbbest; // [win][SMAX] (size << 32 | ~root pixel) of the kept cluster
+  uint32_t* dbn;              // [win] points per frame
+  int* dbbeg;                 // [win] segment offsets for the sort
+  int* dbend;
+  void* dbtmp;                // CUB temporary storage
+  size_t dbtmp_bytes;
+  int32_t DBP;                // points per frame capacity
 };
 
 // ---- map state ---------------------------------------------------------------------------

@@ -16,6 +16,9 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
                   bool release = false);
 int launch_stage2(const WinDesc& wd, const WinBufs& wb, const MapState& M, const FrameScratch& X, const Params& P,
                   bool sem, int nsm, int nres, cudaStream_t st);
+// NEXT f3 (k_dbscan.cu): DBSCAN denoise replacing K1b / K1c when P.db_eps > 0; returns launches
+int launch_dbscan(const WinDesc& wd, const WinBufs& wb, const Params& P, int* err, bool sem, int nsm, cudaStream_t st);
+size_t dbscan_tmp_bytes(int n_items, int n_seg);
 // the key-hash-sharded map (k_map.cu: stage-2 phases per frame; k_shard.cu: stage-1 exchange)
 // phase 0 lookup, 1 association (one CTA), 2 apply
 void launch_stage2_sharded_frame(int phase, int f, const FrameMeta* meta, const WinBufs& wb, const MapState& M,

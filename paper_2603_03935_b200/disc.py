@@ -31,7 +31,8 @@ class disc_config(C.Structure):
         ("voxel_size", C.c_float), ("tau_geo", C.c_float), ("tau_vis", C.c_float),
         ("depth_min", C.c_float), ("depth_max", C.c_float), ("mask_min_conf", C.c_float),
         ("mask_max_aspect", C.c_float), ("mask_min_area", C.c_int32), ("cover_min", C.c_float),
-        ("lambda_size", C.c_float), ("eps_distinct", C.c_float), ("feat_dim", C.c_int32),
+        ("lambda_size", C.c_float), ("eps_distinct", C.c_float), ("dbscan_eps", C.c_float),
+        ("dbscan_min_pts", C.c_int32), ("feat_dim", C.c_int32),
         ("track_dim", C.c_int32), ("max_memberships", C.c_int64), ("max_instances", C.c_int32),
         ("max_masks", C.c_int32), ("max_pixels", C.c_int32), ("max_patches", C.c_int32),
         ("max_pairs_per_frame", C.c_int32), ("window", C.c_int32), ("device", C.c_int32),
