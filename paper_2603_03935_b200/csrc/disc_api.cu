@@ -1417,6 +1417,7 @@ disc_status disc_get_stats(disc_map* m, disc_stats* s) {
     return cuda_check(m, "disc_get_stats");
   }
   if (getenv("DISC_K6PROF") || getenv("DISC_S2PROF")) k6_prof_dump();
+  if (getenv("DISC_SLOT_STATS") && !m->grp) slot_stats(m->M, m->last_stream);
   int64_t ctr[8];
   cudaMemcpy(ctr, m->M.counters, sizeof(ctr), cudaMemcpyDeviceToHost);
   m->stats.pairs = ctr[4];

@@ -77,6 +77,7 @@ int64_t run_classify(const MapState& M, int Df, int64_t next_id, const float* ta
                      size_t scratch_bytes);
 int run_dense_transfer(const MapState& M, float r, const float* pts_host, int64_t P, float d_assign, int64_t* out_host,
                        cudaStream_t st, void* scratch, size_t scratch_bytes);
+void slot_stats(const MapState& M, cudaStream_t st);   // DISC_SLOT_STATS diagnostic
 int32_t run_query(const MapState& M, int Df, int64_t next_id, const float* q_host, int32_t k, int64_t* ids,
                   float* scores, cudaStream_t st, void* scratch, size_t scratch_bytes);
 }  // namespace disc

@@ -1,5 +1,6 @@
 // k_query.cu -- off-path readers of the map: Q1 query, Q2 instance export
 // and the membership export used by the parity tests.
+#include <cstdio>
 #include <vector>
 
 #include <cub/cub.cuh>
@@ -386,6 +387,47 @@ int run_dense_transfer(const MapState& M, float r, const float* pts_host, int64_
   cudaMemcpyAsync(out_host, out, sizeof(int64_t) * P, cudaMemcpyDeviceToHost, st);
   cudaStreamSynchronize(st);
   return 0;
+}
+
+// Diagnostic (DISC_SLOT_STATS, printed by disc_get_stats): label-list shape over the voxel hash --
+// keys, live labels, tombstones, keys with overflow chunks, chunks on the longest list.
+__global__ void k_slot_stats(MapState M, unsigned long long* out) {
+  unsigned long long keys = 0, live = 0, tomb = 0, ovf = 0, maxch = 0;
+  for (uint64_t h = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; h < M.MC; h += (uint64_t)gridDim.x * blockDim.x) {
+    const KeySlot& ks = M.slots[h];
+    if (ks.key == KEY_EMPTY) continue;
+    ++keys;
+    for (int i = 0; i < INLINE_LABELS; ++i) {
+      if (ks.lab[i] == U32_EMPTY) break;
+      if (ks.lab[i] == LAB_TOMB) ++tomb; else ++live;
+    }
+    unsigned long long ch = 0;
+    for (uint32_t nx = ks.ovf; nx != U32_EMPTY; nx = M.ovf[nx].next) {
+      ++ch;
+      for (int i = 0; i < CHUNK_LABELS; ++i) {
+        const uint32_t L = M.ovf[nx].lab[i];
+        if (L == U32_EMPTY) break;
+        if (L == LAB_TOMB) ++tomb; else ++live;
+      }
+    }
+    if (ch) ++ovf;
+    maxch = max(maxch, ch);
+  }
+  atomicAdd(&out[0], keys); atomicAdd(&out[1], live); atomicAdd(&out[2], tomb); atomicAdd(&out[3], ovf);
+  atomicMax(&out[4], maxch);
+}
+
+void slot_stats(const MapState& M, cudaStream_t st) {
+  unsigned long long* d = nullptr;
+  unsigned long long h[5] = {0, 0, 0, 0, 0};
+  if (cudaMalloc(&d, sizeof(h)) != cudaSuccess) return;
+  cudaMemsetAsync(d, 0, sizeof(h), st);
+  k_slot_stats<<<1024, 256, 0, st>>>(M, d);
+  cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  cudaFree(d);
+  fprintf(stderr, "slot stats: keys %llu live labels %llu tombstones %llu keys with overflow chunks %llu longest chain %llu\n",
+          h[0], h[1], h[2], h[3], h[4]);
 }
 
 }  // namespace disc

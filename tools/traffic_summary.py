@@ -17,7 +17,7 @@ for mode, path in zip(["M1", "M2"], sys.argv[2:4]):
     for r in rows[h + 1:]:
         if len(r) < len(hdr):
             continue
-        k = r[ix["Kernel Name"]].split("(")[0].split("<")[0].replace("disc::", "")
+        k = r[ix["Kernel Name"]].split("(")[0].split("<")[0].replace("disc::", "").replace("void ", "").strip()
         v = r[ix["Metric Value"]].replace(",", "")
         try:
             per[k][r[ix["Metric Name"]]] += float(v)
