@@ -434,7 +434,8 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(W.pmode = dalloc<uint8_t>(m, (size_t)win * SM));
   chk(W.k1ctr = dalloc<uint32_t>(m, 2));
   if (cfg->dbscan_eps > 0.0f) {   // NEXT f3: per-frame (mask, point) records of the DBSCAN denoise
-    W.DBP = (int32_t)std::min<int64_t>(1 << 24, std::max<int64_t>(2 * (int64_t)cfg->max_pixels, PMAX));
+    // (overlapping masks put a pixel into several masks' clouds: up to 8 per pixel, or PMAX)
+    W.DBP = (int32_t)std::min<int64_t>(1 << 24, std::max<int64_t>((int64_t)std::min(SM, 8) * cfg->max_pixels, PMAX));
     const size_t nd = (size_t)win * W.DBP;
     chk(W.dbk = dalloc<unsigned long long>(m, nd));
     chk(W.dbv = dalloc<uint32_t>(m, nd));
