@@ -189,10 +189,13 @@ __device__ __forceinline__ void count_add(const FrameScratch& X, uint64_t code, 
 // LK_Q pairs per lane, their hash probes in lockstep, so each lane keeps LK_Q independent
 // memory chains in flight (the lookup is a latency chain: attributes -> slot -> labels ->
 // count table).
+#ifndef LK_AGG2
+#define LK_AGG2 1   // warp-aggregate the second label too (0: round-1 behaviour, per-lane shared atomics)
+#endif
 #ifndef LK_Q
 #define LK_Q 3   // unique (s, key) pairs per lane in flight (lookup; 4 held more registers than it hid latency)
 #endif
-__device__ unsigned long long g_lkprof[4];   // DISC_S2PROF: lookup sub-phases on CTA 0 (init, loop, flush)
+__device__ unsigned long long g_lkprof[8];   // DISC_S2PROF: lookup sub-phases on CTA 0 (init, loop, flush; loop steps 3..6)
 __device__ __forceinline__ void lk_probe(int i, unsigned long long& tp) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t_;
@@ -255,6 +258,7 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
         key[q] = wb.pkey[fo + idx[q]];
       }
     }
+    lk_probe(7, tp);   // pair records loaded
 #pragma unroll
     for (int q = 0; q < LK_Q; ++q) {
       act[q] = idx[q] < np && stf[s[q]] == 0;   // (a few L1 lines: no staging round trip)
@@ -283,9 +287,13 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
         else h[q] = (h[q] + 1) & hmask;
       }
     }
-    uint64_t first[LK_Q];
+    // each pair's first two live labels (s, j) are counted warp-aggregated (a frame's keys mostly carry
+    // one or two labels, and a warp's pairs mostly the same ones: per-lane shared atomics on one hot
+    // counter serialise); further labels (rare) directly
+    lk_probe(3, tp);   // status + probes done
+    uint64_t first[LK_Q], second[LK_Q];
 #pragma unroll
-    for (int q = 0; q < LK_Q; ++q) first[q] = KEY_EMPTY;   // each pair's first label (s, j), warp-aggregated
+    for (int q = 0; q < LK_Q; ++q) { first[q] = KEY_EMPTY; second[q] = KEY_EMPTY; }
 #pragma unroll
     for (int q = 0; q < LK_Q; ++q) {
       if (idx[q] < np) {
@@ -312,6 +320,7 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
         if (!ok[i]) continue;
         const uint64_t c = ((uint64_t)s[q] << 32) | id[i];
         if (nl == 0) first[q] = c;
+        else if (LK_AGG2 && nl == 1) second[q] = c;
         else cta_add(c, 1);
         nl++;
       }
@@ -325,6 +334,7 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
             if (L == LAB_TOMB) continue;
             const uint64_t c = ((uint64_t)s[q] << 32) | L;
             if (nl == 0) first[q] = c;
+            else if (LK_AGG2 && nl == 1) second[q] = c;
             else cta_add(c, 1);
             nl++;
           }
@@ -332,13 +342,21 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
         }
       }
     }
+    lk_probe(4, tp);   // labels walked, records stored
 #pragma unroll
-    for (int q = 0; q < LK_Q; ++q) {   // warp aggregation of the first label's count
+    for (int q = 0; q < LK_Q; ++q) {   // warp aggregation of the first (and second) label's count
       const unsigned peers = __match_any_sync(0xffffffffu, first[q]);
       if (first[q] != KEY_EMPTY && lane == __ffs(peers) - 1) cta_add(first[q], __popc(peers));
+      if (LK_AGG2) {
+        const unsigned p2 = __match_any_sync(0xffffffffu, second[q]);
+        if (second[q] != KEY_EMPTY && lane == __ffs(p2) - 1) cta_add(second[q], __popc(p2));
+      }
     }
+    lk_probe(5, tp);   // aggregated
   }
+  lk_probe(-1, tp);
   __syncthreads();
+  lk_probe(6, tp);   // barrier: the CTA's slowest warp
   lk_probe(1, tp);
   for (int i = threadIdx.x; i < LK_CT; i += blockDim.x)   // flush the CTA's counts
     if (cc[i]) count_add(X, ck[i], cc[i], M.err);
@@ -407,8 +425,10 @@ __device__ unsigned long long g_tgprof[4];   // DISC_S2PROF: target-update warp 
     }                                                                                        \
   } while (0)
 
+// fresh: the CTA's static shared counters are not known to be zero (first frame of a launch); later
+// frames find them zeroed by the previous frame's association, and skip one barrier
 __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBufs& wb, const MapState& M,
-                                         const FrameScratch& X, const Params& P, int sem) {
+                                         const FrameScratch& X, const Params& P, int sem, bool fresh = true) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // Layout: the shared-memory tables hold up to X.TCS (s, j) triples; a denser frame (hierarchical
   // SAM-"everything" masks overlapping many instances, BASELINE configs[4]) runs the same steps on
@@ -464,7 +484,7 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
   }
   if (tid == 0) {
     if (ntr_all > (uint32_t)X.TCAP) raise_err(M.err, DERR_TRIPLES);
-    n_j = 0; n_tgt = 0; n_seg = 0; rel_s = 0; merged_s = 0; edges_s = 0; n_cand = 0;
+    if (fresh) { n_j = 0; n_tgt = 0; n_seg = 0; rel_s = 0; merged_s = 0; edges_s = 0; n_cand = 0; }
     // the map counters this step reads, all in one round trip (only this thread writes 0, 1, 3,
     // 4, 6, 7; counter 2 is K7's)
     const int64_t c0 = M.counters[0], c1 = M.counters[1], c2 = M.counters[2], c3 = M.counters[3];
@@ -480,7 +500,7 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
     comp_best[i] = 0;
     comp_tgt[i] = -1;
   }
-  __syncthreads();   // counters above
+  if (fresh) __syncthreads();   // the zeroed counters above (n_cand before the triples' atomics)
   for (int i = tid; i < S; i += blockDim.x) {   // (loads in flight with the triples' below)
     has_edge[i] = 0;
     d_tgt[i] = -1;
@@ -874,6 +894,7 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
     *X.ntrip = 0;
   }
   __syncthreads();
+  if (tid == 0) { n_j = 0; n_tgt = 0; n_seg = 0; rel_s = 0; merged_s = 0; edges_s = 0; n_cand = 0; }   // next frame
   K6_PROBE(12);
 }
 
@@ -1480,8 +1501,9 @@ void k6_prof_dump() {
     fprintf(stderr, "s2 per-CTA work: lookup sum %llu max %llu, apply sum %llu max %llu\n", c[0], c[1], c[4], c[5]);
     cudaMemcpyFromSymbol(c, g_s2items, 4 * sizeof(unsigned long long));
     fprintf(stderr, "s2 K7 items: pairs %llu relabels %llu moves %llu targets %llu\n", c[0], c[1], c[2], c[3]);
-    cudaMemcpyFromSymbol(c, g_lkprof, 3 * sizeof(unsigned long long));
-    fprintf(stderr, "s2 lookup CTA0: init %llu loop %llu flush %llu\n", c[0], c[1], c[2]);
+    cudaMemcpyFromSymbol(c, g_lkprof, 8 * sizeof(unsigned long long));
+    fprintf(stderr, "s2 lookup CTA0 (thread 0): init %llu flush %llu | records %llu status+probes %llu labels %llu aggregate %llu wait-for-CTA %llu\n",
+            c[0], c[2], c[7], c[3], c[4], c[5], c[6]);
     cudaMemcpyFromSymbol(c, g_tgprof, 3 * sizeof(unsigned long long));
     fprintf(stderr, "s2 target warps: sum %llu max %llu count %llu\n", c[0], c[1], c[2]);
   }
@@ -1548,7 +1570,7 @@ __global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb
     grid_sync(wb.s2bar, G * ++ep);
     probe(0);
     if (blockIdx.x == 0) {
-      s2_assoc(f, F, wb, M, X, P, sem);
+      s2_assoc(f, F, wb, M, X, P, sem, f == 0);
     } else {
       if (P.Dt > 0) s2_gate(f, wb, M, X, P);
       if (f + 1 < wd.n) {

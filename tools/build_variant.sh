@@ -7,7 +7,7 @@ cd "$(dirname "$0")/../paper_2603_03935_b200/csrc"
 mkdir -p build/var_$tag
 A="-gencode arch=compute_100a,code=sm_100a"
 objs=""
-for src in disc_api k_frame k_map k_query; do
+for src in disc_api k_frame k_map k_query k_shard k_final k_dbscan; do
   /usr/local/cuda/bin/nvcc $A -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr "$@" -c $src.cu -o build/var_$tag/$src.o &
   objs="$objs build/var_$tag/$src.o"
 done
