@@ -65,6 +65,9 @@ typedef struct {
   float dbscan_eps;        /* > 0: DBSCAN denoise of each segment's points before voxelisation */
                            /* (R42): the largest cluster is kept; 0 = off (R7) */
   int32_t dbscan_min_pts;  /* core threshold (points within eps, the point included), >= 1      */
+  int32_t refine_active;   /* 1: after each frame's update, instance pairs of the frame's active   */
+                           /* set that pass the same test merge, to a fixpoint (S:327 step (3),    */
+                           /* P:98 "among all candidates"; R43); 0 = off (R14)                     */
   int32_t feat_dim;        /* Df in [4,1024], multiple of 4 (CLIP token width)               */
   int32_t track_dim;       /* Dt in [0,512]; 0 = no visual gate (DINO tracking width)        */
   /* capacities (device memory is sized from these at create time) */
@@ -123,6 +126,8 @@ typedef struct {                       /* per-frame report       
   int64_t new_memberships;             /* net growth of the membership relation             */
   int64_t relabeled;                   /* sum of |V_j| over merged-away instances j         */
   int64_t live_instances, live_memberships;
+  int64_t refine_rounds;               /* refine_active: rounds of instance-pair merges (R43) */
+  int64_t refine_merged;               /* refine_active: instances merged away by them        */
 } disc_frame_report;
 
 typedef struct {

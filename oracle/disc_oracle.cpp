@@ -678,6 +678,7 @@ extern "C" int32_t ora_integrate(ora_map* m, const ora_frame* f, ora_report* rep
   /* O12 apply */
   int64_t live_before = 0;
   for (const auto& kv : m->inst) live_before += (int64_t)kv.second.V.size();
+  std::map<Id, Id> merged_into;   // O12's erased ids -> their component root (refinement, R43)
   std::vector<std::vector<Id>> cJ(ncomp);
   std::vector<std::vector<int32_t>> cS(ncomp);
   for (const auto& kv : comp) {
@@ -732,6 +733,7 @@ extern "C" int32_t ora_integrate(ora_map* m, const ora_frame* f, ora_report* rep
         ids.insert(root);
       }
       m->inst.erase(J[a]);
+      merged_into[J[a]] = root;
       R.merged_away++;
     }
     for (int32_t s : Sd)
@@ -755,6 +757,92 @@ extern "C" int32_t ora_integrate(ora_map* m, const ora_frame* f, ora_report* rep
     m->inst.emplace(id, std::move(I));
     d.target = id;
     R.created++;
+  }
+
+  /* R43 (refine_active; S:327 step (3) "within the active set, merge existing instance pairs meeting
+   * the same (tau_geo, tau_vis) test, keeping the lower id and the higher-Q semantic feature; repeat
+   * pairwise merging until no pair qualifies"; "merged ... among all candidates").  Active set =
+   * the instances the frame's detections overlapped (the C triples' j, taken to their O12 survivor)
+   * and the frame's targets (survivors and new ids).  Rounds of R35's snapshot union-find over the
+   * active pairs (R36's test on c_ij = |V_i ∩ V_j|, R37's merge), the active set taken to the
+   * survivors after each round, until no active pair qualifies. */
+  if (c.refine_active) {
+    std::set<Id> A;
+    for (const auto& kv : C) {
+      Id j = kv.first.second;
+      auto it = merged_into.find(j);
+      A.insert(it == merged_into.end() ? j : it->second);
+    }
+    for (int32_t s = 0; s < S; ++s)
+      if (det[s].status == ORA_KEPT && det[s].target >= 0) A.insert(det[s].target);
+    while (true) {
+      std::map<Id, std::vector<Id>> adj;
+      int64_t nedge = 0;
+      for (auto ia = A.begin(); ia != A.end(); ++ia)
+        for (auto ib = std::next(ia); ib != A.end(); ++ib) {
+          const Inst& I = m->inst.at(*ia);
+          const Inst& J2 = m->inst.at(*ib);
+          std::vector<Key> out;
+          std::set_intersection(I.V.begin(), I.V.end(), J2.V.begin(), J2.V.end(), std::back_inserter(out));
+          const int64_t cij = (int64_t)out.size();
+          const int64_t mn = std::min((int64_t)I.V.size(), (int64_t)J2.V.size());
+          if (!(cij >= 1 && (double)cij >= (double)c.tau_geo * (double)mn)) continue;
+          if (Dt > 0) {
+            const double aa = ora_dot_pin(Dt, I.T.data(), I.T.data());
+            const double bb = ora_dot_pin(Dt, J2.T.data(), J2.T.data());
+            double cosv = -2.0;
+            if (aa > 0.0 && bb > 0.0) cosv = ora_dot_pin(Dt, I.T.data(), J2.T.data()) / std::sqrt(aa) / std::sqrt(bb);
+            if (!(cosv >= (double)c.tau_vis)) continue;
+          }
+          adj[*ia].push_back(*ib);
+          adj[*ib].push_back(*ia);
+          nedge++;
+        }
+      if (nedge == 0) break;
+      R.refine_rounds++;
+      std::set<Id> seen;
+      std::map<Id, Id> root_of;
+      for (const auto& kv : adj) {
+        if (seen.count(kv.first)) continue;
+        std::vector<Id> comp;
+        std::deque<Id> q{kv.first};
+        seen.insert(kv.first);
+        while (!q.empty()) {
+          const Id x = q.front();
+          q.pop_front();
+          comp.push_back(x);
+          for (Id y : adj[x])
+            if (!seen.count(y)) { seen.insert(y); q.push_back(y); }
+        }
+        std::sort(comp.begin(), comp.end());
+        const Id root = comp.front();
+        Inst& Rt = m->inst.at(root);
+        for (size_t a = 1; a < comp.size(); ++a) {
+          Inst& Ij = m->inst.at(comp[a]);
+          R.relabeled += (int64_t)Ij.V.size();
+          Rt.V.insert(Ij.V.begin(), Ij.V.end());
+          Rt.obs += Ij.obs;
+          Rt.last_seen = std::max(Rt.last_seen, Ij.last_seen);
+          for (int32_t k = 0; k < Dt; ++k) Rt.T[k] = Rt.T[k] + Ij.T[k];
+          if (Ij.Q > Rt.Q) { Rt.Q = Ij.Q; Rt.e = Ij.e; }
+          for (Obs& o : Ij.accept) add_accept(Rt, o.q, o.e);
+          for (const Key& k : Ij.V) {
+            auto& ids = m->mem[k];
+            ids.erase(comp[a]);
+            ids.insert(root);
+          }
+          m->inst.erase(comp[a]);
+          root_of[comp[a]] = root;
+          R.merged_away++;
+          R.refine_merged++;
+        }
+        for (int32_t s = 0; s < S; ++s)
+          if (det[s].target >= 0 && root_of.count(det[s].target)) det[s].target = root;
+      }
+      std::set<Id> A2;
+      for (Id a : A) A2.insert(root_of.count(a) ? root_of[a] : a);
+      A.swap(A2);
+    }
   }
 
   /* O13 report */

@@ -37,6 +37,7 @@ typedef struct {
   float eps_distinct;      /* 1e-6                               R16       */
   float dbscan_eps;        /* > 0: DBSCAN denoise (R42), metres; 0 = off (R7) */
   int32_t dbscan_min_pts;  /* core threshold, neighbours incl. the point itself     */
+  int32_t refine_active;   /* 1: per-frame instance x instance refinement (S:327 (3), R43) */
   int32_t feat_dim;        /* Df > 0                                       */
   int32_t track_dim;       /* Dt >= 0, 0 = no visual gate                  */
 } ora_config;
@@ -66,6 +67,8 @@ typedef struct {
   int64_t new_memberships;   /* net growth of the membership relation this frame           */
   int64_t relabeled;         /* sum of |V_j| over merged-away instances j                  */
   int64_t live_instances, live_memberships;
+  int64_t refine_rounds;     /* refine_active: union-find rounds that merged instance pairs     */
+  int64_t refine_merged;     /* refine_active: instances merged away by the refinement          */
 } ora_report;
 
 /* mask status codes (O1, O3, O7) */

@@ -26,7 +26,7 @@ class OraConfig(C.Structure):
         ("depth_min", C.c_float), ("depth_max", C.c_float),
         ("mask_min_conf", C.c_float), ("mask_max_aspect", C.c_float), ("mask_min_area", C.c_int32),
         ("cover_min", C.c_float), ("lambda_size", C.c_float), ("eps_distinct", C.c_float),
-        ("dbscan_eps", C.c_float), ("dbscan_min_pts", C.c_int32),
+        ("dbscan_eps", C.c_float), ("dbscan_min_pts", C.c_int32), ("refine_active", C.c_int32),
         ("feat_dim", C.c_int32), ("track_dim", C.c_int32),
     ]
 
@@ -48,6 +48,7 @@ REPORT_FIELDS = [
     ("key_out_of_range", C.c_int64), ("unique_pairs", C.c_int64), ("edges", C.c_int64),
     ("created", C.c_int64), ("merged_away", C.c_int64), ("new_memberships", C.c_int64),
     ("relabeled", C.c_int64), ("live_instances", C.c_int64), ("live_memberships", C.c_int64),
+    ("refine_rounds", C.c_int64), ("refine_merged", C.c_int64),
 ]
 
 
@@ -122,7 +123,7 @@ def _c(a, dtype):
 
 DEFAULTS = dict(voxel_size=0.05, tau_geo=0.3, tau_vis=0.8, depth_min=0.1, depth_max=10.0,
                 mask_min_conf=0.5, mask_max_aspect=10.0, mask_min_area=400, cover_min=0.25,
-                lambda_size=3.3, eps_distinct=1e-6, dbscan_eps=0.0, dbscan_min_pts=8, feat_dim=64, track_dim=0)
+                lambda_size=3.3, eps_distinct=1e-6, dbscan_eps=0.0, dbscan_min_pts=8, refine_active=0, feat_dim=64, track_dim=0)
 
 
 def make_config(**kw) -> OraConfig:

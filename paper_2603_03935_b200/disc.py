@@ -32,7 +32,7 @@ class disc_config(C.Structure):
         ("depth_min", C.c_float), ("depth_max", C.c_float), ("mask_min_conf", C.c_float),
         ("mask_max_aspect", C.c_float), ("mask_min_area", C.c_int32), ("cover_min", C.c_float),
         ("lambda_size", C.c_float), ("eps_distinct", C.c_float), ("dbscan_eps", C.c_float),
-        ("dbscan_min_pts", C.c_int32), ("feat_dim", C.c_int32),
+        ("dbscan_min_pts", C.c_int32), ("refine_active", C.c_int32), ("feat_dim", C.c_int32),
         ("track_dim", C.c_int32), ("max_memberships", C.c_int64), ("max_instances", C.c_int32),
         ("max_masks", C.c_int32), ("max_pixels", C.c_int32), ("max_patches", C.c_int32),
         ("max_pairs_per_frame", C.c_int32), ("window", C.c_int32), ("device", C.c_int32),
@@ -57,6 +57,7 @@ REPORT_FIELDS = [
     ("key_out_of_range", C.c_int64), ("unique_pairs", C.c_int64), ("edges", C.c_int64),
     ("created", C.c_int64), ("merged_away", C.c_int64), ("new_memberships", C.c_int64),
     ("relabeled", C.c_int64), ("live_instances", C.c_int64), ("live_memberships", C.c_int64),
+    ("refine_rounds", C.c_int64), ("refine_merged", C.c_int64),
 ]
 
 
