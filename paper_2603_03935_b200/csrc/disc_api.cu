@@ -295,6 +295,7 @@ disc_status disc_config_init(disc_config* c) {
   c->eps_distinct = 1e-6f;
   c->dbscan_eps = 0.0f;      // R7: off unless asked for
   c->dbscan_min_pts = 8;
+  c->refine_active = 0;      // R14 unless asked for (R43)
   c->feat_dim = 1024;
   c->track_dim = 384;
   c->max_memberships = 1ll << 22;
@@ -329,6 +330,7 @@ static std::string validate_config(const disc_config* c) {
   if (c->max_pixels < 1 || c->max_patches < 1) return "bad max_pixels / max_patches";
   if (c->max_pairs_per_frame < 1 || c->max_pairs_per_frame > (1 << 22)) return "max_pairs_per_frame in [1, 2^22]";
   if (c->window < 1 || c->window > MAXWIN) return "window in [1,32]";
+  if (c->refine_active != 0 && c->refine_active != 1) return "refine_active in {0, 1}";
   if (c->max_instances < 1 || c->max_instances > (1 << 30)) return "bad max_instances";
   // <= 2^28: the voxel hash (2^29 slots) and the key-list arena (8 * 2^28 + 2^20 entries) stay
   // indexable by 32-bit slot numbers / list offsets below the U32_EMPTY sentinel
@@ -385,7 +387,7 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   P.dmin = cfg->depth_min; P.dmax = cfg->depth_max; P.min_conf = cfg->mask_min_conf;
   P.max_aspect = cfg->mask_max_aspect; P.cover_min = cfg->cover_min; P.lambda = cfg->lambda_size;
   P.eps = cfg->eps_distinct; P.min_area = cfg->mask_min_area; P.Df = cfg->feat_dim; P.Dt = cfg->track_dim;
-  P.db_eps = cfg->dbscan_eps; P.db_min = cfg->dbscan_min_pts;
+  P.db_eps = cfg->dbscan_eps; P.db_min = cfg->dbscan_min_pts; P.refine = cfg->refine_active;
 
   const int win = cfg->window, SM = cfg->max_masks, Df = cfg->feat_dim, Dt = cfg->track_dim;
   const int64_t PMAX = cfg->max_pairs_per_frame, PMP = cfg->max_patches;
@@ -543,6 +545,24 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(X.nrel = dalloc<uint32_t>(m, 1));
   chk(X.work = dalloc<uint32_t>(m, 1));
   chk(X.rep = dalloc<disc_frame_report>(m, MAXWIN));
+  if (cfg->refine_active) {   // NEXT f2 buffers (k_refine)
+    X.RCAP = X.TCAP + SM;
+    X.RPC = (int32_t)next_pow2(std::max<int64_t>(1 << 16, 4 * (int64_t)X.RCAP));
+    chk(X.rf_pkey = dalloc<unsigned long long>(m, X.RPC, 0xFF));
+    chk(X.rf_pcnt = dalloc<uint32_t>(m, X.RPC));
+    chk(X.rf_act = dalloc<uint32_t>(m, X.RCAP));
+    chk(X.rf_act2 = dalloc<uint32_t>(m, X.RCAP));
+    chk(X.rf_n = dalloc<uint32_t>(m, 8));
+    chk(X.rf_croot = dalloc<uint32_t>(m, X.RCAP));
+    chk(X.rf_cadd = dalloc<uint32_t>(m, X.RCAP));
+    chk(X.rf_cbase = dalloc<uint32_t>(m, X.RCAP));
+    chk(X.rf_coff = dalloc<unsigned long long>(m, X.RCAP));
+    chk(X.rf_sL = dalloc<uint32_t>(m, X.RCAP));
+    chk(X.rf_sc = dalloc<uint32_t>(m, X.RCAP));
+    chk(X.rf_sbase = dalloc<unsigned long long>(m, X.RCAP));
+    chk(X.rf_slen = dalloc<uint32_t>(m, X.RCAP));
+    chk(X.rf_spre = dalloc<uint32_t>(m, X.RCAP + 1));
+  }
   chk(X.live_before = dalloc<int64_t>(m, 1));
   chk(X.ntrip_last = dalloc<uint32_t>(m, 1));
   {
@@ -684,6 +704,7 @@ static void group_destroy(disc_map* m) {
 
 static disc_status group_create(const disc_config* cfg, disc_map** out) {
   const int G = cfg->world_size;
+  if (cfg->refine_active) return DISC_ERR_UNSUPPORTED;   // (the refinement's key lists span every shard)
   const bool nccl = cfg->nccl_unique_id != nullptr;
   if (G < 2 || G > MAX_LOCAL_SHARDS * 64) return DISC_ERR_INVALID;
   if (nccl ? (cfg->rank < 0 || cfg->rank >= G) : (cfg->rank != 0 || G > MAX_LOCAL_SHARDS)) return DISC_ERR_INVALID;

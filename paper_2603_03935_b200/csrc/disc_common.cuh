@@ -74,6 +74,7 @@ struct Params {                   // method constants
   int32_t min_area, Df, Dt;
   float db_eps;                   // DBSCAN denoise (R42): 0 = off
   int32_t db_min;
+  int32_t refine;                 // f2 active-set refinement (R43): 0 = off
 };
 
 // ---- per-window stage-1 buffers (device pointers, strides per frame) -----------------
@@ -224,6 +225,23 @@ struct FrameScratch {
   uint32_t* work;                // [1] K7 insert-chunk counter (zeroed by K6)
   disc_frame_report* rep;        // [MAXWIN] device reports
   int64_t* live_before;          // [1]
+  // NEXT f2: per-frame active-set refinement (refine_active; k_refine).  RCAP = TCAP + SMAX active
+  // instances at most, RPC-slot pair table
+  unsigned long long* rf_pkey;   // [RPC] (i << 32 | j), i < j
+  uint32_t* rf_pcnt;             // [RPC]
+  int32_t RPC, RCAP;
+  uint32_t* rf_act;              // [RCAP] active ids (unsorted), then ascending
+  uint32_t* rf_act2;             // [RCAP]
+  uint32_t* rf_n;                // [8]: 0 candidates, 1 edges, 2 components, 3 segments, 4 relabel items, 5 active
+  uint32_t* rf_croot;            // [RCAP] component root id
+  uint32_t* rf_cadd;             // [RCAP] new memberships of the root this round
+  uint32_t* rf_cbase;            // [RCAP] root's list length before
+  unsigned long long* rf_coff;   // [RCAP] root's list offset (after a move)
+  uint32_t* rf_sL;               // [RCAP] relabel segment: member's physical label
+  uint32_t* rf_sc;               // [RCAP]   its component
+  unsigned long long* rf_sbase;  // [RCAP]   its key list offset
+  uint32_t* rf_slen;             // [RCAP]   length
+  uint32_t* rf_spre;             // [RCAP + 1] item prefix
   uint32_t* ntrip_last;          // [1] (debug export)
 };
 

@@ -1532,7 +1532,7 @@ __device__ __forceinline__ void grid_sync(uint32_t* bar, uint32_t target) {
 // (K5 lookup with the previous frame's K7 tail, K6 association on CTA 0, K7 apply) in one
 // persistent launch.
 __global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb, MapState M, FrameScratch X,
-                                                        Params P, int sem, int prof, int spec) {
+                                                        Params P, int sem, int prof, int spec, int f0, int fn) {
   const uint32_t G = gridDim.x;
   uint32_t ep = 0;
   unsigned long long t_prev = 0;
@@ -1561,19 +1561,20 @@ __global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb
       c0 = t_;
     }
   };
-  for (int f = 0; f < wd.n; ++f) {
+  const int fe = f0 + fn;   // frames [f0, fe) of the window (refine_active: one per launch)
+  for (int f = f0; f < fe; ++f) {
     const FrameDesc& F = wd.f[f];
     cta_t(-1);
-    s2_lookup(f, wb, M, X, P.Dt, spec && f > 0 && G > 1);
-    if (f > 0) s2_finalize(f - 1, M, X);
+    s2_lookup(f, wb, M, X, P.Dt, spec && f > f0 && G > 1);
+    if (f > f0) s2_finalize(f - 1, M, X);
     cta_t(0);
     grid_sync(wb.s2bar, G * ++ep);
     probe(0);
     if (blockIdx.x == 0) {
-      s2_assoc(f, F, wb, M, X, P, sem, f == 0);
+      s2_assoc(f, F, wb, M, X, P, sem, f == f0);
     } else {
       if (P.Dt > 0) s2_gate(f, wb, M, X, P);
-      if (f + 1 < wd.n) {
+      if (f + 1 < fe) {
         if (spec) s2_spec(f + 1, wb, M);
         else s2_prefetch_hint(f + 1, wb, M);
       }
@@ -1586,7 +1587,7 @@ __global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb
     grid_sync(wb.s2bar, G * ++ep);
     probe(2);
   }
-  if (wd.n > 0) s2_finalize(wd.n - 1, M, X);
+  if (fe > f0) s2_finalize(fe - 1, M, X);
   if (prof && blockIdx.x == 0 && threadIdx.x == 0) {   // the kernel's own span (CTA 0)
     unsigned long long t_;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
@@ -1726,6 +1727,316 @@ void launch_finalize_sum(int f, const MapState& M, const FrameScratch& X, const 
   debug_check(st, "k_s2_finalize_sum", f);
 }
 
+// ------------------------------------------------------------------------------------------
+// NEXT f2 (refine_active, reading R43): after frame f's update, the instance pairs of the frame's
+// active set -- the instances its detections overlapped (the C triples' j, still alive) and its
+// targets (component roots, new ids) -- that pass R36's test (the association's tau_geo / tau_vis)
+// merge into their min id (R37), in rounds until no active pair qualifies (S:327 step (3)).
+// One cooperative kernel per frame, rounds looped on the device:
+//   active set (generation stamps, ids sorted by rank) -> pair counts c_ij from the key lists of
+//   the active instances (each shared key counted from the lower id's list) -> R36 test, lock-free
+//   union-find rooted at the min id -> warp per component: T summed in ascending id order, (e, Q)
+//   replaced iff strictly higher, obs summed, last_seen max, AABB union, the root's key list sized for
+//   the merge -> relabel items (the members' key lists): the root's label inserted (appended to its
+//   list when new), the member's tombstoned -> |V|, list lengths, counters, report.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void rf_pair_add(const FrameScratch& X, unsigned long long code, int* err) {
+  uint32_t h = (uint32_t)mix64(code) & (uint32_t)(X.RPC - 1);
+  for (int probe = 0; probe < X.RPC; ++probe) {
+    unsigned long long k = __ldcg(&X.rf_pkey[h]);
+    if (k == KEY_EMPTY) {
+      k = atomicCAS(&X.rf_pkey[h], KEY_EMPTY, code);
+      if (k == KEY_EMPTY) k = code;
+    }
+    if (k == code) {
+      atomicAdd(&X.rf_pcnt[h], 1u);
+      return;
+    }
+    h = (h + 1) & (uint32_t)(X.RPC - 1);
+  }
+  raise_err(err, DERR_TRIPLES);
+}
+
+__device__ uint32_t rf_find(int32_t* par, uint32_t x) {
+  while (true) {
+    const uint32_t p = (uint32_t)__ldcg(&par[x]);
+    if (p == x) return x;
+    const uint32_t gp = (uint32_t)__ldcg(&par[p]);
+    if (gp != p) atomicCAS(&par[x], (int32_t)p, (int32_t)gp);
+    x = p;
+  }
+}
+
+__global__ void __launch_bounds__(K6_THREADS, 1) k_refine(int f, WinBufs wb, MapState M, FrameScratch X, Params P) {
+  const uint32_t G = gridDim.x;
+  uint32_t ep = 0;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t gt = blockIdx.x * blockDim.x + tid, gn = G * blockDim.x;
+  const uint32_t gw = gt >> 5, gwn = gn >> 5;
+  const int Dt = P.Dt, Df = P.Df;
+  __shared__ uint32_t gen_s;
+  // ---- active set: frame targets and the triples' (still alive) instances, deduplicated ----
+  if (tid == 0) gen_s = (uint32_t)(__ldcg((const unsigned long long*)&M.counters[3]) + 1);
+  __syncthreads();
+  const uint32_t gen = gen_s;
+  const uint32_t ntr = min(__ldcg(X.ntrip_last), (uint32_t)X.TCAP);
+  const int ntg = *X.ntgt;
+  for (uint32_t i = gt; i < ntr + (uint32_t)ntg; i += gn) {
+    const uint32_t j = i < ntr ? X.trip_j[i] : X.tgt_root[i - ntr];
+    if (!M.alive[j]) continue;
+    if (atomicExch(&M.stamp[j], gen) != gen) {
+      const uint32_t a = atomicAdd(&X.rf_n[5], 1u);
+      if (a < (uint32_t)X.RCAP) X.rf_act[a] = j;
+      else raise_err(M.err, DERR_TRIPLES);
+    }
+  }
+  grid_sync(wb.s2bar, G * ++ep);
+  if (gt == 0) M.counters[3] = gen;   // (the next frame's association takes gen + 1)
+  disc_frame_report& R = X.rep[f];
+  for (int round = 0;; ++round) {
+    // active ids ascending (rank sort: a few hundred at most), union-find reset, counters reset
+    const uint32_t nact = min(__ldcg(&X.rf_n[5]), (uint32_t)X.RCAP);
+    for (uint32_t a = gt; a < nact; a += gn) {
+      const uint32_t v = __ldcg(&X.rf_act[a]);
+      uint32_t rk = 0;
+      for (uint32_t b = 0; b < nact; ++b) rk += __ldcg(&X.rf_act[b]) < v;
+      X.rf_act2[rk] = v;
+      M.local[v] = (int32_t)v;   // union-find parent
+    }
+    if (gt == 0) { X.rf_n[1] = 0; X.rf_n[2] = 0; X.rf_n[3] = 0; }
+    grid_sync(wb.s2bar, G * ++ep);
+    // pair counts over the active instances' key lists: key k of V_i with an active label j > i
+    for (uint32_t a = blockIdx.x; a < nact; a += G) {
+      const uint32_t i = __ldcg(&X.rf_act2[a]);
+      const uint32_t Li = M.phys_of[i];
+      const unsigned long long off = M.lst_off[Li];
+      const uint32_t len = M.lst_len[Li];
+      for (uint32_t k = tid; k < len; k += blockDim.x) {
+        const uint32_t slot = M.arena[off + k];
+        const uint32_t* labs = M.slots[slot].lab;
+        int nl = INLINE_LABELS;
+        uint32_t nx = M.slots[slot].ovf;
+        bool done = false;
+        while (!done) {
+          for (int c = 0; c < nl; ++c) {
+            const uint32_t L = __ldcg(&labs[c]);
+            if (L == U32_EMPTY) { done = true; break; }
+            if (L == LAB_TOMB || L == Li) continue;
+            const uint32_t j = M.id_of[L];
+            if (j > i && __ldcg(&M.stamp[j]) == gen && M.alive[j]) rf_pair_add(X, ((unsigned long long)i << 32) | j, M.err);
+          }
+          if (done || nx == U32_EMPTY) break;
+          labs = M.ovf[nx].lab;
+          nl = CHUNK_LABELS;
+          nx = __ldcg(&M.ovf[nx].next);
+        }
+      }
+    }
+    grid_sync(wb.s2bar, G * ++ep);
+    // R36 test (warp per pair-table slot), union at the min id; the table is emptied
+    for (uint32_t e = gw; e < (uint32_t)X.RPC; e += gwn) {
+      const unsigned long long code = __ldcg(&X.rf_pkey[e]);
+      if (code == KEY_EMPTY) continue;
+      const uint32_t c = __ldcg(&X.rf_pcnt[e]);
+      const uint32_t i = (uint32_t)(code >> 32), j = (uint32_t)code;
+      const int64_t mn = min(M.vcount[i], M.vcount[j]);
+      bool ok = c >= 1 && (double)c >= (double)P.tau_geo * (double)mn;
+      if (ok && Dt > 0) {
+        const double ti = M.TT[i], tj = M.TT[j];
+        const double d = dot_pin_reg(M.T + (size_t)i * Dt, M.T + (size_t)j * Dt, Dt);
+        double cosv = -2.0;
+        if (ti > 0.0 && tj > 0.0) cosv = __ddiv_rn(__ddiv_rn(d, __dsqrt_rn(ti)), __dsqrt_rn(tj));
+        ok = cosv >= (double)P.tau_vis;
+      }
+      if (lane == 0) {
+        if (ok) {
+          atomicAdd(&X.rf_n[1], 1u);
+          uint32_t a = i, b = j;
+          while (true) {
+            a = rf_find(M.local, a);
+            b = rf_find(M.local, b);
+            if (a == b) break;
+            if (a > b) { const uint32_t t = a; a = b; b = t; }
+            if (atomicCAS(&M.local[b], (int32_t)b, (int32_t)a) == (int32_t)b) break;
+          }
+        }
+        X.rf_pkey[e] = KEY_EMPTY;
+        X.rf_pcnt[e] = 0;
+      }
+      __syncwarp();
+    }
+    grid_sync(wb.s2bar, G * ++ep);
+    if (__ldcg(&X.rf_n[1]) == 0) break;   // fixpoint (uniform)
+    // warp per component root (ascending member order = the sorted active list)
+    for (uint32_t a = gw; a < nact; a += gwn) {
+      const uint32_t r = __ldcg(&X.rf_act2[a]);
+      if (rf_find(M.local, r) != r) continue;   // a member, not a root
+      uint32_t nm = 0;
+      for (uint32_t b = lane; b < nact; b += 32) nm += (X.rf_act2[b] != r && rf_find(M.local, X.rf_act2[b]) == r);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) nm += __shfl_xor_sync(0xffffffffu, nm, o);
+      if (nm == 0) continue;
+      // T: ((T_r + T_m1) + T_m2) ..., members ascending
+      for (int d = lane; d < Dt; d += 32) {
+        double acc = M.T[(size_t)r * Dt + d];
+        for (uint32_t b = 0; b < nact; ++b) {
+          const uint32_t m = X.rf_act2[b];
+          if (m != r && rf_find(M.local, m) == r) acc = __dadd_rn(acc, M.T[(size_t)m * Dt + d]);
+        }
+        M.T[(size_t)r * Dt + d] = acc;
+      }
+      __syncwarp();
+      if (Dt > 0) {
+        const double tt = dot_pin_reg(M.T + (size_t)r * Dt, M.T + (size_t)r * Dt, Dt);
+        if (lane == 0) M.TT[r] = tt;
+      }
+      // (e, Q), obs, last_seen, AABB, key-list capacity, relabel segments (lane 0, ascending)
+      uint32_t src = r, base_w = 0;
+      unsigned long long off_w = 0, noff_w = 0;
+      if (lane == 0) {
+        float q = M.q[r];
+        int obs = M.obs[r];
+        int64_t ls = M.last_seen[r];
+        int32_t ab[6];
+        for (int k = 0; k < 6; ++k) ab[k] = M.aabb[(size_t)r * 6 + k];
+        const uint32_t Lr = M.phys_of[r];
+        const uint32_t base = M.lst_len[Lr], cap = M.lst_cap[Lr];
+        const unsigned long long off = M.lst_off[Lr];
+        uint64_t need = base;
+        unsigned long long rel = 0;
+        const uint32_t c = atomicAdd(&X.rf_n[2], 1u);
+        for (uint32_t b = 0; b < nact; ++b) {
+          const uint32_t m = X.rf_act2[b];
+          if (m == r || rf_find(M.local, m) != r) continue;
+          if (M.q[m] > q) { q = M.q[m]; src = m; }
+          obs += M.obs[m];
+          ls = max(ls, M.last_seen[m]);
+          for (int k = 0; k < 3; ++k) {
+            ab[k] = min(ab[k], M.aabb[(size_t)m * 6 + k]);
+            ab[3 + k] = max(ab[3 + k], M.aabb[(size_t)m * 6 + 3 + k]);
+          }
+          const uint32_t Lm = M.phys_of[m];
+          const uint32_t sg = atomicAdd(&X.rf_n[3], 1u);
+          if (sg < (uint32_t)X.RCAP) {
+            X.rf_sL[sg] = Lm;
+            X.rf_sc[sg] = c;
+            X.rf_sbase[sg] = M.lst_off[Lm];
+            X.rf_slen[sg] = M.lst_len[Lm];
+          } else {
+            raise_err(M.err, DERR_TRIPLES);
+          }
+          need += M.lst_len[Lm];
+          rel += (unsigned long long)M.vcount[m];
+          M.lst_len[Lm] = 0;
+          M.lst_cap[Lm] = 0;
+          M.alive[m] = 0;
+          M.phys_of[m] = U32_EMPTY;
+        }
+        unsigned long long noff = off;
+        if (need > cap) {   // the root's list moves to a region sized for the merge (old entries copied below)
+          const uint32_t nc = (uint32_t)max(max(2ull * cap, (unsigned long long)need), 64ull);
+          const unsigned long long o = atomicAdd(M.arena_top, (unsigned long long)nc);
+          if (o + nc > M.ARENA) {
+            raise_err(M.err, DERR_ARENA);
+          } else {
+            noff = o;
+            M.lst_off[Lr] = o;
+            M.lst_cap[Lr] = nc;
+          }
+        }
+        X.rf_croot[c] = r;
+        X.rf_cbase[c] = base;
+        X.rf_coff[c] = noff;
+        X.rf_cadd[c] = 0;
+        M.q[r] = q;
+        M.obs[r] = obs;
+        M.last_seen[r] = ls;
+        for (int k = 0; k < 6; ++k) M.aabb[(size_t)r * 6 + k] = ab[k];
+        atomicAdd((unsigned long long*)&R.merged_away, (unsigned long long)nm);
+        atomicAdd((unsigned long long*)&R.refine_merged, (unsigned long long)nm);
+        atomicAdd((unsigned long long*)&R.relabeled, rel);
+        base_w = base;
+        off_w = off;
+        noff_w = noff;
+      }
+      src = __shfl_sync(0xffffffffu, src, 0);
+      base_w = __shfl_sync(0xffffffffu, base_w, 0);
+      off_w = __shfl_sync(0xffffffffu, off_w, 0);
+      noff_w = __shfl_sync(0xffffffffu, noff_w, 0);
+      if (noff_w != off_w)   // the moved list's old entries, copied by the warp
+        for (uint32_t k = lane; k < base_w; k += 32) M.arena[noff_w + k] = M.arena[off_w + k];
+      if (src != r)
+        for (int d = lane; d < Df; d += 32) M.E[(size_t)r * Df + d] = M.E[(size_t)src * Df + d];
+    }
+    grid_sync(wb.s2bar, G * ++ep);
+    // relabel segment prefix (a few hundred segments: one thread)
+    const uint32_t nseg = min(__ldcg(&X.rf_n[3]), (uint32_t)X.RCAP);
+    if (gt == 0) {
+      uint32_t acc = 0;
+      for (uint32_t g = 0; g < nseg; ++g) { X.rf_spre[g] = acc; acc += X.rf_slen[g]; }
+      X.rf_spre[nseg] = acc;
+    }
+    grid_sync(wb.s2bar, G * ++ep);
+    // relabel items: the root's label onto each member key (appended to the root's list when new),
+    // the member's label tombstoned
+    const uint32_t nit = __ldcg(&X.rf_spre[nseg]);
+    int delta = 0;
+    for (uint32_t it = gt; it < nit; it += gn) {
+      int lo = 0, hi = (int)nseg - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldcg(&X.rf_spre[mid]) <= it) lo = mid;
+        else hi = mid - 1;
+      }
+      const uint32_t c = X.rf_sc[lo];
+      const uint32_t slot = M.arena[X.rf_sbase[lo] + (it - X.rf_spre[lo])];
+      const uint32_t Lr = M.phys_of[X.rf_croot[c]];
+      if (label_insert(M, slot, Lr)) {
+        const uint32_t pos = atomicAdd(&X.rf_cadd[c], 1u);
+        M.arena[X.rf_coff[c] + X.rf_cbase[c] + pos] = slot;
+        ++delta;
+      }
+      if (label_tomb(M, slot, X.rf_sL[lo])) --delta;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) delta += __shfl_xor_sync(0xffffffffu, delta, o);
+    if (lane == 0 && delta) atomicAdd((unsigned long long*)&M.counters[2], (unsigned long long)(int64_t)delta);
+    grid_sync(wb.s2bar, G * ++ep);
+    // tails: the roots' |V| and list lengths; the active set keeps the survivors
+    const uint32_t ncomp = min(__ldcg(&X.rf_n[2]), (uint32_t)X.RCAP);
+    for (uint32_t c = gt; c < ncomp; c += gn) {
+      const uint32_t r = X.rf_croot[c];
+      const uint32_t add = X.rf_cadd[c];
+      M.lst_len[M.phys_of[r]] = X.rf_cbase[c] + add;
+      M.vcount[r] += add;
+    }
+    if (gt == 0) {
+      R.refine_rounds += 1;
+      uint32_t w = 0;
+      for (uint32_t a = 0; a < nact; ++a)
+        if (M.alive[X.rf_act2[a]]) X.rf_act[w++] = X.rf_act2[a];
+      X.rf_n[5] = w;
+      M.counters[1] -= (int64_t)(nact - w);
+    }
+    grid_sync(wb.s2bar, G * ++ep);
+  }
+  if (gt == 0) {   // the report's live counts after the refinement
+    R.live_instances = M.counters[1];
+    R.live_memberships = M.counters[2];
+    R.new_memberships = M.counters[2] - *X.live_before;
+    X.rf_n[5] = 0;
+  }
+}
+
+void launch_refine(int f, const WinBufs& wb, const MapState& M, const FrameScratch& X, const Params& P, int grid,
+                   cudaStream_t st) {
+  cudaMemsetAsync(wb.s2bar, 0, sizeof(uint32_t), st);
+  int ff = f;
+  void* args[] = {(void*)&ff, (void*)&wb, (void*)&M, (void*)&X, (void*)&P};
+  cudaLaunchCooperativeKernel((const void*)k_refine, dim3(grid), dim3(K6_THREADS), args, 0, st);
+  debug_check(st, "k_refine", f);
+}
+
 int launch_stage2(const WinDesc& wd, const WinBufs& wb, const MapState& M, const FrameScratch& X, const Params& P,
                   bool sem, int nsm, int nres, cudaStream_t st) {
   const size_t sm6 = k6_smem_bytes(wb.SMAX, X.TCS);
@@ -1740,10 +2051,24 @@ int launch_stage2(const WinDesc& wd, const WinBufs& wb, const MapState& M, const
   // be guaranteed, not assumed
   int semi = sem ? 1 : 0;
   static const int spec = getenv("DISC_S2_SPEC") ? atoi(getenv("DISC_S2_SPEC")) : 1;   // speculative lookups
-  void* args[] = {(void*)&wd, (void*)&wb, (void*)&M, (void*)&X, (void*)&P, (void*)&semi, (void*)&prof, (void*)&spec};
-  cudaLaunchCooperativeKernel((const void*)k_stage2, dim3(grid), dim3(K6_THREADS), args, sm6, st);
-  debug_check(st, "k_stage2", -1);
-  return 1;
+  int f0 = 0, fn = wd.n;
+  void* args[] = {(void*)&wd, (void*)&wb, (void*)&M, (void*)&X, (void*)&P, (void*)&semi, (void*)&prof, (void*)&spec,
+                  (void*)&f0, (void*)&fn};
+  if (!P.refine) {
+    cudaLaunchCooperativeKernel((const void*)k_stage2, dim3(grid), dim3(K6_THREADS), args, sm6, st);
+    debug_check(st, "k_stage2", -1);
+    return 1;
+  }
+  // refine_active: each frame's update, then its refinement, before the next frame's lookup
+  for (int f = 0; f < wd.n; ++f) {
+    f0 = f;
+    fn = 1;
+    cudaMemsetAsync(wb.s2bar, 0, sizeof(uint32_t), st);
+    cudaLaunchCooperativeKernel((const void*)k_stage2, dim3(grid), dim3(K6_THREADS), args, sm6, st);
+    debug_check(st, "k_stage2", f);
+    launch_refine(f, wb, M, X, P, grid, st);
+  }
+  return 2 * wd.n;
 }
 
 }  // namespace disc
