@@ -14,7 +14,7 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
                   int maxHp, int maxW, int maxWp, int maxP, int rows_cap, int nsm, int nres, cudaStream_t st,
                   cudaEvent_t ev0, cudaEvent_t ev1, bool fill_ktab = true, bool fill_nsum = true,
                   bool release = false);
-void launch_refine(int f, const WinBufs& wb, const MapState& M, const FrameScratch& X, const Params& P, int grid,
+void launch_refine(int f, int S, const WinBufs& wb, const MapState& M, const FrameScratch& X, const Params& P, int grid,
                    cudaStream_t st);
 int launch_stage2(const WinDesc& wd, const WinBufs& wb, const MapState& M, const FrameScratch& X, const Params& P,
                   bool sem, int nsm, int nres, cudaStream_t st);

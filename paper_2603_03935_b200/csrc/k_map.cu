@@ -1767,7 +1767,7 @@ __device__ uint32_t rf_find(int32_t* par, uint32_t x) {
   }
 }
 
-__global__ void __launch_bounds__(K6_THREADS, 1) k_refine(int f, WinBufs wb, MapState M, FrameScratch X, Params P) {
+__global__ void __launch_bounds__(K6_THREADS, 1) k_refine(int f, int S, WinBufs wb, MapState M, FrameScratch X, Params P) {
   const uint32_t G = gridDim.x;
   uint32_t ep = 0;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -2010,6 +2010,10 @@ __global__ void __launch_bounds__(K6_THREADS, 1) k_refine(int f, WinBufs wb, Map
       M.lst_len[M.phys_of[r]] = X.rf_cbase[c] + add;
       M.vcount[r] += add;
     }
+    for (int s = (int)gt; s < S; s += (int)gn) {   // the detections' instances follow the merges (debug export)
+      const int64_t t = X.det_id[s];
+      if (t >= 0 && !M.alive[t]) X.det_id[s] = rf_find(M.local, (uint32_t)t);
+    }
     if (gt == 0) {
       R.refine_rounds += 1;
       uint32_t w = 0;
@@ -2028,11 +2032,11 @@ __global__ void __launch_bounds__(K6_THREADS, 1) k_refine(int f, WinBufs wb, Map
   }
 }
 
-void launch_refine(int f, const WinBufs& wb, const MapState& M, const FrameScratch& X, const Params& P, int grid,
+void launch_refine(int f, int S, const WinBufs& wb, const MapState& M, const FrameScratch& X, const Params& P, int grid,
                    cudaStream_t st) {
   cudaMemsetAsync(wb.s2bar, 0, sizeof(uint32_t), st);
-  int ff = f;
-  void* args[] = {(void*)&ff, (void*)&wb, (void*)&M, (void*)&X, (void*)&P};
+  int ff = f, SS = S;
+  void* args[] = {(void*)&ff, (void*)&SS, (void*)&wb, (void*)&M, (void*)&X, (void*)&P};
   cudaLaunchCooperativeKernel((const void*)k_refine, dim3(grid), dim3(K6_THREADS), args, 0, st);
   debug_check(st, "k_refine", f);
 }
@@ -2066,7 +2070,7 @@ int launch_stage2(const WinDesc& wd, const WinBufs& wb, const MapState& M, const
     cudaMemsetAsync(wb.s2bar, 0, sizeof(uint32_t), st);
     cudaLaunchCooperativeKernel((const void*)k_stage2, dim3(grid), dim3(K6_THREADS), args, sm6, st);
     debug_check(st, "k_stage2", f);
-    launch_refine(f, wb, M, X, P, grid, st);
+    launch_refine(f, wd.f[f].S, wb, M, X, P, grid, st);
   }
   return 2 * wd.n;
 }
