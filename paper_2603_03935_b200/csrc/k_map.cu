@@ -886,6 +886,8 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
     atomicAdd((unsigned long long*)&M.counters[6], (unsigned long long)acc);
     R.merged_away = (int64_t)merged_s;
     R.relabeled = (int64_t)rel_s;
+    R.refine_rounds = 0;   // (k_refine adds to these when refine_active)
+    R.refine_merged = 0;
     const int64_t live = cnt_s[1] - (int64_t)merged_s;
     M.counters[1] = live;
     R.live_instances = live;
