@@ -39,6 +39,11 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ float4 ld_f4_ef(const float4* p, uint64_t pol) {
   float4 r;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
@@ -915,8 +920,8 @@ __global__ void __launch_bounds__(K2_THREADS) k_pairs(WinDesc wd, WinBufs wb, Pa
 // ------------------------------------------------------------------------------------------
 constexpr int K3_ROWS = 64;
 
-__global__ void __launch_bounds__(256) k_fbar_part(WinDesc wd, WinBufs wb, int Df) {
-  const int f = blockIdx.y;
+__global__ void __launch_bounds__(256) k_fbar_part(WinDesc wd, WinBufs wb, int Df, int f0) {
+  const int f = f0 + blockIdx.y;   // frames [f0, f0 + gridDim.y): one L2-sized group (launch_stage1)
   if (f >= wd.n) return;
   const FrameDesc& F = wd.f[f];
   if (!F.feats) return;
@@ -926,7 +931,7 @@ __global__ void __launch_bounds__(256) k_fbar_part(WinDesc wd, WinBufs wb, int D
   if (p0 >= P) return;
   const int p1 = min(P, p0 + K3_ROWS);
   double* part = wb.fpart + ((size_t)f * wb.FCHUNKS + ch) * Df;
-  const uint64_t pol = policy_evict_first();
+  const uint64_t pol = policy_evict_last();   // the group's tokens stay in L2 for k_poolr's pass
   for (int d4 = threadIdx.x; d4 < Df / 4; d4 += blockDim.x) {
     double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
     for (int p = p0; p < p1; ++p) {
@@ -937,8 +942,8 @@ __global__ void __launch_bounds__(256) k_fbar_part(WinDesc wd, WinBufs wb, int D
   }
 }
 
-__global__ void __launch_bounds__(256) k_fbar(WinDesc wd, WinBufs wb, int Df) {
-  const int f = blockIdx.y;
+__global__ void __launch_bounds__(256) k_fbar(WinDesc wd, WinBufs wb, int Df, int f0) {
+  const int f = f0 + blockIdx.y;
   if (f >= wd.n) return;
   const FrameDesc& F = wd.f[f];
   if (!F.feats) return;
@@ -1138,8 +1143,8 @@ size_t k4r_smem_bytes(int Df, int Dt, bool bulk) {
 // BULK: a warp's patch rows (CLIP row + tracking row) arrive by bulk async copies into a
 // two-stage shared-memory ring, the next patch in flight while this one is reduced.
 template <bool SEM, bool BULK>
-__global__ void __launch_bounds__(K4R_WARPS * 32, K4R_MINB) k_poolr(WinDesc wd, WinBufs wb, Params P) {
-  const int f = blockIdx.y;
+__global__ void __launch_bounds__(K4R_WARPS * 32, K4R_MINB) k_poolr(WinDesc wd, WinBufs wb, Params P, int f0) {
+  const int f = f0 + blockIdx.y;
   if (f >= wd.n) return;
   const FrameDesc& F = wd.f[f];
   const int H = F.H, W = F.W, Hp = F.Hp, Wp = F.Wp, S = F.S, Df = P.Df, Dt = P.Dt;
@@ -1531,17 +1536,10 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
     debug_check(st, "k_release", -1);
     ++launches;
   }
-  if (sem) {
-    const int nch = (maxP + K3_ROWS - 1) / K3_ROWS;
-    k_fbar_part<<<dim3(nch, n), 256, 0, st>>>(wd, wb, P.Df);
-    debug_check(st, "k_fbar_part", -1);
-    k_fbar<<<dim3((P.Df + 255) / 256, n), 256, 0, st>>>(wd, wb, P.Df);
-    debug_check(st, "k_fbar", -1);
-  }
   int segs = 1;
   for (int i = 0; i < n; ++i)
     segs = std::max(segs, wd.f[i].Hp * ((wd.f[i].Wp + K4R_SEG - 1) / K4R_SEG));
-  const dim3 gpr((segs + K4R_WARPS - 1) / K4R_WARPS, n);
+  const int gx = (segs + K4R_WARPS - 1) / K4R_WARPS;
   // bulk path: 16-byte rows (Df % 4 == 0 holds; Dt % 8 == 0) and 16-byte aligned token arrays
   // the bulk-copy variant measured slower (fewer resident warps for its staging rings): opt-in
   static const bool bulk_ok = getenv("DISC_POOLR_BULK") != nullptr;
@@ -1563,9 +1561,21 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
   if (sem) {
     k_filter<true><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
     debug_check(st, "k_filter", -1);
-    if (bulk) k_poolr<true, true><<<gpr, K4R_WARPS * 32, smr, st>>>(wd, wb, P);
-    else k_poolr<true, false><<<gpr, K4R_WARPS * 32, smr, st>>>(wd, wb, P);
-    debug_check(st, "k_poolr", -1);
+    // Eq.1's mean f-bar and the pooling pass read the same CLIP tokens: run them per group of frames
+    // whose tokens fit in L2 (<= 48 MB), so the second read hits L2 (first read evict-last, second
+    // evict-first) instead of streaming the window's tokens from HBM twice
+    const int nch = (maxP + K3_ROWS - 1) / K3_ROWS;
+    const int64_t tok_bytes = std::max<int64_t>(1, (int64_t)maxP * P.Df * 4);
+    const int gsz = (int)std::max<int64_t>(1, std::min<int64_t>(n, (48ll << 20) / tok_bytes));
+    for (int g0 = 0; g0 < n; g0 += gsz) {
+      const int gn = std::min(gsz, n - g0);
+      k_fbar_part<<<dim3(nch, gn), 256, 0, st>>>(wd, wb, P.Df, g0);
+      k_fbar<<<dim3((P.Df + 255) / 256, gn), 256, 0, st>>>(wd, wb, P.Df, g0);
+      if (bulk) k_poolr<true, true><<<dim3(gx, gn), K4R_WARPS * 32, smr, st>>>(wd, wb, P, g0);
+      else k_poolr<true, false><<<dim3(gx, gn), K4R_WARPS * 32, smr, st>>>(wd, wb, P, g0);
+      launches += 3;
+    }
+    debug_check(st, "k_fbar_part / k_fbar / k_poolr", -1);
     k_dmap<<<n, 1024, 0, st>>>(wd, wb, P);
     debug_check(st, "k_dmap", -1);
     k_fallback<true><<<dim3(K4_CTAS, maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
@@ -1575,13 +1585,13 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
   } else {
     k_filter<false><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
     debug_check(st, "k_filter", -1);
-    if (bulk) k_poolr<false, true><<<gpr, K4R_WARPS * 32, smr, st>>>(wd, wb, P);
-    else k_poolr<false, false><<<gpr, K4R_WARPS * 32, smr, st>>>(wd, wb, P);
+    if (bulk) k_poolr<false, true><<<dim3(gx, n), K4R_WARPS * 32, smr, st>>>(wd, wb, P, 0);
+    else k_poolr<false, false><<<dim3(gx, n), K4R_WARPS * 32, smr, st>>>(wd, wb, P, 0);
     debug_check(st, "k_poolr", -1);
     k_finalize<false><<<dim3(maxS, n), K4_THREADS, 0, st>>>(wd, wb, P);
     debug_check(st, "k_finalize", -1);
   }
-  return (sem ? 12 : 8) + launches;   // the launches above on s1, counted exactly (bench.py reports them)
+  return (sem ? 9 : 8) + launches;   // the launches above on s1, counted exactly (bench.py reports them)
 }
 
 }  // namespace disc
