@@ -415,7 +415,9 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(W.bbox = dalloc<int32_t>(m, (size_t)win * SM * 4));
   chk(W.vs = dalloc<uint32_t>(m, (size_t)win * SM));
   chk(W.daabb = dalloc<int32_t>(m, (size_t)win * SM * 6));
-  chk(W.ang_sum = dalloc<float>(m, (size_t)win * SM));
+  chk(W.ang64 = dalloc<unsigned long long>(m, (size_t)win * SM));
+  chk(W.pw = dalloc<uint32_t>(m, (size_t)win * SM));
+  chk(W.xmax = dalloc<float>(m, (size_t)win));
   chk(W.ang_cnt = dalloc<uint32_t>(m, (size_t)win * SM));
   chk(W.oor = dalloc<unsigned long long>(m, win));
   chk(W.pkey = dalloc<unsigned long long>(m, (size_t)win * PMAX));
@@ -427,10 +429,11 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(W.fbar = dalloc<float>(m, (size_t)win * Df));
   chk(W.rp = dalloc<float>(m, (size_t)win * PMP));
   chk(W.rbar = dalloc<double>(m, (size_t)win));
-  chk(W.psum = dalloc<double>(m, (size_t)win * SM * 3));
+  chk(W.psum64 = dalloc<long long>(m, (size_t)win * SM * 3));
   chk(W.status = dalloc<int32_t>(m, (size_t)win * SM));
   chk(W.qf = dalloc<float>(m, (size_t)win * SM * 6));
   chk(W.emb = dalloc<float>(m, (size_t)win * SM * Df));
+  chk(W.emb64 = dalloc<long long>(m, (size_t)win * SM * Df));
   chk(W.trk = dalloc<double>(m, (size_t)win * SM * std::max(Dt, 1)));
   chk(W.tok = dalloc<uint8_t>(m, (size_t)win * SM));
   chk(W.pmode = dalloc<uint8_t>(m, (size_t)win * SM));

@@ -95,7 +95,7 @@ struct WinBufs {
   int32_t* bbox;              // [win][SMAX][4] umin, vmin, umax, vmax
   uint32_t* vs;               // [win][SMAX] |V_s|
   int32_t* daabb;             // [win][SMAX][6] key-space aabb of V_s
-  float* ang_sum;             // [win][SMAX]
+
   uint32_t* ang_cnt;          // [win][SMAX]
   unsigned long long* oor;    // [win] key_out_of_range
   // pair records for stage 2
@@ -109,7 +109,14 @@ struct WinBufs {
   float* fbar;                // [win][Df]
   float* rp;                  // [win][PMAXP] residual norms r_p (D_p after k_dmap)
   double* rbar;               // [win] mean r_p (Eq.1)
-  double* psum;               // [win][SMAX][3] R18 / R19 sums with r_p for D_p: weight sum, sum cover r, sum cover
+  // Order-independent (bit-reproducible) accumulation: the pooled sums, the R18 / R19 sums and the
+  // S_angle sums are 64-bit fixed point (integer atomics are associative), with a per-frame power-of-two
+  // scale from the tokens' largest |component| (xmax, k_fbar_part) -- see pool_scale()
+  long long* emb64;           // [win][SMAX][Df] pooled sum y_s x 2^ke
+  long long* psum64;          // [win][SMAX][3] R18 / R19 sums (with r_p for D_p) x 2^kp: weight, cover r, cover
+  unsigned long long* ang64;  // [win][SMAX] S_angle term sum x 2^40
+  uint32_t* pw;               // [win][SMAX] 1: some weight > 0 (R18: else unweighted pooling)
+  float* xmax;                // [win] max |token component| of the frame
   int32_t* status;            // [win][SMAX]
   float* qf;                  // [win][SMAX][6] s_size, s_angle, s_sem, s_dist, q, dbar
   float* emb;                 // [win][SMAX][Df]
@@ -254,6 +261,17 @@ struct FrameMeta {
 };
 
 // ---- helpers -------------------------------------------------------------------------
+// Fixed-point scales of a frame's pooling sums (powers of two: conversions are exact scalings before
+// one rounding).  |w x| <= |r| xmax <= 2 sqrt(Df) xmax^2 per term (r = |f_p - fbar|), summed over <= P
+// patches; the bound below (P 2 Df xmax^2) keeps every sum under 2^61.
+__host__ __device__ __forceinline__ int pool_scale_exp(int P, int Df, float xmax, bool cover) {
+  const double b = cover ? (double)P * (2.0 * (double)Df * (double)xmax + 1.0)
+                         : (double)P * 2.0 * (double)Df * (double)xmax * (double)xmax;
+  int e = 0;
+  frexp(b + 1.0, &e);   // b + 1 < 2^e
+  return 61 - e;
+}
+constexpr double ANG_SCALE = 1099511627776.0;   // 2^40: S_angle terms in [0, 1]
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x ^= x >> 30;
   x *= 0xbf58476d1ce4e5b9ull;

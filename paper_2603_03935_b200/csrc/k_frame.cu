@@ -70,9 +70,10 @@ __global__ void k_win_init(WinDesc wd, WinBufs wb) {
   for (int s = threadIdx.x + blockIdx.x * blockDim.x; s < S; s += blockDim.x * gridDim.x) {
     const size_t i = (size_t)f * wb.SMAX + s;
     wb.vs[i] = 0;
-    wb.ang_sum[i] = 0.f;
+    wb.ang64[i] = 0ull;
+    wb.pw[i] = 0u;
     wb.ang_cnt[i] = 0;
-    wb.psum[3 * i] = 0.0; wb.psum[3 * i + 1] = 0.0; wb.psum[3 * i + 2] = 0.0;
+    wb.psum64[3 * i] = 0; wb.psum64[3 * i + 1] = 0; wb.psum64[3 * i + 2] = 0;
     wb.bbox[4 * i + 0] = INT32_MAX;
     wb.bbox[4 * i + 1] = INT32_MAX;
     wb.bbox[4 * i + 2] = -1;
@@ -84,7 +85,7 @@ __global__ void k_win_init(WinDesc wd, WinBufs wb) {
   }
   // pooling / tracking accumulators of this frame's masks (k_pool reduces into them)
   for (size_t i = threadIdx.x + blockIdx.x * blockDim.x; i < (size_t)S * wd.Df; i += blockDim.x * gridDim.x)
-    wb.emb[(size_t)f * wb.SMAX * wd.Df + i] = 0.f;
+    wb.emb64[(size_t)f * wb.SMAX * wd.Df + i] = 0;
   for (size_t i = threadIdx.x + blockIdx.x * blockDim.x; i < (size_t)S * wd.Dt; i += blockDim.x * gridDim.x)
     wb.trk[(size_t)f * wb.SMAX * wd.Dt + i] = 0.0;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -92,6 +93,7 @@ __global__ void k_win_init(WinDesc wd, WinBufs wb) {
     wb.rcount[f] = 0;
     wb.oor[f] = 0;
     if (f == 0) { wb.k1ctr[0] = 0; wb.k1ctr[1] = 0; *wb.s2bar = 0; }   // K1a/K1b work counters, stage-2 barrier
+    wb.xmax[f] = 0.f;
   }
   // per-patch pixel counts are accumulated with atomics by K1: zero the rows this frame uses
   const int P = wd.f[f].Hp * wd.f[f].Wp;
@@ -888,13 +890,14 @@ __global__ void __launch_bounds__(K2_THREADS) k_pairs(WinDesc wd, WinBufs wb, Pa
         const int leader = __ffs(pending) - 1;
         const uint32_t s0 = __shfl_sync(0xffffffffu, sv, leader);
         const bool in = sv == s0;
-        float v = in ? term : 0.f;
+        // fixed point before any sum: the result does not depend on which warp a term lands in
+        unsigned long long v = in ? (unsigned long long)llrint((double)term * ANG_SCALE) : 0ull;
 #pragma unroll
         for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         const unsigned inb = __ballot_sync(0xffffffffu, in);
         if (lane == leader) {
           const size_t gi = (size_t)f * wb.SMAX + s0;
-          atomicAdd(&wb.ang_sum[gi], v);
+          atomicAdd(&wb.ang64[gi], v);
           atomicAdd(&wb.ang_cnt[gi], (uint32_t)__popc(inb));
         }
         pending &= ~inb;
@@ -932,14 +935,19 @@ __global__ void __launch_bounds__(256) k_fbar_part(WinDesc wd, WinBufs wb, int D
   const int p1 = min(P, p0 + K3_ROWS);
   double* part = wb.fpart + ((size_t)f * wb.FCHUNKS + ch) * Df;
   const uint64_t pol = policy_evict_last();   // the group's tokens stay in L2 for k_poolr's pass
+  float xm = 0.f;
   for (int d4 = threadIdx.x; d4 < Df / 4; d4 += blockDim.x) {
     double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
     for (int p = p0; p < p1; ++p) {
       const float4 x = ld_f4_ef((const float4*)(F.feats + (size_t)p * Df) + d4, pol);
       a0 += x.x; a1 += x.y; a2 += x.z; a3 += x.w;
+      xm = fmaxf(xm, fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
     }
     part[4 * d4 + 0] = a0; part[4 * d4 + 1] = a1; part[4 * d4 + 2] = a2; part[4 * d4 + 3] = a3;
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) xm = fmaxf(xm, __shfl_xor_sync(0xffffffffu, xm, o));
+  if ((threadIdx.x & 31) == 0 && xm > 0.f) atomicMax((int*)&wb.xmax[f], __float_as_int(xm));   // (>= 0: int order)
 }
 
 __global__ void __launch_bounds__(256) k_fbar(WinDesc wd, WinBufs wb, int Df, int f0) {
@@ -1181,22 +1189,32 @@ __global__ void __launch_bounds__(K4R_WARPS * 32, K4R_MINB) k_poolr(WinDesc wd, 
   const int rows = ((pr + 1) * H + Hp - 1) / Hp - (pr * H + Hp - 1) / Hp;
   int cur = -1;                     // mask whose sums the warp's slice holds
   double sc0 = 0, sc1 = 0, sc2 = 0; // its R18 / R19 scalar sums
+  bool scw = false;                 // some weight > 0 (R18)
+  const float xmx = pool ? __ldcg(&wb.xmax[f]) : 0.f;
+  const double se = ldexp(1.0, pool_scale_exp(Hp * Wp, Df, xmx, false));   // fixed-point scales (exact)
+  const double sp = ldexp(1.0, pool_scale_exp(Hp * Wp, Df, xmx, true));
+  auto fx = [&](float v) { return (unsigned long long)llrint((double)v * se); };
+  auto fxp = [&](double v) { return (unsigned long long)llrint(v * sp); };
   auto flush = [&]() {
     if (cur < 0) return;
     const size_t gi = gbase + cur;
     if (pool) {
-      float4* y = (float4*)(wb.emb + gi * Df);
+      unsigned long long* y = (unsigned long long*)(wb.emb64 + gi * Df);
       for (int d4 = lane; d4 < D4; d4 += 32) {
-        red_add4(&y[d4], ((float4*)ya)[d4]);
+        const float4 a = ((float4*)ya)[d4];
+        atomicAdd(&y[4 * d4 + 0], fx(a.x)); atomicAdd(&y[4 * d4 + 1], fx(a.y));
+        atomicAdd(&y[4 * d4 + 2], fx(a.z)); atomicAdd(&y[4 * d4 + 3], fx(a.w));
         ((float4*)ya)[d4] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
       if (lane == 0) {
-        double* ps = wb.psum + gi * 3;
-        atomicAdd(&ps[0], sc0);
-        atomicAdd(&ps[1], sc1);
-        atomicAdd(&ps[2], sc2);
+        unsigned long long* ps = (unsigned long long*)(wb.psum64 + gi * 3);
+        atomicAdd(&ps[0], fxp(sc0));
+        atomicAdd(&ps[1], fxp(sc1));
+        atomicAdd(&ps[2], fxp(sc2));
+        if (scw) wb.pw[gi] = 1u;
       }
     }
+    scw = false;
     double* u = wb.trk + gi * Dt;
     for (int d = lane; d < Dt; d += 32) {
       if (ua[d] != 0.0) atomicAdd(&u[d], ua[d]);
@@ -1296,6 +1314,7 @@ __global__ void __launch_bounds__(K4R_WARPS * 32, K4R_MINB) k_poolr(WinDesc wd, 
                 }
               }
               sc0 += (double)r * cov;
+              scw = scw || (r > 0.f && cov > 0.0);
             }
             sc1 += cov * (double)r;
             sc2 += cov;
@@ -1319,17 +1338,23 @@ __global__ void __launch_bounds__(K4R_WARPS * 32, K4R_MINB) k_poolr(WinDesc wd, 
           const size_t gi = gbase + s;
           if (pool) {
             if (use) {
-              float4* y = (float4*)(wb.emb + gi * Df);
+              unsigned long long* y = (unsigned long long*)(wb.emb64 + gi * Df);
 #pragma unroll
               for (int i = 0; i < 8; ++i)
-                if (i < nq4 && lane + 32 * i < D4)
-                  red_add4(&y[lane + 32 * i], make_float4(w * x[i].x, w * x[i].y, w * x[i].z, w * x[i].w));
+                if (i < nq4 && lane + 32 * i < D4) {
+                  const int d = 4 * (lane + 32 * i);
+                  atomicAdd(&y[d + 0], fx(w * x[i].x)); atomicAdd(&y[d + 1], fx(w * x[i].y));
+                  atomicAdd(&y[d + 2], fx(w * x[i].z)); atomicAdd(&y[d + 3], fx(w * x[i].w));
+                }
             }
             if (lane == 0) {
-              double* ps = wb.psum + gi * 3;
-              if (use) atomicAdd(&ps[0], (double)r * cov);
-              atomicAdd(&ps[1], cov * (double)r);
-              atomicAdd(&ps[2], cov);
+              unsigned long long* ps = (unsigned long long*)(wb.psum64 + gi * 3);
+              if (use) {
+                atomicAdd(&ps[0], fxp((double)r * cov));
+                if (r > 0.f && cov > 0.0) wb.pw[gi] = 1u;
+              }
+              atomicAdd(&ps[1], fxp(cov * (double)r));
+              atomicAdd(&ps[2], fxp(cov));
             }
           }
           double* u = wb.trk + gi * Dt;
@@ -1369,18 +1394,19 @@ __global__ void __launch_bounds__(K4_THREADS) k_fallback(WinDesc wd, WinBufs wb,
   const int s = blockIdx.y;
   if (s >= F.S || !F.feats) return;
   const size_t gi = (size_t)f * wb.SMAX + s;
-  if (wb.status[gi] != 0 || wb.psum[gi * 3] > 0.0) return;
+  if (wb.status[gi] != 0 || wb.pw[gi]) return;
   const int H = F.H, W = F.W, Hp = F.Hp, Wp = F.Wp, Df = P.Df;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const BoxPatches B(wb, gi, H, W, Hp, Wp);
   const int stride = K4_CTAS * K4_WARPS;
   const uint32_t* cnt = wb.cnt + (size_t)f * wb.SMAX * wb.PMAXP + (size_t)s * wb.PMAXP;
-  float* y = wb.emb + gi * Df;
+  unsigned long long* y = (unsigned long long*)(wb.emb64 + gi * Df);
+  const double se = ldexp(1.0, pool_scale_exp(Hp * Wp, Df, __ldcg(&wb.xmax[f]), false));
   for (int k = blockIdx.x * K4_WARPS + warp; k < B.n; k += stride) {
     const int p = B.patch(k, Wp);
     if (!cnt[p]) continue;
     const float* row = F.feats + (size_t)p * Df;
-    for (int d = lane; d < Df; d += 32) atomicAdd(&y[d], row[d]);
+    for (int d = lane; d < Df; d += 32) atomicAdd(&y[d], (unsigned long long)llrint((double)row[d] * se));
   }
 }
 
@@ -1398,8 +1424,13 @@ __global__ void __launch_bounds__(K4_THREADS) k_finalize(WinDesc wd, WinBufs wb,
   float* qf = wb.qf + 6 * gi;
   if (SEM && F.feats) {
     float* emb = wb.emb + gi * Df;
+    const long long* y64 = wb.emb64 + gi * Df;
+    const double sinv = ldexp(1.0, -pool_scale_exp(F.Hp * F.Wp, Df, wb.xmax[f], false));
     double yy = 0;
-    for (int d = threadIdx.x; d < Df; d += blockDim.x) yy += (double)emb[d] * emb[d];
+    for (int d = threadIdx.x; d < Df; d += blockDim.x) {
+      const double y = (double)y64[d] * sinv;
+      yy += y * y;
+    }
     yy = block_sum_d(yy, red);
     if (!(yy > 0.0)) {
       if (threadIdx.x == 0) {
@@ -1409,10 +1440,10 @@ __global__ void __launch_bounds__(K4_THREADS) k_finalize(WinDesc wd, WinBufs wb,
       }
       return;
     }
-    const float rn = (float)(1.0 / sqrt(yy));
+    const double rn = 1.0 / sqrt(yy);
     double eg = 0, gg = 0;
     for (int d = threadIdx.x; d < Df; d += blockDim.x) {
-      const float e = emb[d] * rn;
+      const float e = (float)((double)y64[d] * sinv * rn);
       emb[d] = e;
       if (F.gemb) {
         const double g = (double)F.gemb[d];
@@ -1425,14 +1456,14 @@ __global__ void __launch_bounds__(K4_THREADS) k_finalize(WinDesc wd, WinBufs wb,
     if (threadIdx.x == 0) {
       const double s_size = fmin((double)P.lambda * (double)wb.area[gi] / ((double)H * (double)W), 1.0);
       const uint32_t ac = wb.ang_cnt[gi];
-      const double s_angle = ac ? (double)wb.ang_sum[gi] / (double)ac : 0.0;
+      const double s_angle = ac ? (double)wb.ang64[gi] / ANG_SCALE / (double)ac : 0.0;
       double s_sem = 1.0;
       if (F.gemb) s_sem = gg > 0 ? fmin(fmax(eg / sqrt(gg), 0.0), 1.0) : 0.0;
       // R19: D-bar = sum(cover D) / sum(cover) with D = r / (rbar + eps)
-      const double* ps = wb.psum + gi * 3;
-      const double dbar = ps[2] > 0.0 ? ps[1] / ps[2] / (wb.rbar[f] + (double)P.eps) : 0.0;
+      const long long* ps = wb.psum64 + gi * 3;   // (both scaled by 2^kp: the ratio is unchanged)
+      const double dbar = ps[2] > 0 ? (double)ps[1] / (double)ps[2] / (wb.rbar[f] + (double)P.eps) : 0.0;
       qf[5] = (float)dbar;
-      wb.pmode[gi] = ps[0] > 0.0 ? 0 : 1;   // 1: all-zero weights -> unweighted pooling (R18)
+      wb.pmode[gi] = wb.pw[gi] ? 0 : 1;   // 1: all-zero weights -> unweighted pooling (R18)
       const double s_dist = 0.5 + 0.5 * dbar;
       qf[0] = (float)s_size; qf[1] = (float)s_angle; qf[2] = (float)s_sem; qf[3] = (float)s_dist;
       qf[4] = (float)(((s_size * s_angle) * s_sem) * s_dist);
