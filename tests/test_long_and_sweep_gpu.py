@@ -64,7 +64,7 @@ def test_stress_grid(voxel, n_masks, Df):
     c = g.cfg
     kw = disc_config_kwargs(c)
     gm = DiscMap(**gpu_config(kw, c.H, c.W, c.Hp, c.Wp, S=max(64, n_masks), window=4,
-                              max_pairs=min(1 << 22, 4 * c.H * c.W)))
+                              max_pairs=1 << 22))   # 1 cm x 200 overlapping masks: ~1.5 M unique pairs per frame
     om = OracleMap(**kw)
     frames = [g.frame(f, with_feats=True) for f in range(4)]
     for fr, rg in zip(frames, gm.integrate_frames(frames, report=True)):
