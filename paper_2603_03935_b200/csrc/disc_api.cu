@@ -403,12 +403,12 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   W.FCHUNKS = (int32_t)((PMP + 63) / 64);
   chk(W.ktab = dalloc<unsigned long long>(m, (size_t)win * PC, 0xFF));
   chk(W.ptab = dalloc<uint32_t>(m, (size_t)win * PC, 0xFF));
-  chk(W.nsum = dalloc<float4>(m, (size_t)win * PC, 0));
+  chk(W.nsum = dalloc<NSum>(m, (size_t)win * PC, 0));
   chk(W.plist = dalloc<uint32_t>(m, (size_t)win * PMAX));
   chk(W.npairs = dalloc<uint32_t>(m, win));
   chk(W.rkey = dalloc<unsigned long long>(m, (size_t)win * PMAX));
   chk(W.rs = dalloc<uint32_t>(m, (size_t)win * PMAX));
-  chk(W.rn = dalloc<float4>(m, (size_t)win * PMAX));
+  chk(W.rn = dalloc<NSum>(m, (size_t)win * PMAX));
   chk(W.rcount = dalloc<uint32_t>(m, win));
   chk(W.cnt = dalloc<uint32_t>(m, (size_t)win * SM * PMP));
   chk(W.area = dalloc<uint32_t>(m, (size_t)win * SM));
@@ -464,7 +464,7 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   }
   {  // K1 normal-sum scratch, shared by both window buffers (K1 launches are stream-ordered)
     const int nsmid = k1_nsmid();
-    float4* scr = dalloc<float4>(m, (size_t)nsmid * K1_SLOTS_PER_SM * K1_PT, 0);
+    NSum* scr = dalloc<NSum>(m, (size_t)nsmid * K1_SLOTS_PER_SM * K1_PT, 0);
     uint32_t* slot = dalloc<uint32_t>(m, (size_t)nsmid, 0);
     chk(scr); chk(slot);
     for (int wbi = 0; wbi < 2; ++wbi) { m->Wb[wbi].k1scr = scr; m->Wb[wbi].k1slot = slot; }

@@ -49,6 +49,13 @@ struct __align__(32) OvfChunk {
   uint32_t next;
 };
 
+// A (mask, voxel) pair's sum of pixel normals (R21) in 64-bit fixed point (x 2^40): integer atomics
+// are order-independent, so S_angle (and Q) are bit-reproducible whatever the order of the adds
+struct __align__(32) NSum {
+  long long x, y, z, pad;
+};
+constexpr double NSCALE = 1099511627776.0;   // 2^40
+
 struct FrameDesc {                // one frame's inputs, passed by value to kernels
   const float* depth;
   const uint8_t* masks;
@@ -81,13 +88,13 @@ struct Params {                   // method constants
 struct WinBufs {
   unsigned long long* ktab;   // [win][PC] frame key table (packed key)
   uint32_t* ptab;             // [win][PC] frame (s,kslot) pair table (code = s<<24 | kslot)
-  float4* nsum;               // [win][PC] per-pair normal sums (semantic mode; w unused)
+  NSum* nsum;                 // [win][PC] per-pair normal sums (semantic mode)
   uint32_t* plist;            // [win][PMAX] pair slots in insertion order
   uint32_t* npairs;           // [win]
   // K1b -> K1c: each tile's distinct (s, key) items with their normal sums
   unsigned long long* rkey;   // [win][PMAX] key
   uint32_t* rs;               // [win][PMAX] mask index s
-  float4* rn;                 // [win][PMAX] normal sum (semantic mode)
+  NSum* rn;                   // [win][PMAX] normal sum (semantic mode)
   uint32_t* rcount;           // [win] records reserved; a tile whose block passes RCAP inserts its
                               // items itself and writes KEY_EMPTY into its records below RCAP
   uint32_t* cnt;              // [win][SMAX][PMAXP] mask pixels per patch
@@ -124,7 +131,7 @@ struct WinBufs {
   uint8_t* tok;               // [win][SMAX] t_s defined (nonzero norm)
   uint8_t* pmode;             // [win][SMAX] 1: unweighted pooling fallback (R18)
   // K1 per-CTA normal-sum scratch: one K1_PT-slot block per resident K1 CTA, acquired per SM
-  float4* k1scr;              // [nsmid][K1_SLOTS_PER_SM][K1_PT], all-zero between CTAs
+  NSum* k1scr;                // [nsmid][K1_SLOTS_PER_SM][K1_PT], all-zero between CTAs
   uint32_t* k1slot;           // [nsmid] bitmask of the SM's blocks in use
   uint32_t* k1ctr;            // [2] K1a / K1b work-item counters (zeroed by K0)
   uint16_t* m0map;            // [win][MPIX] per pixel: first mask (low byte, 0xFF none), bit 8 = in a

@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(256) k_db_emit(WinDesc wd, WinBufs wb, Params 
   const uint32_t tmask = (uint32_t)wb.PC - 1;
   unsigned long long* ktab = wb.ktab + (size_t)f * wb.PC;
   uint32_t* ptab = wb.ptab + (size_t)f * wb.PC;
-  float4* nsum = wb.nsum + (size_t)f * wb.PC;
+  NSum* nsum = wb.nsum + (size_t)f * wb.PC;
   const float rinv = 1.0f / P.r;
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const size_t o = (size_t)f * wb.DBP + j;
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(256) k_db_emit(WinDesc wd, WinBufs wb, Params 
       if (u >= 1 && u + 1 < F.W && v >= 1 && v + 1 < F.H && db_point(F, P, u - 1, v, pl) &&
           db_point(F, P, u + 1, v, pr) && db_point(F, P, u, v - 1, pu) && db_point(F, P, u, v + 1, pd) &&
           normal_from(F, pc, pl, pr, pu, pd, nn))
-        red_add3(&nsum[pslot], nn[0], nn[1], nn[2]);
+        nsum_add(&nsum[pslot], nn[0], nn[1], nn[2]);
     }
     if (fresh) {
       atomicAdd(&wb.vs[(size_t)f * wb.SMAX + s], 1u);

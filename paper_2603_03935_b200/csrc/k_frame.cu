@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
     if (tile >= ntx * nty) continue;
     const int ty = tile / ntx, tx = tile - ty * ntx;
     const int ut0 = tx * TILE_W, vt0 = ty * K1_TILE_H;
-    float4* nscr = SEM ? wb.k1scr + (size_t)slot_s * K1_PT : nullptr;
+    NSum* nscr = SEM ? wb.k1scr + (size_t)slot_s * K1_PT : nullptr;
     for (int i = threadIdx.x; i < S; i += blockDim.x) vs_s[i] = 0;
     for (int i = threadIdx.x; i < K1_KT; i += blockDim.x) kt[i] = KEY_EMPTY;
     for (int i = threadIdx.x; i < 2 * K1_KT; i += blockDim.x) ptc[i] = U32_EMPTY;
@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
     const uint32_t tmask = (uint32_t)wb.PC - 1;
     unsigned long long* ktab = wb.ktab + (size_t)f * wb.PC;
     uint32_t* ptab = wb.ptab + (size_t)f * wb.PC;
-    float4* nsum = wb.nsum + (size_t)f * wb.PC;
+    NSum* nsum = wb.nsum + (size_t)f * wb.PC;
     // CTA key table -> local key index; at most K1_KT_PROBES probes, so a table that far views
     // (up to a voxel per pixel) fill up fails fast and the item takes the record list
     auto kt_insert = [&](uint64_t key) -> uint16_t {
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
         }
       }
       if (ps < 0) return false;
-      if (SEM && (n0 != 0.f || n1 != 0.f || n2 != 0.f)) red_add3(&nscr[ps], n0, n1, n2);
+      if (SEM && (n0 != 0.f || n1 != 0.f || n2 != 0.f)) nsum_add(&nscr[ps], n0, n1, n2);
       return true;
     };
     auto emit = [&](uint32_t s, uint64_t key, float n0, float n1, float n2) -> int {
@@ -511,13 +511,11 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
       }
       const bool hasn = SEM && (n0 != 0.f || n1 != 0.f || n2 != 0.f);
       if (ps >= 0) {
-        if (hasn) red_add3(&nscr[ps], n0, n1, n2);
+        if (hasn) nsum_add(&nscr[ps], n0, n1, n2);
         return ps;
       }
       const uint32_t g = global_insert(key, s);
-      if (hasn && g != U32_EMPTY) {
-        red_add3(&nsum[g], n0, n1, n2);
-      }
+      if (hasn && g != U32_EMPTY) nsum_add(&nsum[g], n0, n1, n2);
       return -1;
     };
 
@@ -592,10 +590,10 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
                 const size_t o = (size_t)f * wb.PMAX + r;
                 __stcg(&wb.rkey[o], key);
                 __stcg(&wb.rs[o], s);
-                if (SEM) __stcg(&wb.rn[o], make_float4(a, b, c, 0.f));
+                if (SEM) wb.rn[o] = NSum{llrint((double)a * NSCALE), llrint((double)b * NSCALE), llrint((double)c * NSCALE), 0};
               } else {
                 const uint32_t g = global_insert(key, s);
-                if (SEM && g != U32_EMPTY && (a != 0.f || b != 0.f || c != 0.f)) red_add3(&nsum[g], a, b, c);
+                if (SEM && g != U32_EMPTY && (a != 0.f || b != 0.f || c != 0.f)) nsum_add(&nsum[g], a, b, c);
               }
             }
           }
@@ -706,21 +704,21 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
     for (int i = threadIdx.x; i < 2 * K1_KT; i += blockDim.x) {
       const uint32_t s = ptc[i];
       if (s == U32_EMPTY) continue;
-      float4 nn = make_float4(0.f, 0.f, 0.f, 0.f);
+      NSum nn{0, 0, 0, 0};
       if (SEM) {
-        nn = __ldcg(&nscr[i]);
-        if (nn.x != 0.f || nn.y != 0.f || nn.z != 0.f) __stcg(&nscr[i], make_float4(0.f, 0.f, 0.f, 0.f));
+        nn.x = __ldcg(&nscr[i].x); nn.y = __ldcg(&nscr[i].y); nn.z = __ldcg(&nscr[i].z);
+        if (nn.x || nn.y || nn.z) nscr[i] = NSum{0, 0, 0, 0};
       }
       if (!direct) {
         const size_t o = (size_t)f * wb.PMAX + r++;
         __stcg(&wb.rkey[o], kt[i >> 1]);
         __stcg(&wb.rs[o], s);
-        if (SEM) __stcg(&wb.rn[o], nn);
+        if (SEM) wb.rn[o] = nn;
       } else {
         if (r < (uint32_t)wb.RCAP) __stcg(&wb.rkey[(size_t)f * wb.PMAX + r], (unsigned long long)KEY_EMPTY);
         ++r;
         const uint32_t g = global_insert(kt[i >> 1], s);
-        if (SEM && g != U32_EMPTY && (nn.x != 0.f || nn.y != 0.f || nn.z != 0.f)) red_add3(&nsum[g], nn.x, nn.y, nn.z);
+        if (SEM && g != U32_EMPTY) nsum_add_fx(&nsum[g], nn.x, nn.y, nn.z);
       }
     }
     __syncthreads();
@@ -763,7 +761,7 @@ __global__ void __launch_bounds__(256) k_dedup(WinDesc wd, WinBufs wb, int* err)
   const uint32_t tmask = (uint32_t)wb.PC - 1;
   unsigned long long* ktab = wb.ktab + (size_t)f * wb.PC;
   uint32_t* ptab = wb.ptab + (size_t)f * wb.PC;
-  float4* nsum = wb.nsum + (size_t)f * wb.PC;
+  NSum* nsum = wb.nsum + (size_t)f * wb.PC;
   for (uint32_t b = blockIdx.x * blockDim.x; b < n; b += gridDim.x * blockDim.x) {
     const uint32_t i = b + threadIdx.x;
     bool fresh = false;
@@ -775,8 +773,8 @@ __global__ void __launch_bounds__(256) k_dedup(WinDesc wd, WinBufs wb, int* err)
       const uint32_t kslot = key == KEY_EMPTY ? U32_EMPTY : ktab_insert(ktab, tmask, key, err);
       if (kslot != U32_EMPTY) pslot = ptab_insert(ptab, tmask, (s << 24) | kslot, &fresh, err);
       if (SEM && pslot != U32_EMPTY) {
-        const float4 nn = __ldcs(&wb.rn[o]);
-        if (nn.x != 0.f || nn.y != 0.f || nn.z != 0.f) red_add3(&nsum[pslot], nn.x, nn.y, nn.z);
+        const NSum nn = wb.rn[o];
+        nsum_add_fx(&nsum[pslot], nn.x, nn.y, nn.z);
       }
       if (fresh) atomicAdd(&vsd_s[s], 1u);
     }
@@ -840,7 +838,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_pairs(WinDesc wd, WinBufs wb, Pa
   const size_t fo = (size_t)f * wb.PMAX;
   uint32_t* ptab = wb.ptab + (size_t)f * wb.PC;
   const unsigned long long* ktab = wb.ktab + (size_t)f * wb.PC;
-  float4* nsum = wb.nsum + (size_t)f * wb.PC;
+  NSum* nsum = wb.nsum + (size_t)f * wb.PC;
   const int lane = threadIdx.x & 31;
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < np; base += stride) {
@@ -867,8 +865,9 @@ __global__ void __launch_bounds__(K2_THREADS) k_pairs(WinDesc wd, WinBufs wb, Pa
             atomicMax(&ab_s[6 * s + 3 + a], k3[a]);
           }
         if (SEM && !(abl & 1)) {
-          const float4 nv = __ldcg(&nsum[ps]);
-          const float n0 = nv.x, n1 = nv.y, n2 = nv.z;
+          const float n0 = (float)((double)__ldcg(&nsum[ps].x) / NSCALE);
+          const float n1 = (float)((double)__ldcg(&nsum[ps].y) / NSCALE);
+          const float n2 = (float)((double)__ldcg(&nsum[ps].z) / NSCALE);
           const float nl = sqrtf(n0 * n0 + n1 * n1 + n2 * n2);
           if (nl > 0.f) {
             const float r0 = ((float)k3[0] + 0.5f) * P.r - F.pose[3];
@@ -1513,7 +1512,7 @@ __global__ void __launch_bounds__(256) k_release(WinDesc wd, WinBufs wb, int sem
     if (ks < (uint32_t)wb.PC) __stcs(&wb.ktab[to + ks], (unsigned long long)KEY_EMPTY);
     if (sem) {
       const uint32_t ps = wb.plist[fo + i];
-      if (ps < (uint32_t)wb.PC) __stcs(&wb.nsum[to + ps], make_float4(0.f, 0.f, 0.f, 0.f));
+      if (ps < (uint32_t)wb.PC) wb.nsum[to + ps] = NSum{0, 0, 0, 0};
     }
   }
 }
@@ -1532,7 +1531,7 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
   // window (tables sized close to the frames' pair counts: scattered zeroing of partial lines costs
   // more) or, when the previous window released its slots (k_release), nothing to do
   int launches = 0;
-  if (sem && fill_nsum) { k_fill_cs<<<4 * nsm, 256, 0, st>>>((uint4*)wb.nsum, (size_t)n * wb.PC, 0u); ++launches; }
+  if (sem && fill_nsum) { k_fill_cs<<<4 * nsm, 256, 0, st>>>((uint4*)wb.nsum, (size_t)n * wb.PC * 2, 0u); ++launches; }
   if (fill_ktab) { k_fill_cs<<<4 * nsm, 256, 0, st>>>((uint4*)wb.ktab, (size_t)n * wb.PC / 2, 0xFFFFFFFFu); ++launches; }
   if (ev0) cudaEventRecord(ev0, st);
   int64_t maxHW = 1;

@@ -94,6 +94,15 @@ __device__ __forceinline__ uint32_t ptab_insert(uint32_t* tab, uint32_t mask, ui
 }
 
 // native vector float reduction at L2 (fire-and-forget; shared-memory float atomics are CAS loops)
+// fixed-point normal sums (NSum): fire-and-forget 64-bit integer reductions
+__device__ __forceinline__ void nsum_add_fx(NSum* p, long long a, long long b, long long c) {
+  if (a) atomicAdd((unsigned long long*)&p->x, (unsigned long long)a);
+  if (b) atomicAdd((unsigned long long*)&p->y, (unsigned long long)b);
+  if (c) atomicAdd((unsigned long long*)&p->z, (unsigned long long)c);
+}
+__device__ __forceinline__ void nsum_add(NSum* p, float a, float b, float c) {
+  nsum_add_fx(p, llrint((double)a * NSCALE), llrint((double)b * NSCALE), llrint((double)c * NSCALE));
+}
 __device__ __forceinline__ void red_add3(float4* p, float a, float b, float c) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(0.f)
                : "memory");
