@@ -61,9 +61,16 @@ struct disc_map {
   std::vector<EvPair> ev_pending;
   std::vector<cudaEvent_t> ev_pool;
   disc_stats stats{};
-  // host-input staging
-  uint8_t* stage = nullptr;
+  // host-input staging: two window-sized buffers, so window w+1's H2D copies overlap window w's
+  // kernels (ev_stage: stage 1 of the window that used the buffer is done reading it)
+  uint8_t* stage = nullptr;           // the buffer being filled
+  uint8_t* stage_buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev_stage[2] = {nullptr, nullptr};
+  bool stage_pending[2] = {false, false};
+  int stage_next = 0;
   size_t stage_bytes = 0;
+  disc_frame_report* h_rep_all = nullptr;   // pinned, reports of a host-input call (copied once)
+  int64_t h_rep_cap = 0;
   // export scratch
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -601,7 +608,11 @@ void disc_map_destroy(disc_map* m) {
   if (m->h_err) cudaFreeHost(m->h_err);
   if (m->h_rep) cudaFreeHost(m->h_rep);
   if (m->h_np) cudaFreeHost(m->h_np);
-  if (m->stage) cudaFree(m->stage);
+  for (int i = 0; i < 2; ++i) {
+    if (m->stage_buf[i]) cudaFree(m->stage_buf[i]);
+    if (m->ev_stage[i]) cudaEventDestroy(m->ev_stage[i]);
+  }
+  if (m->h_rep_all) cudaFreeHost(m->h_rep_all);
   if (m->scratch) cudaFree(m->scratch);
   for (auto& p : m->ev_pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   for (auto e : m->ev_pool) cudaEventDestroy(e);
@@ -1000,16 +1011,19 @@ static int stage2_reserve(disc_map* m, bool sem) {
 
 // host-input staging: one window of frames' inputs (pinned host -> device, stream-ordered)
 static disc_status ensure_stage(disc_map* m) {
-  if (m->stage) return DISC_OK;
+  if (m->stage_buf[0]) return DISC_OK;
   const disc_config& c = m->cfg;
   m->stage_bytes = (size_t)c.window * ((size_t)c.max_pixels * (4 + c.max_masks) + (size_t)c.max_masks * 4 + 256 +
                                        (size_t)c.max_patches * ((size_t)c.feat_dim * 4 + (size_t)c.track_dim * 2) +
                                        (size_t)c.feat_dim * 4 + 4096);
-  if (cudaMalloc((void**)&m->stage, m->stage_bytes) != cudaSuccess) {
-    cudaGetLastError();
-    m->stage = nullptr;
-    return fail(m, DISC_ERR_CAPACITY, "cannot allocate host-input staging buffers");
+  for (int i = 0; i < 2; ++i) {
+    if (cudaMalloc((void**)&m->stage_buf[i], m->stage_bytes) != cudaSuccess ||
+        cudaEventCreateWithFlags(&m->ev_stage[i], cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(m, DISC_ERR_CAPACITY, "cannot allocate host-input staging buffers");
+    }
   }
+  m->stage = m->stage_buf[0];
   return DISC_OK;
 }
 
@@ -1050,6 +1064,16 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
   if (host_inputs) {
     const disc_status ss = ensure_stage(m);
     if (ss != DISC_OK) return ss;
+    if (reports && m->h_rep_cap < n) {
+      if (m->h_rep_all) cudaFreeHost(m->h_rep_all);
+      m->h_rep_all = nullptr;
+      m->h_rep_cap = 0;
+      if (cudaMallocHost(&m->h_rep_all, sizeof(disc_frame_report) * (size_t)std::max(n, 64)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(m, DISC_ERR_CAPACITY, "cannot allocate pinned report buffer");
+      }
+      m->h_rep_cap = std::max(n, 64);
+    }
   }
   // stream-ordered after the caller's prior work on `st`; stage 1 on s1, stage 2 on s2
   cudaEventRecord(m->ev_in, st);
@@ -1069,6 +1093,13 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
     int maxS = 1, maxHp = 1, maxW = 1, maxWp = 1, maxP = 1, rows = 4;
     bool sem = false;
     size_t so = 0;
+    int sb = 0;
+    if (host_inputs) {   // the staging buffer stage 1 of the window before last has finished reading
+      sb = m->stage_next;
+      m->stage_next ^= 1;
+      if (m->stage_pending[sb]) cudaStreamWaitEvent(s1, m->ev_stage[sb], 0);
+      m->stage = m->stage_buf[sb];
+    }
     for (int i = 0; i < nw; ++i) {
       disc_frame f = frames[w0 + i];
       if (host_inputs) stage_frame(m, so, f, s1);   // this frame's inputs to device staging
@@ -1097,6 +1128,10 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
                                        nres_w, s1, e0, e1, !m->ktab_clean[b], !m->nsum_clean[b], release);
     m->ktab_clean[b] = release;
     if (sem) m->nsum_clean[b] = release;
+    if (host_inputs) {
+      cudaEventRecord(m->ev_stage[sb], s1);
+      m->stage_pending[sb] = true;
+    }
     cudaMemcpyAsync(m->h_np + (size_t)b * MAXWIN, Wbuf.npairs, sizeof(uint32_t) * nw, cudaMemcpyDeviceToHost, s1);
     cudaEventRecord(m->ev_np[b], s1);
     m->np_pending[b] = nw;
@@ -1117,7 +1152,9 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
     m->stats.frames += nw;
     disc_status cs = cuda_check(m, "integrate launch");
     if (cs != DISC_OK) return cs;
-    if (reports) {
+    if (reports && host_inputs) {   // (stream-ordered before the next window's stage 2 rewrites X.rep)
+      cudaMemcpyAsync(m->h_rep_all + w0, m->X.rep, sizeof(disc_frame_report) * nw, cudaMemcpyDeviceToHost, s2);
+    } else if (reports) {
       cudaMemcpyAsync(m->h_rep, m->X.rep, sizeof(disc_frame_report) * nw, cudaMemcpyDeviceToHost, s2);
       disc_status ss = sync_check(m, s2);
       if (ss != DISC_OK) return ss;
@@ -1134,9 +1171,10 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
   cudaEventRecord(m->ev_done, s2);
   cudaEventRecord(m->ev_s1done, s1);
   cudaStreamWaitEvent(st, m->ev_s1done, 0);
-  if (host_inputs) {   // staging is reused by the next call: keep ordering simple
-    disc_status ss = sync_check(m, st);
+  if (host_inputs) {   // the caller's host buffers are free again on return; reports complete
+    disc_status ss = sync_check(m, reports ? s2 : st);
     if (ss != DISC_OK) return ss;
+    if (reports) std::memcpy(reports, m->h_rep_all, sizeof(disc_frame_report) * n);
   }
   return cuda_check(m, "integrate launch");
 }
@@ -1162,14 +1200,8 @@ disc_status disc_integrate_frames_host(disc_map* m, const disc_frame* f, int32_t
     const std::string v = validate_frame(m, f[i], true);
     if (!v.empty()) return fail(m, DISC_ERR_INVALID, "frame " + std::to_string(i) + ": " + v);
   }
-  // the staging buffer holds one window: process window by window
-  const int win = m->cfg.window;
-  for (int w0 = 0; w0 < n; w0 += win) {
-    const int nw = std::min(win, n - w0);
-    disc_status s = integrate_impl(m, f + w0, nw, stream, report ? report + w0 : nullptr, true);
-    if (s != DISC_OK) return s;
-  }
-  return DISC_OK;
+  // windows pipelined over two staging buffers; one synchronisation at the end of the call
+  return integrate_impl(m, f, n, stream, report, true);
 }
 
 static disc_status ensure_scratch(disc_map* m, size_t bytes) {
