@@ -380,10 +380,10 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
     // longer windows amortise stage 1's per-window work, so stage 2 gets a few more SMs (measured
     // on R: 16-frame windows best at 20, 32-frame windows at 26)
     m->nres = e ? std::atoi(e) : (cfg->window > 16 ? 26 : 20);
-    m->nres = std::max(0, std::min(m->nres, m->nsm / 2));
+    m->nres = std::max(0, std::min(m->nres, m->nsm * 3 / 4));
     const char* eg = std::getenv("DISC_S2_SMS_GEO");
     m->nres_geo = eg ? std::atoi(eg) : (cfg->window > 16 ? 48 : 40);
-    m->nres_geo = std::max(0, std::min(m->nres_geo, m->nsm / 2));
+    m->nres_geo = std::max(0, std::min(m->nres_geo, m->nsm * 3 / 4));
     const char* ea = std::getenv("DISC_S2_ADAPT");   // 0: fixed split (tuning)
     m->adapt = !(ea && std::atoi(ea) == 0);
     const char* er = std::getenv("DISC_TAB_RELEASE_RATIO");   // tuning: 1e30 = always fill
@@ -1006,7 +1006,7 @@ static int stage2_reserve(disc_map* m, bool sem) {
   const int base = sem ? m->nres : m->nres_geo;
   int extra = 0;
   if (m->adapt && base > 0 && m->np_avg > 24000.0) extra = (int)std::min(44.0, (m->np_avg - 24000.0) / 2000.0);
-  return std::min(base + extra, m->nsm / 2);
+  return std::min(base + extra, m->nsm * 3 / 4);
 }
 
 // host-input staging: one window of frames' inputs (pinned host -> device, stream-ordered)
