@@ -428,7 +428,8 @@ __device__ unsigned long long g_tgprof[4];   // DISC_S2PROF: target-update warp 
 // fresh: the CTA's static shared counters are not known to be zero (first frame of a launch); later
 // frames find them zeroed by the previous frame's association, and skip one barrier
 __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBufs& wb, const MapState& M,
-                                         const FrameScratch& X, const Params& P, int sem, bool fresh = true) {
+                                         const FrameScratch& X, const Params& P, int sem, bool fresh = true,
+                                         bool dbg = true) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // Layout: the shared-memory tables hold up to X.TCS (s, j) triples; a denser frame (hierarchical
   // SAM-"everything" masks overlapping many instances, BASELINE configs[4]) runs the same steps on
@@ -770,18 +771,25 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
   for (int s2 = tid; s2 < S; s2 += blockDim.x) X.det_target[s2] = d_tgt[s2];
   __syncthreads();
   K6_PROBE(8);
-  // ---- debug copies of the triples, edge count ----
+  // ---- triple ids (refinement, debug export), debug copies (a window's last frame: the only one the
+  // export reads), edge count; nothing below reads them before the next barrier ----
   for (uint32_t t = tid; t < ntr; t += blockDim.x) {
-    X.trip_c[t] = t_c[t];
-    X.trip_j[t] = t_j[t];   // (ids, for the debug export; the gate CTAs are done with the labels)
-    X.trip_edge[t] = t_e[t];
+    X.trip_j[t] = t_j[t];   // (the gate CTAs are done with the labels)
+    if (dbg) {
+      X.trip_c[t] = t_c[t];
+      X.trip_edge[t] = t_e[t];
+    }
     if (t_e[t]) atomicAdd(&edges_s, 1ull);
   }
-  __syncthreads();
   K6_PROBE(9);
   // relabel segment offsets: block-wide exclusive scan of the lengths (chunk per thread)
   const uint32_t ns = min(n_seg, (uint32_t)TC);
-  {
+  if (ns == 0) {   // (no merge this frame: nothing to scan)
+    if (tid == 0) {
+      X.seg_off[0] = 0;
+      nrel_s = 0;
+    }
+  } else {
     const uint32_t per = (ns + blockDim.x - 1) / blockDim.x;
     const uint32_t g0 = min(ns, tid * per), g1 = min(ns, g0 + per);
     uint32_t sum = 0;
@@ -1573,7 +1581,7 @@ __global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb
     grid_sync(wb.s2bar, G * ++ep);
     probe(0);
     if (blockIdx.x == 0) {
-      s2_assoc(f, F, wb, M, X, P, sem, f == f0);
+      s2_assoc(f, F, wb, M, X, P, sem, f == f0, f == fe - 1);
     } else {
       if (P.Dt > 0) s2_gate(f, wb, M, X, P);
       if (f + 1 < fe) {

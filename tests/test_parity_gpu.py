@@ -416,3 +416,21 @@ def test_s_angle_fixtures(case):
         fr = semantic_t0(0, depth=depth, masks=np.ones((1, 48, 64), np.uint8))
         fr["pose"] = pose
     _fixture_pair(dict(voxel_size=0.05, feat_dim=16, track_dim=0), [fr], True, 0)
+
+
+@pytest.mark.parametrize("name,nf", [("N", 10), ("H", 6), ("R", 4)])
+def test_every_frame_debug_export(name, nf):
+    """Full-size frames one call each, so the per-frame debug export (statuses, |V_s|, the unique
+    (s, key) pairs, C triples, edges, targets, Q factors, e_s, t_s) is compared on EVERY frame, not only a
+    window's last one; the map state after each frame too."""
+    dev = _dev()
+    g = Generator(name, device=dev)
+    c = g.cfg
+    kw = disc_config_kwargs(c)
+    gm = _disc_map(kw, c.H, c.W, c.Hp, c.Wp, window=1, S=min(255, max(64, int(c.n_masks * 1.2) + 8)))
+    om = OracleMap(**kw)
+    for f in range(nf):
+        fr = g.frame(f, with_feats=True)
+        compare_reports(gm.integrate_frame(fr), om.integrate(frame_to_numpy(fr)))
+        compare_frame_debug(gm.last_frame(), om.last_frame(), True, c.Dt)
+        compare_state(gm, om, True, c.Dt)

@@ -129,3 +129,20 @@ def test_sharded_host_input_path():
     host = [{k: (v.cpu().pin_memory() if isinstance(v, torch.Tensor) else v) for k, v in fr.items()} for fr in frames]
     assert a.integrate_frames_host(host, report=True) == b.integrate_frames(frames, report=True)
     assert np.array_equal(a.memberships()[0], b.memberships()[0])
+
+
+def test_sharded_with_dbscan():
+    """The DBSCAN denoise (f3) runs in every shard's stage 1: a G = 2 map with dbscan on equals the
+    oracle (small N frames, noisy depth)."""
+    dev = _dev()
+    g = Generator("N", device=dev, H=96, W=128, Hp=6, Wp=9, fx=115.5, fy=115.7, cx=63.8, cy=48.5, min_area=40)
+    c = g.cfg
+    kw = disc_config_kwargs(c)
+    kw.update(dbscan_eps=0.1, dbscan_min_pts=8)
+    gm = _map(kw, c, 2, 4, 64)
+    om = OracleMap(**kw)
+    frames = [g.frame(f) for f in range(6)]
+    for rg, ro in zip(_run(gm, frames, 4), [om.integrate(frame_to_numpy(fr)) for fr in frames]):
+        compare_reports(rg, ro)
+    compare_frame_debug(gm.last_frame(), om.last_frame(), True, c.Dt)
+    compare_state(gm, om, True, c.Dt)
