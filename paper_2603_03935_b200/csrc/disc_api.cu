@@ -1005,10 +1005,11 @@ static int stage2_reserve(disc_map* m, bool sem) {
   }
   const int base = sem ? m->nres : m->nres_geo;
   int extra = 0;
-  // (geometry-only windows: stage 1 is light enough to give stage 2 up to ~3/4 of the GPU; measured
-  // on the prefilled H map, 85 k pairs per frame: 74 SMs 13.8 k, 104 SMs 14.5 k frames/s)
+  // (geometry-only windows: stage 1 is light enough to give stage 2 up to 100 SMs; measured on the
+  // prefilled H map, 85 k pairs per frame: 74 SMs 13.8 k, 104 SMs 14.5 k frames/s; at ~110 stage 1
+  // turns critical)
   if (m->adapt && base > 0 && m->np_avg > 24000.0)
-    extra = sem ? (int)std::min(44.0, (m->np_avg - 24000.0) / 2000.0) : (int)std::min(62.0, (m->np_avg - 24000.0) / 1000.0);
+    extra = sem ? (int)std::min(44.0, (m->np_avg - 24000.0) / 2000.0) : (int)std::min(52.0, (m->np_avg - 24000.0) / 1000.0);
   return std::min(base + extra, m->nsm * 3 / 4);
 }
 

@@ -922,7 +922,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_pairs(WinDesc wd, WinBufs wb, Pa
 // ------------------------------------------------------------------------------------------
 constexpr int K3_ROWS = 64;
 
-__global__ void __launch_bounds__(256) k_fbar_part(WinDesc wd, WinBufs wb, int Df, int f0) {
+__global__ void __launch_bounds__(256) k_fbar_part(WinDesc wd, WinBufs wb, int Df, int f0, int evict_last) {
   const int f = f0 + blockIdx.y;   // frames [f0, f0 + gridDim.y): one L2-sized group (launch_stage1)
   if (f >= wd.n) return;
   const FrameDesc& F = wd.f[f];
@@ -933,7 +933,7 @@ __global__ void __launch_bounds__(256) k_fbar_part(WinDesc wd, WinBufs wb, int D
   if (p0 >= P) return;
   const int p1 = min(P, p0 + K3_ROWS);
   double* part = wb.fpart + ((size_t)f * wb.FCHUNKS + ch) * Df;
-  const uint64_t pol = policy_evict_last();   // the group's tokens stay in L2 for k_poolr's pass
+  const uint64_t pol = evict_last ? policy_evict_last() : policy_evict_first();   // grouped: kept for k_poolr
   float xm = 0.f;
   for (int d4 = threadIdx.x; d4 < Df / 4; d4 += blockDim.x) {
     double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
@@ -1594,12 +1594,16 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
     // Eq.1's mean f-bar and the pooling pass read the same CLIP tokens: run them per group of frames
     // whose tokens fit in L2 (<= 48 MB), so the second read hits L2 (first read evict-last, second
     // evict-first) instead of streaming the window's tokens from HBM twice
+    // (measured: per-group launches leave the GPU under-filled and serialise -- stage 1 per window
+    // +0.26 ms on H, +1 ms on R -- more than the second HBM read costs, so one group by default;
+    // DISC_CLIP_GROUP_MB=<L2 budget> enables the grouping)
     const int nch = (maxP + K3_ROWS - 1) / K3_ROWS;
     const int64_t tok_bytes = std::max<int64_t>(1, (int64_t)maxP * P.Df * 4);
-    const int gsz = (int)std::max<int64_t>(1, std::min<int64_t>(n, (48ll << 20) / tok_bytes));
+    static const int64_t grp_mb = getenv("DISC_CLIP_GROUP_MB") ? atoll(getenv("DISC_CLIP_GROUP_MB")) : 0;
+    const int gsz = grp_mb > 0 ? (int)std::max<int64_t>(1, std::min<int64_t>(n, (grp_mb << 20) / tok_bytes)) : n;
     for (int g0 = 0; g0 < n; g0 += gsz) {
       const int gn = std::min(gsz, n - g0);
-      k_fbar_part<<<dim3(nch, gn), 256, 0, st>>>(wd, wb, P.Df, g0);
+      k_fbar_part<<<dim3(nch, gn), 256, 0, st>>>(wd, wb, P.Df, g0, gsz < n ? 1 : 0);
       k_fbar<<<dim3((P.Df + 255) / 256, gn), 256, 0, st>>>(wd, wb, P.Df, g0);
       if (bulk) k_poolr<true, true><<<dim3(gx, gn), K4R_WARPS * 32, smr, st>>>(wd, wb, P, g0);
       else k_poolr<true, false><<<dim3(gx, gn), K4R_WARPS * 32, smr, st>>>(wd, wb, P, g0);
