@@ -28,6 +28,7 @@ struct disc_map {
   int dev = 0, nsm = 148;
   int nres = 0;       // SMs reserved for stage 2 (0 = no partition), windows with CLIP tokens
   int nres_geo = 0;   // the same for geometry-only windows (lighter stage 1: more SMs to stage 2)
+  uint32_t s2_tag = 0;   // next slot-chain tag of stage 2's speculative counting (launch_stage2)
   MapState M{};
   WinBufs Wb[2]{};               // double-buffered window buffers (stage 1 of window w+1 overlaps
                                  // stage 2 of window w)
@@ -432,6 +433,7 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(W.pfk = dalloc<uint32_t>(m, (size_t)win * PMAX));
   chk(W.pms = dalloc<uint32_t>(m, (size_t)win * PMAX));
   chk(W.plab = dalloc<uint2>(m, (size_t)win * PMAX));
+  chk(W.pnext = dalloc<uint32_t>(m, (size_t)win * PMAX));
   chk(W.fpart = dalloc<double>(m, (size_t)win * W.FCHUNKS * Df));
   chk(W.fbar = dalloc<float>(m, (size_t)win * Df));
   chk(W.rp = dalloc<float>(m, (size_t)win * PMP));
@@ -484,6 +486,7 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   M.ARENA = (unsigned long long)(8 * cfg->max_memberships + (1 << 20));
   M.IMAX = (int32_t)IM;
   chk(M.slots = dalloc<KeySlot>(m, M.MC, 0xFF));
+  chk(M.slh = dalloc<unsigned long long>(m, M.MC, 0));
   chk(M.ovf = dalloc<OvfChunk>(m, M.OVFCAP, 0xFF));
   chk(M.ovf_top = dalloc<uint32_t>(m, 1));
   chk(M.alive = dalloc<uint8_t>(m, IM));
@@ -528,6 +531,14 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
   chk(X.trip_j = dalloc<uint32_t>(m, X.TCAP));
   chk(X.trip_c = dalloc<uint32_t>(m, X.TCAP));
   chk(X.trip_edge = dalloc<uint8_t>(m, X.TCAP));
+  chk(X.trip_sd = dalloc<uint32_t>(m, X.TCAP));
+  chk(X.trip_jd = dalloc<uint32_t>(m, X.TCAP));
+  chk(X.ctab_key2 = dalloc<unsigned long long>(m, X.CC, 0xFF));
+  chk(X.ctab_cnt2 = dalloc<uint32_t>(m, X.CC));
+  chk(X.ctab_idx2 = dalloc<uint32_t>(m, X.TCAP));
+  chk(X.ntrip2 = dalloc<uint32_t>(m, 1));
+  chk(X.trip_s2 = dalloc<uint32_t>(m, X.TCAP));
+  chk(X.trip_j2 = dalloc<uint32_t>(m, X.TCAP));
   chk(X.det_target = dalloc<int32_t>(m, SM));
   chk(X.det_id = dalloc<int64_t>(m, SM));
   chk(X.tgt_phys = dalloc<uint32_t>(m, SM));
@@ -1144,7 +1155,7 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
     cudaStreamWaitEvent(s2, m->ev_s1[b], 0);
     if (m->timing) cudaEventRecord(t1b, s2);
     tl_mark(s2, "s2_begin", -1);
-    m->stats.launches += launch_stage2(wd, Wbuf, m->M, m->X, m->P, sem, m->nsm, nres_w, s2);
+    m->stats.launches += launch_stage2(wd, Wbuf, m->M, m->X, m->P, sem, m->nsm, nres_w, &m->s2_tag, s2);
     if (m->timing) {
       cudaEventRecord(t2, s2);
       m->ev_pending.push_back({e0, e1, 0});
@@ -1382,18 +1393,24 @@ disc_status disc_debug_last_frame(disc_map* m, disc_frame_debug* d) {
   nt = std::min<uint32_t>(nt, (uint32_t)m->X.TCAP);
   std::vector<uint32_t> ts(nt), tj(nt), tc(nt);
   std::vector<uint8_t> te(nt);
-  cudaMemcpy(ts.data(), m->X.trip_s, 4ull * nt, cudaMemcpyDeviceToHost);
-  cudaMemcpy(tj.data(), m->X.trip_j, 4ull * nt, cudaMemcpyDeviceToHost);
+  cudaMemcpy(ts.data(), m->X.trip_sd, 4ull * nt, cudaMemcpyDeviceToHost);
+  cudaMemcpy(tj.data(), m->X.trip_jd, 4ull * nt, cudaMemcpyDeviceToHost);
   cudaMemcpy(tc.data(), m->X.trip_c, 4ull * nt, cudaMemcpyDeviceToHost);
   cudaMemcpy(te.data(), m->X.trip_edge, 1ull * nt, cudaMemcpyDeviceToHost);
-  if (d->trip_s)
-    for (uint32_t i = 0; i < nt && i < (uint32_t)d->trip_cap; ++i) {
-      d->trip_s[i] = (int32_t)ts[i];
-      d->trip_j[i] = tj[i];
-      d->trip_c[i] = tc[i];
-      d->trip_edge[i] = te[i];
+  // a speculatively counted frame's table can hold (s, label) entries whose count its predecessor's
+  // update took back to 0 (a merged-away label): not triples of C
+  uint32_t kt = 0;
+  for (uint32_t i = 0; i < nt; ++i) {
+    if (tc[i] == 0) continue;
+    if (d->trip_s && kt < (uint32_t)d->trip_cap) {
+      d->trip_s[kt] = (int32_t)ts[i];
+      d->trip_j[kt] = tj[i];
+      d->trip_c[kt] = tc[i];
+      d->trip_edge[kt] = te[i];
     }
-  d->n_trip = nt;
+    kt++;
+  }
+  d->n_trip = kt;
   return cuda_check(m, "disc_debug_last_frame");
 }
 

@@ -111,6 +111,7 @@ struct WinBufs {
   uint32_t* pfk;              // [win][PMAX] frame key-table slot
   uint32_t* pms;              // [win][PMAX] map slot found by K5 (or U32_EMPTY)
   uint2* plab;                // [win][PMAX] the slot's first two labels seen by K5 (K7 skips inserts of a present label)
+  uint32_t* pnext;            // [win][PMAX] next pair of the frame on the same map slot (speculative counting)
   // semantic
   double* fpart;              // [win][FCHUNKS][Df] partial column sums
   float* fbar;                // [win][Df]
@@ -163,6 +164,8 @@ struct WinBufs {
 // ---- map state ---------------------------------------------------------------------------
 struct MapState {
   KeySlot* slots;             // [MC]
+  unsigned long long* slh;    // [MC] (tag << 32 | first pair) of the speculatively counted frame tagged `tag` on
+                              // this slot (wb.pnext chains its other pairs); other tags: none
   OvfChunk* ovf;              // [OVFCAP]
   uint32_t* ovf_top;
   uint32_t OVFCAP;
@@ -205,6 +208,12 @@ struct FrameScratch {
   uint32_t* trip_j;
   uint32_t* trip_c;
   uint8_t* trip_edge;
+  uint32_t* trip_sd;             // [TCAP] debug export of the association's triples (s, id; trip_c, trip_edge)
+  uint32_t* trip_jd;
+  // the second count table (speculative counting: frame f+1 is counted while frame f is associated);
+  // frame f of a launch uses table (f - f0) & 1, ct2 holds table 1's pointers
+  unsigned long long* ctab_key2;
+  uint32_t *ctab_cnt2, *ctab_idx2, *ntrip2, *trip_s2, *trip_j2;
   int32_t CC, TCAP;               // count-table slots (power of 2, >= 2 TCAP); triple capacity per frame
   int32_t TCS;                     // triples the association holds in shared memory (denser frames: k6g)
   unsigned char* k6g;            // global-memory association layout for TCAP triples (K6Smem(SMAX, TCAP))

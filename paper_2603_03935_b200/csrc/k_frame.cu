@@ -124,7 +124,7 @@ __global__ void k_win_init(WinDesc wd, WinBufs wb) {
 #define K1A_PERSIST 6
 #endif
 #ifndef K1B_PERSIST
-#define K1B_PERSIST 8
+#define K1B_PERSIST 7   // K1b CTAs per SM (A/B r02: 7 beat 8 and 6 on R and H, M1 and M2)
 #endif
 #ifndef K1_NF
 #define K1_NF 4   // mask planes in flight per lane (K1a)

@@ -159,18 +159,38 @@ __device__ bool label_tomb(const MapState& M, uint32_t slot, uint32_t L) {
 // ------------------------------------------------------------------------------------------
 // K5: lookup + overlap counts
 // ------------------------------------------------------------------------------------------
-__device__ __forceinline__ void count_add(const FrameScratch& X, uint64_t code, uint32_t add, int* err) {
+// A frame's (s, j) count table: table 0 (FrameScratch's ctab_* / ntrip / trip_s / trip_j) or table
+// 1 (the *2 fields; speculative counting alternates them between consecutive frames)
+struct CTab {
+  unsigned long long* key;
+  uint32_t *cnt, *idx, *ntrip, *ts, *tj;
+  int32_t CC, TCAP;
+};
+__device__ __forceinline__ CTab ctab(const FrameScratch& X, int p) {
+  CTab C;
+  C.key = p ? X.ctab_key2 : X.ctab_key;
+  C.cnt = p ? X.ctab_cnt2 : X.ctab_cnt;
+  C.idx = p ? X.ctab_idx2 : X.ctab_idx;
+  C.ntrip = p ? X.ntrip2 : X.ntrip;
+  C.ts = p ? X.trip_s2 : X.trip_s;
+  C.tj = p ? X.trip_j2 : X.trip_j;
+  C.CC = X.CC;
+  C.TCAP = X.TCAP;
+  return C;
+}
+
+__device__ __forceinline__ void count_add(const CTab& X, uint64_t code, uint32_t add, int* err) {
   uint32_t h = (uint32_t)mix64(code) & (uint32_t)(X.CC - 1);
   for (int probe = 0; probe < X.CC; ++probe) {
-    unsigned long long k = __ldcg(&X.ctab_key[h]);
+    unsigned long long k = __ldcg(&X.key[h]);
     if (k == KEY_EMPTY) {
-      k = atomicCAS(&X.ctab_key[h], KEY_EMPTY, (unsigned long long)code);
+      k = atomicCAS(&X.key[h], KEY_EMPTY, (unsigned long long)code);
       if (k == KEY_EMPTY) {
         const uint32_t t = atomicAdd(X.ntrip, 1u);
         if (t < (uint32_t)X.TCAP) {
-          X.trip_s[t] = (uint32_t)(code >> 32);
-          X.trip_j[t] = (uint32_t)code;
-          X.ctab_idx[t] = h;   // slot of triple t
+          X.ts[t] = (uint32_t)(code >> 32);
+          X.tj[t] = (uint32_t)code;
+          X.idx[t] = h;   // slot of triple t
         } else {
           raise_err(err, DERR_TRIPLES);
         }
@@ -178,7 +198,7 @@ __device__ __forceinline__ void count_add(const FrameScratch& X, uint64_t code, 
       }
     }
     if (k == code) {
-      atomicAdd(&X.ctab_cnt[h], add);
+      atomicAdd(&X.cnt[h], add);
       return;
     }
     h = (h + 1) & (uint32_t)(X.CC - 1);
@@ -209,9 +229,15 @@ constexpr int LK_CT = 2048;   // per-CTA (s, j) count table slots (in the dynami
 // spec: the pair's slot index was found by s2_spec during the previous frame's association (pms,
 // U32_EMPTY = key absent then): keys never move in the open-addressing table, so the probe starts
 // at that slot and matches at once; only keys absent then (new keys) probe from their home slot
+//
+// b0 > 0: run on CTAs b0.. only.  tag != 0: the speculative counting of frame f during the
+// previous frame's association -- a kept pair whose key is absent gets the key's slot created (no
+// labels: counts nothing; K7 of this frame fills it anyway), and every kept pair is chained onto its
+// slot (M.slh[slot] = tag << 32 | pair, wb.pnext) for the previous frame's K7 to find the pairs whose
+// counts its label changes correct.
 __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapState& M, const FrameScratch& X,
-                                          int Dt, bool spec = false) {
-  const uint32_t np = min(wb.npairs[f], (uint32_t)wb.PMAX);
+                                          const CTab& C, bool spec = false, int b0 = 0, uint32_t tag = 0) {
+  const uint32_t np = min(__ldcg(&wb.npairs[f]), (uint32_t)wb.PMAX);
   const size_t fo = (size_t)f * wb.PMAX;
   const int lane = threadIdx.x & 31;
   // the association's shared memory is free during this phase: a CTA table of (s, j) counts
@@ -239,13 +265,14 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
       }
       h = (h + 1) & (LK_CT - 1);
     }
-    count_add(X, code, add, M.err);
+    count_add(C, code, add, M.err);
   };
-  const uint32_t stride = LK_Q * gridDim.x * blockDim.x;
+  const uint32_t nb = gridDim.x - b0;
+  const uint32_t stride = LK_Q * nb * blockDim.x;
   const uint32_t hmask = (uint32_t)(M.MC - 1);
-  const uint32_t gthreads = gridDim.x * blockDim.x;
+  const uint32_t gthreads = nb * blockDim.x;
   // pair q of a lane: base + q * (grid threads), so every CTA gets an equal share
-  for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < np; base += stride) {
+  for (uint32_t base = (blockIdx.x - b0) * blockDim.x + (threadIdx.x & ~31u); base < np; base += stride) {
     uint32_t idx[LK_Q], s[LK_Q], slot[LK_Q], h[LK_Q];
     unsigned long long key[LK_Q];
     bool act[LK_Q];
@@ -268,6 +295,9 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
         if (ps != U32_EMPTY) h[q] = ps;
       }
     }
+    bool kept[LK_Q];
+#pragma unroll
+    for (int q = 0; q < LK_Q; ++q) kept[q] = act[q];
     SlotV sv[LK_Q];
     auto any_act = [&]() {
       bool a = false;
@@ -286,6 +316,28 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
         else if (sv[q].key == KEY_EMPTY) act[q] = false;
         else h[q] = (h[q] + 1) & hmask;
       }
+    }
+    if (tag) {   // (speculative counting) absent keys created, every kept pair chained onto its slot
+#pragma unroll
+      for (int q = 0; q < LK_Q; ++q) {
+        if (kept[q] && slot[q] == U32_EMPTY) {
+          bool created = false;
+          slot[q] = map_insert_key_c(M, key[q], &created);
+          sv[q].lab[0] = sv[q].lab[1] = U32_EMPTY;   // (a slot created now has no labels)
+          sv[q].ovf = U32_EMPTY;
+#pragma unroll
+          for (int i = 2; i < INLINE_LABELS; ++i) sv[q].lab[i] = U32_EMPTY;
+        }
+      }
+      unsigned long long old[LK_Q];
+#pragma unroll
+      for (int q = 0; q < LK_Q; ++q)
+        if (kept[q] && slot[q] != U32_EMPTY)
+          old[q] = atomicExch(&M.slh[slot[q]], ((unsigned long long)tag << 32) | idx[q]);
+#pragma unroll
+      for (int q = 0; q < LK_Q; ++q)
+        if (kept[q] && slot[q] != U32_EMPTY)
+          wb.pnext[fo + idx[q]] = (uint32_t)(old[q] >> 32) == tag ? (uint32_t)old[q] : U32_EMPTY;
     }
     // each pair's first two live labels (s, j) are counted warp-aggregated (a frame's keys mostly carry
     // one or two labels, and a warp's pairs mostly the same ones: per-lane shared atomics on one hot
@@ -359,7 +411,7 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
   lk_probe(6, tp);   // barrier: the CTA's slowest warp
   lk_probe(1, tp);
   for (int i = threadIdx.x; i < LK_CT; i += blockDim.x)   // flush the CTA's counts
-    if (cc[i]) count_add(X, ck[i], cc[i], M.err);
+    if (cc[i]) count_add(C, ck[i], cc[i], M.err);
   __syncthreads();
   lk_probe(2, tp);
 }
@@ -428,14 +480,14 @@ __device__ unsigned long long g_tgprof[4];   // DISC_S2PROF: target-update warp 
 // fresh: the CTA's static shared counters are not known to be zero (first frame of a launch); later
 // frames find them zeroed by the previous frame's association, and skip one barrier
 __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBufs& wb, const MapState& M,
-                                         const FrameScratch& X, const Params& P, int sem, bool fresh = true,
-                                         bool dbg = true) {
+                                         const FrameScratch& X, const CTab& C, const Params& P, int sem,
+                                         bool fresh = true, bool dbg = true) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // Layout: the shared-memory tables hold up to X.TCS (s, j) triples; a denser frame (hierarchical
   // SAM-"everything" masks overlapping many instances, BASELINE configs[4]) runs the same steps on
   // the same layout in a global-memory scratch sized for X.TCAP triples (block-scope atomics and
   // __syncthreads order it exactly as in shared memory).  Only a frame past X.TCAP fails (loudly).
-  const uint32_t ntr_all = __ldcg(X.ntrip);
+  const uint32_t ntr_all = __ldcg(C.ntrip);
   const uint32_t ntr = min(ntr_all, (uint32_t)X.TCAP);
   const bool gmode = ntr > (uint32_t)X.TCS;
   const int TC = gmode ? X.TCAP : X.TCS;
@@ -515,14 +567,14 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
   // ---- triples (count table released) + O10 exact fp64 geometric test (R10), thread per
   // triple; candidates for the visual gate are compacted ----
   for (uint32_t t = tid; t < ntr; t += blockDim.x) {
-    const uint32_t h = X.ctab_idx[t];
+    const uint32_t h = C.idx[t];
     // the lookup counted by physical label: its live id (after the previous frame's update every
     // label in the map is a live instance's physical label)
-    const uint32_t s = X.trip_s[t], j = __ldcg(&M.id_of[X.trip_j[t]]);
-    const uint32_t c = X.ctab_cnt[h];
+    const uint32_t s = C.ts[t], j = __ldcg(&M.id_of[C.tj[t]]);
+    const uint32_t c = C.cnt[h];
     const int64_t vj = M.vcount[j];
-    X.ctab_cnt[h] = 0;
-    X.ctab_key[h] = KEY_EMPTY;
+    C.cnt[h] = 0;
+    C.key[h] = KEY_EMPTY;
     t_s[t] = (uint8_t)s;
     t_j[t] = j;
     t_c[t] = c;
@@ -774,8 +826,10 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
   // ---- triple ids (refinement, debug export), debug copies (a window's last frame: the only one the
   // export reads), edge count; nothing below reads them before the next barrier ----
   for (uint32_t t = tid; t < ntr; t += blockDim.x) {
-    X.trip_j[t] = t_j[t];   // (the gate CTAs are done with the labels)
+    C.tj[t] = t_j[t];   // (the gate CTAs are done with the labels; k_refine reads table 0's)
     if (dbg) {
+      X.trip_sd[t] = t_s[t];
+      X.trip_jd[t] = t_j[t];
       X.trip_c[t] = t_c[t];
       X.trip_edge[t] = t_e[t];
     }
@@ -901,7 +955,7 @@ __device__ __forceinline__ void s2_assoc(int f, const FrameDesc& F, const WinBuf
     R.live_instances = live;
     *X.live_before = cnt_s[2];
     *X.ntrip_last = ntr;
-    *X.ntrip = 0;
+    *C.ntrip = 0;
   }
   __syncthreads();
   if (tid == 0) { n_j = 0; n_tgt = 0; n_seg = 0; rel_s = 0; merged_s = 0; edges_s = 0; n_cand = 0; }   // next frame
@@ -1228,8 +1282,15 @@ __device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc&
   if (lane < 6) M.aabb[(size_t)root * 6 + lane] = ab[lane];
 }
 
+// tagn != 0: frame f+1 was counted speculatively against the map before this update (into Cn; its
+// pairs chained on their slots under tagn): every label this update adds to (+1) or tombstones on (-1)
+// a slot corrects c_{s,label} of each of frame f+1's pairs (s, key) on that slot, so that frame f+1's
+// counts are exactly those its own lookup after this update would find (aggregated per CTA in shared
+// memory, added to Cn at the end).
+constexpr int DT_CT = 1024;   // per-CTA correction table slots
 __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBufs& wb, const MapState& M,
-                                         const FrameScratch& X, const Params& P, int sem) {
+                                         const FrameScratch& X, const Params& P, int sem,
+                                         const CTab& Cn, uint32_t tagn = 0) {
   const int lane = threadIdx.x & 31;
   // targets spread over the CTAs first (warp w of CTA b takes target w * G + b), so no CTA holds
   // them all and the items are shared out evenly
@@ -1247,16 +1308,38 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
     tb_s[t] = X.tgt_base[t];
     to_s[t] = X.tg_newoff[t];
   }
+  uint32_t dyn;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+  // the correction table at the end of the dynamic shared memory
+  const uint32_t dtb = (dyn - DT_CT * 12u) & ~15u;
+  unsigned long long* dk = (unsigned long long*)(smem_raw + dtb);
+  uint32_t* dc = (uint32_t*)(dk + DT_CT);
+  if (tagn)
+    for (int i = threadIdx.x; i < DT_CT; i += blockDim.x) { dk[i] = KEY_EMPTY; dc[i] = 0; }
   __syncthreads();
+  auto dt_add = [&](unsigned long long code, uint32_t add) {
+    uint32_t h = (uint32_t)mix64(code) & (DT_CT - 1);
+    for (int probe = 0; probe < 32; ++probe) {
+      unsigned long long k = dk[h];
+      if (k == KEY_EMPTY) {
+        k = atomicCAS(&dk[h], KEY_EMPTY, code);
+        if (k == KEY_EMPTY) k = code;
+      }
+      if (k == code) {
+        atomicAdd(&dc[h], add);
+        return;
+      }
+      h = (h + 1) & (DT_CT - 1);
+    }
+    count_add(Cn, code, add, M.err);
+  };
   // shared staging for the target warps' tracking rows (warps 0 .. K7_STG_WARPS-1, if it fits)
   double* stg = nullptr;
   {
-    uint32_t dyn;
-    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
     const size_t base = ((size_t)wb.SMAX * 20 + 127) & ~(size_t)127;
     const size_t per = ((size_t)K7_STG_ROWS * P.Dt * 8 + (size_t)P.Df * 4 + 15) & ~(size_t)15;   // rows + e
     const int w = threadIdx.x >> 5;
-    if (P.Dt > 0 && (P.Dt & 1) == 0 && w < K7_STG_WARPS && base + (size_t)K7_STG_WARPS * per <= dyn)
+    if (P.Dt > 0 && (P.Dt & 1) == 0 && w < K7_STG_WARPS && base + (size_t)K7_STG_WARPS * per <= dtb)
       stg = (double*)(smem_raw + base + (size_t)w * per);
   }
   for (int t = gw; t < ntgt; t += nw) {
@@ -1281,6 +1364,7 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
     atomicAdd(&g_s2items[3], (unsigned long long)ntgt);
   }
   const size_t fo = (size_t)f * wb.PMAX;
+  const size_t f1o = fo + wb.PMAX;   // frame f+1's pair records (tagn)
   const int nseg = *X.nseg;
   int delta = 0;
   // items: frame pairs (inserts), relabel items, entries of lists K6 moved (copies), two items per
@@ -1319,6 +1403,8 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
       const uint32_t it = itq[q];
       int tnew = -1;
       uint32_t snew = 0;
+      uint32_t dslot = U32_EMPTY;   // the slot whose labels changed (tagn)
+      uint32_t dLi = U32_EMPTY, dLt = U32_EMPTY;   // label added / tombstoned on it
       if (it < np) {
         const int t = dt_s[sq[q]];
         if (t >= 0) {
@@ -1344,7 +1430,7 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
               } else {
                 ins = label_insert(M, slot, L);
               }
-              if (ins) { tnew = t; snew = slot; delta++; }
+              if (ins) { tnew = t; snew = slot; delta++; dslot = slot; dLi = L; }
             }
           }
         }
@@ -1359,8 +1445,10 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
         const int t = X.seg_tgt[lo];
         const uint32_t L = tp_s[t];
         const uint32_t slot = M.arena[X.seg_base[lo] + (r - X.seg_off[lo])];
-        if (label_insert(M, slot, L)) { tnew = t; snew = slot; delta++; }
-        if (label_tomb(M, slot, X.seg_phys[lo])) delta--;
+        if (label_insert(M, slot, L)) { tnew = t; snew = slot; delta++; dLi = L; }
+        const uint32_t Lo = X.seg_phys[lo];
+        if (label_tomb(M, slot, Lo)) { delta--; dLt = Lo; }
+        dslot = slot;
       } else if (!stat && it < total) {
         const uint32_t r = it - np - nrel;
         int lo = 0, hi = ntgt - 1;   // last target with tg_mvoff <= r
@@ -1383,19 +1471,44 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
         const uint32_t pos = tb_s[tnew] + pb + __popc(peers & ((1u << lane) - 1u));
         M.arena[to_s[tnew] + pos] = snew;
       }
+      if (tagn) {   // count corrections of frame f+1 (warp-aggregated per (s, label) and sign)
+        uint32_t pi = U32_EMPTY;
+        if (dslot != U32_EMPTY && (dLi != U32_EMPTY || dLt != U32_EMPTY)) {
+          const unsigned long long v = __ldcg(&M.slh[dslot]);
+          if ((uint32_t)(v >> 32) == tagn) pi = (uint32_t)v;
+        }
+        while (__any_sync(0xffffffffu, pi != U32_EMPTY)) {
+          unsigned long long ci = KEY_EMPTY, ct = KEY_EMPTY;
+          if (pi != U32_EMPTY) {
+            const unsigned long long sh = (unsigned long long)__ldcg(&wb.pinfo[f1o + pi]) << 32;
+            if (dLi != U32_EMPTY) ci = sh | dLi;
+            if (dLt != U32_EMPTY) ct = sh | dLt;
+            pi = __ldcg(&wb.pnext[f1o + pi]);
+          }
+          const unsigned pa = __match_any_sync(0xffffffffu, ci);
+          if (ci != KEY_EMPTY && lane == __ffs(pa) - 1) dt_add(ci, (uint32_t)__popc(pa));
+          const unsigned pt = __match_any_sync(0xffffffffu, ct);
+          if (ct != KEY_EMPTY && lane == __ffs(pt) - 1) dt_add(ct, (uint32_t)(-__popc(pt)));
+        }
+      }
     }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) delta += __shfl_xor_sync(0xffffffffu, delta, o);
   if (lane == 0 && delta) atomicAdd((unsigned long long*)&M.counters[2], (unsigned long long)(int64_t)delta);
+  if (tagn) {   // the CTA's corrections into frame f+1's count table
+    __syncthreads();
+    for (int i = threadIdx.x; i < DT_CT; i += blockDim.x)
+      if (dc[i]) count_add(Cn, dk[i], dc[i], M.err);
+  }
 }
 
 // While CTA 0 starts the association of frame f, CTAs 1.. evaluate the pinned fp64 visual gate
 // (R15) of every (s, j) triple of the frame, warp per triple (the association keeps the geometric
 // edges whose gate passed).  Same dot_pin_reg as the single-CTA path: the same bits.
 __device__ __forceinline__ void s2_gate(int f, const WinBufs& wb, const MapState& M, const FrameScratch& X,
-                                     const Params& P) {
-  const uint32_t ntr = min(__ldcg(X.ntrip), (uint32_t)X.TCAP);
+                                     const CTab& C, const Params& P) {
+  const uint32_t ntr = min(__ldcg(C.ntrip), (uint32_t)X.TCAP);
   const size_t fo = (size_t)f * wb.SMAX;
   const double* trk = wb.trk + fo * P.Dt;
   const int lane = threadIdx.x & 31;
@@ -1403,7 +1516,7 @@ __device__ __forceinline__ void s2_gate(int f, const WinBufs& wb, const MapState
   const uint32_t w = (blockIdx.x - 1) * nwc + (threadIdx.x >> 5), nw = (gridDim.x - 1) * nwc;
   uint32_t done = 0;
   for (uint32_t t = w; t < ntr; t += nw) {
-    const uint32_t s = __ldcg(&X.trip_s[t]), j = __ldcg(&M.id_of[__ldcg(&X.trip_j[t])]);
+    const uint32_t s = __ldcg(&C.ts[t]), j = __ldcg(&M.id_of[__ldcg(&C.tj[t])]);
     const double TT = __ldcg(&M.TT[j]);
     const uint8_t tok = wb.tok[fo + s];
     const double dt = dot_pin_reg(trk + (size_t)s * P.Dt, M.T + (size_t)j * P.Dt, P.Dt);
@@ -1479,14 +1592,17 @@ __device__ __forceinline__ void s2_prefetch_hint(int f, const WinBufs& wb, const
 
 // K7 tail, run in the next phase: list lengths and exact |V| of the frame's targets, insert counter,
 // membership report fields
-__device__ __forceinline__ void s2_finalize(int f, const MapState& M, const FrameScratch& X) {
+// (cta0: CTA 0 alone runs it, before the next association)
+__device__ __forceinline__ void s2_finalize(int f, const MapState& M, const FrameScratch& X, bool cta0 = false) {
   const int ntgt = *X.ntgt;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     disc_frame_report& R = X.rep[f];
     R.live_memberships = M.counters[2];
     R.new_memberships = M.counters[2] - *X.live_before;
   }
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntgt; t += gridDim.x * blockDim.x) {
+  const int t0 = cta0 ? threadIdx.x : blockIdx.x * blockDim.x + threadIdx.x;
+  const int tn = cta0 ? blockDim.x : gridDim.x * blockDim.x;
+  for (int t = t0; t < ntgt; t += tn) {
     const uint32_t add = X.tgt_stage[t];
     M.lst_len[X.tgt_phys[t]] = X.tgt_base[t] + add;
     M.vcount[X.tgt_root[t]] += add;
@@ -1538,65 +1654,79 @@ __device__ __forceinline__ void grid_sync(uint32_t* bar, uint32_t target) {
   __syncthreads();
 }
 
-// Stage 2 of a window: the frames' map updates in order, three grid-synchronised phases per frame
-// (K5 lookup with the previous frame's K7 tail, K6 association on CTA 0, K7 apply) in one
-// persistent launch.
-__global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb, MapState M, FrameScratch X,
-                                                        Params P, int sem, int prof, int spec, int f0, int fn) {
+// Stage 2 of a window: the frames' map updates in order, in one persistent launch.  Frame f's
+// phases: K5 lookup (with frame f-1's K7 tail) | K6 association on CTA 0, the visual gate and the
+// next frame's speculative work on CTAs 1.. | K7 apply, grid-synchronised.
+//
+// spec 2 (default): frame f+1 is counted during frame f's association (against the map before
+// frame f's update) and frame f's K7 corrects those counts for every label it adds or tombstones on
+// a key of frame f+1 (s2_apply), so frame f+1 needs no lookup phase: two barriers per frame instead
+// of three.  spec 1: only frame f+1's slots are found early (its lookup re-reads them); 0: L2 hints.
+// Frame f counts into table (f - f0) & 1 (Xc); Xn is the other one.
+__device__ __forceinline__ void s2_frame(int f, int f0, int fe, const WinDesc& wd, const WinBufs& wb,
+                                         const MapState& M, const FrameScratch& X, const Params& P, int sem,
+                                         int spec, uint32_t& ep, int prof, uint32_t tag0) {
   const uint32_t G = gridDim.x;
-  uint32_t ep = 0;
-  unsigned long long t_prev = 0;
-  auto probe = [&](int i) {   // DISC_S2PROF: phase durations on CTA 0 (profiling aid)
+  const FrameDesc& F = wd.f[f];
+  const int p = (f - f0) & 1;
+  const CTab Cc = ctab(X, p), Cn = ctab(X, p ^ 1);   // this frame's count table, the next one's
+  const bool sp = spec >= 2 && f > f0 && G > 1;        // this frame was counted speculatively
+  const bool spn = spec >= 2 && f + 1 < fe && G > 1;   // the next one will be
+  auto probe = [&](int i) {   // DISC_S2PROF: phase end times on CTA 0 (profiling aid)
     if (prof && blockIdx.x == 0 && threadIdx.x == 0) {
       unsigned long long t_;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
-      if (i >= 0) atomicAdd(&g_s2prof[i], t_ - t_prev);
-      t_prev = t_;
+      atomicAdd(&g_s2prof[i], t_ - g_s2prof[5]);
+      g_s2prof[5] = t_;
     }
   };
-  probe(-1);
-  unsigned long long t_k0 = 0;
-  if (prof && blockIdx.x == 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_k0));
-  if (prof == 2) {   // DISC_S2PROF=2: cost of 64 empty grid barriers (profiling aid)
-    for (int i = 0; i < 64; ++i) grid_sync(wb.s2bar, G * ++ep);
-    probe(7);
-  }
-  unsigned long long c0 = 0;
-  auto cta_t = [&](int i) {   // this CTA's own work time in phase i (before its barrier wait)
-    if (prof) __syncthreads();   // (prof is grid-uniform)
-    if (prof && threadIdx.x == 0) {
-      unsigned long long t_;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
-      if (i >= 0) { atomicAdd(&g_s2cta[2 * i], t_ - c0); atomicMax(&g_s2cta[2 * i + 1], t_ - c0); }
-      c0 = t_;
-    }
-  };
-  const int fe = f0 + fn;   // frames [f0, fe) of the window (refine_active: one per launch)
-  for (int f = f0; f < fe; ++f) {
-    const FrameDesc& F = wd.f[f];
-    cta_t(-1);
-    s2_lookup(f, wb, M, X, P.Dt, spec && f > f0 && G > 1);
+  if (!sp) {
+    s2_lookup(f, wb, M, X, Cc, spec == 1 && f > f0 && G > 1);
     if (f > f0) s2_finalize(f - 1, M, X);
-    cta_t(0);
     grid_sync(wb.s2bar, G * ++ep);
     probe(0);
-    if (blockIdx.x == 0) {
-      s2_assoc(f, F, wb, M, X, P, sem, f == f0, f == fe - 1);
-    } else {
-      if (P.Dt > 0) s2_gate(f, wb, M, X, P);
-      if (f + 1 < fe) {
-        if (spec) s2_spec(f + 1, wb, M);
-        else s2_prefetch_hint(f + 1, wb, M);
-      }
-    }
-    grid_sync(wb.s2bar, G * ++ep);
-    probe(1);
-    cta_t(-1);
-    s2_apply(f, F, wb, M, X, P, sem);
-    cta_t(2);
-    grid_sync(wb.s2bar, G * ++ep);
-    probe(2);
+  } else if (blockIdx.x == 0) {
+    s2_finalize(f - 1, M, X, true);
+    __syncthreads();
   }
+  if (blockIdx.x == 0) {
+    s2_assoc(f, F, wb, M, X, Cc, P, sem, f == f0, f == fe - 1);
+  } else {
+    if (P.Dt > 0) s2_gate(f, wb, M, X, Cc, P);
+    if (spn) s2_lookup(f + 1, wb, M, X, Cn, false, 1, tag0 + (uint32_t)(f + 1));
+    else if (f + 1 < fe) {
+      if (spec) s2_spec(f + 1, wb, M);
+      else s2_prefetch_hint(f + 1, wb, M);
+    }
+  }
+  grid_sync(wb.s2bar, G * ++ep);
+  probe(1);
+  s2_apply(f, F, wb, M, X, P, sem, Cn, spn ? tag0 + (uint32_t)(f + 1) : 0u);
+  grid_sync(wb.s2bar, G * ++ep);
+  probe(2);
+}
+
+__global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb, MapState M, FrameScratch X,
+                                                        Params P, int sem, int prof, int spec, int f0, int fn,
+                                                        uint32_t tag0) {
+  const uint32_t G = gridDim.x;
+  uint32_t ep = 0;
+  unsigned long long t_k0 = 0;
+  if (prof && blockIdx.x == 0 && threadIdx.x == 0) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_k0));
+    g_s2prof[5] = t_k0;
+  }
+  if (prof == 2) {   // DISC_S2PROF=2: cost of 64 empty grid barriers (profiling aid)
+    for (int i = 0; i < 64; ++i) grid_sync(wb.s2bar, G * ++ep);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      atomicAdd(&g_s2prof[7], t_ - t_k0);
+      g_s2prof[5] = t_;
+    }
+  }
+  const int fe = f0 + fn;   // frames [f0, fe) of the window (refine_active: one per launch)
+  for (int f = f0; f < fe; ++f) s2_frame(f, f0, fe, wd, wb, M, X, P, sem, spec, ep, prof, tag0);
   if (fe > f0) s2_finalize(fe - 1, M, X);
   if (prof && blockIdx.x == 0 && threadIdx.x == 0) {   // the kernel's own span (CTA 0)
     unsigned long long t_;
@@ -1621,7 +1751,7 @@ __device__ __forceinline__ FrameDesc meta_desc(const FrameMeta* meta, int f) {
 }
 
 __global__ void __launch_bounds__(K6_THREADS, 1) k_s2_lookup(int f, WinBufs wb, MapState M, FrameScratch X, Params P) {
-  s2_lookup(f, wb, M, X, P.Dt);
+  s2_lookup(f, wb, M, X, ctab(X, 0));
 }
 
 // X1 send side: this shard's partial (s, physical label, count) triples of frame f
@@ -1648,20 +1778,20 @@ __global__ void __launch_bounds__(256) k_trip_merge(FrameScratch X, const uint32
     const uint32_t* b = all + (size_t)g * stride;
     const uint32_t n = b[0];
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
-      count_add(X, ((uint64_t)b[1 + 3 * t] << 32) | b[2 + 3 * t], b[3 + 3 * t], err);
+      count_add(ctab(X, 0), ((uint64_t)b[1 + 3 * t] << 32) | b[2 + 3 * t], b[3 + 3 * t], err);
   }
 }
 
 __global__ void __launch_bounds__(K6_THREADS, 1) k_s2_assoc(int f, const FrameMeta* meta, WinBufs wb, MapState M,
                                                             FrameScratch X, Params P, int sem) {
   const FrameDesc F = meta_desc(meta, f);
-  s2_assoc(f, F, wb, M, X, P, sem);   // one CTA: it evaluates the visual gate of its candidates itself
+  s2_assoc(f, F, wb, M, X, ctab(X, 0), P, sem);   // one CTA: it evaluates the visual gate of its candidates itself
 }
 
 __global__ void __launch_bounds__(K6_THREADS, 1) k_s2_apply(int f, const FrameMeta* meta, WinBufs wb, MapState M,
                                                             FrameScratch X, Params P, int sem) {
   const FrameDesc F = meta_desc(meta, f);
-  s2_apply(f, F, wb, M, X, P, sem);
+  s2_apply(f, F, wb, M, X, P, sem, ctab(X, 0));
 }
 
 // X2 send side: this shard's new memberships per target (own keys), its live count and the live
@@ -2052,7 +2182,7 @@ void launch_refine(int f, int S, const WinBufs& wb, const MapState& M, const Fra
 }
 
 int launch_stage2(const WinDesc& wd, const WinBufs& wb, const MapState& M, const FrameScratch& X, const Params& P,
-                  bool sem, int nsm, int nres, cudaStream_t st) {
+                  bool sem, int nsm, int nres, uint32_t* tag_seq, cudaStream_t st) {
   const size_t sm6 = k6_smem_bytes(wb.SMAX, X.TCS);
   static size_t set_for = 0;
   if (set_for != sm6) {
@@ -2064,10 +2194,19 @@ int launch_stage2(const WinDesc& wd, const WinBufs& wb, const MapState& M, const
   // cooperative launch: its CTAs wait on one another at the grid barriers, so co-residency must
   // be guaranteed, not assumed
   int semi = sem ? 1 : 0;
-  static const int spec = getenv("DISC_S2_SPEC") ? atoi(getenv("DISC_S2_SPEC")) : 1;   // speculative lookups
+  // speculative work during the association (k_stage2): 2 counting + corrections, 1 slots, 0 hints
+  static const int spec = getenv("DISC_S2_SPEC") ? atoi(getenv("DISC_S2_SPEC")) : 2;
   int f0 = 0, fn = wd.n;
+  // slot-chain tags of the speculatively counted frames: the map's own sequence (never reused
+  // between clears of M.slh, so no clearing per frame); 0 = none
+  if (*tag_seq == 0 || *tag_seq + (uint32_t)wd.n + 1 < *tag_seq) {   // first use / wrap: clear, restart
+    cudaMemsetAsync(M.slh, 0, sizeof(unsigned long long) * M.MC, st);
+    *tag_seq = 1;
+  }
+  uint32_t tag0 = *tag_seq;
+  *tag_seq += (uint32_t)wd.n + 1;
   void* args[] = {(void*)&wd, (void*)&wb, (void*)&M, (void*)&X, (void*)&P, (void*)&semi, (void*)&prof, (void*)&spec,
-                  (void*)&f0, (void*)&fn};
+                  (void*)&f0, (void*)&fn, (void*)&tag0};
   if (!P.refine) {
     cudaLaunchCooperativeKernel((const void*)k_stage2, dim3(grid), dim3(K6_THREADS), args, sm6, st);
     debug_check(st, "k_stage2", -1);
