@@ -476,7 +476,9 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
     NSum* scr = dalloc<NSum>(m, (size_t)nsmid * K1_SLOTS_PER_SM * K1_PT, 0);
     uint32_t* slot = dalloc<uint32_t>(m, (size_t)nsmid, 0);
     chk(scr); chk(slot);
-    for (int wbi = 0; wbi < 2; ++wbi) { m->Wb[wbi].k1scr = scr; m->Wb[wbi].k1slot = slot; }
+    uint32_t* s2sm = dalloc<uint32_t>(m, 8, 0);
+    chk(s2sm);
+    for (int wbi = 0; wbi < 2; ++wbi) { m->Wb[wbi].k1scr = scr; m->Wb[wbi].k1slot = slot; m->Wb[wbi].s2sm = s2sm; }
   }
   // ---- map ----
   MapState& M = m->M;

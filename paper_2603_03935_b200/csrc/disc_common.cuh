@@ -112,6 +112,8 @@ struct WinBufs {
   uint32_t* pms;              // [win][PMAX] map slot found by K5 (or U32_EMPTY)
   uint2* plab;                // [win][PMAX] the slot's first two labels seen by K5 (K7 skips inserts of a present label)
   uint32_t* pnext;            // [win][PMAX] next pair of the frame on the same map slot (speculative counting)
+  uint32_t* s2sm;             // [8] (shared by both buffers) SMs hosting a running k_stage2 CTA: bits [0, 5) words,
+                              // [5] running k_stage2 CTAs -- stage 1's persistent CTAs keep off exactly those SMs
   // semantic
   double* fpart;              // [win][FCHUNKS][Df] partial column sums
   float* fbar;                // [win][Df]

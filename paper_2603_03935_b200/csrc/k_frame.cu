@@ -179,9 +179,16 @@ __device__ __forceinline__ uint32_t range_bits(int a, int b) {   // bits [a, b),
   return (b >= 32 ? 0xFFFFFFFFu : ((1u << b) - 1u)) & ~((1u << a) - 1u);
 }
 
-__device__ __forceinline__ bool on_reserved_sm(int reserve) {
+// Stage 2's persistent grid (cooperative, one CTA per SM) lands where the hardware puts it.  While
+// one runs, a stage-1 CTA keeps off exactly the SMs it occupies (s2sm: its CTAs' SM bits and count);
+// otherwise off SMs [0, reserve), which stays free for the next stage-2 launch.  (A fixed [0, reserve)
+// alone left stage 1 the SMs >= reserve minus the stage-2 CTAs placed there: ~16 instead of 48 SMs
+// when a stage-2 grid started first and spread over the GPU.)
+__device__ __forceinline__ bool on_reserved_sm(int reserve, const uint32_t* s2sm) {
+  if (reserve <= 0) return false;
   uint32_t sm;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  if (*(volatile const uint32_t*)(s2sm + 5) > 0) return (*(volatile const uint32_t*)(s2sm + (sm >> 5)) >> (sm & 31)) & 1u;
   return (int)sm < reserve;
 }
 
@@ -204,7 +211,7 @@ constexpr int K1A_SECT = K1_THREADS;   // sectors per item
 template <bool VEC>
 __global__ void __launch_bounds__(K1_THREADS, K1A_PERSIST) k_masks(WinDesc wd, WinBufs wb, int items_f, int reserve,
                                                                   int ablate) {
-  if (on_reserved_sm(reserve)) return;
+  if (on_reserved_sm(reserve, wb.s2sm)) return;
   extern __shared__ int32_t bb_s[];          // [S][4] umin, vmin, umax, vmax
   __shared__ uint32_t item_s;
   const uint32_t total = (uint32_t)items_f * (uint32_t)wd.n;
@@ -387,7 +394,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1A_PERSIST) k_masks(WinDesc wd, W
 template <bool SEM>
 __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, WinBufs wb, Params P, int* err,
                                                                  int tiles_x, int reserve, int ablate) {
-  if (on_reserved_sm(reserve)) return;
+  if (on_reserved_sm(reserve, wb.s2sm)) return;
   extern __shared__ uint32_t vs_s[];                        // [S] |V_s| contributions
   __shared__ unsigned long long kt[K1_KT];                  // CTA key table
   __shared__ uint32_t ptc[2 * K1_KT];                       // pair slots 2 li, 2 li + 1: s or EMPTY

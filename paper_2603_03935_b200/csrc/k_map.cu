@@ -466,7 +466,10 @@ __device__ unsigned long long g_k6prof[16];
 __device__ unsigned long long g_s2prof[8];   // DISC_S2PROF phase sums
 __device__ unsigned long long g_s2cta[8];
 __device__ unsigned long long g_s2items[4];
-__device__ unsigned long long g_tgprof[4];   // DISC_S2PROF: target-update warp time sum / max, count, item-loop time sum   // DISC_S2PROF: K7 items: pairs, relabels, list-move copies, targets
+__device__ unsigned long long g_tgprof[4];   // DISC_S2PROF: target-update warp time sum / max, count
+__device__ unsigned long long g_approf[8];
+__device__ unsigned long long g_s2place[4];   // k_stage2 CTA placement: launches, CTAs, CTAs on SMs >= the grid size
+__device__ unsigned long long g_tghist[24];   // DISC_S2PROF: target time sum / count / max by candidates (new, <=2, <=4, <=8, <=16, <=32, more)   // DISC_S2PROF: K7 sub-steps, per-frame maxima [0..3], summed [4..7]
 #define K6_PROBE(i)                                                                          \
   do {                                                                                       \
     if (threadIdx.x == 0) {                                                                  \
@@ -1097,12 +1100,6 @@ __device__ void apply_target_warp_general(int t, int f, const FrameDesc& F, cons
 // descriptors; member / detection ids; their attributes and T / t rows together; the embedding
 // copy — with T_root's sums and dot_pin(T, T) kept in registers (same lane / element order as
 // dot_pin_reg: lane l holds d = l, l + 32, ... ascending).
-#ifndef K7_STG_ROWS
-#define K7_STG_ROWS 8    // tracking rows per staged batch of a target warp
-#endif
-#ifndef K7_STG_WARPS
-#define K7_STG_WARPS 2   // warps per CTA with a staging area (targets go to warp w of CTA b as w * G + b)
-#endif
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
@@ -1110,12 +1107,54 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
+// 1-D TMA: a bulk global -> shared copy completing on a shared-memory mbarrier
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n\tfence.mbarrier_init.release.cluster;" ::"r"(b) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst), b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+               "l"(src), "r"(bytes), "r"(b)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t ph) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT;\n\t}" ::"r"(b),
+      "r"(ph)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 
-// stg: this warp's shared staging area for K7_STG_ROWS tracking rows (nullptr: register path)
+__device__ unsigned long long g_tgstep[8];   // DISC_S2PROF (-DTG_PROF): fast-path target sub-step time sums
+#ifdef TG_PROF
+#define TG_STEP(i)                                                          \
+  do {                                                                      \
+    unsigned long long t_;                                                  \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
+    if (i >= 0 && lane == 0) atomicAdd(&g_tgstep[i], t_ - tg_t);          \
+    tg_t = t_;                                                              \
+  } while (0)
+#else
+#define TG_STEP(i) do { } while (0)
+#endif
+// stg: this warp's shared staging area for `rows` tracking rows and an embedding row, filled by 1-D
+// TMA bulk copies completing on the mbarrier `bar` (phase ph) (nullptr: register path)
 __device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc& F, const WinBufs& wb,
                                                   const MapState& M, const FrameScratch& X, const Params& P, int sem,
-                                                  double* stg) {
+                                                  double* stg, int rows, uint64_t* bar, uint32_t& ph) {
   const int lane = threadIdx.x & 31;
+  unsigned long long tg_t = 0;
+  TG_STEP(-1);
   const size_t fo = (size_t)f * wb.SMAX;
   const double* trk = wb.trk + fo * P.Dt;
   const int kind = X.tg_kind[t];
@@ -1133,6 +1172,7 @@ __device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc&
   const bool is_mem = (uint32_t)lane < mcnt, is_det = !is_mem && (uint32_t)lane < n;
   const uint32_t cid = (is_mem || is_det) ? X.tg_cand[t * 32 + lane] : 0u;
 
+  TG_STEP(0);
   // attributes of the candidate
   int obs = 0;
   float qi = -INFINITY;
@@ -1148,6 +1188,7 @@ __device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc&
     qi = wb.qf[(fo + cid) * 6 + 4];
     for (int k = 0; k < 6; ++k) ab[k] = wb.daabb[(fo + cid) * 6 + k];
   }
+  TG_STEP(1);
   // T sums, pinned order: T_root (new instance: t_s1) then J ascending then Sd ascending
   double acc[16];
   const int nt = (Dt + 31) / 32;
@@ -1155,26 +1196,31 @@ __device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc&
   // new instance: its embedding row goes to shared memory with the tracking rows' first batch
   // (staged path; no registers held across the sums), else it is copied at the end
   const int D4 = Df / 4;
-  float4* stg_e = stg ? (float4*)(stg + (size_t)K7_STG_ROWS * Dt) : nullptr;
-  if (stg && kind == 1 && sem)
-    for (int d4 = lane; d4 < D4; d4 += 32) cp_async16(stg_e + d4, (const float4*)(wb.emb + (fo + cid0) * Df) + d4);
+  float4* stg_e = stg ? (float4*)(stg + (size_t)rows * Dt) : nullptr;
+  const bool e_stg = stg && kind == 1 && sem;
   if (stg) {
-    // the candidates' rows (candidate 0 = the base: T_root = T of mem[0], the min id, or t_s1)
-    // staged K7_STG_ROWS at a time with async copies, so a batch costs one memory round trip;
-    // summed in the pinned order from shared memory
+    // the candidates' rows (candidate 0 = the base: T_root = T of mem[0], the min id, or t_s1),
+    // `rows` at a time: lane i copies candidate i's row with one bulk copy (the TMA engine moves
+    // them, not the warp's load slots), one round trip per batch; summed in the pinned order from
+    // shared memory
 #pragma unroll
     for (int k = 0; k < 16; ++k) acc[k] = 0.0;
-    const int c16 = Dt / 2;   // 16-byte chunks per row
-    for (uint32_t i0 = 0; i0 < n; i0 += K7_STG_ROWS) {
-      const uint32_t nb = min((uint32_t)K7_STG_ROWS, n - i0);
-      for (uint32_t b = 0; b < nb; ++b) {
-        const uint32_t i = i0 + b;
-        const uint32_t id = __shfl_sync(0xffffffffu, cid, i);
-        const double* row = (kind == 0 && i < mcnt) ? M.T + (size_t)id * Dt : trk + (size_t)id * Dt;
-        for (int c = lane; c < c16; c += 32) cp_async16(stg + (size_t)b * Dt + 2 * c, row + 2 * c);
-      }
-      cp_async_wait_all();
+    const uint32_t rb = (uint32_t)Dt * 8u;   // bytes per row
+    for (uint32_t i0 = 0; i0 < n; i0 += (uint32_t)rows) {
+      const uint32_t nb = min((uint32_t)rows, n - i0);
+      fence_proxy_async_smem();   // (this warp's reads of the previous batch before the async writes)
       __syncwarp();
+      const bool e_now = e_stg && i0 == 0;
+      if (lane == 0) mbar_expect(bar, nb * rb + (e_now ? (uint32_t)Df * 4u : 0u));
+      __syncwarp();
+      if ((uint32_t)lane >= i0 && (uint32_t)lane < i0 + nb) {
+        const uint32_t i = (uint32_t)lane;
+        const double* row = (kind == 0 && i < mcnt) ? M.T + (size_t)cid * Dt : trk + (size_t)cid * Dt;
+        bulk_g2s(stg + (size_t)(i - i0) * Dt, row, rb, bar);
+      }
+      if (e_now && lane == 31) bulk_g2s(stg_e, wb.emb + (fo + cid0) * Df, (uint32_t)Df * 4u, bar);
+      mbar_wait(bar, ph);
+      ph ^= 1u;
       for (uint32_t b = 0; b < nb; ++b) {
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
@@ -1205,6 +1251,7 @@ __device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc&
       }
     }
   }
+  TG_STEP(2);
   double tt = 0.0;
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
@@ -1250,6 +1297,7 @@ __device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc&
   } else if (has_e) {
     for (int d4 = lane; d4 < Df / 4; d4 += 32) ed[d4] = es[d4];
   }
+  TG_STEP(3);
   if (kind == 0 && is_mem) {   // members: lists of other physical labels reset, J killed
     if (pm != L) {
       M.lst_len[pm] = 0;
@@ -1280,6 +1328,7 @@ __device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc&
     if (Dt > 0) M.TT[root] = tt;
   }
   if (lane < 6) M.aabb[(size_t)root * 6 + lane] = ab[lane];
+  TG_STEP(4);
 }
 
 // tagn != 0: frame f+1 was counted speculatively against the map before this update (into Cn; its
@@ -1288,10 +1337,25 @@ __device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc&
 // counts are exactly those its own lookup after this update would find (aggregated per CTA in shared
 // memory, added to Cn at the end).
 constexpr int DT_CT = 1024;   // per-CTA correction table slots
+#ifndef K7_DYN
+#define K7_DYN 0
+#endif
+#ifndef K7_TGT_NOCHUNK
+#define K7_TGT_NOCHUNK 0
+#endif
 __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBufs& wb, const MapState& M,
                                          const FrameScratch& X, const Params& P, int sem,
-                                         const CTab& Cn, uint32_t tagn = 0) {
+                                         const CTab& Cn, uint32_t tagn = 0, int prof = 0) {
   const int lane = threadIdx.x & 31;
+  unsigned long long ta0 = 0;
+  auto amark = [&](int i) {   // DISC_S2PROF: sub-step end times (max over the warps, this frame)
+    if (!prof || lane != 0) return;
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    if (i < 0) ta0 = t_;
+    else atomicMax(&g_approf[i], t_ - ta0);
+  };
+  amark(-1);
   // targets spread over the CTAs first (warp w of CTA b takes target w * G + b), so no CTA holds
   // them all and the items are shared out evenly
   const int gw = (threadIdx.x >> 5) * gridDim.x + blockIdx.x, nw = gridDim.x * (blockDim.x >> 5);
@@ -1317,6 +1381,7 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
   if (tagn)
     for (int i = threadIdx.x; i < DT_CT; i += blockDim.x) { dk[i] = KEY_EMPTY; dc[i] = 0; }
   __syncthreads();
+  amark(0);
   auto dt_add = [&](unsigned long long code, uint32_t add) {
     uint32_t h = (uint32_t)mix64(code) & (DT_CT - 1);
     for (int probe = 0; probe < 32; ++probe) {
@@ -1333,26 +1398,43 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
     }
     count_add(Cn, code, add, M.err);
   };
-  // shared staging for the target warps' tracking rows (warps 0 .. K7_STG_WARPS-1, if it fits)
+  // shared staging (TMA bulk copies) for warp 0's tracking rows: the targets of a frame (a few dozen,
+  // fewer than the CTAs) are each warp 0 of one CTA; up to 32 rows (a fast-path target's candidates
+  // in one round trip) as far as the bytes between the routing and the correction tables allow
   double* stg = nullptr;
+  uint64_t* bar = nullptr;
+  int rows = 0;
+  uint32_t ph = 0;
   {
     const size_t base = ((size_t)wb.SMAX * 20 + 127) & ~(size_t)127;
-    const size_t per = ((size_t)K7_STG_ROWS * P.Dt * 8 + (size_t)P.Df * 4 + 15) & ~(size_t)15;   // rows + e
-    const int w = threadIdx.x >> 5;
-    if (P.Dt > 0 && (P.Dt & 1) == 0 && w < K7_STG_WARPS && base + (size_t)K7_STG_WARPS * per <= dtb)
-      stg = (double*)(smem_raw + base + (size_t)w * per);
-  }
-  for (int t = gw; t < ntgt; t += nw) {
-    unsigned long long t0_, t1_;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0_));
-    apply_target_warp(t, f, F, wb, M, X, P, sem, stg);
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1_));
-    if (lane == 0) {
-      atomicAdd(&g_tgprof[0], t1_ - t0_);
-      atomicMax(&g_tgprof[1], t1_ - t0_);
-      atomicAdd(&g_tgprof[2], 1ull);
+    const size_t room = dtb > base + 128 + (size_t)P.Df * 4 ? dtb - base - 128 - (size_t)P.Df * 4 : 0;
+    rows = P.Dt > 0 ? (int)min((size_t)32, room / ((size_t)P.Dt * 8)) : 0;
+    if (P.Dt > 0 && (P.Dt & 1) == 0 && (P.Df & 3) == 0 && rows >= 4 && (threadIdx.x >> 5) == 0) {
+      bar = (uint64_t*)(smem_raw + base);
+      stg = (double*)(smem_raw + base + 128);
+      if (lane == 0) mbar_init(bar);
+      __syncwarp();
     }
   }
+  for (int t = gw; t < ntgt; t += nw) {
+    unsigned long long t0_ = 0, t1_;
+    if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0_));
+    apply_target_warp(t, f, F, wb, M, X, P, sem, stg, rows, bar, ph);
+    if (prof) {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1_));
+      if (lane == 0) {
+        atomicAdd(&g_tgprof[0], t1_ - t0_);
+        atomicMax(&g_tgprof[1], t1_ - t0_);
+        atomicAdd(&g_tgprof[2], 1ull);
+        const uint32_t n = X.tg_kind[t] ? 0u : min(33u, X.tg_mcnt[t] + X.tg_dcnt[t]);   // 0: new instance
+        const int b = n == 0 ? 0 : n <= 2 ? 1 : n <= 4 ? 2 : n <= 8 ? 3 : n <= 16 ? 4 : n <= 32 ? 5 : 6;
+        atomicAdd(&g_tghist[b], t1_ - t0_);
+        atomicAdd(&g_tghist[8 + b], 1ull);
+        atomicMax(&g_tghist[16 + b], t1_ - t0_);
+      }
+    }
+  }
+  amark(1);
   const uint32_t np = min(wb.npairs[f], (uint32_t)wb.PMAX);
   const uint32_t nrel = *X.nrel;
   const uint32_t nmove = X.tg_mvoff[ntgt];
@@ -1373,14 +1455,25 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
   // relabel / copy items (uneven) come in 64-item chunks from a counter.  (All chunks from one
   // counter serialised ~1.5 k atomics per H frame on one L2 address.)
   const uint32_t npb = (np + 63) / 64;   // pair blocks
-  uint32_t sblk = (uint32_t)gw;
+  // block b goes to warp (b + ntgt) mod nw: the target warps (gw < ntgt) get one only when there are
+  // more blocks than other warps
+  uint32_t sblk = ((uint32_t)gw + (uint32_t)nw - (uint32_t)min(ntgt, nw)) % (uint32_t)nw;
+  // K7_DYN 0: the relabel / copy blocks (items np .. total) follow the pair blocks in the same static
+  // round robin (no shared counter: every warp's one atomic on it serialised ~1.6 k atomics per frame
+  // on one L2 address); 1: they come in 64-item chunks from X.work
+  const uint32_t nbt = npb + (K7_DYN ? 0u : (nrel + nmove + 63) / 64);
   for (;;) {
     uint32_t base = 0;
     const bool stat = sblk < npb;   // a static pair block: its items past np are nobody's
     if (stat) {
       base = sblk * 64u;
       sblk += (uint32_t)nw;
+    } else if (!K7_DYN) {
+      if (sblk >= nbt) break;
+      base = np + (sblk - npb) * 64u;
+      sblk += (uint32_t)nw;
     } else {
+      if (K7_TGT_NOCHUNK && gw < ntgt) break;   // (target warps leave the uneven items to the others)
       if (lane == 0) base = atomicAdd(X.work, 64u);
       base = __shfl_sync(0xffffffffu, base, 0) + npb * 64u;
       if (base >= npb * 64u + nrel + nmove) break;
@@ -1493,6 +1586,7 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
       }
     }
   }
+  amark(2);
 #pragma unroll
   for (int o = 16; o; o >>= 1) delta += __shfl_xor_sync(0xffffffffu, delta, o);
   if (lane == 0 && delta) atomicAdd((unsigned long long*)&M.counters[2], (unsigned long long)(int64_t)delta);
@@ -1501,19 +1595,21 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
     for (int i = threadIdx.x; i < DT_CT; i += blockDim.x)
       if (dc[i]) count_add(Cn, dk[i], dc[i], M.err);
   }
+  amark(3);
 }
 
 // While CTA 0 starts the association of frame f, CTAs 1.. evaluate the pinned fp64 visual gate
 // (R15) of every (s, j) triple of the frame, warp per triple (the association keeps the geometric
 // edges whose gate passed).  Same dot_pin_reg as the single-CTA path: the same bits.
+// (on CTAs 1 .. gc)
 __device__ __forceinline__ void s2_gate(int f, const WinBufs& wb, const MapState& M, const FrameScratch& X,
-                                     const CTab& C, const Params& P) {
+                                     const CTab& C, const Params& P, uint32_t gc) {
   const uint32_t ntr = min(__ldcg(C.ntrip), (uint32_t)X.TCAP);
   const size_t fo = (size_t)f * wb.SMAX;
   const double* trk = wb.trk + fo * P.Dt;
   const int lane = threadIdx.x & 31;
   const uint32_t nwc = blockDim.x >> 5;
-  const uint32_t w = (blockIdx.x - 1) * nwc + (threadIdx.x >> 5), nw = (gridDim.x - 1) * nwc;
+  const uint32_t w = (blockIdx.x - 1) * nwc + (threadIdx.x >> 5), nw = gc * nwc;
   uint32_t done = 0;
   for (uint32_t t = w; t < ntr; t += nw) {
     const uint32_t s = __ldcg(&C.ts[t]), j = __ldcg(&M.id_of[__ldcg(&C.tj[t])]);
@@ -1624,15 +1720,31 @@ void k6_prof_dump() {
     fprintf(stderr, "s2 phase ns: lookup %llu assoc %llu apply %llu kernel span %llu (64 barriers x launches: %llu)\n", g[0], g[1], g[2], g[6], g[7]);
     unsigned long long c[8];
     cudaMemcpyFromSymbol(c, g_s2cta, sizeof(c));
-    fprintf(stderr, "s2 per-CTA work: lookup sum %llu max %llu, apply sum %llu max %llu\n", c[0], c[1], c[4], c[5]);
+    fprintf(stderr, "s2 per-frame CTA work maxima, summed: association (CTA 0) %llu, gate + next frame's counting %llu, apply %llu\n",
+            c[4], c[5], c[6]);
     cudaMemcpyFromSymbol(c, g_s2items, 4 * sizeof(unsigned long long));
     fprintf(stderr, "s2 K7 items: pairs %llu relabels %llu moves %llu targets %llu\n", c[0], c[1], c[2], c[3]);
     cudaMemcpyFromSymbol(c, g_lkprof, 8 * sizeof(unsigned long long));
     fprintf(stderr, "s2 lookup CTA0 (thread 0): init %llu flush %llu | records %llu status+probes %llu labels %llu aggregate %llu wait-for-CTA %llu\n",
             c[0], c[2], c[7], c[3], c[4], c[5], c[6]);
+    cudaMemcpyFromSymbol(c, g_approf, 8 * sizeof(unsigned long long));
+    fprintf(stderr, "s2 apply sub-steps (per-frame max end time, summed): routing %llu targets %llu items %llu flush %llu\n",
+            c[4], c[5], c[6], c[7]);
+    unsigned long long hh[24];
+    cudaMemcpyFromSymbol(hh, g_tghist, sizeof(hh));
+    fprintf(stderr, "s2 target time by candidates (sum ns / count / max ns):");
+    const char* nm[7] = {"new", "<=2", "<=4", "<=8", "<=16", "<=32", ">32"};
+    for (int b = 0; b < 7; ++b) fprintf(stderr, " %s %llu/%llu/%llu", nm[b], hh[b], hh[8 + b], hh[16 + b]);
+    fprintf(stderr, "\n");
+    cudaMemcpyFromSymbol(c, g_tgstep, 5 * sizeof(unsigned long long));
+    fprintf(stderr, "s2 fast-path target steps (sums, -DTG_PROF): descriptors %llu attributes %llu rows+sums %llu e/Q %llu writes %llu\n",
+            c[0], c[1], c[2], c[3], c[4]);
     cudaMemcpyFromSymbol(c, g_tgprof, 3 * sizeof(unsigned long long));
     fprintf(stderr, "s2 target warps: sum %llu max %llu count %llu\n", c[0], c[1], c[2]);
   }
+  unsigned long long pl[4];
+  cudaMemcpyFromSymbol(pl, g_s2place, sizeof(pl));
+  fprintf(stderr, "s2 placement: %llu launches, %llu CTAs, %llu on SMs outside [0, grid)\n", pl[0], pl[1], pl[2]);
   unsigned long long h[16];
   cudaMemcpyFromSymbol(h, g_k6prof, sizeof(h));
   fprintf(stderr, "k6 phase ns (cumulative):");
@@ -1689,21 +1801,55 @@ __device__ __forceinline__ void s2_frame(int f, int f0, int fe, const WinDesc& w
     s2_finalize(f - 1, M, X, true);
     __syncthreads();
   }
+  unsigned long long tph = 0;   // DISC_S2PROF: this CTA's work time per phase (max over the CTAs)
+  auto cta_mark = [&](int slot) {
+    if (!prof) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      if (slot >= 0) atomicMax(&g_s2cta[slot], t_ - tph);
+      tph = t_;
+    }
+  };
+  auto cta_fold = [&]() {   // (CTA 0 after a barrier: per-frame maxima into the sums)
+    if (prof && blockIdx.x == 0 && threadIdx.x == 0) {
+      for (int i = 0; i < 3; ++i) { g_s2cta[4 + i] += g_s2cta[i]; g_s2cta[i] = 0; }
+      for (int i = 0; i < 4; ++i) { g_approf[4 + i] += g_approf[i]; g_approf[i] = 0; }
+    }
+  };
+  cta_mark(-1);
+  // spec 3: the gate on CTAs 1 .. gc (a triple per warp), frame f+1's counting on the others
+  const uint32_t ntr_c = P.Dt > 0 && spec >= 3 ? min(__ldcg(Cc.ntrip), (uint32_t)X.TCAP) : 0u;
+  const uint32_t gc = P.Dt > 0 ? min(max(1u, G / 4), max(1u, (ntr_c + 15) / 16)) : 0u;
   if (blockIdx.x == 0) {
     s2_assoc(f, F, wb, M, X, Cc, P, sem, f == f0, f == fe - 1);
+    cta_mark(0);
+  } else if (spec >= 3 && G > 2) {
+    if (blockIdx.x <= gc) {
+      if (P.Dt > 0) s2_gate(f, wb, M, X, Cc, P, gc);
+    } else if (spn) {
+      s2_lookup(f + 1, wb, M, X, Cn, false, 1 + gc, tag0 + (uint32_t)(f + 1));
+    }
+    cta_mark(1);
   } else {
-    if (P.Dt > 0) s2_gate(f, wb, M, X, Cc, P);
+    if (P.Dt > 0) s2_gate(f, wb, M, X, Cc, P, G - 1);
     if (spn) s2_lookup(f + 1, wb, M, X, Cn, false, 1, tag0 + (uint32_t)(f + 1));
     else if (f + 1 < fe) {
       if (spec) s2_spec(f + 1, wb, M);
       else s2_prefetch_hint(f + 1, wb, M);
     }
+    cta_mark(1);
   }
   grid_sync(wb.s2bar, G * ++ep);
   probe(1);
-  s2_apply(f, F, wb, M, X, P, sem, Cn, spn ? tag0 + (uint32_t)(f + 1) : 0u);
+  cta_fold();
+  cta_mark(-1);
+  s2_apply(f, F, wb, M, X, P, sem, Cn, spn ? tag0 + (uint32_t)(f + 1) : 0u, prof);
+  cta_mark(2);
   grid_sync(wb.s2bar, G * ++ep);
   probe(2);
+  cta_fold();
 }
 
 __global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb, MapState M, FrameScratch X,
@@ -1725,9 +1871,22 @@ __global__ void __launch_bounds__(K6_THREADS, 1) k_stage2(WinDesc wd, WinBufs wb
       g_s2prof[5] = t_;
     }
   }
+  uint32_t sm_ = 0;
+  if (threadIdx.x == 0) {   // this CTA's SM, published to stage 1 (on_reserved_sm); placement record
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));
+    atomicOr(&wb.s2sm[sm_ >> 5], 1u << (sm_ & 31));
+    atomicAdd(&wb.s2sm[5], 1u);
+    if (blockIdx.x == 0) atomicAdd(&g_s2place[0], 1ull);
+    atomicAdd(&g_s2place[1], 1ull);
+    if (sm_ >= G) atomicAdd(&g_s2place[2], 1ull);
+  }
   const int fe = f0 + fn;   // frames [f0, fe) of the window (refine_active: one per launch)
   for (int f = f0; f < fe; ++f) s2_frame(f, f0, fe, wd, wb, M, X, P, sem, spec, ep, prof, tag0);
   if (fe > f0) s2_finalize(fe - 1, M, X);
+  if (threadIdx.x == 0) {
+    atomicSub(&wb.s2sm[5], 1u);
+    atomicAnd(&wb.s2sm[sm_ >> 5], ~(1u << (sm_ & 31)));
+  }
   if (prof && blockIdx.x == 0 && threadIdx.x == 0) {   // the kernel's own span (CTA 0)
     unsigned long long t_;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
