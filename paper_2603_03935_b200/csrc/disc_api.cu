@@ -1018,11 +1018,12 @@ static int stage2_reserve(disc_map* m, bool sem) {
   }
   const int base = sem ? m->nres : m->nres_geo;
   int extra = 0;
-  // (geometry-only windows: stage 1 is light enough to give stage 2 up to 100 SMs; measured on the
-  // prefilled H map, 85 k pairs per frame: 74 SMs 13.8 k, 104 SMs 14.5 k frames/s; at ~110 stage 1
-  // turns critical)
+  // one more SM per 1 k pairs above 24 k per frame, up to 100 SMs for geometry-only windows (measured
+  // on the prefilled H map, 85 k pairs per frame: 74 SMs 13.8 k, 104 SMs 14.5 k frames/s; at ~110
+  // stage 1 turns critical) and 88 for windows with CLIP tokens (H M2, round 2 with stage 1 kept off
+  // stage 2's SMs: 56 SMs 9.5 k, 72 10.3 k, 80 10.7 k, 88 10.75 k frames/s, stage 1 then 2.4 ms/window)
   if (m->adapt && base > 0 && m->np_avg > 24000.0)
-    extra = sem ? (int)std::min(44.0, (m->np_avg - 24000.0) / 2000.0) : (int)std::min(52.0, (m->np_avg - 24000.0) / 1000.0);
+    extra = (int)std::min(sem ? 62.0 : 52.0, (m->np_avg - 24000.0) / 1000.0);
   return std::min(base + extra, m->nsm * 3 / 4);
 }
 

@@ -215,12 +215,14 @@ __device__ __forceinline__ void count_add(const CTab& X, uint64_t code, uint32_t
 #ifndef LK_Q
 #define LK_Q 3   // unique (s, key) pairs per lane in flight (lookup; 4 held more registers than it hid latency)
 #endif
-__device__ unsigned long long g_lkprof[8];   // DISC_S2PROF: lookup sub-phases on CTA 0 (init, loop, flush; loop steps 3..6)
-__device__ __forceinline__ void lk_probe(int i, unsigned long long& tp) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+// DISC_S2PROF: lookup sub-phases on the first CTA of the lookup (init, loop, flush; loop steps 3..8),
+// [0..9] the per-frame lookup phase, [10..19] the speculative counting
+__device__ unsigned long long g_lkprof[20];
+__device__ __forceinline__ void lk_probe(int i, unsigned long long& tp, int b0) {
+  if (blockIdx.x == (unsigned)b0 && threadIdx.x == 0) {
     unsigned long long t_;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
-    if (i >= 0) atomicAdd(&g_lkprof[i], t_ - tp);
+    if (i >= 0) atomicAdd(&g_lkprof[i + (b0 ? 10 : 0)], t_ - tp);
     tp = t_;
   }
 }
@@ -247,10 +249,10 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
   uint32_t* cc = (uint32_t*)(ck + LK_CT);                                 // [LK_CT] counts
   const int32_t* stf = wb.status + (size_t)f * wb.SMAX;                   // the frame's statuses
   unsigned long long tp = 0;
-  lk_probe(-1, tp);
+  lk_probe(-1, tp, b0);
   for (int i = threadIdx.x; i < LK_CT; i += blockDim.x) { ck[i] = KEY_EMPTY; cc[i] = 0; }
   __syncthreads();
-  lk_probe(0, tp);
+  lk_probe(0, tp, b0);
   auto cta_add = [&](uint64_t code, uint32_t add) {   // CTA table, else straight to the frame's
     uint32_t h = (uint32_t)mix64(code) & (LK_CT - 1);
     for (int probe = 0; probe < 64; ++probe) {
@@ -285,7 +287,7 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
         key[q] = wb.pkey[fo + idx[q]];
       }
     }
-    lk_probe(7, tp);   // pair records loaded
+    lk_probe(7, tp, b0);   // pair records loaded
 #pragma unroll
     for (int q = 0; q < LK_Q; ++q) {
       act[q] = idx[q] < np && stf[s[q]] == 0;   // (a few L1 lines: no staging round trip)
@@ -317,6 +319,7 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
         else h[q] = (h[q] + 1) & hmask;
       }
     }
+    lk_probe(3, tp, b0);   // status + probes done
     if (tag) {   // (speculative counting) absent keys created, every kept pair chained onto its slot
 #pragma unroll
       for (int q = 0; q < LK_Q; ++q) {
@@ -338,11 +341,11 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
       for (int q = 0; q < LK_Q; ++q)
         if (kept[q] && slot[q] != U32_EMPTY)
           wb.pnext[fo + idx[q]] = (uint32_t)(old[q] >> 32) == tag ? (uint32_t)old[q] : U32_EMPTY;
+      lk_probe(8, tp, b0);   // slot chains (their exchanges' round trip)
     }
     // each pair's first two live labels (s, j) are counted warp-aggregated (a frame's keys mostly carry
     // one or two labels, and a warp's pairs mostly the same ones: per-lane shared atomics on one hot
     // counter serialise); further labels (rare) directly
-    lk_probe(3, tp);   // status + probes done
     uint64_t first[LK_Q], second[LK_Q];
 #pragma unroll
     for (int q = 0; q < LK_Q; ++q) { first[q] = KEY_EMPTY; second[q] = KEY_EMPTY; }
@@ -394,7 +397,7 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
         }
       }
     }
-    lk_probe(4, tp);   // labels walked, records stored
+    lk_probe(4, tp, b0);   // labels walked, records stored
 #pragma unroll
     for (int q = 0; q < LK_Q; ++q) {   // warp aggregation of the first (and second) label's count
       const unsigned peers = __match_any_sync(0xffffffffu, first[q]);
@@ -404,16 +407,16 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
         if (second[q] != KEY_EMPTY && lane == __ffs(p2) - 1) cta_add(second[q], __popc(p2));
       }
     }
-    lk_probe(5, tp);   // aggregated
+    lk_probe(5, tp, b0);   // aggregated
   }
-  lk_probe(-1, tp);
+  lk_probe(-1, tp, b0);
   __syncthreads();
-  lk_probe(6, tp);   // barrier: the CTA's slowest warp
-  lk_probe(1, tp);
+  lk_probe(6, tp, b0);   // barrier: the CTA's slowest warp
+  lk_probe(1, tp, b0);
   for (int i = threadIdx.x; i < LK_CT; i += blockDim.x)   // flush the CTA's counts
     if (cc[i]) count_add(C, ck[i], cc[i], M.err);
   __syncthreads();
-  lk_probe(2, tp);
+  lk_probe(2, tp, b0);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1340,12 +1343,38 @@ constexpr int DT_CT = 1024;   // per-CTA correction table slots
 #ifndef K7_DYN
 #define K7_DYN 0
 #endif
+// Frame pf's pair records, home slots and slot-chain words pulled into L2 by every warp of the grid
+// (one pair per lane per step): the speculative counting of frame pf runs two phases later against a
+// 2 GB table whose random slot reads otherwise dominate it
+__device__ __forceinline__ void s2_prefetch_frame(int pf, const WinBufs& wb, const MapState& M) {
+  const uint32_t np = min(__ldcg(&wb.npairs[pf]), (uint32_t)wb.PMAX);
+  const size_t fo = (size_t)pf * wb.PMAX;
+  const uint32_t hmask = (uint32_t)(M.MC - 1);
+  const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x, gn = gridDim.x * blockDim.x;
+  for (uint32_t i = gt; i < np; i += gn) {
+    if ((i & 31) == 0) {
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(wb.pinfo + fo + i));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(wb.pkey + fo + i + 16));
+    }
+    const unsigned long long key = __ldcg(&wb.pkey[fo + i]);
+    const uint32_t h = (uint32_t)mix64(key) & hmask;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(M.slots + h));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(M.slh + h));
+  }
+}
+
+#ifndef K7_PREFETCH
+#define K7_PREFETCH 0   // (measured no net gain: -3 us counting, +2.5 us apply) frame f+2's map lines into L2 during frame f's apply
+#endif
+#ifndef K7_LOCKSTEP
+#define K7_LOCKSTEP 1   // the two items of a lane in lockstep (0: one after the other, round 1)
+#endif
 #ifndef K7_TGT_NOCHUNK
 #define K7_TGT_NOCHUNK 0
 #endif
 __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBufs& wb, const MapState& M,
                                          const FrameScratch& X, const Params& P, int sem,
-                                         const CTab& Cn, uint32_t tagn = 0, int prof = 0) {
+                                         const CTab& Cn, uint32_t tagn = 0, int prof = 0, int pfn = -1) {
   const int lane = threadIdx.x & 31;
   unsigned long long ta0 = 0;
   auto amark = [&](int i) {   // DISC_S2PROF: sub-step end times (max over the warps, this frame)
@@ -1491,6 +1520,148 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
         plq[q] = wb.plab[fo + itq[q]];
       }
     }
+#if K7_LOCKSTEP
+    // both items of the lane advance together, stage by stage, so that their independent memory
+    // operations (records, slot reads, label CAS / tombstone, list appends, corrections) are in
+    // flight at once instead of one item's chain after the other's
+    int kd[2], tq[2], eq[2], tc[2];   // kind (0 none, 1 insert, 2 relabel), target, insert cell, tomb cell
+    uint32_t Lq[2], Lo[2], sl[2];
+    bool ins[2], tomb[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {   // classify; relabel items: their slot from the old label's list
+      const uint32_t it = itq[q];
+      kd[q] = 0; tq[q] = -1; eq[q] = -1; tc[q] = -1; Lq[q] = U32_EMPTY; Lo[q] = U32_EMPTY; sl[q] = U32_EMPTY;
+      ins[q] = false; tomb[q] = false;
+      if (it < np) {
+        const int t = dt_s[sq[q]];
+        if (t >= 0) {
+          const uint32_t L = tp_s[t];
+          const uint32_t slot = slotq[q];
+          if (!(slot != U32_EMPTY && (plq[q].x == L || plq[q].y == L))) {   // else: already a member
+            kd[q] = 1; tq[q] = t; Lq[q] = L; sl[q] = slot;
+            // first EMPTY cell as the lookup saw it, when it saw the whole inline list (at most one
+            // label): a CAS there without reading the slot again; any other outcome than EMPTY or L
+            // takes the general insert
+            if (slot != U32_EMPTY && plq[q].y == U32_EMPTY) eq[q] = plq[q].x == U32_EMPTY ? 0 : 1;
+          }
+        }
+      } else if (!stat && it < np + nrel) {
+        const uint32_t r = it - np;
+        int lo = 0, hi = nseg - 1;   // last segment with seg_off <= r
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (X.seg_off[mid] <= r) lo = mid;
+          else hi = mid - 1;
+        }
+        kd[q] = 2;
+        tq[q] = X.seg_tgt[lo];
+        Lq[q] = tp_s[tq[q]];
+        Lo[q] = X.seg_phys[lo];
+        sl[q] = M.arena[X.seg_base[lo] + (r - X.seg_off[lo])];
+      } else if (!stat && it < total) {
+        const uint32_t r = it - np - nrel;
+        int lo = 0, hi = ntgt - 1;   // last target with tg_mvoff <= r
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (X.tg_mvoff[mid] <= r) lo = mid;
+          else hi = mid - 1;
+        }
+        const uint32_t i = r - X.tg_mvoff[lo];
+        M.arena[X.tg_newoff[lo] + i] = M.arena[X.tg_movesrc[lo] + i];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {   // keys absent at lookup time (new this frame or since)
+      if (kd[q] == 1 && sl[q] == U32_EMPTY) {
+        bool created = false;
+        sl[q] = map_insert_key_c(M, wb.pkey[fo + itq[q]], &created);
+        if (sl[q] == U32_EMPTY) kd[q] = 0;
+        else if (created) eq[q] = 0;
+      }
+    }
+    SlotV sv[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)   // relabel items: one read of each slot's inline labels
+      if (kd[q] == 2) sv[q] = slot_load(M, sl[q]);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {   // relabel: insert cell (first EMPTY, L absent), tomb cell (Lo's)
+      if (kd[q] != 2) continue;
+      bool present = false, full = true;
+      int e = -1, c = -1;
+#pragma unroll
+      for (int i = 0; i < INLINE_LABELS; ++i) {
+        const uint32_t v = sv[q].lab[i];
+        if (!full) continue;   // (labels occupy a prefix: nothing after the first EMPTY)
+        if (v == U32_EMPTY) { full = false; e = i; continue; }
+        if (v == Lq[q]) present = true;
+        if (v == Lo[q]) c = i;
+      }
+      eq[q] = present ? -2 : (full ? -1 : e);   // -2: L already there; -1: general insert
+      tc[q] = c >= 0 ? c : (full ? -1 : -2);    // -2: Lo not on the key; -1: general tombstone
+    }
+    uint32_t old[2] = {U32_EMPTY, U32_EMPTY};
+#pragma unroll
+    for (int q = 0; q < 2; ++q)   // the insert CASes of both items, then the tombstones
+      if (kd[q] != 0 && eq[q] >= 0) old[q] = atomicCAS(&M.slots[sl[q]].lab[eq[q]], U32_EMPTY, Lq[q]);
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      if (kd[q] == 2 && tc[q] >= 0) { atomicExch(&M.slots[sl[q]].lab[tc[q]], LAB_TOMB); tomb[q] = true; }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {   // outcomes; the general routines for everything else
+      if (kd[q] == 0) continue;
+      if (eq[q] >= 0) ins[q] = old[q] == U32_EMPTY ? true : (old[q] == Lq[q] ? false : label_insert(M, sl[q], Lq[q]));
+      else if (eq[q] == -1) ins[q] = label_insert(M, sl[q], Lq[q]);
+      if (kd[q] == 2 && tc[q] == -1) tomb[q] = label_tomb(M, sl[q], Lo[q]);
+      delta += (ins[q] ? 1 : 0) - (tomb[q] ? 1 : 0);
+    }
+    // append the new (target, slot) entries to the targets' lists (warp-aggregated positions; K6
+    // reserved the room): both items' atomics, then both items' stores
+    unsigned peers[2];
+    uint32_t pb[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int tn = ins[q] ? tq[q] : -1;
+      peers[q] = __match_any_sync(0xffffffffu, tn);
+      pb[q] = 0;
+      if (tn >= 0 && lane == __ffs(peers[q]) - 1) pb[q] = atomicAdd(&X.tgt_stage[tn], (uint32_t)__popc(peers[q]));
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int tn = ins[q] ? tq[q] : -1;
+      const uint32_t b = __shfl_sync(0xffffffffu, pb[q], __ffs(peers[q]) - 1);
+      if (tn >= 0) M.arena[to_s[tn] + tb_s[tn] + b + __popc(peers[q] & ((1u << lane) - 1u))] = sl[q];
+    }
+    if (tagn) {   // count corrections of frame f+1 (warp-aggregated per (s, label) and sign)
+      uint32_t pi[2];
+      unsigned long long v[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        v[q] = 0;
+        if (ins[q] || tomb[q]) v[q] = __ldcg(&M.slh[sl[q]]);
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) pi[q] = (ins[q] || tomb[q]) && (uint32_t)(v[q] >> 32) == tagn ? (uint32_t)v[q] : U32_EMPTY;
+      while (__any_sync(0xffffffffu, pi[0] != U32_EMPTY || pi[1] != U32_EMPTY)) {
+        unsigned long long sh[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) sh[q] = pi[q] != U32_EMPTY ? (unsigned long long)__ldcg(&wb.pinfo[f1o + pi[q]]) << 32 : 0;
+        uint32_t nx[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) nx[q] = pi[q] != U32_EMPTY ? __ldcg(&wb.pnext[f1o + pi[q]]) : U32_EMPTY;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const unsigned long long ci = pi[q] != U32_EMPTY && ins[q] ? sh[q] | Lq[q] : KEY_EMPTY;
+          const unsigned long long ct = pi[q] != U32_EMPTY && tomb[q] ? sh[q] | Lo[q] : KEY_EMPTY;
+          const unsigned pa = __match_any_sync(0xffffffffu, ci);
+          if (ci != KEY_EMPTY && lane == __ffs(pa) - 1) dt_add(ci, (uint32_t)__popc(pa));
+          const unsigned pt = __match_any_sync(0xffffffffu, ct);
+          if (ct != KEY_EMPTY && lane == __ffs(pt) - 1) dt_add(ct, (uint32_t)(-__popc(pt)));
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) pi[q] = nx[q];
+      }
+    }
+#else
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const uint32_t it = itq[q];
@@ -1585,8 +1756,10 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
         }
       }
     }
+#endif
   }
   amark(2);
+  if (K7_PREFETCH && pfn >= 0) s2_prefetch_frame(pfn, wb, M);
 #pragma unroll
   for (int o = 16; o; o >>= 1) delta += __shfl_xor_sync(0xffffffffu, delta, o);
   if (lane == 0 && delta) atomicAdd((unsigned long long*)&M.counters[2], (unsigned long long)(int64_t)delta);
@@ -1724,9 +1897,13 @@ void k6_prof_dump() {
             c[4], c[5], c[6]);
     cudaMemcpyFromSymbol(c, g_s2items, 4 * sizeof(unsigned long long));
     fprintf(stderr, "s2 K7 items: pairs %llu relabels %llu moves %llu targets %llu\n", c[0], c[1], c[2], c[3]);
-    cudaMemcpyFromSymbol(c, g_lkprof, 8 * sizeof(unsigned long long));
-    fprintf(stderr, "s2 lookup CTA0 (thread 0): init %llu flush %llu | records %llu status+probes %llu labels %llu aggregate %llu wait-for-CTA %llu\n",
-            c[0], c[2], c[7], c[3], c[4], c[5], c[6]);
+    unsigned long long lk[20];
+    cudaMemcpyFromSymbol(lk, g_lkprof, sizeof(lk));
+    for (int m = 0; m < 2; ++m) {
+      const unsigned long long* c2 = lk + 10 * m;
+      fprintf(stderr, "s2 %s (first CTA, thread 0): init %llu flush %llu | records %llu status+probes %llu slot-chains %llu labels %llu aggregate %llu wait-for-CTA %llu\n",
+              m ? "speculative counting" : "lookup phase", c2[0], c2[2], c2[7], c2[3], c2[8], c2[4], c2[5], c2[6]);
+    }
     cudaMemcpyFromSymbol(c, g_approf, 8 * sizeof(unsigned long long));
     fprintf(stderr, "s2 apply sub-steps (per-frame max end time, summed): routing %llu targets %llu items %llu flush %llu\n",
             c[4], c[5], c[6], c[7]);
@@ -1793,6 +1970,7 @@ __device__ __forceinline__ void s2_frame(int f, int f0, int fe, const WinDesc& w
     }
   };
   if (!sp) {
+    if (K7_PREFETCH && spn) s2_prefetch_frame(f + 1, wb, M);   // (the window's first frame)
     s2_lookup(f, wb, M, X, Cc, spec == 1 && f > f0 && G > 1);
     if (f > f0) s2_finalize(f - 1, M, X);
     grid_sync(wb.s2bar, G * ++ep);
@@ -1845,7 +2023,9 @@ __device__ __forceinline__ void s2_frame(int f, int f0, int fe, const WinDesc& w
   probe(1);
   cta_fold();
   cta_mark(-1);
-  s2_apply(f, F, wb, M, X, P, sem, Cn, spn ? tag0 + (uint32_t)(f + 1) : 0u, prof);
+  // (frame f+2 is counted during frame f+1's association: its map lines into L2 now)
+  s2_apply(f, F, wb, M, X, P, sem, Cn, spn ? tag0 + (uint32_t)(f + 1) : 0u, prof,
+           spec >= 2 && f + 2 < fe && G > 1 ? f + 2 : -1);
   cta_mark(2);
   grid_sync(wb.s2bar, G * ++ep);
   probe(2);
