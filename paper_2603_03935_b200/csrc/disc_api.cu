@@ -29,6 +29,7 @@ struct disc_map {
   int nres = 0;       // SMs reserved for stage 2 (0 = no partition), windows with CLIP tokens
   int nres_geo = 0;   // the same for geometry-only windows (lighter stage 1: more SMs to stage 2)
   uint32_t s2_tag = 0;   // next slot-chain tag of stage 2's speculative counting (launch_stage2)
+  int s2_spec = 2;       // stage 2's speculative work (DISC_S2_SPEC at creation): 2 counting, 1 slots, 0 hints
   MapState M{};
   WinBufs Wb[2]{};               // double-buffered window buffers (stage 1 of window w+1 overlaps
                                  // stage 2 of window w)
@@ -126,6 +127,7 @@ const char* dev_err_text(int code) {
     case DERR_TRIPLES: return "per-frame (segment, instance) count table full";
     case DERR_INSTANCES: return "max_instances exceeded";
     case DERR_STAGE: return "per-frame staging list full: raise max_memberships";
+    case DERR_BOUNDS: return "internal index out of bounds (DISC_BOUNDS build)";
     default: {
       static thread_local char buf[96];
       if (code >= 1000) {
@@ -386,6 +388,7 @@ disc_status disc_map_create(const disc_config* cfg, disc_map** out) {
     m->nres_geo = eg ? std::atoi(eg) : (cfg->window > 16 ? 48 : 40);
     m->nres_geo = std::max(0, std::min(m->nres_geo, m->nsm * 3 / 4));
     const char* ea = std::getenv("DISC_S2_ADAPT");   // 0: fixed split (tuning)
+    if (const char* es = std::getenv("DISC_S2_SPEC")) m->s2_spec = std::max(0, std::min(3, std::atoi(es)));
     m->adapt = !(ea && std::atoi(ea) == 0);
     const char* er = std::getenv("DISC_TAB_RELEASE_RATIO");   // tuning: 1e30 = always fill
     if (er) m->tab_ratio = std::atof(er);
@@ -1158,7 +1161,7 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
     cudaStreamWaitEvent(s2, m->ev_s1[b], 0);
     if (m->timing) cudaEventRecord(t1b, s2);
     tl_mark(s2, "s2_begin", -1);
-    m->stats.launches += launch_stage2(wd, Wbuf, m->M, m->X, m->P, sem, m->nsm, nres_w, &m->s2_tag, s2);
+    m->stats.launches += launch_stage2(wd, Wbuf, m->M, m->X, m->P, sem, m->nsm, nres_w, &m->s2_tag, m->s2_spec, s2);
     if (m->timing) {
       cudaEventRecord(t2, s2);
       m->ev_pending.push_back({e0, e1, 0});

@@ -33,6 +33,7 @@ enum DevErr : int {
   DERR_TRIPLES = 5,         // per-frame (s,j) count table full
   DERR_INSTANCES = 6,       // max_instances exceeded
   DERR_STAGE = 7,           // per-frame staging list full
+  DERR_BOUNDS = 8,          // an index past its array (only raised by a -DDISC_BOUNDS build)
 };
 
 // ---- voxel map (stage 2) -------------------------------------------------------------
@@ -321,6 +322,22 @@ __device__ __forceinline__ void unpack_key(uint64_t k, int& ix, int& iy, int& iz
   iz = (int)(k & 0x1FFFFF) - KEY_BIAS;
 }
 __device__ __forceinline__ void raise_err(int* err, int code) { atomicMax(err, code); }
+// -DDISC_BOUNDS: device-side bounds checks on the computed indices of the hot kernels (the check
+// compute-sanitizer memcheck would do; that tool is closed on the GPU pool).  A violation prints
+// the condition and raises DERR_BOUNDS, so the map's next synchronising call fails.
+#ifdef DISC_BOUNDS
+#define DBOUND(cond, err)                                                                    \
+  do {                                                                                       \
+    if (!(cond)) {                                                                           \
+      printf("DISC_BOUNDS %s:%d: %s\n", __FILE__, __LINE__, #cond);                          \
+      raise_err((err), DERR_BOUNDS);                                                         \
+    }                                                                                        \
+  } while (0)
+#else
+#define DBOUND(cond, err) \
+  do {                    \
+  } while (0)
+#endif
 // internal invariant check: records 1000 + source line in the sticky error flag
 #define DISC_CHECK(err, cond)                       \
   do {                                              \

@@ -17,7 +17,7 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
 void launch_refine(int f, int S, const WinBufs& wb, const MapState& M, const FrameScratch& X, const Params& P, int grid,
                    cudaStream_t st);
 int launch_stage2(const WinDesc& wd, const WinBufs& wb, const MapState& M, const FrameScratch& X, const Params& P,
-                  bool sem, int nsm, int nres, uint32_t* tag_seq, cudaStream_t st);
+                  bool sem, int nsm, int nres, uint32_t* tag_seq, int spec_mode, cudaStream_t st);
 // NEXT f3 (k_dbscan.cu): DBSCAN denoise replacing K1b / K1c when P.db_eps > 0; returns launches
 int launch_dbscan(const WinDesc& wd, const WinBufs& wb, const Params& P, int* err, bool sem, int nsm, cudaStream_t st);
 size_t dbscan_tmp_bytes(int n_items, int n_seg);

@@ -717,6 +717,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
         if (nn.x || nn.y || nn.z) nscr[i] = NSum{0, 0, 0, 0};
       }
       if (!direct) {
+        DBOUND(r < (uint32_t)wb.RCAP, err);
         const size_t o = (size_t)f * wb.PMAX + r++;
         __stcg(&wb.rkey[o], kt[i >> 1]);
         __stcg(&wb.rs[o], s);

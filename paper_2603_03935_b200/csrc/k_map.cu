@@ -285,6 +285,7 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
       if (idx[q] < np) {
         s[q] = wb.pinfo[fo + idx[q]];
         key[q] = wb.pkey[fo + idx[q]];
+        DBOUND(s[q] < (uint32_t)wb.SMAX, M.err);
       }
     }
     lk_probe(7, tp, b0);   // pair records loaded
@@ -326,6 +327,7 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
         if (kept[q] && slot[q] == U32_EMPTY) {
           bool created = false;
           slot[q] = map_insert_key_c(M, key[q], &created);
+          DBOUND(slot[q] == U32_EMPTY || slot[q] < M.MC, M.err);
           sv[q].lab[0] = sv[q].lab[1] = U32_EMPTY;   // (a slot created now has no labels)
           sv[q].ovf = U32_EMPTY;
 #pragma unroll
@@ -1170,10 +1172,13 @@ __device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc&
     return;
   }
   const uint32_t n = mcnt + dcnt;
+  DBOUND(root < (uint32_t)M.IMAX && (kind == 1 || L < (uint32_t)M.IMAX), M.err);
   // candidate of this lane: members (ids ascending) then detections (s ascending); K6 wrote them
   // side by side (tg_cand), one read with the descriptors
   const bool is_mem = (uint32_t)lane < mcnt, is_det = !is_mem && (uint32_t)lane < n;
   const uint32_t cid = (is_mem || is_det) ? X.tg_cand[t * 32 + lane] : 0u;
+  DBOUND(!is_mem || cid < (uint32_t)M.IMAX, M.err);
+  DBOUND(!is_det || cid < (uint32_t)F.S, M.err);
 
   TG_STEP(0);
   // attributes of the candidate
@@ -1218,6 +1223,7 @@ __device__ __forceinline__ void apply_target_warp(int t, int f, const FrameDesc&
       __syncwarp();
       if ((uint32_t)lane >= i0 && (uint32_t)lane < i0 + nb) {
         const uint32_t i = (uint32_t)lane;
+        DBOUND(i - i0 < (uint32_t)rows, M.err);
         const double* row = (kind == 0 && i < mcnt) ? M.T + (size_t)cid * Dt : trk + (size_t)cid * Dt;
         bulk_g2s(stg + (size_t)(i - i0) * Dt, row, rb, bar);
       }
@@ -1533,10 +1539,13 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
       kd[q] = 0; tq[q] = -1; eq[q] = -1; tc[q] = -1; Lq[q] = U32_EMPTY; Lo[q] = U32_EMPTY; sl[q] = U32_EMPTY;
       ins[q] = false; tomb[q] = false;
       if (it < np) {
+        DBOUND(sq[q] < (uint32_t)F.S, M.err);
         const int t = dt_s[sq[q]];
+        DBOUND(t < ntgt, M.err);
         if (t >= 0) {
           const uint32_t L = tp_s[t];
           const uint32_t slot = slotq[q];
+          DBOUND(slot == U32_EMPTY || slot < M.MC, M.err);
           if (!(slot != U32_EMPTY && (plq[q].x == L || plq[q].y == L))) {   // else: already a member
             kd[q] = 1; tq[q] = t; Lq[q] = L; sl[q] = slot;
             // first EMPTY cell as the lookup saw it, when it saw the whole inline list (at most one
@@ -1555,9 +1564,12 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
         }
         kd[q] = 2;
         tq[q] = X.seg_tgt[lo];
+        DBOUND(lo >= 0 && lo < nseg && tq[q] >= 0 && tq[q] < ntgt, M.err);
+        DBOUND(X.seg_base[lo] + (r - X.seg_off[lo]) < M.ARENA, M.err);
         Lq[q] = tp_s[tq[q]];
         Lo[q] = X.seg_phys[lo];
         sl[q] = M.arena[X.seg_base[lo] + (r - X.seg_off[lo])];
+        DBOUND(sl[q] < M.MC, M.err);
       } else if (!stat && it < total) {
         const uint32_t r = it - np - nrel;
         int lo = 0, hi = ntgt - 1;   // last target with tg_mvoff <= r
@@ -1567,6 +1579,7 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
           else hi = mid - 1;
         }
         const uint32_t i = r - X.tg_mvoff[lo];
+        DBOUND(X.tg_newoff[lo] + i < M.ARENA && X.tg_movesrc[lo] + i < M.ARENA, M.err);
         M.arena[X.tg_newoff[lo] + i] = M.arena[X.tg_movesrc[lo] + i];
       }
     }
@@ -1629,7 +1642,10 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
     for (int q = 0; q < 2; ++q) {
       const int tn = ins[q] ? tq[q] : -1;
       const uint32_t b = __shfl_sync(0xffffffffu, pb[q], __ffs(peers[q]) - 1);
-      if (tn >= 0) M.arena[to_s[tn] + tb_s[tn] + b + __popc(peers[q] & ((1u << lane) - 1u))] = sl[q];
+      if (tn >= 0) {
+        DBOUND(to_s[tn] + tb_s[tn] + b + __popc(peers[q] & ((1u << lane) - 1u)) < M.ARENA, M.err);
+        M.arena[to_s[tn] + tb_s[tn] + b + __popc(peers[q] & ((1u << lane) - 1u))] = sl[q];
+      }
     }
     if (tagn) {   // count corrections of frame f+1 (warp-aggregated per (s, label) and sign)
       uint32_t pi[2];
@@ -1643,6 +1659,8 @@ __device__ __forceinline__ void s2_apply(int f, const FrameDesc& F, const WinBuf
       for (int q = 0; q < 2; ++q) pi[q] = (ins[q] || tomb[q]) && (uint32_t)(v[q] >> 32) == tagn ? (uint32_t)v[q] : U32_EMPTY;
       while (__any_sync(0xffffffffu, pi[0] != U32_EMPTY || pi[1] != U32_EMPTY)) {
         unsigned long long sh[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) DBOUND(pi[q] == U32_EMPTY || pi[q] < (uint32_t)wb.PMAX, M.err);
 #pragma unroll
         for (int q = 0; q < 2; ++q) sh[q] = pi[q] != U32_EMPTY ? (unsigned long long)__ldcg(&wb.pinfo[f1o + pi[q]]) << 32 : 0;
         uint32_t nx[2];
@@ -1873,6 +1891,7 @@ __device__ __forceinline__ void s2_finalize(int f, const MapState& M, const Fram
   const int tn = cta0 ? blockDim.x : gridDim.x * blockDim.x;
   for (int t = t0; t < ntgt; t += tn) {
     const uint32_t add = X.tgt_stage[t];
+    DBOUND(X.tgt_phys[t] < (uint32_t)M.IMAX && X.tgt_root[t] < (uint32_t)M.IMAX, M.err);
     M.lst_len[X.tgt_phys[t]] = X.tgt_base[t] + add;
     M.vcount[X.tgt_root[t]] += add;
     if (add) atomicAdd((unsigned long long*)&M.counters[5], (unsigned long long)add);
@@ -2521,7 +2540,7 @@ void launch_refine(int f, int S, const WinBufs& wb, const MapState& M, const Fra
 }
 
 int launch_stage2(const WinDesc& wd, const WinBufs& wb, const MapState& M, const FrameScratch& X, const Params& P,
-                  bool sem, int nsm, int nres, uint32_t* tag_seq, cudaStream_t st) {
+                  bool sem, int nsm, int nres, uint32_t* tag_seq, int spec_mode, cudaStream_t st) {
   const size_t sm6 = k6_smem_bytes(wb.SMAX, X.TCS);
   static size_t set_for = 0;
   if (set_for != sm6) {
@@ -2534,7 +2553,7 @@ int launch_stage2(const WinDesc& wd, const WinBufs& wb, const MapState& M, const
   // be guaranteed, not assumed
   int semi = sem ? 1 : 0;
   // speculative work during the association (k_stage2): 2 counting + corrections, 1 slots, 0 hints
-  static const int spec = getenv("DISC_S2_SPEC") ? atoi(getenv("DISC_S2_SPEC")) : 2;
+  int spec = spec_mode;
   int f0 = 0, fn = wd.n;
   // slot-chain tags of the speculatively counted frames: the map's own sequence (never reused
   // between clears of M.slh, so no clearing per frame); 0 = none

@@ -434,3 +434,15 @@ def test_every_frame_debug_export(name, nf):
         compare_reports(gm.integrate_frame(fr), om.integrate(frame_to_numpy(fr)))
         compare_frame_debug(gm.last_frame(), om.last_frame(), True, c.Dt)
         compare_state(gm, om, True, c.Dt)
+
+
+@pytest.mark.parametrize("spec", ["0", "1", "2", "3"])
+@pytest.mark.parametrize("name,nf,window", [("R", 8, 4), ("H", 6, 6)])
+def test_stage2_speculation_modes(spec, name, nf, window, monkeypatch):
+    """Stage 2's speculative work (DISC_S2_SPEC, read at map creation): 2 (default) counts frame f+1
+    during frame f's association and corrects the counts in frame f's update; 3 the same with the gate
+    on CTAs of its own; 1 only finds the slots early; 0 L2 hints.  Every mode gives the oracle's
+    per-frame reports, the window's last-frame debug export (a speculatively counted frame in 2 / 3)
+    and the map state."""
+    monkeypatch.setenv("DISC_S2_SPEC", spec)
+    _stream_parity(name, nf, True, window=window)
