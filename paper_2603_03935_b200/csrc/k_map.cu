@@ -212,6 +212,9 @@ __device__ __forceinline__ void count_add(const CTab& X, uint64_t code, uint32_t
 #ifndef LK_AGG2
 #define LK_AGG2 1   // warp-aggregate the second label too (0: round-1 behaviour, per-lane shared atomics)
 #endif
+#ifndef LK_REV
+#define LK_REV 1
+#endif
 #ifndef LK_Q
 #define LK_Q 3   // unique (s, key) pairs per lane in flight (lookup; 4 held more registers than it hid latency)
 #endif
@@ -274,7 +277,10 @@ __device__ __forceinline__ void s2_lookup(int f, const WinBufs& wb, const MapSta
   const uint32_t hmask = (uint32_t)(M.MC - 1);
   const uint32_t gthreads = nb * blockDim.x;
   // pair q of a lane: base + q * (grid threads), so every CTA gets an equal share
-  for (uint32_t base = (blockIdx.x - b0) * blockDim.x + (threadIdx.x & ~31u); base < np; base += stride) {
+  // (speculative counting: CTA b takes share G-1-b, so CTAs 1.., which evaluate the visual gate
+  // first, get the last shares -- one pair per lane where the first shares have two)
+  const uint32_t cb = b0 > 0 && LK_REV ? gridDim.x - 1 - blockIdx.x : blockIdx.x - b0;
+  for (uint32_t base = cb * blockDim.x + (threadIdx.x & ~31u); base < np; base += stride) {
     uint32_t idx[LK_Q], s[LK_Q], slot[LK_Q], h[LK_Q];
     unsigned long long key[LK_Q];
     bool act[LK_Q];
