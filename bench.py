@@ -58,6 +58,8 @@ def parse():
     p.add_argument("--prefill-max-frames", type=int, default=8192)
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--oracle-seconds", type=float, default=12.0)
+    p.add_argument("--mask-format", default="bits", choices=["bits", "u8"],
+                   help="mask planes as disc_frame::mask_bits (1 bit/pixel, default) or u8 byte planes")
     p.add_argument("--no-m2", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
@@ -176,7 +178,7 @@ RANK = par.Rank(1, 0, 0, None)
 
 def frame_bytes(fr) -> int:
     n = 0
-    for k in ["depth", "masks", "mask_conf", "patch_feats", "global_embed", "track_feats"]:
+    for k in ["depth", "masks", "mask_bits", "mask_conf", "patch_feats", "global_embed", "track_feats"]:
         t = fr.get(k)
         if t is not None:
             n += t.numel() * t.element_size()
@@ -197,6 +199,15 @@ def run_oracle_frames(frames_np, cfg_kw, budget_s, min_frames=1):
     return n, time.perf_counter() - t0
 
 
+def nmasks(fr: dict) -> int:
+    return (fr["masks"] if fr.get("masks") is not None else fr["mask_bits"]).shape[0]
+
+
+def nmask_bytes(fr: dict) -> int:
+    t = fr["masks"] if fr.get("masks") is not None else fr["mask_bits"]
+    return t.numel() * t.element_size()
+
+
 def m1(fr: dict) -> dict:
     """M1 input of a frame: no CLIP tokens (association + refinement only)."""
     return dict(fr, patch_feats=None, global_embed=None)
@@ -210,7 +221,7 @@ def run_reference(args, ws, rank):
     if rank != 0:
         return
     import torch
-    from synth import Generator, disc_config_kwargs, frame_to_numpy
+    from synth import Generator, disc_config_kwargs, frame_to_numpy, pack_mask_bits
     from oracle.oracle import OracleMap
     dev = "cuda:0" if torch.cuda.is_available() else "cpu"
     g = Generator(args.config, device=dev)
@@ -270,7 +281,7 @@ def main():
         run_reference(args, ws, rank)
         return
     import torch
-    from synth import Generator, disc_config_kwargs, frame_to_numpy
+    from synth import Generator, disc_config_kwargs, frame_to_numpy, pack_mask_bits
     from synth.scenes import seed_of
     from paper_2603_03935_b200 import DiscMap
 
@@ -301,6 +312,9 @@ def main():
         out = [g.frame(f, with_feats=feats) for f in range(nxt, nxt + n) if not sharded or f % ws == rank]
         if not feats:
             out = [m1(fr) for fr in out]
+        if args.mask_format == "bits":   # the same masks, bit-packed (input layout; generated untimed)
+            out = [{k: v for k, v in fr.items() if k != "masks"} | {"mask_bits": pack_mask_bits(fr["masks"])}
+                   for fr in out]
         torch.cuda.synchronize()
         t_gen += time.perf_counter() - t0
         nxt += n
@@ -352,13 +366,14 @@ def main():
         timed = frames[args.warmup * Fr:]
         n = len(timed)
         in_bytes = sum(frame_bytes(fr) for fr in timed)
-        k1_bytes = sum(fr["masks"].numel() + fr["depth"].numel() * 4 for fr in timed)
+        k1_bytes = sum(nmask_bytes(fr) + fr["depth"].numel() * 4 for fr in timed)
         s2_bytes = stage2_bytes(d, c.Dt)
         k1_ms, s2_ms = d["k1_ms"], d["stage2_ms"]
         kern = {
             "K1": {"kernel": "K1 mask pass (k_masks + k_walk + k_dedup)", "bound": "hbm",
                    "algorithmic_bytes_per_launch": k1_bytes / max(d["k1_launches"], 1),
-                   "bytes_per_unit": "S*H*W mask bytes + 4*H*W depth bytes per frame (every input byte once)",
+                   "bytes_per_unit": ("S*ceil(H*W/32)*4 bit-packed mask bytes" if args.mask_format == "bits" else
+                                      "S*H*W mask bytes") + " + 4*H*W depth bytes per frame (every input byte once)",
                    "avg_launch_ms": k1_ms / max(d["k1_launches"], 1), "launches": d["k1_launches"],
                    "achieved": k1_bytes / (k1_ms / 1e3) / 1e9 if k1_ms > 0 else None,
                    "share_of_step": k1_ms / ms if ms > 0 else None},
@@ -394,7 +409,9 @@ def main():
                    "mode": "M1 = voxel association + refinement (A0-A3, A5b, A6-A8; no CLIP tokens)",
                    "l2": f"no flush: inputs per step {sum(frame_bytes(fr) for fr in timed) / args.steps / 1e9:.2f} GB > 126 MB L2",
                    "frames_timed_per_rank": args.steps * Fr,
-                   "masks_per_frame_mean": round(sum(fr["masks"].shape[0] for fr in timed) / len(timed), 1),
+                   "masks_per_frame_mean": round(sum(nmasks(fr) for fr in timed) / len(timed), 1),
+                   "mask_format": ("bit-packed planes (disc_frame::mask_bits, 1 bit per pixel)" if args.mask_format == "bits"
+                                   else "u8 byte planes"),
                    "prefill_frames": prefill_frames, "prefill_seconds": round(t_pf, 1),
                    "live_memberships_before_timing": int(live),
                    "parallelism": (f"one stream, key-hash-sharded map over {ws} GPUs (NCCL)" if sharded else

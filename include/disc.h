@@ -115,6 +115,11 @@ typedef struct {
                                        /* only mode (no embedding, Q = -1)                   */
   const float* global_embed;           /* [Df] or NULL (S_sem = 1)                           */
   const uint16_t* track_feats;         /* [Hp][Wp][Dt] bf16 bit patterns; required iff Dt>0  */
+  const uint32_t* mask_bits;           /* the masks bit-packed, instead of `masks` (exactly  */
+                                       /* one of the two non-NULL when S > 0): plane s is    */
+                                       /* ceil(H*W/32) little-endian words, pixel p = v*W+u  */
+                                       /* is bit p%32 of word p/32 (bits past H*W ignored);  */
+                                       /* 1/8 of the bytes to move and to read   */
 } disc_frame;
 
 typedef struct {                       /* per-frame report                     */

@@ -68,6 +68,8 @@ struct disc_map {
   uint8_t* stage = nullptr;           // the buffer being filled
   uint8_t* stage_buf[2] = {nullptr, nullptr};
   cudaEvent_t ev_stage[2] = {nullptr, nullptr};
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr};   // a staging buffer's H2D copies issued (on s0)
+  cudaStream_t s0 = nullptr;                    // host-input copies: beside stage 1 and stage 2
   bool stage_pending[2] = {false, false};
   int stage_next = 0;
   size_t stage_bytes = 0;
@@ -172,7 +174,7 @@ std::string validate_frame(const disc_map* m, const disc_frame& f, bool host) {
   if ((int64_t)f.height * f.width > c.max_pixels) return "H*W exceeds max_pixels";
   if (!f.depth) return "null depth";
   if (f.num_masks < 0 || f.num_masks > c.max_masks) return "num_masks outside [0, max_masks]";
-  if (f.num_masks > 0 && !f.masks) return "null masks";
+  if (f.num_masks > 0 && !f.masks == !f.mask_bits) return "exactly one of masks / mask_bits must be given";
   if (f.patch_h < 1 || f.patch_h > f.height || f.patch_w < 1 || f.patch_w > f.width) return "bad patch grid";
   if ((int64_t)f.patch_h * f.patch_w > c.max_patches) return "Hp*Wp exceeds max_patches";
   if (f.patch_w > 65535) return "patch_w too large";
@@ -190,6 +192,7 @@ FrameDesc make_desc(const disc_frame& f) {
   FrameDesc d{};
   d.depth = f.depth;
   d.masks = f.masks;
+  d.mbits = f.mask_bits;
   d.conf = f.mask_conf;
   d.feats = f.patch_feats;
   d.gemb = f.global_embed;
@@ -627,7 +630,9 @@ void disc_map_destroy(disc_map* m) {
   for (int i = 0; i < 2; ++i) {
     if (m->stage_buf[i]) cudaFree(m->stage_buf[i]);
     if (m->ev_stage[i]) cudaEventDestroy(m->ev_stage[i]);
+    if (m->ev_h2d[i]) cudaEventDestroy(m->ev_h2d[i]);
   }
+  if (m->s0) cudaStreamDestroy(m->s0);
   if (m->h_rep_all) cudaFreeHost(m->h_rep_all);
   if (m->scratch) cudaFree(m->scratch);
   for (auto& p : m->ev_pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
@@ -1039,10 +1044,15 @@ static disc_status ensure_stage(disc_map* m) {
                                        (size_t)c.feat_dim * 4 + 4096);
   for (int i = 0; i < 2; ++i) {
     if (cudaMalloc((void**)&m->stage_buf[i], m->stage_bytes) != cudaSuccess ||
-        cudaEventCreateWithFlags(&m->ev_stage[i], cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&m->ev_stage[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&m->ev_h2d[i], cudaEventDisableTiming) != cudaSuccess) {
       cudaGetLastError();
       return fail(m, DISC_ERR_CAPACITY, "cannot allocate host-input staging buffers");
     }
+  }
+  if (cudaStreamCreateWithFlags(&m->s0, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(m, DISC_ERR_CUDA, "cannot create the host-input copy stream");
   }
   m->stage = m->stage_buf[0];
   return DISC_OK;
@@ -1061,6 +1071,7 @@ static void stage_frame(disc_map* m, size_t& so, disc_frame& f, cudaStream_t st)
   const size_t HW = (size_t)f.height * f.width, Pn = (size_t)f.patch_h * f.patch_w;
   f.depth = (const float*)put(f.depth, HW * 4);
   f.masks = (const uint8_t*)put(f.masks, HW * f.num_masks);
+  f.mask_bits = (const uint32_t*)put(f.mask_bits, (HW + 31) / 32 * 4 * f.num_masks);
   f.mask_conf = (const float*)put(f.mask_conf, (size_t)f.num_masks * 4);
   f.patch_feats = (const float*)put(f.patch_feats, Pn * Df * 4);
   f.global_embed = (const float*)put(f.global_embed, (size_t)Df * 4);
@@ -1100,6 +1111,7 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
   cudaEventRecord(m->ev_in, st);
   cudaStreamWaitEvent(m->s1, m->ev_in, 0);
   cudaStreamWaitEvent(m->s2, m->ev_in, 0);
+  if (host_inputs) cudaStreamWaitEvent(m->s0, m->ev_in, 0);
   cudaStream_t s1 = m->s1, s2 = m->s2;
   for (int w0 = 0; w0 < n; w0 += win) {
     const int nw = std::min(win, n - w0);
@@ -1118,12 +1130,14 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
     if (host_inputs) {   // the staging buffer stage 1 of the window before last has finished reading
       sb = m->stage_next;
       m->stage_next ^= 1;
-      if (m->stage_pending[sb]) cudaStreamWaitEvent(s1, m->ev_stage[sb], 0);
+      if (m->stage_pending[sb]) cudaStreamWaitEvent(m->s0, m->ev_stage[sb], 0);
       m->stage = m->stage_buf[sb];
     }
     for (int i = 0; i < nw; ++i) {
       disc_frame f = frames[w0 + i];
-      if (host_inputs) stage_frame(m, so, f, s1);   // this frame's inputs to device staging
+      // this frame's inputs to device staging, on the copy stream: window w+1's copies run beside
+      // window w's stage 1 and stage 2 (two staging buffers), stage 1 waits for its own
+      if (host_inputs) stage_frame(m, so, f, m->s0);
       wd.f[i] = make_desc(f);
       maxS = std::max(maxS, f.num_masks);
       maxHp = std::max(maxHp, f.patch_h);
@@ -1135,6 +1149,10 @@ static disc_status integrate_impl(disc_map* m, const disc_frame* frames, int32_t
       m->stats.depth_bytes += (int64_t)f.height * f.width * 4;
       m->stats.track_bytes += (int64_t)f.patch_h * f.patch_w * Dt * 2;
       if (f.patch_feats) m->stats.feat_bytes += (int64_t)f.patch_h * f.patch_w * Df * 4;
+    }
+    if (host_inputs) {
+      cudaEventRecord(m->ev_h2d[sb], m->s0);
+      cudaStreamWaitEvent(s1, m->ev_h2d[sb], 0);
     }
     cudaEvent_t e0 = nullptr, e1 = nullptr, t0 = nullptr, t1 = nullptr, t1b = nullptr, t2 = nullptr;
     if (m->timing) {

@@ -64,12 +64,19 @@ struct FrameDesc {                // one frame's inputs, passed by value to kern
   const float* feats;
   const float* gemb;
   const uint16_t* track;
+  const uint32_t* mbits;          // bit-packed masks (disc_frame::mask_bits) or nullptr: `masks`
   float pose[12];                 // rows 0..2 of the camera->world matrix
   float fx, fy, cx, cy;
   int64_t frame_id;
   int32_t H, W, S, Hp, Wp;
   int32_t vec16;                  // vector path: H*W % 32 == 0, masks 32-B and depth 16-B aligned
 };
+
+// pixel p (= v*W + u) of mask s, from whichever of the two plane formats the frame carries
+__device__ __forceinline__ bool mask_at(const FrameDesc& F, int s, size_t p) {
+  if (F.mbits) return (__ldg(F.mbits + (size_t)s * (((size_t)F.H * F.W + 31) >> 5) + (p >> 5)) >> (p & 31)) & 1u;
+  return F.masks[(size_t)s * F.H * F.W + p] != 0;
+}
 
 struct WinDesc {
   FrameDesc f[MAXWIN];

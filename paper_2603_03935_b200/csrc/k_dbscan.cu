@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(256) k_db_points(WinDesc wd, WinBufs wb, Param
     if (!point_key_fast(p, P.r, rinv, key)) { ++oor; continue; }
     const int cx = (int)floorf(p[0] * cinv), cy = (int)floorf(p[1] * cinv), cz = (int)floorf(p[2] * cinv);
     for (int s = 0; s < F.S; ++s) {
-      if (!F.masks[(size_t)s * HW + i]) continue;
+      if (!mask_at(F, s, (size_t)i)) continue;
       const uint32_t slot = atomicAdd(&wb.dbn[f], 1u);
       if (slot >= (uint32_t)wb.DBP) { raise_err(err, DERR_FRAME_PAIRS); continue; }
       wb.dbk[(size_t)f * wb.DBP + slot] = db_cell_key((uint32_t)s, cx, cy, cz);

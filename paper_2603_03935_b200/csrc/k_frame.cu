@@ -126,6 +126,9 @@ __global__ void k_win_init(WinDesc wd, WinBufs wb) {
 #ifndef K1B_PERSIST
 #define K1B_PERSIST 7   // K1b CTAs per SM (A/B r02: 7 beat 8 and 6 on R and H, M1 and M2)
 #endif
+#ifndef K1_NFB
+#define K1_NFB 16   // bit-packed mask words in flight per lane (K1a)
+#endif
 #ifndef K1_NF
 #define K1_NF 4   // mask planes in flight per lane (K1a)
 #endif
@@ -163,6 +166,15 @@ __device__ __forceinline__ void ld_stream32(const uint8_t* p, uint32_t r[8]) {
                : "l"(p));
 #endif
 }
+// (bit-packed mask words) read-only path, no L1 allocation, L2 evict-first through a cache policy
+// (the .L2::evict_first qualifier form needs a 32-byte vector)
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p, uint64_t pol) {
+  uint32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
+// 4 mask bits -> 4 bytes of 0 / 1 (bit i -> byte i; the shifted copies of the nibble never overlap)
+__device__ __forceinline__ uint32_t nib_bytes(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
 __device__ __forceinline__ uint4 ld_mask16(const uint8_t* p) {
   uint4 r;
 #if K1_MASK_L2 == 1
@@ -208,7 +220,8 @@ __device__ __forceinline__ int next_item(uint32_t* ctr, uint32_t total, uint32_t
 // sector only for the planes that touch it.
 constexpr int K1A_SECT = K1_THREADS;   // sectors per item
 
-template <bool VEC>
+// BM: mask planes of the window's frames -- 0 all byte planes, 1 all bit-packed, 2 mixed (per frame)
+template <bool VEC, int BM>
 __global__ void __launch_bounds__(K1_THREADS, K1A_PERSIST) k_masks(WinDesc wd, WinBufs wb, int items_f, int reserve,
                                                                   int ablate) {
   if (on_reserved_sm(reserve, wb.s2sm)) return;
@@ -233,6 +246,11 @@ __global__ void __launch_bounds__(K1_THREADS, K1A_PERSIST) k_masks(WinDesc wd, W
     const int v0 = nv ? (int)((uint32_t)p0 / (uint32_t)W) : 0;
     const int u0 = nv ? (int)p0 - v0 * W : 0;
     uint32_t* cnt_f = wb.cnt + (size_t)f * wb.SMAX * wb.PMAXP;
+    // bit-packed planes: the sector is exactly word p0/32 of the plane (one 4-byte load instead of 32),
+    // kept raw in w[0] until used
+    const bool bits = BM == 1 || (BM == 2 && F.mbits != nullptr);
+    const uint32_t* mbp = bits ? F.mbits + (p0 >> 5) : nullptr;
+    const size_t wpl = ((size_t)HW + 31) >> 5;
     auto load = [&](int s, uint32_t w[8]) {
       const uint8_t* mp = F.masks + (size_t)s * HW + p0;
       if (VEC) {
@@ -276,86 +294,122 @@ __global__ void __launch_bounds__(K1_THREADS, K1A_PERSIST) k_masks(WinDesc wd, W
     }
     const int jb = u0 + nv > W ? W - u0 : 32;   // first pixel of the second row
     const uint32_t rowA = jb >= 32 ? 0xFFFFFFFFu : ((1u << jb) - 1u);
-    uint32_t m0[8], ovf = 0;
+    uint32_t m0[8], ovf = 0, unset_b = 0xFFFFFFFFu;   // (unset_b: bit-packed path, pixels without a mask yet)
 #pragma unroll
     for (int t = 0; t < 8; ++t) m0[t] = 0xFFFFFFFFu;   // no mask yet
     const int Sl = (nv && !(ablate & 1)) ? S : 0;
-    uint32_t buf[K1_NF][8];
+    // per-patch pixel counts (O5, regardless of depth, R17) and bbox of mask s over the sector's
+    // pixels `set` (bit j = pixel p0 + j)
+    auto tally = [&](int s, uint32_t set) {
+      if (fast) {   // per-patch pixel counts (O5, regardless of depth, R17) and bbox
+        uint32_t sb = segbits;
 #pragma unroll
-    for (int k = 0; k < K1_NF; ++k)
-      if (k < Sl) load(k, buf[k]);
-    for (int s0 = 0; s0 < Sl; s0 += K1_NF) {
-#pragma unroll
-      for (int k = 0; k < K1_NF; ++k) {
-        const int s = s0 + k;
-        if (s >= Sl) break;
-        uint32_t* w = buf[k];
-        if ((w[0] | w[1] | w[2] | w[3] | w[4] | w[5] | w[6] | w[7]) == 0) {
-          if (s + K1_NF < Sl) load(s + K1_NF, buf[k]);   // refill the ring slot
-          continue;
+        for (int k = 0; k < K1A_NSEG; ++k) {
+          if (k >= nseg) break;
+          const int a0 = __ffs(sb) - 1;
+          sb &= sb - 1;
+          const int b0 = sb ? __ffs(sb) - 1 : 32;
+          const int cn = __popc(set & range_bits(a0, b0));
+          if (cn) atomicAdd(&cnt_f[(size_t)s * wb.PMAXP + pidx[k]], (uint32_t)cn);
         }
-        uint32_t set = 0;
-        const uint32_t splat = (uint32_t)s * 0x01010101u;
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const uint32_t sb = __vcmpne4(w[t], 0u);                // 0xFF where the pixel is in s
-          set |= (((sb & 0x08040201u) * 0x01010101u) >> 24) << (4 * t);
-          const uint32_t unset = __vcmpeq4(m0[t], 0xFFFFFFFFu);   // 0xFF where no mask yet
-          const uint32_t fresh = sb & unset, again = sb & ~unset;
-          m0[t] = (m0[t] & ~fresh) | (splat & fresh);
-          ovf |= (((again & 0x08040201u) * 0x01010101u) >> 24) << (4 * t);
+        const uint32_t sa = set & rowA, sb2 = set & ~rowA;
+        if (sa) {
+          atomicMin(&bb_s[4 * s + 0], u0 + __ffs(sa) - 1);
+          atomicMax(&bb_s[4 * s + 2], u0 + 31 - __clz(sa));
+          atomicMin(&bb_s[4 * s + 1], v0);
+          atomicMax(&bb_s[4 * s + 3], v0);
         }
-        if (s + K1_NF < Sl) load(s + K1_NF, buf[k]);   // refill the ring slot
-        set &= inb;
-        if (!set) continue;
-        if (fast) {   // per-patch pixel counts (O5, regardless of depth, R17) and bbox
-          uint32_t sb = segbits;
-#pragma unroll
-          for (int k = 0; k < K1A_NSEG; ++k) {
-            if (k >= nseg) break;
-            const int a0 = __ffs(sb) - 1;
-            sb &= sb - 1;
-            const int b0 = sb ? __ffs(sb) - 1 : 32;
-            const int cn = __popc(set & range_bits(a0, b0));
-            if (cn) atomicAdd(&cnt_f[(size_t)s * wb.PMAXP + pidx[k]], (uint32_t)cn);
-          }
-          const uint32_t sa = set & rowA, sb2 = set & ~rowA;
-          if (sa) {
-            atomicMin(&bb_s[4 * s + 0], u0 + __ffs(sa) - 1);
-            atomicMax(&bb_s[4 * s + 2], u0 + 31 - __clz(sa));
-            atomicMin(&bb_s[4 * s + 1], v0);
-            atomicMax(&bb_s[4 * s + 3], v0);
-          }
-          if (sb2) {
-            atomicMin(&bb_s[4 * s + 0], __ffs(sb2) - 1 - jb);
-            atomicMax(&bb_s[4 * s + 2], 31 - __clz(sb2) - jb);
-            atomicMin(&bb_s[4 * s + 1], v0 + 1);
-            atomicMax(&bb_s[4 * s + 3], v0 + 1);
-          }
-          continue;
+        if (sb2) {
+          atomicMin(&bb_s[4 * s + 0], __ffs(sb2) - 1 - jb);
+          atomicMax(&bb_s[4 * s + 2], 31 - __clz(sb2) - jb);
+          atomicMin(&bb_s[4 * s + 1], v0 + 1);
+          atomicMax(&bb_s[4 * s + 3], v0 + 1);
         }
-        // general: row segments of the sector, and patch segments inside them
-        int j = 0, v = v0, u = u0;
-        while (j < nv) {
-          const int len = min(W - u, nv - j);
-          const uint32_t rowb = set & range_bits(j, j + len);
-          if (rowb) {
-            const int prow = (v * Hp) / H * Wp;
-            int pcol = (u * Wp) / W;
-            int jj = j, uu = u;
-            while (jj < j + len) {
-              const int ub = ((pcol + 1) * W + Wp - 1) / Wp;   // first u of the next patch column
-              const int l2 = min(j + len - jj, ub - uu);
-              const int cn = __popc(set & range_bits(jj, jj + l2));
-              if (cn) atomicAdd(&cnt_f[(size_t)s * wb.PMAXP + prow + pcol], (uint32_t)cn);
-              jj += l2; uu += l2; ++pcol;
+        return;
+      }
+      // general: row segments of the sector, and patch segments inside them
+      int j = 0, v = v0, u = u0;
+      while (j < nv) {
+        const int len = min(W - u, nv - j);
+        const uint32_t rowb = set & range_bits(j, j + len);
+        if (rowb) {
+          const int prow = (v * Hp) / H * Wp;
+          int pcol = (u * Wp) / W;
+          int jj = j, uu = u;
+          while (jj < j + len) {
+            const int ub = ((pcol + 1) * W + Wp - 1) / Wp;   // first u of the next patch column
+            const int l2 = min(j + len - jj, ub - uu);
+            const int cn = __popc(set & range_bits(jj, jj + l2));
+            if (cn) atomicAdd(&cnt_f[(size_t)s * wb.PMAXP + prow + pcol], (uint32_t)cn);
+            jj += l2; uu += l2; ++pcol;
+          }
+          atomicMin(&bb_s[4 * s + 0], u + (__ffs(rowb) - 1 - j));
+          atomicMax(&bb_s[4 * s + 2], u + (31 - __clz(rowb) - j));
+          atomicMin(&bb_s[4 * s + 1], v);
+          atomicMax(&bb_s[4 * s + 3], v);
+        }
+        j += len; ++v; u = 0;
+      }
+    };
+    if (BM != 0 && bits) {
+      // bit-packed planes: one word per plane and sector, K1_NFB planes in flight per lane (4-byte
+      // loads: a deeper ring than the byte planes' 32-byte ones for the same bytes in flight); the
+      // first-mask bytes are touched only for pixels meeting their first mask
+      uint32_t rb[K1_NFB];
+      const uint64_t pol = policy_evict_first();
+#pragma unroll
+      for (int k = 0; k < K1_NFB; ++k) rb[k] = k < Sl ? ld_stream_u32(mbp + (size_t)k * wpl, pol) & inb : 0u;
+      for (int s0 = 0; s0 < Sl; s0 += K1_NFB) {
+#pragma unroll
+        for (int k = 0; k < K1_NFB; ++k) {
+          const int s = s0 + k;
+          if (s >= Sl) break;
+          const uint32_t set = rb[k];
+          if (s + K1_NFB < Sl) rb[k] = ld_stream_u32(mbp + (size_t)(s + K1_NFB) * wpl, pol) & inb;   // refill
+          if (!set) continue;
+          const uint32_t fresh = set & unset_b;
+          ovf |= set & ~unset_b;
+          unset_b &= ~set;
+          if (fresh) {
+            const uint32_t splat = (uint32_t)s * 0x01010101u;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+              const uint32_t fm = nib_bytes((fresh >> (4 * t)) & 0xFu) * 0xFFu;
+              m0[t] = (m0[t] & ~fm) | (splat & fm);
             }
-            atomicMin(&bb_s[4 * s + 0], u + (__ffs(rowb) - 1 - j));
-            atomicMax(&bb_s[4 * s + 2], u + (31 - __clz(rowb) - j));
-            atomicMin(&bb_s[4 * s + 1], v);
-            atomicMax(&bb_s[4 * s + 3], v);
           }
-          j += len; ++v; u = 0;
+          tally(s, set);
+        }
+      }
+    } else if (BM != 1) {
+      uint32_t buf[K1_NF][8];
+#pragma unroll
+      for (int k = 0; k < K1_NF; ++k)
+        if (k < Sl) load(k, buf[k]);
+      for (int s0 = 0; s0 < Sl; s0 += K1_NF) {
+#pragma unroll
+        for (int k = 0; k < K1_NF; ++k) {
+          const int s = s0 + k;
+          if (s >= Sl) break;
+          uint32_t* w = buf[k];
+          if ((w[0] | w[1] | w[2] | w[3] | w[4] | w[5] | w[6] | w[7]) == 0) {
+            if (s + K1_NF < Sl) load(s + K1_NF, buf[k]);   // refill the ring slot
+            continue;
+          }
+          uint32_t set = 0;
+          const uint32_t splat = (uint32_t)s * 0x01010101u;
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const uint32_t sb = __vcmpne4(w[t], 0u);                // 0xFF where the pixel is in s
+            set |= (((sb & 0x08040201u) * 0x01010101u) >> 24) << (4 * t);
+            const uint32_t unset = __vcmpeq4(m0[t], 0xFFFFFFFFu);   // 0xFF where no mask yet
+            const uint32_t fresh = sb & unset, again = sb & ~unset;
+            m0[t] = (m0[t] & ~fresh) | (splat & fresh);
+            ovf |= (((again & 0x08040201u) * 0x01010101u) >> 24) << (4 * t);
+          }
+          if (s + K1_NF < Sl) load(s + K1_NF, buf[k]);   // refill the ring slot
+          set &= inb;
+          if (set) tally(s, set);
         }
       }
     }
@@ -672,7 +726,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1B_PERSIST) k_walk(WinDesc wd, Wi
           if (mv_c >> 8) {   // other masks of this pixel (R9), per pixel
             const size_t pix = (size_t)vv * W + u;
             for (int s2 = (int)m + 1; s2 < S; ++s2)
-              if (F.masks[(size_t)s2 * H * W + pix]) emit((uint32_t)s2, kc, n0, n1, n2);
+              if (mask_at(F, s2, pix)) emit((uint32_t)s2, kc, n0, n1, n2);
           }
         }
         pu[0] = pc[0]; pu[1] = pc[1]; pu[2] = pc[2]; vu = vc;
@@ -1544,13 +1598,20 @@ int launch_stage1(const WinDesc& wd, const WinBufs& wb, const Params& P, int* er
   if (ev0) cudaEventRecord(ev0, st);
   int64_t maxHW = 1;
   bool vec = true;
+  int nbits = 0, nbytes = 0;   // frames with bit-packed / byte mask planes (frames without masks: either)
   for (int i = 0; i < n; ++i) {
     maxHW = std::max(maxHW, (int64_t)wd.f[i].H * wd.f[i].W);
     vec = vec && wd.f[i].vec16;
+    if (wd.f[i].S > 0) (wd.f[i].mbits ? nbits : nbytes)++;
   }
   const int items_a = (int)((maxHW + 32 * K1A_SECT - 1) / (32 * K1A_SECT));
-  if (vec) k_masks<true><<<K1A_PERSIST * nsm, K1_THREADS, (size_t)maxS * 16, st>>>(wd, wb, items_a, nres, k1_ablate());
-  else k_masks<false><<<K1A_PERSIST * nsm, K1_THREADS, (size_t)maxS * 16, st>>>(wd, wb, items_a, nres, k1_ablate());
+  const dim3 ga(K1A_PERSIST * nsm), ba(K1_THREADS);
+  const size_t sa = (size_t)maxS * 16;
+  if (nbits && nbytes) k_masks<false, 2><<<ga, ba, sa, st>>>(wd, wb, items_a, nres, k1_ablate());
+  else if (nbits && vec) k_masks<true, 1><<<ga, ba, sa, st>>>(wd, wb, items_a, nres, k1_ablate());
+  else if (nbits) k_masks<false, 1><<<ga, ba, sa, st>>>(wd, wb, items_a, nres, k1_ablate());
+  else if (vec) k_masks<true, 0><<<ga, ba, sa, st>>>(wd, wb, items_a, nres, k1_ablate());
+  else k_masks<false, 0><<<ga, ba, sa, st>>>(wd, wb, items_a, nres, k1_ablate());
   debug_check(st, "k_masks", -1);
   if (P.db_eps > 0.f) {   // NEXT f3: DBSCAN denoise, then the kept points into the frame tables (k_dbscan.cu)
     launches += launch_dbscan(wd, wb, P, err, sem, nsm, st) - 2;

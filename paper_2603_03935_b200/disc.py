@@ -47,7 +47,7 @@ class disc_frame(C.Structure):
         ("pose", C.c_float * 16), ("depth", C.c_void_p), ("num_masks", C.c_int32),
         ("masks", C.c_void_p), ("mask_conf", C.c_void_p), ("patch_h", C.c_int32),
         ("patch_w", C.c_int32), ("patch_feats", C.c_void_p), ("global_embed", C.c_void_p),
-        ("track_feats", C.c_void_p),
+        ("track_feats", C.c_void_p), ("mask_bits", C.c_void_p),
     ]
 
 
@@ -210,13 +210,15 @@ class DiscMap:
     # ---- marshalling ------------------------------------------------------------------
     @staticmethod
     def make_frame(fr: dict, keep: list) -> disc_frame:
-        """fr: dict with torch CUDA tensors (depth, masks, mask_conf, patch_feats,
-        global_embed, track_feats [bf16]) and host scalars / pose."""
+        """fr: dict with torch CUDA tensors (depth, masks [S,H,W] u8 -- or mask_bits [S, ceil(H*W/32)]
+        int32, the bit-packed planes of disc_frame::mask_bits --, mask_conf, patch_feats, global_embed,
+        track_feats [bf16]) and host scalars / pose."""
         import torch
         tf = fr.get("track_feats")
         if tf is not None and tf.dtype == torch.bfloat16:
             tf = tf.view(torch.int16)
-        ts = [fr["depth"], fr["masks"], fr.get("mask_conf"), fr.get("patch_feats"), fr.get("global_embed"), tf]
+        mk, mb = fr.get("masks"), fr.get("mask_bits")
+        ts = [fr["depth"], mk, mb, fr.get("mask_conf"), fr.get("patch_feats"), fr.get("global_embed"), tf]
         for t in ts:
             if t is not None and not t.is_contiguous():
                 raise ValueError("inputs must be contiguous")
@@ -225,7 +227,9 @@ class DiscMap:
         pose = (C.c_float * 16)(*[float(x) for x in np.asarray(fr["pose"], np.float32).reshape(16)])
         return disc_frame(frame_id=int(fr["frame_id"]), height=H, width=W, fx=fr["fx"], fy=fr["fy"],
                           cx=fr["cx"], cy=fr["cy"], pose=pose, depth=_ptr(fr["depth"]),
-                          num_masks=int(fr["masks"].shape[0]), masks=_ptr(fr["masks"]),
+                          num_masks=int(fr["num_masks"] if "num_masks" in fr else
+                                        (mk if mk is not None else mb).shape[0]), masks=_ptr(mk),
+                          mask_bits=_ptr(mb),
                           mask_conf=_ptr(fr.get("mask_conf")), patch_h=int(fr["patch_h"]),
                           patch_w=int(fr["patch_w"]), patch_feats=_ptr(fr.get("patch_feats")),
                           global_embed=_ptr(fr.get("global_embed")), track_feats=_ptr(tf))

@@ -593,3 +593,18 @@ def frame_to_numpy(fr: dict) -> dict:
         else:
             out[k] = v
     return out
+
+
+def pack_mask_bits(masks: torch.Tensor) -> torch.Tensor:
+    """[S, H, W] masks (nonzero = in mask) -> [S, ceil(H*W/32)] int32 words in the layout of
+    disc_frame::mask_bits: pixel p = v*W + u of plane s is bit p % 32 of word p / 32 (little-endian
+    words; bits past H*W zero).  A layout change only: the same binary masks, 1/8 of the bytes."""
+    S = masks.shape[0]
+    flat = (masks.reshape(S, -1) != 0)
+    n = flat.shape[1]
+    pad = (-n) % 32
+    if pad:
+        flat = torch.cat([flat, flat.new_zeros((S, pad))], dim=1)
+    w = flat.reshape(S, -1, 32).to(torch.int64) << torch.arange(32, device=masks.device, dtype=torch.int64)
+    words = w.sum(dim=2)                                    # < 2^32: every bit once
+    return (words - ((words >> 31) << 32)).to(torch.int32)  # the same 32 bits as int32

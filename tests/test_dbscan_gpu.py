@@ -42,10 +42,12 @@ def test_t0_outlier_patch_removed():
     ("N", dict(H=96, W=128, Hp=6, Wp=9, fx=115.5, fy=115.7, cx=63.8, cy=48.5, min_area=40, voxel=0.02), 0.04, 5),
     ("X", dict(H=96, W=128, Hp=6, Wp=9, fx=115.5, fy=115.7, cx=63.8, cy=48.5, min_area=40, n_masks=30, Df=64), 0.1, 8),
 ])
-def test_stream_with_dbscan(name, over, eps, mp):
+@pytest.mark.parametrize("bits", [False, True])
+def test_stream_with_dbscan(name, over, eps, mp, bits):
     """Streams with DBSCAN on (noisy N depth: holes and far-tail noise make minor clusters; X:
-    overlapping masks), every frame compared; windows of 4 frames."""
+    overlapping masks), every frame compared; windows of 4 frames; byte or bit-packed mask planes."""
     from paper_2603_03935_b200 import DiscMap
+    from synth import pack_mask_bits
     dev = _dev()
     g = Generator(name, device=dev, **over)
     c = g.cfg
@@ -57,8 +59,10 @@ def test_stream_with_dbscan(name, over, eps, mp):
     nf = 3 if name == "T" else 6
     frames = [g.frame(f) for f in range(nf)]
     reps_g = []
+    gframes = [{k: v for k, v in fr.items() if k != "masks"} | {"mask_bits": pack_mask_bits(fr["masks"])}
+               for fr in frames] if bits else frames
     for w0 in range(0, nf, 4):
-        reps_g += gm.integrate_frames(frames[w0:w0 + 4], report=True)
+        reps_g += gm.integrate_frames(gframes[w0:w0 + 4], report=True)
     removed = 0
     for fr, rg in zip(frames, reps_g):
         ro = om.integrate(frame_to_numpy(fr))

@@ -11,7 +11,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 from oracle.oracle import OracleMap  # noqa: E402
-from synth import Generator, disc_config_kwargs, frame_to_numpy, t0_frame  # noqa: E402
+from synth import pack_mask_bits, Generator, disc_config_kwargs, frame_to_numpy, t0_frame  # noqa: E402
 from tests.parity_util import compare_frame_debug, compare_reports, compare_state, gpu_config  # noqa: E402
 
 
@@ -89,7 +89,14 @@ def test_tiny_config_every_frame(semantic):
         compare_state(gm, om, semantic, c.Dt)
 
 
-def _stream_parity(name, nframes, semantic, window, every=1, caps=None, reports=True, **over):
+def _bits(fr):
+    """The frame with its masks bit-packed (disc_frame::mask_bits) instead of byte planes."""
+    out = {k: v for k, v in fr.items() if k != "masks"}
+    out["mask_bits"] = pack_mask_bits(fr["masks"])
+    return out
+
+
+def _stream_parity(name, nframes, semantic, window, every=1, caps=None, reports=True, bits=False, **over):
     dev = _dev()
     g = Generator(name, device=dev, **over)
     c = g.cfg
@@ -97,11 +104,13 @@ def _stream_parity(name, nframes, semantic, window, every=1, caps=None, reports=
     gm = _disc_map(kw, c.H, c.W, c.Hp, c.Wp, window=window, S=min(255, max(64, int(c.n_masks * 1.2) + 8)), **(caps or {}))
     om = OracleMap(**kw)
     frames = [g.frame(f, with_feats=semantic) for f in range(nframes)]
+    # (the oracle always reads byte planes; bits="mixed": every other frame packed, one window mixes both)
+    gframes = [(_bits(fr) if (bits is True or i % 2) else fr) for i, fr in enumerate(frames)] if bits else frames
     # windowed GPU integration (the launch configuration bench.py times)
     # (without reports no call waits for its window: window w+1's stage 1 overlaps w's stage 2)
     reps_g = []
     for w0 in range(0, nframes, window):
-        r = gm.integrate_frames(frames[w0:w0 + window], report=reports)
+        r = gm.integrate_frames(gframes[w0:w0 + window], report=reports)
         reps_g += r if reports else []
     reps_o = [om.integrate(frame_to_numpy(fr)) for fr in frames]
     for rg, ro in zip(reps_g, reps_o):
@@ -446,3 +455,55 @@ def test_stage2_speculation_modes(spec, name, nf, window, monkeypatch):
     and the map state."""
     monkeypatch.setenv("DISC_S2_SPEC", spec)
     _stream_parity(name, nf, True, window=window)
+
+
+@pytest.mark.parametrize("name,nf,window,over", [
+    ("R", 8, 4, {}),                                                                   # vector K1a path
+    ("X", 4, 4, dict(n_masks=60, Df=256)),                                             # overlapping masks (R9)
+    ("N", 4, 2, dict(H=239, W=317, Hp=17, Wp=22, fx=290.0, fy=290.0, cx=158.0, cy=119.0)),   # H*W % 32 != 0
+    ("H", 6, 6, {}),
+])
+def test_bit_packed_masks(name, nf, window, over):
+    """disc_frame::mask_bits (masks bit-packed, 1/8 of the bytes) gives exactly the oracle's results
+    on its byte planes: per-frame reports, the last frame's debug export, the map."""
+    _stream_parity(name, nf, True, window=window, bits=True, **over)
+
+
+def test_mixed_mask_formats_in_a_window():
+    """Byte and bit-packed planes in one window (K1a's per-frame variant)."""
+    _stream_parity("R", 6, True, window=6, bits="mixed")
+
+
+def test_bit_packed_masks_host_path():
+    """The host-input path stages the packed planes (ceil(H*W/32) words per mask) and gives the same
+    map as the device path with byte planes."""
+    dev = _dev()
+    g = Generator("N", device=dev)
+    c = g.cfg
+    kw = disc_config_kwargs(c)
+    frames = [g.frame(f) for f in range(6)]
+    a = _disc_map(kw, c.H, c.W, c.Hp, c.Wp, window=3)
+    b = _disc_map(kw, c.H, c.W, c.Hp, c.Wp, window=3)
+    ra = a.integrate_frames(frames, report=True)
+    host = [{k: (v.cpu().pin_memory() if isinstance(v, torch.Tensor) else v) for k, v in _bits(fr).items()}
+            for fr in frames]
+    rb = b.integrate_frames_host(host, report=True)
+    assert ra == rb
+    assert np.array_equal(a.memberships()[0], b.memberships()[0])
+    A, B = a.instances(), b.instances()
+    for k in ["id", "vcount", "obs", "aabb", "T", "e", "q"]:
+        assert np.array_equal(A[k], B[k])
+
+
+def test_mask_formats_exclusive():
+    """Exactly one of masks / mask_bits: both or neither (S > 0) is DISC_ERR_INVALID."""
+    from paper_2603_03935_b200.disc import DiscError
+    dev = _dev()
+    g = Generator("T", device=dev)
+    c = g.cfg
+    m = _disc_map(disc_config_kwargs(c), c.H, c.W, c.Hp, c.Wp)
+    fr = g.frame(0)
+    with pytest.raises(DiscError):
+        m.integrate_frame(dict(fr, mask_bits=pack_mask_bits(fr["masks"])))
+    with pytest.raises(DiscError):
+        m.integrate_frame({k: v for k, v in fr.items() if k != "masks"} | {"masks": None, "num_masks": 2})

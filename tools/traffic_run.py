@@ -9,7 +9,9 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_2603_03935_b200 import DiscMap  # noqa: E402
-from synth import Generator, disc_config_kwargs  # noqa: E402
+from synth import Generator, disc_config_kwargs, pack_mask_bits  # noqa: E402
+import os  # noqa: E402
+BITS = os.environ.get("DISC_MASK_FORMAT", "bits") == "bits"   # bench.py's default input layout
 
 name = sys.argv[1] if len(sys.argv) > 1 else "H"
 prefill = float(sys.argv[2]) if len(sys.argv) > 2 else (1e7 if name == "H" else 0)
@@ -26,6 +28,8 @@ def gen(n, feats):
     out = [g.frame(f, with_feats=feats) for f in range(nxt, nxt + n)]
     if not feats:
         out = [dict(fr, patch_feats=None, global_embed=None) for fr in out]
+    if BITS:
+        out = [{k: v for k, v in fr.items() if k != "masks"} | {"mask_bits": pack_mask_bits(fr["masks"])} for fr in out]
     nxt += n
     torch.cuda.synchronize()
     return out
