@@ -56,7 +56,8 @@ def parse():
     p.add_argument("--prefill-memberships", type=float, default=None,
                    help="untimed prefill until the map holds this many live memberships (H: 1e7, else 0)")
     p.add_argument("--prefill-max-frames", type=int, default=8192)
-    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--e2e-steps", type=int, default=None,
+                   help="windows timed end to end (default: --steps, as far as 4 GB of pinned inputs allow)")
     p.add_argument("--oracle-seconds", type=float, default=12.0)
     p.add_argument("--mask-format", default="bits", choices=["bits", "u8"],
                    help="mask planes as disc_frame::mask_bits (1 bit/pixel, default) or u8 byte planes")
@@ -439,9 +440,13 @@ def main():
 
     # ---- e2e: the public API with pinned HOST inputs (M1), copies inside the timed region ----
     if not args.no_e2e:
-        E = max(1, min(args.e2e_steps, args.steps))
+        probe = gen(F, False)   # one window: its bytes bound how many windows fit in 4 GB pinned
+        wbytes = sum(frame_bytes(fr) for fr in probe)
+        E = args.e2e_steps if args.e2e_steps is not None else args.steps
+        E = max(1, min(E, args.steps, int(4e9 // max(wbytes, 1)) - 1))
         host = [{k: (v.cpu().pin_memory() if isinstance(v, torch.Tensor) else v) for k, v in fr.items()}
-                for fr in gen((E + 1) * F, False)]
+                for fr in probe + gen(E * F, False)]
+        del probe
         m.integrate_frames_host(host[:Fr], report=True)   # warm-up step
         h2d = sum(frame_bytes(fr) for fr in host[Fr:]) / E
         barrier(ws)

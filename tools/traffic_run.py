@@ -47,5 +47,5 @@ for mode, feats in [("M1", False), ("M2", True)]:
         m.integrate_frames(frames[w * F:(w + 1) * F])
     m.sync()
     torch.cuda.nvtx.range_pop()
-    print(mode, "frames", 2 * F, "masks/frame", sum(fr["masks"].shape[0] for fr in frames[F:]) / (2 * F),
+    print(mode, "frames", 2 * F, "masks/frame", sum((fr["masks"] if fr.get("masks") is not None else fr["mask_bits"]).shape[0] for fr in frames[F:]) / (2 * F),
           "wall ms/window", (time.perf_counter() - t0) * 500, file=sys.stderr, flush=True)
