@@ -146,9 +146,9 @@ def test_hm3d_prefix():
     _stream_parity("H", 8, True, window=8)
 
 
-@pytest.mark.parametrize("name,pmax", [("H", 1 << 19), ("N", 1 << 16)])
+@pytest.mark.parametrize("name,pmax", [("H", 1 << 18), ("N", 1 << 16)])
 def test_bench_launch_configuration_h_n(name, pmax):
-    """`bench.py --config H|N`'s launch configuration: 32-frame windows, its capacities (pairs 2^19
+    """`bench.py --config H|N`'s launch configuration: 32-frame windows, its capacities (pairs 2^18
     per frame for H, 2^16 for N), no per-window reports (window 2's stage 1 beside window 1's
     stage 2), a ragged second window of 8 frames; the last frame's debug export and the whole map
     compared with the oracle."""

@@ -17,7 +17,7 @@ g = Generator(name, device="cuda:0")
 c = g.cfg
 m = DiscMap(**disc_config_kwargs(c), max_pixels=c.H * c.W, max_patches=c.Hp * c.Wp, max_masks=96, window=32,
             max_memberships=int(sys.argv[4]) if len(sys.argv) > 4 else 1 << 25, max_instances=1 << 20,
-            max_pairs_per_frame=1 << 19)
+            max_pairs_per_frame=1 << 18)
 F, nxt, live = 32, 0, 0
 
 

@@ -19,7 +19,7 @@ g = Generator(name, device="cuda:0")
 c = g.cfg
 m = DiscMap(**disc_config_kwargs(c), max_pixels=c.H * c.W, max_patches=c.Hp * c.Wp, max_masks=int(c.n_masks * 1.2) + 8,
             window=32, max_memberships=1 << 25 if prefill > 0 else 1 << 23, max_instances=1 << 20,
-            max_pairs_per_frame=1 << 19 if name == "H" else 1 << 17)
+            max_pairs_per_frame=1 << 18 if name == "H" else 1 << 17)
 F, nxt, live = 32, 0, 0
 
 
