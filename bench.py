@@ -301,7 +301,7 @@ def main():
                 max_memberships=1 << 25 if prefill > 0 else 1 << 23, max_instances=1 << 20,
                 # per-frame (mask, voxel) pair capacity: R and N frames stay below ~40k unique pairs, H's far
                 # views reach ~1 pair per pixel (2 cm voxels, 480x640): 2^19.  Past it: loud CAPACITY error
-                max_pairs_per_frame=int(os.environ.get("BENCH_PMAX", 1 << 18 if args.config == "H" else 1 << 17)),
+                max_pairs_per_frame=int(os.environ.get("BENCH_PMAX", 1 << 18 if args.config == "H" else 1 << 16)),
                 device=local)
     m = DiscMap(**cfg_kw, **caps, **(par.sharded_map_kwargs(RANK) if sharded else {}))
     t_gen = 0.0
