@@ -127,7 +127,7 @@ __global__ void k_win_init(WinDesc wd, WinBufs wb) {
 #define K1B_PERSIST 7   // K1b CTAs per SM (A/B r02: 7 beat 8 and 6 on R and H, M1 and M2)
 #endif
 #ifndef K1_NFB
-#define K1_NFB 16   // bit-packed mask words in flight per lane (K1a)
+#define K1_NFB 4   // bit-packed mask words in flight per lane (K1a; measured H: 4 139, 8 150, 16 219 us per window)
 #endif
 #ifndef K1_NF
 #define K1_NF 4   // mask planes in flight per lane (K1a)
@@ -358,14 +358,14 @@ __global__ void __launch_bounds__(K1_THREADS, K1A_PERSIST) k_masks(WinDesc wd, W
       uint32_t rb[K1_NFB];
       const uint64_t pol = policy_evict_first();
 #pragma unroll
-      for (int k = 0; k < K1_NFB; ++k) rb[k] = k < Sl ? ld_stream_u32(mbp + (size_t)k * wpl, pol) & inb : 0u;
+      for (int k = 0; k < K1_NFB; ++k) rb[k] = k < Sl ? ld_stream_u32(mbp + (size_t)k * wpl, pol) : 0u;
       for (int s0 = 0; s0 < Sl; s0 += K1_NFB) {
 #pragma unroll
         for (int k = 0; k < K1_NFB; ++k) {
           const int s = s0 + k;
           if (s >= Sl) break;
-          const uint32_t set = rb[k];
-          if (s + K1_NFB < Sl) rb[k] = ld_stream_u32(mbp + (size_t)(s + K1_NFB) * wpl, pol) & inb;   // refill
+          const uint32_t set = rb[k] & inb;   // (the raw word: consuming a load at its refill would wait for it)
+          if (s + K1_NFB < Sl) rb[k] = ld_stream_u32(mbp + (size_t)(s + K1_NFB) * wpl, pol);   // refill
           if (!set) continue;
           const uint32_t fresh = set & unset_b;
           ovf |= set & ~unset_b;
