@@ -146,3 +146,25 @@ def test_sharded_with_dbscan():
         compare_reports(rg, ro)
     compare_frame_debug(gm.last_frame(), om.last_frame(), True, c.Dt)
     compare_state(gm, om, True, c.Dt)
+
+
+@pytest.mark.parametrize("host", [False, True])
+def test_sharded_bit_packed_masks(host):
+    """Bit-packed mask planes (disc_frame::mask_bits) on a 2-shard map, device and host-input paths:
+    the same reports and map as the unsharded map on byte planes."""
+    from synth import pack_mask_bits
+    dev = _dev()
+    g = Generator("R", device=dev)
+    c = g.cfg
+    kw = disc_config_kwargs(c)
+    frames = [g.frame(f) for f in range(6)]
+    packed = [{k: v for k, v in fr.items() if k != "masks"} | {"mask_bits": pack_mask_bits(fr["masks"])} for fr in frames]
+    a = _map(kw, c, 2, 6, 64)
+    b = _map(kw, c, 1, 6, 64)
+    if host:
+        packed = [{k: (v.cpu().pin_memory() if isinstance(v, torch.Tensor) else v) for k, v in fr.items()} for fr in packed]
+        ra = a.integrate_frames_host(packed, report=True)
+    else:
+        ra = a.integrate_frames(packed, report=True)
+    assert ra == b.integrate_frames(frames, report=True)
+    assert np.array_equal(a.memberships()[0], b.memberships()[0])
