@@ -216,7 +216,9 @@ __device__ __forceinline__ void count_add(const CTab& X, uint64_t code, uint32_t
 #define LK_REV 1
 #endif
 #ifndef LK_Q
-#define LK_Q 3   // unique (s, key) pairs per lane in flight (lookup; 4 held more registers than it hid latency)
+#define LK_Q 1   // unique (s, key) pairs per lane in flight.  The persistent kernel shares one register
+                 // allocation: LK_Q 3 spilled 664 B per thread across all phases, 2 316 B, 1 72 B (H
+                 // bench r02: M1 14.3 k / 15.1 k / 16.5 k frames/s)
 #endif
 // DISC_S2PROF: lookup sub-phases on the first CTA of the lookup (init, loop, flush; loop steps 3..8),
 // [0..9] the per-frame lookup phase, [10..19] the speculative counting
