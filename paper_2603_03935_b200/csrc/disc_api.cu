@@ -1026,13 +1026,14 @@ static int stage2_reserve(disc_map* m, bool sem) {
   }
   const int base = sem ? m->nres : m->nres_geo;
   int extra = 0;
-  // one more SM per 1 k pairs above 24 k per frame, up to 108 SMs for geometry-only windows (with the
-  // bit-packed K1a, H M1: 100 SMs 14.6-14.7 k, 110 SMs 14.8 k frames/s, stage 1 1.66 ms < stage 2; before it, measured
+  // one more SM per 1 k pairs above 24 k per frame, up to 100 SMs for geometry-only windows and 80 for
+  // CLIP windows (final round-2 build, H, two runs each: 100/80 M1 16.9/16.8 k, M2 12.3/12.3 k;
+  // 108/88 16.5/16.6 k, 12.2/12.2 k; 116/96 16.0/16.4 k, 11.8/11.7 k); earlier builds, measured
   // on the prefilled H map, 85 k pairs per frame: 74 SMs 13.8 k, 104 SMs 14.5 k frames/s; at ~110
   // stage 1 turns critical) and 88 for windows with CLIP tokens (H M2, round 2 with stage 1 kept off
   // stage 2's SMs: 56 SMs 9.5 k, 72 10.3 k, 80 10.7 k, 88 10.75 k frames/s, stage 1 then 2.4 ms/window)
   if (m->adapt && base > 0 && m->np_avg > 24000.0)
-    extra = (int)std::min(sem ? 62.0 : 60.0, (m->np_avg - 24000.0) / 1000.0);
+    extra = (int)std::min(sem ? 54.0 : 52.0, (m->np_avg - 24000.0) / 1000.0);
   return std::min(base + extra, m->nsm * 3 / 4);
 }
 
